@@ -1,0 +1,120 @@
+"""Self-oracle properties of the CPU oracle (SPEC.md §4 style): FD gradients, tiling invariance,
+SP=P == SP=1, attention agnosticism, replication equivalence."""
+import numpy as np
+import pytest
+
+from oracle import sptrain_oracle as O
+
+MINI = O.LayerConfig(hidden=16, q_heads=4, kv_heads=2, head_dim=4, intermediate=32, vocab=50)
+
+
+def _params(cfg, seed=0, wstd=0.3):
+    return O.LayerParams(**O.synth_params(cfg, seed, wstd=wstd)).astype(np.float64)
+
+
+def _loss(params, cfg, x, lab, pos, **kw):
+    return O.layer_step(params, cfg, x, lab, pos, **kw).loss
+
+
+@pytest.mark.parametrize("name", ["wqkv", "wo", "wg", "wd", "wlm", "g1", "g3"])
+def test_layer_fd_gradients(name):
+    """tape grads vs central differences, rel err < 1e-6 at f64."""
+    cfg = MINI
+    p = _params(cfg)
+    x, lab, pos = O.synth_batch(cfg, 8, seed=1)
+    x = x.astype(np.float64)
+    res = O.layer_step(p, cfg, x, lab, pos, P=1, mlp_tiles=3, loss_tile=3)
+    w = getattr(p, name)
+    rng = np.random.default_rng(2)
+    idx = [tuple(rng.integers(0, s) for s in w.shape) for _ in range(6)]
+    for i in idx:
+        old = w[i]
+        w[i] = old + 1e-5
+        fp = _loss(p, cfg, x, lab, pos, mlp_tiles=3, loss_tile=3)
+        w[i] = old - 1e-5
+        fm = _loss(p, cfg, x, lab, pos, mlp_tiles=3, loss_tile=3)
+        w[i] = old
+        fd = (fp - fm) / 2e-5
+        g = res.grads[name][i]
+        assert abs(fd - g) <= 1e-6 * max(1e-3, abs(fd)) + 1e-9, (name, i, fd, g)
+
+
+def test_layer_fd_dx():
+    cfg = MINI
+    p = _params(cfg)
+    x, lab, pos = O.synth_batch(cfg, 8, seed=3)
+    x = x.astype(np.float64)
+    res = O.layer_step(p, cfg, x, lab, pos)
+    for i in [(0, 1), (5, 7), (7, 15)]:
+        old = x[i]
+        x[i] = old + 1e-5
+        fp = _loss(p, cfg, x, lab, pos)
+        x[i] = old - 1e-5
+        fm = _loss(p, cfg, x, lab, pos)
+        x[i] = old
+        fd = (fp - fm) / 2e-5
+        assert abs(fd - res.dx[i]) <= 1e-6 * max(1e-3, abs(fd)) + 1e-9
+
+
+@pytest.mark.parametrize("tiles", [1, 2, 3, 7, 16])
+def test_tiling_invariance(tiles):
+    """values bit-exact per tile count; grads <= 1e-10."""
+    cfg = MINI
+    p = _params(cfg)
+    x, lab, pos = O.synth_batch(cfg, 16, seed=4)
+    base = O.layer_step(p, cfg, x, lab, pos, mlp_tiles=1, loss_tile=16)
+    t = O.layer_step(p, cfg, x, lab, pos, mlp_tiles=tiles, loss_tile=max(1, 16 // tiles))
+    assert t.count == base.count
+    assert abs(t.loss_sum - base.loss_sum) <= 1e-10 * abs(base.loss_sum)
+    for k in O.LayerParams.NAMES:
+        assert np.max(np.abs(t.grads[k] - base.grads[k])) <= 1e-10
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("packed", [False, True])
+def test_sp_equivalence(P, packed):
+    """SP=P loss and grads equal SP=1 to <= 1e-10 (f64); block-diag callback (:341)."""
+    cfg = MINI
+    p = _params(cfg)
+    x, lab, pos = O.synth_batch(cfg, 16, seed=5, packed=packed)
+    base = O.layer_step(p, cfg, x, lab, pos, P=1)
+    sp = O.layer_step(p, cfg, x, lab, pos, P=P)
+    assert abs(sp.loss - base.loss) <= 1e-10
+    assert np.max(np.abs(sp.dx - base.dx)) <= 1e-10
+    for k in O.LayerParams.NAMES:
+        assert np.max(np.abs(sp.grads[k] - base.grads[k])) <= 1e-10, k
+
+
+def test_kv_replication_equivalence():
+    """(Hq=4, Hkv=1, P=4) kv-projection grads equal the P=1 baseline."""
+    cfg = O.LayerConfig(hidden=16, q_heads=4, kv_heads=1, head_dim=4, intermediate=32, vocab=50)
+    p = _params(cfg)
+    x, lab, pos = O.synth_batch(cfg, 16, seed=6)
+    base = O.layer_step(p, cfg, x, lab, pos, P=1)
+    sp = O.layer_step(p, cfg, x, lab, pos, P=4)
+    assert np.max(np.abs(sp.grads["wqkv"] - base.grads["wqkv"])) <= 1e-10
+
+
+def test_block_diag_equals_separate_samples():
+    """block-diagonal attention on packed samples == per-sample attention."""
+    rng = np.random.default_rng(7)
+    runs = [5, 3, 8]
+    pos = np.concatenate([np.arange(r) for r in runs])
+    s = pos.size
+    q, k, v = (rng.standard_normal((s, 4, 8)) for _ in range(3))
+    k, v = k[:, :2], v[:, :2]
+    o, _ = O.attention_fwd(q, k, v, O.block_causal_starts(pos))
+    a = 0
+    for r in runs:
+        o2, _ = O.attention_fwd(q[a:a + r], k[a:a + r], v[a:a + r])
+        assert np.max(np.abs(o[a:a + r] - o2)) <= 1e-12
+        a += r
+
+
+def test_all_ignored_loss():
+    """all labels -100 -> (0,0) and zero d hidden."""
+    cfg = MINI
+    p = _params(cfg)
+    x, lab, pos = O.synth_batch(cfg, 8, seed=8)
+    s, c, dh, dw = O.tiled_logits_loss(x.astype(np.float64) @ np.eye(16), p.wlm, np.full(8, -100), 3, grad_scale=1.0)
+    assert (s, c) == (0.0, 0) and not dh.any() and not dw.any()
