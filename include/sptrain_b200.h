@@ -1,0 +1,207 @@
+/*
+ * sptrain_b200 — C-ABI of the B200-native ALST (arXiv 2506.13996) sequence-parallel layer step.
+ *
+ * The reference's public surface for this path is the C++ namespace `sptrain`
+ * (/root/reference/proj/include/sptrain/*.hpp) plus the operations SPEC.md specifies on top of it
+ * (plan_head_shards, seq_to_head, head_to_seq, replicate_kv, ulysses_attention, tiled_mlp,
+ * tiled_logits_loss, cross_entropy, preshift/shard/pad, all_to_all, all_reduce_sum).  Each entry
+ * point below names the reference interface it replaces.  Plain pointers and sizes only; every
+ * device pointer is caller-owned; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Errors: every call returns spt_status (the errors.hpp:12-72 taxonomy) and sets a thread-local
+ * message readable with spt_last_error().  There is no CPU fallback: without a usable sm_100a
+ * device the compute entry points fail with SPT_ERR_CUDA.
+ *
+ * Integration notes (ctypes / C++ bindings): see INTEGRATION.md.
+ */
+#ifndef SPTRAIN_B200_H
+#define SPTRAIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:12-72 -> status codes */
+typedef enum {
+    SPT_OK = 0,
+    SPT_ERR_SHAPE = 1,       /* errors.hpp:19 ShapeError */
+    SPT_ERR_VALIDATION = 2,  /* errors.hpp:13 ValidationError (labels, position ids, head plans) */
+    SPT_ERR_COLLECTIVE = 3,  /* errors.hpp:25 CollectiveError */
+    SPT_ERR_PROTOCOL = 4,    /* errors.hpp:31 ProtocolError (NCCL async error / timeout) */
+    SPT_ERR_OOM = 5,         /* errors.hpp:55 SimulatedOomError (ledger budget) or cudaMalloc failure */
+    SPT_ERR_CUDA = 6,        /* CUDA runtime / driver failure, missing device */
+    SPT_ERR_CONFIG = 7,      /* errors.hpp:68 ConfigError */
+    SPT_ERR_DETERMINISM = 8, /* errors.hpp:37 DeterminismError */
+    SPT_ERR_INTERNAL = 9
+} spt_status;
+
+const char* spt_last_error(void);
+const char* spt_version(void);
+
+/* ============================ host-only logic (no GPU needed) ============================ */
+
+/* SPEC.md:286-292 HeadShardPlan */
+typedef struct {
+    int32_t sp_degree;
+    int32_t q_heads;
+    int32_t kv_heads;
+    int32_t q_heads_per_rank;
+    int32_t kv_heads_per_rank;
+    int32_t kv_replication; /* r */
+} spt_head_shard_plan;
+
+/* SPEC.md:296-305 plan_head_shards. Rejects Hq % P != 0 ("q_heads not divisible by SP degree"),
+ * Hkv >= P with Hkv % P != 0, and P % Hkv != 0 when Hkv < P, with SPT_ERR_VALIDATION. */
+spt_status spt_plan_head_shards(int32_t q_heads, int32_t kv_heads, int32_t sp_degree, spt_head_shard_plan* out);
+/* Global head indices rank `rank` owns after seq_to_head. kind 0 = q heads, 1 = kv heads. */
+spt_status spt_plan_heads_of(const spt_head_shard_plan* plan, int32_t rank, int32_t kind, int32_t* out_heads,
+                             int32_t capacity, int32_t* n_out);
+
+/* SPEC.md:512-519 preshift_labels: out[i] = labels[i+1], out[s-1] = -100. */
+spt_status spt_preshift_labels(const int64_t* labels, int64_t s, int64_t* out);
+/* SPEC.md:531-535 pad_to_multiple: returns the padded length; fills the tail (token 0, label -100,
+ * isolated position run) into the caller's buffers when they have room for it (cap >= padded). */
+spt_status spt_pad_to_multiple(int64_t* input_ids, int64_t* position_ids, int64_t* shift_labels, int64_t s,
+                               int32_t sp_degree, int64_t cap, int64_t* padded_len);
+/* SPEC.md:243-251 derive_block_causal_mask_predicate, host validation + start index per token. */
+spt_status spt_block_causal_starts(const int64_t* position_ids, int64_t s, int64_t* starts_out);
+
+/* All-to-all schedule of the Ulysses reshard for one rank.
+ * direction 0 = seq_to_head of fused QKV, 1 = head_to_seq of O, 2 = seq_to_head of dO,
+ * 3 = head_to_seq of dQKV.  Element counts (bf16) per peer, in rank order. */
+spt_status spt_a2a_counts(const spt_head_shard_plan* plan, int64_t s_loc, int32_t head_dim, int32_t direction,
+                          int64_t* send_counts, int64_t* recv_counts);
+
+/* ==================================== device kernels ==================================== */
+
+/* matmul on tcgen05: C[m,n] = alpha * sum_k A(m,k) B(n,k) (+ residual | + C).
+ * A(m,k) = A[m*lda+k] if !a_mn_major else A[k*lda+m]; same for B. c_f32: C is fp32 else bf16.
+ * accumulate: fp32 C += result. residual: bf16 [M, ldr] added (bf16 output only). N % 64 == 0. */
+spt_status spt_gemm_bf16(const void* A, int64_t lda, int32_t a_mn_major, const void* B, int64_t ldb,
+                         int32_t b_mn_major, void* C, int64_t ldc, int32_t c_f32, int32_t accumulate,
+                         const void* residual, int64_t ldr, int64_t M, int64_t N, int64_t K, float alpha, void* stream);
+
+/* RMSNorm. y = x * rstd * gamma, rstd fp32 [n]. */
+spt_status spt_rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int64_t n, int64_t h, float eps,
+                           void* stream);
+/* dx = dres + d(rmsnorm)(dy);  dgamma_accum (fp32 [h]) += sum_t dy*xhat, deterministic two-stage.
+ * dres may be NULL. workspace: spt_rmsnorm_bwd_workspace(n, h) bytes. */
+size_t spt_rmsnorm_bwd_workspace(int64_t n, int64_t h);
+spt_status spt_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy, const void* dres,
+                           void* dx, float* dgamma_accum, void* workspace, int64_t n, int64_t h, void* stream);
+
+/* seq_to_head send side (K1): qkv [s_loc, heads_in, d] -> send [P][s_loc][heads_out][d] with
+ * send[j][t][a] = qkv[t][head_map[j*heads_out + a]] (kv replication = repeated head ids).
+ * head_map is a DEVICE int32 array of P*heads_out entries. */
+spt_status spt_reshard_pack(const void* src, int64_t s_loc, int32_t heads_in, int32_t head_dim, int32_t P,
+                            int32_t heads_out, const int32_t* head_map, void* dst, void* stream);
+/* head_to_seq receive side (K2): recv [P][s_loc][heads_in][d] -> out [s_loc][heads_out][d];
+ * out[t][h] = sum over the (src rank, slot) pairs listed for h, in rank order (replicate_kv backward,
+ * SPEC.md:326).  gather: DEVICE int32 [heads_out][max_src] of (rank*heads_in + slot), -1 = unused. */
+spt_status spt_reshard_unpack(const void* recv, int64_t s_loc, int32_t heads_in, int32_t head_dim, int32_t P,
+                              int32_t heads_out, const int32_t* gather, int32_t max_src, void* dst, void* stream);
+
+/* Inner attention callback: causal GQA flash attention over the full
+ * sequence for the local heads.  qkv: [s][hq + 2*hkv][d] bf16 (q heads, k heads, v heads);
+ * seg_start: DEVICE int32 [s] start of each token's packed run, or NULL for plain causal.
+ * o: [s][hq][d] bf16, lse: [hq][s] fp32. */
+spt_status spt_attn_fwd(const void* qkv, int64_t s, int32_t hq, int32_t hkv, int32_t head_dim,
+                        const int32_t* seg_start, float scale, void* o, float* lse, void* stream);
+/* Deterministic backward: dqkv [s][hq + 2*hkv][d] bf16.  workspace: spt_attn_bwd_workspace bytes. */
+size_t spt_attn_bwd_workspace(int64_t s, int32_t hq, int32_t hkv, int32_t head_dim);
+spt_status spt_attn_bwd(const void* qkv, const void* o, const float* lse, const void* dout, int64_t s, int32_t hq,
+                        int32_t hkv, int32_t head_dim, const int32_t* seg_start, float scale, void* dqkv,
+                        void* workspace, void* stream);
+
+/* Label pre-pass of cross_entropy: count of non-ignored labels (int64, added to
+ * *count_accum) and a device error flag set to 1 when a label is outside [0,V) U {-100}. */
+spt_status spt_label_stats(const int64_t* labels, int64_t n, int64_t vocab, int64_t* count_accum, int32_t* err_flag,
+                           void* stream);
+/* position_ids -> run starts (int32) + device error flag for malformed runs. */
+spt_status spt_segment_starts(const int64_t* position_ids, int64_t n, int32_t* starts, int32_t* err_flag,
+                              void* stream);
+
+/* tiled_logits_loss fused fwd+bwd: for each tile of `tile_n` tokens,
+ * logits = x W^T (fp32, [tile_n, V] workspace only), CE (sum, count), dlogits scaled by
+ * *grad_scale_dev (1/global count, device scalar), dx = dlogits W (bf16), dW (fp32) +=
+ * dlogits^T x in ascending tile order.  loss_sum_accum (fp64 device scalar) += sum of NLL.
+ * dw_accumulate: 0 overwrites dW with the first tile's contribution. */
+size_t spt_flce_workspace(int64_t tile_n, int64_t vocab);
+spt_status spt_flce(const void* x, const void* w, const int64_t* labels, int64_t n, int64_t h, int64_t vocab,
+                    int64_t tile_n, const float* grad_scale_dev, double* loss_sum_accum, void* dx, float* dw,
+                    int32_t dw_accumulate, int32_t* err_flag, void* workspace, void* stream);
+
+/* tiled_mlp. wgu: [2I, h] bf16 with gate/up rows interleaved in blocks of 32
+ * (rows 64j..64j+31 = W_gate[32j..], rows 64j+32..64j+63 = W_up[32j..]); wd: [h, I].
+ * Forward: y = x_res + W_d(silu(W_g x) * W_u x) per tile (x_res may be NULL).  Backward recomputes
+ * gate/up per tile and accumulates dwgu / dwd (fp32) in ascending tile order. */
+size_t spt_mlp_workspace(int64_t tile_n, int64_t inter);
+spt_status spt_mlp_fwd(const void* x, const void* wgu, const void* wd, const void* x_res, void* y, int64_t n, int64_t h,
+                       int64_t inter, int64_t tile_n, void* workspace, void* stream);
+spt_status spt_mlp_bwd(const void* x, const void* wgu, const void* wd, const void* dy, void* dx, float* dwgu,
+                       float* dwd, int32_t accumulate, int64_t n, int64_t h, int64_t inter, int64_t tile_n,
+                       void* workspace, void* stream);
+
+/* ===================================== communicator ===================================== */
+
+/* ProcessGroup over NCCL (one process per GPU) or a loopback group of P virtual
+ * ranks on one GPU (the in-process SPMD of SPEC.md:183, with device-to-device copies). */
+typedef struct spt_comm spt_comm;
+spt_status spt_comm_unique_id(uint8_t out_id[128]);
+spt_status spt_comm_init_rank(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, spt_comm** out);
+spt_status spt_comm_init_loopback(int32_t nranks, int32_t device, spt_comm** out);
+spt_status spt_comm_destroy(spt_comm* comm);
+/* CommStats as JSON: per collective call count and bytes sent per rank. */
+spt_status spt_comm_stats_json(spt_comm* comm, char* buf, size_t cap);
+
+/* ================================= layer step engine ================================= */
+
+/* ModelConfig for one layer + lm_head; head_dim explicit. */
+typedef struct {
+    int32_t hidden;
+    int32_t q_heads;
+    int32_t kv_heads;
+    int32_t head_dim;
+    int32_t intermediate;
+    int64_t vocab;
+    int64_t seq_len;   /* global sequence length (sum over ranks), bs = 1 */
+    int32_t mlp_tiles; /* 0 -> ceil(s_loc / hidden) */
+    int64_t loss_tile; /* tokens per logits tile, 0 -> auto */
+    float rms_eps;     /* 0 -> 1e-5 */
+    int32_t packed;    /* 1: block-causal attention from position_ids */
+    float lr;          /* >0: plain SGD update of the bf16 weights at the end of the step */
+} spt_layer_config;
+
+typedef struct spt_layer spt_layer;
+spt_status spt_layer_create(const spt_layer_config* cfg, spt_comm* comm, spt_layer** out);
+spt_status spt_layer_destroy(spt_layer* layer);
+/* name in {g1, wqkv, wo, g2, wg, wu, wd, g3, wlm}; data = bf16 bits in [out, in] row-major. */
+spt_status spt_layer_set_param(spt_layer* layer, const char* name, const void* data, int32_t data_on_host);
+/* One fwd+bwd step.  x: bf16 [local_ranks * s_loc, hidden] (loopback: the whole sequence),
+ * shift_labels / position_ids: int64 [local_ranks * s_loc] (already pre-shifted).
+ * inputs_on_host: 1 -> host buffers (copied in inside the call), 0 -> device buffers.
+ * loss_out / count_out are host scalars (global mean loss and global valid count). */
+spt_status spt_layer_step(spt_layer* layer, const void* x, const int64_t* shift_labels, const int64_t* position_ids,
+                          int32_t inputs_on_host, float* loss_out, int64_t* count_out, void* stream);
+/* Same step, but leaves loss/count on the device (no host sync); read with spt_layer_read_loss. */
+spt_status spt_layer_step_async(spt_layer* layer, const void* x, const int64_t* shift_labels,
+                                const int64_t* position_ids, int32_t inputs_on_host, void* stream);
+spt_status spt_layer_read_loss(spt_layer* layer, float* loss_out, int64_t* count_out, void* stream);
+/* fp32 weight gradient (SP-group all-reduced) copied to host [out, in]. */
+spt_status spt_layer_get_grad(spt_layer* layer, const char* name, float* host_out);
+/* d loss / d x (bf16 bits, same layout as x) copied to host. */
+spt_status spt_layer_get_dx(spt_layer* layer, void* host_out);
+/* MemoryLedger::summary_json (ledger.hpp:85) of the device tier + cudaMemGetInfo cross-check. */
+spt_status spt_layer_memory_json(spt_layer* layer, char* buf, size_t cap);
+/* Per-phase CUDA-event timings of the last step (ms) as JSON (requires spt_layer_set_profiling(1)). */
+spt_status spt_layer_set_profiling(spt_layer* layer, int32_t on);
+spt_status spt_layer_timing_json(spt_layer* layer, char* buf, size_t cap);
+/* Number of CUDA kernels this library launched since load (gpu_launches evidence). */
+int64_t spt_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPTRAIN_B200_H */

@@ -1,0 +1,327 @@
+"""B200-native ALST (arXiv 2506.13996) sequence-parallel layer step — Python host mirror.
+
+The product is `libsptrain_b200.so` (C++ host engine + sm_100a CUDA kernels behind the C-ABI in
+`include/sptrain_b200.h`).  This module is a thin ctypes binding that mirrors the reference's
+operation names (SPEC.md: plan_head_shards, preshift_labels, pad_to_multiple, ProcessGroup,
+ulysses layer step).  There is no CPU fallback: if the library is missing or the device is not
+sm_100a the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsptrain_b200.so")
+
+SPT_OK = 0
+STATUS_NAMES = {0: "OK", 1: "SHAPE", 2: "VALIDATION", 3: "COLLECTIVE", 4: "PROTOCOL", 5: "OOM", 6: "CUDA",
+                7: "CONFIG", 8: "DETERMINISM", 9: "INTERNAL"}
+
+
+class SptError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{STATUS_NAMES.get(status, status)}] {msg}")
+        self.status = status
+
+
+class ValidationError(SptError, ValueError):
+    """errors.hpp:13"""
+
+
+class ShapeError(ValidationError):
+    """errors.hpp:19"""
+
+
+class ConfigError(SptError):
+    """errors.hpp:68"""
+
+
+_EXC = {1: ShapeError, 2: ValidationError, 7: ConfigError}
+
+_lib = None
+
+
+class HeadShardPlan(C.Structure):
+    """SPEC.md:286-292"""
+
+    _fields_ = [("sp_degree", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32),
+                ("q_heads_per_rank", C.c_int32), ("kv_heads_per_rank", C.c_int32), ("kv_replication", C.c_int32)]
+
+
+class LayerConfig(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("intermediate", C.c_int32), ("vocab", C.c_int64), ("seq_len", C.c_int64), ("mlp_tiles", C.c_int32),
+                ("loss_tile", C.c_int64), ("rms_eps", C.c_float), ("packed", C.c_int32), ("lr", C.c_float)]
+
+
+P = C.c_void_p
+I32, I64, F32, SZ = C.c_int32, C.c_int64, C.c_float, C.c_size_t
+PI32, PI64, PF32 = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_float)
+
+SIGNATURES = {
+    "spt_last_error": (C.c_char_p, []),
+    "spt_version": (C.c_char_p, []),
+    "spt_plan_head_shards": (I32, [I32, I32, I32, C.POINTER(HeadShardPlan)]),
+    "spt_plan_heads_of": (I32, [C.POINTER(HeadShardPlan), I32, I32, PI32, I32, PI32]),
+    "spt_preshift_labels": (I32, [P, I64, P]),
+    "spt_pad_to_multiple": (I32, [P, P, P, I64, I32, I64, PI64]),
+    "spt_block_causal_starts": (I32, [P, I64, P]),
+    "spt_a2a_counts": (I32, [C.POINTER(HeadShardPlan), I64, I32, I32, P, P]),
+    "spt_gemm_bf16": (I32, [P, I64, I32, P, I64, I32, P, I64, I32, I32, P, I64, I64, I64, I64, F32, P]),
+    "spt_rmsnorm_fwd": (I32, [P, P, P, P, I64, I64, F32, P]),
+    "spt_rmsnorm_bwd_workspace": (SZ, [I64, I64]),
+    "spt_rmsnorm_bwd": (I32, [P, P, P, P, P, P, P, P, I64, I64, P]),
+    "spt_reshard_pack": (I32, [P, I64, I32, I32, I32, I32, P, P, P]),
+    "spt_reshard_unpack": (I32, [P, I64, I32, I32, I32, I32, P, I32, P, P]),
+    "spt_attn_fwd": (I32, [P, I64, I32, I32, I32, P, F32, P, P, P]),
+    "spt_attn_bwd_workspace": (SZ, [I64, I32, I32, I32]),
+    "spt_attn_bwd": (I32, [P, P, P, P, I64, I32, I32, I32, P, F32, P, P, P]),
+    "spt_label_stats": (I32, [P, I64, I64, P, P, P]),
+    "spt_segment_starts": (I32, [P, I64, P, P, P]),
+    "spt_flce_workspace": (SZ, [I64, I64]),
+    "spt_flce": (I32, [P, P, P, I64, I64, I64, I64, P, P, P, P, I32, P, P, P]),
+    "spt_mlp_workspace": (SZ, [I64, I64]),
+    "spt_mlp_fwd": (I32, [P, P, P, P, P, I64, I64, I64, I64, P, P]),
+    "spt_mlp_bwd": (I32, [P, P, P, P, P, P, P, I32, I64, I64, I64, I64, P, P]),
+    "spt_comm_unique_id": (I32, [P]),
+    "spt_comm_init_rank": (I32, [P, I32, I32, I32, C.POINTER(P)]),
+    "spt_comm_init_loopback": (I32, [I32, I32, C.POINTER(P)]),
+    "spt_comm_destroy": (I32, [P]),
+    "spt_comm_stats_json": (I32, [P, C.c_char_p, SZ]),
+    "spt_layer_create": (I32, [C.POINTER(LayerConfig), P, C.POINTER(P)]),
+    "spt_layer_destroy": (I32, [P]),
+    "spt_layer_set_param": (I32, [P, C.c_char_p, P, I32]),
+    "spt_layer_step": (I32, [P, P, P, P, I32, PF32, PI64, P]),
+    "spt_layer_step_async": (I32, [P, P, P, P, I32, P]),
+    "spt_layer_read_loss": (I32, [P, PF32, PI64, P]),
+    "spt_layer_get_grad": (I32, [P, C.c_char_p, P]),
+    "spt_layer_get_dx": (I32, [P, P]),
+    "spt_layer_memory_json": (I32, [P, C.c_char_p, SZ]),
+    "spt_layer_set_profiling": (I32, [P, I32]),
+    "spt_layer_timing_json": (I32, [P, C.c_char_p, SZ]),
+    "spt_kernel_launch_count": (I64, []),
+}
+
+
+def lib():
+    """Load the in-tree library (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing — run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int):
+    if status != SPT_OK:
+        msg = lib().spt_last_error().decode()
+        raise _EXC.get(status, SptError)(status, msg)
+
+
+def ptr(t) -> int | None:
+    """Raw pointer of a torch tensor / numpy array / int / None."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+# ----------------------------------------------------------------- host-only mirror (SPEC ops)
+def plan_head_shards(q_heads: int, kv_heads: int, sp: int) -> HeadShardPlan:
+    """SPEC.md:296-305"""
+    p = HeadShardPlan()
+    check(lib().spt_plan_head_shards(q_heads, kv_heads, sp, C.byref(p)))
+    return p
+
+
+def heads_of(plan: HeadShardPlan, rank: int, kind: int) -> list[int]:
+    buf = (C.c_int32 * 1024)()
+    n = C.c_int32()
+    check(lib().spt_plan_heads_of(C.byref(plan), rank, kind, buf, 1024, C.byref(n)))
+    return list(buf[: n.value])
+
+
+def preshift_labels(labels):
+    """SPEC.md:512-519"""
+    import numpy as np
+
+    a = np.ascontiguousarray(labels, dtype=np.int64)
+    out = np.empty_like(a)
+    check(lib().spt_preshift_labels(ptr(a), a.size, ptr(out)))
+    return out
+
+
+def pad_to_multiple(input_ids, position_ids, shift_labels, sp: int):
+    """SPEC.md:531-535"""
+    import numpy as np
+
+    s = len(input_ids)
+    n = C.c_int64()
+    check(lib().spt_pad_to_multiple(None, None, None, s, sp, 0, C.byref(n)))
+    bufs = []
+    for a in (input_ids, position_ids, shift_labels):
+        b = np.zeros(n.value, dtype=np.int64)
+        b[:s] = a
+        bufs.append(b)
+    check(lib().spt_pad_to_multiple(ptr(bufs[0]), ptr(bufs[1]), ptr(bufs[2]), s, sp, n.value, C.byref(n)))
+    return tuple(bufs)
+
+
+def block_causal_starts(position_ids):
+    import numpy as np
+
+    a = np.ascontiguousarray(position_ids, dtype=np.int64)
+    out = np.empty_like(a)
+    check(lib().spt_block_causal_starts(ptr(a), a.size, ptr(out)))
+    return out
+
+
+def a2a_counts(plan: HeadShardPlan, s_loc: int, head_dim: int, direction: int):
+    import numpy as np
+
+    s = np.zeros(plan.sp_degree, np.int64)
+    r = np.zeros(plan.sp_degree, np.int64)
+    check(lib().spt_a2a_counts(C.byref(plan), s_loc, head_dim, direction, ptr(s), ptr(r)))
+    return s, r
+
+
+# ----------------------------------------------------------------- process group + layer engine
+class ProcessGroup:
+    """SPEC.md:131-136 over NCCL (one process per GPU) or loopback virtual ranks on one GPU."""
+
+    def __init__(self, handle, world_size: int, rank: int, loopback: bool):
+        self.handle, self.world_size, self.rank, self.loopback = handle, world_size, rank, loopback
+
+    @classmethod
+    def loopback_group(cls, world_size: int, device: int = 0) -> "ProcessGroup":
+        h = C.c_void_p()
+        check(lib().spt_comm_init_loopback(world_size, device, C.byref(h)))
+        return cls(h, world_size, 0, True)
+
+    @classmethod
+    def nccl_group(cls, unique_id: bytes, world_size: int, rank: int, device: int) -> "ProcessGroup":
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib().spt_comm_init_rank(buf, world_size, rank, device, C.byref(h)))
+        return cls(h, world_size, rank, False)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().spt_comm_unique_id(buf))
+        return bytes(buf)
+
+    def stats(self) -> dict:
+        b = C.create_string_buffer(1 << 16)
+        check(lib().spt_comm_stats_json(self.handle, b, len(b)))
+        return json.loads(b.value.decode())
+
+    def close(self):
+        if self.handle:
+            check(lib().spt_comm_destroy(self.handle))
+            self.handle = None
+
+
+@dataclass
+class ModelShape:
+    hidden: int
+    q_heads: int
+    kv_heads: int
+    head_dim: int
+    intermediate: int
+    vocab: int
+
+
+TINY = ModelShape(256, 8, 2, 32, 1024, 32000)
+LLAMA8B = ModelShape(4096, 32, 8, 128, 14336, 128256)
+QWEN32B = ModelShape(5120, 64, 8, 128, 25600, 151936)
+
+PARAM_NAMES = ("g1", "wqkv", "wo", "g2", "wg", "wu", "wd", "g3", "wlm")
+
+
+class UlyssesLayerStep:
+    """One decoder layer + lm_head fwd+bwd with Ulysses SP, TiledMLP and tiled logits+loss."""
+
+    def __init__(self, shape: ModelShape, seq_len: int, group: ProcessGroup, mlp_tiles: int = 0,
+                 loss_tile: int = 0, packed: bool = False, lr: float = 0.0, rms_eps: float = 1e-5):
+        self.shape, self.seq_len, self.group = shape, seq_len, group
+        self.cfg = LayerConfig(shape.hidden, shape.q_heads, shape.kv_heads, shape.head_dim, shape.intermediate,
+                               shape.vocab, seq_len, mlp_tiles, loss_tile, rms_eps, int(packed), lr)
+        h = C.c_void_p()
+        check(lib().spt_layer_create(C.byref(self.cfg), group.handle, C.byref(h)))
+        self.handle = h
+
+    def set_param(self, name: str, data, on_host: bool | None = None):
+        if on_host is None:
+            on_host = not hasattr(data, "is_cuda") or not data.is_cuda
+        check(lib().spt_layer_set_param(self.handle, name.encode(), ptr(data), int(on_host)))
+
+    def step(self, x, shift_labels, position_ids=None, on_host: bool | None = None, stream=None):
+        if on_host is None:
+            on_host = not hasattr(x, "is_cuda") or not x.is_cuda
+        loss, cnt = C.c_float(), C.c_int64()
+        check(lib().spt_layer_step(self.handle, ptr(x), ptr(shift_labels), ptr(position_ids), int(on_host),
+                                   C.byref(loss), C.byref(cnt), ptr(stream)))
+        return loss.value, cnt.value
+
+    def step_async(self, x, shift_labels, position_ids=None, on_host=False, stream=None):
+        check(lib().spt_layer_step_async(self.handle, ptr(x), ptr(shift_labels), ptr(position_ids), int(on_host),
+                                         ptr(stream)))
+
+    def read_loss(self, stream=None):
+        loss, cnt = C.c_float(), C.c_int64()
+        check(lib().spt_layer_read_loss(self.handle, C.byref(loss), C.byref(cnt), ptr(stream)))
+        return loss.value, cnt.value
+
+    def grad(self, name: str):
+        import numpy as np
+
+        s = self.shape
+        shapes = {"g1": (s.hidden,), "g2": (s.hidden,), "g3": (s.hidden,),
+                  "wqkv": ((s.q_heads + 2 * s.kv_heads) * s.head_dim, s.hidden),
+                  "wo": (s.hidden, s.q_heads * s.head_dim), "wg": (s.intermediate, s.hidden),
+                  "wu": (s.intermediate, s.hidden), "wd": (s.hidden, s.intermediate), "wlm": (s.vocab, s.hidden)}
+        out = np.empty(shapes[name], dtype=np.float32)
+        check(lib().spt_layer_get_grad(self.handle, name.encode(), ptr(out)))
+        return out
+
+    def dx_bits(self, n_tokens: int):
+        import numpy as np
+
+        out = np.empty((n_tokens, self.shape.hidden), dtype=np.uint16)
+        check(lib().spt_layer_get_dx(self.handle, ptr(out)))
+        return out
+
+    def memory(self) -> dict:
+        b = C.create_string_buffer(1 << 16)
+        check(lib().spt_layer_memory_json(self.handle, b, len(b)))
+        return json.loads(b.value.decode())
+
+    def set_profiling(self, on: bool):
+        check(lib().spt_layer_set_profiling(self.handle, int(on)))
+
+    def timing(self) -> dict:
+        b = C.create_string_buffer(1 << 16)
+        check(lib().spt_layer_timing_json(self.handle, b, len(b)))
+        return json.loads(b.value.decode())
+
+    def close(self):
+        if self.handle:
+            check(lib().spt_layer_destroy(self.handle))
+            self.handle = None
+
+
+def kernel_launch_count() -> int:
+    return lib().spt_kernel_launch_count()

@@ -1,0 +1,56 @@
+"""Build libsptrain_b200.so in-tree for sm_100a (nvcc cross-compiles; no GPU needed)."""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libsptrain_b200.so")
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
+         "-I" + os.path.join(ROOT, "include"), "-I/usr/include"]
+SOURCES = ["util.cpp", "plan.cpp", "comm.cpp", "gemm.cu", "kernels.cu", "attention.cu", "tiled.cu", "engine.cu"]
+DEPS_HDR = [f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + ["../../include/sptrain_b200.h"]
+
+
+def _newest_header() -> float:
+    return max(os.path.getmtime(os.path.join(CSRC, f)) for f in DEPS_HDR)
+
+
+def _compile(src: str, verbose: bool) -> str:
+    out = os.path.join(OBJ, src + ".o")
+    s = os.path.join(CSRC, src)
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(s), _newest_header()):
+        return out
+    cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", out]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    if verbose and r.stderr:
+        print(r.stderr)
+    return out
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,691 @@
+// The sptrain layer-step engine: one Llama-shaped decoder layer + lm_head, fwd + bwd, Ulysses SP.
+//
+//   forward:  x1 = x + Wo . ulysses_attention(Wqkv . rms1(x))
+//                                  x2 = x1 + tiled_mlp(rms2(x1))
+//                                  (loss_sum, count) = tiled_logits_loss(rms3(x2))
+//   backward : explicit reverse of the above (the tape order of autograd.hpp:14-17, fixed at build
+//              time instead of recorded), weight grads all-reduced over the SP group.
+//
+// ulysses_attention: K1 pack -> all_to_all (NCCL / loopback) -> attention over the
+// full sequence for the local heads -> all_to_all -> K2 unpack; the backward mirrors it with the
+// replicate_kv reduction folded into K2.  With the payload layout of SPEC.md:351 the
+// seq_to_head receive buffer IS the attention input ([s][heads][d]) and the head_to_seq send buffer
+// IS the attention output, so exactly one permutation kernel runs per direction.
+//
+// Memory: every device byte goes through a MemoryLedger-compatible device ledger (ledger.hpp:37-113
+// semantics: per-tag live/peak, largest_single, budgets, summary_json) — the peak-HBM observable.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <unordered_map>
+#include <vector>
+
+#include "comm.h"
+#include "common.h"
+#include "gemm.cuh"
+#include "launch.h"
+#include "plan.h"
+
+namespace spt {
+
+size_t flce_workspace(int64_t tile_n, int64_t V);
+void flce(const void* x, const void* w, const int64_t* labels, int64_t n, int64_t h, int64_t V, int64_t tile_n,
+          const float* scale_dev, double* loss_sum_accum, void* dx, float* dw, bool dw_accumulate, int32_t* err,
+          void* ws, cudaStream_t st);
+size_t mlp_workspace(int64_t tile_n, int64_t I);
+void mlp_fwd(const void* x, const void* wgu, const void* wd, const void* x_res, void* y, int64_t n, int64_t h,
+             int64_t I, int64_t tile_n, void* ws, cudaStream_t st);
+void mlp_bwd(const void* x, const void* wgu, const void* wd, const void* dy, void* dx, float* dwgu, float* dwd,
+             bool accumulate, int64_t n, int64_t h, int64_t I, int64_t tile_n, void* ws, cudaStream_t st);
+
+// ---------------------------------------------------------------- device ledger (ledger.hpp:19-113)
+enum Tag { kWeights = 0, kGrads, kOptimizer, kActivationCkpt, kLogits, kWorkspace, kCommBuffer, kNumTags };
+static const char* tag_name(int t) {
+    static const char* n[] = {"weights", "grads", "optimizer", "activation-checkpoint", "logits", "workspace",
+                              "comm-buffer"};
+    return n[t];
+}
+
+struct DeviceLedger {
+    uint64_t live = 0, peak = 0, budget = 0;
+    uint64_t tag_live[kNumTags] = {}, tag_peak[kNumTags] = {}, largest[kNumTags] = {};
+    uint64_t events = 0;
+    std::unordered_map<void*, std::pair<int, size_t>> allocs;
+
+    void* alloc(size_t bytes, int tag) {
+        if (budget && live + bytes > budget)
+            SPT_THROW(SPT_ERR_OOM, "simulated device OOM: required " + std::to_string(live + bytes) +
+                                       " bytes, available " + std::to_string(budget));
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+        if (e != cudaSuccess)
+            SPT_THROW(SPT_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+        live += bytes;
+        peak = std::max(peak, live);
+        tag_live[tag] += bytes;
+        tag_peak[tag] = std::max(tag_peak[tag], tag_live[tag]);
+        largest[tag] = std::max<uint64_t>(largest[tag], bytes);
+        allocs[p] = {tag, bytes};
+        ++events;
+        return p;
+    }
+    void release(void* p) {
+        auto it = allocs.find(p);
+        if (it == allocs.end()) return;
+        live -= it->second.second;
+        tag_live[it->second.first] -= it->second.second;
+        cudaFree(p);
+        allocs.erase(it);
+        ++events;
+    }
+    void release_all() {
+        std::vector<void*> ps;
+        for (auto& kv : allocs) ps.push_back(kv.first);
+        for (void* p : ps) release(p);
+    }
+    std::string summary_json() const {
+        std::ostringstream os;
+        os << "{\"device\":{\"live_bytes\":" << live << ",\"peak_bytes\":" << peak << ",\"tags\":{";
+        for (int t = 0; t < kNumTags; ++t)
+            os << (t ? "," : "") << "\"" << tag_name(t) << "\":{\"live\":" << tag_live[t] << ",\"peak\":" << tag_peak[t]
+               << "}";
+        os << "}},\"largest_single\":{";
+        for (int t = 0; t < kNumTags; ++t) os << (t ? "," : "") << "\"" << tag_name(t) << "\":" << largest[t];
+        os << "},\"events\":" << events;
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+            os << ",\"cuda_mem_used_bytes\":" << (tot - fr) << ",\"cuda_mem_total_bytes\":" << tot;
+        os << "}";
+        return os.str();
+    }
+};
+
+// ---------------------------------------------------------------- per-kernel-class event timing
+struct Prof {
+    bool on = false;
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+        double flops, bytes;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    static constexpr int NCLS = 8;
+    static const char* name(int c) {
+        static const char* n[] = {"gemm", "attn_fwd", "attn_bwd", "rmsnorm", "reshard", "ce_rows", "comm", "other"};
+        return n[c];
+    }
+    cudaEvent_t ev() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            SPT_CUDA(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void reset() {
+        recs.clear();
+        used = 0;
+    }
+    template <class F>
+    void run(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
+        if (!on) {
+            f();
+            return;
+        }
+        cudaEvent_t a = ev(), b = ev();
+        SPT_CUDA(cudaEventRecord(a, st));
+        f();
+        SPT_CUDA(cudaEventRecord(b, st));
+        recs.push_back({cls, a, b, flops, bytes});
+    }
+    std::string json() {
+        double ms[NCLS] = {}, fl[NCLS] = {}, by[NCLS] = {};
+        int cnt[NCLS] = {};
+        for (auto& r : recs) {
+            float t = 0;
+            SPT_CUDA(cudaEventSynchronize(r.b));
+            SPT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            ms[r.cls] += t;
+            fl[r.cls] += r.flops;
+            by[r.cls] += r.bytes;
+            cnt[r.cls] += 1;
+        }
+        std::ostringstream os;
+        os << "{";
+        for (int c = 0; c < NCLS; ++c)
+            os << (c ? "," : "") << "\"" << name(c) << "\":{\"ms\":" << ms[c] << ",\"launches\":" << cnt[c]
+               << ",\"flops\":" << fl[c] << ",\"bytes\":" << by[c] << "}";
+        os << "}";
+        return os.str();
+    }
+};
+enum { P_GEMM = 0, P_ATTN_F, P_ATTN_B, P_NORM, P_RESHARD, P_CE, P_COMM, P_OTHER };
+
+}  // namespace spt
+
+using namespace spt;
+
+struct Scalars {
+    double loss_sum;
+    int64_t count;
+    float scale;
+    float loss;
+    int32_t err_label;
+    int32_t err_pos;
+};
+
+struct RankBufs {
+    bf16 *x, *xn1, *qkv, *o, *x1, *xn2, *x2, *z;
+    float *rstd1, *rstd2, *rstd3, *lse;
+    int64_t *labels, *pos;
+    bf16 *send_qkv, *qkv_head, *o_head, *recv_o;
+    bf16 *dz, *dx1, *dO, *dx, *send_do, *do_head, *dqkv_head, *recv_dqkv, *dqkv;
+};
+
+struct spt_layer {
+    spt_layer_config cfg;
+    spt_comm* comm;
+    spt_head_shard_plan plan;
+    int P, L;
+    int64_t N, n_loc, h, I, V, qkv_out, qd, qkv_loc, hq_loc, hkv_loc, mlp_tile, loss_tile;
+    float eps;
+    DeviceLedger led;
+    Prof prof;
+    // weights
+    bf16 *g1, *wqkv, *wo, *g2, *wgu, *wd, *g3, *wlm;
+    // grads (one contiguous fp32 buffer; SP all-reduce is one call)
+    float* gbuf;
+    size_t gsize;
+    float *dg1, *dwqkv, *dwo, *dg2, *dwgu, *dwd, *dg3, *dwlm;
+    std::vector<RankBufs> rb;
+    void *ws_flce, *ws_mlp, *ws_rms, *ws_attn;
+    int32_t *map_qkv, *map_q, *gather_o, *gather_qkv;
+    int max_src_o, max_src_qkv;
+    int32_t* seg;
+    int64_t* pos_full;
+    Scalars* sc;
+    Scalars* sc_host;
+    cudaEvent_t ev_step0, ev_step1;
+    float last_step_ms = 0.f;
+
+    bf16* abf(int64_t n, int tag = kWorkspace) { return (bf16*)led.alloc((size_t)n * 2, tag); }
+    float* af32(int64_t n, int tag = kWorkspace) { return (float*)led.alloc((size_t)n * 4, tag); }
+};
+
+static void build_layer(spt_layer* Ly) {
+    auto& c = Ly->cfg;
+    spt_comm* cm = Ly->comm;
+    SPT_CHECK(c.hidden > 0 && c.q_heads > 0 && c.kv_heads > 0 && c.head_dim > 0 && c.intermediate > 0 && c.vocab >= 2,
+              SPT_ERR_CONFIG, "invalid layer config");
+    Ly->P = cm->nranks;
+    Ly->L = cm->local_ranks();
+    Ly->plan = plan_head_shards(c.q_heads, c.kv_heads, Ly->P);
+    SPT_CHECK(c.seq_len % Ly->P == 0, SPT_ERR_SHAPE,
+              "seq_len " + std::to_string(c.seq_len) + " not divisible by SP degree; pad_to_multiple first");
+    Ly->N = c.seq_len;
+    Ly->n_loc = c.seq_len / Ly->P;
+    Ly->h = c.hidden;
+    Ly->I = c.intermediate;
+    Ly->V = c.vocab;
+    Ly->qd = (int64_t)c.q_heads * c.head_dim;
+    Ly->qkv_out = (int64_t)(c.q_heads + 2 * c.kv_heads) * c.head_dim;
+    Ly->hq_loc = Ly->plan.q_heads_per_rank;
+    Ly->hkv_loc = Ly->plan.kv_heads_per_rank;
+    Ly->qkv_loc = Ly->hq_loc + 2 * Ly->hkv_loc;
+    Ly->eps = c.rms_eps > 0 ? c.rms_eps : 1e-5f;
+    SPT_CHECK(Ly->h % 64 == 0 && Ly->qkv_out % 64 == 0 && Ly->I % 32 == 0 && Ly->V % 64 == 0, SPT_ERR_CONFIG,
+              "hidden, qkv width and vocab must be multiples of 64, intermediate of 32");
+    SPT_CHECK(Ly->N % 128 == 0, SPT_ERR_CONFIG, "seq_len must be a multiple of 128 (attention tile)");
+    const int64_t mtiles = c.mlp_tiles > 0 ? c.mlp_tiles : std::max<int64_t>(1, (Ly->n_loc + Ly->h - 1) / Ly->h);
+    Ly->mlp_tile = (Ly->n_loc + mtiles - 1) / mtiles;  // SPEC.md:398 ceil(s/h) tiles
+    if (c.loss_tile > 0) Ly->loss_tile = std::min<int64_t>(c.loss_tile, Ly->n_loc);
+    else {
+        int64_t t = (int64_t)((2ll << 30) / (Ly->V * 4));  // tile_len * V * 4 <= 2 GiB
+        t = std::max<int64_t>(128, t / 128 * 128);
+        Ly->loss_tile = std::min<int64_t>(t, Ly->n_loc);
+    }
+    auto& L_ = Ly->led;
+    const int64_t h = Ly->h, I = Ly->I, V = Ly->V;
+    // weights
+    Ly->g1 = Ly->abf(h, kWeights);
+    Ly->wqkv = Ly->abf(Ly->qkv_out * h, kWeights);
+    Ly->wo = Ly->abf(h * Ly->qd, kWeights);
+    Ly->g2 = Ly->abf(h, kWeights);
+    Ly->wgu = Ly->abf(2 * I * h, kWeights);
+    Ly->wd = Ly->abf(h * I, kWeights);
+    Ly->g3 = Ly->abf(h, kWeights);
+    Ly->wlm = Ly->abf(V * h, kWeights);
+    // grads
+    const size_t sz[8] = {(size_t)h, (size_t)(Ly->qkv_out * h), (size_t)(h * Ly->qd), (size_t)h, (size_t)(2 * I * h),
+                          (size_t)(h * I), (size_t)h, (size_t)(V * h)};
+    size_t tot = 0;
+    for (size_t s : sz) tot += (s + 63) / 64 * 64;
+    Ly->gsize = tot;
+    Ly->gbuf = Ly->af32(tot, kGrads);
+    float* gp = Ly->gbuf;
+    float** dst[8] = {&Ly->dg1, &Ly->dwqkv, &Ly->dwo, &Ly->dg2, &Ly->dwgu, &Ly->dwd, &Ly->dg3, &Ly->dwlm};
+    for (int i = 0; i < 8; ++i) {
+        *dst[i] = gp;
+        gp += (sz[i] + 63) / 64 * 64;
+    }
+    // per-rank activations
+    const int64_t nl = Ly->n_loc, N = Ly->N, P = Ly->P;
+    Ly->rb.resize(Ly->L);
+    for (auto& r : Ly->rb) {
+        r.x = Ly->abf(nl * h, kActivationCkpt);
+        r.xn1 = Ly->abf(nl * h);
+        r.qkv = Ly->abf(nl * Ly->qkv_out);
+        r.o = Ly->abf(nl * Ly->qd);
+        r.x1 = Ly->abf(nl * h);
+        r.xn2 = Ly->abf(nl * h);
+        r.x2 = Ly->abf(nl * h);
+        r.z = Ly->abf(nl * h);
+        r.rstd1 = Ly->af32(nl);
+        r.rstd2 = Ly->af32(nl);
+        r.rstd3 = Ly->af32(nl);
+        r.lse = Ly->af32(Ly->hq_loc * N);
+        r.labels = (int64_t*)L_.alloc(nl * 8, kWorkspace);
+        r.pos = (int64_t*)L_.alloc(nl * 8, kWorkspace);
+        r.dz = Ly->abf(nl * h);
+        r.dx1 = Ly->abf(nl * h);
+        r.dO = Ly->abf(nl * Ly->qd);
+        r.dx = Ly->abf(nl * h);
+        if (P > 1) {
+            r.send_qkv = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
+            r.qkv_head = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
+            r.o_head = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
+            r.recv_o = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
+            r.send_do = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
+            r.do_head = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
+            r.dqkv_head = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
+            r.recv_dqkv = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
+            r.dqkv = Ly->abf(nl * Ly->qkv_out);
+        } else {
+            r.send_qkv = r.recv_o = r.send_do = r.recv_dqkv = nullptr;
+            r.qkv_head = r.qkv;
+            r.o_head = r.o;
+            r.do_head = r.dO;
+            r.dqkv = Ly->abf(nl * Ly->qkv_out);
+            r.dqkv_head = r.dqkv;
+        }
+    }
+    // workspaces (shared by local ranks; phases run back to back on one stream)
+    Ly->ws_flce = L_.alloc(flce_workspace(Ly->loss_tile, V), kLogits);
+    Ly->ws_mlp = L_.alloc(mlp_workspace(Ly->mlp_tile, I), kWorkspace);
+    Ly->ws_rms = L_.alloc(rmsnorm_bwd_workspace(nl, h), kWorkspace);
+    Ly->ws_attn = L_.alloc(attn_bwd_workspace(N, Ly->hq_loc, Ly->hkv_loc, c.head_dim), kWorkspace);
+    // reshard tables
+    auto up = [&](const std::vector<int32_t>& v) {
+        int32_t* d = (int32_t*)L_.alloc(v.size() * 4, kWorkspace);
+        SPT_CUDA(cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+        return d;
+    };
+    Ly->map_qkv = up(qkv_pack_map(Ly->plan));
+    Ly->map_q = up(q_pack_map(Ly->plan));
+    Ly->gather_o = up(o_gather_map(Ly->plan, &Ly->max_src_o));
+    Ly->gather_qkv = up(qkv_gather_map(Ly->plan, &Ly->max_src_qkv));
+    Ly->seg = c.packed ? (int32_t*)L_.alloc(N * 4, kWorkspace) : nullptr;
+    Ly->pos_full = c.packed ? (int64_t*)L_.alloc(N * 8, kWorkspace) : nullptr;
+    Ly->sc = (Scalars*)L_.alloc(sizeof(Scalars), kWorkspace);
+    SPT_CUDA(cudaMallocHost(&Ly->sc_host, sizeof(Scalars)));
+    SPT_CUDA(cudaEventCreate(&Ly->ev_step0));
+    SPT_CUDA(cudaEventCreate(&Ly->ev_step1));
+}
+
+static double gflop(int64_t m, int64_t n, int64_t k) { return 2.0 * (double)m * n * k; }
+
+static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, const int64_t* pos, bool on_host,
+                       cudaStream_t st) {
+    auto& c = Ly->cfg;
+    spt_comm* cm = Ly->comm;
+    const int L = Ly->L, P = Ly->P, d = c.head_dim;
+    const int64_t nl = Ly->n_loc, N = Ly->N, h = Ly->h, I = Ly->I, V = Ly->V, qd = Ly->qd, qo = Ly->qkv_out;
+    const int hq = Ly->hq_loc, hkv = Ly->hkv_loc;
+    const float scale = 1.f / std::sqrt((float)d);
+    Prof& pf = Ly->prof;
+    pf.reset();
+    SPT_CUDA(cudaEventRecord(Ly->ev_step0, st));
+    const cudaMemcpyKind kind = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+
+    // ---- inputs, label pre-pass, global count
+    SPT_CUDA(cudaMemsetAsync(Ly->sc, 0, sizeof(Scalars), st));
+    for (int r = 0; r < L; ++r) {
+        auto& b = Ly->rb[r];
+        SPT_CUDA(cudaMemcpyAsync(b.x, (const bf16*)x + r * nl * h, nl * h * 2, kind, st));
+        SPT_CUDA(cudaMemcpyAsync(b.labels, labels + r * nl, nl * 8, kind, st));
+        if (c.packed) SPT_CUDA(cudaMemcpyAsync(b.pos, pos + r * nl, nl * 8, kind, st));
+        label_stats(b.labels, nl, V, &Ly->sc->count, &Ly->sc->err_label, st);
+    }
+    cm->all_reduce("all_reduce_count", &Ly->sc->count, 1, ncclInt64, st);
+    finalize_scale(&Ly->sc->count, &Ly->sc->scale, st);
+    if (c.packed) {  // position_ids_full -> run starts
+        if (cm->loopback) {
+            for (int r = 0; r < L; ++r)
+                SPT_CUDA(cudaMemcpyAsync(Ly->pos_full + r * nl, Ly->rb[r].pos, nl * 8, cudaMemcpyDeviceToDevice, st));
+        } else {
+            cm->all_gather("all_gather_position_ids", Ly->rb[0].pos, Ly->pos_full, nl * 8, st);
+        }
+        segment_starts(Ly->pos_full, N, Ly->seg, &Ly->sc->err_pos, st);
+    }
+    SPT_CUDA(cudaMemsetAsync(Ly->dg1, 0, h * 4, st));
+    SPT_CUDA(cudaMemsetAsync(Ly->dg2, 0, h * 4, st));
+    SPT_CUDA(cudaMemsetAsync(Ly->dg3, 0, h * 4, st));
+
+    // ---- forward phase A: rms1, fused QKV projection, K1 pack
+    for (int r = 0; r < L; ++r) {
+        auto& b = Ly->rb[r];
+        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x, Ly->g1, b.xn1, b.rstd1, nl, h, Ly->eps, st); });
+        EpiParams e;
+        e.C = b.qkv;
+        e.ldc = qo;
+        pf.run(P_GEMM, gflop(nl, qo, h), 0, st, [&] { gemm({b.xn1, h, false}, {Ly->wqkv, h, false}, nl, qo, h, EPI_BF16, e, st); });
+        if (P > 1)
+            pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
+                reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv, st);
+            });
+    }
+    const size_t qkv_peer = (size_t)nl * Ly->qkv_loc * d * 2;
+    const size_t o_peer = (size_t)nl * hq * d * 2;
+    auto sends = [&](bf16* RankBufs::*m) {
+        std::vector<const void*> v;
+        for (auto& b : Ly->rb) v.push_back(b.*m);
+        return v;
+    };
+    auto recvs = [&](bf16* RankBufs::*m) {
+        std::vector<void*> v;
+        for (auto& b : Ly->rb) v.push_back(b.*m);
+        return v;
+    };
+    if (P > 1)
+        pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st,
+               [&] { cm->all_to_all("all_to_all_qkv", sends(&RankBufs::send_qkv), recvs(&RankBufs::qkv_head), qkv_peer, st); });
+    // ---- attention over the full sequence, local heads
+    const double attn_f = 4.0 * (double)N * N * hq * d / 2.0;  // causal half
+    for (int r = 0; r < L; ++r) {
+        auto& b = Ly->rb[r];
+        pf.run(P_ATTN_F, attn_f, 0, st, [&] { attn_fwd(b.qkv_head, N, hq, hkv, d, Ly->seg, scale, b.o_head, b.lse, st); });
+    }
+    if (P > 1) {
+        pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
+               [&] { cm->all_to_all("all_to_all_o", sends(&RankBufs::o_head), recvs(&RankBufs::recv_o), o_peer, st); });
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st, [&] {
+                reshard_unpack(b.recv_o, nl, hq, d, P, c.q_heads, Ly->gather_o, Ly->max_src_o, b.o, st);
+            });
+        }
+    }
+    // ---- forward phase B + loss + backward down to the attention output
+    for (int r = 0; r < L; ++r) {
+        auto& b = Ly->rb[r];
+        const bool acc = r > 0;  // loopback ranks share the grad buffer: rank-ascending accumulation
+        EpiParams e;
+        e.C = b.x1;
+        e.ldc = h;
+        e.R = b.x;
+        e.ldr = h;
+        pf.run(P_GEMM, gflop(nl, h, qd), 0, st, [&] { gemm({b.o, qd, false}, {Ly->wo, qd, false}, nl, h, qd, EPI_BF16, e, st); });
+        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x1, Ly->g2, b.xn2, b.rstd2, nl, h, Ly->eps, st); });
+        pf.run(P_GEMM, gflop(nl, 3 * I, h), 0, st,
+               [&] { mlp_fwd(b.xn2, Ly->wgu, Ly->wd, b.x1, b.x2, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st); });
+        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x2, Ly->g3, b.z, b.rstd3, nl, h, Ly->eps, st); });
+        pf.run(P_GEMM, gflop(nl, V, h) * 3, 0, st, [&] {
+            flce(b.z, Ly->wlm, b.labels, nl, h, V, Ly->loss_tile, &Ly->sc->scale, &Ly->sc->loss_sum, b.dz, Ly->dwlm,
+                 acc, &Ly->sc->err_label, Ly->ws_flce, st);
+        });
+        // backward
+        bf16* dx2 = b.dx;  // scratch until the final dx is produced
+        pf.run(P_NORM, 0, 3.0 * nl * h * 2, st,
+               [&] { rmsnorm_bwd(b.x2, Ly->g3, b.rstd3, b.dz, nullptr, dx2, Ly->dg3, Ly->ws_rms, nl, h, st); });
+        bf16* dxn2 = b.dz;
+        pf.run(P_GEMM, gflop(nl, I, h) * 8, 0, st, [&] {
+            mlp_bwd(b.xn2, Ly->wgu, Ly->wd, dx2, dxn2, Ly->dwgu, Ly->dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
+        });
+        pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
+               [&] { rmsnorm_bwd(b.x1, Ly->g2, b.rstd2, dxn2, dx2, b.dx1, Ly->dg2, Ly->ws_rms, nl, h, st); });
+        EpiParams e1;
+        e1.C = b.dO;
+        e1.ldc = qd;
+        pf.run(P_GEMM, gflop(nl, qd, h), 0, st, [&] { gemm({b.dx1, h, false}, {Ly->wo, qd, true}, nl, qd, h, EPI_BF16, e1, st); });
+        EpiParams e2;
+        e2.C = Ly->dwo;
+        e2.ldc = qd;
+        e2.accumulate = acc;
+        pf.run(P_GEMM, gflop(h, qd, nl), 0, st, [&] { gemm({b.dx1, h, true}, {b.o, qd, true}, h, qd, nl, EPI_F32, e2, st); });
+        if (P > 1)
+            pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st,
+                   [&] { reshard_pack(b.dO, nl, c.q_heads, d, P, hq, Ly->map_q, b.send_do, st); });
+    }
+    if (P > 1)
+        pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
+               [&] { cm->all_to_all("all_to_all_do", sends(&RankBufs::send_do), recvs(&RankBufs::do_head), o_peer, st); });
+    for (int r = 0; r < L; ++r) {
+        auto& b = Ly->rb[r];
+        pf.run(P_ATTN_B, attn_f * 2.5, 0, st, [&] {
+            attn_bwd(b.qkv_head, b.o_head, b.lse, b.do_head, N, hq, hkv, d, Ly->seg, scale, b.dqkv_head, Ly->ws_attn, st);
+        });
+    }
+    if (P > 1) {
+        pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st, [&] {
+            cm->all_to_all("all_to_all_dqkv", sends(&RankBufs::dqkv_head), recvs(&RankBufs::recv_dqkv), qkv_peer, st);
+        });
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            pf.run(P_RESHARD, 0, 2.0 * nl * qo * 2, st, [&] {
+                reshard_unpack(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, P, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
+                               Ly->max_src_qkv, b.dqkv, st);
+            });
+        }
+    }
+    for (int r = 0; r < L; ++r) {
+        auto& b = Ly->rb[r];
+        const bool acc = r > 0;
+        bf16* dxn1 = b.dz;
+        EpiParams e1;
+        e1.C = dxn1;
+        e1.ldc = h;
+        pf.run(P_GEMM, gflop(nl, h, qo), 0, st, [&] { gemm({b.dqkv, qo, false}, {Ly->wqkv, h, true}, nl, h, qo, EPI_BF16, e1, st); });
+        EpiParams e2;
+        e2.C = Ly->dwqkv;
+        e2.ldc = h;
+        e2.accumulate = acc;
+        pf.run(P_GEMM, gflop(qo, h, nl), 0, st, [&] { gemm({b.dqkv, qo, true}, {b.xn1, h, true}, qo, h, nl, EPI_F32, e2, st); });
+        pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
+               [&] { rmsnorm_bwd(b.x, Ly->g1, b.rstd1, dxn1, b.dx1, b.dx, Ly->dg1, Ly->ws_rms, nl, h, st); });
+    }
+    // ---- SP-group reductions
+    pf.run(P_COMM, 0, (double)Ly->gsize * 4, st, [&] {
+        cm->all_reduce("all_reduce_grads", Ly->gbuf, Ly->gsize, ncclFloat32, st);
+        cm->all_reduce("all_reduce_loss_sum", &Ly->sc->loss_sum, 1, ncclFloat64, st);
+    });
+    finalize_loss(&Ly->sc->loss_sum, &Ly->sc->count, &Ly->sc->loss, st);
+    if (c.lr > 0.f) {
+        pf.run(P_OTHER, 0, 0, st, [&] {
+            sgd_update(Ly->wqkv, Ly->dwqkv, qo * h, c.lr, st);
+            sgd_update(Ly->wo, Ly->dwo, h * qd, c.lr, st);
+            sgd_update(Ly->wgu, Ly->dwgu, 2 * I * h, c.lr, st);
+            sgd_update(Ly->wd, Ly->dwd, h * I, c.lr, st);
+            sgd_update(Ly->wlm, Ly->dwlm, V * h, c.lr, st);
+            sgd_update(Ly->g1, Ly->dg1, h, c.lr, st);
+            sgd_update(Ly->g2, Ly->dg2, h, c.lr, st);
+            sgd_update(Ly->g3, Ly->dg3, h, c.lr, st);
+        });
+    }
+    SPT_CUDA(cudaEventRecord(Ly->ev_step1, st));
+    cm->check_async();
+}
+
+static void read_scalars(spt_layer* Ly, cudaStream_t st, float* loss, int64_t* count) {
+    SPT_CUDA(cudaMemcpyAsync(Ly->sc_host, Ly->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+    SPT_CUDA(cudaStreamSynchronize(st));
+    Ly->comm->check_async();
+    SPT_CHECK(Ly->sc_host->err_label == 0, SPT_ERR_VALIDATION, "label out of range [0, vocab) and != -100");
+    SPT_CHECK(Ly->sc_host->err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
+    if (loss) *loss = Ly->sc_host->loss;
+    if (count) *count = Ly->sc_host->count;
+}
+
+static bf16* param_ptr(spt_layer* Ly, const std::string& n, int64_t* numel) {
+    const int64_t h = Ly->h, I = Ly->I;
+    if (n == "g1") return *numel = h, Ly->g1;
+    if (n == "g2") return *numel = h, Ly->g2;
+    if (n == "g3") return *numel = h, Ly->g3;
+    if (n == "wqkv") return *numel = Ly->qkv_out * h, Ly->wqkv;
+    if (n == "wo") return *numel = h * Ly->qd, Ly->wo;
+    if (n == "wd") return *numel = h * I, Ly->wd;
+    if (n == "wlm") return *numel = Ly->V * h, Ly->wlm;
+    if (n == "wg" || n == "wu") return *numel = I * h, nullptr;
+    SPT_THROW(SPT_ERR_VALIDATION, "unknown parameter name '" + n + "'");
+}
+
+static float* grad_ptr(spt_layer* Ly, const std::string& n) {
+    if (n == "g1") return Ly->dg1;
+    if (n == "g2") return Ly->dg2;
+    if (n == "g3") return Ly->dg3;
+    if (n == "wqkv") return Ly->dwqkv;
+    if (n == "wo") return Ly->dwo;
+    if (n == "wd") return Ly->dwd;
+    if (n == "wlm") return Ly->dwlm;
+    SPT_THROW(SPT_ERR_VALIDATION, "unknown parameter name '" + n + "'");
+}
+
+extern "C" {
+
+spt_status spt_layer_create(const spt_layer_config* cfg, spt_comm* comm, spt_layer** out) {
+    return capi_guard([&] {
+        SPT_CHECK(cfg && comm && out, SPT_ERR_CONFIG, "null argument");
+        SPT_CUDA(cudaSetDevice(comm->device));
+        (void)num_sms();  // validates sm_100
+        auto Ly = std::make_unique<spt_layer>();  // value-init: POD members zeroed
+        Ly->cfg = *cfg;
+        Ly->comm = comm;
+        try {
+            build_layer(Ly.get());
+        } catch (...) {
+            Ly->led.release_all();
+            throw;
+        }
+        *out = Ly.release();
+    });
+}
+
+spt_status spt_layer_destroy(spt_layer* Ly) {
+    return capi_guard([&] {
+        if (!Ly) return;
+        cudaDeviceSynchronize();
+        Ly->led.release_all();
+        if (Ly->sc_host) cudaFreeHost(Ly->sc_host);
+        for (auto e : Ly->prof.pool) cudaEventDestroy(e);
+        cudaEventDestroy(Ly->ev_step0);
+        cudaEventDestroy(Ly->ev_step1);
+        delete Ly;
+    });
+}
+
+spt_status spt_layer_set_param(spt_layer* Ly, const char* name, const void* data, int32_t data_on_host) {
+    return capi_guard([&] {
+        int64_t n = 0;
+        std::string nm(name);
+        bf16* p = param_ptr(Ly, nm, &n);
+        const cudaMemcpyKind k = data_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        if (p) {
+            SPT_CUDA(cudaMemcpy(p, data, n * 2, k));
+            return;
+        }
+        // gate / up rows go into the interleaved [2I, h] weight
+        void* tmp = nullptr;
+        SPT_CUDA(cudaMalloc(&tmp, n * 2));
+        SPT_CUDA(cudaMemcpy(tmp, data, n * 2, k));
+        interleave_gu(nm == "wg" ? tmp : nullptr, nm == "wu" ? tmp : nullptr, Ly->wgu, Ly->I, Ly->h, 0);
+        SPT_CUDA(cudaDeviceSynchronize());
+        cudaFree(tmp);
+    });
+}
+
+spt_status spt_layer_step_async(spt_layer* Ly, const void* x, const int64_t* shift_labels, const int64_t* position_ids,
+                                int32_t inputs_on_host, void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
+        layer_step(Ly, x, shift_labels, position_ids, inputs_on_host != 0, (cudaStream_t)stream);
+    });
+}
+
+spt_status spt_layer_read_loss(spt_layer* Ly, float* loss_out, int64_t* count_out, void* stream) {
+    return capi_guard([&] { read_scalars(Ly, (cudaStream_t)stream, loss_out, count_out); });
+}
+
+spt_status spt_layer_step(spt_layer* Ly, const void* x, const int64_t* shift_labels, const int64_t* position_ids,
+                          int32_t inputs_on_host, float* loss_out, int64_t* count_out, void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
+        layer_step(Ly, x, shift_labels, position_ids, inputs_on_host != 0, (cudaStream_t)stream);
+        read_scalars(Ly, (cudaStream_t)stream, loss_out, count_out);
+    });
+}
+
+spt_status spt_layer_get_grad(spt_layer* Ly, const char* name, float* host_out) {
+    return capi_guard([&] {
+        std::string n(name);
+        SPT_CUDA(cudaDeviceSynchronize());
+        if (n == "wg" || n == "wu") {
+            const size_t cnt = (size_t)Ly->I * Ly->h;
+            float *g = nullptr, *u = nullptr;
+            SPT_CUDA(cudaMalloc(&g, cnt * 4));
+            SPT_CUDA(cudaMalloc(&u, cnt * 4));
+            deinterleave_gu_f32(Ly->dwgu, g, u, Ly->I, Ly->h, 0);
+            SPT_CUDA(cudaMemcpy(host_out, n == "wg" ? g : u, cnt * 4, cudaMemcpyDeviceToHost));
+            cudaFree(g);
+            cudaFree(u);
+            return;
+        }
+        int64_t numel = 0;
+        param_ptr(Ly, n, &numel);
+        SPT_CUDA(cudaMemcpy(host_out, grad_ptr(Ly, n), numel * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+spt_status spt_layer_get_dx(spt_layer* Ly, void* host_out) {
+    return capi_guard([&] {
+        SPT_CUDA(cudaDeviceSynchronize());
+        const size_t per = (size_t)Ly->n_loc * Ly->h * 2;
+        for (int r = 0; r < Ly->L; ++r)
+            SPT_CUDA(cudaMemcpy((char*)host_out + r * per, Ly->rb[r].dx, per, cudaMemcpyDeviceToHost));
+    });
+}
+
+spt_status spt_layer_memory_json(spt_layer* Ly, char* buf, size_t cap) {
+    return capi_guard([&] {
+        std::ostringstream os;
+        os << "{\"ledger\":" << Ly->led.summary_json() << ",\"tokens_per_rank\":" << Ly->n_loc
+           << ",\"local_ranks\":" << Ly->L << ",\"mlp_tile\":" << Ly->mlp_tile << ",\"loss_tile\":" << Ly->loss_tile
+           << ",\"comm\":" << Ly->comm->stats_json() << "}";
+        std::string s = os.str();
+        SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+spt_status spt_layer_set_profiling(spt_layer* Ly, int32_t on) {
+    return capi_guard([&] { Ly->prof.on = on != 0; });
+}
+
+spt_status spt_layer_timing_json(spt_layer* Ly, char* buf, size_t cap) {
+    return capi_guard([&] {
+        SPT_CUDA(cudaEventSynchronize(Ly->ev_step1));
+        float ms = 0;
+        SPT_CUDA(cudaEventElapsedTime(&ms, Ly->ev_step0, Ly->ev_step1));
+        std::ostringstream os;
+        os << "{\"step_ms\":" << ms << ",\"classes\":" << Ly->prof.json() << "}";
+        std::string s = os.str();
+        SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Host side of the tcgen05 GEMM: TMA descriptor encoding, instantiation dispatch, C-ABI entry.
+#include <mutex>
+
+#include "common.h"
+#include "gemm.cuh"
+#include "launch.h"
+
+namespace spt {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    });
+    SPT_CHECK(fn != nullptr, SPT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+    return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [outer, inner] view with row pitch ld (elements), SW128.
+CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                              uint32_t box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    SPT_CHECK((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, SPT_ERR_SHAPE, "TMA base must be 16-byte aligned");
+    SPT_CHECK((ld * 2) % 16 == 0, SPT_ERR_SHAPE, "row pitch must be a multiple of 16 bytes");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SPT_CHECK(r == CUDA_SUCCESS, SPT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+template <int BN, bool A_MN, bool B_MN, int KIND>
+static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep,
+                        cudaStream_t st) {
+    auto kern = gemm_tc_kernel<BN, A_MN, B_MN, KIND>;
+    constexpr int smem = GemmCfg<BN>::SMEM_BYTES;
+    static bool attr_done = false;
+    if (!attr_done) {
+        SPT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_done = true;
+    }
+    const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
+    const int grid = std::min(ntiles, num_sms());
+    kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep,
+          cudaStream_t st) {
+    SPT_CHECK(M > 0 && N > 0 && K > 0, SPT_ERR_SHAPE, "gemm: empty problem");
+    SPT_CHECK(N % 64 == 0, SPT_ERR_SHAPE, "gemm: N must be a multiple of 64, got " + std::to_string(N));
+    SPT_CHECK(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), SPT_ERR_SHAPE, "gemm: dims exceed int32");
+    constexpr int BN = 256;
+    CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
+                                : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
+    CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)
+                                : make_tmap_bf16_2d(B.ptr, K, N, B.ld, GEMM_BK, BN);
+    const int m = (int)M, n = (int)N, k = (int)K;
+    const int sel = (A.mn_major ? 2 : 0) + (B.mn_major ? 1 : 0);
+    switch (sel * 8 + kind) {
+        case 0 * 8 + EPI_BF16: launch_gemm<BN, false, false, EPI_BF16>(ta, tb, m, n, k, ep, st); break;
+        case 0 * 8 + EPI_F32: launch_gemm<BN, false, false, EPI_F32>(ta, tb, m, n, k, ep, st); break;
+        case 0 * 8 + EPI_SWIGLU: launch_gemm<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); break;
+        case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); break;
+        case 1 * 8 + EPI_BF16: launch_gemm<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); break;
+        case 1 * 8 + EPI_F32: launch_gemm<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); break;
+        case 3 * 8 + EPI_BF16: launch_gemm<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); break;
+        case 3 * 8 + EPI_F32: launch_gemm<BN, true, true, EPI_F32>(ta, tb, m, n, k, ep, st); break;
+        default: SPT_THROW(SPT_ERR_INTERNAL, "gemm: unsupported major/epilogue combination");
+    }
+}
+
+}  // namespace spt
+
+extern "C" spt_status spt_gemm_bf16(const void* A, int64_t lda, int32_t a_mn_major, const void* B, int64_t ldb,
+                                    int32_t b_mn_major, void* C, int64_t ldc, int32_t c_f32, int32_t accumulate,
+                                    const void* residual, int64_t ldr, int64_t M, int64_t N, int64_t K, float alpha,
+                                    void* stream) {
+    return spt::capi_guard([&] {
+        spt::EpiParams ep;
+        ep.C = C;
+        ep.ldc = ldc;
+        ep.R = reinterpret_cast<const spt::bf16*>(residual);
+        ep.ldr = ldr;
+        ep.accumulate = accumulate;
+        ep.alpha = alpha;
+        spt::gemm({A, lda, a_mn_major != 0}, {B, ldb, b_mn_major != 0}, M, N, K, c_f32 ? spt::EPI_F32 : spt::EPI_BF16,
+                  ep, reinterpret_cast<cudaStream_t>(stream));
+    });
+}

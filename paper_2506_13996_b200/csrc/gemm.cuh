@@ -1,0 +1,304 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[m, n] = sum_k A(m, k) * B(n, k)          bf16 x bf16 -> fp32 in TMEM -> fused epilogue
+//
+// A(m,k) is read from A[m*lda + k] (K-major) or A[k*lda + m] (MN-major); likewise B.  That covers
+// the three shapes of a Linear layer: forward (X W^T: K,K), dgrad (dY W: K,MN) and wgrad
+// (dY^T X: MN,MN), so every projection of the layer step, TiledMLP and the fused logits+loss run
+// on this one kernel family.
+//
+// Roles (256 threads, 1 CTA/SM, grid = #SMs, static round-robin tile schedule):
+//   warp 0      TMA producer (one elected lane), STAGES-deep smem ring, 128B swizzle
+//   warp 1      MMA issuer (one lane): tcgen05.mma M=128, N=BN, K=16, accumulators in TMEM
+//   warp 2      TMEM allocator (2*BN columns: double-buffered accumulator)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
+// The epilogue of tile i overlaps the MMA main loop of tile i+1 (TMEM double buffer).
+#pragma once
+
+#include "sm100.cuh"
+
+namespace spt {
+
+enum EpiKind : int {
+    EPI_BF16 = 0,        // C(bf16) = acc * alpha (+ R)
+    EPI_F32 = 1,         // C(f32) = acc * alpha (+ C if accumulate)
+    EPI_SWIGLU = 2,      // columns interleaved [g32|u32]...: C(bf16)[m, n/2] = silu(g) * u
+    EPI_SWIGLU_BWD = 3,  // same interleave; aux = dA[m, n/2]; C = dGU (interleaved), C2 = A = silu(g)u
+};
+
+struct EpiParams {
+    void* C = nullptr;
+    int64_t ldc = 0;
+    const bf16* R = nullptr;  // residual (EPI_BF16), optional
+    int64_t ldr = 0;
+    const bf16* aux = nullptr;  // dA for EPI_SWIGLU_BWD
+    int64_t ldaux = 0;
+    bf16* C2 = nullptr;  // activation output for EPI_SWIGLU_BWD
+    int64_t ldc2 = 0;
+    int accumulate = 0;  // EPI_F32: C += acc
+    float alpha = 1.f;
+};
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 256;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;  // 16 KiB
+    static constexpr int B_BYTES = BN * GEMM_BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+
+__device__ __forceinline__ void store_bf16x32(bf16* dst, const float* v) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+        w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+        w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+        w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+        d[q] = w;
+    }
+}
+__device__ __forceinline__ void load_bf16x32(const bf16* src, float* v) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint4 w = s[q];
+        float2 a = unpack_bf16x2(w.x), b = unpack_bf16x2(w.y), c = unpack_bf16x2(w.z), d = unpack_bf16x2(w.w);
+        v[8 * q + 0] = a.x; v[8 * q + 1] = a.y; v[8 * q + 2] = b.x; v[8 * q + 3] = b.y;
+        v[8 * q + 4] = c.x; v[8 * q + 5] = c.y; v[8 * q + 6] = d.x; v[8 * q + 7] = d.y;
+    }
+}
+
+// One 32-column chunk (or a g/u pair of chunks for the SwiGLU kinds) of one row.
+template <int KIND>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row, int64_t col, const uint32_t (&r0)[32],
+                                               const uint32_t (&r1)[32]) {
+    float v[32];
+    if constexpr (KIND == EPI_BF16) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t* r = h ? r1 : r0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * ep.alpha;
+            if (ep.R != nullptr) {
+                float rr[32];
+                load_bf16x32(ep.R + row * ep.ldr + col + 32 * h, rr);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] += rr[i];
+            }
+            store_bf16x32(reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col + 32 * h, v);
+        }
+    } else if constexpr (KIND == EPI_F32) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t* r = h ? r1 : r0;
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + row * ep.ldc + col + 32 * h);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float4 o = make_float4(__uint_as_float(r[4 * q]) * ep.alpha, __uint_as_float(r[4 * q + 1]) * ep.alpha,
+                                       __uint_as_float(r[4 * q + 2]) * ep.alpha, __uint_as_float(r[4 * q + 3]) * ep.alpha);
+                if (ep.accumulate) {
+                    float4 c = dst[q];
+                    o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+                }
+                dst[q] = o;
+            }
+        }
+    } else if constexpr (KIND == EPI_SWIGLU) {
+        // r0 = g[j..j+32), r1 = u[j..j+32) with j = col/2
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float g = __uint_as_float(r0[i]), u = __uint_as_float(r1[i]);
+            v[i] = silu_f(g) * u;
+        }
+        store_bf16x32(reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col / 2, v);
+    } else {  // EPI_SWIGLU_BWD
+        float da[32], dg[32], du[32];
+        load_bf16x32(ep.aux + row * ep.ldaux + col / 2, da);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float g = __uint_as_float(r0[i]), u = __uint_as_float(r1[i]);
+            const float sg = 1.f / (1.f + __expf(-g));
+            const float si = g * sg;
+            v[i] = si * u;
+            du[i] = da[i] * si;
+            dg[i] = da[i] * u * sg * (1.f + g * (1.f - sg));
+        }
+        store_bf16x32(ep.C2 + row * ep.ldc2 + col / 2, v);
+        bf16* dgu = reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col;
+        store_bf16x32(dgu, dg);
+        store_bf16x32(dgu + 32, du);
+    }
+}
+
+template <int BN, bool A_MN, bool B_MN, int KIND>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, EpiParams ep) {
+    using Cfg = GemmCfg<BN>;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = warp_id(), lane = lane_id();
+    const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
+    const int num_n = (N + BN - 1) / BN;
+    const int ntiles = num_m * num_n;
+    const int nk = (K + GEMM_BK - 1) / GEMM_BK;
+    constexpr int GROUP_M = 16;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 2) {
+        tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto tile_coords = [&](int t, int& mb, int& nb) {
+        const int per_group = GROUP_M * num_n;
+        const int gid = t / per_group;
+        const int first_m = gid * GROUP_M;
+        const int gsz = min(num_m - first_m, GROUP_M);
+        const int in = t % per_group;
+        mb = first_m + in % gsz;
+        nb = in / gsz;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mb, nb;
+                tile_coords(t, mb, nb);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+                    uint8_t* sB = sA + Cfg::A_BYTES;
+                    mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+                    if constexpr (!A_MN) {
+                        tma_load_2d(&tmA, &full[stage], sA, kb * GEMM_BK, mb * GEMM_BM);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < GEMM_BM / 64; ++i)
+                            tma_load_2d(&tmA, &full[stage], sA + i * 8192, mb * GEMM_BM + i * 64, kb * GEMM_BK);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d(&tmB, &full[stage], sB, kb * GEMM_BK, nb * BN);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i)
+                            tma_load_2d(&tmB, &full[stage], sB + i * 8192, nb * BN + i * 64, kb * GEMM_BK);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < GEMM_BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? make_sdesc_sw128(a0 + k * 2048, 8192, 1024)
+                                                 : make_sdesc_sw128(a0 + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? make_sdesc_sw128(b0 + k * 2048, 8192, 1024)
+                                                 : make_sdesc_sw128(b0 + k * 32, 16, 1024);
+                        mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int sub = warp & 3;  // TMEM lane quarter this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int mb, nb;
+            tile_coords(t, mb, nb);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row = (int64_t)mb * GEMM_BM + sub * 32 + lane;
+            const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 64) {
+                const int64_t col = (int64_t)nb * BN + c;
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tbase + c, r0);
+                tmem_ld32(tbase + c + 32, r1);
+                tmem_ld_wait();
+                if (row < M && col < N) epilogue_chunk<KIND>(ep, row, col, r0, r1);
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+}  // namespace spt

@@ -1,0 +1,460 @@
+// HBM-bound kernels of the layer step: RMSNorm fwd/bwd, Ulysses pack/unpack (K1/K2), label /
+// position-id pre-passes (K10), row-wise cross-entropy, deterministic reductions, SGD update.
+// All use 128-bit vectorised, coalesced accesses and 64-bit indexing (N*h reaches 2^32 at 1M tokens).
+#include <algorithm>
+
+#include "common.h"
+#include "launch.h"
+#include "sm100.cuh"
+
+namespace spt {
+
+static inline int grid_for(int64_t work, int threads, int per_sm = 8) {
+    int64_t g = (work + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * per_sm));
+}
+
+// ------------------------------------------------------------------ block reduce helpers
+template <int MAXW>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float t = 0.f;
+    for (int i = 0; i < nw; ++i) t += red[i];  // fixed order -> deterministic
+    return t;
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// One thread owns 8 consecutive columns (one uint4); blockDim = max(32, h/8).
+__global__ void rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, bf16* __restrict__ y,
+                                   float* __restrict__ rstd, int64_t n, int h, float eps) {
+    __shared__ float red[32];
+    const int c = threadIdx.x * 8;
+    const bool act = c < h;
+    float gv[8];
+    if (act) load8(g + c, gv);
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        float xv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (act) load8(x + r * h + c, xv);
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss += xv[i] * xv[i];
+        const float tot = block_sum<32>(ss, red);
+        const float rs = rsqrtf(tot / (float)h + eps);
+        if (act) {
+            float o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = xv[i] * rs * gv[i];
+            store8(y + r * h + c, o);
+        }
+        if (threadIdx.x == 0) rstd[r] = rs;
+    }
+}
+
+__global__ void rmsnorm_bwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                   const float* __restrict__ rstd, const bf16* __restrict__ dy,
+                                   const bf16* __restrict__ dres, bf16* __restrict__ dx, float* __restrict__ part,
+                                   int64_t n, int h, int64_t rows_per_cta) {
+    __shared__ float red[32];
+    const int c = threadIdx.x * 8;
+    const bool act = c < h;
+    float gv[8], dga[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (act) load8(g + c, gv);
+    const int64_t r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+    for (int64_t r = r0; r < r1; ++r) {
+        float xv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (act) {
+            load8(x + r * h + c, xv);
+            load8(dy + r * h + c, dv);
+        }
+        const float rs = rstd[r];
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot += dv[i] * gv[i] * xv[i] * rs;
+        const float tot = block_sum<32>(dot, red) / (float)h;
+        if (act) {
+            float o[8], rr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (dres) load8(dres + r * h + c, rr);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float xh = xv[i] * rs;
+                o[i] = rs * (dv[i] * gv[i] - xh * tot) + rr[i];
+                dga[i] += dv[i] * xh;
+            }
+            store8(dx + r * h + c, o);
+        }
+    }
+    if (act) {
+        float4* p = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * h + c);
+        p[0] = make_float4(dga[0], dga[1], dga[2], dga[3]);
+        p[1] = make_float4(dga[4], dga[5], dga[6], dga[7]);
+    }
+}
+
+__global__ void colsum_accum_kernel(const float* __restrict__ part, int nparts, int h, float* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= h) return;
+    float s = 0.f;
+    for (int i = 0; i < nparts; ++i) s += part[(int64_t)i * h + c];
+    out[c] += s;
+}
+
+static int rms_threads(int64_t h) {
+    SPT_CHECK(h % 8 == 0 && h / 8 <= 1024, SPT_ERR_SHAPE, "rmsnorm: hidden must be a multiple of 8 and <= 8192");
+    return std::max<int>(32, (int)((h / 8 + 31) / 32 * 32));
+}
+
+void rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int64_t n, int64_t h, float eps,
+                 cudaStream_t st) {
+    if (n == 0) return;
+    const int th = rms_threads(h);
+    rmsnorm_fwd_kernel<<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd, n,
+                                                         (int)h, eps);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+static int rms_bwd_ctas(int64_t n) { return (int)std::min<int64_t>(n, (int64_t)num_sms() * 4); }
+
+size_t rmsnorm_bwd_workspace(int64_t n, int64_t h) { return (size_t)std::max(1, rms_bwd_ctas(n)) * h * 4; }
+
+void rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy, const void* dres, void* dx,
+                 float* dgamma_accum, void* ws, int64_t n, int64_t h, cudaStream_t st) {
+    if (n == 0) return;
+    const int th = rms_threads(h);
+    const int ctas = rms_bwd_ctas(n);
+    const int64_t per = (n + ctas - 1) / ctas;
+    const int used = (int)((n + per - 1) / per);
+    rmsnorm_bwd_kernel<<<used, th, 0, st>>>((const bf16*)x, (const bf16*)gamma, rstd, (const bf16*)dy,
+                                            (const bf16*)dres, (bf16*)dx, (float*)ws, n, (int)h, per);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+    colsum_accum_kernel<<<(int)((h + 255) / 256), 256, 0, st>>>((const float*)ws, used, (int)h, dgamma_accum);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ Ulysses reshard K1 / K2
+// K1: send[j][t][a][:] = src[t][head_map[j*heads_out + a]][:]   (payload layout :351)
+__global__ void reshard_pack_kernel(const uint4* __restrict__ src, int64_t s_loc, int heads_in, int vpd, int P,
+                                    int heads_out, const int32_t* __restrict__ head_map, uint4* __restrict__ dst) {
+    const int64_t total = (int64_t)P * s_loc * heads_out * vpd;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = (int)(i % vpd);
+        int64_t q = i / vpd;
+        const int a = (int)(q % heads_out);
+        q /= heads_out;
+        const int64_t t = q % s_loc;
+        const int j = (int)(q / s_loc);
+        const int hsrc = __ldg(head_map + j * heads_out + a);
+        dst[i] = __ldg(src + (t * heads_in + hsrc) * vpd + v);
+    }
+}
+
+// K2: dst[t][h][:] = sum_e recv[i_e][t][a_e][:] over the listed sources, rank order
+__global__ void reshard_unpack_kernel(const uint4* __restrict__ recv, int64_t s_loc, int heads_in, int vpd,
+                                      int heads_out, const int32_t* __restrict__ gather, int max_src,
+                                      uint4* __restrict__ dst) {
+    const int64_t total = s_loc * heads_out * vpd;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = (int)(i % vpd);
+        int64_t q = i / vpd;
+        const int h = (int)(q % heads_out);
+        const int64_t t = q / heads_out;
+        const int32_t* gl = gather + h * max_src;
+        const int g0 = __ldg(gl);
+        auto src_of = [&](int gidx) {
+            const int rank = gidx / heads_in, slot = gidx % heads_in;
+            return recv + (((int64_t)rank * s_loc + t) * heads_in + slot) * vpd + v;
+        };
+        int nsrc = 1;
+        while (nsrc < max_src && __ldg(gl + nsrc) >= 0) ++nsrc;
+        if (nsrc == 1) {
+            dst[i] = __ldg(src_of(g0));  // plain permutation: bit-exact
+        } else {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int e = 0; e < nsrc; ++e) {
+                uint4 w = __ldg(src_of(__ldg(gl + e)));
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float2 f = unpack_bf16x2(ws[k]);
+                    acc[2 * k] += f.x;
+                    acc[2 * k + 1] += f.y;
+                }
+            }
+            uint4 o;
+            o.x = pack_bf16x2(acc[0], acc[1]);
+            o.y = pack_bf16x2(acc[2], acc[3]);
+            o.z = pack_bf16x2(acc[4], acc[5]);
+            o.w = pack_bf16x2(acc[6], acc[7]);
+            dst[i] = o;
+        }
+    }
+}
+
+void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                  const int32_t* head_map, void* dst, cudaStream_t st) {
+    SPT_CHECK(head_dim % 8 == 0, SPT_ERR_SHAPE, "head_dim must be a multiple of 8");
+    const int vpd = head_dim / 8;
+    const int64_t total = (int64_t)P * s_loc * heads_out * vpd;
+    if (total == 0) return;
+    reshard_pack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)src, s_loc, heads_in, vpd, P, heads_out,
+                                                               head_map, (uint4*)dst);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                    const int32_t* gather, int max_src, void* dst, cudaStream_t st) {
+    SPT_CHECK(head_dim % 8 == 0, SPT_ERR_SHAPE, "head_dim must be a multiple of 8");
+    (void)P;
+    const int vpd = head_dim / 8;
+    const int64_t total = s_loc * heads_out * vpd;
+    if (total == 0) return;
+    reshard_unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)recv, s_loc, heads_in, vpd, heads_out,
+                                                                 gather, max_src, (uint4*)dst);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ K10 label / position pre-passes
+__global__ void label_stats_kernel(const int64_t* __restrict__ labels, int64_t n, int64_t V, int64_t* count,
+                                   int32_t* err) {
+    __shared__ long long red[32];
+    long long c = 0;
+    int bad = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t l = labels[i];
+        if (l == -100) continue;
+        if (l < 0 || l >= V) bad = 1;
+        else ++c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    bad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    if (bad && (threadIdx.x & 31) == 0) *err = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        *count += t;
+    }
+}
+
+void label_stats(const int64_t* labels, int64_t n, int64_t vocab, int64_t* count_accum, int32_t* err,
+                 cudaStream_t st) {
+    if (n == 0) return;
+    label_stats_kernel<<<1, 1024, 0, st>>>(labels, n, vocab, count_accum, err);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+__global__ void segment_starts_kernel(const int64_t* __restrict__ pos, int64_t n, int32_t* __restrict__ starts,
+                                      int32_t* err) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = pos[t];
+        const bool ok = (t == 0) ? (p == 0) : (p == 0 || p == pos[t - 1] + 1);
+        if (!ok) *err = 2;
+        starts[t] = (int32_t)(t - p);
+    }
+}
+
+void segment_starts(const int64_t* pos, int64_t n, int32_t* starts, int32_t* err, cudaStream_t st) {
+    if (n == 0) return;
+    segment_starts_kernel<<<grid_for(n, 256), 256, 0, st>>>(pos, n, starts, err);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ cross-entropy rows
+// One CTA per row: one pass online (max, sumexp), block combine, then dlogits = (p - onehot) * scale.
+__global__ void __launch_bounds__(512) ce_rows_kernel(const float* __restrict__ logits, const int64_t* __restrict__ labels,
+                                                      int64_t V, const float* __restrict__ scale_dev,
+                                                      float* __restrict__ loss_rows, bf16* __restrict__ dlogits,
+                                                      int32_t* err) {
+    __shared__ float sm_m[32], sm_s[32];
+    __shared__ float sh_lse;
+    const int64_t r = blockIdx.x;
+    const float* row = logits + r * V;
+    const int64_t label = labels[r];
+    const bool valid = label != -100 && label >= 0 && label < V;
+    if (label != -100 && !valid && threadIdx.x == 0) *err = 1;
+    bf16* drow = dlogits + r * V;
+    const int64_t nv = V / 8;  // V % 8 == 0 enforced by host
+    if (!valid) {
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) reinterpret_cast<uint4*>(drow)[i] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x == 0) loss_rows[r] = 0.f;
+        return;
+    }
+    float m = -INFINITY, s = 0.f;
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        const float4 a = reinterpret_cast<const float4*>(row)[2 * i];
+        const float4 b = reinterpret_cast<const float4*>(row)[2 * i + 1];
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        float mx = v[0];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) mx = fmaxf(mx, v[k]);
+        const float nm = fmaxf(m, mx);
+        float acc = s * __expf(m - nm);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += __expf(v[k] - nm);
+        s = acc;
+        m = nm;
+    }
+    // warp combine
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+        const float nm = fmaxf(m, om);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sm_m[w] = m;
+        sm_s[w] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY, S = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            const float nm = fmaxf(M, sm_m[i]);
+            S = (M == -INFINITY ? 0.f : S * __expf(M - nm)) + (sm_m[i] == -INFINITY ? 0.f : sm_s[i] * __expf(sm_m[i] - nm));
+            M = nm;
+        }
+        const float lse = M + __logf(S);
+        sh_lse = lse;
+        loss_rows[r] = lse - row[label];
+    }
+    __syncthreads();
+    const float lse = sh_lse;
+    const float scale = *scale_dev;
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        const float4 a = reinterpret_cast<const float4*>(row)[2 * i];
+        const float4 b = reinterpret_cast<const float4*>(row)[2 * i + 1];
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = __expf(v[k] - lse);
+            if (8 * i + k == label) v[k] -= 1.f;
+            v[k] *= scale;
+        }
+        store8(drow + 8 * i, v);
+    }
+}
+
+void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V, const float* scale_dev,
+             float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st) {
+    SPT_CHECK(V % 8 == 0, SPT_ERR_SHAPE, "vocab must be a multiple of 8");
+    if (rows == 0) return;
+    ce_rows_kernel<<<(unsigned)rows, 512, 0, st>>>(logits, labels, V, scale_dev, loss_rows, (bf16*)dlogits, err);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+__global__ void sum_rows_kernel(const float* __restrict__ v, int64_t n, double* accum) {
+    __shared__ double red[32];
+    double s = 0.0;
+    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t a = threadIdx.x * per, b = min(n, a + per);
+    for (int64_t i = a; i < b; ++i) s += (double)v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        *accum += t;
+    }
+}
+
+void sum_rows(const float* v, int64_t n, double* accum, cudaStream_t st) {
+    if (n == 0) return;
+    sum_rows_kernel<<<1, 1024, 0, st>>>(v, n, accum);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+__global__ void finalize_scale_kernel(const int64_t* count, float* scale) {
+    const int64_t c = *count;
+    *scale = c > 0 ? (float)(1.0 / (double)c) : 0.f;
+}
+__global__ void finalize_loss_kernel(const double* sum, const int64_t* count, float* loss) {
+    const int64_t c = *count;
+    *loss = c > 0 ? (float)(*sum / (double)c) : 0.f;
+}
+void finalize_scale(const int64_t* count, float* scale, cudaStream_t st) {
+    finalize_scale_kernel<<<1, 1, 0, st>>>(count, scale);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st) {
+    finalize_loss_kernel<<<1, 1, 0, st>>>(loss_sum, count, loss_out);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ SGD + weight layout helpers
+__global__ void sgd_kernel(bf16* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8; i < n; i += (int64_t)gridDim.x * blockDim.x * 8) {
+        float wv[8];
+        load8(w + i, wv);
+        const float4 a = *reinterpret_cast<const float4*>(g + i), b = *reinterpret_cast<const float4*>(g + i + 4);
+        const float gv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wv[k] -= lr * gv[k];
+        store8(w + i, wv);
+    }
+}
+void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st) {
+    SPT_CHECK(n % 8 == 0, SPT_ERR_SHAPE, "sgd: size must be a multiple of 8");
+    if (n == 0) return;
+    sgd_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>((bf16*)w, g, n, lr);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+__global__ void interleave_gu_kernel(const uint4* __restrict__ wg, const uint4* __restrict__ wu, uint4* __restrict__ out,
+                                     int64_t inter, int64_t vrow) {
+    const int64_t total = 2 * inter * vrow;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / vrow, v = i % vrow;
+        const int64_t blk = r / 64, w = r % 64;
+        if (w < 32) {
+            if (wg) out[i] = wg[(blk * 32 + w) * vrow + v];
+        } else if (wu) {
+            out[i] = wu[(blk * 32 + w - 32) * vrow + v];
+        }
+    }
+}
+void interleave_gu(const void* wg, const void* wu, void* wgu, int64_t inter, int64_t h, cudaStream_t st) {
+    SPT_CHECK(inter % 32 == 0 && h % 8 == 0, SPT_ERR_SHAPE, "intermediate must be a multiple of 32");
+    interleave_gu_kernel<<<grid_for(2 * inter * h / 8, 256), 256, 0, st>>>((const uint4*)wg, (const uint4*)wu,
+                                                                           (uint4*)wgu, inter, h / 8);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+__global__ void deinterleave_gu_kernel(const float4* __restrict__ gu, float4* __restrict__ g, float4* __restrict__ u,
+                                       int64_t inter, int64_t vrow) {
+    const int64_t total = 2 * inter * vrow;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / vrow, v = i % vrow;
+        const int64_t blk = r / 64, w = r % 64;
+        if (w < 32) g[(blk * 32 + w) * vrow + v] = gu[i];
+        else u[(blk * 32 + w - 32) * vrow + v] = gu[i];
+    }
+}
+void deinterleave_gu_f32(const float* gu, float* g, float* u, int64_t inter, int64_t h, cudaStream_t st) {
+    deinterleave_gu_kernel<<<grid_for(2 * inter * h / 4, 256), 256, 0, st>>>((const float4*)gu, (float4*)g, (float4*)u,
+                                                                             inter, h / 4);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+}  // namespace spt

@@ -1,0 +1,62 @@
+// Internal launch API shared by the kernel translation units and the C++ host engine.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace spt {
+
+struct EpiParams;
+
+struct GemmOperand {
+    const void* ptr;
+    int64_t ld;     // row pitch in elements of the stored matrix
+    bool mn_major;  // false: element (row, k) at ptr[row*ld + k]; true: at ptr[k*ld + row]
+};
+
+void count_launch();
+int64_t launch_count();
+
+CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                              uint32_t box_outer);
+
+// C[m,n] = sum_k A(m,k) B(n,k) with the fused epilogue `kind` (EpiKind in gemm.cuh).
+void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep,
+          cudaStream_t st);
+
+// kernels.cu
+void rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int64_t n, int64_t h, float eps,
+                 cudaStream_t st);
+size_t rmsnorm_bwd_workspace(int64_t n, int64_t h);
+void rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy, const void* dres, void* dx,
+                 float* dgamma_accum, void* ws, int64_t n, int64_t h, cudaStream_t st);
+void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                  const int32_t* head_map, void* dst, cudaStream_t st);
+void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                    const int32_t* gather, int max_src, void* dst, cudaStream_t st);
+void label_stats(const int64_t* labels, int64_t n, int64_t vocab, int64_t* count_accum, int32_t* err, cudaStream_t st);
+void segment_starts(const int64_t* pos, int64_t n, int32_t* starts, int32_t* err, cudaStream_t st);
+// Row-wise CE over fp32 logits [rows, V]: loss_rows[r] (0 if ignored), dlogits bf16 = (softmax-onehot)*scale.
+void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V, const float* scale_dev,
+             float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st);
+// Deterministic fixed-order sum of n fp32 values into an fp64 accumulator.
+void sum_rows(const float* v, int64_t n, double* accum, cudaStream_t st);
+// loss = loss_sum / count (device scalars) and scale = 1/count.
+void finalize_scale(const int64_t* count, float* scale, cudaStream_t st);
+void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st);
+// W(bf16) -= lr * G(fp32)
+void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st);
+// Interleave/deinterleave gate/up in blocks of 32 rows: dst [2I, h] from wg [I,h], wu [I,h].
+void interleave_gu(const void* wg, const void* wu, void* wgu, int64_t inter, int64_t h, cudaStream_t st);
+void deinterleave_gu_f32(const float* gu, float* g, float* u, int64_t inter, int64_t h, cudaStream_t st);
+
+// attention.cu
+void attn_fwd(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg_start, float scale, void* o,
+              float* lse, cudaStream_t st);
+size_t attn_bwd_workspace(int64_t s, int hq, int hkv, int d);
+void attn_bwd(const void* qkv, const void* o, const float* lse, const void* dout, int64_t s, int hq, int hkv, int d,
+              const int32_t* seg_start, float scale, void* dqkv, void* ws, cudaStream_t st);
+
+}  // namespace spt

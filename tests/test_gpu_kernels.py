@@ -1,0 +1,304 @@
+"""GPU parity of every kernel against the CPU oracle, through the C-ABI (pytest -m gpu)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import sptrain_oracle as O
+from tests.gpu_util import bf16_dev, rel_err, to_np, torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2506_13996_b200 as S  # noqa: E402
+
+
+def _lib():
+    return S.lib()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    T = torch()
+    assert T.cuda.is_available(), "GPU tests need a B200"
+    yield
+
+
+# ------------------------------------------------------------------ GEMM (tcgen05)
+@pytest.mark.parametrize("a_mn,b_mn,f32,acc", [(0, 0, 0, 0), (0, 1, 0, 0), (1, 1, 1, 0), (1, 1, 1, 1), (0, 0, 1, 0),
+                                                (0, 1, 1, 0), (1, 1, 0, 0)])
+@pytest.mark.parametrize("M,N,K", [(320, 384, 320), (128, 256, 64), (1000, 512, 4160)])
+def test_gemm_majors(a_mn, b_mn, f32, acc, M, N, K):
+    T = torch()
+    g = T.Generator(device="cuda").manual_seed(M + N + K)
+    A = T.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = T.randn(N, K, device="cuda", generator=g).bfloat16()
+    Ast = A.t().contiguous() if a_mn else A  # MN-major storage is [K, M]
+    Bst = B.t().contiguous() if b_mn else B
+    ref = A.float() @ B.float().t()
+    if f32:
+        C = T.randn(M, N, device="cuda", generator=g) if acc else T.empty(M, N, device="cuda")
+        base = C.clone()
+    else:
+        C = T.empty(M, N, device="cuda", dtype=T.bfloat16)
+    S.check(_lib().spt_gemm_bf16(Ast.data_ptr(), Ast.shape[1], a_mn, Bst.data_ptr(), Bst.shape[1], b_mn, C.data_ptr(),
+                                 N, f32, acc, None, 0, M, N, K, 1.0, None))
+    T.cuda.synchronize()
+    if f32 and acc:
+        ref = ref + base
+    err = rel_err(to_np(C), to_np(ref))
+    assert err < (1e-5 if f32 else 5e-3), err
+
+
+def test_gemm_residual_alpha():
+    T = torch()
+    M, N, K = 256, 320, 192
+    A = T.randn(M, K, device="cuda").bfloat16()
+    B = T.randn(N, K, device="cuda").bfloat16()
+    R = T.randn(M, N, device="cuda").bfloat16()
+    C = T.empty(M, N, device="cuda", dtype=T.bfloat16)
+    S.check(_lib().spt_gemm_bf16(A.data_ptr(), K, 0, B.data_ptr(), K, 0, C.data_ptr(), N, 0, 0, R.data_ptr(), N, M, N,
+                                 K, 0.5, None))
+    ref = 0.5 * (A.float() @ B.float().t()) + R.float()
+    assert rel_err(to_np(C), to_np(ref)) < 5e-3
+
+
+def test_gemm_rejects_bad_n():
+    T = torch()
+    A = T.zeros(128, 64, device="cuda").bfloat16()
+    C = T.zeros(128, 96, device="cuda").bfloat16()
+    with pytest.raises(S.ShapeError):
+        S.check(_lib().spt_gemm_bf16(A.data_ptr(), 64, 0, A.data_ptr(), 64, 0, C.data_ptr(), 96, 0, 0, None, 0, 128,
+                                     96, 64, 1.0, None))
+
+
+# ------------------------------------------------------------------ RMSNorm
+@pytest.mark.parametrize("n,h", [(300, 256), (64, 4096)])
+def test_rmsnorm_fwd_bwd(n, h):
+    T = torch()
+    rng = np.random.default_rng(n)
+    x = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    g = O.round_bf16(1 + 0.05 * rng.standard_normal(h, dtype=np.float32))
+    dy = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    dres = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    xd, gd, dyd, dresd = bf16_dev(x), bf16_dev(g), bf16_dev(dy), bf16_dev(dres)
+    y = T.empty_like(xd)
+    rstd = T.empty(n, device="cuda")
+    S.check(_lib().spt_rmsnorm_fwd(xd.data_ptr(), gd.data_ptr(), y.data_ptr(), rstd.data_ptr(), n, h, 1e-5, None))
+    yr, rr = O.rmsnorm_fwd(x.astype(np.float64), g.astype(np.float64))
+    assert rel_err(to_np(y), yr) < 4e-3
+    assert rel_err(to_np(rstd), rr[:, 0]) < 1e-5
+    dx = T.empty_like(xd)
+    dg = T.zeros(h, device="cuda")
+    ws = T.empty(_lib().spt_rmsnorm_bwd_workspace(n, h), dtype=T.uint8, device="cuda")
+    S.check(_lib().spt_rmsnorm_bwd(xd.data_ptr(), gd.data_ptr(), rstd.data_ptr(), dyd.data_ptr(), dresd.data_ptr(),
+                                   dx.data_ptr(), dg.data_ptr(), ws.data_ptr(), n, h, None))
+    dxr, dgr = O.rmsnorm_bwd(x.astype(np.float64), g.astype(np.float64), rr, dy.astype(np.float64))
+    assert rel_err(to_np(dx), dxr + dres) < 5e-3
+    assert rel_err(to_np(dg), dgr) < 1e-4
+    # determinism: bitwise identical rerun
+    dg2 = T.zeros(h, device="cuda")
+    S.check(_lib().spt_rmsnorm_bwd(xd.data_ptr(), gd.data_ptr(), rstd.data_ptr(), dyd.data_ptr(), dresd.data_ptr(),
+                                   dx.data_ptr(), dg2.data_ptr(), ws.data_ptr(), n, h, None))
+    assert T.equal(dg, dg2)
+
+
+# ------------------------------------------------------------------ Ulysses reshard (bit-exact)
+@pytest.mark.parametrize("Hq,Hkv,P", [(8, 2, 2), (8, 2, 4), (8, 2, 8), (32, 8, 8), (4, 4, 2)])
+def test_reshard_pack_unpack_bitexact(Hq, Hkv, P):
+    """K1 + loopback all_to_all + K2 == oracle seq_to_head / head_to_seq, bit for bit."""
+    T = torch()
+    d, s_loc = 32, 24
+    rng = np.random.default_rng(P * 100 + Hq)
+    plan = O.plan_head_shards(Hq, Hkv, P)
+    Hl = plan.q_heads_per_rank + 2 * plan.kv_heads_per_rank
+    xs = [O.round_bf16(rng.standard_normal((s_loc, Hq + 2 * Hkv, d), dtype=np.float32)) for _ in range(P)]
+    # oracle: fused-qkv seq_to_head (q heads, k heads, v heads of the local plan)
+    def heads(j):
+        return (plan.q_heads_of(j) + [Hq + h for h in plan.kv_heads_of(j)] +
+                [Hq + Hkv + h for h in plan.kv_heads_of(j)])
+    ys = O.seq_to_head(xs, heads)
+    cplan = S.plan_head_shards(Hq, Hkv, P)
+    hmap = []
+    for j in range(P):
+        hmap += heads(j)
+    hmap_d = T.tensor(hmap, dtype=T.int32, device="cuda")
+    sends = []
+    for r in range(P):
+        src = bf16_dev(xs[r])
+        dst = T.empty(P, s_loc, Hl, d, dtype=T.bfloat16, device="cuda")
+        S.check(_lib().spt_reshard_pack(src.data_ptr(), s_loc, Hq + 2 * Hkv, d, P, Hl, hmap_d.data_ptr(),
+                                        dst.data_ptr(), None))
+        sends.append(dst)
+    recv = [T.stack([sends[i][j] for i in range(P)]) for j in range(P)]  # all_to_all
+    for j in range(P):
+        got = recv[j].reshape(P * s_loc, Hl, d)
+        exp = O.f32_to_bf16_bits(ys[j]).view(np.int16)
+        assert np.array_equal(got.view(T.int16).cpu().numpy(), exp)
+    # backward direction: head_to_seq with replica sum; with r == 1 it is an exact permutation
+    gathers = {}
+    for j in range(P):
+        for a, hglob in enumerate(heads(j)):
+            gathers.setdefault(hglob, []).append(j * Hl + a)
+    ms = max(len(v) for v in gathers.values())
+    gt = np.full((Hq + 2 * Hkv, ms), -1, np.int32)
+    for hglob, lst in gathers.items():
+        gt[hglob, :len(lst)] = lst
+    gt_d = T.from_numpy(gt).cuda()
+    grads = [O.round_bf16(rng.standard_normal((P * s_loc, Hl, d), dtype=np.float32)) for _ in range(P)]
+    back_o = O.head_to_seq(grads, heads, Hq + 2 * Hkv, reduce_replicas=True)
+    gd = [bf16_dev(g_) for g_ in grads]
+    for i in range(P):
+        recv_i = T.stack([gd[j].reshape(P, s_loc, Hl, d)[i] for j in range(P)])
+        out = T.empty(s_loc, Hq + 2 * Hkv, d, dtype=T.bfloat16, device="cuda")
+        S.check(_lib().spt_reshard_unpack(recv_i.data_ptr(), s_loc, Hl, d, P, Hq + 2 * Hkv, gt_d.data_ptr(), ms,
+                                          out.data_ptr(), None))
+        if plan.kv_replication == 1:
+            assert np.array_equal(out.view(T.int16).cpu().numpy(), O.f32_to_bf16_bits(back_o[i]).view(np.int16))
+        else:
+            assert rel_err(to_np(out), back_o[i]) < 4e-3
+            q = plan.q_heads
+            assert np.array_equal(out[:, :q].view(T.int16).cpu().numpy(),
+                                  O.f32_to_bf16_bits(back_o[i][:, :q]).view(np.int16))
+
+
+# ------------------------------------------------------------------ label / position pre-passes
+def test_label_stats_and_segments():
+    T = torch()
+    lab = np.array([3, -100, 7, 0, -100, 31999], np.int64)
+    ld = T.from_numpy(lab).cuda()
+    cnt = T.zeros(1, dtype=T.int64, device="cuda")
+    err = T.zeros(1, dtype=T.int32, device="cuda")
+    S.check(_lib().spt_label_stats(ld.data_ptr(), lab.size, 32000, cnt.data_ptr(), err.data_ptr(), None))
+    assert int(cnt) == 4 and int(err) == 0
+    bad = T.tensor([1, 32000], dtype=T.int64, device="cuda")
+    S.check(_lib().spt_label_stats(bad.data_ptr(), 2, 32000, cnt.data_ptr(), err.data_ptr(), None))
+    assert int(err) == 1
+    pos = np.array([0, 1, 2, 0, 1, 0, 1, 2, 3], np.int64)
+    st = T.empty(pos.size, dtype=T.int32, device="cuda")
+    e2 = T.zeros(1, dtype=T.int32, device="cuda")
+    S.check(_lib().spt_segment_starts(T.from_numpy(pos).cuda().data_ptr(), pos.size, st.data_ptr(), e2.data_ptr(),
+                                      None))
+    assert st.cpu().numpy().tolist() == O.block_causal_starts(pos).tolist() and int(e2) == 0
+    bad_pos = T.tensor([0, 2], dtype=T.int64, device="cuda")
+    S.check(_lib().spt_segment_starts(bad_pos.data_ptr(), 2, st.data_ptr(), e2.data_ptr(), None))
+    assert int(e2) != 0
+
+
+# ------------------------------------------------------------------ attention
+def _attn_case(s, hq, hkv, d, packed, seed):
+    rng = np.random.default_rng(seed)
+    qkv = O.round_bf16(rng.standard_normal((s, hq + 2 * hkv, d), dtype=np.float32))
+    dout = O.round_bf16(rng.standard_normal((s, hq, d), dtype=np.float32))
+    if packed:
+        runs = []
+        while sum(runs) < s:
+            runs.append(int(rng.integers(1, s // 2)))
+        pos = np.concatenate([np.arange(r) for r in runs])[:s]
+        starts = O.block_causal_starts(pos)
+    else:
+        starts = None
+    return qkv, dout, starts
+
+
+@pytest.mark.parametrize("s,hq,hkv,d,packed", [(256, 4, 2, 32, False), (384, 4, 1, 128, False), (512, 2, 2, 64, True),
+                                               (256, 8, 2, 128, True)])
+def test_attention_fwd_bwd(s, hq, hkv, d, packed):
+    T = torch()
+    qkv, dout, starts = _attn_case(s, hq, hkv, d, packed, s + d)
+    q, k, v = qkv[:, :hq], qkv[:, hq:hq + hkv], qkv[:, hq + hkv:]
+    o_r, lse_r = O.attention_fwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), starts)
+    qkvd, doutd = bf16_dev(qkv), bf16_dev(dout)
+    o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+    lse = T.empty(hq, s, device="cuda")
+    seg = T.from_numpy(starts.astype(np.int32)).cuda() if starts is not None else None
+    scale = 1.0 / math.sqrt(d)
+    S.check(_lib().spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, S.ptr(seg), scale, o.data_ptr(), lse.data_ptr(), None))
+    T.cuda.synchronize()
+    assert rel_err(to_np(o), o_r) < 1e-2
+    assert np.max(np.abs(to_np(lse) - lse_r)) < 2e-3
+    # backward, oracle fed the GPU's (bf16) O for consistency of D = rowsum(dO*O)
+    o_bf = to_np(o).astype(np.float64)
+    dq_r, dk_r, dv_r = O.attention_bwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), o_bf, lse_r,
+                                       dout.astype(np.float64), starts)
+    dqkv = T.zeros(s, hq + 2 * hkv, d, dtype=T.bfloat16, device="cuda")
+    ws = T.empty(_lib().spt_attn_bwd_workspace(s, hq, hkv, d), dtype=T.uint8, device="cuda")
+    S.check(_lib().spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
+                                S.ptr(seg), scale, dqkv.data_ptr(), ws.data_ptr(), None))
+    T.cuda.synchronize()
+    g = to_np(dqkv)
+    assert rel_err(g[:, :hq], dq_r) < 2e-2
+    assert rel_err(g[:, hq:hq + hkv], dk_r) < 2e-2
+    assert rel_err(g[:, hq + hkv:], dv_r) < 2e-2
+    # bitwise deterministic backward
+    dqkv2 = T.zeros_like(dqkv)
+    S.check(_lib().spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
+                                S.ptr(seg), scale, dqkv2.data_ptr(), ws.data_ptr(), None))
+    assert T.equal(dqkv.view(T.int16), dqkv2.view(T.int16))
+
+
+# ------------------------------------------------------------------ fused logits + CE (tiled)
+@pytest.mark.parametrize("n,h,V,tile", [(384, 256, 32000, 128), (200, 128, 1024, 64), (256, 256, 512, 256)])
+def test_flce(n, h, V, tile):
+    T = torch()
+    rng = np.random.default_rng(n + V)
+    x = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    w = O.round_bf16(0.05 * rng.standard_normal((V, h), dtype=np.float32))
+    lab = rng.integers(0, V, n).astype(np.int64)
+    lab[rng.random(n) < 0.1] = -100
+    cnt = int((lab != -100).sum())
+    ls, c, dh, dw = O.tiled_logits_loss(x.astype(np.float64), w.astype(np.float64), lab, tile, grad_scale=1.0 / cnt)
+    xd, wd = bf16_dev(x), bf16_dev(w)
+    ld = T.from_numpy(lab).cuda()
+    scale = T.tensor([1.0 / cnt], device="cuda")
+    loss = T.zeros(1, dtype=T.float64, device="cuda")
+    dx = T.empty(n, h, dtype=T.bfloat16, device="cuda")
+    dW = T.empty(V, h, device="cuda")
+    err = T.zeros(1, dtype=T.int32, device="cuda")
+    ws = T.empty(_lib().spt_flce_workspace(tile, V), dtype=T.uint8, device="cuda")
+    S.check(_lib().spt_flce(xd.data_ptr(), wd.data_ptr(), ld.data_ptr(), n, h, V, tile, scale.data_ptr(),
+                            loss.data_ptr(), dx.data_ptr(), dW.data_ptr(), 0, err.data_ptr(), ws.data_ptr(), None))
+    T.cuda.synchronize()
+    assert int(err) == 0
+    assert abs(float(loss) - ls) / abs(ls) < 1e-4
+    assert rel_err(to_np(dx), dh) < 2e-2
+    assert rel_err(to_np(dW), dw) < 2e-2
+
+
+# ------------------------------------------------------------------ TiledMLP
+@pytest.mark.parametrize("n,h,I,tile", [(256, 256, 1024, 128), (300, 128, 512, 100)])
+def test_tiled_mlp(n, h, I, tile):
+    T = torch()
+    rng = np.random.default_rng(n + I)
+    x = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    wg = O.round_bf16(0.05 * rng.standard_normal((I, h), dtype=np.float32))
+    wu = O.round_bf16(0.05 * rng.standard_normal((I, h), dtype=np.float32))
+    wdn = O.round_bf16(0.05 * rng.standard_normal((h, I), dtype=np.float32))
+    dy = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    xr = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    f64 = lambda a: a.astype(np.float64)  # noqa: E731
+    y_r = O.tiled_mlp(f64(x), f64(wg), f64(wu), f64(wdn), num_tiles=-(-n // tile)) + xr
+    dx_r, dwg_r, dwu_r, dwd_r = O.tiled_mlp_bwd(f64(x), f64(wg), f64(wu), f64(wdn), f64(dy), num_tiles=-(-n // tile))
+    wgu = np.empty((2 * I, h), np.float32)
+    for j in range(I // 32):
+        wgu[64 * j:64 * j + 32] = wg[32 * j:32 * j + 32]
+        wgu[64 * j + 32:64 * j + 64] = wu[32 * j:32 * j + 32]
+    xd, wgud, wdd, dyd, xrd = bf16_dev(x), bf16_dev(wgu), bf16_dev(wdn), bf16_dev(dy), bf16_dev(xr)
+    ws = T.empty(_lib().spt_mlp_workspace(tile, I), dtype=T.uint8, device="cuda")
+    y = T.empty(n, h, dtype=T.bfloat16, device="cuda")
+    S.check(_lib().spt_mlp_fwd(xd.data_ptr(), wgud.data_ptr(), wdd.data_ptr(), xrd.data_ptr(), y.data_ptr(), n, h, I,
+                               tile, ws.data_ptr(), None))
+    T.cuda.synchronize()
+    assert rel_err(to_np(y), y_r) < 1e-2
+    dx = T.empty(n, h, dtype=T.bfloat16, device="cuda")
+    dwgu = T.empty(2 * I, h, device="cuda")
+    dwd = T.empty(h, I, device="cuda")
+    S.check(_lib().spt_mlp_bwd(xd.data_ptr(), wgud.data_ptr(), wdd.data_ptr(), dyd.data_ptr(), dx.data_ptr(),
+                               dwgu.data_ptr(), dwd.data_ptr(), 0, n, h, I, tile, ws.data_ptr(), None))
+    T.cuda.synchronize()
+    g = to_np(dwgu)
+    dwg = np.concatenate([g[64 * j:64 * j + 32] for j in range(I // 32)])
+    dwu = np.concatenate([g[64 * j + 32:64 * j + 64] for j in range(I // 32)])
+    assert rel_err(to_np(dx), dx_r) < 2e-2
+    assert rel_err(dwg, dwg_r) < 2e-2
+    assert rel_err(dwu, dwu_r) < 2e-2
+    assert rel_err(to_np(dwd), dwd_r) < 2e-2
