@@ -16,7 +16,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I/usr/include"]
-SOURCES = ["util.cpp", "plan.cpp", "comm.cpp", "gemm.cu", "kernels.cu", "attention.cu", "tiled.cu", "engine.cu"]
+SOURCES = ["util.cpp", "plan.cpp", "comm.cpp", "gemm.cu", "kernels.cu", "attention.cu", "attention_tc.cu", "tiled.cu", "engine.cu"]
 DEPS_HDR = [f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + ["../../include/sptrain_b200.h"]
 
 

@@ -13,6 +13,8 @@
 // group's q heads and the visible q blocks) + dQ pass (Q-outer): no atomics, bitwise deterministic
 // (SPEC.md:102).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.h"
 #include "launch.h"
@@ -619,9 +621,21 @@ static void check_attn(int64_t s, int hq, int hkv, int d) {
     SPT_CHECK(d == 32 || d == 64 || d == 128, SPT_ERR_SHAPE, "attention: head_dim must be 32, 64 or 128");
 }
 
+bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
+                 float* lse, cudaStream_t st);
+
+static int attn_impl() {
+    static int v = [] {
+        const char* e = getenv("SPT_ATTN_IMPL");  // "mma" forces the mma.sync kernels (A/B comparisons)
+        return (e && std::string(e) == "mma") ? 0 : 1;
+    }();
+    return v;
+}
+
 void attn_fwd(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o, float* lse,
               cudaStream_t st) {
     check_attn(s, hq, hkv, d);
+    if (attn_impl() == 1 && attn_fwd_tc(qkv, s, hq, hkv, d, seg, scale, o, lse, st)) return;
     if (d == 128) attn_fwd_t<128>(qkv, s, hq, hkv, seg, scale, o, lse, st);
     else if (d == 64) attn_fwd_t<64>(qkv, s, hq, hkv, seg, scale, o, lse, st);
     else attn_fwd_t<32>(qkv, s, hq, hkv, seg, scale, o, lse, st);

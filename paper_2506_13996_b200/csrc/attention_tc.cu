@@ -1,0 +1,317 @@
+// tcgen05 / TMEM / TMA flash-attention forward for head_dim 128 (K3, Blackwell-native).
+//
+// CTA = (pair of consecutive 128-row query tiles, q head); 10 warps:
+//   warps 0-3  softmax warpgroup for tile 0, warps 4-7 for tile 1 (thread = query row)
+//   warp 8     MMA issuer (one lane) + TMEM owner (512 columns: S0 | S1 | O0 | O1)
+//   warp 9     TMA producer: Q tiles once, then K_j / V_j through a 3-slot ring
+// Per 128-key block j and tile t:  S_t = Q_t K_j^T (TMEM) -> softmax warps read S_t, mask
+// (causal / block-causal runs), online max with lazy rescale (only when the running
+// max grows by > 2^8, then O_t is rescaled in TMEM), P_t (bf16) -> swizzled smem -> O_t += P_t V_j.
+// MMA order S0 S1 | PV0 S0' PV1 S1' | ... keeps one tile's softmax overlapped with the other tile's
+// MMAs.  tcgen05 ops complete in issue order, so the commit that signals S_t(j+1) also certifies
+// PV_t(j) is done (P_t buffer reusable, O_t stable for a rescale).
+#include <algorithm>
+
+#include "common.h"
+#include "launch.h"
+#include "sm100.cuh"
+
+namespace spt {
+namespace fatc {
+
+constexpr int D = 128;
+constexpr int BQ = 128;   // rows per query tile
+constexpr int BK = 128;   // keys per block
+constexpr int TILE_BYTES = BQ * D * 2;  // 32 KiB (two 16 KiB SW128 column regions)
+constexpr int NSLOT = 3;
+constexpr int SMEM_Q = 0;
+constexpr int SMEM_P = 2 * TILE_BYTES;
+constexpr int SMEM_KV = 4 * TILE_BYTES;
+constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
+constexpr int SMEM_BYTES = SMEM_BAR + 256 + 1024;
+constexpr int THREADS = 320;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+constexpr float RESCALE_THRESHOLD = 8.f;  // log2 units
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+// K-major SW128 descriptor over a [128 rows][128 cols] bf16 tile stored as two 16 KiB column regions.
+__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk) {
+    return make_sdesc_sw128(tile + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+}
+// MN-major SW128 descriptor (rows = K, 64-wide MN blocks 16 KiB apart) advanced by kk*16 rows.
+__device__ __forceinline__ uint64_t mndesc(uint32_t tile, int kk) {
+    return make_sdesc_sw128(tile + kk * 2048, 16384, 1024);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
+                  float scale_log2, bf16* __restrict__ o, float* __restrict__ lse) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+    uint64_t* q_full = bar;
+    uint64_t* kv_full = bar + 1;
+    uint64_t* kv_empty = bar + 1 + NSLOT;
+    uint64_t* s_full = bar + 1 + 2 * NSLOT;  // [2]
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* o_done = p_full + 2;           // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+    const int warp = warp_id(), lane = lane_id();
+    const int npairs = (int)(s / (2 * BQ));
+    const int pair = npairs - 1 - (int)blockIdx.x;  // longest causal rows first
+    const int h = blockIdx.y;
+    const int kvh = h / (hq / hkv);
+    const int64_t q0 = (int64_t)pair * 2 * BQ;
+    // key-block ranges per tile
+    int jb[2], je[2];
+    for (int t = 0; t < 2; ++t) {
+        const int64_t first = q0 + t * BQ;
+        je[t] = (int)((first + BQ - 1) / BK);
+        jb[t] = seg ? (int)(seg[first] / BK) : 0;
+    }
+    const int jlo = min(jb[0], jb[1]), jhi = max(je[0], je[1]);
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < NSLOT; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 128);
+            mbar_init(&o_done[t], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 8) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sbase = smem_u32(smem);
+
+    if (warp == 9) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tm);
+            mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
+            for (int t = 0; t < 2; ++t)
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tm, q_full, smem + SMEM_Q + t * TILE_BYTES + r * 16384, h * D + 64 * r,
+                                (int)(q0 + t * BQ));
+            int li = 0;
+            for (int j = jlo; j <= jhi; ++j) {
+                for (int w = 0; w < 2; ++w, ++li) {  // w=0: K_j, w=1: V_j
+                    const int slot = li % NSLOT;
+                    const uint32_t ph = (li / NSLOT) & 1;
+                    mbar_wait(&kv_empty[slot], ph ^ 1);
+                    mbar_arrive_expect_tx(&kv_full[slot], TILE_BYTES);
+                    const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                    for (int r = 0; r < 2; ++r)
+                        tma_load_2d(&tm, &kv_full[slot], smem + SMEM_KV + slot * TILE_BYTES + r * 16384, col + 64 * r,
+                                    j * BK);
+                }
+            }
+        }
+    } else if (warp == 8) {
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BK, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(BQ, D, false, true);
+            mbar_wait(q_full, 0);
+            int pv_count[2] = {0, 0};
+            auto uses = [&](int t, int j) { return j >= jb[t] && j <= je[t]; };
+            auto slot_of = [&](int j, int w) { return (2 * (j - jlo) + w) % NSLOT; };
+            auto phase_of = [&](int j, int w) { return (uint32_t)(((2 * (j - jlo) + w) / NSLOT) & 1); };
+            auto issue_s = [&](int t, int j) {
+                mbar_wait(&kv_full[slot_of(j, 0)], phase_of(j, 0));
+                tc_fence_after();
+                const uint32_t qa = sbase + SMEM_Q + t * TILE_BYTES;
+                const uint32_t kb = sbase + SMEM_KV + slot_of(j, 0) * TILE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) mma_bf16_ss(tmem + t * BK, kdesc(qa, kk), kdesc(kb, kk), idesc_s, kk > 0);
+                mma_commit(&s_full[t]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                mbar_wait(&p_full[t], pv_count[t] & 1);
+                mbar_wait(&kv_full[slot_of(j, 1)], phase_of(j, 1));
+                tc_fence_after();
+                const uint32_t pa = sbase + SMEM_P + t * TILE_BYTES;
+                const uint32_t vb = sbase + SMEM_KV + slot_of(j, 1) * TILE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                    mma_bf16_ss(tmem + 256 + t * D, kdesc(pa, kk), mndesc(vb, kk), idesc_o, (pv_count[t] > 0 || kk > 0));
+                ++pv_count[t];
+            };
+            if (uses(0, jlo)) issue_s(0, jlo);
+            if (uses(1, jlo)) issue_s(1, jlo);
+            mma_commit(&kv_empty[slot_of(jlo, 0)]);
+            for (int j = jlo; j <= jhi; ++j) {
+                if (uses(0, j)) issue_pv(0, j);
+                if (j + 1 <= jhi && uses(0, j + 1)) issue_s(0, j + 1);
+                if (uses(1, j)) issue_pv(1, j);
+                mma_commit(&kv_empty[slot_of(j, 1)]);
+                if (j + 1 <= jhi) {
+                    if (uses(1, j + 1)) issue_s(1, j + 1);
+                    mma_commit(&kv_empty[slot_of(j + 1, 0)]);
+                }
+            }
+            mma_commit(&o_done[0]);
+            mma_commit(&o_done[1]);
+        }
+    } else {
+        // ---------------- softmax warpgroups
+        const int t = warp >> 2;
+        const int sub = warp & 3;
+        const int r = sub * 32 + lane;
+        const int64_t q = q0 + t * BQ + r;
+        const int start = seg ? seg[q] : 0;
+        const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+        const uint32_t s_tm = tmem + lane_off + t * BK;
+        const uint32_t o_tm = tmem + lane_off + 256 + t * D;
+        uint8_t* prow = smem + SMEM_P + t * TILE_BYTES + r * 128;
+        float m_use = -INFINITY, l = 0.f;
+        int n = 0;
+        for (int j = jb[t]; j <= je[t]; ++j, ++n) {
+            mbar_wait(&s_full[t], n & 1);
+            tc_fence_after();
+            uint32_t v[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(s_tm + c * 32, v[c]);
+            tmem_ld_wait();
+            const int64_t k0 = (int64_t)j * BK;
+            const bool need_mask = seg != nullptr || (k0 + BK - 1 > q0 + t * BQ);
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    float x = __uint_as_float(v[c][i]) * scale_log2;
+                    if (need_mask) {
+                        const int64_t key = k0 + c * 32 + i;
+                        if (key > q || key < start) x = -INFINITY;
+                    }
+                    v[c][i] = __float_as_uint(x);
+                    mx = fmaxf(mx, x);
+                }
+            }
+            if (mx > m_use + RESCALE_THRESHOLD) {
+                if (m_use != -INFINITY && n > 0) {
+                    const float alpha = ex2(m_use - mx);
+                    l *= alpha;
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t ov[32];
+                        tmem_ld32(o_tm + c * 32, ov);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                        tmem_st32(o_tm + c * 32, ov);
+                    }
+                    tmem_st_wait();
+                }
+                m_use = mx;
+            }
+            const float base = m_use == -INFINITY ? 0.f : m_use;
+            float rs = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                // 32 keys -> 4 chunks of 8 bf16 in region c/2, chunks (c&1)*4 .. +3
+                uint8_t* reg = prow + (c >> 1) * 16384;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float p[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        p[e] = ex2(__uint_as_float(v[c][8 * k + e]) - base);
+                        rs += p[e];
+                    }
+                    const int chunk = (c & 1) * 4 + k;
+                    uint4 w;
+                    w.x = pack_bf16x2(p[0], p[1]);
+                    w.y = pack_bf16x2(p[2], p[3]);
+                    w.z = pack_bf16x2(p[4], p[5]);
+                    w.w = pack_bf16x2(p[6], p[7]);
+                    *reinterpret_cast<uint4*>(reg + ((chunk ^ (r & 7)) << 4)) = w;
+                }
+            }
+            l += rs;
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(&p_full[t]);
+        }
+        // epilogue: O_t / l -> global, lse
+        mbar_wait(&o_done[t], 0);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* orow = o + (q * hq + h) * D;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(o_tm + c * 32, ov);
+            tmem_ld_wait();
+            float f[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(ov[i]) * inv;
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 w;
+                w.x = pack_bf16x2(f[8 * k + 0], f[8 * k + 1]);
+                w.y = pack_bf16x2(f[8 * k + 2], f[8 * k + 3]);
+                w.z = pack_bf16x2(f[8 * k + 4], f[8 * k + 5]);
+                w.w = pack_bf16x2(f[8 * k + 6], f[8 * k + 7]);
+                dst[k] = w;
+            }
+        }
+        lse[(int64_t)h * s + q] = l > 0.f ? (m_use + __log2f(l)) * LN2 : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace fatc
+
+bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
+                 float* lse, cudaStream_t st) {
+    if (d != fatc::D || s % 256 != 0) return false;
+    const int64_t width = (int64_t)(hq + 2 * hkv) * d;
+    CUtensorMap tm = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
+    auto k = fatc::fwd_tc_kernel;
+    static bool attr = false;
+    if (!attr) {
+        SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::SMEM_BYTES));
+        attr = true;
+    }
+    dim3 grid((unsigned)(s / 256), (unsigned)hq);
+    k<<<grid, fatc::THREADS, fatc::SMEM_BYTES, st>>>(tm, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+    return true;
+}
+
+}  // namespace spt

@@ -201,7 +201,8 @@ def _attn_case(s, hq, hkv, d, packed, seed):
 
 
 @pytest.mark.parametrize("s,hq,hkv,d,packed", [(256, 4, 2, 32, False), (384, 4, 1, 128, False), (512, 2, 2, 64, True),
-                                               (256, 8, 2, 128, True)])
+                                               (256, 8, 2, 128, True), (1024, 4, 2, 128, False),
+                                               (2048, 2, 1, 128, True), (1536, 2, 2, 128, False)])
 def test_attention_fwd_bwd(s, hq, hkv, d, packed):
     T = torch()
     qkv, dout, starts = _attn_case(s, hq, hkv, d, packed, s + d)
