@@ -579,6 +579,10 @@ static void attn_fwd_t(const void* qkv, int64_t s, int hq, int hkv, const int32_
     SPT_CUDA(cudaGetLastError());
 }
 
+bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* Dv, int64_t s, int hq, int hkv,
+                 int d, const int32_t* seg, float scale, void* dqkv, cudaStream_t st);
+static int attn_impl();
+
 template <int D>
 static void attn_bwd_t(const void* qkv, const void* o, const float* lse, const void* dout, int64_t s, int hq, int hkv,
                        const int32_t* seg, float scale, void* dqkv, void* ws, cudaStream_t st) {
@@ -587,6 +591,7 @@ static void attn_bwd_t(const void* qkv, const void* o, const float* lse, const v
         (const bf16*)o, (const bf16*)dout, s, hq, Dv);
     count_launch();
     SPT_CUDA(cudaGetLastError());
+    if (attn_impl() == 1 && attn_bwd_tc(qkv, dout, lse, Dv, s, hq, hkv, D, seg, scale, dqkv, st)) return;
     {
         constexpr int smem = (2 * 128 + 4 * 64) * D * 2 + 4 * 64 * 4;
         auto k = fa::bwd_dkdv_kernel<D>;

@@ -55,7 +55,7 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
     const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
     const int grid = std::min(ntiles, num_sms());
     kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep);
-    count_launch();
+    count_launch("gemm");
     SPT_CUDA(cudaGetLastError());
 }
 

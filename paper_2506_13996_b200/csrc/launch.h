@@ -16,7 +16,7 @@ struct GemmOperand {
     bool mn_major;  // false: element (row, k) at ptr[row*ld + k]; true: at ptr[k*ld + row]
 };
 
-void count_launch();
+void count_launch(const char* tag = nullptr);
 int64_t launch_count();
 
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,

@@ -1,5 +1,7 @@
 // Process-wide plumbing: last-error slot, SM count, launch counter, version.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -14,7 +16,21 @@ static std::atomic<int64_t> g_launches{0};
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// SPT_TRACE=1: synchronise after every launch and log it (debugging hangs / async faults).
+void count_launch(const char* tag) {
+    const int64_t n = g_launches.fetch_add(1, std::memory_order_relaxed);
+    static const bool trace = [] {
+        const char* e = getenv("SPT_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (trace) {
+        fprintf(stderr, "[spt] launch %lld %s ...", (long long)n, tag ? tag : "");
+        fflush(stderr);
+        cudaError_t e = cudaDeviceSynchronize();
+        fprintf(stderr, " %s\n", cudaGetErrorString(e));
+        fflush(stderr);
+    }
+}
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {

@@ -185,9 +185,9 @@ def test_label_stats_and_segments():
 
 
 # ------------------------------------------------------------------ attention
-def _attn_case(s, hq, hkv, d, packed, seed):
+def _attn_case(s, hq, hkv, d, packed, seed, amp=1.0):
     rng = np.random.default_rng(seed)
-    qkv = O.round_bf16(rng.standard_normal((s, hq + 2 * hkv, d), dtype=np.float32))
+    qkv = O.round_bf16(amp * rng.standard_normal((s, hq + 2 * hkv, d), dtype=np.float32))
     dout = O.round_bf16(rng.standard_normal((s, hq, d), dtype=np.float32))
     if packed:
         runs = []
@@ -200,12 +200,15 @@ def _attn_case(s, hq, hkv, d, packed, seed):
     return qkv, dout, starts
 
 
-@pytest.mark.parametrize("s,hq,hkv,d,packed", [(256, 4, 2, 32, False), (384, 4, 1, 128, False), (512, 2, 2, 64, True),
-                                               (256, 8, 2, 128, True), (1024, 4, 2, 128, False),
-                                               (2048, 2, 1, 128, True), (1536, 2, 2, 128, False)])
-def test_attention_fwd_bwd(s, hq, hkv, d, packed):
+@pytest.mark.parametrize("s,hq,hkv,d,packed,amp", [(256, 4, 2, 32, False, 1), (384, 4, 1, 128, False, 1),
+                                                   (512, 2, 2, 64, True, 1), (256, 8, 2, 128, True, 1),
+                                                   (1024, 4, 2, 128, False, 1), (2048, 2, 1, 128, True, 1),
+                                                   (1536, 2, 2, 128, False, 1), (1024, 2, 1, 128, False, 2.5),
+                                                   (1024, 2, 2, 128, True, 2.5)])
+def test_attention_fwd_bwd(s, hq, hkv, d, packed, amp):
+    """amp > 1 gives peaked softmax rows: exercises the lazy O-rescale path of the tcgen05 forward."""
     T = torch()
-    qkv, dout, starts = _attn_case(s, hq, hkv, d, packed, s + d)
+    qkv, dout, starts = _attn_case(s, hq, hkv, d, packed, s + d, amp)
     q, k, v = qkv[:, :hq], qkv[:, hq:hq + hkv], qkv[:, hq + hkv:]
     o_r, lse_r = O.attention_fwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), starts)
     qkvd, doutd = bf16_dev(qkv), bf16_dev(dout)
