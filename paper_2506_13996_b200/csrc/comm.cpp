@@ -1,15 +1,67 @@
 #include "comm.h"
 
+#include <dlfcn.h>
+
 #include <cstring>
+#include <mutex>
 #include <sstream>
 
 #include "common.h"
 
 namespace spt {
-#define SPT_NCCL(call)                                                                                       \
-    do {                                                                                                     \
-        ncclResult_t r_ = (call);                                                                            \
-        if (r_ != ncclSuccess) SPT_THROW(SPT_ERR_COLLECTIVE, std::string(#call " failed: ") + ncclGetErrorString(r_)); \
+// NCCL is resolved lazily with dlopen when the first NCCL communicator is created, so loading this
+// library never pins an NCCL build into the process: if PyTorch already loaded its NCCL, dlopen
+// returns that same library; otherwise the system libnccl.so.2 is used.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
+    const char* (*GetErrorString)(ncclResult_t);
+};
+
+static const NcclApi& nccl_api() {
+    static NcclApi api{};
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+            return;
+        }
+        auto sym = [&](const char* n) {
+            void* p = dlsym(h, n);
+            if (!p && err.empty()) err = std::string("libnccl.so.2 lacks ") + n;
+            return p;
+        };
+        api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+        api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+        api.Send = (decltype(api.Send))sym("ncclSend");
+        api.Recv = (decltype(api.Recv))sym("ncclRecv");
+        api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+        api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+        api.CommGetAsyncError = (decltype(api.CommGetAsyncError))sym("ncclCommGetAsyncError");
+        api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    });
+    SPT_CHECK(err.empty(), SPT_ERR_COLLECTIVE, err);
+    return api;
+}
+
+#define SPT_NCCL(call)                                                                                             \
+    do {                                                                                                           \
+        ncclResult_t r_ = nccl_api().call;                                                                         \
+        if (r_ != ncclSuccess)                                                                                     \
+            SPT_THROW(SPT_ERR_COLLECTIVE, std::string("nccl" #call " failed: ") + nccl_api().GetErrorString(r_)); \
     } while (0)
 }  // namespace spt
 
@@ -28,12 +80,12 @@ void spt_comm::all_to_all(const char* tag, const std::vector<const void*>& send,
                                          cudaMemcpyDeviceToDevice, st));
         return;
     }
-    SPT_NCCL(ncclGroupStart());
+    SPT_NCCL(GroupStart());
     for (int j = 0; j < nranks; ++j) {
-        SPT_NCCL(ncclSend((const char*)send[0] + (size_t)j * bytes_per_peer, bytes_per_peer, ncclChar, j, nccl, st));
-        SPT_NCCL(ncclRecv((char*)recv[0] + (size_t)j * bytes_per_peer, bytes_per_peer, ncclChar, j, nccl, st));
+        SPT_NCCL(Send((const char*)send[0] + (size_t)j * bytes_per_peer, bytes_per_peer, ncclChar, j, nccl, st));
+        SPT_NCCL(Recv((char*)recv[0] + (size_t)j * bytes_per_peer, bytes_per_peer, ncclChar, j, nccl, st));
     }
-    SPT_NCCL(ncclGroupEnd());
+    SPT_NCCL(GroupEnd());
 }
 
 void spt_comm::all_reduce(const char* tag, void* buf, size_t count, ncclDataType_t dt, cudaStream_t st) {
@@ -42,7 +94,7 @@ void spt_comm::all_reduce(const char* tag, void* buf, size_t count, ncclDataType
     size_t es = dt == ncclFloat32 ? 4 : dt == ncclFloat64 || dt == ncclInt64 ? 8 : dt == ncclBfloat16 ? 2 : 4;
     s.bytes_sent += (int64_t)(count * es * 2 * (nranks - 1) / std::max(1, nranks));
     if (loopback || nranks == 1) return;
-    SPT_NCCL(ncclAllReduce(buf, buf, count, dt, ncclSum, nccl, st));
+    SPT_NCCL(AllReduce(buf, buf, count, dt, ncclSum, nccl, st));
 }
 
 void spt_comm::all_gather(const char* tag, const void* in, void* out, size_t bytes, cudaStream_t st) {
@@ -53,15 +105,15 @@ void spt_comm::all_gather(const char* tag, const void* in, void* out, size_t byt
         if (out != in) SPT_CUDA(cudaMemcpyAsync(out, in, bytes * (loopback ? nranks : 1), cudaMemcpyDeviceToDevice, st));
         return;
     }
-    SPT_NCCL(ncclAllGather(in, out, bytes, ncclChar, nccl, st));
+    SPT_NCCL(AllGather(in, out, bytes, ncclChar, nccl, st));
 }
 
 void spt_comm::check_async() {
     if (loopback || !nccl) return;
     ncclResult_t ar;
-    SPT_NCCL(ncclCommGetAsyncError(nccl, &ar));
+    SPT_NCCL(CommGetAsyncError(nccl, &ar));
     if (ar != ncclSuccess && ar != ncclInProgress)
-        SPT_THROW(SPT_ERR_PROTOCOL, std::string("NCCL async error: ") + ncclGetErrorString(ar));
+        SPT_THROW(SPT_ERR_PROTOCOL, std::string("NCCL async error: ") + nccl_api().GetErrorString(ar));
 }
 
 std::string spt_comm::stats_json() const {
@@ -82,7 +134,7 @@ extern "C" {
 spt_status spt_comm_unique_id(uint8_t out_id[128]) {
     return capi_guard([&] {
         ncclUniqueId id;
-        SPT_NCCL(ncclGetUniqueId(&id));
+        SPT_NCCL(GetUniqueId(&id));
         static_assert(sizeof(id) == 128, "ncclUniqueId size");
         std::memcpy(out_id, &id, 128);
     });
@@ -99,10 +151,10 @@ spt_status spt_comm_init_rank(const uint8_t id[128], int32_t nranks, int32_t ran
         if (nranks > 1) {
             ncclUniqueId uid;
             std::memcpy(&uid, id, 128);
-            ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
+            ncclResult_t r = nccl_api().CommInitRank(&c->nccl, nranks, uid, rank);
             if (r != ncclSuccess) {
                 delete c;
-                SPT_THROW(SPT_ERR_COLLECTIVE, std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r));
+                SPT_THROW(SPT_ERR_COLLECTIVE, std::string("ncclCommInitRank failed: ") + nccl_api().GetErrorString(r));
             }
         }
         *out = c;
@@ -125,7 +177,7 @@ spt_status spt_comm_init_loopback(int32_t nranks, int32_t device, spt_comm** out
 spt_status spt_comm_destroy(spt_comm* comm) {
     return capi_guard([&] {
         if (!comm) return;
-        if (comm->nccl) ncclCommDestroy(comm->nccl);
+        if (comm->nccl) nccl_api().CommDestroy(comm->nccl);
         delete comm;
     });
 }
