@@ -41,14 +41,21 @@ def peaks():
 
 
 # ------------------------------------------------------------------------------- CPU reference arm
+_CPU_CACHE = {}
+
+
 def cpu_layer_sample(n_tokens: int, seed: int = 0):
+    """One oracle layer step (fwd+bwd) on an n_tokens sample of the workload; returns (seconds, loss)."""
     import numpy as np
 
     from oracle import sptrain_oracle as O
 
     cfg = O.LLAMA8B
-    p = O.LayerParams(**O.synth_params(cfg, seed)).astype(np.float32)
-    x, lab, pos = O.synth_batch(cfg, n_tokens, seed)
+    key = (n_tokens, seed)
+    if key not in _CPU_CACHE:  # synthetic weights/batch are set-up, not part of the timed step
+        p = O.LayerParams(**O.synth_params(cfg, seed)).astype(np.float32)
+        _CPU_CACHE[key] = (p, O.synth_batch(cfg, n_tokens, seed))
+    p, (x, lab, pos) = _CPU_CACHE[key]
     t0 = time.perf_counter()
     res = O.layer_step(p, cfg, x.astype(np.float32), lab, None, P=1, dtype=np.float32)
     return time.perf_counter() - t0, res.loss

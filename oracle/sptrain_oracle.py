@@ -494,7 +494,7 @@ class LayerParams:
     wlm: np.ndarray  # [V, h]
 
     def astype(self, dt):
-        return LayerParams(**{k: getattr(self, k).astype(dt) for k in self.__dataclass_fields__})
+        return LayerParams(**{k: np.asarray(getattr(self, k), dtype=dt) for k in self.__dataclass_fields__})
 
     NAMES = ("g1", "wqkv", "wo", "g2", "wg", "wu", "wd", "g3", "wlm")
 

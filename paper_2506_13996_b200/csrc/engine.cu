@@ -29,6 +29,7 @@
 #include "gemm.cuh"
 #include "launch.h"
 #include "plan.h"
+#include "prof.h"
 
 namespace spt {
 
@@ -104,68 +105,7 @@ struct DeviceLedger {
     }
 };
 
-// ---------------------------------------------------------------- per-kernel-class event timing
-struct Prof {
-    bool on = false;
-    struct Rec {
-        int cls;
-        cudaEvent_t a, b;
-        double flops, bytes;
-    };
-    std::vector<Rec> recs;
-    std::vector<cudaEvent_t> pool;
-    size_t used = 0;
-    static constexpr int NCLS = 8;
-    static const char* name(int c) {
-        static const char* n[] = {"gemm", "attn_fwd", "attn_bwd", "rmsnorm", "reshard", "ce_rows", "comm", "other"};
-        return n[c];
-    }
-    cudaEvent_t ev() {
-        if (used == pool.size()) {
-            cudaEvent_t e;
-            SPT_CUDA(cudaEventCreate(&e));
-            pool.push_back(e);
-        }
-        return pool[used++];
-    }
-    void reset() {
-        recs.clear();
-        used = 0;
-    }
-    template <class F>
-    void run(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
-        if (!on) {
-            f();
-            return;
-        }
-        cudaEvent_t a = ev(), b = ev();
-        SPT_CUDA(cudaEventRecord(a, st));
-        f();
-        SPT_CUDA(cudaEventRecord(b, st));
-        recs.push_back({cls, a, b, flops, bytes});
-    }
-    std::string json() {
-        double ms[NCLS] = {}, fl[NCLS] = {}, by[NCLS] = {};
-        int cnt[NCLS] = {};
-        for (auto& r : recs) {
-            float t = 0;
-            SPT_CUDA(cudaEventSynchronize(r.b));
-            SPT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
-            ms[r.cls] += t;
-            fl[r.cls] += r.flops;
-            by[r.cls] += r.bytes;
-            cnt[r.cls] += 1;
-        }
-        std::ostringstream os;
-        os << "{";
-        for (int c = 0; c < NCLS; ++c)
-            os << (c ? "," : "") << "\"" << name(c) << "\":{\"ms\":" << ms[c] << ",\"launches\":" << cnt[c]
-               << ",\"flops\":" << fl[c] << ",\"bytes\":" << by[c] << "}";
-        os << "}";
-        return os.str();
-    }
-};
-enum { P_GEMM = 0, P_ATTN_F, P_ATTN_B, P_NORM, P_RESHARD, P_CE, P_COMM, P_OTHER };
+
 
 }  // namespace spt
 
@@ -350,6 +290,10 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     const float scale = 1.f / std::sqrt((float)d);
     Prof& pf = Ly->prof;
     pf.reset();
+    current_prof() = &pf;
+    struct ProfReset {
+        ~ProfReset() { current_prof() = nullptr; }
+    } prof_reset_guard;
     SPT_CUDA(cudaEventRecord(Ly->ev_step0, st));
     const cudaMemcpyKind kind = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
 
@@ -384,7 +328,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         EpiParams e;
         e.C = b.qkv;
         e.ldc = qo;
-        pf.run(P_GEMM, gflop(nl, qo, h), 0, st, [&] { gemm({b.xn1, h, false}, {Ly->wqkv, h, false}, nl, qo, h, EPI_BF16, e, st); });
+        gemm({b.xn1, h, false}, {Ly->wqkv, h, false}, nl, qo, h, EPI_BF16, e, st);
         if (P > 1)
             pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
                 reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv, st);
@@ -430,34 +374,29 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         e.ldc = h;
         e.R = b.x;
         e.ldr = h;
-        pf.run(P_GEMM, gflop(nl, h, qd), 0, st, [&] { gemm({b.o, qd, false}, {Ly->wo, qd, false}, nl, h, qd, EPI_BF16, e, st); });
+        gemm({b.o, qd, false}, {Ly->wo, qd, false}, nl, h, qd, EPI_BF16, e, st);
         pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x1, Ly->g2, b.xn2, b.rstd2, nl, h, Ly->eps, st); });
-        pf.run(P_GEMM, gflop(nl, 3 * I, h), 0, st,
-               [&] { mlp_fwd(b.xn2, Ly->wgu, Ly->wd, b.x1, b.x2, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st); });
+        mlp_fwd(b.xn2, Ly->wgu, Ly->wd, b.x1, b.x2, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
         pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x2, Ly->g3, b.z, b.rstd3, nl, h, Ly->eps, st); });
-        pf.run(P_GEMM, gflop(nl, V, h) * 3, 0, st, [&] {
-            flce(b.z, Ly->wlm, b.labels, nl, h, V, Ly->loss_tile, &Ly->sc->scale, &Ly->sc->loss_sum, b.dz, Ly->dwlm,
+        flce(b.z, Ly->wlm, b.labels, nl, h, V, Ly->loss_tile, &Ly->sc->scale, &Ly->sc->loss_sum, b.dz, Ly->dwlm,
                  acc, &Ly->sc->err_label, Ly->ws_flce, st);
-        });
         // backward
         bf16* dx2 = b.dx;  // scratch until the final dx is produced
         pf.run(P_NORM, 0, 3.0 * nl * h * 2, st,
                [&] { rmsnorm_bwd(b.x2, Ly->g3, b.rstd3, b.dz, nullptr, dx2, Ly->dg3, Ly->ws_rms, nl, h, st); });
         bf16* dxn2 = b.dz;
-        pf.run(P_GEMM, gflop(nl, I, h) * 8, 0, st, [&] {
-            mlp_bwd(b.xn2, Ly->wgu, Ly->wd, dx2, dxn2, Ly->dwgu, Ly->dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
-        });
+        mlp_bwd(b.xn2, Ly->wgu, Ly->wd, dx2, dxn2, Ly->dwgu, Ly->dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
         pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
                [&] { rmsnorm_bwd(b.x1, Ly->g2, b.rstd2, dxn2, dx2, b.dx1, Ly->dg2, Ly->ws_rms, nl, h, st); });
         EpiParams e1;
         e1.C = b.dO;
         e1.ldc = qd;
-        pf.run(P_GEMM, gflop(nl, qd, h), 0, st, [&] { gemm({b.dx1, h, false}, {Ly->wo, qd, true}, nl, qd, h, EPI_BF16, e1, st); });
+        gemm({b.dx1, h, false}, {Ly->wo, qd, true}, nl, qd, h, EPI_BF16, e1, st);
         EpiParams e2;
         e2.C = Ly->dwo;
         e2.ldc = qd;
         e2.accumulate = acc;
-        pf.run(P_GEMM, gflop(h, qd, nl), 0, st, [&] { gemm({b.dx1, h, true}, {b.o, qd, true}, h, qd, nl, EPI_F32, e2, st); });
+        gemm({b.dx1, h, true}, {b.o, qd, true}, h, qd, nl, EPI_F32, e2, st);
         if (P > 1)
             pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st,
                    [&] { reshard_pack(b.dO, nl, c.q_heads, d, P, hq, Ly->map_q, b.send_do, st); });
@@ -490,12 +429,12 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         EpiParams e1;
         e1.C = dxn1;
         e1.ldc = h;
-        pf.run(P_GEMM, gflop(nl, h, qo), 0, st, [&] { gemm({b.dqkv, qo, false}, {Ly->wqkv, h, true}, nl, h, qo, EPI_BF16, e1, st); });
+        gemm({b.dqkv, qo, false}, {Ly->wqkv, h, true}, nl, h, qo, EPI_BF16, e1, st);
         EpiParams e2;
         e2.C = Ly->dwqkv;
         e2.ldc = h;
         e2.accumulate = acc;
-        pf.run(P_GEMM, gflop(qo, h, nl), 0, st, [&] { gemm({b.dqkv, qo, true}, {b.xn1, h, true}, qo, h, nl, EPI_F32, e2, st); });
+        gemm({b.dqkv, qo, true}, {b.xn1, h, true}, qo, h, nl, EPI_F32, e2, st);
         pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
                [&] { rmsnorm_bwd(b.x, Ly->g1, b.rstd1, dxn1, b.dx1, b.dx, Ly->dg1, Ly->ws_rms, nl, h, st); });
     }

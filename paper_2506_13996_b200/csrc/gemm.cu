@@ -4,6 +4,7 @@
 #include "common.h"
 #include "gemm.cuh"
 #include "launch.h"
+#include "prof.h"
 
 namespace spt {
 
@@ -54,8 +55,10 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
     }
     const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
     const int grid = std::min(ntiles, num_sms());
-    kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep);
-    count_launch("gemm");
+    prof_run(P_GEMM, 2.0 * M * N * K, 0, st, [&] {
+        kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep);
+        count_launch("gemm");
+    });
     SPT_CUDA(cudaGetLastError());
 }
 

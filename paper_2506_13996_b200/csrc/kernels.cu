@@ -5,6 +5,7 @@
 
 #include "common.h"
 #include "launch.h"
+#include "prof.h"
 #include "sm100.cuh"
 
 namespace spt {
@@ -352,8 +353,10 @@ void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V
              float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st) {
     SPT_CHECK(V % 8 == 0, SPT_ERR_SHAPE, "vocab must be a multiple of 8");
     if (rows == 0) return;
-    ce_rows_kernel<<<(unsigned)rows, 512, 0, st>>>(logits, labels, V, scale_dev, loss_rows, (bf16*)dlogits, err);
-    count_launch();
+    prof_run(P_CE, 0, 6.0 * rows * V, st, [&] {
+        ce_rows_kernel<<<(unsigned)rows, 512, 0, st>>>(logits, labels, V, scale_dev, loss_rows, (bf16*)dlogits, err);
+        count_launch("ce_rows");
+    });
     SPT_CUDA(cudaGetLastError());
 }
 

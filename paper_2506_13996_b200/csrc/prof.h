@@ -1,0 +1,91 @@
+// Per-kernel-class CUDA-event timing inside the timed region (bench roofline evidence).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "launch.h"
+
+namespace spt {
+
+// ---------------------------------------------------------------- per-kernel-class event timing
+struct Prof {
+    bool on = false;
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+        double flops, bytes;
+        int64_t launches;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    static constexpr int NCLS = 8;
+    static const char* name(int c) {
+        static const char* n[] = {"gemm", "attn_fwd", "attn_bwd", "rmsnorm", "reshard", "ce_rows", "comm", "other"};
+        return n[c];
+    }
+    cudaEvent_t ev() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            SPT_CUDA(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void reset() {
+        recs.clear();
+        used = 0;
+    }
+    template <class F>
+    void run(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
+        if (!on) {
+            f();
+            return;
+        }
+        cudaEvent_t a = ev(), b = ev();
+        const int64_t n0 = launch_count();
+        SPT_CUDA(cudaEventRecord(a, st));
+        f();
+        SPT_CUDA(cudaEventRecord(b, st));
+        recs.push_back({cls, a, b, flops, bytes, launch_count() - n0});
+    }
+    std::string json() {
+        double ms[NCLS] = {}, fl[NCLS] = {}, by[NCLS] = {};
+        int cnt[NCLS] = {};
+        for (auto& r : recs) {
+            float t = 0;
+            SPT_CUDA(cudaEventSynchronize(r.b));
+            SPT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            ms[r.cls] += t;
+            fl[r.cls] += r.flops;
+            by[r.cls] += r.bytes;
+            cnt[r.cls] += (int)r.launches;
+        }
+        std::ostringstream os;
+        os << "{";
+        for (int c = 0; c < NCLS; ++c)
+            os << (c ? "," : "") << "\"" << name(c) << "\":{\"ms\":" << ms[c] << ",\"launches\":" << cnt[c]
+               << ",\"flops\":" << fl[c] << ",\"bytes\":" << by[c] << "}";
+        os << "}";
+        return os.str();
+    }
+};
+enum { P_GEMM = 0, P_ATTN_F, P_ATTN_B, P_NORM, P_RESHARD, P_CE, P_COMM, P_OTHER };
+
+// The engine installs its Prof here for the duration of a step; library launchers (gemm, ce_rows)
+// self-report so multi-kernel helpers (flce, mlp) are attributed per kernel class.
+Prof*& current_prof();
+
+template <class F>
+inline void prof_run(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
+    Prof* p = current_prof();
+    if (p && p->on) p->run(cls, flops, bytes, st, f);
+    else f();
+}
+
+}  // namespace spt

@@ -33,6 +33,12 @@ void count_launch(const char* tag) {
 }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+struct Prof;
+Prof*& current_prof() {
+    static thread_local Prof* p = nullptr;
+    return p;
+}
+
 int num_sms() {
     static thread_local int dev_cached = -1, sms = 0;
     int dev = 0;
