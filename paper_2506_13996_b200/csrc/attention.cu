@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(256) fwd_kernel(const bf16* __restrict__ qkv, 
 // ------------------------------------------------------------------ backward
 // D_i = sum_d dO_i * O_i  per (token, head), fp32 [hq][s]
 template <int D>
-__global__ void bwd_dot_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, int64_t s, int hq,
-                               float* __restrict__ Dv) {
+__global__ void bwd_dot_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, const float* __restrict__ lse,
+                               int64_t s, int hq, float* __restrict__ Dv, float* __restrict__ lse2) {
     const int64_t n = s * hq;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = i / hq;
@@ -281,6 +281,7 @@ __global__ void bwd_dot_kernel(const bf16* __restrict__ o, const bf16* __restric
             for (int k = 0; k < 8; ++k) acc += x[k] * y[k];
         }
         Dv[(int64_t)h * s + t] = acc;
+        lse2[(int64_t)h * s + t] = lse[(int64_t)h * s + t] * LOG2E;
     }
 }
 
@@ -587,11 +588,12 @@ template <int D>
 static void attn_bwd_t(const void* qkv, const void* o, const float* lse, const void* dout, int64_t s, int hq, int hkv,
                        const int32_t* seg, float scale, void* dqkv, void* ws, cudaStream_t st) {
     float* Dv = (float*)ws;
+    float* lse2 = Dv + s * hq;
     fa::bwd_dot_kernel<D><<<(unsigned)std::min<int64_t>((s * hq + 255) / 256, 148 * 16), 256, 0, st>>>(
-        (const bf16*)o, (const bf16*)dout, s, hq, Dv);
+        (const bf16*)o, (const bf16*)dout, lse, s, hq, Dv, lse2);
     count_launch();
     SPT_CUDA(cudaGetLastError());
-    if (attn_impl() == 1 && attn_bwd_tc(qkv, dout, lse, Dv, s, hq, hkv, D, seg, scale, dqkv, st)) return;
+    if (attn_impl() == 1 && attn_bwd_tc(qkv, dout, lse2, Dv, s, hq, hkv, D, seg, scale, dqkv, st)) return;
     {
         constexpr int smem = (2 * 128 + 4 * 64) * D * 2 + 4 * 64 * 4;
         auto k = fa::bwd_dkdv_kernel<D>;
@@ -649,7 +651,7 @@ void attn_fwd(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t*
 size_t attn_bwd_workspace(int64_t s, int hq, int hkv, int d) {
     (void)hkv;
     (void)d;
-    return (size_t)s * hq * 4;
+    return (size_t)s * hq * 4 * 2;  // D = rowsum(dO*O) and lse*log2(e)
 }
 
 void attn_bwd(const void* qkv, const void* o, const float* lse, const void* dout, int64_t s, int hq, int hkv, int d,

@@ -40,6 +40,10 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -189,32 +193,40 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
         const uint32_t s_tm = tmem + lane_off + t * BK;
         const uint32_t o_tm = tmem + lane_off + 256 + t * D;
-        uint8_t* prow = smem + SMEM_P + t * TILE_BYTES + r * 128;
-        float m_use = -INFINITY, l = 0.f;
+        const uint32_t prow = sbase + SMEM_P + t * TILE_BYTES + r * 128;
+        float m_use = -INFINITY, l = 0.f;  // running max in log2 units (scaled)
         int n = 0;
-        for (int j = jb[t]; j <= je[t]; ++j, ++n) {
+        const int jb_t = t ? jb[1] : jb[0], je_t = t ? je[1] : je[0];
+        for (int j = jb_t; j <= je_t; ++j, ++n) {
             mbar_wait(&s_full[t], n & 1);
             tc_fence_after();
-            uint32_t v[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(s_tm + c * 32, v[c]);
-            tmem_ld_wait();
             const int64_t k0 = (int64_t)j * BK;
-            const bool need_mask = seg != nullptr || (k0 + BK - 1 > q0 + t * BQ);
-            float mx = -INFINITY;
+            const bool need_mask = seg != nullptr || (k0 + BK - 1 > q0 + t * BQ);  // warp-uniform
+            // pass 1: row max of raw scores (scale > 0 commutes with max)
+            float mraw = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t v[2][32];
+                tmem_ld32(s_tm + h2 * 64, v[0]);
+                tmem_ld32(s_tm + h2 * 64 + 32, v[1]);
+                tmem_ld_wait();
+                if (need_mask) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float x = __uint_as_float(v[c][i]) * scale_log2;
-                    if (need_mask) {
-                        const int64_t key = k0 + c * 32 + i;
-                        if (key > q || key < start) x = -INFINITY;
-                    }
-                    v[c][i] = __float_as_uint(x);
-                    mx = fmaxf(mx, x);
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int64_t key = k0 + h2 * 64 + c * 32 + i;
+                            const float x = (key > q || key < start) ? -INFINITY : __uint_as_float(v[c][i]);
+                            mraw = fmaxf(mraw, x);
+                        }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(v[c][i]));
                 }
             }
+            const float mx = mraw * scale_log2;
             // lazy rescale; tcgen05.ld/st are warp-collective, so the O rescale runs warp-uniformly
             const bool grow = mx > m_use + RESCALE_THRESHOLD;
             const bool resc = grow && m_use != -INFINITY && n > 0;
@@ -233,27 +245,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             l *= alpha;
             if (grow) m_use = mx;
-            const float base = m_use == -INFINITY ? 0.f : m_use;
+            const float nbase = m_use == -INFINITY ? 0.f : -m_use;
+            // pass 2: p = 2^(s*scale_log2 - m) -> bf16 -> swizzled smem (K-major SW128 A operand)
             float rs = 0.f;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                // 32 keys -> 4 chunks of 8 bf16 in region c/2, chunks (c&1)*4 .. +3
-                uint8_t* reg = prow + (c >> 1) * 16384;
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t v[2][32];
+                tmem_ld32(s_tm + h2 * 64, v[0]);
+                tmem_ld32(s_tm + h2 * 64 + 32, v[1]);
+                tmem_ld_wait();
+                const uint32_t reg = prow + h2 * 16384;  // keys [64*h2, 64*h2+64) -> column region h2
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 8; ++k) {
                     float p[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        p[e] = ex2(__uint_as_float(v[c][8 * k + e]) - base);
+                        const int col = 8 * k + e;
+                        p[e] = ex2(fmaf(__uint_as_float(v[col >> 5][col & 31]), scale_log2, nbase));
+                        if (need_mask) {
+                            const int64_t key = k0 + h2 * 64 + col;
+                            if (key > q || key < start) p[e] = 0.f;
+                        }
                         rs += p[e];
                     }
-                    const int chunk = (c & 1) * 4 + k;
-                    uint4 w;
-                    w.x = pack_bf16x2(p[0], p[1]);
-                    w.y = pack_bf16x2(p[2], p[3]);
-                    w.z = pack_bf16x2(p[4], p[5]);
-                    w.w = pack_bf16x2(p[6], p[7]);
-                    *reinterpret_cast<uint4*>(reg + ((chunk ^ (r & 7)) << 4)) = w;
+                    sts128(reg + ((k ^ (r & 7)) << 4), pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]),
+                           pack_bf16x2(p[4], p[5]), pack_bf16x2(p[6], p[7]));
                 }
             }
             l += rs;
@@ -322,7 +338,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 __global__ void __launch_bounds__(THREADS, 1)
     dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                  const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
-                 const float* __restrict__ lse, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
+                 const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
     using namespace dq;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -445,14 +461,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int r = sub * 32 + lane;
         const int64_t q = q0 + t * 128 + r;
         const int start = seg ? seg[q] : 0;
-        const float lse2 = lse[(int64_t)h * s + q] * LOG2E;
+        const float nlse2 = -lse2v[(int64_t)h * s + q];  // -(lse * log2 e), precomputed
         const float Dq = Dv[(int64_t)h * s + q];
         const float sl2 = scale * LOG2E;
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         const uint32_t s_tm = tmem + lo + t * 256, dp_tm = s_tm + 64, dq_tm = s_tm + 128;
-        uint8_t* dsrow = smem + OFF_DS + t * DS_BYTES + r * 128;
+        const uint32_t dsrow = sbase + OFF_DS + t * DS_BYTES + r * 128;
+        const int jb_t = t ? jb[1] : jb[0], je_t = t ? je[1] : je[0];
         int n = 0;
-        for (int j = jb[t]; j <= je[t]; ++j, ++n) {
+        for (int j = jb_t; j <= je_t; ++j, ++n) {
             mbar_wait(&s_full[t], n & 1);
             tc_fence_after();
             uint32_t sv[2][32], dv[2][32];
@@ -464,28 +481,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t k0 = (int64_t)j * BKB;
             const bool need_mask = seg != nullptr || (k0 + BKB - 1 > q0 + t * 128);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
+            for (int k = 0; k < 8; ++k) {
+                float d8[8];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    float d8[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int i = 8 * k + e;
-                        float p = ex2(__uint_as_float(sv[c][i]) * sl2 - lse2);
-                        if (need_mask) {
-                            const int64_t key = k0 + c * 32 + i;
-                            if (key > q || key < start) p = 0.f;
-                        }
-                        d8[e] = p * (__uint_as_float(dv[c][i]) - Dq);
+                for (int e = 0; e < 8; ++e) {
+                    const int col = 8 * k + e;
+                    float p = ex2(fmaf(__uint_as_float(sv[col >> 5][col & 31]), sl2, nlse2));
+                    if (need_mask) {
+                        const int64_t key = k0 + col;
+                        if (key > q || key < start) p = 0.f;
                     }
-                    uint4 w;
-                    w.x = pack_bf16x2(d8[0], d8[1]);
-                    w.y = pack_bf16x2(d8[2], d8[3]);
-                    w.z = pack_bf16x2(d8[4], d8[5]);
-                    w.w = pack_bf16x2(d8[6], d8[7]);
-                    const int chunk = c * 4 + k;
-                    *reinterpret_cast<uint4*>(dsrow + ((chunk ^ (r & 7)) << 4)) = w;
+                    d8[e] = p * (__uint_as_float(dv[col >> 5][col & 31]) - Dq);
                 }
+                sts128(dsrow + ((k ^ (r & 7)) << 4), pack_bf16x2(d8[0], d8[1]), pack_bf16x2(d8[2], d8[3]),
+                       pack_bf16x2(d8[4], d8[5]), pack_bf16x2(d8[6], d8[7]));
             }
             fence_proxy_async();
             tc_fence_before();
@@ -537,7 +546,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 __global__ void __launch_bounds__(THREADS, 1)
     dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                    const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
-                   const float* __restrict__ lse, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
+                   const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
     using namespace dkv;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -672,11 +681,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
             tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
             tmem_ld_wait();
-            const float4* l4 = reinterpret_cast<const float4*>(lse + (int64_t)hh * s + qq);
+            const float4* l4 = reinterpret_cast<const float4*>(lse2v + (int64_t)hh * s + qq);
             const float4* d4 = reinterpret_cast<const float4*>(Dv + (int64_t)hh * s + qq);
             const bool need_mask = seg != nullptr || qq < k0 + 127;
-            uint8_t* prow = smem + OFF_PT + b * 2 * PT_BYTES + r * 128;
-            uint8_t* drow = prow + PT_BYTES;
+            const uint32_t prow = sbase + OFF_PT + b * 2 * PT_BYTES + r * 128;
+            const uint32_t drow = prow + PT_BYTES;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const float4 la = __ldg(l4 + 2 * k), lb = __ldg(l4 + 2 * k + 1);
@@ -687,7 +696,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int i = 8 * k + e;
-                    float p = ex2(__uint_as_float(sv[i]) * sl2 - lv[e] * LOG2E);
+                    float p = ex2(fmaf(__uint_as_float(sv[i]), sl2, -lv[e]));
                     if (need_mask) {
                         const int64_t qi = qq + i;
                         if (key > qi || (seg && key < seg[qi])) p = 0.f;
@@ -696,17 +705,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     s8[e] = p * (__uint_as_float(dv[i]) - dd[e]);
                 }
                 const int chunk = half * 4 + k;
-                uint4 w;
-                w.x = pack_bf16x2(p8[0], p8[1]);
-                w.y = pack_bf16x2(p8[2], p8[3]);
-                w.z = pack_bf16x2(p8[4], p8[5]);
-                w.w = pack_bf16x2(p8[6], p8[7]);
-                *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = w;
-                w.x = pack_bf16x2(s8[0], s8[1]);
-                w.y = pack_bf16x2(s8[2], s8[3]);
-                w.z = pack_bf16x2(s8[4], s8[5]);
-                w.w = pack_bf16x2(s8[6], s8[7]);
-                *reinterpret_cast<uint4*>(drow + ((chunk ^ (r & 7)) << 4)) = w;
+                const uint32_t off = (uint32_t)((chunk ^ (r & 7)) << 4);
+                sts128(prow + off, pack_bf16x2(p8[0], p8[1]), pack_bf16x2(p8[2], p8[3]), pack_bf16x2(p8[4], p8[5]),
+                       pack_bf16x2(p8[6], p8[7]));
+                sts128(drow + off, pack_bf16x2(s8[0], s8[1]), pack_bf16x2(s8[2], s8[3]), pack_bf16x2(s8[4], s8[5]),
+                       pack_bf16x2(s8[6], s8[7]));
             }
             fence_proxy_async();
             tc_fence_before();
@@ -770,7 +773,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
 }
 
 // Deterministic tcgen05 backward (d = 128, s % 256 == 0).  Dv = rowsum(dO * O) must be precomputed.
-bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* Dv, int64_t s, int hq, int hkv,
+bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const float* Dv, int64_t s, int hq, int hkv,
                  int d, const int32_t* seg, float scale, void* dqkv, cudaStream_t st) {
     if (d != fatc::D || s % 256 != 0) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
@@ -786,11 +789,11 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const floa
         attr = true;
     }
     fatc::dkdv_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::THREADS, fatc::dkv::SMEM, st>>>(
-        t128, t64, do64, s, hq, hkv, seg, lse, Dv, scale, (bf16*)dqkv);
+        t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
     fatc::dq_tc_kernel<<<dim3((unsigned)(s / 256), (unsigned)hq), fatc::THREADS, fatc::dq::SMEM, st>>>(
-        t128, t64, do128, s, hq, hkv, seg, lse, Dv, scale, (bf16*)dqkv);
+        t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dq_tc");
     SPT_CUDA(cudaGetLastError());
     return true;
