@@ -322,15 +322,16 @@ __device__ __forceinline__ uint64_t mndesc_r(uint32_t tile, int kk, uint32_t reg
 }
 
 // ------------------------------------------------------------------ dQ pass
-// CTA = (pair of 128-row q tiles, q head).  Per 64-key block j and tile t:
-//   S_t = Q_t K_j^T, dP_t = dO_t V_j^T (TMEM) -> dS_t = P (dP - D) (bf16, smem) -> dQ_t += dS_t K_j.
+// CTA = (128-row q tile, q head).  Per 64-key block j (double-buffered in TMEM):
+//   S_j = Q K_j^T, dP_j = dO V_j^T -> dS_j = P (dP - D) (bf16, smem, double-buffered) -> dQ += dS_j K_j.
+// 8 elementwise warps (2 per TMEM lane quarter, each owning 32 of the 64 key columns), 6-slot K/V ring.
 namespace dq {
 constexpr int BKB = 64;
 constexpr int Q_BYTES = 128 * D * 2;        // 32 KiB
 constexpr int KV_BYTES = BKB * D * 2;       // 16 KiB (two 8 KiB regions)
 constexpr int DS_BYTES = 128 * BKB * 2;     // 16 KiB (one region)
-constexpr int NSL = 4;
-constexpr int OFF_Q = 0, OFF_DO = 2 * Q_BYTES, OFF_DS = 4 * Q_BYTES, OFF_KV = OFF_DS + 2 * DS_BYTES;
+constexpr int NSL = 6;
+constexpr int OFF_Q = 0, OFF_DO = Q_BYTES, OFF_DS = 2 * Q_BYTES, OFF_KV = OFF_DS + 2 * DS_BYTES;
 constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dq
@@ -348,21 +349,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* kv_empty = kv_full + NSL;
     uint64_t* s_full = kv_empty + NSL;  // [2]
     uint64_t* ds_full = s_full + 2;      // [2]
-    uint64_t* dq_done = ds_full + 2;     // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 2);
+    uint64_t* dq_done = ds_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
     const int warp = warp_id(), lane = lane_id();
-    const int npairs = (int)(s / 256);
-    const int pair = npairs - 1 - (int)blockIdx.x;
+    const int nqb = (int)(s / 128);
+    const int qb = nqb - 1 - (int)blockIdx.x;  // longest rows first
     const int h = blockIdx.y;
     const int kvh = h / (hq / hkv);
-    const int64_t q0 = (int64_t)pair * 256;
-    int jb[2], je[2];
-    for (int t = 0; t < 2; ++t) {
-        const int64_t first = q0 + t * 128;
-        je[t] = (int)((first + 127) / BKB);
-        jb[t] = seg ? (int)(seg[first] / BKB) : 0;
-    }
-    const int jlo = min(jb[0], jb[1]), jhi = max(je[0], je[1]);
+    const int64_t q0 = (int64_t)qb * 128;
+    const int jb = seg ? (int)(seg[q0] / BKB) : 0;
+    const int je = (int)((q0 + 127) / BKB);
+    const int nblk = je - jb + 1;
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
         for (int i = 0; i < NSL; ++i) {
@@ -371,9 +368,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&ds_full[t], 128);
-            mbar_init(&dq_done[t], 1);
+            mbar_init(&ds_full[t], 256);
         }
+        mbar_init(dq_done, 1);
         fence_barrier_init();
     }
     if (warp == 8) {
@@ -387,126 +384,111 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t sbase = smem_u32(smem);
     if (warp == 9) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, 4 * Q_BYTES);
-            for (int t = 0; t < 2; ++t)
-                for (int r = 0; r < 2; ++r) {
-                    tma_load_2d(&tq, q_full, smem + OFF_Q + t * Q_BYTES + r * 16384, h * D + 64 * r, (int)(q0 + t * 128));
-                    tma_load_2d(&tdo, q_full, smem + OFF_DO + t * Q_BYTES + r * 16384, h * D + 64 * r,
-                                (int)(q0 + t * 128));
-                }
-            int li = 0;
-            for (int j = jlo; j <= jhi; ++j)
-                for (int w = 0; w < 2; ++w, ++li) {  // 0: K_j, 1: V_j
-                    const int slot = li % NSL;
-                    mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
-                    const int col = (hq + (w ? hkv : 0) + kvh) * D;
-                    for (int r = 0; r < 2; ++r)
-                        tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
-                                    j * BKB);
-                }
+            mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
+            for (int r = 0; r < 2; ++r) {
+                tma_load_2d(&tq, q_full, smem + OFF_Q + r * 16384, h * D + 64 * r, (int)q0);
+                tma_load_2d(&tdo, q_full, smem + OFF_DO + r * 16384, h * D + 64 * r, (int)q0);
+            }
+            for (int li = 0; li < 2 * nblk; ++li) {  // K_j, V_j, K_j+1, ...
+                const int j = jb + li / 2, w = li & 1;
+                const int slot = li % NSL;
+                mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
+                const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
+                                j * BKB);
+            }
         }
     } else if (warp == 8) {
         if (lane == 0) {
             constexpr uint32_t id_s = make_idesc_bf16(128, BKB, false, false);
             constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);
             mbar_wait(q_full, 0);
-            int nq[2] = {0, 0};
-            auto uses = [&](int t, int j) { return j >= jb[t] && j <= je[t]; };
-            auto slot = [&](int j, int w) { return (2 * (j - jlo) + w) % NSL; };
-            auto ph = [&](int j, int w) { return (uint32_t)(((2 * (j - jlo) + w) / NSL) & 1); };
-            auto issue_sdp = [&](int t, int j) {
-                mbar_wait(&kv_full[slot(j, 0)], ph(j, 0));
-                mbar_wait(&kv_full[slot(j, 1)], ph(j, 1));
+            const uint32_t qa = sbase + OFF_Q, da = sbase + OFF_DO;
+            auto issue_sdp = [&](int it) {
+                const int ks = (2 * it) % NSL, vs = (2 * it + 1) % NSL;
+                mbar_wait(&kv_full[ks], ((2 * it) / NSL) & 1);
+                mbar_wait(&kv_full[vs], ((2 * it + 1) / NSL) & 1);
                 tc_fence_after();
-                const uint32_t qa = sbase + OFF_Q + t * Q_BYTES, da = sbase + OFF_DO + t * Q_BYTES;
-                const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES, vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
+                const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES, vb = sbase + OFF_KV + vs * KV_BYTES;
+                const uint32_t d_s = tmem + (it & 1) * 128;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(tmem + t * 256, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), id_s, kk > 0);
+                    mma_bf16_ss(d_s, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), id_s, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(tmem + t * 256 + 64, kdesc_r(da, kk, 16384), kdesc_r(vb, kk, 8192), id_s, kk > 0);
-                mma_commit(&s_full[t]);
+                    mma_bf16_ss(d_s + 64, kdesc_r(da, kk, 16384), kdesc_r(vb, kk, 8192), id_s, kk > 0);
+                mma_commit(&s_full[it & 1]);
+                mma_commit(&kv_empty[vs]);  // V_j only feeds dP
             };
-            auto issue_dq = [&](int t, int j) {
-                mbar_wait(&ds_full[t], nq[t] & 1);
+            auto issue_dq = [&](int it) {
+                mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
                 tc_fence_after();
-                const uint32_t dsa = sbase + OFF_DS + t * DS_BYTES;
-                const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES;
+                const int ks = (2 * it) % NSL;
+                const uint32_t dsa = sbase + OFF_DS + (it & 1) * DS_BYTES;
+                const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ss(tmem + t * 256 + 128, kdesc_r(dsa, kk, 8192), mndesc_r(kb, kk, 8192), id_q,
-                                (nq[t] > 0 || kk > 0));
-                ++nq[t];
+                    mma_bf16_ss(tmem + 256, kdesc_r(dsa, kk, 8192), mndesc_r(kb, kk, 8192), id_q, (it > 0 || kk > 0));
+                mma_commit(&kv_empty[ks]);
             };
-            if (uses(0, jlo)) issue_sdp(0, jlo);
-            if (uses(1, jlo)) issue_sdp(1, jlo);
-            mma_commit(&kv_empty[slot(jlo, 1)]);  // V_jlo no longer needed
-            for (int j = jlo; j <= jhi; ++j) {
-                if (uses(0, j)) issue_dq(0, j);
-                if (j + 1 <= jhi && uses(0, j + 1)) issue_sdp(0, j + 1);
-                if (uses(1, j)) issue_dq(1, j);
-                mma_commit(&kv_empty[slot(j, 0)]);  // K_j done
-                if (j + 1 <= jhi) {
-                    if (uses(1, j + 1)) issue_sdp(1, j + 1);
-                    mma_commit(&kv_empty[slot(j + 1, 1)]);
-                }
+            issue_sdp(0);
+            if (nblk > 1) issue_sdp(1);
+            for (int it = 0; it < nblk; ++it) {
+                issue_dq(it);
+                if (it + 2 < nblk) issue_sdp(it + 2);
             }
-            mma_commit(&dq_done[0]);
-            mma_commit(&dq_done[1]);
+            mma_commit(dq_done);
         }
     } else {
-        const int t = warp >> 2, sub = warp & 3;
+        const int sub = warp & 3, half = warp >> 2;
         const int r = sub * 32 + lane;
-        const int64_t q = q0 + t * 128 + r;
+        const int64_t q = q0 + r;
         const int start = seg ? seg[q] : 0;
         const float nlse2 = -lse2v[(int64_t)h * s + q];  // -(lse * log2 e), precomputed
         const float Dq = Dv[(int64_t)h * s + q];
         const float sl2 = scale * LOG2E;
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
-        const uint32_t s_tm = tmem + lo + t * 256, dp_tm = s_tm + 64, dq_tm = s_tm + 128;
-        const uint32_t dsrow = sbase + OFF_DS + t * DS_BYTES + r * 128;
-        const int jb_t = t ? jb[1] : jb[0], je_t = t ? je[1] : je[0];
-        int n = 0;
-        for (int j = jb_t; j <= je_t; ++j, ++n) {
-            mbar_wait(&s_full[t], n & 1);
+        for (int it = 0; it < nblk; ++it) {
+            const int b = it & 1;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
-            uint32_t sv[2][32], dv[2][32];
-            tmem_ld32(s_tm, sv[0]);
-            tmem_ld32(s_tm + 32, sv[1]);
-            tmem_ld32(dp_tm, dv[0]);
-            tmem_ld32(dp_tm + 32, dv[1]);
+            uint32_t sv[32], dv[32];
+            tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
+            tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
             tmem_ld_wait();
-            const int64_t k0 = (int64_t)j * BKB;
-            const bool need_mask = seg != nullptr || (k0 + BKB - 1 > q0 + t * 128);
+            const int64_t k0 = (int64_t)(jb + it) * BKB + half * 32;
+            const bool need_mask = seg != nullptr || (k0 + 31 > q0);
+            const uint32_t dsrow = sbase + OFF_DS + b * DS_BYTES + r * 128;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < 4; ++k) {
                 float d8[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const int col = 8 * k + e;
-                    float p = ex2(fmaf(__uint_as_float(sv[col >> 5][col & 31]), sl2, nlse2));
+                    const int i = 8 * k + e;
+                    float p = ex2(fmaf(__uint_as_float(sv[i]), sl2, nlse2));
                     if (need_mask) {
-                        const int64_t key = k0 + col;
+                        const int64_t key = k0 + i;
                         if (key > q || key < start) p = 0.f;
                     }
-                    d8[e] = p * (__uint_as_float(dv[col >> 5][col & 31]) - Dq);
+                    d8[e] = p * (__uint_as_float(dv[i]) - Dq);
                 }
-                sts128(dsrow + ((k ^ (r & 7)) << 4), pack_bf16x2(d8[0], d8[1]), pack_bf16x2(d8[2], d8[3]),
+                const int chunk = half * 4 + k;
+                sts128(dsrow + ((chunk ^ (r & 7)) << 4), pack_bf16x2(d8[0], d8[1]), pack_bf16x2(d8[2], d8[3]),
                        pack_bf16x2(d8[4], d8[5]), pack_bf16x2(d8[6], d8[7]));
             }
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(&ds_full[t]);
+            mbar_arrive(&ds_full[b]);
         }
-        mbar_wait(&dq_done[t], 0);
+        mbar_wait(dq_done, 0);
         tc_fence_after();
-        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * D;
+        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * D + half * 64;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
             uint32_t v[32];
-            tmem_ld32(dq_tm + c * 32, v);
+            tmem_ld32(tmem + lo + 256 + half * 64 + c * 32, v);
             tmem_ld_wait();
             uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
@@ -537,8 +519,9 @@ constexpr int BQB = 64;
 constexpr int KB_BYTES = 128 * D * 2;              // K or V block, 32 KiB
 constexpr int QS_BYTES = BQB * D * 2;              // Q or dO tile, 16 KiB (two 8 KiB regions)
 constexpr int PT_BYTES = 128 * BQB * 2;            // P^T / dS^T, 16 KiB
-constexpr int OFF_K = 0, OFF_V = KB_BYTES, OFF_QS = 2 * KB_BYTES;  // 2 stages x (Q, dO)
-constexpr int OFF_PT = OFF_QS + 4 * QS_BYTES;                       // [2 bufs] x (P^T, dS^T)
+constexpr int NQS = 3;                                              // Q/dO ring stages
+constexpr int OFF_K = 0, OFF_V = KB_BYTES, OFF_QS = 2 * KB_BYTES;  // NQS stages x (Q, dO)
+constexpr int OFF_PT = OFF_QS + NQS * 2 * QS_BYTES;                 // [2 bufs] x (P^T, dS^T)
 constexpr int OFF_BAR = OFF_PT + 4 * PT_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dkv
@@ -552,12 +535,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     uint64_t* kv_full = bar;
-    uint64_t* qs_full = bar + 1;   // [2]
-    uint64_t* qs_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;    // [2]
-    uint64_t* pd_full = bar + 7;   // [2]
-    uint64_t* acc_done = bar + 9;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+    uint64_t* qs_full = bar + 1;          // [NQS]
+    uint64_t* qs_empty = qs_full + NQS;   // [NQS]
+    uint64_t* s_full = qs_empty + NQS;    // [2]
+    uint64_t* pd_full = s_full + 2;       // [2]
+    uint64_t* acc_done = pd_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
     const int warp = warp_id(), lane = lane_id();
     const int nkb = (int)(s / 128);
     const int kb = (int)blockIdx.x;  // small kb = most work: launched first
@@ -582,9 +565,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int total = nqb * grp;
     if (threadIdx.x == 0) {
         mbar_init(kv_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NQS; ++i) {
             mbar_init(&qs_full[i], 1);
             mbar_init(&qs_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&pd_full[i], 256);
         }
@@ -610,8 +595,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
             }
             for (int it = 0; it < total; ++it) {
-                const int st = it & 1;
-                mbar_wait(&qs_empty[st], ((it >> 1) & 1) ^ 1);
+                const int st = it % NQS;
+                mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES);
                 const int hh = it_head(it);
                 const int qq = (int)it_q0(it);
@@ -629,32 +614,32 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(kv_full, 0);
             const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V;
             auto issue_sdp = [&](int it) {
-                const int st = it & 1;
-                mbar_wait(&qs_full[st], (it >> 1) & 1);
+                const int st = it % NQS;
+                mbar_wait(&qs_full[st], (it / NQS) & 1);
                 tc_fence_after();
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
-                const uint32_t d_s = tmem + st * 128;
+                const uint32_t d_s = tmem + (it & 1) * 128;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     mma_bf16_ss(d_s, kdesc_r(ka, kk, 16384), kdesc_r(qb_, kk, 8192), id_s, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     mma_bf16_ss(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
-                mma_commit(&s_full[st]);
+                mma_commit(&s_full[it & 1]);
             };
             auto issue_acc = [&](int it) {
-                const int b = it & 1;
+                const int b = it & 1, st = it % NQS;
                 mbar_wait(&pd_full[b], (it >> 1) & 1);
                 tc_fence_after();
                 const uint32_t pt = sbase + OFF_PT + b * 2 * PT_BYTES, dst_ = pt + PT_BYTES;
-                const uint32_t qb_ = sbase + OFF_QS + b * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+                const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
                     mma_bf16_ss(tmem + 256, kdesc_r(pt, kk, 8192), mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
                     mma_bf16_ss(tmem + 384, kdesc_r(dst_, kk, 8192), mndesc_r(qb_, kk, 8192), id_a, (it > 0 || kk > 0));
-                mma_commit(&qs_empty[b]);
+                mma_commit(&qs_empty[st]);
             };
             if (total > 0) issue_sdp(0);
             if (total > 1) issue_sdp(1);
@@ -792,7 +777,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
-    fatc::dq_tc_kernel<<<dim3((unsigned)(s / 256), (unsigned)hq), fatc::THREADS, fatc::dq::SMEM, st>>>(
+    fatc::dq_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hq), fatc::THREADS, fatc::dq::SMEM, st>>>(
         t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dq_tc");
     SPT_CUDA(cudaGetLastError());
