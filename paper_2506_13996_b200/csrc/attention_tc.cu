@@ -1,15 +1,11 @@
-// tcgen05 / TMEM / TMA flash-attention forward for head_dim 128 (K3, Blackwell-native).
+// tcgen05 / TMEM / TMA flash attention for head_dim 128 (K3 forward, K4 backward), Blackwell-native.
 //
-// CTA = (pair of consecutive 128-row query tiles, q head); 10 warps:
-//   warps 0-3  softmax warpgroup for tile 0, warps 4-7 for tile 1 (thread = query row)
-//   warp 8     MMA issuer (one lane) + TMEM owner (512 columns: S0 | S1 | O0 | O1)
-//   warp 9     TMA producer: Q tiles once, then K_j / V_j through a 3-slot ring
-// Per 128-key block j and tile t:  S_t = Q_t K_j^T (TMEM) -> softmax warps read S_t, mask
-// (causal / block-causal runs), online max with lazy rescale (only when the running
-// max grows by > 2^8, then O_t is rescaled in TMEM), P_t (bf16) -> swizzled smem -> O_t += P_t V_j.
-// MMA order S0 S1 | PV0 S0' PV1 S1' | ... keeps one tile's softmax overlapped with the other tile's
-// MMAs.  tcgen05 ops complete in issue order, so the commit that signals S_t(j+1) also certifies
-// PV_t(j) is done (P_t buffer reusable, O_t stable for a rescale).
+// All kernels: 10 warps — 8 elementwise/softmax warps (thread = one TMEM lane = one matrix row),
+// warp 8 = MMA issuer (one lane) + TMEM owner, warp 9 = TMA producer.  Scores are computed by
+// tcgen05.mma into TMEM, read with tcgen05.ld, masked lazily (causal / block-causal runs,
+// SPEC.md:243-251), and the probabilities go back either into TMEM (forward: P aliases the consumed
+// score columns and is the A operand of the PV MMA) or into swizzled smem (backward).  Online softmax
+// uses a lazy rescale: O is only rescaled in TMEM when the running max grows by > 2^8.
 #include <algorithm>
 
 #include "common.h"
@@ -21,14 +17,6 @@ namespace fatc {
 
 constexpr int D = 128;
 constexpr int BQ = 128;   // rows per query tile
-constexpr int BK = 128;   // keys per block
-constexpr int TILE_BYTES = BQ * D * 2;  // 32 KiB (two 16 KiB SW128 column regions)
-constexpr int NSLOT = 3;
-constexpr int SMEM_Q = 0;
-constexpr int SMEM_P = 2 * TILE_BYTES;
-constexpr int SMEM_KV = 4 * TILE_BYTES;
-constexpr int SMEM_BAR = SMEM_KV + NSLOT * TILE_BYTES;
-constexpr int SMEM_BYTES = SMEM_BAR + 256 + 1024;
 constexpr int THREADS = 320;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -55,27 +43,45 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
 }
 
-// K-major SW128 descriptor over a [128 rows][128 cols] bf16 tile stored as two 16 KiB column regions.
-__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk) {
-    return make_sdesc_sw128(tile + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+// Generic SW128 descriptors for tiles made of 128 B-wide column regions `region` bytes apart.
+__device__ __forceinline__ uint64_t kdesc_r(uint32_t tile, int kk, uint32_t region) {
+    return make_sdesc_sw128(tile + (kk >> 2) * region + (kk & 3) * 32, 16, 1024);
 }
-// MN-major SW128 descriptor (rows = K, 64-wide MN blocks 16 KiB apart) advanced by kk*16 rows.
-__device__ __forceinline__ uint64_t mndesc(uint32_t tile, int kk) {
-    return make_sdesc_sw128(tile + kk * 2048, 16384, 1024);
+__device__ __forceinline__ uint64_t mndesc_r(uint32_t tile, int kk, uint32_t region) {
+    return make_sdesc_sw128(tile + kk * 2048, region, 1024);
 }
 
+// ------------------------------------------------------------------ forward
+// CTA = (pair of consecutive 128-row query tiles, q head).  64-key blocks.  TMEM (512 columns):
+//   tile t: S_t[0] | S_t[1] (64 columns each, double-buffered) | O_t (128)  at t*256.
+// P_t (bf16) is written into the consumed S_t[b] columns and fed to the PV MMA from TMEM.
+// MMA order per key block j: PV0(j) PV1(j) S0(j+2) S1(j+2): the score MMAs for block j+2 run while
+// the softmax of block j+1 executes, so softmax and tensor core overlap within a tile too.
+namespace fw {
+constexpr int BKB = 64;
+constexpr int Q_BYTES = BQ * D * 2;    // 32 KiB per tile
+constexpr int KV_BYTES = BKB * D * 2;  // 16 KiB per K or V block (two 8 KiB regions)
+constexpr int NSL = 10;
+constexpr int OFF_Q = 0, OFF_KV = 2 * Q_BYTES;
+constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
+constexpr int SMEM = OFF_BAR + 512 + 1024;
+}  // namespace fw
+
 __global__ void __launch_bounds__(THREADS, 1)
-    fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
-                  float scale_log2, bf16* __restrict__ o, float* __restrict__ lse) {
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
+                  int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
+                  float* __restrict__ lse) {
+    using namespace fw;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     uint64_t* q_full = bar;
     uint64_t* kv_full = bar + 1;
-    uint64_t* kv_empty = bar + 1 + NSLOT;
-    uint64_t* s_full = bar + 1 + 2 * NSLOT;  // [2]
-    uint64_t* p_full = s_full + 2;           // [2]
-    uint64_t* o_done = p_full + 2;           // [2]
+    uint64_t* kv_empty = kv_full + NSL;
+    uint64_t* s_full = kv_empty + NSL;  // [t*2 + b]
+    uint64_t* p_full = s_full + 4;      // [t*2 + b]  per buffer: the softmax may run 2 blocks ahead
+    uint64_t* pv_done = p_full + 4;     // [t]
+    uint64_t* o_done = pv_done + 2;     // [t]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
     const int warp = warp_id(), lane = lane_id();
@@ -84,24 +90,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int h = blockIdx.y;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)pair * 2 * BQ;
-    // key-block ranges per tile
-    int jb[2], je[2];
-    for (int t = 0; t < 2; ++t) {
-        const int64_t first = q0 + t * BQ;
-        je[t] = (int)((first + BQ - 1) / BK);
-        jb[t] = seg ? (int)(seg[first] / BK) : 0;
-    }
-    const int jlo = min(jb[0], jb[1]), jhi = max(je[0], je[1]);
+    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = seg ? (int)(seg[q0 + BQ] / BKB) : 0;
+    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = (int)((q0 + 2 * BQ - 1) / BKB);
+    const int jlo = jb0, jhi = je1;  // jb0 <= jb1 (starts are monotone), je0 < je1
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
-        for (int i = 0; i < NSLOT; ++i) {
+        for (int i = 0; i < NSL; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+        }
         for (int t = 0; t < 2; ++t) {
-            mbar_init(&s_full[t], 1);
-            mbar_init(&p_full[t], 128);
+            mbar_init(&pv_done[t], 1);
             mbar_init(&o_done[t], 1);
         }
         fence_barrier_init();
@@ -118,120 +122,143 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp == 9) {
         if (lane == 0) {
-            tma_prefetch_desc(&tm);
-            mbar_arrive_expect_tx(q_full, 2 * TILE_BYTES);
+            tma_prefetch_desc(&tq);
+            tma_prefetch_desc(&tkv);
+            mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
             for (int t = 0; t < 2; ++t)
                 for (int r = 0; r < 2; ++r)
-                    tma_load_2d(&tm, q_full, smem + SMEM_Q + t * TILE_BYTES + r * 16384, h * D + 64 * r,
+                    tma_load_2d(&tq, q_full, smem + OFF_Q + t * Q_BYTES + r * 16384, h * D + 64 * r,
                                 (int)(q0 + t * BQ));
-            int li = 0;
-            for (int j = jlo; j <= jhi; ++j) {
-                for (int w = 0; w < 2; ++w, ++li) {  // w=0: K_j, w=1: V_j
-                    const int slot = li % NSLOT;
-                    const uint32_t ph = (li / NSLOT) & 1;
-                    mbar_wait(&kv_empty[slot], ph ^ 1);
-                    mbar_arrive_expect_tx(&kv_full[slot], TILE_BYTES);
-                    const int col = (hq + (w ? hkv : 0) + kvh) * D;
-                    for (int r = 0; r < 2; ++r)
-                        tma_load_2d(&tm, &kv_full[slot], smem + SMEM_KV + slot * TILE_BYTES + r * 16384, col + 64 * r,
-                                    j * BK);
-                }
+            const int nload = 2 * (jhi - jlo + 1);
+            for (int li = 0; li < nload; ++li) {
+                const int j = jlo + li / 2, w = li & 1;
+                const int slot = li % NSL;
+                mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
+                const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r, j * BKB);
             }
         }
     } else if (warp == 8) {
         if (lane == 0) {
-            constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BK, false, false);
+            constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKB, false, false);
             constexpr uint32_t idesc_o = make_idesc_bf16(BQ, D, false, true);
             mbar_wait(q_full, 0);
+            const int jb[2] = {jb0, jb1}, je[2] = {je0, je1};
             int pv_count[2] = {0, 0};
             auto uses = [&](int t, int j) { return j >= jb[t] && j <= je[t]; };
-            auto slot_of = [&](int j, int w) { return (2 * (j - jlo) + w) % NSLOT; };
-            auto phase_of = [&](int j, int w) { return (uint32_t)(((2 * (j - jlo) + w) / NSLOT) & 1); };
+            auto slot = [&](int j, int w) { return (2 * (j - jlo) + w) % NSL; };
+            auto phase = [&](int j, int w) { return (uint32_t)(((2 * (j - jlo) + w) / NSL) & 1); };
             auto issue_s = [&](int t, int j) {
-                mbar_wait(&kv_full[slot_of(j, 0)], phase_of(j, 0));
+                mbar_wait(&kv_full[slot(j, 0)], phase(j, 0));
                 tc_fence_after();
-                const uint32_t qa = sbase + SMEM_Q + t * TILE_BYTES;
-                const uint32_t kb = sbase + SMEM_KV + slot_of(j, 0) * TILE_BYTES;
+                const int b = (j - jb[t]) & 1;
+                const uint32_t qa = sbase + OFF_Q + t * Q_BYTES;
+                const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) mma_bf16_ss(tmem + t * BK, kdesc(qa, kk), kdesc(kb, kk), idesc_s, kk > 0);
-                mma_commit(&s_full[t]);
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss(tmem + t * 256 + b * 64, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), idesc_s, kk > 0);
+                mma_commit(&s_full[t * 2 + b]);
             };
             auto issue_pv = [&](int t, int j) {
-                mbar_wait(&p_full[t], pv_count[t] & 1);
-                mbar_wait(&kv_full[slot_of(j, 1)], phase_of(j, 1));
+#ifdef SPT_WATCHDOG
+                {
+                    long long sp = 0;
+                    while (!mbar_try_wait(smem_u32(&p_full[t * 2 + ((j - jb[t]) & 1)]), ((j - jb[t]) >> 1) & 1)) {
+                        if (++sp == (1ll << 23)) {
+                            volatile int* dbg = reinterpret_cast<volatile int*>(tmem_slot + 4);
+                            printf("[fwd dbg] blk (%d,%d) waiting p_full[%d] j=%d; progress t0=(%d,%d) t1=(%d,%d)\n",
+                                   blockIdx.x, blockIdx.y, t, j, dbg[0], dbg[1], dbg[2], dbg[3]);
+                        }
+                    }
+                }
+#endif
+                mbar_wait(&p_full[t * 2 + ((j - jb[t]) & 1)], ((j - jb[t]) >> 1) & 1);
+                mbar_wait(&kv_full[slot(j, 1)], phase(j, 1));
                 tc_fence_after();
-                const uint32_t pa = sbase + SMEM_P + t * TILE_BYTES;
-                const uint32_t vb = sbase + SMEM_KV + slot_of(j, 1) * TILE_BYTES;
+                const int b = (j - jb[t]) & 1;
+                const uint32_t vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk)
-                    mma_bf16_ss(tmem + 256 + t * D, kdesc(pa, kk), mndesc(vb, kk), idesc_o, (pv_count[t] > 0 || kk > 0));
+                for (int kk = 0; kk < BKB / 16; ++kk)
+                    mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + b * 64 + kk * 8, mndesc_r(vb, kk, 8192), idesc_o,
+                                (pv_count[t] > 0 || kk > 0));
+                mma_commit(&pv_done[t]);
                 ++pv_count[t];
             };
-            if (uses(0, jlo)) issue_s(0, jlo);
-            if (uses(1, jlo)) issue_s(1, jlo);
-            mma_commit(&kv_empty[slot_of(jlo, 0)]);
+            // prologue: score MMAs for the first two blocks of each tile
+            for (int j = jlo; j <= min(jlo + 1, jhi); ++j) {
+                if (uses(0, j)) issue_s(0, j);
+                if (uses(1, j)) issue_s(1, j);
+                mma_commit(&kv_empty[slot(j, 0)]);  // K_j consumed by both tiles' S MMAs
+            }
             for (int j = jlo; j <= jhi; ++j) {
                 if (uses(0, j)) issue_pv(0, j);
-                if (j + 1 <= jhi && uses(0, j + 1)) issue_s(0, j + 1);
                 if (uses(1, j)) issue_pv(1, j);
-                mma_commit(&kv_empty[slot_of(j, 1)]);
-                if (j + 1 <= jhi) {
-                    if (uses(1, j + 1)) issue_s(1, j + 1);
-                    mma_commit(&kv_empty[slot_of(j + 1, 0)]);
+                mma_commit(&kv_empty[slot(j, 1)]);  // V_j consumed
+                if (j + 2 <= jhi) {
+                    if (uses(0, j + 2)) issue_s(0, j + 2);
+                    if (uses(1, j + 2)) issue_s(1, j + 2);
+                    mma_commit(&kv_empty[slot(j + 2, 0)]);
                 }
             }
             mma_commit(&o_done[0]);
             mma_commit(&o_done[1]);
         }
     } else {
-        // ---------------- softmax warpgroups
+        // ---------------- softmax warpgroups (thread = query row)
         const int t = warp >> 2;
         const int sub = warp & 3;
         const int r = sub * 32 + lane;
         const int64_t q = q0 + t * BQ + r;
         const int start = seg ? seg[q] : 0;
         const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
-        const uint32_t s_tm = tmem + lane_off + t * BK;
-        const uint32_t o_tm = tmem + lane_off + 256 + t * D;
-        const uint32_t prow = sbase + SMEM_P + t * TILE_BYTES + r * 128;
+        const uint32_t t_tm = tmem + lane_off + t * 256;
+        const uint32_t o_tm = t_tm + 128;
+        const int jb_t = t ? jb1 : jb0, je_t = t ? je1 : je0;
         float m_use = -INFINITY, l = 0.f;  // running max in log2 units (scaled)
-        int n = 0;
-        const int jb_t = t ? jb[1] : jb[0], je_t = t ? je[1] : je[0];
-        for (int j = jb_t; j <= je_t; ++j, ++n) {
-            mbar_wait(&s_full[t], n & 1);
+        for (int j = jb_t; j <= je_t; ++j) {
+            const int n = j - jb_t, b = n & 1;
+            const uint32_t s_tm = t_tm + b * 64;
+#ifdef SPT_WATCHDOG
+            volatile int* dbg = reinterpret_cast<volatile int*>(tmem_slot + 4);
+            if (r == 0) { dbg[2 * t] = j; dbg[2 * t + 1] = 1; }
+#endif
+            mbar_wait(&s_full[t * 2 + b], (n >> 1) & 1);
+#ifdef SPT_WATCHDOG
+            if (r == 0) dbg[2 * t + 1] = 2;
+#endif
             tc_fence_after();
-            const int64_t k0 = (int64_t)j * BK;
-            const bool need_mask = seg != nullptr || (k0 + BK - 1 > q0 + t * BQ);  // warp-uniform
-            // pass 1: row max of raw scores (scale > 0 commutes with max)
+            const int64_t k0 = (int64_t)j * BKB;
+            const bool need_mask = seg != nullptr || (k0 + BKB - 1 > q0 + t * BQ);  // warp-uniform
+            uint32_t v[2][32];
+            tmem_ld32(s_tm, v[0]);
+            tmem_ld32(s_tm + 32, v[1]);
+            tmem_ld_wait();
             float mraw = -INFINITY;
+            if (need_mask) {
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                uint32_t v[2][32];
-                tmem_ld32(s_tm + h2 * 64, v[0]);
-                tmem_ld32(s_tm + h2 * 64 + 32, v[1]);
-                tmem_ld_wait();
-                if (need_mask) {
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
+                    for (int i = 0; i < 32; ++i) {
+                        const int64_t key = k0 + c * 32 + i;
+                        if (key > q || key < start) v[c][i] = __float_as_uint(-INFINITY);
+                        mraw = fmaxf(mraw, __uint_as_float(v[c][i]));
+                    }
+            } else {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const int64_t key = k0 + h2 * 64 + c * 32 + i;
-                            const float x = (key > q || key < start) ? -INFINITY : __uint_as_float(v[c][i]);
-                            mraw = fmaxf(mraw, x);
-                        }
-                } else {
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(v[c][i]));
-                }
+                    for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(v[c][i]));
             }
             const float mx = mraw * scale_log2;
-            // lazy rescale; tcgen05.ld/st are warp-collective, so the O rescale runs warp-uniformly
+            // lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective); needs PV_t(j-1) complete
             const bool grow = mx > m_use + RESCALE_THRESHOLD;
             const bool resc = grow && m_use != -INFINITY && n > 0;
             const float alpha = resc ? ex2(m_use - mx) : 1.f;
             if (__any_sync(0xffffffffu, resc)) {
+                mbar_wait(&pv_done[t], (n - 1) & 1);
+                tc_fence_after();
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     uint32_t ov[32];
@@ -241,41 +268,31 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
                     tmem_st32(o_tm + c * 32, ov);
                 }
-                tmem_st_wait();
             }
             l *= alpha;
             if (grow) m_use = mx;
             const float nbase = m_use == -INFINITY ? 0.f : -m_use;
-            // pass 2: p = 2^(s*scale_log2 - m) -> bf16 -> swizzled smem (K-major SW128 A operand)
             float rs = 0.f;
+            uint32_t pw[32];
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                uint32_t v[2][32];
-                tmem_ld32(s_tm + h2 * 64, v[0]);
-                tmem_ld32(s_tm + h2 * 64 + 32, v[1]);
-                tmem_ld_wait();
-                const uint32_t reg = prow + h2 * 16384;  // keys [64*h2, 64*h2+64) -> column region h2
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    float p[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int col = 8 * k + e;
-                        p[e] = ex2(fmaf(__uint_as_float(v[col >> 5][col & 31]), scale_log2, nbase));
-                        if (need_mask) {
-                            const int64_t key = k0 + h2 * 64 + col;
-                            if (key > q || key < start) p[e] = 0.f;
-                        }
-                        rs += p[e];
-                    }
-                    sts128(reg + ((k ^ (r & 7)) << 4), pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]),
-                           pack_bf16x2(p[4], p[5]), pack_bf16x2(p[6], p[7]));
-                }
+            for (int k = 0; k < 32; ++k) {
+                const int c0 = 2 * k;
+                const float p0 = ex2(fmaf(__uint_as_float(v[c0 >> 5][c0 & 31]), scale_log2, nbase));
+                const float p1 = ex2(fmaf(__uint_as_float(v[c0 >> 5][(c0 + 1) & 31]), scale_log2, nbase));
+                rs += p0 + p1;
+                pw[k] = pack_bf16x2(p0, p1);
             }
             l += rs;
-            fence_proxy_async();
+#ifdef SPT_WATCHDOG
+            if (r == 0) dbg[2 * t + 1] = 3;
+#endif
+            tmem_st32(s_tm, pw);  // packed P over the consumed S columns [0, 32)
+            tmem_st_wait();
+#ifdef SPT_WATCHDOG
+            if (r == 0) dbg[2 * t + 1] = 4;
+#endif
             tc_fence_before();
-            mbar_arrive(&p_full[t]);
+            mbar_arrive(&p_full[t * 2 + b]);
         }
         // epilogue: O_t / l -> global, lse
         mbar_wait(&o_done[t], 0);
@@ -287,17 +304,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ov[32];
             tmem_ld32(o_tm + c * 32, ov);
             tmem_ld_wait();
-            float f[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(ov[i]) * inv;
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 uint4 w;
-                w.x = pack_bf16x2(f[8 * k + 0], f[8 * k + 1]);
-                w.y = pack_bf16x2(f[8 * k + 2], f[8 * k + 3]);
-                w.z = pack_bf16x2(f[8 * k + 4], f[8 * k + 5]);
-                w.w = pack_bf16x2(f[8 * k + 6], f[8 * k + 7]);
+                w.x = pack_bf16x2(__uint_as_float(ov[8 * k + 0]) * inv, __uint_as_float(ov[8 * k + 1]) * inv);
+                w.y = pack_bf16x2(__uint_as_float(ov[8 * k + 2]) * inv, __uint_as_float(ov[8 * k + 3]) * inv);
+                w.z = pack_bf16x2(__uint_as_float(ov[8 * k + 4]) * inv, __uint_as_float(ov[8 * k + 5]) * inv);
+                w.w = pack_bf16x2(__uint_as_float(ov[8 * k + 6]) * inv, __uint_as_float(ov[8 * k + 7]) * inv);
                 dst[k] = w;
             }
         }
@@ -306,20 +320,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 8) {
+        __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
 }
 
-
 // ===================================================================================== backward
-// Generic SW128 descriptors for tiles made of 128 B-wide column regions `region` bytes apart.
-__device__ __forceinline__ uint64_t kdesc_r(uint32_t tile, int kk, uint32_t region) {
-    return make_sdesc_sw128(tile + (kk >> 2) * region + (kk & 3) * 32, 16, 1024);
-}
-__device__ __forceinline__ uint64_t mndesc_r(uint32_t tile, int kk, uint32_t region) {
-    return make_sdesc_sw128(tile + kk * 2048, region, 1024);
-}
 
 // ------------------------------------------------------------------ dQ pass
 // CTA = (128-row q tile, q head).  Per 64-key block j (double-buffered in TMEM):
@@ -505,6 +512,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 8) {
+        __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -732,6 +740,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 8) {
+        __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -743,15 +752,16 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                  float* lse, cudaStream_t st) {
     if (d != fatc::D || s % 256 != 0) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
-    CUtensorMap tm = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
+    CUtensorMap tq = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
+    CUtensorMap tkv = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);
     auto k = fatc::fwd_tc_kernel;
     static bool attr = false;
     if (!attr) {
-        SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::SMEM_BYTES));
+        SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
         attr = true;
     }
     dim3 grid((unsigned)(s / 256), (unsigned)hq);
-    k<<<grid, fatc::THREADS, fatc::SMEM_BYTES, st>>>(tm, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse);
+    k<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse);
     count_launch("attn_fwd_tc");
     SPT_CUDA(cudaGetLastError());
     return true;

@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
+        __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace spt {
 
@@ -48,8 +49,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+#ifdef SPT_WATCHDOG
+    // debug builds: report and trap instead of hanging forever
+    long long spins = 0;
+    while (!mbar_try_wait(a, parity)) {
+        ++spins;
+        if (spins == (1ll << 24) && (threadIdx.x & 31) == 0)
+            printf("[spt watchdog] block (%d,%d) thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+                   blockIdx.y, threadIdx.x, a, parity);
+        if (spins == (1ll << 27)) __trap();
+    }
+#else
     while (!mbar_try_wait(a, parity)) {
     }
+#endif
 }
 
 // ------------------------------------------------------------------ TMA
