@@ -336,9 +336,8 @@ namespace dq {
 constexpr int BKB = 64;
 constexpr int Q_BYTES = 128 * D * 2;        // 32 KiB
 constexpr int KV_BYTES = BKB * D * 2;       // 16 KiB (two 8 KiB regions)
-constexpr int DS_BYTES = 128 * BKB * 2;     // 16 KiB (one region)
-constexpr int NSL = 6;
-constexpr int OFF_Q = 0, OFF_DO = Q_BYTES, OFF_DS = 2 * Q_BYTES, OFF_KV = OFF_DS + 2 * DS_BYTES;
+constexpr int NSL = 8;
+constexpr int OFF_Q = 0, OFF_DO = Q_BYTES, OFF_KV = 2 * Q_BYTES;  // dS lives in TMEM (A operand of dQ)
 constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dq
@@ -433,11 +432,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
                 tc_fence_after();
                 const int ks = (2 * it) % NSL;
-                const uint32_t dsa = sbase + OFF_DS + (it & 1) * DS_BYTES;
                 const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES;
+                // A = dS in TMEM: keys [32h, 32h+32) packed in S columns [32h, 32h+16) of buffer it&1
 #pragma unroll
                 for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ss(tmem + 256, kdesc_r(dsa, kk, 8192), mndesc_r(kb, kk, 8192), id_q, (it > 0 || kk > 0));
+                    mma_bf16_ts(tmem + 256, tmem + (it & 1) * 128 + (kk >> 1) * 32 + (kk & 1) * 8, mndesc_r(kb, kk, 8192),
+                                id_q, (it > 0 || kk > 0));
                 mma_commit(&kv_empty[ks]);
             };
             issue_sdp(0);
@@ -467,25 +467,24 @@ __global__ void __launch_bounds__(THREADS, 1)
             tmem_ld_wait();
             const int64_t k0 = (int64_t)(jb + it) * BKB + half * 32;
             const bool need_mask = seg != nullptr || (k0 + 31 > q0);
-            const uint32_t dsrow = sbase + OFF_DS + b * DS_BYTES + r * 128;
+            uint32_t w[16];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float d8[8];
+            for (int k = 0; k < 16; ++k) {
+                float d2[2];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int i = 8 * k + e;
+                for (int e = 0; e < 2; ++e) {
+                    const int i = 2 * k + e;
                     float p = ex2(fmaf(__uint_as_float(sv[i]), sl2, nlse2));
                     if (need_mask) {
                         const int64_t key = k0 + i;
                         if (key > q || key < start) p = 0.f;
                     }
-                    d8[e] = p * (__uint_as_float(dv[i]) - Dq);
+                    d2[e] = p * (__uint_as_float(dv[i]) - Dq);
                 }
-                const int chunk = half * 4 + k;
-                sts128(dsrow + ((chunk ^ (r & 7)) << 4), pack_bf16x2(d8[0], d8[1]), pack_bf16x2(d8[2], d8[3]),
-                       pack_bf16x2(d8[4], d8[5]), pack_bf16x2(d8[6], d8[7]));
+                w[k] = pack_bf16x2(d2[0], d2[1]);
             }
-            fence_proxy_async();
+            tmem_st16(tmem + lo + b * 128 + half * 32, w);  // over this warp's consumed S columns
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&ds_full[b]);
         }
@@ -526,11 +525,10 @@ namespace dkv {
 constexpr int BQB = 64;
 constexpr int KB_BYTES = 128 * D * 2;              // K or V block, 32 KiB
 constexpr int QS_BYTES = BQB * D * 2;              // Q or dO tile, 16 KiB (two 8 KiB regions)
-constexpr int PT_BYTES = 128 * BQB * 2;            // P^T / dS^T, 16 KiB
-constexpr int NQS = 3;                                              // Q/dO ring stages
+constexpr int NQS = 4;                                              // Q/dO ring stages
 constexpr int OFF_K = 0, OFF_V = KB_BYTES, OFF_QS = 2 * KB_BYTES;  // NQS stages x (Q, dO)
-constexpr int OFF_PT = OFF_QS + NQS * 2 * QS_BYTES;                 // [2 bufs] x (P^T, dS^T)
-constexpr int OFF_BAR = OFF_PT + 4 * PT_BYTES;
+constexpr int OFF_LD = OFF_QS + NQS * 2 * QS_BYTES;                 // NQS x (lse*log2e[64], D[64]) fp32
+constexpr int OFF_BAR = OFF_LD + NQS * 512;                         // P^T / dS^T live in TMEM
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dkv
 
@@ -605,7 +603,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int it = 0; it < total; ++it) {
                 const int st = it % NQS;
                 mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);
-                mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES);
+                mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES + 512);
                 const int hh = it_head(it);
                 const int qq = (int)it_q0(it);
                 uint8_t* base = smem + OFF_QS + st * 2 * QS_BYTES;
@@ -613,6 +611,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tma_load_2d(&tq, &qs_full[st], base + r * 8192, hh * D + 64 * r, qq);
                     tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hh * D + 64 * r, qq);
                 }
+                // per-column softmax statistics of this q block (lse*log2e, D) for the elementwise warps
+                bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hh * s + qq, 256, &qs_full[st]);
+                bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hh * s + qq, 256, &qs_full[st]);
             }
         }
     } else if (warp == 8) {
@@ -639,14 +640,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int b = it & 1, st = it % NQS;
                 mbar_wait(&pd_full[b], (it >> 1) & 1);
                 tc_fence_after();
-                const uint32_t pt = sbase + OFF_PT + b * 2 * PT_BYTES, dst_ = pt + PT_BYTES;
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+                // A operands from TMEM: warp half h packed P^T for q [32h, 32h+32) into S^T columns
+                // [32h, 32h+16) and dS^T into [32h+16, 32h+32) of buffer b
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ss(tmem + 256, kdesc_r(pt, kk, 8192), mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
+                    mma_bf16_ts(tmem + 256, tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8, mndesc_r(dob, kk, 8192), id_a,
+                                (it > 0 || kk > 0));
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ss(tmem + 384, kdesc_r(dst_, kk, 8192), mndesc_r(qb_, kk, 8192), id_a, (it > 0 || kk > 0));
+                    mma_bf16_ts(tmem + 384, tmem + b * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8, mndesc_r(qb_, kk, 8192),
+                                id_a, (it > 0 || kk > 0));
                 mma_commit(&qs_empty[st]);
             };
             if (total > 0) issue_sdp(0);
@@ -666,7 +670,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float sl2 = scale * LOG2E;
         for (int it = 0; it < total; ++it) {
             const int b = it & 1;
-            const int hh = it_head(it);
             const int64_t qq = it_q0(it) + half * 32;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
@@ -674,15 +677,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
             tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
             tmem_ld_wait();
-            const float4* l4 = reinterpret_cast<const float4*>(lse2v + (int64_t)hh * s + qq);
-            const float4* d4 = reinterpret_cast<const float4*>(Dv + (int64_t)hh * s + qq);
+            // the stage's statistics landed with Q/dO (s_full(it) follows the MMA's qs_full wait) and the
+            // stage is not recycled before acc(it) completes, which needs this warp's arrival
+            const float4* l4 = reinterpret_cast<const float4*>(smem + OFF_LD + (it % NQS) * 512 + half * 128);
+            const float4* d4 = reinterpret_cast<const float4*>(smem + OFF_LD + (it % NQS) * 512 + 256 + half * 128);
             const bool need_mask = seg != nullptr || qq < k0 + 127;
-            const uint32_t prow = sbase + OFF_PT + b * 2 * PT_BYTES + r * 128;
-            const uint32_t drow = prow + PT_BYTES;
+            uint32_t pw[16], sw[16];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float4 la = __ldg(l4 + 2 * k), lb = __ldg(l4 + 2 * k + 1);
-                const float4 da = __ldg(d4 + 2 * k), db = __ldg(d4 + 2 * k + 1);
+                const float4 la = l4[2 * k], lb = l4[2 * k + 1];
+                const float4 da = d4[2 * k], db = d4[2 * k + 1];
                 const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
                 const float dd[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
                 float p8[8], s8[8];
@@ -697,14 +701,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                     p8[e] = p;
                     s8[e] = p * (__uint_as_float(dv[i]) - dd[e]);
                 }
-                const int chunk = half * 4 + k;
-                const uint32_t off = (uint32_t)((chunk ^ (r & 7)) << 4);
-                sts128(prow + off, pack_bf16x2(p8[0], p8[1]), pack_bf16x2(p8[2], p8[3]), pack_bf16x2(p8[4], p8[5]),
-                       pack_bf16x2(p8[6], p8[7]));
-                sts128(drow + off, pack_bf16x2(s8[0], s8[1]), pack_bf16x2(s8[2], s8[3]), pack_bf16x2(s8[4], s8[5]),
-                       pack_bf16x2(s8[6], s8[7]));
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    pw[4 * k + e] = pack_bf16x2(p8[2 * e], p8[2 * e + 1]);
+                    sw[4 * k + e] = pack_bf16x2(s8[2 * e], s8[2 * e + 1]);
+                }
             }
-            fence_proxy_async();
+            tmem_st16(tmem + lo + b * 128 + half * 32, pw);
+            tmem_st16(tmem + lo + b * 128 + half * 32 + 16, sw);
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&pd_full[b]);
         }
