@@ -44,11 +44,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 
 // Generic SW128 descriptors for tiles made of 128 B-wide column regions `region` bytes apart.
+// The start-address field is the low 14 bits (16-byte units); smem offsets < 256 KiB never carry out,
+// so a K step is a plain add on a loop-invariant base descriptor (keeps the single MMA-issuing thread
+// at ~1 uniform op per tcgen05.mma — the N=64 score MMAs only last ~32 tensor cycles each).
 __device__ __forceinline__ uint64_t kdesc_r(uint32_t tile, int kk, uint32_t region) {
-    return make_sdesc_sw128(tile + (kk >> 2) * region + (kk & 3) * 32, 16, 1024);
+    return make_sdesc_sw128(tile, 16, 1024) + (uint64_t)(((kk >> 2) * region + (kk & 3) * 32) >> 4);
 }
 __device__ __forceinline__ uint64_t mndesc_r(uint32_t tile, int kk, uint32_t region) {
-    return make_sdesc_sw128(tile + kk * 2048, region, 1024);
+    return make_sdesc_sw128(tile, region, 1024) + (uint64_t)((kk * 2048) >> 4);
 }
 
 // ------------------------------------------------------------------ forward
@@ -337,6 +340,8 @@ constexpr int BKB = 64;
 constexpr int Q_BYTES = 128 * D * 2;        // 32 KiB
 constexpr int KV_BYTES = BKB * D * 2;       // 16 KiB (two 8 KiB regions)
 constexpr int NSL = 8;
+constexpr int NB = 3;          // S/dP TMEM buffers (128 columns each): the MMA runs NB-1 blocks ahead
+constexpr int DQ_COL = 384;    // dQ accumulator columns [384, 512)
 constexpr int OFF_Q = 0, OFF_DO = Q_BYTES, OFF_KV = 2 * Q_BYTES;  // dS lives in TMEM (A operand of dQ)
 constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
@@ -353,9 +358,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* q_full = bar;
     uint64_t* kv_full = bar + 1;
     uint64_t* kv_empty = kv_full + NSL;
-    uint64_t* s_full = kv_empty + NSL;  // [2]
-    uint64_t* ds_full = s_full + 2;      // [2]
-    uint64_t* dq_done = ds_full + 2;
+    uint64_t* s_full = kv_empty + NSL;  // [NB]
+    uint64_t* ds_full = s_full + NB;     // [NB]
+    uint64_t* dq_done = ds_full + NB;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
     const int warp = warp_id(), lane = lane_id();
     const int nqb = (int)(s / 128);
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < NB; ++t) {
             mbar_init(&s_full[t], 1);
             mbar_init(&ds_full[t], 256);
         }
@@ -418,33 +423,32 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&kv_full[vs], ((2 * it + 1) / NSL) & 1);
                 tc_fence_after();
                 const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES, vb = sbase + OFF_KV + vs * KV_BYTES;
-                const uint32_t d_s = tmem + (it & 1) * 128;
+                const uint32_t d_s = tmem + (it % NB) * 128;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     mma_bf16_ss(d_s, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), id_s, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     mma_bf16_ss(d_s + 64, kdesc_r(da, kk, 16384), kdesc_r(vb, kk, 8192), id_s, kk > 0);
-                mma_commit(&s_full[it & 1]);
+                mma_commit(&s_full[it % NB]);
                 mma_commit(&kv_empty[vs]);  // V_j only feeds dP
             };
             auto issue_dq = [&](int it) {
-                mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
+                mbar_wait(&ds_full[it % NB], (it / NB) & 1);
                 tc_fence_after();
                 const int ks = (2 * it) % NSL;
                 const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES;
-                // A = dS in TMEM: keys [32h, 32h+32) packed in S columns [32h, 32h+16) of buffer it&1
+                // A = dS in TMEM: keys [32h, 32h+32) packed in S columns [32h, 32h+16) of buffer it%NB
 #pragma unroll
                 for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ts(tmem + 256, tmem + (it & 1) * 128 + (kk >> 1) * 32 + (kk & 1) * 8, mndesc_r(kb, kk, 8192),
-                                id_q, (it > 0 || kk > 0));
+                    mma_bf16_ts(tmem + DQ_COL, tmem + (it % NB) * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
+                                mndesc_r(kb, kk, 8192), id_q, (it > 0 || kk > 0));
                 mma_commit(&kv_empty[ks]);
             };
-            issue_sdp(0);
-            if (nblk > 1) issue_sdp(1);
+            for (int it = 0; it < min(NB, nblk); ++it) issue_sdp(it);
             for (int it = 0; it < nblk; ++it) {
                 issue_dq(it);
-                if (it + 2 < nblk) issue_sdp(it + 2);
+                if (it + NB < nblk) issue_sdp(it + NB);
             }
             mma_commit(dq_done);
         }
@@ -458,8 +462,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float sl2 = scale * LOG2E;
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         for (int it = 0; it < nblk; ++it) {
-            const int b = it & 1;
-            mbar_wait(&s_full[b], (it >> 1) & 1);
+            const int b = it % NB;
+            mbar_wait(&s_full[b], (it / NB) & 1);
             tc_fence_after();
             uint32_t sv[32], dv[32];
             tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
             uint32_t v[32];
-            tmem_ld32(tmem + lo + 256 + half * 64 + c * 32, v);
+            tmem_ld32(tmem + lo + DQ_COL + half * 64 + c * 32, v);
             tmem_ld_wait();
             uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll

@@ -244,12 +244,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
                     const uint32_t b0 = a0 + Cfg::A_BYTES;
+                    const uint64_t ad0 = A_MN ? make_sdesc_sw128(a0, 8192, 1024) : make_sdesc_sw128(a0, 16, 1024);
+                    const uint64_t bd0 = B_MN ? make_sdesc_sw128(b0, 8192, 1024) : make_sdesc_sw128(b0, 16, 1024);
 #pragma unroll
                     for (int k = 0; k < GEMM_BK / 16; ++k) {
-                        const uint64_t ad = A_MN ? make_sdesc_sw128(a0 + k * 2048, 8192, 1024)
-                                                 : make_sdesc_sw128(a0 + k * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? make_sdesc_sw128(b0 + k * 2048, 8192, 1024)
-                                                 : make_sdesc_sw128(b0 + k * 32, 16, 1024);
+                        // K step of 16: +32 B (K-major) or +16 rows = 2048 B (MN-major), in 16-byte units
+                        const uint64_t ad = ad0 + (A_MN ? 128 : 2) * k;
+                        const uint64_t bd = bd0 + (B_MN ? 128 : 2) * k;
                         mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
                     mma_commit(&empty[stage]);
