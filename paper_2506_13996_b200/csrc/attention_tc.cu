@@ -677,6 +677,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t qq = it_q0(it) + half * 32;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
+#ifdef SPT_EXP_NO_ELEM
+            tc_fence_before();
+            mbar_arrive(&pd_full[b]);
+            continue;
+#endif
             uint32_t sv[32], dv[32];
             tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
             tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
