@@ -186,7 +186,9 @@ static void build_layer(spt_layer* Ly) {
     Ly->mlp_tile = (Ly->n_loc + mtiles - 1) / mtiles;  // SPEC.md:398 ceil(s/h) tiles
     if (c.loss_tile > 0) Ly->loss_tile = std::min<int64_t>(c.loss_tile, Ly->n_loc);
     else {
-        int64_t t = (int64_t)((2ll << 30) / (Ly->V * 4));  // tile_len * V * 4 <= 2 GiB
+        // tile_len * V * 4 <= 4 GiB (SPEC.md:423 budget).  8192 tokens at V=128256: the 4096 x 4096
+        // dx GEMM then has 2x the cluster tiles (no wave-quantisation tail) and dW is re-read half as often.
+        int64_t t = (int64_t)((4ll << 30) / (Ly->V * 4));
         t = std::max<int64_t>(128, t / 128 * 128);
         Ly->loss_tile = std::min<int64_t>(t, Ly->n_loc);
     }

@@ -1,4 +1,5 @@
 // Host side of the tcgen05 GEMM: TMA descriptor encoding, instantiation dispatch, C-ABI entry.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.h"
@@ -62,12 +63,69 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
     SPT_CUDA(cudaGetLastError());
 }
 
+template <int BN, bool A_MN, bool B_MN, int KIND>
+static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep,
+                         cudaStream_t st) {
+    auto kern = gemm_tc2_kernel<BN, A_MN, B_MN, KIND>;
+    constexpr int smem = Gemm2Cfg<BN>::SMEM_BYTES;
+    static bool attr_done = false;
+    if (!attr_done) {
+        SPT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_done = true;
+    }
+    const int ntiles = ((M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((N + BN - 1) / BN);
+    const int clusters = std::min(ntiles, num_sms() / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    prof_run(P_GEMM, 2.0 * M * N * K, 0, st, [&] {
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep));
+        count_launch("gemm2");
+    });
+}
+
+static bool use_pair_gemm() {
+    static const bool v = [] {
+        const char* e = getenv("SPT_GEMM_1SM");
+        return !(e && e[0] == '1');
+    }();
+    return v;
+}
+
 void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep,
           cudaStream_t st) {
     SPT_CHECK(M > 0 && N > 0 && K > 0, SPT_ERR_SHAPE, "gemm: empty problem");
     SPT_CHECK(N % 64 == 0, SPT_ERR_SHAPE, "gemm: N must be a multiple of 64, got " + std::to_string(N));
     SPT_CHECK(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), SPT_ERR_SHAPE, "gemm: dims exceed int32");
     constexpr int BN = 256;
+    if (M >= 2 * GEMM_BM && use_pair_gemm()) {
+        CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
+                                    : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
+        CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)
+                                    : make_tmap_bf16_2d(B.ptr, K, N, B.ld, GEMM_BK, BN / 2);
+        const int m = (int)M, n = (int)N, k = (int)K;
+        const int sel = (A.mn_major ? 2 : 0) + (B.mn_major ? 1 : 0);
+        switch (sel * 8 + kind) {
+            case 0 * 8 + EPI_BF16: launch_gemm2<BN, false, false, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
+            case 0 * 8 + EPI_F32: launch_gemm2<BN, false, false, EPI_F32>(ta, tb, m, n, k, ep, st); return;
+            case 0 * 8 + EPI_SWIGLU: launch_gemm2<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); return;
+            case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm2<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); return;
+            case 1 * 8 + EPI_BF16: launch_gemm2<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
+            case 1 * 8 + EPI_F32: launch_gemm2<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
+            case 3 * 8 + EPI_BF16: launch_gemm2<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
+            case 3 * 8 + EPI_F32: launch_gemm2<BN, true, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
+            default: SPT_THROW(SPT_ERR_INTERNAL, "gemm: unsupported major/epilogue combination");
+        }
+    }
     CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
                                 : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
     CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)

@@ -303,4 +303,188 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
 }
 
+// ----------------------------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2): cluster tile 256 x BN, each CTA holds
+// 128 rows of A and BN/2 rows of B per stage and receives 128 rows x BN of the accumulator in its
+// own TMEM.  Per SM this halves the B-operand smem traffic and TMA bytes per flop, and doubles the
+// prefetch distance of the same smem budget.  The leader (rank 0) issues all MMAs; both CTAs run
+// producer and epilogue roles.  Stage/accumulator release is multicast to both CTAs.
+template <int BN>
+struct Gemm2Cfg {
+    static constexpr int STAGES = 6;
+    static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;        // 16 KiB (this CTA's 128 rows)
+    static constexpr int B_BYTES = (BN / 2) * GEMM_BK * 2;       // this CTA's half of B
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN, int KIND>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, EpiParams ep) {
+    using Cfg = Gemm2Cfg<BN>;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int num_m = (M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);
+    const int num_n = (N + BN - 1) / BN;
+    const int ntiles = num_m * num_n;
+    const int nk = (K + GEMM_BK - 1) / GEMM_BK;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    constexpr int GROUP_M = 8;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 2) {
+        tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+        tmem_relinquish_pair();
+    }
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto tile_coords = [&](int t, int& mb, int& nb) {
+        const int per_group = GROUP_M * num_n;
+        const int gid = t / per_group;
+        const int first_m = gid * GROUP_M;
+        const int gsz = min(num_m - first_m, GROUP_M);
+        const int in = t % per_group;
+        mb = first_m + in % gsz;
+        nb = in / gsz;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cid; t < ntiles; t += ncl) {
+                int mb, nb;
+                tile_coords(t, mb, nb);
+                const int m0 = mb * 2 * GEMM_BM + rank * GEMM_BM;
+                const int n0 = nb * BN + rank * (BN / 2);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+                    uint8_t* sB = sA + Cfg::A_BYTES;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+                    if constexpr (!A_MN) {
+                        tma_load_2d_pair(&tmA, &full[stage], sA, kb * GEMM_BK, m0);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < GEMM_BM / 64; ++i)
+                            tma_load_2d_pair(&tmA, &full[stage], sA + i * 8192, m0 + i * 64, kb * GEMM_BK);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d_pair(&tmB, &full[stage], sB, kb * GEMM_BK, n0);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < BN / 128; ++i)
+                            tma_load_2d_pair(&tmB, &full[stage], sB + i * 8192, n0 + i * 64, kb * GEMM_BK);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = make_idesc_bf16(2 * GEMM_BM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cid; t < ntiles; t += ncl) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+                    const uint64_t ad0 = A_MN ? make_sdesc_sw128(a0, 8192, 1024) : make_sdesc_sw128(a0, 16, 1024);
+                    const uint64_t bd0 = B_MN ? make_sdesc_sw128(b0, 8192, 1024) : make_sdesc_sw128(b0, 16, 1024);
+#pragma unroll
+                    for (int k = 0; k < GEMM_BK / 16; ++k)
+                        mma_bf16_ss_pair(d_tmem, ad0 + (A_MN ? 128 : 2) * k, bd0 + (B_MN ? 128 : 2) * k, idesc,
+                                         (kb | k) != 0);
+                    mma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit_pair(&tfull[acc], 0x3);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int sub = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+        for (int t = cid; t < ntiles; t += ncl) {
+            int mb, nb;
+            tile_coords(t, mb, nb);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row = (int64_t)mb * 2 * GEMM_BM + rank * GEMM_BM + sub * 32 + lane;
+            const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 64) {
+                const int64_t col = (int64_t)nb * BN + c;
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tbase + c, r0);
+                tmem_ld32(tbase + c + 32, r1);
+                tmem_ld_wait();
+                if (row < M && col < N) epilogue_chunk<KIND>(ep, row, col, r0, r1);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // peer TMEM is written by the leader's MMAs: both CTAs done before dealloc
+    if (warp == 2) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
 }  // namespace spt
