@@ -194,12 +194,20 @@ def run_ours(args, rank, world, local_rank):
     n0 = S.kernel_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prof_acc = {}
+    sites_acc = {}
     with Clocks(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             eng.step_async(x, lab, None, on_host=False, stream=sp)
             t = eng.timing()  # syncs on the step's end event only after it is recorded: accumulate per step
+            for site, v in t["classes"].get("sites", {}).items():
+                a = sites_acc.setdefault(site, {"ms": 0.0, "calls": 0})
+                a["ms"] += v["ms"]
+                a["calls"] += v["calls"]
+                a["tflops"] = v["tflops"]
             for c, v in t["classes"].items():
+                if c == "sites":
+                    continue
                 a = prof_acc.setdefault(c, {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0})
                 for kk in a:
                     a[kk] += v[kk]
@@ -293,6 +301,8 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "roofline": roof,
         "breakdown_ms_per_step": breakdown, "class_tflops": tflops,
+        "gemm_sites": {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "tflops": round(v["tflops"], 1)}
+                       for k, v in sorted(sites_acc.items(), key=lambda kv: -kv[1]["ms"])},
         "clocks": clk.summary(),
         "cpu_baseline": cpu_v,
     }

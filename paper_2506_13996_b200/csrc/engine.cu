@@ -188,9 +188,10 @@ static void build_layer(spt_layer* Ly) {
     else {
         // tile_len * V * 4 <= 4 GiB (SPEC.md:423 budget).  8192 tokens at V=128256: the 4096 x 4096
         // dx GEMM then has 2x the cluster tiles (no wave-quantisation tail) and dW is re-read half as often.
-        int64_t t = (int64_t)((4ll << 30) / (Ly->V * 4));
-        t = std::max<int64_t>(128, t / 128 * 128);
-        Ly->loss_tile = std::min<int64_t>(t, Ly->n_loc);
+        const int64_t tmax = std::max<int64_t>(128, (int64_t)((4ll << 30) / (Ly->V * 4)) / 128 * 128);
+        const int64_t ntl = (Ly->n_loc + tmax - 1) / tmax;            // fewest tiles within the budget,
+        const int64_t t = ((Ly->n_loc + ntl - 1) / ntl + 127) / 128 * 128;  // split evenly
+        Ly->loss_tile = std::min<int64_t>(std::min(t, tmax), Ly->n_loc);
     }
     auto& L_ = Ly->led;
     const int64_t h = Ly->h, I = Ly->I, V = Ly->V;

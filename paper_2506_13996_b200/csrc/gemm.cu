@@ -103,11 +103,18 @@ static bool use_pair_gemm() {
 
 void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep,
           cudaStream_t st) {
+    if (Prof* pf = current_prof(); pf && pf->on) {
+        static const char* kn[] = {"bf16", "f32", "swiglu", "swiglu_bwd", "f32_stats"};
+        pf->next_tag = std::string(A.mn_major ? "MN" : "K") + (B.mn_major ? "MN" : "K") + "_" + kn[kind] + "_" +
+                       std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K);
+    }
     SPT_CHECK(M > 0 && N > 0 && K > 0, SPT_ERR_SHAPE, "gemm: empty problem");
     SPT_CHECK(N % 64 == 0, SPT_ERR_SHAPE, "gemm: N must be a multiple of 64, got " + std::to_string(N));
     SPT_CHECK(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), SPT_ERR_SHAPE, "gemm: dims exceed int32");
     constexpr int BN = 256;
-    if (M >= 2 * GEMM_BM && use_pair_gemm()) {
+    // CTA pairs win for K-major x K-major (forward / logits) GEMMs; with MN-major operands the 1-SM
+    // kernel measured faster inside the layer step (profiles/README.md, per-site breakdown).
+    if (M >= 2 * GEMM_BM && !A.mn_major && !B.mn_major && use_pair_gemm()) {
         CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
                                     : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
         CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)
@@ -119,6 +126,7 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
             case 0 * 8 + EPI_F32: launch_gemm2<BN, false, false, EPI_F32>(ta, tb, m, n, k, ep, st); return;
             case 0 * 8 + EPI_SWIGLU: launch_gemm2<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); return;
             case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm2<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); return;
+            case 0 * 8 + EPI_F32_STATS: launch_gemm2<BN, false, false, EPI_F32_STATS>(ta, tb, m, n, k, ep, st); return;
             case 1 * 8 + EPI_BF16: launch_gemm2<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
             case 1 * 8 + EPI_F32: launch_gemm2<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
             case 3 * 8 + EPI_BF16: launch_gemm2<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
@@ -137,6 +145,7 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
         case 0 * 8 + EPI_F32: launch_gemm<BN, false, false, EPI_F32>(ta, tb, m, n, k, ep, st); break;
         case 0 * 8 + EPI_SWIGLU: launch_gemm<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); break;
         case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); break;
+        case 0 * 8 + EPI_F32_STATS: launch_gemm<BN, false, false, EPI_F32_STATS>(ta, tb, m, n, k, ep, st); break;
         case 1 * 8 + EPI_BF16: launch_gemm<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); break;
         case 1 * 8 + EPI_F32: launch_gemm<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); break;
         case 3 * 8 + EPI_BF16: launch_gemm<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); break;

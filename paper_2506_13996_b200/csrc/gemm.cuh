@@ -24,6 +24,7 @@ enum EpiKind : int {
     EPI_F32 = 1,         // C(f32) = acc * alpha (+ C if accumulate)
     EPI_SWIGLU = 2,      // columns interleaved [g32|u32]...: C(bf16)[m, n/2] = silu(g) * u
     EPI_SWIGLU_BWD = 3,  // same interleave; aux = dA[m, n/2]; C = dGU (interleaved), C2 = A = silu(g)u
+    EPI_F32_STATS = 4,   // C(f32) = acc, plus per-(row, BN-column tile) softmax stats (max, sum exp(x-max))
 };
 
 struct EpiParams {
@@ -37,6 +38,8 @@ struct EpiParams {
     int64_t ldc2 = 0;
     int accumulate = 0;  // EPI_F32: C += acc
     float alpha = 1.f;
+    float* stats = nullptr;  // EPI_F32_STATS: [M][ld_stats] float2 (max, sumexp) per 256-column tile
+    int64_t ld_stats = 0;
 };
 
 constexpr int GEMM_BM = 128;
@@ -97,7 +100,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
             }
             store_bf16x32(reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col + 32 * h, v);
         }
-    } else if constexpr (KIND == EPI_F32) {
+    } else if constexpr (KIND == EPI_F32 || KIND == EPI_F32_STATS) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t* r = h ? r1 : r0;
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tc_fence_after();
             const int64_t row = (int64_t)mb * GEMM_BM + sub * 32 + lane;
             const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
+            float st_m = -INFINITY, st_s = 0.f;  // EPI_F32_STATS running (max, sum exp) over the tile row
 #pragma unroll 1
             for (int c = 0; c < BN; c += 64) {
                 const int64_t col = (int64_t)nb * BN + c;
@@ -284,7 +288,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld32(tbase + c, r0);
                 tmem_ld32(tbase + c + 32, r1);
                 tmem_ld_wait();
-                if (row < M && col < N) epilogue_chunk<KIND>(ep, row, col, r0, r1);
+                if (row < M && col < N) {
+                    epilogue_chunk<KIND>(ep, row, col, r0, r1);
+                    if constexpr (KIND == EPI_F32_STATS) {
+                        float mx = st_m;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[i]), __uint_as_float(r1[i])));
+                        float acc_s = st_s * __expf(st_m - mx);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            acc_s += __expf(__uint_as_float(r0[i]) - mx) + __expf(__uint_as_float(r1[i]) - mx);
+                        st_m = mx;
+                        st_s = acc_s;
+                    }
+                }
+            }
+            if constexpr (KIND == EPI_F32_STATS) {
+                if (row < M && (int64_t)nb * BN < N)
+                    reinterpret_cast<float2*>(ep.stats)[row * ep.ld_stats + nb] = make_float2(st_m, st_s);
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
@@ -459,6 +480,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tc_fence_after();
             const int64_t row = (int64_t)mb * 2 * GEMM_BM + rank * GEMM_BM + sub * 32 + lane;
             const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
+            float st_m = -INFINITY, st_s = 0.f;  // EPI_F32_STATS running (max, sum exp) over the tile row
 #pragma unroll 1
             for (int c = 0; c < BN; c += 64) {
                 const int64_t col = (int64_t)nb * BN + c;
@@ -466,7 +488,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld32(tbase + c, r0);
                 tmem_ld32(tbase + c + 32, r1);
                 tmem_ld_wait();
-                if (row < M && col < N) epilogue_chunk<KIND>(ep, row, col, r0, r1);
+                if (row < M && col < N) {
+                    epilogue_chunk<KIND>(ep, row, col, r0, r1);
+                    if constexpr (KIND == EPI_F32_STATS) {
+                        float mx = st_m;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[i]), __uint_as_float(r1[i])));
+                        float acc_s = st_s * __expf(st_m - mx);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            acc_s += __expf(__uint_as_float(r0[i]) - mx) + __expf(__uint_as_float(r1[i]) - mx);
+                        st_m = mx;
+                        st_s = acc_s;
+                    }
+                }
+            }
+            if constexpr (KIND == EPI_F32_STATS) {
+                if (row < M && (int64_t)nb * BN < N)
+                    reinterpret_cast<float2*>(ep.stats)[row * ep.ld_stats + nb] = make_float2(st_m, st_s);
             }
             tc_fence_before();
             __syncwarp();

@@ -349,6 +349,88 @@ __global__ void __launch_bounds__(512) ce_rows_kernel(const float* __restrict__ 
     }
 }
 
+// Variant fed by the logits GEMM's epilogue statistics: per (row, 256-column tile) (max, sum exp(x - max)).
+// The row's log-sum-exp is combined from ntile pairs, so the fp32 logits are read exactly once.
+__global__ void __launch_bounds__(512) ce_rows_stats_kernel(const float* __restrict__ logits,
+                                                            const float2* __restrict__ stats, int ntile,
+                                                            const int64_t* __restrict__ labels, int64_t V,
+                                                            const float* __restrict__ scale_dev,
+                                                            float* __restrict__ loss_rows, bf16* __restrict__ dlogits,
+                                                            int32_t* err) {
+    __shared__ float sm_m[32], sm_s[32];
+    __shared__ float sh_lse;
+    const int64_t r = blockIdx.x;
+    const float* row = logits + r * V;
+    const int64_t label = labels[r];
+    const bool valid = label != -100 && label >= 0 && label < V;
+    if (label != -100 && !valid && threadIdx.x == 0) *err = 1;
+    bf16* drow = dlogits + r * V;
+    const int64_t nv = V / 8;
+    if (!valid) {
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) reinterpret_cast<uint4*>(drow)[i] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x == 0) loss_rows[r] = 0.f;
+        return;
+    }
+    float m = -INFINITY, s = 0.f;
+    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+        const float2 p = stats[r * ntile + i];
+        const float nm = fmaxf(m, p.x);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (p.x == -INFINITY ? 0.f : p.y * __expf(p.x - nm));
+        m = nm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+        const float nm = fmaxf(m, om);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sm_m[w] = m;
+        sm_s[w] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY, S = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            const float nm = fmaxf(M, sm_m[i]);
+            S = (M == -INFINITY ? 0.f : S * __expf(M - nm)) + (sm_m[i] == -INFINITY ? 0.f : sm_s[i] * __expf(sm_m[i] - nm));
+            M = nm;
+        }
+        const float lse = M + __logf(S);
+        sh_lse = lse;
+        loss_rows[r] = lse - row[label];
+    }
+    __syncthreads();
+    const float lse = sh_lse;
+    const float scale = *scale_dev;
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(row) + 2 * i);
+        const float4 b = __ldcs(reinterpret_cast<const float4*>(row) + 2 * i + 1);
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = __expf(v[k] - lse);
+            if (8 * i + k == label) v[k] -= 1.f;
+            v[k] *= scale;
+        }
+        store8(drow + 8 * i, v);
+    }
+}
+
+void ce_rows_stats(const float* logits, const float* stats, int ntile, const int64_t* labels, int64_t rows, int64_t V,
+                   const float* scale_dev, float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st) {
+    SPT_CHECK(V % 8 == 0, SPT_ERR_SHAPE, "vocab must be a multiple of 8");
+    if (rows == 0) return;
+    prof_run(P_CE, 0, 4.0 * rows * V + 2.0 * rows * V, st, [&] {
+        ce_rows_stats_kernel<<<(unsigned)rows, 512, 0, st>>>(logits, (const float2*)stats, ntile, labels, V, scale_dev,
+                                                             loss_rows, (bf16*)dlogits, err);
+        count_launch("ce_rows_stats");
+    });
+    SPT_CUDA(cudaGetLastError());
+}
+
 void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V, const float* scale_dev,
              float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st) {
     SPT_CHECK(V % 8 == 0, SPT_ERR_SHAPE, "vocab must be a multiple of 8");

@@ -41,6 +41,9 @@ void segment_starts(const int64_t* pos, int64_t n, int32_t* starts, int32_t* err
 // Row-wise CE over fp32 logits [rows, V]: loss_rows[r] (0 if ignored), dlogits bf16 = (softmax-onehot)*scale.
 void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V, const float* scale_dev,
              float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st);
+// Same, from per-(row, 256-column tile) (max, sumexp) stats written by the logits GEMM epilogue.
+void ce_rows_stats(const float* logits, const float* stats, int ntile, const int64_t* labels, int64_t rows, int64_t V,
+                   const float* scale_dev, float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st);
 // Deterministic fixed-order sum of n fp32 values into an fp64 accumulator.
 void sum_rows(const float* v, int64_t n, double* accum, cudaStream_t st);
 // loss = loss_sum / count (device scalars) and scale = 1/count.

@@ -20,7 +20,9 @@ struct Prof {
         cudaEvent_t a, b;
         double flops, bytes;
         int64_t launches;
+        std::string tag;  // optional finer key (e.g. GEMM shape/epilogue) for the per-site breakdown
     };
+    std::string next_tag;
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
@@ -52,7 +54,8 @@ struct Prof {
         SPT_CUDA(cudaEventRecord(a, st));
         f();
         SPT_CUDA(cudaEventRecord(b, st));
-        recs.push_back({cls, a, b, flops, bytes, launch_count() - n0});
+        recs.push_back({cls, a, b, flops, bytes, launch_count() - n0, next_tag});
+        next_tag.clear();
     }
     std::string json() {
         double ms[NCLS] = {}, fl[NCLS] = {}, by[NCLS] = {};
@@ -67,7 +70,31 @@ struct Prof {
             cnt[r.cls] += (int)r.launches;
         }
         std::ostringstream os;
-        os << "{";
+        // per-tag breakdown (GEMM call sites)
+        std::vector<std::string> tags;
+        std::vector<double> tms, tfl;
+        std::vector<int> tn;
+        for (auto& r : recs) {
+            if (r.tag.empty()) continue;
+            float t = 0;
+            SPT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            size_t i = 0;
+            while (i < tags.size() && tags[i] != r.tag) ++i;
+            if (i == tags.size()) {
+                tags.push_back(r.tag);
+                tms.push_back(0);
+                tfl.push_back(0);
+                tn.push_back(0);
+            }
+            tms[i] += t;
+            tfl[i] += r.flops;
+            tn[i] += 1;
+        }
+        os << "{\"sites\":{";
+        for (size_t i = 0; i < tags.size(); ++i)
+            os << (i ? "," : "") << "\"" << tags[i] << "\":{\"ms\":" << tms[i] << ",\"calls\":" << tn[i]
+               << ",\"tflops\":" << (tms[i] > 0 ? tfl[i] / (tms[i] * 1e9) : 0) << "}";
+        os << "},";
         for (int c = 0; c < NCLS; ++c)
             os << (c ? "," : "") << "\"" << name(c) << "\":{\"ms\":" << ms[c] << ",\"launches\":" << cnt[c]
                << ",\"flops\":" << fl[c] << ",\"bytes\":" << by[c] << "}";

@@ -11,8 +11,11 @@ namespace spt {
 static inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // ---------------------------------------------------------------- K5: fused logits + CE
+static int64_t flce_ntile(int64_t V) { return (V + 255) / 256; }
+
 size_t flce_workspace(int64_t tile_n, int64_t V) {
-    return align256((size_t)tile_n * V * 4) + align256((size_t)tile_n * V * 2) + align256((size_t)tile_n * 4);
+    return align256((size_t)tile_n * V * 4) + align256((size_t)tile_n * V * 2) + align256((size_t)tile_n * 4) +
+           align256((size_t)tile_n * flce_ntile(V) * 8);
 }
 
 // Per tile t (ascending): logits_t = x_t W^T (fp32, never more than [tile_n, V] live — SPEC.md:408),
@@ -29,14 +32,21 @@ void flce(const void* x, const void* w, const int64_t* labels, int64_t n, int64_
     bf16* dlog = (bf16*)p;
     p += align256((size_t)tile_n * V * 2);
     float* loss_rows = (float*)p;
+    p += align256((size_t)tile_n * 4);
+    float* stats = (float*)p;
+    const int64_t ntile = flce_ntile(V);
     const bf16* xb = (const bf16*)x;
     for (int64_t a = 0, t = 0; a < n; a += tile_n, ++t) {
         const int64_t rows = std::min(tile_n, n - a);
+        // logits + per-(row, 256-col tile) softmax stats from the GEMM epilogue: the CE pass reads the
+        // fp32 logits once (SPEC.md:69 cross_entropy on the tile, never an [s, V] tensor — :408)
         EpiParams e1;
         e1.C = logits;
         e1.ldc = V;
-        gemm({xb + a * h, h, false}, {w, h, false}, rows, V, h, EPI_F32, e1, st);
-        ce_rows(logits, labels + a, rows, V, scale_dev, loss_rows, dlog, err, st);
+        e1.stats = stats;
+        e1.ld_stats = ntile;
+        gemm({xb + a * h, h, false}, {w, h, false}, rows, V, h, EPI_F32_STATS, e1, st);
+        ce_rows_stats(logits, stats, (int)ntile, labels + a, rows, V, scale_dev, loss_rows, dlog, err, st);
         sum_rows(loss_rows, rows, loss_sum_accum, st);
         EpiParams e2;
         e2.C = (bf16*)dx + a * h;
