@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 8) {
-        if (lane == 0) {
+        {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
             constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKB, false, false);
             constexpr uint32_t idesc_o = make_idesc_bf16(BQ, D, false, true);
             mbar_wait(q_full, 0);
@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(tmem + t * 256 + b * 64, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), idesc_s, kk > 0);
-                mma_commit(&s_full[t * 2 + b]);
+                    mma_bf16_ss_w(tmem + t * 256 + b * 64, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), idesc_s, kk > 0);
+                mma_commit_w(&s_full[t * 2 + b]);
             };
             auto issue_pv = [&](int t, int j) {
 #ifdef SPT_WATCHDOG
@@ -184,29 +184,29 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + b * 64 + kk * 8, mndesc_r(vb, kk, 8192), idesc_o,
+                    mma_bf16_ts_w(tmem + t * 256 + 128, tmem + t * 256 + b * 64 + kk * 8, mndesc_r(vb, kk, 8192), idesc_o,
                                 (pv_count[t] > 0 || kk > 0));
-                mma_commit(&pv_done[t]);
+                mma_commit_w(&pv_done[t]);
                 ++pv_count[t];
             };
             // prologue: score MMAs for the first two blocks of each tile
             for (int j = jlo; j <= min(jlo + 1, jhi); ++j) {
                 if (uses(0, j)) issue_s(0, j);
                 if (uses(1, j)) issue_s(1, j);
-                mma_commit(&kv_empty[slot(j, 0)]);  // K_j consumed by both tiles' S MMAs
+                mma_commit_w(&kv_empty[slot(j, 0)]);  // K_j consumed by both tiles' S MMAs
             }
             for (int j = jlo; j <= jhi; ++j) {
                 if (uses(0, j)) issue_pv(0, j);
                 if (uses(1, j)) issue_pv(1, j);
-                mma_commit(&kv_empty[slot(j, 1)]);  // V_j consumed
+                mma_commit_w(&kv_empty[slot(j, 1)]);  // V_j consumed
                 if (j + 2 <= jhi) {
                     if (uses(0, j + 2)) issue_s(0, j + 2);
                     if (uses(1, j + 2)) issue_s(1, j + 2);
-                    mma_commit(&kv_empty[slot(j + 2, 0)]);
+                    mma_commit_w(&kv_empty[slot(j + 2, 0)]);
                 }
             }
-            mma_commit(&o_done[0]);
-            mma_commit(&o_done[1]);
+            mma_commit_w(&o_done[0]);
+            mma_commit_w(&o_done[1]);
         }
     } else {
         // ---------------- softmax warpgroups (thread = query row)
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 8) {
-        if (lane == 0) {
+        {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
             constexpr uint32_t id_s = make_idesc_bf16(128, BKB, false, false);
             constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);
             mbar_wait(q_full, 0);
@@ -426,12 +426,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t d_s = tmem + (it % NB) * 128;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(d_s, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), id_s, kk > 0);
+                    mma_bf16_ss_w(d_s, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 8192), id_s, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(d_s + 64, kdesc_r(da, kk, 16384), kdesc_r(vb, kk, 8192), id_s, kk > 0);
-                mma_commit(&s_full[it % NB]);
-                mma_commit(&kv_empty[vs]);  // V_j only feeds dP
+                    mma_bf16_ss_w(d_s + 64, kdesc_r(da, kk, 16384), kdesc_r(vb, kk, 8192), id_s, kk > 0);
+                mma_commit_w(&s_full[it % NB]);
+                mma_commit_w(&kv_empty[vs]);  // V_j only feeds dP
             };
             auto issue_dq = [&](int it) {
                 mbar_wait(&ds_full[it % NB], (it / NB) & 1);
@@ -441,16 +441,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // A = dS in TMEM: keys [32h, 32h+32) packed in S columns [32h, 32h+16) of buffer it%NB
 #pragma unroll
                 for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ts(tmem + DQ_COL, tmem + (it % NB) * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
+                    mma_bf16_ts_w(tmem + DQ_COL, tmem + (it % NB) * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
                                 mndesc_r(kb, kk, 8192), id_q, (it > 0 || kk > 0));
-                mma_commit(&kv_empty[ks]);
+                mma_commit_w(&kv_empty[ks]);
             };
             for (int it = 0; it < min(NB, nblk); ++it) issue_sdp(it);
             for (int it = 0; it < nblk; ++it) {
                 issue_dq(it);
                 if (it + NB < nblk) issue_sdp(it + NB);
             }
-            mma_commit(dq_done);
+            mma_commit_w(dq_done);
         }
     } else {
         const int sub = warp & 3, half = warp >> 2;
@@ -465,6 +465,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int b = it % NB;
             mbar_wait(&s_full[b], (it / NB) & 1);
             tc_fence_after();
+#ifdef SPT_EXP_NO_ELEM
+            tc_fence_before();
+            mbar_arrive(&ds_full[b]);
+            continue;
+#endif
             uint32_t sv[32], dv[32];
             tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
             tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
@@ -621,7 +626,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 8) {
-        if (lane == 0) {
+        {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
             constexpr uint32_t id_s = make_idesc_bf16(128, BQB, false, false);
             constexpr uint32_t id_a = make_idesc_bf16(128, D, false, true);
             mbar_wait(kv_full, 0);
@@ -634,11 +639,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t d_s = tmem + (it & 1) * 128;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(d_s, kdesc_r(ka, kk, 16384), kdesc_r(qb_, kk, 8192), id_s, kk > 0);
+                    mma_bf16_ss_w(d_s, kdesc_r(ka, kk, 16384), kdesc_r(qb_, kk, 8192), id_s, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
-                mma_commit(&s_full[it & 1]);
+                    mma_bf16_ss_w(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
+                mma_commit_w(&s_full[it & 1]);
             };
             auto issue_acc = [&](int it) {
                 const int b = it & 1, st = it % NQS;
@@ -649,13 +654,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // [32h, 32h+16) and dS^T into [32h+16, 32h+32) of buffer b
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ts(tmem + 256, tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8, mndesc_r(dob, kk, 8192), id_a,
+                    mma_bf16_ts_w(tmem + 256, tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8, mndesc_r(dob, kk, 8192), id_a,
                                 (it > 0 || kk > 0));
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ts(tmem + 384, tmem + b * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8, mndesc_r(qb_, kk, 8192),
+                    mma_bf16_ts_w(tmem + 384, tmem + b * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8, mndesc_r(qb_, kk, 8192),
                                 id_a, (it > 0 || kk > 0));
-                mma_commit(&qs_empty[st]);
+                mma_commit_w(&qs_empty[st]);
             };
             if (total > 0) issue_sdp(0);
             if (total > 1) issue_sdp(1);
@@ -663,7 +668,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 issue_acc(it);
                 if (it + 2 < total) issue_sdp(it + 2);
             }
-            mma_commit(acc_done);
+            mma_commit_w(acc_done);
         }
     } else {
         // elementwise: warp w: TMEM lanes (w&3)*32.., columns half (w>>2)*32 of the 64 q columns
