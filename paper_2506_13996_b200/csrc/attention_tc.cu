@@ -28,6 +28,10 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+__device__ __forceinline__ void lds128(uint32_t addr, float& a, float& b, float& c, float& d) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
+}
+
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -42,6 +46,18 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+// Backward kernels: 16 elementwise warps (4 per TMEM lane quarter, 16 of the 64 block columns each),
+// warp 16 = MMA issuer / TMEM owner, warp 17 = TMA producer.
+constexpr int BW_NEW = 16;
+constexpr int BW_THREADS = (BW_NEW + 2) * 32;
+constexpr int BW_MMA = BW_NEW, BW_TMA = BW_NEW + 1;
 
 // Generic SW128 descriptors for tiles made of 128 B-wide column regions `region` bytes apart.
 // The start-address field is the low 14 bits (16-byte units); smem offsets < 256 KiB never carry out,
@@ -347,7 +363,7 @@ constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dq
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(BW_THREADS, 1)
     dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                  const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
                  const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
@@ -379,12 +395,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int t = 0; t < NB; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&ds_full[t], 256);
+            mbar_init(&ds_full[t], BW_NEW * 32);
         }
         mbar_init(dq_done, 1);
         fence_barrier_init();
     }
-    if (warp == 8) {
+    if (warp == BW_MMA) {
         tmem_alloc(tmem_slot, 512);
         tmem_relinquish();
     }
@@ -393,7 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t sbase = smem_u32(smem);
-    if (warp == 9) {
+    if (warp == BW_TMA) {
         if (lane == 0) {
             mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
             for (int r = 0; r < 2; ++r) {
@@ -411,7 +427,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 j * BKB);
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == BW_MMA) {
         {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
             constexpr uint32_t id_s = make_idesc_bf16(128, BKB, false, false);
             constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);
@@ -438,11 +454,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_fence_after();
                 const int ks = (2 * it) % NSL;
                 const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES;
-                // A = dS in TMEM: keys [32h, 32h+32) packed in S columns [32h, 32h+16) of buffer it%NB
+                // A = dS in TMEM: keys [16g, 16g+16) packed in S columns [16g, 16g+8) of buffer it%NB
 #pragma unroll
                 for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ts_w(tmem + DQ_COL, tmem + (it % NB) * 128 + (kk >> 1) * 32 + (kk & 1) * 8,
-                                mndesc_r(kb, kk, 8192), id_q, (it > 0 || kk > 0));
+                    mma_bf16_ts_w(tmem + DQ_COL, tmem + (it % NB) * 128 + kk * 16, mndesc_r(kb, kk, 8192), id_q,
+                                  (it > 0 || kk > 0));
                 mma_commit_w(&kv_empty[ks]);
             };
             for (int it = 0; it < min(NB, nblk); ++it) issue_sdp(it);
@@ -453,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mma_commit_w(dq_done);
         }
     } else {
-        const int sub = warp & 3, half = warp >> 2;
+        const int sub = warp & 3, grp = warp >> 2;  // lanes [32 sub, +32), keys [16 grp, +16) of each block
         const int r = sub * 32 + lane;
         const int64_t q = q0 + r;
         const int start = seg ? seg[q] : 0;
@@ -470,15 +486,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_arrive(&ds_full[b]);
             continue;
 #endif
-            uint32_t sv[32], dv[32];
-            tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
-            tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
+            uint32_t sv[16], dv[16];
+            tmem_ld16(tmem + lo + b * 128 + grp * 16, sv);
+            tmem_ld16(tmem + lo + b * 128 + 64 + grp * 16, dv);
             tmem_ld_wait();
-            const int64_t k0 = (int64_t)(jb + it) * BKB + half * 32;
-            const bool need_mask = seg != nullptr || (k0 + 31 > q0);
-            uint32_t w[16];
+            const int64_t k0 = (int64_t)(jb + it) * BKB + grp * 16;
+            const bool need_mask = seg != nullptr || (k0 + 15 > q0);
+            uint32_t w[8];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < 8; ++k) {
                 float d2[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
@@ -492,20 +508,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 w[k] = pack_bf16x2(d2[0], d2[1]);
             }
-            tmem_st16(tmem + lo + b * 128 + half * 32, w);  // over this warp's consumed S columns
+            tmem_st8(tmem + lo + b * 128 + grp * 16, w);  // over this warp's consumed S columns
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&ds_full[b]);
         }
         mbar_wait(dq_done, 0);
         tc_fence_after();
-        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * D + half * 64;
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
+        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * D + grp * 32;
+        {
             uint32_t v[32];
-            tmem_ld32(tmem + lo + DQ_COL + half * 64 + c * 32, v);
+            tmem_ld32(tmem + lo + DQ_COL + grp * 32, v);
             tmem_ld_wait();
-            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 uint4 w;
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == BW_MMA) {
         __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -541,7 +556,7 @@ constexpr int OFF_BAR = OFF_LD + NQS * 512;                         // P^T / dS^
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dkv
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(BW_THREADS, 1)
     dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                    const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
                    const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
@@ -586,12 +601,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&pd_full[i], 256);
+            mbar_init(&pd_full[i], BW_NEW * 32);
         }
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
-    if (warp == 8) {
+    if (warp == BW_MMA) {
         tmem_alloc(tmem_slot, 512);
         tmem_relinquish();
     }
@@ -602,7 +617,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t sbase = smem_u32(smem);
     auto it_head = [&](int it) { return kvh * grp + it / nqb; };
     auto it_q0 = [&](int it) { return (int64_t)(qb_first + it % nqb) * BQB; };
-    if (warp == 9) {
+    if (warp == BW_TMA) {
         if (lane == 0) {
             mbar_arrive_expect_tx(kv_full, 2 * KB_BYTES);
             for (int r = 0; r < 2; ++r) {
@@ -625,7 +640,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hh * s + qq, 256, &qs_full[st]);
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == BW_MMA) {
         {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
             constexpr uint32_t id_s = make_idesc_bf16(128, BQB, false, false);
             constexpr uint32_t id_a = make_idesc_bf16(128, D, false, true);
@@ -650,16 +665,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&pd_full[b], (it >> 1) & 1);
                 tc_fence_after();
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
-                // A operands from TMEM: warp half h packed P^T for q [32h, 32h+32) into S^T columns
-                // [32h, 32h+16) and dS^T into [32h+16, 32h+32) of buffer b
+                // A operands from TMEM: column group g packed P^T for q [16g, 16g+16) into S^T columns
+                // [16g, 16g+8) and dS^T into [16g+8, 16g+16) of buffer b
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ts_w(tmem + 256, tmem + b * 128 + (kk >> 1) * 32 + (kk & 1) * 8, mndesc_r(dob, kk, 8192), id_a,
-                                (it > 0 || kk > 0));
+                    mma_bf16_ts_w(tmem + 256, tmem + b * 128 + kk * 16, mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ts_w(tmem + 384, tmem + b * 128 + (kk >> 1) * 32 + 16 + (kk & 1) * 8, mndesc_r(qb_, kk, 8192),
-                                id_a, (it > 0 || kk > 0));
+                    mma_bf16_ts_w(tmem + 384, tmem + b * 128 + kk * 16 + 8, mndesc_r(qb_, kk, 8192), id_a,
+                                  (it > 0 || kk > 0));
                 mma_commit_w(&qs_empty[st]);
             };
             if (total > 0) issue_sdp(0);
@@ -671,15 +685,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             mma_commit_w(acc_done);
         }
     } else {
-        // elementwise: warp w: TMEM lanes (w&3)*32.., columns half (w>>2)*32 of the 64 q columns
-        const int sub = warp & 3, half = warp >> 2;
+        // elementwise: warp w: TMEM lanes (w&3)*32.., q columns [16g, 16g+16) with g = w>>2
+        const int sub = warp & 3, grp = warp >> 2;
         const int r = sub * 32 + lane;  // key row
         const int64_t key = k0 + r;
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         const float sl2 = scale * LOG2E;
         for (int it = 0; it < total; ++it) {
             const int b = it & 1;
-            const int64_t qq = it_q0(it) + half * 32;
+            const int64_t qq = it_q0(it) + grp * 16;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
 #ifdef SPT_EXP_NO_ELEM
@@ -687,22 +701,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_arrive(&pd_full[b]);
             continue;
 #endif
-            uint32_t sv[32], dv[32];
-            tmem_ld32(tmem + lo + b * 128 + half * 32, sv);
-            tmem_ld32(tmem + lo + b * 128 + 64 + half * 32, dv);
+            uint32_t sv[16], dv[16];
+            tmem_ld16(tmem + lo + b * 128 + grp * 16, sv);
+            tmem_ld16(tmem + lo + b * 128 + 64 + grp * 16, dv);
             tmem_ld_wait();
             // the stage's statistics landed with Q/dO (s_full(it) follows the MMA's qs_full wait) and the
             // stage is not recycled before acc(it) completes, which needs this warp's arrival
-            const float4* l4 = reinterpret_cast<const float4*>(smem + OFF_LD + (it % NQS) * 512 + half * 128);
-            const float4* d4 = reinterpret_cast<const float4*>(smem + OFF_LD + (it % NQS) * 512 + 256 + half * 128);
+            const uint32_t lsm = sbase + OFF_LD + (it % NQS) * 512 + grp * 64;
             const bool need_mask = seg != nullptr || qq < k0 + 127;
-            uint32_t pw[16], sw[16];
+            uint32_t pw[8], sw[8];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float4 la = l4[2 * k], lb = l4[2 * k + 1];
-                const float4 da = d4[2 * k], db = d4[2 * k + 1];
-                const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-                const float dd[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+            for (int k = 0; k < 2; ++k) {
+                float lv[8], dd[8];
+                lds128(lsm + 32 * k, lv[0], lv[1], lv[2], lv[3]);
+                lds128(lsm + 32 * k + 16, lv[4], lv[5], lv[6], lv[7]);
+                lds128(lsm + 256 + 32 * k, dd[0], dd[1], dd[2], dd[3]);
+                lds128(lsm + 256 + 32 * k + 16, dd[4], dd[5], dd[6], dd[7]);
                 float p8[8], s8[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
@@ -721,25 +735,27 @@ __global__ void __launch_bounds__(THREADS, 1)
                     sw[4 * k + e] = pack_bf16x2(s8[2 * e], s8[2 * e + 1]);
                 }
             }
-            tmem_st16(tmem + lo + b * 128 + half * 32, pw);
-            tmem_st16(tmem + lo + b * 128 + half * 32 + 16, sw);
+            tmem_st8(tmem + lo + b * 128 + grp * 16, pw);
+            tmem_st8(tmem + lo + b * 128 + grp * 16 + 8, sw);
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&pd_full[b]);
         }
-        // epilogue: half 0 writes dV, half 1 writes dK (scaled)
+        // epilogue: column groups 0,1 write dV, 2,3 write dK (scaled); 64 columns each
         mbar_wait(acc_done, 0);
         tc_fence_after();
         const int64_t rs = (int64_t)(hq + 2 * hkv) * D;
-        bf16* dst = dqkv + key * rs + (int64_t)(half ? (hq + kvh) : (hq + hkv + kvh)) * D;
-        const float mul = half ? scale : 1.f;
-        const uint32_t acc_tm = tmem + lo + (half ? 384 : 256);
+        const bool isk = grp >= 2;
+        const int c0 = (grp & 1) * 64;
+        bf16* dst = dqkv + key * rs + (int64_t)(isk ? (hq + kvh) : (hq + hkv + kvh)) * D + c0;
+        const float mul = isk ? scale : 1.f;
+        const uint32_t acc_tm = tmem + lo + (isk ? 384 : 256) + c0;
         if (total == 0) {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
-            for (int k = 0; k < D / 8; ++k) d4[k] = make_uint4(0, 0, 0, 0);
+            for (int k = 0; k < 8; ++k) d4[k] = make_uint4(0, 0, 0, 0);
         } else {
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t v[32];
                 tmem_ld32(acc_tm + c * 32, v);
                 tmem_ld_wait();
@@ -758,7 +774,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == BW_MMA) {
         __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -802,11 +818,11 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dkv::SMEM));
         attr = true;
     }
-    fatc::dkdv_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::THREADS, fatc::dkv::SMEM, st>>>(
+    fatc::dkdv_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM, st>>>(
         t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
-    fatc::dq_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hq), fatc::THREADS, fatc::dq::SMEM, st>>>(
+    fatc::dq_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hq), fatc::BW_THREADS, fatc::dq::SMEM, st>>>(
         t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dq_tc");
     SPT_CUDA(cudaGetLastError());
