@@ -101,8 +101,18 @@ static bool use_pair_gemm() {
     return v;
 }
 
-void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep,
+static int epi_tstore() {
+    static const int v = [] {
+        const char* e = getenv("SPT_EPI_TSTORE");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v;
+}
+
+void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep_in,
           cudaStream_t st) {
+    EpiParams ep = ep_in;
+    ep.tstore = epi_tstore();
     if (Prof* pf = current_prof(); pf && pf->on) {
         static const char* kn[] = {"bf16", "f32", "swiglu", "swiglu_bwd", "f32_stats"};
         pf->next_tag = std::string(A.mn_major ? "MN" : "K") + (B.mn_major ? "MN" : "K") + "_" + kn[kind] + "_" +

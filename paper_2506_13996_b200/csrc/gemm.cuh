@@ -40,9 +40,13 @@ struct EpiParams {
     float alpha = 1.f;
     float* stats = nullptr;  // EPI_F32_STATS: [M][ld_stats] float2 (max, sumexp) per 256-column tile
     int64_t ld_stats = 0;
+    int tstore = 1;  // fp32 epilogues: coalesced stores through the warp's smem transpose tile
 };
 
 constexpr int GEMM_BM = 128;
+// per epilogue warp: a 32 x 33 fp32 tile used to transpose TMEM rows into coalesced row segments
+constexpr int EPI_TBUF_FLOATS = 32 * 33;
+constexpr int EPI_TBUF_BYTES = 4 * EPI_TBUF_FLOATS * 4;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 256;
 
@@ -53,7 +57,7 @@ struct GemmCfg {
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_TBUF_BYTES;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
@@ -79,6 +83,50 @@ __device__ __forceinline__ void load_bf16x32(const bf16* src, float* v) {
         v[8 * q + 0] = a.x; v[8 * q + 1] = a.y; v[8 * q + 2] = b.x; v[8 * q + 3] = b.y;
         v[8 * q + 4] = c.x; v[8 * q + 5] = c.y; v[8 * q + 6] = d.x; v[8 * q + 7] = d.y;
     }
+}
+
+// Coalesced store of a 32 x 32 block held one-row-per-lane (thread `lane` owns row row0+lane, 32 columns
+// in v[]): transpose through the warp's smem tile so that each store instruction writes 32 consecutive
+// columns of ONE row (128 B fp32 / 64 B bf16 per instruction instead of 32 scattered rows).
+template <int KIND>
+__device__ __forceinline__ void store_block_t(const EpiParams& ep, float* tb, int64_t row0, int64_t col0, int64_t M,
+                                              const float* v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tb[lane * 33 + i] = v[i];
+    __syncwarp();
+    const int nrow = (M - row0) < 32 ? (int)(M - row0) : 32;
+    if constexpr (KIND == EPI_BF16) {
+        bf16* base = reinterpret_cast<bf16*>(ep.C) + row0 * ep.ldc + col0 + lane;
+        if (ep.R != nullptr) {
+            float res[32];  // all residual loads in flight before the stores
+            const bf16* rb = ep.R + row0 * ep.ldr + col0 + lane;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) res[rr] = rr < nrow ? __bfloat162float(rb[rr * ep.ldr]) : 0.f;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr)
+                if (rr < nrow) base[rr * ep.ldc] = __float2bfloat16_rn(tb[rr * 33 + lane] * ep.alpha + res[rr]);
+        } else {
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr)
+                if (rr < nrow) base[rr * ep.ldc] = __float2bfloat16_rn(tb[rr * 33 + lane] * ep.alpha);
+        }
+    } else {
+        float* base = reinterpret_cast<float*>(ep.C) + row0 * ep.ldc + col0 + lane;
+        if (ep.accumulate) {
+            float old[32];  // all 32 loads in flight before the read-modify-write stores
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) old[rr] = rr < nrow ? base[rr * ep.ldc] : 0.f;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr)
+                if (rr < nrow) base[rr * ep.ldc] = tb[rr * 33 + lane] * ep.alpha + old[rr];
+        } else {
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr)
+                if (rr < nrow) base[rr * ep.ldc] = tb[rr * 33 + lane] * ep.alpha;
+        }
+    }
+    __syncwarp();
 }
 
 // One 32-column chunk (or a g/u pair of chunks for the SwiGLU kinds) of one row.
@@ -156,6 +204,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* tbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);  // epilogue transpose tiles
 
     const int warp = warp_id(), lane = lane_id();
     const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
@@ -288,8 +337,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld32(tbase + c, r0);
                 tmem_ld32(tbase + c + 32, r1);
                 tmem_ld_wait();
+                if constexpr (KIND == EPI_F32 || KIND == EPI_F32_STATS) {
+                    if (col < N && ep.tstore) {  // warp-uniform (N % 64 == 0); rows bounds-checked inside
+                        float* tb = tbuf + (warp & 3) * EPI_TBUF_FLOATS;
+                        const int64_t row0 = row - lane;
+                        store_block_t<KIND>(ep, tb, row0, col, M, reinterpret_cast<const float*>(r0));
+                        store_block_t<KIND>(ep, tb, row0, col + 32, M, reinterpret_cast<const float*>(r1));
+                    }
+                }
                 if (row < M && col < N) {
-                    epilogue_chunk<KIND>(ep, row, col, r0, r1);
+                    if (!(KIND == EPI_F32 || KIND == EPI_F32_STATS) || !ep.tstore)
+                        epilogue_chunk<KIND>(ep, row, col, r0, r1);
                     if constexpr (KIND == EPI_F32_STATS) {
                         float mx = st_m;
 #pragma unroll
@@ -337,7 +395,7 @@ struct Gemm2Cfg {
     static constexpr int B_BYTES = (BN / 2) * GEMM_BK * 2;       // this CTA's half of B
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + EPI_TBUF_BYTES;
 };
 
 template <int BN, bool A_MN, bool B_MN, int KIND>
@@ -353,6 +411,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* tbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);  // epilogue transpose tiles
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -488,8 +547,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld32(tbase + c, r0);
                 tmem_ld32(tbase + c + 32, r1);
                 tmem_ld_wait();
+                if constexpr (KIND == EPI_F32 || KIND == EPI_F32_STATS) {
+                    if (col < N && ep.tstore) {  // warp-uniform (N % 64 == 0); rows bounds-checked inside
+                        float* tb = tbuf + (warp & 3) * EPI_TBUF_FLOATS;
+                        const int64_t row0 = row - lane;
+                        store_block_t<KIND>(ep, tb, row0, col, M, reinterpret_cast<const float*>(r0));
+                        store_block_t<KIND>(ep, tb, row0, col + 32, M, reinterpret_cast<const float*>(r1));
+                    }
+                }
                 if (row < M && col < N) {
-                    epilogue_chunk<KIND>(ep, row, col, r0, r1);
+                    if (!(KIND == EPI_F32 || KIND == EPI_F32_STATS) || !ep.tstore)
+                        epilogue_chunk<KIND>(ep, row, col, r0, r1);
                     if constexpr (KIND == EPI_F32_STATS) {
                         float mx = st_m;
 #pragma unroll
