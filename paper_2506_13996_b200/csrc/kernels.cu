@@ -62,7 +62,8 @@ __global__ void rmsnorm_bwd_kernel(const bf16* __restrict__ x, const bf16* __res
     __shared__ float red[32];
     const int c = threadIdx.x * 8;
     const bool act = c < h;
-    float gv[8], dga[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // inactive lanes (h/8 not a multiple of 32) must contribute exact zeros to the row dot
+    float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dga[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (act) load8(g + c, gv);
     const int64_t r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
     for (int64_t r = r0; r < r1; ++r) {

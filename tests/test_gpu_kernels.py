@@ -26,7 +26,7 @@ def _cuda():
 # ------------------------------------------------------------------ GEMM (tcgen05)
 @pytest.mark.parametrize("a_mn,b_mn,f32,acc", [(0, 0, 0, 0), (0, 1, 0, 0), (1, 1, 1, 0), (1, 1, 1, 1), (0, 0, 1, 0),
                                                 (0, 1, 1, 0), (1, 1, 0, 0)])
-@pytest.mark.parametrize("M,N,K", [(320, 384, 320), (128, 256, 64), (1000, 512, 4160)])
+@pytest.mark.parametrize("M,N,K", [(320, 384, 320), (128, 256, 64), (1000, 512, 4160), (1024, 320, 640), (320, 640, 1024)])
 def test_gemm_majors(a_mn, b_mn, f32, acc, M, N, K):
     T = torch()
     g = T.Generator(device="cuda").manual_seed(M + N + K)
@@ -72,7 +72,7 @@ def test_gemm_rejects_bad_n():
 
 
 # ------------------------------------------------------------------ RMSNorm
-@pytest.mark.parametrize("n,h", [(300, 256), (64, 4096)])
+@pytest.mark.parametrize("n,h", [(300, 256), (64, 4096), (1024, 320)])
 def test_rmsnorm_fwd_bwd(n, h):
     T = torch()
     rng = np.random.default_rng(n)
@@ -204,7 +204,8 @@ def _attn_case(s, hq, hkv, d, packed, seed, amp=1.0):
                                                    (512, 2, 2, 64, True, 1), (256, 8, 2, 128, True, 1),
                                                    (1024, 4, 2, 128, False, 1), (2048, 2, 1, 128, True, 1),
                                                    (1536, 2, 2, 128, False, 1), (1024, 2, 1, 128, False, 2.5),
-                                                   (1024, 2, 2, 128, True, 2.5)])
+                                                   (1024, 2, 2, 128, True, 2.5), (1024, 4, 1, 128, False, 1),
+                                                   (1024, 8, 1, 128, True, 1)])
 def test_attention_fwd_bwd(s, hq, hkv, d, packed, amp):
     """amp > 1 gives peaked softmax rows: exercises the lazy O-rescale path of the tcgen05 forward."""
     T = torch()
@@ -269,7 +270,7 @@ def test_flce(n, h, V, tile):
 
 
 # ------------------------------------------------------------------ TiledMLP
-@pytest.mark.parametrize("n,h,I,tile", [(256, 256, 1024, 128), (300, 128, 512, 100)])
+@pytest.mark.parametrize("n,h,I,tile", [(256, 256, 1024, 128), (300, 128, 512, 100), (1024, 320, 640, 1024)])
 def test_tiled_mlp(n, h, I, tile):
     T = torch()
     rng = np.random.default_rng(n + I)

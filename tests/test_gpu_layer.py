@@ -116,3 +116,36 @@ def test_bad_sp_degree_rejected():
     with pytest.raises(S.ValidationError, match="q_heads not divisible by SP degree"):
         S.UlyssesLayerStep(SHAPE, 384, grp)
     grp.close()
+
+
+# ---- head_dim 128 shapes: the layer step runs the tcgen05 attention kernels (fwd_tc / dkdv_tc / dq_tc)
+D128 = O.LayerConfig(hidden=256, q_heads=4, kv_heads=2, head_dim=128, intermediate=512, vocab=2048)
+D128_SHAPE = S.ModelShape(256, 4, 2, 128, 512, 2048)
+QWENISH = O.LayerConfig(hidden=320, q_heads=4, kv_heads=1, head_dim=128, intermediate=640, vocab=1024)  # h != Hq*d
+QWENISH_SHAPE = S.ModelShape(320, 4, 1, 128, 640, 1024)
+
+
+@pytest.mark.parametrize("P,packed", [(1, False), (2, False), (4, True), (4, False)])
+def test_layer_tc_attention_matches_oracle(P, packed):
+    """Llama-like head_dim 128 (tcgen05 attention) at SP=1/2/4 (loopback); P=4 with Hkv=2 replicates kv (r=2)."""
+    N = 1024
+    r = _run(P, N, packed=packed, cfg=D128, shape=D128_SHAPE)
+    ref = _oracle(r, packed=packed, cfg=D128)
+    assert r["count"] == ref.count
+    assert abs(r["loss"] - ref.loss) / abs(ref.loss) <= LOSS_TOL
+    for k in O.LayerParams.NAMES:
+        e = rel_err(r["grads"][k], ref.grads[k])
+        assert e <= GRAD_TOL, (k, e)
+    assert rel_err(r["dx"], ref.dx) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_layer_hidden_ne_heads_times_dim(P):
+    """Qwen3-style shape (attention width Hq*d != hidden, SURVEY App. B #3) with MQA-like Hkv=1 (r=P)."""
+    N = 1024
+    r = _run(P, N, cfg=QWENISH, shape=QWENISH_SHAPE)
+    ref = _oracle(r, cfg=QWENISH)
+    assert abs(r["loss"] - ref.loss) / abs(ref.loss) <= LOSS_TOL
+    for k in O.LayerParams.NAMES:
+        e = rel_err(r["grads"][k], ref.grads[k])
+        assert e <= GRAD_TOL, (k, e)
