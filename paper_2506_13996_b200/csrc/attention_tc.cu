@@ -7,6 +7,7 @@
 // score columns and is the A operand of the PV MMA) or into swizzled smem (backward).  Online softmax
 // uses a lazy rescale: O is only rescaled in TMEM when the running max grows by > 2^8.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.h"
 #include "launch.h"
@@ -27,6 +28,25 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+
+// 2^x on the FMA pipe (Cody-Waite split + degree-3 fit of 2^f on [-1/2, 1/2], max rel err 1.5e-4, far
+// below the bf16 rounding of P).  The forward softmax runs a fraction of its exponentials through this so
+// the MUFU pipe (16 ex2/clk/SM, exactly the rate a 128x64 score tile needs at full tensor throughput) stops
+// being the co-bottleneck.  Inputs below -126 (masked -inf) return exactly 0 like ex2.approx.ftz.
+__device__ __forceinline__ float ex2_poly(float x) {
+    const float xc = fmaxf(x, -127.f);
+    const float t = xc + 12582912.f;  // 1.5 * 2^23: round(xc) lands in the low mantissa bits of t
+    const float rf = t - 12582912.f;
+    const float f = xc - rf;
+    const float p = fmaf(fmaf(fmaf(0.05508868f, f, 0.24260405f), f, 0.69327624f), f, 0.99992894f);
+    const float y = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+    return x < -126.f ? 0.f : y;
+}
+
+#ifndef SPT_FWD_POLY_EVERY
+#define SPT_FWD_POLY_EVERY 0  // N > 0: every N-th exponential pair goes through ex2_poly (measured slower: the
+                              // forward softmax is issue-bound, not MUFU-bound, on B200)
+#endif
 
 __device__ __forceinline__ void lds128(uint32_t addr, float& a, float& b, float& c, float& d) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
@@ -291,16 +311,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             l *= alpha;
             if (grow) m_use = mx;
             const float nbase = m_use == -INFINITY ? 0.f : -m_use;
-            float rs = 0.f;
             uint32_t pw[32];
+            const uint64_t sc2 = f2pack(scale_log2, scale_log2), nb2 = f2pack(nbase, nbase);
+            uint64_t rs2 = f2pack(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const int c0 = 2 * k;
-                const float p0 = ex2(fmaf(__uint_as_float(v[c0 >> 5][c0 & 31]), scale_log2, nbase));
-                const float p1 = ex2(fmaf(__uint_as_float(v[c0 >> 5][(c0 + 1) & 31]), scale_log2, nbase));
-                rs += p0 + p1;
+                const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c0 >> 5][c0 & 31]), __uint_as_float(v[c0 >> 5][(c0 + 1) & 31])),
+                                          sc2, nb2);
+                float x0, x1;
+                f2unpack(x2, x0, x1);
+                const bool poly = SPT_FWD_POLY_EVERY > 0 && (k % (SPT_FWD_POLY_EVERY > 0 ? SPT_FWD_POLY_EVERY : 1)) ==
+                                                                (SPT_FWD_POLY_EVERY > 0 ? SPT_FWD_POLY_EVERY - 1 : 0);
+                const float p0 = poly ? ex2_poly(x0) : ex2(x0);
+                const float p1 = poly ? ex2_poly(x1) : ex2(x1);
+                rs2 = fadd2(rs2, f2pack(p0, p1));
                 pw[k] = pack_bf16x2(p0, p1);
             }
+            float rs0, rs1;
+            f2unpack(rs2, rs0, rs1);
+            const float rs = rs0 + rs1;
             l += rs;
 #ifdef SPT_WATCHDOG
             if (r == 0) dbg[2 * t + 1] = 3;
@@ -472,6 +502,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int sub = warp & 3, grp = warp >> 2;  // lanes [32 sub, +32), keys [16 grp, +16) of each block
         const int r = sub * 32 + lane;
         const int64_t q = q0 + r;
+        const int q32 = (int)q, q0i = (int)q0;  // s < 2^31 (attn_bwd_tc checks)
         const int start = seg ? seg[q] : 0;
         const float nlse2 = -lse2v[(int64_t)h * s + q];  // -(lse * log2 e), precomputed
         const float Dq = Dv[(int64_t)h * s + q];
@@ -490,24 +521,32 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             tmem_ld16(tmem + lo + b * 128 + grp * 16, sv);
             tmem_ld16(tmem + lo + b * 128 + 64 + grp * 16, dv);
             tmem_ld_wait();
-            const int64_t k0 = (int64_t)(jb + it) * BKB + grp * 16;
-            const bool need_mask = seg != nullptr || (k0 + 15 > q0);
+            const int k0 = (jb + it) * BKB + grp * 16;
             uint32_t w[8];
+            // Two straight-line bodies (the branch is warp-uniform): the unmasked blocks carry no per-element
+            // compare/select work at all; masked blocks compare the column index against int32 limits.
+            auto body = [&](auto mask_c) {
+                constexpr bool MASK = decltype(mask_c)::value;
+                const int hi = q32 - k0, lo_ = start - k0;  // keep columns lo_ <= i <= hi
+                const uint64_t sl2x = f2pack(sl2, sl2), nlx = f2pack(nlse2, nlse2), dqx = f2pack(Dq, Dq);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                float d2[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int i = 2 * k + e;
-                    float p = ex2(fmaf(__uint_as_float(sv[i]), sl2, nlse2));
-                    if (need_mask) {
-                        const int64_t key = k0 + i;
-                        if (key > q || key < start) p = 0.f;
+                for (int k = 0; k < 8; ++k) {
+                    float x0, x1;
+                    f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * k]), __uint_as_float(sv[2 * k + 1])), sl2x, nlx), x0, x1);
+                    float p0 = ex2(x0), p1 = ex2(x1);
+                    if constexpr (MASK) {
+                        p0 = (2 * k > hi || 2 * k < lo_) ? 0.f : p0;
+                        p1 = (2 * k + 1 > hi || 2 * k + 1 < lo_) ? 0.f : p1;
                     }
-                    d2[e] = p * (__uint_as_float(dv[i]) - Dq);
+                    const uint64_t ds = fmul2(f2pack(p0, p1),
+                                              fsub2(f2pack(__uint_as_float(dv[2 * k]), __uint_as_float(dv[2 * k + 1])), dqx));
+                    float d0, d1;
+                    f2unpack(ds, d0, d1);
+                    w[k] = pack_bf16x2(d0, d1);
                 }
-                w[k] = pack_bf16x2(d2[0], d2[1]);
-            }
+            };
+            if (seg != nullptr || k0 + 15 > q0i) body(std::true_type{});
+            else body(std::false_type{});
             tmem_st8(tmem + lo + b * 128 + grp * 16, w);  // over this warp's consumed S columns
             tmem_st_wait();
             tc_fence_before();
@@ -615,8 +654,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t sbase = smem_u32(smem);
-    auto it_head = [&](int it) { return kvh * grp + it / nqb; };
-    auto it_q0 = [&](int it) { return (int64_t)(qb_first + it % nqb) * BQB; };
     if (warp == BW_TMA) {
         if (lane == 0) {
             mbar_arrive_expect_tx(kv_full, 2 * KB_BYTES);
@@ -624,20 +661,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
                 tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
             }
+            int hh = kvh * grp, qblk = 0;
             for (int it = 0; it < total; ++it) {
                 const int st = it % NQS;
                 mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES + 512);
-                const int hh = it_head(it);
-                const int qq = (int)it_q0(it);
+                const int qq = (qb_first + qblk) * BQB;
+                const int hcur = hh;
+                if (++qblk == nqb) { qblk = 0; ++hh; }
                 uint8_t* base = smem + OFF_QS + st * 2 * QS_BYTES;
                 for (int r = 0; r < 2; ++r) {
-                    tma_load_2d(&tq, &qs_full[st], base + r * 8192, hh * D + 64 * r, qq);
-                    tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hh * D + 64 * r, qq);
+                    tma_load_2d(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq);
+                    tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq);
                 }
                 // per-column softmax statistics of this q block (lse*log2e, D) for the elementwise warps
-                bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hh * s + qq, 256, &qs_full[st]);
-                bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hh * s + qq, 256, &qs_full[st]);
+                bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st]);
+                bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st]);
             }
         }
     } else if (warp == BW_MMA) {
@@ -689,11 +728,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int sub = warp & 3, grp = warp >> 2;
         const int r = sub * 32 + lane;  // key row
         const int64_t key = k0 + r;
+        const int key32 = (int)key;  // s < 2^31 (attn_bwd_tc checks)
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         const float sl2 = scale * LOG2E;
+        int qblk = 0;  // iteration it = (q head it / nqb, q block qb_first + it % nqb), kept incrementally
         for (int it = 0; it < total; ++it) {
             const int b = it & 1;
-            const int64_t qq = it_q0(it) + grp * 16;
+            const int qq = (qb_first + qblk) * BQB + grp * 16;
+            if (++qblk == nqb) qblk = 0;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
 #ifdef SPT_EXP_NO_ELEM
@@ -708,33 +750,42 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             // the stage's statistics landed with Q/dO (s_full(it) follows the MMA's qs_full wait) and the
             // stage is not recycled before acc(it) completes, which needs this warp's arrival
             const uint32_t lsm = sbase + OFF_LD + (it % NQS) * 512 + grp * 64;
-            const bool need_mask = seg != nullptr || qq < k0 + 127;
             uint32_t pw[8], sw[8];
+            // warp-uniform choice between a straight-line unmasked body and the masked one (int32 limits)
+            auto body = [&](auto mask_c) {
+                constexpr bool MASK = decltype(mask_c)::value;
+                const int lo_ = key32 - qq;  // causal: keep columns i >= key - qq
+                const uint64_t sl2x = f2pack(sl2, sl2);
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                float lv[8], dd[8];
-                lds128(lsm + 32 * k, lv[0], lv[1], lv[2], lv[3]);
-                lds128(lsm + 32 * k + 16, lv[4], lv[5], lv[6], lv[7]);
-                lds128(lsm + 256 + 32 * k, dd[0], dd[1], dd[2], dd[3]);
-                lds128(lsm + 256 + 32 * k + 16, dd[4], dd[5], dd[6], dd[7]);
-                float p8[8], s8[8];
+                for (int k = 0; k < 2; ++k) {
+                    float lv[8], dd[8];
+                    lds128(lsm + 32 * k, lv[0], lv[1], lv[2], lv[3]);
+                    lds128(lsm + 32 * k + 16, lv[4], lv[5], lv[6], lv[7]);
+                    lds128(lsm + 256 + 32 * k, dd[0], dd[1], dd[2], dd[3]);
+                    lds128(lsm + 256 + 32 * k + 16, dd[4], dd[5], dd[6], dd[7]);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int i = 8 * k + e;
-                    float p = ex2(fmaf(__uint_as_float(sv[i]), sl2, -lv[e]));
-                    if (need_mask) {
-                        const int64_t qi = qq + i;
-                        if (key > qi || (seg && key < seg[qi])) p = 0.f;
+                    for (int e = 0; e < 8; e += 2) {
+                        const int i = 8 * k + e;
+                        float x0, x1;
+                        f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sl2x,
+                                       f2pack(-lv[e], -lv[e + 1])),
+                                 x0, x1);
+                        float p0 = ex2(x0), p1 = ex2(x1);
+                        if constexpr (MASK) {
+                            if (i < lo_ || (seg && key32 < seg[qq + i])) p0 = 0.f;
+                            if (i + 1 < lo_ || (seg && key32 < seg[qq + i + 1])) p1 = 0.f;
+                        }
+                        const uint64_t ds = fmul2(f2pack(p0, p1), fsub2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
+                                                                        f2pack(dd[e], dd[e + 1])));
+                        float s0, s1;
+                        f2unpack(ds, s0, s1);
+                        pw[4 * k + e / 2] = pack_bf16x2(p0, p1);
+                        sw[4 * k + e / 2] = pack_bf16x2(s0, s1);
                     }
-                    p8[e] = p;
-                    s8[e] = p * (__uint_as_float(dv[i]) - dd[e]);
                 }
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    pw[4 * k + e] = pack_bf16x2(p8[2 * e], p8[2 * e + 1]);
-                    sw[4 * k + e] = pack_bf16x2(s8[2 * e], s8[2 * e + 1]);
-                }
-            }
+            };
+            if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
+            else body(std::false_type{});
             tmem_st8(tmem + lo + b * 128 + grp * 16, pw);
             tmem_st8(tmem + lo + b * 128 + grp * 16 + 8, sw);
             tmem_st_wait();
@@ -805,7 +856,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
 // Deterministic tcgen05 backward (d = 128, s % 256 == 0).  Dv = rowsum(dO * O) must be precomputed.
 bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const float* Dv, int64_t s, int hq, int hkv,
                  int d, const int32_t* seg, float scale, void* dqkv, cudaStream_t st) {
-    if (d != fatc::D || s % 256 != 0) return false;
+    if (d != fatc::D || s % 256 != 0 || s >= (int64_t(1) << 31) - 256) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap t128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
     CUtensorMap t64 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);

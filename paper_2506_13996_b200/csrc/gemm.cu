@@ -93,11 +93,22 @@ static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, int M, in
     });
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+// Experiment / tuning switches (read once): SPT_GEMM_1SM=1 disables CTA pairs, SPT_GEMM_PAIR_MN=1 also
+// runs MN-major operand shapes as pairs, SPT_GEMM_BN=128|256 forces the N tile (0 = per-shape choice).
 static bool use_pair_gemm() {
-    static const bool v = [] {
-        const char* e = getenv("SPT_GEMM_1SM");
-        return !(e && e[0] == '1');
-    }();
+    static const bool v = env_int("SPT_GEMM_1SM", 0) != 1;
+    return v;
+}
+static bool pair_mn() {
+    static const bool v = env_int("SPT_GEMM_PAIR_MN", 0) == 1;
+    return v;
+}
+static int forced_bn() {
+    static const int v = env_int("SPT_GEMM_BN", 0);
     return v;
 }
 
@@ -109,41 +120,32 @@ static int epi_tstore() {
     return v;
 }
 
-void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep_in,
-          cudaStream_t st) {
-    EpiParams ep = ep_in;
-    ep.tstore = epi_tstore();
-    if (Prof* pf = current_prof(); pf && pf->on) {
-        static const char* kn[] = {"bf16", "f32", "swiglu", "swiglu_bwd", "f32_stats"};
-        pf->next_tag = std::string(A.mn_major ? "MN" : "K") + (B.mn_major ? "MN" : "K") + "_" + kn[kind] + "_" +
-                       std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K);
+template <int BN>
+static void dispatch_pair(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind,
+                          const EpiParams& ep, cudaStream_t st) {
+    CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
+                                : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
+    CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)
+                                : make_tmap_bf16_2d(B.ptr, K, N, B.ld, GEMM_BK, BN / 2);
+    const int m = (int)M, n = (int)N, k = (int)K;
+    const int sel = (A.mn_major ? 2 : 0) + (B.mn_major ? 1 : 0);
+    switch (sel * 8 + kind) {
+        case 0 * 8 + EPI_BF16: launch_gemm2<BN, false, false, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
+        case 0 * 8 + EPI_F32: launch_gemm2<BN, false, false, EPI_F32>(ta, tb, m, n, k, ep, st); return;
+        case 0 * 8 + EPI_SWIGLU: launch_gemm2<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); return;
+        case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm2<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); return;
+        case 0 * 8 + EPI_F32_STATS: launch_gemm2<BN, false, false, EPI_F32_STATS>(ta, tb, m, n, k, ep, st); return;
+        case 1 * 8 + EPI_BF16: launch_gemm2<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
+        case 1 * 8 + EPI_F32: launch_gemm2<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
+        case 3 * 8 + EPI_BF16: launch_gemm2<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
+        case 3 * 8 + EPI_F32: launch_gemm2<BN, true, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
+        default: SPT_THROW(SPT_ERR_INTERNAL, "gemm: unsupported major/epilogue combination");
     }
-    SPT_CHECK(M > 0 && N > 0 && K > 0, SPT_ERR_SHAPE, "gemm: empty problem");
-    SPT_CHECK(N % 64 == 0, SPT_ERR_SHAPE, "gemm: N must be a multiple of 64, got " + std::to_string(N));
-    SPT_CHECK(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), SPT_ERR_SHAPE, "gemm: dims exceed int32");
-    constexpr int BN = 256;
-    // CTA pairs win for K-major x K-major (forward / logits) GEMMs; with MN-major operands the 1-SM
-    // kernel measured faster inside the layer step (profiles/README.md, per-site breakdown).
-    if (M >= 2 * GEMM_BM && !A.mn_major && !B.mn_major && use_pair_gemm()) {
-        CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
-                                    : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
-        CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)
-                                    : make_tmap_bf16_2d(B.ptr, K, N, B.ld, GEMM_BK, BN / 2);
-        const int m = (int)M, n = (int)N, k = (int)K;
-        const int sel = (A.mn_major ? 2 : 0) + (B.mn_major ? 1 : 0);
-        switch (sel * 8 + kind) {
-            case 0 * 8 + EPI_BF16: launch_gemm2<BN, false, false, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
-            case 0 * 8 + EPI_F32: launch_gemm2<BN, false, false, EPI_F32>(ta, tb, m, n, k, ep, st); return;
-            case 0 * 8 + EPI_SWIGLU: launch_gemm2<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); return;
-            case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm2<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); return;
-            case 0 * 8 + EPI_F32_STATS: launch_gemm2<BN, false, false, EPI_F32_STATS>(ta, tb, m, n, k, ep, st); return;
-            case 1 * 8 + EPI_BF16: launch_gemm2<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
-            case 1 * 8 + EPI_F32: launch_gemm2<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
-            case 3 * 8 + EPI_BF16: launch_gemm2<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
-            case 3 * 8 + EPI_F32: launch_gemm2<BN, true, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
-            default: SPT_THROW(SPT_ERR_INTERNAL, "gemm: unsupported major/epilogue combination");
-        }
-    }
+}
+
+template <int BN>
+static void dispatch_1sm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind,
+                         const EpiParams& ep, cudaStream_t st) {
     CUtensorMap ta = A.mn_major ? make_tmap_bf16_2d(A.ptr, M, K, A.ld, 64, GEMM_BK)
                                 : make_tmap_bf16_2d(A.ptr, K, M, A.ld, GEMM_BK, GEMM_BM);
     CUtensorMap tb = B.mn_major ? make_tmap_bf16_2d(B.ptr, N, K, B.ld, 64, GEMM_BK)
@@ -162,6 +164,33 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
         case 3 * 8 + EPI_F32: launch_gemm<BN, true, true, EPI_F32>(ta, tb, m, n, k, ep, st); break;
         default: SPT_THROW(SPT_ERR_INTERNAL, "gemm: unsupported major/epilogue combination");
     }
+}
+
+void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep_in,
+          cudaStream_t st) {
+    EpiParams ep = ep_in;
+    ep.tstore = epi_tstore();
+    if (Prof* pf = current_prof(); pf && pf->on) {
+        static const char* kn[] = {"bf16", "f32", "swiglu", "swiglu_bwd", "f32_stats"};
+        pf->next_tag = std::string(A.mn_major ? "MN" : "K") + (B.mn_major ? "MN" : "K") + "_" + kn[kind] + "_" +
+                       std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K);
+    }
+    SPT_CHECK(M > 0 && N > 0 && K > 0, SPT_ERR_SHAPE, "gemm: empty problem");
+    SPT_CHECK(N % 64 == 0, SPT_ERR_SHAPE, "gemm: N must be a multiple of 64, got " + std::to_string(N));
+    SPT_CHECK(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), SPT_ERR_SHAPE, "gemm: dims exceed int32");
+    // The SwiGLU epilogues pair gate/up 32-column blocks inside a 64-column chunk and the logits stats are
+    // per 256 columns, so those kinds keep BN = 256.
+    const bool bn_free = kind == EPI_BF16 || kind == EPI_F32;
+    const int bn = bn_free && (forced_bn() == 128) ? 128 : 256;
+    // CTA pairs win for K-major x K-major (forward / logits) GEMMs; with MN-major operands the 1-SM
+    // kernel measured faster inside the layer step (profiles/README.md, per-site breakdown).
+    if (M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn()) && use_pair_gemm()) {
+        if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
+        else dispatch_pair<256>(A, B, M, N, K, kind, ep, st);
+        return;
+    }
+    if (bn == 128) dispatch_1sm<128>(A, B, M, N, K, kind, ep, st);
+    else dispatch_1sm<256>(A, B, M, N, K, kind, ep, st);
 }
 
 }  // namespace spt
