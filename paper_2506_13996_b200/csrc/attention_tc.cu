@@ -125,8 +125,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = warp_id(), lane = lane_id();
     const int npairs = (int)(s / (2 * BQ));
-    const int pair = npairs - 1 - (int)blockIdx.x;  // longest causal rows first
-    const int h = blockIdx.y;
+    // grid = (q head, query-tile pair): heads vary fastest so one wave of CTAs streams the K/V of every kv
+    // head at once instead of 148 CTAs hammering the same K/V lines (L2-slice hot spot); longest rows first
+    const int pair = npairs - 1 - (int)blockIdx.y;
+    const int h = blockIdx.x;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)pair * 2 * BQ;
     const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = seg ? (int)(seg[q0 + BQ] / BKB) : 0;
@@ -385,7 +387,10 @@ namespace dq {
 constexpr int BKB = 64;
 constexpr int Q_BYTES = 128 * D * 2;        // 32 KiB
 constexpr int KV_BYTES = BKB * D * 2;       // 16 KiB (two 8 KiB regions)
-constexpr int NSL = 8;
+#ifndef SPT_DQ_NSL
+#define SPT_DQ_NSL 10
+#endif
+constexpr int NSL = SPT_DQ_NSL;  // K/V ring slots (16 KiB each): 5 blocks of K+V in flight
 constexpr int NB = 3;          // S/dP TMEM buffers (128 columns each): the MMA runs NB-1 blocks ahead
 constexpr int DQ_COL = 384;    // dQ accumulator columns [384, 512)
 constexpr int OFF_Q = 0, OFF_DO = Q_BYTES, OFF_KV = 2 * Q_BYTES;  // dS lives in TMEM (A operand of dQ)
@@ -410,8 +415,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
     const int warp = warp_id(), lane = lane_id();
     const int nqb = (int)(s / 128);
-    const int qb = nqb - 1 - (int)blockIdx.x;  // longest rows first
-    const int h = blockIdx.y;
+    const int qb = nqb - 1 - (int)blockIdx.y;  // longest rows first; heads vary fastest (see fwd_tc_kernel)
+    const int h = blockIdx.x;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)qb * 128;
     const int jb = seg ? (int)(seg[q0] / BKB) : 0;
@@ -846,7 +851,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
         SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
         attr = true;
     }
-    dim3 grid((unsigned)(s / 256), (unsigned)hq);
+    dim3 grid((unsigned)hq, (unsigned)(s / 256));
     k<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse);
     count_launch("attn_fwd_tc");
     SPT_CUDA(cudaGetLastError());
@@ -873,7 +878,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
-    fatc::dq_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hq), fatc::BW_THREADS, fatc::dq::SMEM, st>>>(
+    fatc::dq_tc_kernel<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dq::SMEM, st>>>(
         t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
     count_launch("attn_dq_tc");
     SPT_CUDA(cudaGetLastError());

@@ -1,4 +1,4 @@
 # Attention parity tests + timing of the current build.
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q -x -k "attention or layer or fullsize" > gpurun_out/attn_tests.log 2>&1; tail -3 gpurun_out/attn_tests.log
+python -m pytest tests -m gpu -q -x -k "attention or layer or fullsize" > gpurun_out/attn_tests.log 2>&1; tail -1 gpurun_out/attn_tests.log
 python tools/attn_bench.py 2>&1 | tee gpurun_out/attn_bench.txt
