@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // provably warp-uniform: descriptor math stays in uniform registers
     const uint32_t sbase = smem_u32(smem);
 
     if (warp == 9) {
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // provably warp-uniform: descriptor math stays in uniform registers
     const uint32_t sbase = smem_u32(smem);
     if (warp == BW_TMA) {
         if (lane == 0) {
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // provably warp-uniform: descriptor math stays in uniform registers
     const uint32_t sbase = smem_u32(smem);
     if (warp == BW_TMA) {
         if (lane == 0) {

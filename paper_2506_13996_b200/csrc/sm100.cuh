@@ -16,7 +16,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+// warp index broadcast from lane 0: the compiler then treats role branches as warp-uniform and keeps the
+// MMA issuer's descriptor arithmetic on the uniform datapath (call with the warp converged)
+__device__ __forceinline__ int warp_id() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // ------------------------------------------------------------------ mbarrier

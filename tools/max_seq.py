@@ -72,7 +72,7 @@ for n in [int(v) for v in a.n.split(",")]:
                    "ledger_peak_gib": round(led["peak_bytes"] / 2**30, 2),
                    "device_used_bytes": total - free, "wall_s_two_steps": round(time.time() - t0, 1)})
         del x, lab
-    except S.SptError as e:
+    except (S.SptError, torch.OutOfMemoryError) as e:  # engine or input allocation does not fit
         pt.update({"ok": False, "error": str(e)[:200]})
     finally:
         if eng is not None:
