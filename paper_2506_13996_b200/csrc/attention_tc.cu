@@ -276,22 +276,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             tmem_ld32(s_tm, v[0]);
             tmem_ld32(s_tm + 32, v[1]);
             tmem_ld_wait();
-            float mraw = -INFINITY;
+            // row max over the 64 columns: 8 independent partial maxima (short dependency chains; the two
+            // softmax warps per SMSP cannot hide a 64-long serial FMNMX chain)
+            float mp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mp[u] = -INFINITY;
             if (need_mask) {
+                const int hi = (int)(q - k0), lo_ = start - (int)k0;  // keep columns lo_ <= i <= hi
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const int64_t key = k0 + c * 32 + i;
-                        if (key > q || key < start) v[c][i] = __float_as_uint(-INFINITY);
-                        mraw = fmaxf(mraw, __uint_as_float(v[c][i]));
+                        const int col = c * 32 + i;
+                        if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
+                        mp[col & 7] = fmaxf(mp[col & 7], __uint_as_float(v[c][i]));
                     }
             } else {
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(v[c][i]));
+                    for (int i = 0; i < 32; i += 2)
+                        mp[(c * 32 + i) >> 1 & 7] =
+                            fmaxf(mp[(c * 32 + i) >> 1 & 7], fmaxf(__uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1])));
             }
+            const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                     fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
             const float mx = mraw * scale_log2;
             // lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective); needs PV_t(j-1) complete
             const bool grow = mx > m_use + RESCALE_THRESHOLD;
@@ -315,7 +324,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float nbase = m_use == -INFINITY ? 0.f : -m_use;
             uint32_t pw[32];
             const uint64_t sc2 = f2pack(scale_log2, scale_log2), nb2 = f2pack(nbase, nbase);
-            uint64_t rs2 = f2pack(0.f, 0.f);
+            uint64_t rs2[4];  // 4 independent packed row-sum accumulators (short FADD2 chains)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const int c0 = 2 * k;
@@ -327,11 +338,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                                 (SPT_FWD_POLY_EVERY > 0 ? SPT_FWD_POLY_EVERY - 1 : 0);
                 const float p0 = poly ? ex2_poly(x0) : ex2(x0);
                 const float p1 = poly ? ex2_poly(x1) : ex2(x1);
-                rs2 = fadd2(rs2, f2pack(p0, p1));
+                rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
                 pw[k] = pack_bf16x2(p0, p1);
             }
             float rs0, rs1;
-            f2unpack(rs2, rs0, rs1);
+            f2unpack(fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3])), rs0, rs1);
             const float rs = rs0 + rs1;
             l += rs;
 #ifdef SPT_WATCHDOG

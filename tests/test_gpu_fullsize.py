@@ -100,3 +100,54 @@ def test_l1_fullsize_matches_fp32_reference(l1_case, P, packed):
     finally:
         eng.close()
         grp.close()
+
+
+# ---- BASELINE configs[4] shape (Q8: 64 q / 8 kv heads, d=128, hidden 5120 != Hq*d, I=25600, V=151936) at a
+# reduced N on one GPU, with SP=8 through the loopback ranks (r=1) and a kv-replication variant (Hkv=2,
+# SP=8 -> r=4), checked against the same fp32 reference.
+Q8_KV2 = S.ModelShape(5120, 64, 2, 128, 25600, 151936)
+
+
+@pytest.fixture(scope="module")
+def q8_case():
+    T = torch()
+    from tests import torch_ref as R
+
+    out = {}
+    for name, shape in (("q8", S.QWEN32B), ("q8_kv2", Q8_KV2)):
+        params, x, lab, pos = _synth(shape, 8192, False, seed=23)
+        T.backends.cuda.matmul.allow_tf32 = False
+        ref = R.layer_step({k: v.float() for k, v in params.items()}, x.float(), lab, None, shape.q_heads,
+                           shape.kv_heads, shape.head_dim)
+        out[name] = (shape, params, x, lab, ref)
+        T.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.parametrize("name,P", [("q8", 1), ("q8", 8), ("q8_kv2", 8)])
+def test_q8_shape_matches_fp32_reference(q8_case, name, P):
+    T = torch()
+    shape, params, x, lab, (rloss, rcnt, rgrads, rdx) = q8_case[name]
+    N = x.shape[0]
+    plan = S.plan_head_shards(shape.q_heads, shape.kv_heads, P)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(shape, N, grp)
+    try:
+        for k in S.PARAM_NAMES:
+            eng.set_param(k, params[k])
+        loss, cnt = eng.step(x, lab)
+        assert cnt == rcnt
+        errs = {"loss": abs(loss - rloss) / abs(rloss)}
+        assert errs["loss"] <= LOSS_TOL, (loss, rloss)
+        for k in S.PARAM_NAMES:
+            gk = T.from_numpy(eng.grad(k)).cuda()
+            errs[k] = _rel(gk, rgrads[k])
+            assert errs[k] <= GRAD_TOL, (k, errs[k])
+            del gk
+        dx = T.from_numpy(eng.dx_bits(N).view("int16")).cuda().view(T.bfloat16).float()
+        errs["dx"] = _rel(dx, rdx)
+        print(f"\n{name} P={P} kv_replication={plan.kv_replication} " + " ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+        assert errs["dx"] <= GRAD_TOL
+    finally:
+        eng.close()
+        grp.close()
