@@ -581,7 +581,8 @@ static void attn_fwd_t(const void* qkv, int64_t s, int hq, int hkv, const int32_
 }
 
 bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* Dv, int64_t s, int hq, int hkv,
-                 int d, const int32_t* seg, float scale, void* dqkv, cudaStream_t st);
+                 int d, const int32_t* seg, float scale, void* dqkv, void* ws, cudaStream_t st);
+size_t attn_bwd_tc_workspace(int64_t s, int hq);
 static int attn_impl();
 
 template <int D>
@@ -593,7 +594,7 @@ static void attn_bwd_t(const void* qkv, const void* o, const float* lse, const v
         (const bf16*)o, (const bf16*)dout, lse, s, hq, Dv, lse2);
     count_launch();
     SPT_CUDA(cudaGetLastError());
-    if (attn_impl() == 1 && attn_bwd_tc(qkv, dout, lse2, Dv, s, hq, hkv, D, seg, scale, dqkv, st)) return;
+    if (attn_impl() == 1 && attn_bwd_tc(qkv, dout, lse2, Dv, s, hq, hkv, D, seg, scale, dqkv, lse2 + s * hq, st)) return;
     {
         constexpr int smem = (2 * 128 + 4 * 64) * D * 2 + 4 * 64 * 4;
         auto k = fa::bwd_dkdv_kernel<D>;
@@ -650,8 +651,9 @@ void attn_fwd(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t*
 
 size_t attn_bwd_workspace(int64_t s, int hq, int hkv, int d) {
     (void)hkv;
-    (void)d;
-    return (size_t)s * hq * 4 * 2;  // D = rowsum(dO*O) and lse*log2(e)
+    // D = rowsum(dO*O) and lse*log2(e), then (head_dim 128, tcgen05 path) the fp32 dQ accumulator and the
+    // dQ ordering counters of the fused backward
+    return (size_t)s * hq * 4 * 2 + (d == 128 ? attn_bwd_tc_workspace(s, hq) : 0);
 }
 
 void attn_bwd(const void* qkv, const void* o, const float* lse, const void* dout, int64_t s, int hq, int hkv, int d,

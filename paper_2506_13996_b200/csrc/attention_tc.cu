@@ -7,6 +7,7 @@
 // score columns and is the A operand of the PV MMA) or into swizzled smem (backward).  Online softmax
 // uses a lazy rescale: O is only rescaled in TMEM when the running max grows by > 2^8.
 #include <algorithm>
+#include <string>
 #include <type_traits>
 
 #include "common.h"
@@ -848,6 +849,412 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
 }
 
+
+// ------------------------------------------------------------------ fused dK / dV / dQ pass
+// One KV-outer pass computes all three gradients (5 matmuls per tile instead of the 7 of the two-pass
+// scheme): on top of the dK/dV pass above, each iteration also forms dQ^T_partial = K^T dS^T (M = d,
+// N = 64 queries, K = 128 keys) into the consumed dP^T columns of its TMEM buffer, with dS^T staged in
+// swizzled smem as the MN-major B operand.  Four drain warps read dQ^T_partial out of TMEM, transpose it
+// through smem into [q][d] rows and add it into an fp32 dQ accumulator in global memory with bulk
+// reductions (cp.reduce.async.bulk .add.f32).
+//
+// Determinism: the contributions to a (q head, 64-query block) are added in a FIXED order —
+// descending key block, i.e. the diagonal block first — enforced by a per-(head, q block) counter: key
+// block kb adds only after the (j/2 - kb) key blocks above it have published theirs (acquire / release
+// at gpu scope).  CTAs are launched in descending key-block order, so every CTA kb waits only on CTA
+// kb + 1, which was launched earlier (no deadlock); and since CTA kb + 1 reaches any (head, q block) at
+// least two iterations before CTA kb does, the waits are normally already satisfied.  Publication of an
+// iteration is deferred by one iteration (bulk-group completion is waited one group behind), which keeps
+// the drain warps off the L2 round-trip latency.
+namespace dkvq {
+constexpr int BQB = 64;
+constexpr int KB_BYTES = 128 * D * 2;                                // K or V block, 32 KiB
+constexpr int QS_BYTES = BQB * D * 2;                                // Q or dO tile, 16 KiB
+constexpr int NQS = 3;                                               // Q/dO ring stages
+constexpr int DS_BYTES = 128 * BQB * 2;                              // dS^T [128 keys][64 q] bf16, 16 KiB
+constexpr int STG_BYTES = 32 * D * 4;                                // dQ staging half: 32 rows x 512 B
+constexpr int OFF_K = 0, OFF_V = KB_BYTES, OFF_QS = 2 * KB_BYTES;    // NQS stages x (Q, dO)
+constexpr int OFF_DS = OFF_QS + NQS * 2 * QS_BYTES;
+constexpr int OFF_STG = OFF_DS + DS_BYTES;                           // 2 staging halves
+constexpr int OFF_LD = OFF_STG + 2 * STG_BYTES;                      // NQS x (lse*log2e[64], D[64]) fp32
+constexpr int OFF_BAR = OFF_LD + NQS * 512;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr int NDRAIN = 4;                                            // drain warps
+constexpr int THREADS = (BW_NEW + 2 + NDRAIN) * 32;
+constexpr int W_DRAIN0 = BW_NEW + 2;
+static_assert(SMEM <= 232448, "dkvq smem");
+}  // namespace dkvq
+
+__device__ __forceinline__ void bulk_reduce_add_f32(float* g, uint32_t saddr, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(g), "r"(saddr),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void drain_bar() { asm volatile("bar.sync 1, %0;" ::"n"(dkvq::NDRAIN * 32) : "memory"); }
+
+__global__ void __launch_bounds__(dkvq::THREADS, 1)
+    dkdvq_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
+                    const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
+                    const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv,
+                    const __grid_constant__ CUtensorMap tdq, int* __restrict__ dq_cnt) {
+    using namespace dkvq;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* kv_full = bar;
+    uint64_t* qs_full = bar + 1;          // [NQS]
+    uint64_t* qs_empty = qs_full + NQS;   // [NQS]
+    uint64_t* s_full = qs_empty + NQS;    // [2]
+    uint64_t* pd_full = s_full + 2;       // [2]
+    uint64_t* dq_full = pd_full + 2;      // [2]
+    uint64_t* dq_drained = dq_full + 2;   // [2]
+    uint64_t* ds_free = dq_drained + 2;   // dS^T smem consumed by the dQ MMA
+    uint64_t* acc_done = ds_free + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+    const int warp = warp_id(), lane = lane_id();
+    const int nkb = (int)(s / 128);
+    const int kb = nkb - 1 - (int)blockIdx.y;  // DESCENDING key blocks (dQ ordering, see above)
+    const int kvh = blockIdx.x;
+    const int grp = hq / hkv;
+    const int64_t k0 = (int64_t)kb * 128;
+    const int nqb_all = (int)(s / BQB);
+    const int qb_first = (int)(k0 / BQB);
+    int qb_last = nqb_all - 1;
+    if (seg) {
+        const int64_t klast = k0 + 127;
+        int64_t lo = k0, hi = s - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (seg[mid] <= klast) lo = mid;
+            else hi = mid - 1;
+        }
+        qb_last = (int)(lo / BQB);
+    }
+    const int nqb = qb_last - qb_first + 1;
+    const int total = nqb * grp;
+    if (threadIdx.x == 0) {
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < NQS; ++i) {
+            mbar_init(&qs_full[i], 1);
+            mbar_init(&qs_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&pd_full[i], BW_NEW * 32);
+            mbar_init(&dq_full[i], 1);
+            mbar_init(&dq_drained[i], NDRAIN * 32);
+        }
+        mbar_init(ds_free, 1);
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == BW_MMA) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t sbase = smem_u32(smem);
+    if (warp == BW_TMA) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(kv_full, 2 * KB_BYTES);
+            for (int r = 0; r < 2; ++r) {
+                tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
+                tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
+            }
+            int hh = kvh * grp, qblk = 0;
+            for (int it = 0; it < total; ++it) {
+                const int st = it % NQS;
+                mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES + 512);
+                const int qq = (qb_first + qblk) * BQB;
+                const int hcur = hh;
+                if (++qblk == nqb) { qblk = 0; ++hh; }
+                uint8_t* base = smem + OFF_QS + st * 2 * QS_BYTES;
+                for (int r = 0; r < 2; ++r) {
+                    tma_load_2d(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq);
+                    tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq);
+                }
+                bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st]);
+                bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st]);
+            }
+        }
+    } else if (warp == BW_MMA) {
+        constexpr uint32_t id_s = make_idesc_bf16(128, BQB, false, false);
+        constexpr uint32_t id_a = make_idesc_bf16(128, D, false, true);
+        constexpr uint32_t id_q = make_idesc_bf16(128, BQB, true, true);  // dQ^T = K^T dS^T: both MN-major
+        mbar_wait(kv_full, 0);
+        const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V, dsa = sbase + OFF_DS;
+        auto issue_sdp = [&](int it) {
+            const int st = it % NQS;
+            mbar_wait(&qs_full[st], (it / NQS) & 1);
+            tc_fence_after();
+            const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+            const uint32_t d_s = tmem + (it & 1) * 128;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+                mma_bf16_ss_w(d_s, kdesc_r(ka, kk, 16384), kdesc_r(qb_, kk, 8192), id_s, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+                mma_bf16_ss_w(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
+            mma_commit_w(&s_full[it & 1]);
+        };
+        auto issue_acc = [&](int it) {
+            const int b = it & 1, st = it % NQS;
+            mbar_wait(&pd_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+            // dQ^T_partial[d][q] = sum_key K[key][d] dS^T[key][q] -> the dP^T columns of buffer b.  Issued
+            // first so the drain warps read it out of TMEM while dV / dK execute (no bubble before the
+            // next score MMAs into this buffer)
+#pragma unroll
+            for (int kk = 0; kk < 128 / 16; ++kk)
+                mma_bf16_ss_w(tmem + b * 128 + 64, mndesc_r(ka, kk, 16384), mndesc_r(dsa, kk, 16384), id_q, kk > 0);
+            mma_commit_w(&dq_full[b]);
+            mma_commit_w(ds_free);
+#pragma unroll
+            for (int kk = 0; kk < BQB / 16; ++kk)
+                mma_bf16_ts_w(tmem + 256, tmem + b * 128 + kk * 16, mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
+#pragma unroll
+            for (int kk = 0; kk < BQB / 16; ++kk)
+                mma_bf16_ts_w(tmem + 384, tmem + b * 128 + kk * 16 + 8, mndesc_r(qb_, kk, 8192), id_a,
+                              (it > 0 || kk > 0));
+            mma_commit_w(&qs_empty[st]);
+        };
+        if (total > 0) issue_sdp(0);
+        if (total > 1) issue_sdp(1);
+        for (int it = 0; it < total; ++it) {
+            issue_acc(it);
+            if (it + 2 < total) {
+                mbar_wait(&dq_drained[it & 1], (it >> 1) & 1);  // buffer's dQ^T read out of TMEM
+                tc_fence_after();
+                issue_sdp(it + 2);
+            }
+        }
+        mma_commit_w(acc_done);
+    } else if (warp >= W_DRAIN0) {
+        // ---- drain: dQ^T_partial (TMEM lane = d) -> smem rows [q][d] -> ordered bulk add into dq_acc
+        const int dw = warp & 3;  // TMEM lane quarter this warp may access (warp id mod 4)
+        const int d = dw * 32 + lane;
+        const uint32_t lo = (uint32_t)(dw * 32) << 16;
+        const bool leader = threadIdx.x == W_DRAIN0 * 32;
+        int hh = kvh * grp, qblk = 0;
+        int prev_cnt_idx = -1;
+        for (int it = 0; it < total; ++it) {
+            const int b = it & 1;
+            const int jq = qb_first + qblk;
+            const int hcur = hh;
+            if (++qblk == nqb) { qblk = 0; ++hh; }
+            mbar_wait(&dq_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t v[64];
+            tmem_ld32(tmem + lo + b * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+            tmem_ld32(tmem + lo + b * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&dq_drained[b]);
+            const int cnt_idx = hcur * nqb_all + jq;
+#ifdef SPT_EXP_NO_DQRED
+            continue;  // experiment: drain TMEM only (no global dQ accumulation)
+#endif
+            for (int hf = 0; hf < 2; ++hf) {
+                if (leader) bulk_wait_read<1>();  // this half's previous bulk group finished reading smem
+                drain_bar();
+                const uint32_t stg = sbase + OFF_STG + hf * STG_BYTES;
+#pragma unroll
+                for (int r = 0; r < 32; ++r)
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg + r * 512 + d * 4), "f"(__uint_as_float(v[hf * 32 + r]))
+                                 : "memory");
+                fence_proxy_async();
+                drain_bar();
+                if (leader) {
+#ifndef SPT_EXP_NO_DQORDER
+                    if (hf == 0) {
+#else
+                    if (false) {  // experiment: unordered (non-deterministic) accumulation
+#endif
+                        const int need = (jq >> 1) - kb;  // key blocks above this one, all added first
+                        if (ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
+                            const long long t0 = clock64();
+                            while (ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
+                                // ordering bug or lost CTA: fail loudly instead of hanging the device (~20 s)
+                                if (clock64() - t0 > (1ll << 35)) {
+                                    printf("[spt] dQ ordering wait timed out: kb %d head %d qblock %d need %d\n", kb,
+                                           hcur, jq, need);
+                                    __trap();
+                                }
+                            }
+                        }
+                    }
+                    // one TMA tensor reduction: box {d 128, head 1, q 32} of dq_acc[q][head][d] += staging
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                            &tdq),
+                        "r"(0), "r"(hcur), "r"(jq * BQB + hf * 32), "r"(stg)
+                        : "memory");
+                    bulk_commit();
+                }
+            }
+            if (leader) {
+                // publish the PREVIOUS iteration: its two bulk groups are complete once at most the two
+                // groups of this iteration remain in flight
+                if (prev_cnt_idx >= 0) {
+                    bulk_wait<2>();
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
+                }
+                prev_cnt_idx = cnt_idx;
+            }
+        }
+        if (leader && prev_cnt_idx >= 0) {
+            bulk_wait<0>();
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
+        }
+    } else {
+        // elementwise: warp w: TMEM lanes (w&3)*32.., q columns [16g, 16g+16) with g = w>>2
+        const int sub = warp & 3, grp4 = warp >> 2;
+        const int r = sub * 32 + lane;  // key row
+        const int64_t key = k0 + r;
+        const int key32 = (int)key;
+        const uint32_t lo = (uint32_t)(sub * 32) << 16;
+        const float sl2 = scale * LOG2E;
+        // dS^T smem row r: MN-major SW128 (64 q per 128 B row, 8-row atoms of 1 KiB); 16-byte chunks
+        // 2*grp4 and 2*grp4+1 of this row, XOR-swizzled by (r & 7)
+        const uint32_t ds_row = sbase + OFF_DS + (r >> 3) * 1024 + (r & 7) * 128;
+        const uint32_t ds_c0 = ds_row + ((((uint32_t)(2 * grp4)) ^ (r & 7)) << 4);
+        const uint32_t ds_c1 = ds_row + ((((uint32_t)(2 * grp4 + 1)) ^ (r & 7)) << 4);
+        int qblk = 0;
+        for (int it = 0; it < total; ++it) {
+            const int b = it & 1;
+            const int qq = (qb_first + qblk) * BQB + grp4 * 16;
+            if (++qblk == nqb) qblk = 0;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t sv[16], dv[16];
+            tmem_ld16(tmem + lo + b * 128 + grp4 * 16, sv);
+            tmem_ld16(tmem + lo + b * 128 + 64 + grp4 * 16, dv);
+            tmem_ld_wait();
+            const uint32_t lsm = sbase + OFF_LD + (it % NQS) * 512 + grp4 * 64;
+            uint32_t pw[8], sw[8];
+            auto body = [&](auto mask_c) {
+                constexpr bool MASK = decltype(mask_c)::value;
+                const int lo_ = key32 - qq;
+                const uint64_t sl2x = f2pack(sl2, sl2);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float lv[8], dd[8];
+                    lds128(lsm + 32 * k, lv[0], lv[1], lv[2], lv[3]);
+                    lds128(lsm + 32 * k + 16, lv[4], lv[5], lv[6], lv[7]);
+                    lds128(lsm + 256 + 32 * k, dd[0], dd[1], dd[2], dd[3]);
+                    lds128(lsm + 256 + 32 * k + 16, dd[4], dd[5], dd[6], dd[7]);
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int i = 8 * k + e;
+                        float x0, x1;
+                        f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sl2x,
+                                       f2pack(-lv[e], -lv[e + 1])),
+                                 x0, x1);
+                        float p0 = ex2(x0), p1 = ex2(x1);
+                        if constexpr (MASK) {
+                            if (i < lo_ || (seg && key32 < seg[qq + i])) p0 = 0.f;
+                            if (i + 1 < lo_ || (seg && key32 < seg[qq + i + 1])) p1 = 0.f;
+                        }
+                        const uint64_t ds = fmul2(f2pack(p0, p1), fsub2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
+                                                                        f2pack(dd[e], dd[e + 1])));
+                        float s0, s1;
+                        f2unpack(ds, s0, s1);
+                        pw[4 * k + e / 2] = pack_bf16x2(p0, p1);
+                        sw[4 * k + e / 2] = pack_bf16x2(s0, s1);
+                    }
+                }
+            };
+            if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
+            else body(std::false_type{});
+            tmem_st8(tmem + lo + b * 128 + grp4 * 16, pw);
+            tmem_st8(tmem + lo + b * 128 + grp4 * 16 + 8, sw);
+            // dS^T -> smem (B operand of the dQ MMA) once the previous iteration's dQ MMA has read it
+            if (it > 0) mbar_wait(ds_free, (it - 1) & 1);
+            sts128(ds_c0, sw[0], sw[1], sw[2], sw[3]);
+            sts128(ds_c1, sw[4], sw[5], sw[6], sw[7]);
+            fence_proxy_async();
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&pd_full[b]);
+        }
+        // epilogue: column groups 0,1 write dV, 2,3 write dK (scaled); 64 columns each
+        mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const int64_t rs = (int64_t)(hq + 2 * hkv) * D;
+        const bool isk = grp4 >= 2;
+        const int c0 = (grp4 & 1) * 64;
+        bf16* dst = dqkv + key * rs + (int64_t)(isk ? (hq + kvh) : (hq + hkv + kvh)) * D + c0;
+        const float mul = isk ? scale : 1.f;
+        const uint32_t acc_tm = tmem + lo + (isk ? 384 : 256) + c0;
+        if (total == 0) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            for (int k = 0; k < 8; ++k) d4[k] = make_uint4(0, 0, 0, 0);
+        } else {
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                uint32_t v[32];
+                tmem_ld32(acc_tm + c * 32, v);
+                tmem_ld_wait();
+                uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint4 w;
+                    w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+                    w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+                    w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+                    w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+                    d4[k] = w;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == BW_MMA) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// dq (bf16, inside dqkv) = dq_acc * scale
+__global__ void dq_convert_kernel(const float* __restrict__ acc, int64_t s, int hq, int hkv, float scale,
+                                  bf16* __restrict__ dqkv) {
+    const int64_t n8 = s * hq * (D / 8);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / (D / 8), c = (i % (D / 8)) * 8;  // row = q * hq + h
+        const int64_t q = row / hq, h = row % hq;
+        const float4 a = reinterpret_cast<const float4*>(acc + row * D + c)[0];
+        const float4 b = reinterpret_cast<const float4*>(acc + row * D + c)[1];
+        uint4 w;
+        w.x = pack_bf16x2(a.x * scale, a.y * scale);
+        w.y = pack_bf16x2(a.z * scale, a.w * scale);
+        w.z = pack_bf16x2(b.x * scale, b.y * scale);
+        w.w = pack_bf16x2(b.z * scale, b.w * scale);
+        *reinterpret_cast<uint4*>(dqkv + (q * (hq + 2 * hkv) + h) * D + c) = w;
+    }
+}
+
 }  // namespace fatc
 
 bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
@@ -869,9 +1276,29 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
     return true;
 }
 
+// Backward scheme.  Default: two passes (dK/dV KV-outer + dQ Q-outer, 7 matmuls per tile, no global
+// accumulation).  SPT_ATTN_BWD=fused selects the single KV-outer pass with ordered fp32 dQ reductions
+// (5 matmuls): its compute alone runs at 20.8 ms (1059 TF/s) at s=32K, but the 69 GB of fp32 dQ
+// reductions it sends through L2 (32 KiB per 128x64 tile pair) run at ~1.5 TB/s, so the pass takes
+// 52.5 ms against 24.0 ms for the two-pass scheme (profiles/README.md).  Kept for larger tiles / GPUs with
+// faster L2 reductions.
+static int bwd_mode() {
+    static const int v = [] {
+        const char* e = getenv("SPT_ATTN_BWD");
+        return (e && std::string(e) == "fused") ? 1 : 0;
+    }();
+    return v;
+}
+
+size_t attn_bwd_tc_workspace(int64_t s, int hq) {
+    if (bwd_mode() != 1) return 0;
+    return (size_t)s * hq * fatc::D * 4 + (size_t)hq * (s / 64) * 4 + 256;
+}
+
 // Deterministic tcgen05 backward (d = 128, s % 256 == 0).  Dv = rowsum(dO * O) must be precomputed.
+// ws: attn_bwd_tc_workspace bytes (fp32 dQ accumulator + per-(head, q block) ordering counters).
 bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const float* Dv, int64_t s, int hq, int hkv,
-                 int d, const int32_t* seg, float scale, void* dqkv, cudaStream_t st) {
+                 int d, const int32_t* seg, float scale, void* dqkv, void* ws, cudaStream_t st) {
     if (d != fatc::D || s % 256 != 0 || s >= (int64_t(1) << 31) - 256) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap t128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
@@ -883,7 +1310,24 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::dq::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdvq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dkvq::SMEM));
         attr = true;
+    }
+    if (bwd_mode() == 1 && ws != nullptr && attn_bwd_tc_workspace(s, hq) > 0) {
+        float* dq_acc = (float*)ws;
+        int* cnt = (int*)(dq_acc + (size_t)s * hq * fatc::D);
+        SPT_CUDA(cudaMemsetAsync(ws, 0, attn_bwd_tc_workspace(s, hq), st));
+        CUtensorMap tdq = make_tmap_f32_3d(dq_acc, fatc::D, (uint64_t)hq, (uint64_t)s, (uint64_t)fatc::D * 4,
+                                           (uint64_t)hq * fatc::D * 4, fatc::D, 1, 32);
+        fatc::dkdvq_tc_kernel<<<dim3((unsigned)hkv, (unsigned)(s / 128)), fatc::dkvq::THREADS, fatc::dkvq::SMEM, st>>>(
+            t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, tdq, cnt);
+        count_launch("attn_dkdvq_tc");
+        SPT_CUDA(cudaGetLastError());
+        fatc::dq_convert_kernel<<<148 * 8, 256, 0, st>>>(dq_acc, s, hq, hkv, scale, (bf16*)dqkv);
+        count_launch("attn_dq_convert");
+        SPT_CUDA(cudaGetLastError());
+        return true;
     }
     fatc::dkdv_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM, st>>>(
         t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);

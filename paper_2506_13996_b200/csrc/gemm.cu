@@ -44,6 +44,21 @@ CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t inner, uint64_t outer, u
     return m;
 }
 
+CUtensorMap make_tmap_f32_3d(const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                             uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+    cuuint32_t box[3] = {b0, b1, b2};
+    cuuint32_t es[3] = {1, 1, 1};
+    SPT_CHECK((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, SPT_ERR_SHAPE, "TMA base must be 16-byte aligned");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SPT_CHECK(r == CUDA_SUCCESS, SPT_ERR_CUDA, "cuTensorMapEncodeTiled (f32 3d) failed: " + std::to_string((int)r));
+    return m;
+}
+
 template <int BN, bool A_MN, bool B_MN, int KIND>
 static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep,
                         cudaStream_t st) {

@@ -19,6 +19,9 @@ struct GemmOperand {
 void count_launch(const char* tag = nullptr);
 int64_t launch_count();
 
+// 3-D fp32 tensor map (no swizzle): dims {d0, d1, d2} innermost first, byte strides of dims 1 and 2.
+CUtensorMap make_tmap_f32_3d(const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                             uint64_t stride2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                               uint32_t box_outer);
 

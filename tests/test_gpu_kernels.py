@@ -307,3 +307,18 @@ def test_tiled_mlp(n, h, I, tile):
     assert rel_err(dwg, dwg_r) < 2e-2
     assert rel_err(dwu, dwu_r) < 2e-2
     assert rel_err(to_np(dwd), dwd_r) < 2e-2
+
+
+@pytest.mark.parametrize("s,hq,hkv,packed", [(1024, 4, 1, False), (2048, 8, 2, True), (512, 2, 2, False)])
+def test_attention_bwd_fused_scheme(s, hq, hkv, packed):
+    """The opt-in single-pass backward (SPT_ATTN_BWD=fused: ordered fp32 dQ reductions) matches the oracle
+    and is bitwise deterministic.  Run in a subprocess because the scheme is fixed per process."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPT_ATTN_BWD="fused")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "fused_bwd_case.py"), str(s), str(hq), str(hkv),
+                        "1" if packed else "0"], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
