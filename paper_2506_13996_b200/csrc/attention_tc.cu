@@ -1113,7 +1113,11 @@ __global__ void __launch_bounds__(dkvq::THREADS, 1)
             if (leader) {
                 // publish the PREVIOUS iteration: its two bulk groups are complete once at most the two
                 // groups of this iteration remain in flight
+#ifdef SPT_EXP_NO_DQWAIT
+                if (false) {  // experiment: never wait for reduction completion inside the loop
+#else
                 if (prev_cnt_idx >= 0) {
+#endif
                     bulk_wait<2>();
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
@@ -1279,9 +1283,10 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
 // Backward scheme.  Default: two passes (dK/dV KV-outer + dQ Q-outer, 7 matmuls per tile, no global
 // accumulation).  SPT_ATTN_BWD=fused selects the single KV-outer pass with ordered fp32 dQ reductions
 // (5 matmuls): its compute alone runs at 20.8 ms (1059 TF/s) at s=32K, but the 69 GB of fp32 dQ
-// reductions it sends through L2 (32 KiB per 128x64 tile pair) run at ~1.5 TB/s, so the pass takes
-// 52.5 ms against 24.0 ms for the two-pass scheme (profiles/README.md).  Kept for larger tiles / GPUs with
-// faster L2 reductions.
+// reductions it sends through L2 (32 KiB per 128x64 tile pair) make the pass take 52.5 ms against 24.0 ms
+// for the two-pass scheme (profiles/README.md).  Experiments: unordered 47.3 ms; unordered and never
+// waiting for reduction completion 31.9 ms, i.e. the reductions alone sustain only ~2.2 TB/s.  Kept for
+// larger tiles (fewer reduction bytes per flop) / GPUs with faster L2 reductions.
 static int bwd_mode() {
     static const int v = [] {
         const char* e = getenv("SPT_ATTN_BWD");
