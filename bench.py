@@ -28,8 +28,10 @@ SHAPE = dict(hidden=4096, q_heads=32, kv_heads=8, head_dim=128, intermediate=143
 CPU_SAMPLE_TOKENS = 256
 
 
-def workload_name(seq, n):
-    return (f"llama3-8b-shape layer + lm_head (h4096, 32q/8kv d128, I14336, V128256), "
+def workload_name(seq, n, layers=1, offload=False):
+    stack = "layer" if layers == 1 and not offload else (
+        f"{layers}-layer stack (activation checkpoints {'offloaded to host' if offload else 'on device'})")
+    return (f"llama3-8b-shape {stack} + lm_head (h4096, 32q/8kv d128, I14336, V128256), "
             f"seq {seq} over {n} GPU(s), Ulysses SP={n}, TiledMLP + tiled logits/CE")
 
 
@@ -154,15 +156,18 @@ def run_ours(args, rank, world, local_rank):
     seq = args.seq_per_gpu * world
     n_loc = args.seq_per_gpu
     shp = S.ModelShape(**SHAPE)
-    eng = S.UlyssesLayerStep(shp, seq, grp, lr=args.lr)
+    eng = S.UlyssesLayerStep(shp, seq, grp, lr=args.lr, n_layers=args.layers, ckpt_offload=args.offload)
     # random-init weights of the architecture, identical on every rank (same seed)
     g = torch.Generator(device=dev).manual_seed(1234)
     qkv_out = (shp.q_heads + 2 * shp.kv_heads) * shp.head_dim
     wshapes = {"g1": (shp.hidden,), "wqkv": (qkv_out, shp.hidden), "wo": (shp.hidden, shp.q_heads * shp.head_dim),
                "g2": (shp.hidden,), "wg": (shp.intermediate, shp.hidden), "wu": (shp.intermediate, shp.hidden),
                "wd": (shp.hidden, shp.intermediate), "g3": (shp.hidden,), "wlm": (shp.vocab, shp.hidden)}
-    for k, s_ in wshapes.items():
-        if k.startswith("g"):
+    names = [(k, s_) for k, s_ in wshapes.items() if k in ("g3", "wlm")]
+    for i in range(args.layers):
+        names += [(f"layers.{i}.{k}", s_) for k, s_ in wshapes.items() if k not in ("g3", "wlm")]
+    for k, s_ in names:
+        if k.split(".")[-1].startswith("g"):
             w = (1.0 + 0.05 * torch.randn(s_, device=dev, generator=g)).bfloat16()
         else:
             w = (0.02 * torch.randn(s_, device=dev, generator=g)).bfloat16()
@@ -289,10 +294,13 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": tokens / step_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) hidden, uniform labels)",
-        "config": {"workload": workload_name(seq, world), "seq_len": seq, "tokens_per_gpu": n_loc,
+        "config": {"workload": workload_name(seq, world, args.layers, args.offload), "seq_len": seq, "tokens_per_gpu": n_loc,
                    "sp_degree": world, "mlp_tile": mem["mlp_tile"], "loss_tile": mem["loss_tile"],
                    "l2": "inputs larger than L2 (x 256 MiB/GPU, weights 1.5 GiB, activations ~3 GiB per step)",
-                   "optimizer": f"sgd lr={args.lr}" if args.lr > 0 else "none (fwd+bwd+SP grad all-reduce)"},
+                   "optimizer": f"sgd lr={args.lr}" if args.lr > 0 else "none (fwd+bwd+SP grad all-reduce)",
+                   "n_layers": args.layers,
+                   "activation_checkpointing": ("offload to pinned host" if args.offload else
+                                                ("device" if args.layers > 1 else "none (single layer)"))},
         "peak_hbm_bytes": peak_b, "peak_hbm_bytes_per_token": peak_b / n_loc,
         "est_max_seq_per_gpu": est_max,
         "loss": loss, "valid_tokens": cnt,
@@ -320,6 +328,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lr", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers", type=int, default=1,
+                    help="decoder layers (> 1: per-layer activation checkpointing; not the BASELINE config)")
+    ap.add_argument("--offload", action="store_true", help="activation checkpoints in pinned host memory")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -172,12 +172,17 @@ typedef struct {
     float rms_eps;     /* 0 -> 1e-5 */
     int32_t packed;    /* 1: block-causal attention from position_ids */
     float lr;          /* >0: plain SGD update of the bf16 weights at the end of the step */
+    int32_t n_layers;  /* decoder layers (0 -> 1); > 1 turns on per-layer activation checkpointing
+                          (layer inputs saved, each layer re-run in backward) */
+    int32_t ckpt_offload; /* 1: checkpoints in pinned host memory, copied on a side stream
+                             (checkpoint_offload); implies checkpointing */
 } spt_layer_config;
 
 typedef struct spt_layer spt_layer;
 spt_status spt_layer_create(const spt_layer_config* cfg, spt_comm* comm, spt_layer** out);
 spt_status spt_layer_destroy(spt_layer* layer);
-/* name in {g1, wqkv, wo, g2, wg, wu, wd, g3, wlm}; data = bf16 bits in [out, in] row-major. */
+/* name in {g1, wqkv, wo, g2, wg, wu, wd, g3, wlm} (per-layer names address layer 0; "layers.<i>.<name>"
+ * addresses layer i); data = bf16 bits in [out, in] row-major. */
 spt_status spt_layer_set_param(spt_layer* layer, const char* name, const void* data, int32_t data_on_host);
 /* One fwd+bwd step.  x: bf16 [local_ranks * s_loc, hidden] (loopback: the whole sequence),
  * shift_labels / position_ids: int64 [local_ranks * s_loc] (already pre-shifted).

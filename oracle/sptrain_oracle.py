@@ -545,83 +545,61 @@ def synth_batch(cfg: LayerConfig, n: int, seed: int, ignore_frac: float = 0.05, 
     return x, shift, position_ids
 
 
-def layer_step(params: LayerParams, cfg: LayerConfig, x, shift_labels, position_ids=None, P: int = 1,
-               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False) -> StepResult:
-    """One SP=P training step (fwd+bwd) of the layer, as P in-process ranks.
-
-    Forward per rank (SPEC.md:205): x1 = x + Wo·ulysses_attention(Wqkv·rms(x)); x2 = x1 + tiled_mlp(rms(x1));
-    z = rms_final(x2); (loss_sum, count) = tiled_logits_loss(z).  Global mean loss via all_reduce
-    of (sum, count); weight grads all-reduced over the SP group.
-    """
-    p = params.astype(dtype)
-    x = np.asarray(x, dtype=dtype)
-    N, h = x.shape
+def decoder_layer_fwd(p, cfg: LayerConfig, xs: list, starts, P: int, mlp_tiles=None):
+    """One decoder layer forward over P in-process ranks: per rank
+    x1 = x + Wo·ulysses_attention(Wqkv·rms1(x)), x2 = x1 + tiled_mlp(rms2(x1)).  Returns (x2 per rank, cache)."""
     Hq, Hkv, d = cfg.q_heads, cfg.kv_heads, cfg.head_dim
     plan = plan_head_shards(Hq, Hkv, P)
-    if N % P:
-        raise ShapeError(f"N={N} not divisible by P={P}")
-    n_loc = N // P
-    if position_ids is None:
-        position_ids = np.arange(N, dtype=np.int64)
-    starts = block_causal_starts(position_ids)
-    loss_tile = n_loc if loss_tile is None else loss_tile
-    xs = shard_sequence(x, P)
-    labs = shard_sequence(np.asarray(shift_labels, np.int64), P)
-
-    # ---- forward, phase A: norm + qkv projection per rank
-    st = [dict() for _ in range(P)]
-    for r in range(P):
+    n_loc = xs[0].shape[0]
+    st = [dict(x=xs[r]) for r in range(P)]
+    for r in range(P):  # phase A: norm + qkv projection per rank
         xn1, rstd1 = rmsnorm_fwd(xs[r], p.g1)
         qkv = xn1 @ p.wqkv.T
         q = qkv[:, :Hq * d].reshape(n_loc, Hq, d)
         k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(n_loc, Hkv, d)
         v = qkv[:, (Hq + Hkv) * d:].reshape(n_loc, Hkv, d)
         st[r].update(xn1=xn1, rstd1=rstd1, q=q, k=k, v=v)
-    # ---- seq -> head all-to-all (SPEC.md:307)
+    # seq -> head all-to-all (SPEC.md:307), inner attention over the full sequence, head -> seq (SPEC.md:317)
     qh = seq_to_head([s_["q"] for s_ in st], plan.q_heads_of)
     kh = seq_to_head([s_["k"] for s_ in st], plan.kv_heads_of)
     vh = seq_to_head([s_["v"] for s_ in st], plan.kv_heads_of)
-    # ---- inner attention on full sequence, local heads
     oh, lse = [], []
     for j in range(P):
         o_, l_ = attention_fwd(qh[j], kh[j], vh[j], starts)
         oh.append(o_)
         lse.append(l_)
-    # ---- head -> seq (SPEC.md:317)
     os_ = head_to_seq(oh, plan.q_heads_of, Hq)
     for r in range(P):
         o = os_[r].reshape(n_loc, Hq * d)
         x1 = xs[r] + o @ p.wo.T
         xn2, rstd2 = rmsnorm_fwd(x1, p.g2)
         x2 = x1 + tiled_mlp(xn2, p.wg, p.wu, p.wd, mlp_tiles)
-        z, rstd3 = rmsnorm_fwd(x2, p.g3)
-        st[r].update(o=o, x1=x1, xn2=xn2, rstd2=rstd2, x2=x2, z=z, rstd3=rstd3)
-    # ---- global (sum, count) via all-reduce (SPEC.md:424), then grads of mean loss
-    counts = [int(np.sum(l_ != IGNORE_INDEX)) for l_ in labs]
-    count = all_reduce_sum([np.array([c], np.int64) for c in counts])[0][0]
-    scale = 1.0 / count if count > 0 else 0.0
-    sums = []
-    for r in range(P):
-        ls, cnt, dz, dwlm = tiled_logits_loss(st[r]["z"], p.wlm, labs[r], loss_tile, grad_scale=scale)
-        sums.append(np.array([ls], dtype))
-        st[r].update(dz=dz, dwlm=dwlm)
-    loss_sum = float(all_reduce_sum(sums)[0][0])
-    # ---- backward per rank up to the attention output
+        st[r].update(o=o, x1=x1, xn2=xn2, rstd2=rstd2, x2=x2)
+    cache = dict(st=st, qh=qh, kh=kh, vh=vh, oh=oh, lse=lse, plan=plan, starts=starts, mlp_tiles=mlp_tiles)
+    return [s_["x2"] for s_ in st], cache
+
+
+def decoder_layer_bwd(p, cfg: LayerConfig, cache: dict, dys: list, P: int):
+    """Backward of decoder_layer_fwd: d(layer output) per rank -> (d(layer input) per rank, per-rank grads)."""
+    Hq, Hkv, d = cfg.q_heads, cfg.kv_heads, cfg.head_dim
+    st, plan, starts, mlp_tiles = cache["st"], cache["plan"], cache["starts"], cache["mlp_tiles"]
+    n_loc = st[0]["x"].shape[0]
     grads = [dict() for _ in range(P)]
     for r in range(P):
         s_ = st[r]
-        dx2, dg3 = rmsnorm_bwd(s_["x2"], p.g3, s_["rstd3"], s_["dz"])
+        dx2 = dys[r]
         dxn2, dwg, dwu, dwd = tiled_mlp_bwd(s_["xn2"], p.wg, p.wu, p.wd, dx2, mlp_tiles)
         dx1n, dg2 = rmsnorm_bwd(s_["x1"], p.g2, s_["rstd2"], dxn2)
         dx1 = dx2 + dx1n
         do = (dx1 @ p.wo).reshape(n_loc, Hq, d)
         dwo = dx1.T @ s_["o"]
-        grads[r].update(g3=dg3, wg=dwg, wu=dwu, wd=dwd, g2=dg2, wo=dwo, wlm=s_["dwlm"])
+        grads[r].update(wg=dwg, wu=dwu, wd=dwd, g2=dg2, wo=dwo)
         s_.update(dx1=dx1, do=do)
     doh = seq_to_head([s_["do"] for s_ in st], plan.q_heads_of)
     dqh, dkh, dvh = [], [], []
     for j in range(P):
-        a, b, c = attention_bwd(qh[j], kh[j], vh[j], oh[j], lse[j], doh[j], starts)
+        a, b, c = attention_bwd(cache["qh"][j], cache["kh"][j], cache["vh"][j], cache["oh"][j], cache["lse"][j], doh[j],
+                                starts)
         dqh.append(a)
         dkh.append(b)
         dvh.append(c)
@@ -634,15 +612,81 @@ def layer_step(params: LayerParams, cfg: LayerConfig, x, shift_labels, position_
         dqkv = np.concatenate([dqs[r].reshape(n_loc, -1), dks[r].reshape(n_loc, -1), dvs[r].reshape(n_loc, -1)], axis=1)
         grads[r]["wqkv"] = dqkv.T @ s_["xn1"]
         dxn1 = dqkv @ p.wqkv
-        dx0n, dg1 = rmsnorm_bwd(xs[r], p.g1, s_["rstd1"], dxn1)
+        dx0n, dg1 = rmsnorm_bwd(s_["x"], p.g1, s_["rstd1"], dxn1)
         grads[r]["g1"] = dg1
         dxs.append(s_["dx1"] + dx0n)
-    # ---- SP-group weight-grad all-reduce, rank-ascending
-    out_grads = {k: all_reduce_sum([grads[r][k] for r in range(P)])[0] for k in LayerParams.NAMES}
-    res = StepResult(loss_sum=loss_sum, count=int(count), loss=loss_sum * scale,
-                     dx=np.concatenate(dxs, axis=0), grads=out_grads)
+    return dxs, grads
+
+
+LAYER_NAMES = ("g1", "wqkv", "wo", "g2", "wg", "wu", "wd")
+
+
+def model_step(layers: list, g3, wlm, cfg: LayerConfig, x, shift_labels, position_ids=None, P: int = 1,
+               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False) -> StepResult:
+    """One SP=P training step (fwd+bwd) of an L-layer decoder stack + final norm + lm_head as
+    P in-process ranks.  `layers` holds one dict / LayerParams-like object per layer with LAYER_NAMES.
+    Global mean loss via all_reduce of (sum, count); weight grads all-reduced over the SP group
+    (SPEC.md:353).  Activation checkpointing and offload do not change these values,
+    so this uncheckpointed restatement is the oracle for every checkpoint mode.
+    Grads are returned as {"layers.<i>.<name>": ..., "g3": ..., "wlm": ...} (plus bare names for layer 0)."""
+    def get(o, k):
+        return np.asarray(o[k] if isinstance(o, dict) else getattr(o, k), dtype=dtype)
+
+    ps = [type("LP", (), {k: get(lp, k) for k in LAYER_NAMES}) for lp in layers]
+    g3 = np.asarray(g3, dtype=dtype)
+    wlm = np.asarray(wlm, dtype=dtype)
+    x = np.asarray(x, dtype=dtype)
+    N, h = x.shape
+    if N % P:
+        raise ShapeError(f"N={N} not divisible by P={P}")
+    plan_head_shards(cfg.q_heads, cfg.kv_heads, P)  # validates the SP degree
+    n_loc = N // P
+    if position_ids is None:
+        position_ids = np.arange(N, dtype=np.int64)
+    starts = block_causal_starts(position_ids)
+    loss_tile = n_loc if loss_tile is None else loss_tile
+    xs = shard_sequence(x, P)
+    labs = shard_sequence(np.asarray(shift_labels, np.int64), P)
+    caches = []
+    for p in ps:
+        xs, cache = decoder_layer_fwd(p, cfg, xs, starts, P, mlp_tiles)
+        caches.append(cache)
+    # final norm + tiled logits/loss; global (sum, count) via all-reduce (SPEC.md:424)
+    counts = [int(np.sum(l_ != IGNORE_INDEX)) for l_ in labs]
+    count = all_reduce_sum([np.array([c], np.int64) for c in counts])[0][0]
+    scale = 1.0 / count if count > 0 else 0.0
+    sums, dys, zs, head_grads = [], [], [], []
+    for r in range(P):
+        z, rstd3 = rmsnorm_fwd(xs[r], g3)
+        ls, cnt, dz, dwlm = tiled_logits_loss(z, wlm, labs[r], loss_tile, grad_scale=scale)
+        sums.append(np.array([ls], dtype))
+        dx2, dg3 = rmsnorm_bwd(xs[r], g3, rstd3, dz)
+        dys.append(dx2)
+        zs.append(z)
+        head_grads.append(dict(g3=dg3, wlm=dwlm))
+    loss_sum = float(all_reduce_sum(sums)[0][0])
+    out_grads = {k: all_reduce_sum([head_grads[r][k] for r in range(P)])[0] for k in ("g3", "wlm")}
+    for i in range(len(ps) - 1, -1, -1):
+        dys, grads = decoder_layer_bwd(ps[i], cfg, caches[i], dys, P)
+        for k in LAYER_NAMES:  # SP-group weight-grad all-reduce, rank-ascending (SPEC.md:353, :158)
+            out_grads[f"layers.{i}.{k}"] = all_reduce_sum([grads[r][k] for r in range(P)])[0]
+    for k in LAYER_NAMES:
+        out_grads[k] = out_grads[f"layers.0.{k}"]
+    res = StepResult(loss_sum=loss_sum, count=int(count), loss=loss_sum * scale, dx=np.concatenate(dys, axis=0),
+                     grads=out_grads)
     if keep_out:
-        res.out_hidden = np.concatenate([s_["z"] for s_ in st], axis=0)
+        res.out_hidden = np.concatenate(zs, axis=0)
+    return res
+
+
+def layer_step(params: LayerParams, cfg: LayerConfig, x, shift_labels, position_ids=None, P: int = 1,
+               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False) -> StepResult:
+    """One SP=P training step (fwd+bwd) of ONE decoder layer + final norm + lm_head, as P in-process ranks:
+    model_step with a single layer.  Forward per rank (SPEC.md:205): x1 = x + Wo·ulysses_attention(Wqkv·rms(x));
+    x2 = x1 + tiled_mlp(rms(x1)); z = rms_final(x2); (loss_sum, count) = tiled_logits_loss(z)."""
+    p = params.astype(dtype)
+    res = model_step([p], p.g3, p.wlm, cfg, x, shift_labels, position_ids, P, mlp_tiles, loss_tile, dtype, keep_out)
+    res.grads = {k: res.grads[k] for k in LayerParams.NAMES}
     return res
 
 

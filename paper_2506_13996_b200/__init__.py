@@ -54,7 +54,8 @@ class HeadShardPlan(C.Structure):
 class LayerConfig(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("intermediate", C.c_int32), ("vocab", C.c_int64), ("seq_len", C.c_int64), ("mlp_tiles", C.c_int32),
-                ("loss_tile", C.c_int64), ("rms_eps", C.c_float), ("packed", C.c_int32), ("lr", C.c_float)]
+                ("loss_tile", C.c_int64), ("rms_eps", C.c_float), ("packed", C.c_int32), ("lr", C.c_float),
+                ("n_layers", C.c_int32), ("ckpt_offload", C.c_int32)]
 
 
 P = C.c_void_p
@@ -255,10 +256,12 @@ class UlyssesLayerStep:
     """One decoder layer + lm_head fwd+bwd with Ulysses SP, TiledMLP and tiled logits+loss."""
 
     def __init__(self, shape: ModelShape, seq_len: int, group: ProcessGroup, mlp_tiles: int = 0,
-                 loss_tile: int = 0, packed: bool = False, lr: float = 0.0, rms_eps: float = 1e-5):
-        self.shape, self.seq_len, self.group = shape, seq_len, group
+                 loss_tile: int = 0, packed: bool = False, lr: float = 0.0, rms_eps: float = 1e-5,
+                 n_layers: int = 1, ckpt_offload: bool = False):
+        self.shape, self.seq_len, self.group, self.n_layers = shape, seq_len, group, n_layers
         self.cfg = LayerConfig(shape.hidden, shape.q_heads, shape.kv_heads, shape.head_dim, shape.intermediate,
-                               shape.vocab, seq_len, mlp_tiles, loss_tile, rms_eps, int(packed), lr)
+                               shape.vocab, seq_len, mlp_tiles, loss_tile, rms_eps, int(packed), lr, n_layers,
+                               int(ckpt_offload))
         h = C.c_void_p()
         check(lib().spt_layer_create(C.byref(self.cfg), group.handle, C.byref(h)))
         self.handle = h
@@ -289,11 +292,12 @@ class UlyssesLayerStep:
         import numpy as np
 
         s = self.shape
+        bare = name.split(".", 2)[2] if name.startswith("layers.") else name
         shapes = {"g1": (s.hidden,), "g2": (s.hidden,), "g3": (s.hidden,),
                   "wqkv": ((s.q_heads + 2 * s.kv_heads) * s.head_dim, s.hidden),
                   "wo": (s.hidden, s.q_heads * s.head_dim), "wg": (s.intermediate, s.hidden),
                   "wu": (s.intermediate, s.hidden), "wd": (s.hidden, s.intermediate), "wlm": (s.vocab, s.hidden)}
-        out = np.empty(shapes[name], dtype=np.float32)
+        out = np.empty(shapes[bare], dtype=np.float32)
         check(lib().spt_layer_get_grad(self.handle, name.encode(), ptr(out)))
         return out
 

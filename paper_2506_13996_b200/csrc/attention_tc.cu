@@ -44,6 +44,9 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return x < -126.f ? 0.f : y;
 }
 
+#ifndef SPT_DQ_POLY_EVERY
+#define SPT_DQ_POLY_EVERY 0
+#endif
 #ifndef SPT_FWD_POLY_EVERY
 #define SPT_FWD_POLY_EVERY 0  // N > 0: every N-th exponential pair goes through ex2_poly (measured slower: the
                               // forward softmax is issue-bound, not MUFU-bound, on B200)
@@ -550,7 +553,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 for (int k = 0; k < 8; ++k) {
                     float x0, x1;
                     f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * k]), __uint_as_float(sv[2 * k + 1])), sl2x, nlx), x0, x1);
-                    float p0 = ex2(x0), p1 = ex2(x1);
+                    // part of the exponentials on the FMA pipe: this pass is MUFU-queue-bound, not issue-bound
+                    const bool poly = SPT_DQ_POLY_EVERY > 0 && (k % (SPT_DQ_POLY_EVERY > 0 ? SPT_DQ_POLY_EVERY : 1)) ==
+                                                                     (SPT_DQ_POLY_EVERY > 0 ? SPT_DQ_POLY_EVERY - 1 : 0);
+                    float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
                     if constexpr (MASK) {
                         p0 = (2 * k > hi || 2 * k < lo_) ? 0.f : p0;
                         p1 = (2 * k + 1 > hi || 2 * k + 1 < lo_) ? 0.f : p1;

@@ -1,4 +1,10 @@
-// The sptrain layer-step engine: one Llama-shaped decoder layer + lm_head, fwd + bwd, Ulysses SP.
+// The sptrain layer-step engine: n_layers Llama-shaped decoder layers + lm_head, fwd + bwd, Ulysses SP.
+//
+// n_layers == 1 and no offload: the layer's activations stay live from forward to backward.  Otherwise
+// every layer input is an activation checkpoint (autograd.hpp:23 CheckpointMode): forward
+// keeps only the checkpoints, backward re-runs each layer's forward before its backward; with
+// ckpt_offload the checkpoints live in pinned host memory (SPEC.md:462-475 checkpoint_offload), copied
+// out on a side stream during forward and prefetched one layer ahead during backward.
 //
 //   forward:  x1 = x + Wo . ulysses_attention(Wqkv . rms1(x))
 //                                  x2 = x1 + tiled_mlp(rms2(x1))
@@ -52,6 +58,8 @@ static const char* tag_name(int t) {
 }
 
 struct DeviceLedger {
+    uint64_t host_live = 0, host_peak = 0;  // slow tier: pinned host activation checkpoints
+    std::unordered_map<void*, size_t> host_allocs;
     uint64_t live = 0, peak = 0, budget = 0;
     uint64_t tag_live[kNumTags] = {}, tag_peak[kNumTags] = {}, largest[kNumTags] = {};
     uint64_t events = 0;
@@ -83,10 +91,27 @@ struct DeviceLedger {
         allocs.erase(it);
         ++events;
     }
+    void* alloc_host(size_t bytes) {
+        void* p = nullptr;
+        cudaError_t e = cudaMallocHost(&p, std::max<size_t>(bytes, 256));
+        if (e != cudaSuccess)
+            SPT_THROW(SPT_ERR_OOM, "host OOM: cudaMallocHost(" + std::to_string(bytes) + ") failed: " +
+                                       cudaGetErrorString(e));
+        host_live += bytes;
+        host_peak = std::max(host_peak, host_live);
+        host_allocs[p] = bytes;
+        ++events;
+        return p;
+    }
     void release_all() {
         std::vector<void*> ps;
         for (auto& kv : allocs) ps.push_back(kv.first);
         for (void* p : ps) release(p);
+        for (auto& kv : host_allocs) {
+            cudaFreeHost(kv.first);
+            host_live -= kv.second;
+        }
+        host_allocs.clear();
     }
     std::string summary_json() const {
         std::ostringstream os;
@@ -96,7 +121,9 @@ struct DeviceLedger {
                << "}";
         os << "}},\"largest_single\":{";
         for (int t = 0; t < kNumTags; ++t) os << (t ? "," : "") << "\"" << tag_name(t) << "\":" << largest[t];
-        os << "},\"events\":" << events;
+        os << "},\"host\":{\"live_bytes\":" << host_live << ",\"peak_bytes\":" << host_peak
+           << ",\"tags\":{\"activation-checkpoint\":{\"live\":" << host_live << ",\"peak\":" << host_peak << "}}}";
+        os << ",\"events\":" << events;
         size_t fr = 0, tot = 0;
         if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
             os << ",\"cuda_mem_used_bytes\":" << (tot - fr) << ",\"cuda_mem_total_bytes\":" << tot;
@@ -137,13 +164,25 @@ struct spt_layer {
     float eps;
     DeviceLedger led;
     Prof prof;
-    // weights
-    bf16 *g1, *wqkv, *wo, *g2, *wgu, *wd, *g3, *wlm;
+    // weights: per decoder layer + the shared final norm / lm_head
+    struct LayerW {
+        bf16 *g1, *wqkv, *wo, *g2, *wgu, *wd;
+        float *dg1, *dwqkv, *dwo, *dg2, *dwgu, *dwd;
+    };
+    int NL = 1;            // decoder layers
+    bool ckpt = false;     // activation checkpointing (every layer input saved, layers re-run in backward)
+    bool offload = false;  // checkpoints in pinned host memory
+    std::vector<LayerW> lw;
+    bf16 *g3, *wlm;
     // grads (one contiguous fp32 buffer; SP all-reduce is one call)
     float* gbuf;
     size_t gsize;
-    float *dg1, *dwqkv, *dwo, *dg2, *dwgu, *dwd, *dg3, *dwlm;
+    float *dg3, *dwlm;
     std::vector<RankBufs> rb;
+    std::vector<std::vector<bf16*>> ck;  // [layer][local rank] checkpointed layer inputs (device or host)
+    std::vector<bf16*> xpf;              // [local rank] prefetch buffer for offloaded checkpoints
+    cudaStream_t cstream = nullptr;      // checkpoint copy stream
+    cudaEvent_t ev_x_ready = nullptr, ev_ck_done = nullptr, ev_pf_free = nullptr, ev_pf_done = nullptr;
     void *ws_flce, *ws_mlp, *ws_rms, *ws_attn;
     int32_t *map_qkv, *map_q, *gather_o, *gather_qkv;
     int max_src_o, max_src_qkv;
@@ -195,33 +234,48 @@ static void build_layer(spt_layer* Ly) {
     }
     auto& L_ = Ly->led;
     const int64_t h = Ly->h, I = Ly->I, V = Ly->V;
+    Ly->NL = std::max(1, c.n_layers);
+    Ly->offload = c.ckpt_offload != 0;
+    Ly->ckpt = Ly->NL > 1 || Ly->offload;
     // weights
-    Ly->g1 = Ly->abf(h, kWeights);
-    Ly->wqkv = Ly->abf(Ly->qkv_out * h, kWeights);
-    Ly->wo = Ly->abf(h * Ly->qd, kWeights);
-    Ly->g2 = Ly->abf(h, kWeights);
-    Ly->wgu = Ly->abf(2 * I * h, kWeights);
-    Ly->wd = Ly->abf(h * I, kWeights);
+    Ly->lw.resize(Ly->NL);
+    for (auto& w : Ly->lw) {
+        w.g1 = Ly->abf(h, kWeights);
+        w.wqkv = Ly->abf(Ly->qkv_out * h, kWeights);
+        w.wo = Ly->abf(h * Ly->qd, kWeights);
+        w.g2 = Ly->abf(h, kWeights);
+        w.wgu = Ly->abf(2 * I * h, kWeights);
+        w.wd = Ly->abf(h * I, kWeights);
+    }
     Ly->g3 = Ly->abf(h, kWeights);
     Ly->wlm = Ly->abf(V * h, kWeights);
-    // grads
-    const size_t sz[8] = {(size_t)h, (size_t)(Ly->qkv_out * h), (size_t)(h * Ly->qd), (size_t)h, (size_t)(2 * I * h),
-                          (size_t)(h * I), (size_t)h, (size_t)(V * h)};
-    size_t tot = 0;
-    for (size_t s : sz) tot += (s + 63) / 64 * 64;
+    // grads: [layer 0 .. NL-1: g1, wqkv, wo, g2, wgu, wd] [g3] [wlm], 64-float aligned segments
+    const size_t lsz[6] = {(size_t)h, (size_t)(Ly->qkv_out * h), (size_t)(h * Ly->qd), (size_t)h, (size_t)(2 * I * h),
+                           (size_t)(h * I)};
+    auto al = [](size_t s) { return (s + 63) / 64 * 64; };
+    size_t tot = al((size_t)h) + al((size_t)(V * h));
+    for (int l = 0; l < Ly->NL; ++l)
+        for (size_t s : lsz) tot += al(s);
     Ly->gsize = tot;
     Ly->gbuf = Ly->af32(tot, kGrads);
     float* gp = Ly->gbuf;
-    float** dst[8] = {&Ly->dg1, &Ly->dwqkv, &Ly->dwo, &Ly->dg2, &Ly->dwgu, &Ly->dwd, &Ly->dg3, &Ly->dwlm};
-    for (int i = 0; i < 8; ++i) {
-        *dst[i] = gp;
-        gp += (sz[i] + 63) / 64 * 64;
+    for (auto& w : Ly->lw) {
+        float** dst[6] = {&w.dg1, &w.dwqkv, &w.dwo, &w.dg2, &w.dwgu, &w.dwd};
+        for (int i = 0; i < 6; ++i) {
+            *dst[i] = gp;
+            gp += al(lsz[i]);
+        }
     }
+    Ly->dg3 = gp;
+    gp += al((size_t)h);
+    Ly->dwlm = gp;
     // per-rank activations
     const int64_t nl = Ly->n_loc, N = Ly->N, P = Ly->P;
     Ly->rb.resize(Ly->L);
     for (auto& r : Ly->rb) {
-        r.x = Ly->abf(nl * h, kActivationCkpt);
+        // the layer input: it IS the saved activation when layers are not checkpointed; with checkpointing the
+        // saved copies live in Ly->ck and this is the working buffer
+        r.x = Ly->abf(nl * h, Ly->ckpt ? kWorkspace : kActivationCkpt);
         r.xn1 = Ly->abf(nl * h);
         r.qkv = Ly->abf(nl * Ly->qkv_out);
         r.o = Ly->abf(nl * Ly->qd);
@@ -258,6 +312,20 @@ static void build_layer(spt_layer* Ly) {
             r.dqkv_head = r.dqkv;
         }
     }
+    // activation checkpoints: L * (s/P) * h * 2 bytes per rank (SPEC.md:470 closed form)
+    if (Ly->ckpt) {
+        Ly->ck.assign(Ly->NL, std::vector<bf16*>(Ly->L, nullptr));
+        for (int l = 0; l < Ly->NL; ++l)
+            for (int r = 0; r < Ly->L; ++r)
+                Ly->ck[l][r] = Ly->offload ? (bf16*)L_.alloc_host((size_t)nl * h * 2) : Ly->abf(nl * h, kActivationCkpt);
+        if (Ly->offload) {
+            Ly->xpf.resize(Ly->L);
+            for (auto& p : Ly->xpf) p = Ly->abf(nl * h);
+            SPT_CUDA(cudaStreamCreateWithFlags(&Ly->cstream, cudaStreamNonBlocking));
+            for (cudaEvent_t* e : {&Ly->ev_x_ready, &Ly->ev_ck_done, &Ly->ev_pf_free, &Ly->ev_pf_done})
+                SPT_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+    }
     // workspaces (shared by local ranks; phases run back to back on one stream)
     Ly->ws_flce = L_.alloc(flce_workspace(Ly->loss_tile, V), kLogits);
     Ly->ws_mlp = L_.alloc(mlp_workspace(Ly->mlp_tile, I), kWorkspace);
@@ -287,7 +355,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
                        cudaStream_t st) {
     auto& c = Ly->cfg;
     spt_comm* cm = Ly->comm;
-    const int L = Ly->L, P = Ly->P, d = c.head_dim;
+    const int L = Ly->L, P = Ly->P, d = c.head_dim, NL = Ly->NL;
     const int64_t nl = Ly->n_loc, N = Ly->N, h = Ly->h, I = Ly->I, V = Ly->V, qd = Ly->qd, qo = Ly->qkv_out;
     const int hq = Ly->hq_loc, hkv = Ly->hkv_loc;
     const float scale = 1.f / std::sqrt((float)d);
@@ -320,23 +388,12 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         }
         segment_starts(Ly->pos_full, N, Ly->seg, &Ly->sc->err_pos, st);
     }
-    SPT_CUDA(cudaMemsetAsync(Ly->dg1, 0, h * 4, st));
-    SPT_CUDA(cudaMemsetAsync(Ly->dg2, 0, h * 4, st));
     SPT_CUDA(cudaMemsetAsync(Ly->dg3, 0, h * 4, st));
-
-    // ---- forward phase A: rms1, fused QKV projection, K1 pack
-    for (int r = 0; r < L; ++r) {
-        auto& b = Ly->rb[r];
-        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x, Ly->g1, b.xn1, b.rstd1, nl, h, Ly->eps, st); });
-        EpiParams e;
-        e.C = b.qkv;
-        e.ldc = qo;
-        gemm({b.xn1, h, false}, {Ly->wqkv, h, false}, nl, qo, h, EPI_BF16, e, st);
-        if (P > 1)
-            pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
-                reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv, st);
-            });
+    for (auto& w : Ly->lw) {
+        SPT_CUDA(cudaMemsetAsync(w.dg1, 0, h * 4, st));
+        SPT_CUDA(cudaMemsetAsync(w.dg2, 0, h * 4, st));
     }
+
     const size_t qkv_peer = (size_t)nl * Ly->qkv_loc * d * 2;
     const size_t o_peer = (size_t)nl * hq * d * 2;
     auto sends = [&](bf16* RankBufs::*m) {
@@ -349,97 +406,176 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         for (auto& b : Ly->rb) v.push_back(b.*m);
         return v;
     };
-    if (P > 1)
-        pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st,
-               [&] { cm->all_to_all("all_to_all_qkv", sends(&RankBufs::send_qkv), recvs(&RankBufs::qkv_head), qkv_peer, st); });
-    // ---- attention over the full sequence, local heads
     const double attn_f = 4.0 * (double)N * N * hq * d / 2.0;  // causal half
-    for (int r = 0; r < L; ++r) {
-        auto& b = Ly->rb[r];
-        pf.run(P_ATTN_F, attn_f, 0, st, [&] { attn_fwd(b.qkv_head, N, hq, hkv, d, Ly->seg, scale, b.o_head, b.lse, st); });
-    }
-    if (P > 1) {
-        pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
-               [&] { cm->all_to_all("all_to_all_o", sends(&RankBufs::o_head), recvs(&RankBufs::recv_o), o_peer, st); });
-        for (int r = 0; r < L; ++r) {
+
+    // ---- one decoder layer forward: b.x -> b.x2 (intermediates left in the rank buffers)
+    auto layer_fwd = [&](const spt_layer::LayerW& w) {
+        for (int r = 0; r < L; ++r) {  // phase A: rms1, fused QKV projection, K1 pack
             auto& b = Ly->rb[r];
-            pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st, [&] {
-                reshard_unpack(b.recv_o, nl, hq, d, P, c.q_heads, Ly->gather_o, Ly->max_src_o, b.o, st);
-            });
+            pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x, w.g1, b.xn1, b.rstd1, nl, h, Ly->eps, st); });
+            EpiParams e;
+            e.C = b.qkv;
+            e.ldc = qo;
+            gemm({b.xn1, h, false}, {w.wqkv, h, false}, nl, qo, h, EPI_BF16, e, st);
+            if (P > 1)
+                pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
+                    reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv,
+                                 st);
+                });
         }
-    }
-    // ---- forward phase B + loss + backward down to the attention output
-    for (int r = 0; r < L; ++r) {
-        auto& b = Ly->rb[r];
-        const bool acc = r > 0;  // loopback ranks share the grad buffer: rank-ascending accumulation
-        EpiParams e;
-        e.C = b.x1;
-        e.ldc = h;
-        e.R = b.x;
-        e.ldr = h;
-        gemm({b.o, qd, false}, {Ly->wo, qd, false}, nl, h, qd, EPI_BF16, e, st);
-        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x1, Ly->g2, b.xn2, b.rstd2, nl, h, Ly->eps, st); });
-        mlp_fwd(b.xn2, Ly->wgu, Ly->wd, b.x1, b.x2, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
-        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x2, Ly->g3, b.z, b.rstd3, nl, h, Ly->eps, st); });
-        flce(b.z, Ly->wlm, b.labels, nl, h, V, Ly->loss_tile, &Ly->sc->scale, &Ly->sc->loss_sum, b.dz, Ly->dwlm,
-                 acc, &Ly->sc->err_label, Ly->ws_flce, st);
-        // backward
-        bf16* dx2 = b.dx;  // scratch until the final dx is produced
-        pf.run(P_NORM, 0, 3.0 * nl * h * 2, st,
-               [&] { rmsnorm_bwd(b.x2, Ly->g3, b.rstd3, b.dz, nullptr, dx2, Ly->dg3, Ly->ws_rms, nl, h, st); });
-        bf16* dxn2 = b.dz;
-        mlp_bwd(b.xn2, Ly->wgu, Ly->wd, dx2, dxn2, Ly->dwgu, Ly->dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
-        pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
-               [&] { rmsnorm_bwd(b.x1, Ly->g2, b.rstd2, dxn2, dx2, b.dx1, Ly->dg2, Ly->ws_rms, nl, h, st); });
-        EpiParams e1;
-        e1.C = b.dO;
-        e1.ldc = qd;
-        gemm({b.dx1, h, false}, {Ly->wo, qd, true}, nl, qd, h, EPI_BF16, e1, st);
-        EpiParams e2;
-        e2.C = Ly->dwo;
-        e2.ldc = qd;
-        e2.accumulate = acc;
-        gemm({b.dx1, h, true}, {b.o, qd, true}, h, qd, nl, EPI_F32, e2, st);
         if (P > 1)
-            pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st,
-                   [&] { reshard_pack(b.dO, nl, c.q_heads, d, P, hq, Ly->map_q, b.send_do, st); });
-    }
-    if (P > 1)
-        pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
-               [&] { cm->all_to_all("all_to_all_do", sends(&RankBufs::send_do), recvs(&RankBufs::do_head), o_peer, st); });
-    for (int r = 0; r < L; ++r) {
-        auto& b = Ly->rb[r];
-        pf.run(P_ATTN_B, attn_f * 2.5, 0, st, [&] {
-            attn_bwd(b.qkv_head, b.o_head, b.lse, b.do_head, N, hq, hkv, d, Ly->seg, scale, b.dqkv_head, Ly->ws_attn, st);
-        });
-    }
-    if (P > 1) {
-        pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st, [&] {
-            cm->all_to_all("all_to_all_dqkv", sends(&RankBufs::dqkv_head), recvs(&RankBufs::recv_dqkv), qkv_peer, st);
-        });
+            pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st, [&] {
+                cm->all_to_all("all_to_all_qkv", sends(&RankBufs::send_qkv), recvs(&RankBufs::qkv_head), qkv_peer, st);
+            });
+        for (int r = 0; r < L; ++r) {  // attention over the full sequence, local heads
+            auto& b = Ly->rb[r];
+            pf.run(P_ATTN_F, attn_f, 0, st, [&] { attn_fwd(b.qkv_head, N, hq, hkv, d, Ly->seg, scale, b.o_head, b.lse, st); });
+        }
+        if (P > 1) {
+            pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
+                   [&] { cm->all_to_all("all_to_all_o", sends(&RankBufs::o_head), recvs(&RankBufs::recv_o), o_peer, st); });
+            for (int r = 0; r < L; ++r) {
+                auto& b = Ly->rb[r];
+                pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st, [&] {
+                    reshard_unpack(b.recv_o, nl, hq, d, P, c.q_heads, Ly->gather_o, Ly->max_src_o, b.o, st);
+                });
+            }
+        }
+        for (int r = 0; r < L; ++r) {  // phase B: O projection + residual, rms2, TiledMLP + residual
+            auto& b = Ly->rb[r];
+            EpiParams e;
+            e.C = b.x1;
+            e.ldc = h;
+            e.R = b.x;
+            e.ldr = h;
+            gemm({b.o, qd, false}, {w.wo, qd, false}, nl, h, qd, EPI_BF16, e, st);
+            pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x1, w.g2, b.xn2, b.rstd2, nl, h, Ly->eps, st); });
+            mlp_fwd(b.xn2, w.wgu, w.wd, b.x1, b.x2, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
+        }
+    };
+    // ---- one decoder layer backward: dy = b.dx (d of the layer output) -> b.dx (d of the layer input)
+    auto layer_bwd = [&](const spt_layer::LayerW& w) {
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
-            pf.run(P_RESHARD, 0, 2.0 * nl * qo * 2, st, [&] {
-                reshard_unpack(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, P, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
-                               Ly->max_src_qkv, b.dqkv, st);
+            const bool acc = r > 0;  // loopback ranks share the grad buffer: rank-ascending accumulation
+            bf16* dx2 = b.dx;
+            bf16* dxn2 = b.dz;
+            mlp_bwd(b.xn2, w.wgu, w.wd, dx2, dxn2, w.dwgu, w.dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
+            pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
+                   [&] { rmsnorm_bwd(b.x1, w.g2, b.rstd2, dxn2, dx2, b.dx1, w.dg2, Ly->ws_rms, nl, h, st); });
+            EpiParams e1;
+            e1.C = b.dO;
+            e1.ldc = qd;
+            gemm({b.dx1, h, false}, {w.wo, qd, true}, nl, qd, h, EPI_BF16, e1, st);
+            EpiParams e2;
+            e2.C = w.dwo;
+            e2.ldc = qd;
+            e2.accumulate = acc;
+            gemm({b.dx1, h, true}, {b.o, qd, true}, h, qd, nl, EPI_F32, e2, st);
+            if (P > 1)
+                pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st,
+                       [&] { reshard_pack(b.dO, nl, c.q_heads, d, P, hq, Ly->map_q, b.send_do, st); });
+        }
+        if (P > 1)
+            pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
+                   [&] { cm->all_to_all("all_to_all_do", sends(&RankBufs::send_do), recvs(&RankBufs::do_head), o_peer, st); });
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            pf.run(P_ATTN_B, attn_f * 2.5, 0, st, [&] {
+                attn_bwd(b.qkv_head, b.o_head, b.lse, b.do_head, N, hq, hkv, d, Ly->seg, scale, b.dqkv_head, Ly->ws_attn, st);
             });
         }
+        if (P > 1) {
+            pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st, [&] {
+                cm->all_to_all("all_to_all_dqkv", sends(&RankBufs::dqkv_head), recvs(&RankBufs::recv_dqkv), qkv_peer, st);
+            });
+            for (int r = 0; r < L; ++r) {
+                auto& b = Ly->rb[r];
+                pf.run(P_RESHARD, 0, 2.0 * nl * qo * 2, st, [&] {
+                    reshard_unpack(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, P, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
+                                   Ly->max_src_qkv, b.dqkv, st);
+                });
+            }
+        }
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            const bool acc = r > 0;
+            bf16* dxn1 = b.dz;
+            EpiParams e1;
+            e1.C = dxn1;
+            e1.ldc = h;
+            gemm({b.dqkv, qo, false}, {w.wqkv, h, true}, nl, h, qo, EPI_BF16, e1, st);
+            EpiParams e2;
+            e2.C = w.dwqkv;
+            e2.ldc = h;
+            e2.accumulate = acc;
+            gemm({b.dqkv, qo, true}, {b.xn1, h, true}, qo, h, nl, EPI_F32, e2, st);
+            pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
+                   [&] { rmsnorm_bwd(b.x, w.g1, b.rstd1, dxn1, b.dx1, b.dx, w.dg1, Ly->ws_rms, nl, h, st); });
+        }
+    };
+    // ---- activation checkpoints (offload SPEC.md:462-475)
+    auto ckpt_save = [&](int l) {
+        if (!Ly->offload) {
+            for (int r = 0; r < L; ++r)
+                SPT_CUDA(cudaMemcpyAsync(Ly->ck[l][r], Ly->rb[r].x, nl * h * 2, cudaMemcpyDeviceToDevice, st));
+            return;
+        }
+        // D2H on the copy stream once the layer input is ready; the main stream only waits for it before it
+        // overwrites b.x with the next layer's input (one layer forward later)
+        SPT_CUDA(cudaEventRecord(Ly->ev_x_ready, st));
+        SPT_CUDA(cudaStreamWaitEvent(Ly->cstream, Ly->ev_x_ready, 0));
+        for (int r = 0; r < L; ++r)
+            SPT_CUDA(cudaMemcpyAsync(Ly->ck[l][r], Ly->rb[r].x, nl * h * 2, cudaMemcpyDeviceToHost, Ly->cstream));
+        SPT_CUDA(cudaEventRecord(Ly->ev_ck_done, Ly->cstream));
+    };
+    auto prefetch = [&](int l) {  // offload: H2D of checkpoint l into the prefetch buffers
+        SPT_CUDA(cudaEventRecord(Ly->ev_pf_free, st));
+        SPT_CUDA(cudaStreamWaitEvent(Ly->cstream, Ly->ev_pf_free, 0));
+        for (int r = 0; r < L; ++r)
+            SPT_CUDA(cudaMemcpyAsync(Ly->xpf[r], Ly->ck[l][r], nl * h * 2, cudaMemcpyHostToDevice, Ly->cstream));
+        SPT_CUDA(cudaEventRecord(Ly->ev_pf_done, Ly->cstream));
+    };
+    auto ckpt_restore = [&](int l) {
+        if (!Ly->offload) {
+            for (int r = 0; r < L; ++r)
+                SPT_CUDA(cudaMemcpyAsync(Ly->rb[r].x, Ly->ck[l][r], nl * h * 2, cudaMemcpyDeviceToDevice, st));
+            return;
+        }
+        SPT_CUDA(cudaStreamWaitEvent(st, Ly->ev_pf_done, 0));
+        for (int r = 0; r < L; ++r) std::swap(Ly->rb[r].x, Ly->xpf[r]);
+    };
+
+    // ---- forward through the layers (only the checkpoints survive when checkpointing)
+    for (int l = 0; l < NL; ++l) {
+        if (Ly->ckpt) ckpt_save(l);
+        layer_fwd(Ly->lw[l]);
+        if (l + 1 < NL) {
+            if (Ly->offload) SPT_CUDA(cudaStreamWaitEvent(st, Ly->ev_ck_done, 0));  // b.x copied out
+            for (int r = 0; r < L; ++r)
+                SPT_CUDA(cudaMemcpyAsync(Ly->rb[r].x, Ly->rb[r].x2, nl * h * 2, cudaMemcpyDeviceToDevice, st));
+        }
     }
+    if (Ly->offload) SPT_CUDA(cudaStreamWaitEvent(st, Ly->ev_ck_done, 0));
+    // ---- final norm + tiled logits/loss (fwd+bwd fused) -> dy of the last layer in b.dx
     for (int r = 0; r < L; ++r) {
         auto& b = Ly->rb[r];
         const bool acc = r > 0;
-        bf16* dxn1 = b.dz;
-        EpiParams e1;
-        e1.C = dxn1;
-        e1.ldc = h;
-        gemm({b.dqkv, qo, false}, {Ly->wqkv, h, true}, nl, h, qo, EPI_BF16, e1, st);
-        EpiParams e2;
-        e2.C = Ly->dwqkv;
-        e2.ldc = h;
-        e2.accumulate = acc;
-        gemm({b.dqkv, qo, true}, {b.xn1, h, true}, qo, h, nl, EPI_F32, e2, st);
-        pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
-               [&] { rmsnorm_bwd(b.x, Ly->g1, b.rstd1, dxn1, b.dx1, b.dx, Ly->dg1, Ly->ws_rms, nl, h, st); });
+        pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x2, Ly->g3, b.z, b.rstd3, nl, h, Ly->eps, st); });
+        flce(b.z, Ly->wlm, b.labels, nl, h, V, Ly->loss_tile, &Ly->sc->scale, &Ly->sc->loss_sum, b.dz, Ly->dwlm,
+             acc, &Ly->sc->err_label, Ly->ws_flce, st);
+        pf.run(P_NORM, 0, 3.0 * nl * h * 2, st,
+               [&] { rmsnorm_bwd(b.x2, Ly->g3, b.rstd3, b.dz, nullptr, b.dx, Ly->dg3, Ly->ws_rms, nl, h, st); });
+    }
+    // ---- backward through the layers (re-running each layer's forward from its checkpoint)
+    if (Ly->offload) prefetch(NL - 1);
+    for (int l = NL - 1; l >= 0; --l) {
+        if (Ly->ckpt) {
+            ckpt_restore(l);
+            if (Ly->offload && l > 0) prefetch(l - 1);  // overlaps this layer's recompute + backward
+            layer_fwd(Ly->lw[l]);
+        }
+        layer_bwd(Ly->lw[l]);
     }
     // ---- SP-group reductions
     pf.run(P_COMM, 0, (double)Ly->gsize * 4, st, [&] {
@@ -449,13 +585,15 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     finalize_loss(&Ly->sc->loss_sum, &Ly->sc->count, &Ly->sc->loss, st);
     if (c.lr > 0.f) {
         pf.run(P_OTHER, 0, 0, st, [&] {
-            sgd_update(Ly->wqkv, Ly->dwqkv, qo * h, c.lr, st);
-            sgd_update(Ly->wo, Ly->dwo, h * qd, c.lr, st);
-            sgd_update(Ly->wgu, Ly->dwgu, 2 * I * h, c.lr, st);
-            sgd_update(Ly->wd, Ly->dwd, h * I, c.lr, st);
+            for (auto& w : Ly->lw) {
+                sgd_update(w.wqkv, w.dwqkv, qo * h, c.lr, st);
+                sgd_update(w.wo, w.dwo, h * qd, c.lr, st);
+                sgd_update(w.wgu, w.dwgu, 2 * I * h, c.lr, st);
+                sgd_update(w.wd, w.dwd, h * I, c.lr, st);
+                sgd_update(w.g1, w.dg1, h, c.lr, st);
+                sgd_update(w.g2, w.dg2, h, c.lr, st);
+            }
             sgd_update(Ly->wlm, Ly->dwlm, V * h, c.lr, st);
-            sgd_update(Ly->g1, Ly->dg1, h, c.lr, st);
-            sgd_update(Ly->g2, Ly->dg2, h, c.lr, st);
             sgd_update(Ly->g3, Ly->dg3, h, c.lr, st);
         });
     }
@@ -473,28 +611,51 @@ static void read_scalars(spt_layer* Ly, cudaStream_t st, float* loss, int64_t* c
     if (count) *count = Ly->sc_host->count;
 }
 
-static bf16* param_ptr(spt_layer* Ly, const std::string& n, int64_t* numel) {
-    const int64_t h = Ly->h, I = Ly->I;
-    if (n == "g1") return *numel = h, Ly->g1;
-    if (n == "g2") return *numel = h, Ly->g2;
-    if (n == "g3") return *numel = h, Ly->g3;
-    if (n == "wqkv") return *numel = Ly->qkv_out * h, Ly->wqkv;
-    if (n == "wo") return *numel = h * Ly->qd, Ly->wo;
-    if (n == "wd") return *numel = h * I, Ly->wd;
-    if (n == "wlm") return *numel = Ly->V * h, Ly->wlm;
-    if (n == "wg" || n == "wu") return *numel = I * h, nullptr;
-    SPT_THROW(SPT_ERR_VALIDATION, "unknown parameter name '" + n + "'");
+// Parameter names: "g1", "wqkv", "wo", "g2", "wg", "wu", "wd" (layer 0) or "layers.<i>.<name>" for layer i,
+// plus the shared "g3" and "wlm".  Returns the layer index (-1 for shared) and the bare name.
+static int split_name(spt_layer* Ly, const std::string& full, std::string* bare) {
+    if (full.rfind("layers.", 0) == 0) {
+        const size_t dot = full.find('.', 7);
+        SPT_CHECK(dot != std::string::npos, SPT_ERR_VALIDATION, "bad parameter name '" + full + "'");
+        const int l = std::atoi(full.substr(7, dot - 7).c_str());
+        SPT_CHECK(l >= 0 && l < Ly->NL, SPT_ERR_VALIDATION, "layer index out of range in '" + full + "'");
+        *bare = full.substr(dot + 1);
+        SPT_CHECK(*bare != "g3" && *bare != "wlm", SPT_ERR_VALIDATION, "'" + *bare + "' is not a per-layer parameter");
+        return l;
+    }
+    *bare = full;
+    return (full == "g3" || full == "wlm") ? -1 : 0;
 }
 
-static float* grad_ptr(spt_layer* Ly, const std::string& n) {
-    if (n == "g1") return Ly->dg1;
-    if (n == "g2") return Ly->dg2;
+static bf16* param_ptr(spt_layer* Ly, const std::string& full, int64_t* numel, int* layer = nullptr) {
+    const int64_t h = Ly->h, I = Ly->I;
+    std::string n;
+    const int l = split_name(Ly, full, &n);
+    if (layer) *layer = l;
+    if (n == "g3") return *numel = h, Ly->g3;
+    if (n == "wlm") return *numel = Ly->V * h, Ly->wlm;
+    auto& w = Ly->lw[l];
+    if (n == "g1") return *numel = h, w.g1;
+    if (n == "g2") return *numel = h, w.g2;
+    if (n == "wqkv") return *numel = Ly->qkv_out * h, w.wqkv;
+    if (n == "wo") return *numel = h * Ly->qd, w.wo;
+    if (n == "wd") return *numel = h * I, w.wd;
+    if (n == "wg" || n == "wu") return *numel = I * h, nullptr;
+    SPT_THROW(SPT_ERR_VALIDATION, "unknown parameter name '" + full + "'");
+}
+
+static float* grad_ptr(spt_layer* Ly, const std::string& full) {
+    std::string n;
+    const int l = split_name(Ly, full, &n);
     if (n == "g3") return Ly->dg3;
-    if (n == "wqkv") return Ly->dwqkv;
-    if (n == "wo") return Ly->dwo;
-    if (n == "wd") return Ly->dwd;
     if (n == "wlm") return Ly->dwlm;
-    SPT_THROW(SPT_ERR_VALIDATION, "unknown parameter name '" + n + "'");
+    auto& w = Ly->lw[l];
+    if (n == "g1") return w.dg1;
+    if (n == "g2") return w.dg2;
+    if (n == "wqkv") return w.dwqkv;
+    if (n == "wo") return w.dwo;
+    if (n == "wd") return w.dwd;
+    SPT_THROW(SPT_ERR_VALIDATION, "unknown parameter name '" + full + "'");
 }
 
 extern "C" {
@@ -526,6 +687,9 @@ spt_status spt_layer_destroy(spt_layer* Ly) {
         for (auto e : Ly->prof.pool) cudaEventDestroy(e);
         cudaEventDestroy(Ly->ev_step0);
         cudaEventDestroy(Ly->ev_step1);
+        for (cudaEvent_t e : {Ly->ev_x_ready, Ly->ev_ck_done, Ly->ev_pf_free, Ly->ev_pf_done})
+            if (e) cudaEventDestroy(e);
+        if (Ly->cstream) cudaStreamDestroy(Ly->cstream);
         delete Ly;
     });
 }
@@ -533,8 +697,10 @@ spt_status spt_layer_destroy(spt_layer* Ly) {
 spt_status spt_layer_set_param(spt_layer* Ly, const char* name, const void* data, int32_t data_on_host) {
     return capi_guard([&] {
         int64_t n = 0;
-        std::string nm(name);
-        bf16* p = param_ptr(Ly, nm, &n);
+        std::string full(name), nm;
+        int layer = 0;
+        bf16* p = param_ptr(Ly, full, &n, &layer);
+        split_name(Ly, full, &nm);
         const cudaMemcpyKind k = data_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         if (p) {
             SPT_CUDA(cudaMemcpy(p, data, n * 2, k));
@@ -544,7 +710,7 @@ spt_status spt_layer_set_param(spt_layer* Ly, const char* name, const void* data
         void* tmp = nullptr;
         SPT_CUDA(cudaMalloc(&tmp, n * 2));
         SPT_CUDA(cudaMemcpy(tmp, data, n * 2, k));
-        interleave_gu(nm == "wg" ? tmp : nullptr, nm == "wu" ? tmp : nullptr, Ly->wgu, Ly->I, Ly->h, 0);
+        interleave_gu(nm == "wg" ? tmp : nullptr, nm == "wu" ? tmp : nullptr, Ly->lw[layer].wgu, Ly->I, Ly->h, 0);
         SPT_CUDA(cudaDeviceSynchronize());
         cudaFree(tmp);
     });
@@ -573,22 +739,23 @@ spt_status spt_layer_step(spt_layer* Ly, const void* x, const int64_t* shift_lab
 
 spt_status spt_layer_get_grad(spt_layer* Ly, const char* name, float* host_out) {
     return capi_guard([&] {
-        std::string n(name);
+        std::string full(name), n;
+        const int layer = split_name(Ly, full, &n);
         SPT_CUDA(cudaDeviceSynchronize());
         if (n == "wg" || n == "wu") {
             const size_t cnt = (size_t)Ly->I * Ly->h;
             float *g = nullptr, *u = nullptr;
             SPT_CUDA(cudaMalloc(&g, cnt * 4));
             SPT_CUDA(cudaMalloc(&u, cnt * 4));
-            deinterleave_gu_f32(Ly->dwgu, g, u, Ly->I, Ly->h, 0);
+            deinterleave_gu_f32(Ly->lw[layer].dwgu, g, u, Ly->I, Ly->h, 0);
             SPT_CUDA(cudaMemcpy(host_out, n == "wg" ? g : u, cnt * 4, cudaMemcpyDeviceToHost));
             cudaFree(g);
             cudaFree(u);
             return;
         }
         int64_t numel = 0;
-        param_ptr(Ly, n, &numel);
-        SPT_CUDA(cudaMemcpy(host_out, grad_ptr(Ly, n), numel * 4, cudaMemcpyDeviceToHost));
+        param_ptr(Ly, full, &numel);
+        SPT_CUDA(cudaMemcpy(host_out, grad_ptr(Ly, full), numel * 4, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -605,7 +772,9 @@ spt_status spt_layer_memory_json(spt_layer* Ly, char* buf, size_t cap) {
     return capi_guard([&] {
         std::ostringstream os;
         os << "{\"ledger\":" << Ly->led.summary_json() << ",\"tokens_per_rank\":" << Ly->n_loc
-           << ",\"local_ranks\":" << Ly->L << ",\"mlp_tile\":" << Ly->mlp_tile << ",\"loss_tile\":" << Ly->loss_tile
+           << ",\"local_ranks\":" << Ly->L << ",\"n_layers\":" << Ly->NL << ",\"activation_checkpointing\":"
+           << (Ly->ckpt ? "true" : "false") << ",\"ckpt_offload\":" << (Ly->offload ? "true" : "false")
+           << ",\"mlp_tile\":" << Ly->mlp_tile << ",\"loss_tile\":" << Ly->loss_tile
            << ",\"comm\":" << Ly->comm->stats_json() << "}";
         std::string s = os.str();
         SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small");

@@ -1,0 +1,105 @@
+"""Multi-layer stack with activation checkpointing and checkpoint offload (
+SPEC.md:79-87 checkpoint, :462-475 checkpoint_offload) through the C-ABI engine (pytest -m gpu).
+
+Checker: the oracle's uncheckpointed L-layer restatement `model_step` on the same bf16 inputs (loss rel-err
+<= 1e-3, every per-layer weight grad and d x rel-err <= 2e-2).  Checkpointing / offload must not change any
+value: device-checkpoint and host-offload runs are compared bitwise ("offload preserves training
+exactly").  Ledger closed forms: host checkpoint bytes = L * (s/P) * h * 2 per rank, and with
+offload the device activation-checkpoint peak is independent of L (the Fig. 7 flat structure).
+"""
+import numpy as np
+import pytest
+
+from oracle import sptrain_oracle as O
+from tests.gpu_util import rel_err
+
+pytestmark = pytest.mark.gpu
+
+import paper_2506_13996_b200 as S  # noqa: E402
+
+LOSS_TOL = 1e-3
+GRAD_TOL = 2e-2
+CFG = O.LayerConfig(hidden=256, q_heads=4, kv_heads=2, head_dim=128, intermediate=512, vocab=2048)
+SHAPE = S.ModelShape(256, 4, 2, 128, 512, 2048)
+TINY = O.LayerConfig(hidden=256, q_heads=8, kv_heads=2, head_dim=32, intermediate=1024, vocab=32000)
+TINY_SHAPE = S.ModelShape(256, 8, 2, 32, 1024, 32000)
+
+
+def _params(cfg, L, seed):
+    layers = []
+    for i in range(L):
+        p = O.synth_params(cfg, seed + 101 * i)
+        layers.append({k: p[k] for k in O.LAYER_NAMES})
+    head = O.synth_params(cfg, seed + 7)
+    return layers, head["g3"], head["wlm"]
+
+
+def _run(L, P, N, offload=False, packed=False, cfg=CFG, shape=SHAPE, seed=3):
+    layers, g3, wlm = _params(cfg, L, seed)
+    x, lab, pos = O.synth_batch(cfg, N, seed, packed=packed)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(shape, N, grp, packed=packed, n_layers=L, ckpt_offload=offload)
+    try:
+        for i, lp in enumerate(layers):
+            for k in O.LAYER_NAMES:
+                eng.set_param(f"layers.{i}.{k}", O.f32_to_bf16_bits(lp[k]))
+        eng.set_param("g3", O.f32_to_bf16_bits(g3))
+        eng.set_param("wlm", O.f32_to_bf16_bits(wlm))
+        loss, cnt = eng.step(O.f32_to_bf16_bits(x), lab, pos if packed else None)
+        names = [f"layers.{i}.{k}" for i in range(L) for k in O.LAYER_NAMES] + ["g3", "wlm"]
+        grads = {k: eng.grad(k) for k in names}
+        dx_bits = eng.dx_bits(N)
+        mem = eng.memory()
+    finally:
+        eng.close()
+        grp.close()
+    return dict(loss=loss, count=cnt, grads=grads, dx_bits=dx_bits, mem=mem, layers=layers, g3=g3, wlm=wlm, x=x,
+                lab=lab, pos=pos)
+
+
+def _check(r, L, P, packed=False, cfg=CFG):
+    ref = O.model_step(r["layers"], r["g3"], r["wlm"], cfg, r["x"], r["lab"], r["pos"] if packed else None, P=P)
+    assert r["count"] == ref.count
+    assert abs(r["loss"] - ref.loss) / abs(ref.loss) <= LOSS_TOL, (r["loss"], ref.loss)
+    for k, g in r["grads"].items():
+        e = rel_err(g, ref.grads[k])
+        assert e <= GRAD_TOL, (k, e)
+    assert rel_err(O.bf16_bits_to_f32(r["dx_bits"]), ref.dx) <= GRAD_TOL
+
+
+@pytest.mark.parametrize("L,P,offload,packed", [(2, 1, False, False), (3, 1, True, False), (3, 2, True, False),
+                                                (2, 4, False, True), (1, 1, True, False)])
+def test_multilayer_matches_oracle(L, P, offload, packed):
+    r = _run(L, P, 1024, offload=offload, packed=packed)
+    _check(r, L, P, packed)
+
+
+def test_multilayer_tiny_shape_sp2():
+    """head_dim 32 (mma.sync attention path) through the same checkpointed stack."""
+    r = _run(2, 2, 512, offload=True, cfg=TINY, shape=TINY_SHAPE)
+    _check(r, 2, 2, cfg=TINY)
+
+
+def test_offload_is_bitwise_identical_to_device_checkpoints():
+    a = _run(3, 2, 1024, offload=False)
+    b = _run(3, 2, 1024, offload=True)
+    assert a["loss"] == b["loss"]
+    for k in a["grads"]:
+        assert np.array_equal(a["grads"][k], b["grads"][k]), k
+    assert np.array_equal(a["dx_bits"], b["dx_bits"])
+
+
+def test_offload_ledger_closed_forms():
+    N, P, h = 1024, 2, CFG.hidden
+    peaks = {}
+    for L in (2, 4):
+        r = _run(L, P, N, offload=True)
+        led = r["mem"]["ledger"]
+        assert r["mem"]["ckpt_offload"] and r["mem"]["activation_checkpointing"]
+        # L * (s/P) * h * 2 bytes per rank; the loopback engine hosts all P ranks
+        assert led["host"]["peak_bytes"] == L * (N // P) * h * 2 * P
+        peaks[L] = led["device"]["tags"]["activation-checkpoint"]["peak"]
+        dev = _run(L, P, N, offload=False)["mem"]["ledger"]
+        assert dev["device"]["tags"]["activation-checkpoint"]["peak"] == L * (N // P) * h * 2 * P
+        assert dev["host"]["peak_bytes"] == 0
+    assert peaks[2] == peaks[4] == 0  # flat: device checkpoint bytes independent of L

@@ -118,3 +118,41 @@ def test_all_ignored_loss():
     x, lab, pos = O.synth_batch(cfg, 8, seed=8)
     s, c, dh, dw = O.tiled_logits_loss(x.astype(np.float64) @ np.eye(16), p.wlm, np.full(8, -100), 3, grad_scale=1.0)
     assert (s, c) == (0.0, 0) and not dh.any() and not dw.any()
+
+
+# ---- L-layer stack (model_step): the SPEC's self-oracles extended to several layers
+def test_model_step_sp_equals_sp1_and_fd():
+    cfg = O.LayerConfig(hidden=16, q_heads=4, kv_heads=2, head_dim=4, intermediate=32, vocab=40)
+    rng = np.random.default_rng(5)
+    layers = [{k: v for k, v in O.synth_params(cfg, 11 + i, wstd=0.3).items() if k in O.LAYER_NAMES} for i in range(3)]
+    head = O.synth_params(cfg, 3, wstd=0.3)
+    N = 8
+    x = rng.standard_normal((N, cfg.hidden))
+    lab = rng.integers(0, cfg.vocab, N)
+    lab[3] = -100
+    r1 = O.model_step(layers, head["g3"], head["wlm"], cfg, x, lab, P=1)
+    r2 = O.model_step(layers, head["g3"], head["wlm"], cfg, x, lab, P=2)
+    assert abs(r1.loss - r2.loss) <= 1e-12
+    for k in r1.grads:
+        assert np.max(np.abs(r1.grads[k] - r2.grads[k])) <= 1e-10, k
+    assert np.max(np.abs(r1.dx - r2.dx)) <= 1e-10
+    # central differences on the middle layer's O projection and on the input
+    def loss_with(wo):
+        ls = [dict(l_) for l_ in layers]
+        ls[1]["wo"] = wo
+        return O.model_step(ls, head["g3"], head["wlm"], cfg, x, lab, P=1).loss
+    fd = O.finite_diff_grad(loss_with, np.asarray(layers[1]["wo"], np.float64))
+    assert np.linalg.norm(fd - r1.grads["layers.1.wo"]) / np.linalg.norm(fd) < 1e-6
+    fdx = O.finite_diff_grad(lambda xx: O.model_step(layers, head["g3"], head["wlm"], cfg, xx, lab, P=1).loss, x)
+    assert np.linalg.norm(fdx - r1.dx) / np.linalg.norm(fdx) < 1e-6
+
+
+def test_layer_step_is_one_layer_model_step():
+    cfg = O.LayerConfig(hidden=16, q_heads=4, kv_heads=2, head_dim=4, intermediate=32, vocab=40)
+    p = O.synth_params(cfg, 2, wstd=0.3)
+    x, lab, _ = O.synth_batch(cfg, 8, 2)
+    a = O.layer_step(O.LayerParams(**p), cfg, x, lab)
+    b = O.model_step([{k: p[k] for k in O.LAYER_NAMES}], p["g3"], p["wlm"], cfg, x, lab)
+    assert a.loss == b.loss and np.array_equal(a.dx, b.dx)
+    for k in O.LayerParams.NAMES:
+        assert np.array_equal(a.grads[k], b.grads[k])
