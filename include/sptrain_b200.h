@@ -194,6 +194,14 @@ spt_status spt_layer_step(spt_layer* layer, const void* x, const int64_t* shift_
 spt_status spt_layer_step_async(spt_layer* layer, const void* x, const int64_t* shift_labels,
                                 const int64_t* position_ids, int32_t inputs_on_host, void* stream);
 spt_status spt_layer_read_loss(spt_layer* layer, float* loss_out, int64_t* count_out, void* stream);
+/* Gradient accumulation over a window of micro-steps: each micro-step accumulates the grads of
+ * the loss SUM (first_micro_step = 1 starts a new window); finish all-reduces the accumulated grads over the
+ * SP group, divides them by the window's global valid count, applies the update (lr > 0) and returns the
+ * window's mean loss and count.  Pair with sp_over_dp iteration. */
+spt_status spt_layer_step_accumulate(spt_layer* layer, const void* x, const int64_t* shift_labels,
+                                     const int64_t* position_ids, int32_t inputs_on_host, int32_t first_micro_step,
+                                     void* stream);
+spt_status spt_layer_finish_accumulation(spt_layer* layer, float* loss_out, int64_t* count_out, void* stream);
 /* fp32 weight gradient (SP-group all-reduced) copied to host [out, in]. */
 spt_status spt_layer_get_grad(spt_layer* layer, const char* name, float* host_out);
 /* d loss / d x (bf16 bits, same layout as x) copied to host. */

@@ -98,6 +98,8 @@ SIGNATURES = {
     "spt_layer_step": (I32, [P, P, P, P, I32, PF32, PI64, P]),
     "spt_layer_step_async": (I32, [P, P, P, P, I32, P]),
     "spt_layer_read_loss": (I32, [P, PF32, PI64, P]),
+    "spt_layer_step_accumulate": (I32, [P, P, P, P, I32, I32, P]),
+    "spt_layer_finish_accumulation": (I32, [P, PF32, PI64, P]),
     "spt_layer_get_grad": (I32, [P, C.c_char_p, P]),
     "spt_layer_get_dx": (I32, [P, P]),
     "spt_layer_memory_json": (I32, [P, C.c_char_p, SZ]),
@@ -187,6 +189,51 @@ def block_causal_starts(position_ids):
     out = np.empty_like(a)
     check(lib().spt_block_causal_starts(ptr(a), a.size, ptr(out)))
     return out
+
+
+def sp_over_dp_iterator(loader, group=None, rank: int = 0, world_size: int = 1):
+    """SPEC.md:537-545 / PAPER §4.2 "SP over DP": every rank owns a data stream; the SP group processes ONE
+    rank's batch at a time, collaboratively, iterating over ranks: global order rank0's batch 0, rank1's batch
+    0, ..., rank(P-1)'s batch 0, rank0's batch 1, ...  Each yielded item is (source_rank, input_ids,
+    position_ids, shift_labels) for THIS rank's contiguous sequence shard (already pre-shifted and padded to a
+    multiple of P before sharding).
+
+    `loader` yields dicts with int64 numpy arrays "input_ids", "position_ids" and "labels" (unshifted) for
+    this rank's stream.  With world_size > 1 the batches are exchanged with torch.distributed broadcasts
+    (`group`: a process group, gloo or nccl; only the source rank's batch is sent).  The iterator stops at
+    the shortest stream (every rank learns whether the source still has data)."""
+    import numpy as np
+
+    it = iter(loader)
+    if world_size == 1:
+        for b in it:
+            ids, pos, lab = pad_to_multiple(b["input_ids"], b["position_ids"], preshift_labels(b["labels"]), 1)
+            yield 0, ids, pos, lab
+        return
+    import torch
+    import torch.distributed as dist
+
+    while True:
+        mine = next(it, None)
+        # a round runs only if EVERY stream still has a batch (SPEC.md:542: stop at the shortest stream)
+        have = torch.tensor([0 if mine is None else 1], dtype=torch.int64)
+        dist.all_reduce(have, op=dist.ReduceOp.MIN, group=group)
+        if int(have.item()) == 0:
+            return
+        for src in range(world_size):
+            n = torch.tensor([len(mine["input_ids"]) if src == rank else 0], dtype=torch.int64)
+            dist.broadcast(n, src, group=group)
+            buf = torch.empty(3, int(n.item()), dtype=torch.int64)
+            if src == rank:
+                buf[0] = torch.from_numpy(np.asarray(mine["input_ids"], np.int64))
+                buf[1] = torch.from_numpy(np.asarray(mine["position_ids"], np.int64))
+                buf[2] = torch.from_numpy(np.asarray(mine["labels"], np.int64))
+            dist.broadcast(buf, src, group=group)
+            ids, pos, lab = (buf[i].numpy() for i in range(3))
+            ids, pos, lab = pad_to_multiple(ids, pos, preshift_labels(lab), world_size)
+            s_loc = len(ids) // world_size
+            sl = slice(rank * s_loc, (rank + 1) * s_loc)
+            yield src, ids[sl], pos[sl], lab[sl]
 
 
 def a2a_counts(plan: HeadShardPlan, s_loc: int, head_dim: int, direction: int):
@@ -282,6 +329,20 @@ class UlyssesLayerStep:
     def step_async(self, x, shift_labels, position_ids=None, on_host=False, stream=None):
         check(lib().spt_layer_step_async(self.handle, ptr(x), ptr(shift_labels), ptr(position_ids), int(on_host),
                                          ptr(stream)))
+
+    def step_accumulate(self, x, shift_labels, position_ids=None, first: bool = False, on_host: bool | None = None,
+                        stream=None):
+        """One micro-step of a gradient-accumulation window (grads of the loss sum)."""
+        if on_host is None:
+            on_host = not hasattr(x, "is_cuda") or not x.is_cuda
+        check(lib().spt_layer_step_accumulate(self.handle, ptr(x), ptr(shift_labels), ptr(position_ids), int(on_host),
+                                              int(first), ptr(stream)))
+
+    def finish_accumulation(self, stream=None):
+        """All-reduce the window's grads, divide by its global valid count; returns (mean loss, count)."""
+        loss, cnt = C.c_float(), C.c_int64()
+        check(lib().spt_layer_finish_accumulation(self.handle, C.byref(loss), C.byref(cnt), ptr(stream)))
+        return loss.value, cnt.value
 
     def read_loss(self, stream=None):
         loss, cnt = C.c_float(), C.c_int64()

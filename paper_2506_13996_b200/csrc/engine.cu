@@ -146,6 +146,13 @@ struct Scalars {
     int32_t err_label;
     int32_t err_pos;
 };
+// Gradient-accumulation window ("divide by global valid_count summed over the accumulation
+// window"): micro-steps accumulate grads of the loss SUM; finish divides by the window's global count.
+struct Window {
+    double loss_sum;
+    int64_t count;
+    int64_t one;  // constant 1: finalize_scale(&one) gives the unit grad scale of a micro-step
+};
 
 struct RankBufs {
     bf16 *x, *xn1, *qkv, *o, *x1, *xn2, *x2, *z;
@@ -190,6 +197,7 @@ struct spt_layer {
     int64_t* pos_full;
     Scalars* sc;
     Scalars* sc_host;
+    Window* win;
     cudaEvent_t ev_step0, ev_step1;
     float last_step_ms = 0.f;
 
@@ -344,6 +352,11 @@ static void build_layer(spt_layer* Ly) {
     Ly->seg = c.packed ? (int32_t*)L_.alloc(N * 4, kWorkspace) : nullptr;
     Ly->pos_full = c.packed ? (int64_t*)L_.alloc(N * 8, kWorkspace) : nullptr;
     Ly->sc = (Scalars*)L_.alloc(sizeof(Scalars), kWorkspace);
+    Ly->win = (Window*)L_.alloc(sizeof(Window), kWorkspace);
+    {
+        const Window w0{0.0, 0, 1};
+        SPT_CUDA(cudaMemcpy(Ly->win, &w0, sizeof(Window), cudaMemcpyHostToDevice));
+    }
     SPT_CUDA(cudaMallocHost(&Ly->sc_host, sizeof(Scalars)));
     SPT_CUDA(cudaEventCreate(&Ly->ev_step0));
     SPT_CUDA(cudaEventCreate(&Ly->ev_step1));
@@ -351,9 +364,16 @@ static void build_layer(spt_layer* Ly) {
 
 static double gflop(int64_t m, int64_t n, int64_t k) { return 2.0 * (double)m * n * k; }
 
+static void apply_update(spt_layer* Ly, cudaStream_t st);
+
+// mode 0: one complete step (mean loss of this step, grads all-reduced).  mode 1 / 2: first / later micro-step
+// of a gradient-accumulation window (grads of the loss sum accumulated locally; spt_layer_finish_accumulation
+// all-reduces them and divides by the window's global valid count).
 static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, const int64_t* pos, bool on_host,
-                       cudaStream_t st) {
+                       cudaStream_t st, int mode = 0) {
     auto& c = Ly->cfg;
+    const bool gbase = mode == 2;  // grads accumulate onto the previous micro-steps'
+    const bool micro = mode != 0;
     spt_comm* cm = Ly->comm;
     const int L = Ly->L, P = Ly->P, d = c.head_dim, NL = Ly->NL;
     const int64_t nl = Ly->n_loc, N = Ly->N, h = Ly->h, I = Ly->I, V = Ly->V, qd = Ly->qd, qo = Ly->qkv_out;
@@ -378,7 +398,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         label_stats(b.labels, nl, V, &Ly->sc->count, &Ly->sc->err_label, st);
     }
     cm->all_reduce("all_reduce_count", &Ly->sc->count, 1, ncclInt64, st);
-    finalize_scale(&Ly->sc->count, &Ly->sc->scale, st);
+    finalize_scale(micro ? &Ly->win->one : &Ly->sc->count, &Ly->sc->scale, st);
     if (c.packed) {  // position_ids_full -> run starts
         if (cm->loopback) {
             for (int r = 0; r < L; ++r)
@@ -388,10 +408,12 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         }
         segment_starts(Ly->pos_full, N, Ly->seg, &Ly->sc->err_pos, st);
     }
-    SPT_CUDA(cudaMemsetAsync(Ly->dg3, 0, h * 4, st));
-    for (auto& w : Ly->lw) {
-        SPT_CUDA(cudaMemsetAsync(w.dg1, 0, h * 4, st));
-        SPT_CUDA(cudaMemsetAsync(w.dg2, 0, h * 4, st));
+    if (!gbase) {
+        SPT_CUDA(cudaMemsetAsync(Ly->dg3, 0, h * 4, st));
+        for (auto& w : Ly->lw) {
+            SPT_CUDA(cudaMemsetAsync(w.dg1, 0, h * 4, st));
+            SPT_CUDA(cudaMemsetAsync(w.dg2, 0, h * 4, st));
+        }
     }
 
     const size_t qkv_peer = (size_t)nl * Ly->qkv_loc * d * 2;
@@ -457,7 +479,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     auto layer_bwd = [&](const spt_layer::LayerW& w) {
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
-            const bool acc = r > 0;  // loopback ranks share the grad buffer: rank-ascending accumulation
+            const bool acc = r > 0 || gbase;  // loopback ranks share the grad buffer: rank-ascending
             bf16* dx2 = b.dx;
             bf16* dxn2 = b.dz;
             mlp_bwd(b.xn2, w.wgu, w.wd, dx2, dxn2, w.dwgu, w.dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
@@ -499,7 +521,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         }
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
-            const bool acc = r > 0;
+            const bool acc = r > 0 || gbase;
             bf16* dxn1 = b.dz;
             EpiParams e1;
             e1.C = dxn1;
@@ -560,7 +582,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     // ---- final norm + tiled logits/loss (fwd+bwd fused) -> dy of the last layer in b.dx
     for (int r = 0; r < L; ++r) {
         auto& b = Ly->rb[r];
-        const bool acc = r > 0;
+        const bool acc = r > 0 || gbase;
         pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x2, Ly->g3, b.z, b.rstd3, nl, h, Ly->eps, st); });
         flce(b.z, Ly->wlm, b.labels, nl, h, V, Ly->loss_tile, &Ly->sc->scale, &Ly->sc->loss_sum, b.dz, Ly->dwlm,
              acc, &Ly->sc->err_label, Ly->ws_flce, st);
@@ -578,11 +600,37 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         layer_bwd(Ly->lw[l]);
     }
     // ---- SP-group reductions
+    if (micro) {  // window totals only; the grad all-reduce waits for the end of the window
+        cm->all_reduce("all_reduce_loss_sum", &Ly->sc->loss_sum, 1, ncclFloat64, st);
+        window_accumulate(&Ly->sc->loss_sum, &Ly->sc->count, &Ly->win->loss_sum, &Ly->win->count, mode == 1, st);
+        SPT_CUDA(cudaEventRecord(Ly->ev_step1, st));
+        cm->check_async();
+        return;
+    }
     pf.run(P_COMM, 0, (double)Ly->gsize * 4, st, [&] {
         cm->all_reduce("all_reduce_grads", Ly->gbuf, Ly->gsize, ncclFloat32, st);
         cm->all_reduce("all_reduce_loss_sum", &Ly->sc->loss_sum, 1, ncclFloat64, st);
     });
     finalize_loss(&Ly->sc->loss_sum, &Ly->sc->count, &Ly->sc->loss, st);
+    apply_update(Ly, st);
+    SPT_CUDA(cudaEventRecord(Ly->ev_step1, st));
+    cm->check_async();
+}
+
+// end of an accumulation window: all-reduce the accumulated grads, divide by the window's global count
+static void finish_accumulation(spt_layer* Ly, cudaStream_t st) {
+    spt_comm* cm = Ly->comm;
+    cm->all_reduce("all_reduce_grads", Ly->gbuf, Ly->gsize, ncclFloat32, st);
+    scale_by_inverse_count(Ly->gbuf, (int64_t)Ly->gsize, &Ly->win->count, st);
+    window_finalize(&Ly->win->loss_sum, &Ly->win->count, &Ly->sc->loss_sum, &Ly->sc->count, &Ly->sc->loss, st);
+    apply_update(Ly, st);
+    cm->check_async();
+}
+
+static void apply_update(spt_layer* Ly, cudaStream_t st) {
+    auto& c = Ly->cfg;
+    const int64_t h = Ly->h, I = Ly->I, V = Ly->V, qd = Ly->qd, qo = Ly->qkv_out;
+    Prof& pf = Ly->prof;
     if (c.lr > 0.f) {
         pf.run(P_OTHER, 0, 0, st, [&] {
             for (auto& w : Ly->lw) {
@@ -597,8 +645,6 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             sgd_update(Ly->g3, Ly->dg3, h, c.lr, st);
         });
     }
-    SPT_CUDA(cudaEventRecord(Ly->ev_step1, st));
-    cm->check_async();
 }
 
 static void read_scalars(spt_layer* Ly, cudaStream_t st, float* loss, int64_t* count) {
@@ -721,6 +767,23 @@ spt_status spt_layer_step_async(spt_layer* Ly, const void* x, const int64_t* shi
     return capi_guard([&] {
         SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
         layer_step(Ly, x, shift_labels, position_ids, inputs_on_host != 0, (cudaStream_t)stream);
+    });
+}
+
+spt_status spt_layer_step_accumulate(spt_layer* Ly, const void* x, const int64_t* shift_labels,
+                                     const int64_t* position_ids, int32_t inputs_on_host, int32_t first_micro_step,
+                                     void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
+        layer_step(Ly, x, shift_labels, position_ids, inputs_on_host != 0, (cudaStream_t)stream,
+                   first_micro_step ? 1 : 2);
+    });
+}
+
+spt_status spt_layer_finish_accumulation(spt_layer* Ly, float* loss_out, int64_t* count_out, void* stream) {
+    return capi_guard([&] {
+        finish_accumulation(Ly, (cudaStream_t)stream);
+        read_scalars(Ly, (cudaStream_t)stream, loss_out, count_out);
     });
 }
 

@@ -475,6 +475,40 @@ __global__ void finalize_loss_kernel(const double* sum, const int64_t* count, fl
     const int64_t c = *count;
     *loss = c > 0 ? (float)(*sum / (double)c) : 0.f;
 }
+__global__ void window_accumulate_kernel(const double* loss_sum, const int64_t* count, double* win_sum,
+                                         int64_t* win_count, int first) {
+    *win_sum = (first ? 0.0 : *win_sum) + *loss_sum;
+    *win_count = (first ? 0 : *win_count) + *count;
+}
+void window_accumulate(const double* loss_sum, const int64_t* count, double* win_sum, int64_t* win_count, bool first,
+                       cudaStream_t st) {
+    window_accumulate_kernel<<<1, 1, 0, st>>>(loss_sum, count, win_sum, win_count, first ? 1 : 0);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+__global__ void window_finalize_kernel(const double* win_sum, const int64_t* win_count, double* loss_sum,
+                                       int64_t* count, float* loss) {
+    *loss_sum = *win_sum;
+    *count = *win_count;
+    *loss = *win_count > 0 ? (float)(*win_sum / (double)*win_count) : 0.f;
+}
+void window_finalize(const double* win_sum, const int64_t* win_count, double* loss_sum, int64_t* count, float* loss,
+                     cudaStream_t st) {
+    window_finalize_kernel<<<1, 1, 0, st>>>(win_sum, win_count, loss_sum, count, loss);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+__global__ void scale_by_inverse_count_kernel(float* g, int64_t n, const int64_t* count) {
+    const int64_t c = *count;
+    const float s = c > 0 ? (float)(1.0 / (double)c) : 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        g[i] *= s;
+}
+void scale_by_inverse_count(float* g, int64_t n, const int64_t* count, cudaStream_t st) {
+    scale_by_inverse_count_kernel<<<148 * 8, 256, 0, st>>>(g, n, count);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
 void finalize_scale(const int64_t* count, float* scale, cudaStream_t st) {
     finalize_scale_kernel<<<1, 1, 0, st>>>(count, scale);
     count_launch();

@@ -51,6 +51,11 @@ void ce_rows_stats(const float* logits, const float* stats, int ntile, const int
 void sum_rows(const float* v, int64_t n, double* accum, cudaStream_t st);
 // loss = loss_sum / count (device scalars) and scale = 1/count.
 void finalize_scale(const int64_t* count, float* scale, cudaStream_t st);
+void window_accumulate(const double* loss_sum, const int64_t* count, double* win_sum, int64_t* win_count, bool first,
+                       cudaStream_t st);
+void window_finalize(const double* win_sum, const int64_t* win_count, double* loss_sum, int64_t* count, float* loss,
+                     cudaStream_t st);
+void scale_by_inverse_count(float* g, int64_t n, const int64_t* count, cudaStream_t st);
 void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st);
 // W(bf16) -= lr * G(fp32)
 void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st);

@@ -84,3 +84,62 @@ def test_ulysses_exchange_world2(Hq, Hkv):
         assert p.exitcode == 0
     for rank, a, b, c in res:
         assert a and b and c, (rank, a, b, c)
+
+
+# ---- SP-over-DP iteration over gloo, world size 2
+def _iter_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_2506_13996_b200 as S
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank 0's stream: A, B (, E); rank 1's: C, D -> collaborative order A, C, B, D, then stop (min length)
+        names = [["A", "B", "E"], ["C", "D"]][rank]
+
+        def batch(nm):
+            base = {"A": 1, "B": 100, "C": 200, "D": 300, "E": 400}[nm]
+            n = 7 if nm in ("A", "D") else 8  # odd length exercises pad_to_multiple
+            return {"input_ids": np.arange(base, base + n, dtype=np.int64),
+                    "position_ids": np.arange(n, dtype=np.int64),
+                    "labels": np.arange(base, base + n, dtype=np.int64), "name": nm}
+
+        out = []
+        for src, ids, pos, lab in S.sp_over_dp_iterator((batch(n) for n in names), None, rank, world):
+            out.append((src, ids.tolist(), pos.tolist(), lab.tolist()))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sp_over_dp_iterator_world2():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_iter_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    order = [src for src, *_ in res[0]]
+    assert order == [0, 1, 0, 1] == [src for src, *_ in res[1]]  # A, C, B, D; E dropped (shortest stream)
+    firsts = [res[0][i][1][0] for i in range(4)]
+    assert firsts == [1, 200, 100, 300]
+    for i in range(4):
+        ids = res[0][i][1] + res[1][i][1]
+        lab = res[0][i][3] + res[1][i][3]
+        pos = res[0][i][2] + res[1][i][2]
+        # reconstruction of the padded, pre-shifted source batch
+        base = ids[0]
+        n = 7 if base in (1, 300) else 8
+        src_lab = list(range(base, base + n))
+        exp_ids, exp_pos, exp_lab = O.pad_to_multiple(np.arange(base, base + n), np.arange(n),
+                                                      O.preshift_labels(np.asarray(src_lab)), 2)
+        assert ids == list(exp_ids) and pos == list(exp_pos) and lab == list(exp_lab)
+        assert lab[-1] == -100 and len(ids) % 2 == 0

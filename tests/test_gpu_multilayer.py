@@ -103,3 +103,42 @@ def test_offload_ledger_closed_forms():
         assert dev["device"]["tags"]["activation-checkpoint"]["peak"] == L * (N // P) * h * 2 * P
         assert dev["host"]["peak_bytes"] == 0
     assert peaks[2] == peaks[4] == 0  # flat: device checkpoint bytes independent of L
+
+
+def _engine(L, P, N, cfg=CFG, shape=SHAPE, seed=3):
+    layers, g3, wlm = _params(cfg, L, seed)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(shape, N, grp, n_layers=L)
+    for i, lp in enumerate(layers):
+        for k in O.LAYER_NAMES:
+            eng.set_param(f"layers.{i}.{k}", O.f32_to_bf16_bits(lp[k]))
+    eng.set_param("g3", O.f32_to_bf16_bits(g3))
+    eng.set_param("wlm", O.f32_to_bf16_bits(wlm))
+    return eng, grp, (layers, g3, wlm)
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_grad_accumulation_window_matches_oracle(P):
+    """SPEC.md:548 / PAPER §5.5: a window of micro-steps accumulates grads of the loss SUM and divides by the
+    window's global valid count; equals the oracle's count-weighted combination of the batches."""
+    L, N = 2, 1024
+    eng, grp, (layers, g3, wlm) = _engine(L, P, N)
+    batches = [O.synth_batch(CFG, N, seed) for seed in (11, 12, 13)]
+    try:
+        for i, (x, lab, _) in enumerate(batches):
+            eng.step_accumulate(O.f32_to_bf16_bits(x), lab, first=(i == 0))
+        loss, cnt = eng.finish_accumulation()
+        names = [f"layers.{i}.{k}" for i in range(L) for k in O.LAYER_NAMES] + ["g3", "wlm"]
+        grads = {k: eng.grad(k) for k in names}
+    finally:
+        eng.close()
+        grp.close()
+    refs = [O.model_step(layers, g3, wlm, CFG, x, lab, P=P) for x, lab, _ in batches]
+    tot = sum(r.count for r in refs)
+    assert cnt == tot
+    ref_loss = sum(r.loss_sum for r in refs) / tot
+    assert abs(loss - ref_loss) / abs(ref_loss) <= LOSS_TOL, (loss, ref_loss)
+    for k in names:
+        ref_g = sum(r.grads[k] * r.count for r in refs) / tot
+        e = rel_err(grads[k], ref_g)
+        assert e <= GRAD_TOL, (k, e)
