@@ -198,14 +198,128 @@ __global__ void reshard_unpack_kernel(const uint4* __restrict__ recv, int64_t s_
     }
 }
 
+// Row-parallel variants for head_dim in {32, 64, 128} (VPD = head_dim / 8 uint4 per head): one warp per
+// destination row ((rank, token) for K1, token for K2), index maps staged in shared memory, one integer
+// division per row instead of several per 16-byte element, and loads batched ahead of the stores so each
+// lane keeps several 16-byte requests in flight (the generic kernels above were issue-bound at ~60% of
+// the HBM copy bandwidth).
+template <int VPD>
+__global__ void __launch_bounds__(256) reshard_pack_rows_kernel(const uint4* __restrict__ src, int64_t s_loc,
+                                                                int heads_in, int P, int heads_out,
+                                                                const int32_t* __restrict__ head_map,
+                                                                uint4* __restrict__ dst) {
+    extern __shared__ int32_t smap[];  // [P][heads_out]
+    for (int i = threadIdx.x; i < P * heads_out; i += blockDim.x) smap[i] = head_map[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows = (int64_t)P * s_loc;
+    const int row_elems = heads_out * VPD;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < nrows; r += nw) {
+        const int j = (int)(r / s_loc);
+        const int64_t t = r - (int64_t)j * s_loc;
+        const uint4* srow = src + t * heads_in * VPD;
+        uint4* drow = dst + r * row_elems;
+        const int32_t* m = smap + j * heads_out;
+        for (int e0 = 0; e0 < row_elems; e0 += 32 * 4) {
+            uint4 buf[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 32 + lane;
+                if (e < row_elems) buf[u] = __ldg(srow + m[e / VPD] * VPD + (e % VPD));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 32 + lane;
+                if (e < row_elems) drow[e] = buf[u];
+            }
+        }
+    }
+}
+
+template <int VPD>
+__global__ void __launch_bounds__(256) reshard_unpack_rows_kernel(const uint4* __restrict__ recv, int64_t s_loc,
+                                                                  int heads_in, int heads_out,
+                                                                  const int32_t* __restrict__ gather, int max_src,
+                                                                  uint4* __restrict__ dst) {
+    extern __shared__ int32_t sg[];  // [heads_out][max_src] (rank*heads_in + slot, -1 = unused)
+    for (int i = threadIdx.x; i < heads_out * max_src; i += blockDim.x) sg[i] = gather[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int row_elems = heads_out * VPD;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t rank_stride = s_loc * heads_in * VPD;
+    for (int64_t t = w0; t < s_loc; t += nw) {
+        const uint4* trow = recv + t * heads_in * VPD;
+        uint4* drow = dst + t * row_elems;
+        for (int e0 = 0; e0 < row_elems; e0 += 32 * 4) {
+            uint4 buf[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 32 + lane;
+                if (e >= row_elems) continue;
+                const int h = e / VPD, v = e % VPD;
+                const int32_t* gl = sg + h * max_src;
+                auto at = [&](int g) { return trow + (int64_t)(g / heads_in) * rank_stride + (g % heads_in) * VPD + v; };
+                buf[u] = __ldg(at(gl[0]));
+                if (max_src > 1 && gl[1] >= 0) {  // replicate_kv backward: fp32 sum in rank order
+                    float acc[8];
+                    {
+                        const uint32_t ws[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 f = unpack_bf16x2(ws[k]);
+                            acc[2 * k] = f.x;
+                            acc[2 * k + 1] = f.y;
+                        }
+                    }
+                    for (int s = 1; s < max_src && gl[s] >= 0; ++s) {
+                        const uint4 w = __ldg(at(gl[s]));
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 f = unpack_bf16x2(ws[k]);
+                            acc[2 * k] += f.x;
+                            acc[2 * k + 1] += f.y;
+                        }
+                    }
+                    buf[u].x = pack_bf16x2(acc[0], acc[1]);
+                    buf[u].y = pack_bf16x2(acc[2], acc[3]);
+                    buf[u].z = pack_bf16x2(acc[4], acc[5]);
+                    buf[u].w = pack_bf16x2(acc[6], acc[7]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 32 + lane;
+                if (e < row_elems) drow[e] = buf[u];
+            }
+        }
+    }
+}
+
+static int reshard_rows_grid(int64_t rows) {
+    const int64_t blocks = (rows + 7) / 8;  // 8 warps (rows) per block per pass
+    return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms() * 8));
+}
+
 void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
                   const int32_t* head_map, void* dst, cudaStream_t st) {
     SPT_CHECK(head_dim % 8 == 0, SPT_ERR_SHAPE, "head_dim must be a multiple of 8");
     const int vpd = head_dim / 8;
     const int64_t total = (int64_t)P * s_loc * heads_out * vpd;
     if (total == 0) return;
-    reshard_pack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)src, s_loc, heads_in, vpd, P, heads_out,
-                                                               head_map, (uint4*)dst);
+    const size_t smem = (size_t)P * heads_out * 4;
+    if ((vpd == 4 || vpd == 8 || vpd == 16) && smem <= 48 * 1024) {
+        const int g = reshard_rows_grid((int64_t)P * s_loc);
+        auto k = vpd == 16 ? reshard_pack_rows_kernel<16> : vpd == 8 ? reshard_pack_rows_kernel<8> : reshard_pack_rows_kernel<4>;
+        k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, (uint4*)dst);
+    } else {
+        reshard_pack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)src, s_loc, heads_in, vpd, P, heads_out,
+                                                                   head_map, (uint4*)dst);
+    }
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }
@@ -217,8 +331,16 @@ void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim,
     const int vpd = head_dim / 8;
     const int64_t total = s_loc * heads_out * vpd;
     if (total == 0) return;
-    reshard_unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)recv, s_loc, heads_in, vpd, heads_out,
-                                                                 gather, max_src, (uint4*)dst);
+    const size_t smem = (size_t)heads_out * max_src * 4;
+    if ((vpd == 4 || vpd == 8 || vpd == 16) && smem <= 48 * 1024) {
+        const int g = reshard_rows_grid(s_loc);
+        auto k = vpd == 16 ? reshard_unpack_rows_kernel<16>
+                           : vpd == 8 ? reshard_unpack_rows_kernel<8> : reshard_unpack_rows_kernel<4>;
+        k<<<g, 256, smem, st>>>((const uint4*)recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst);
+    } else {
+        reshard_unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)recv, s_loc, heads_in, vpd,
+                                                                     heads_out, gather, max_src, (uint4*)dst);
+    }
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }
