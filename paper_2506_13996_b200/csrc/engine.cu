@@ -589,10 +589,12 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         pf.run(P_NORM, 0, 3.0 * nl * h * 2, st,
                [&] { rmsnorm_bwd(b.x2, Ly->g3, b.rstd3, b.dz, nullptr, b.dx, Ly->dg3, Ly->ws_rms, nl, h, st); });
     }
-    // ---- backward through the layers (re-running each layer's forward from its checkpoint)
-    if (Ly->offload) prefetch(NL - 1);
+    // ---- backward through the layers (re-running each layer's forward from its checkpoint).  The last
+    // layer's forward state is still live in the rank buffers (the head only touches z/dz/dx), so it is not
+    // re-run; its checkpoint is still saved, keeping the SPEC.md:470 byte count L * (s/P) * h.
+    if (Ly->offload && NL > 1) prefetch(NL - 2);
     for (int l = NL - 1; l >= 0; --l) {
-        if (Ly->ckpt) {
+        if (Ly->ckpt && l < NL - 1) {
             ckpt_restore(l);
             if (Ly->offload && l > 0) prefetch(l - 1);  // overlaps this layer's recompute + backward
             layer_fwd(Ly->lw[l]);
