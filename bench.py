@@ -156,7 +156,8 @@ def run_ours(args, rank, world, local_rank):
     seq = args.seq_per_gpu * world
     n_loc = args.seq_per_gpu
     shp = S.ModelShape(**SHAPE)
-    eng = S.UlyssesLayerStep(shp, seq, grp, lr=args.lr, n_layers=args.layers, ckpt_offload=args.offload)
+    eng = S.UlyssesLayerStep(shp, seq, grp, lr=args.lr, n_layers=args.layers, ckpt_offload=args.offload,
+                             rope_theta=args.rope)
     # random-init weights of the architecture, identical on every rank (same seed)
     g = torch.Generator(device=dev).manual_seed(1234)
     qkv_out = (shp.q_heads + 2 * shp.kv_heads) * shp.head_dim
@@ -298,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
                    "sp_degree": world, "mlp_tile": mem["mlp_tile"], "loss_tile": mem["loss_tile"],
                    "l2": "inputs larger than L2 (x 256 MiB/GPU, weights 1.5 GiB, activations ~3 GiB per step)",
                    "optimizer": f"sgd lr={args.lr}" if args.lr > 0 else "none (fwd+bwd+SP grad all-reduce)",
-                   "n_layers": args.layers,
+                   "n_layers": args.layers, "rope_theta": args.rope,
                    "activation_checkpointing": ("offload to pinned host" if args.offload else
                                                 ("device" if args.layers > 1 else "none (single layer)"))},
         "peak_hbm_bytes": peak_b, "peak_hbm_bytes_per_token": peak_b / n_loc,
@@ -331,6 +332,7 @@ def main():
     ap.add_argument("--layers", type=int, default=1,
                     help="decoder layers (> 1: per-layer activation checkpointing; not the BASELINE config)")
     ap.add_argument("--offload", action="store_true", help="activation checkpoints in pinned host memory")
+    ap.add_argument("--rope", type=float, default=0.0, help="RoPE theta (> 0 turns it on; not the BASELINE config)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

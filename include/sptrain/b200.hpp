@@ -183,6 +183,7 @@ struct StepOptions {
     int64_t loss_tile = 0;       // tokens per logits tile, 0 -> auto
     float lr = 0.f;              // > 0: plain SGD update after the step
     float rms_eps = 1e-5f;
+    float rope_theta = 0.f;      // > 0: rotary embedding on q/k (row f4; the reference model has none)
 };
 
 class UlyssesLayerStep {
@@ -203,6 +204,7 @@ public:
         c.lr = o.lr;
         c.n_layers = o.n_layers;
         c.ckpt_offload = o.ckpt_offload ? 1 : 0;
+        c.rope_theta = o.rope_theta;
         check(spt_layer_create(&c, group.handle(), &l_));
     }
     UlyssesLayerStep(const UlyssesLayerStep&) = delete;

@@ -115,6 +115,11 @@ spt_status spt_attn_bwd(const void* qkv, const void* o, const float* lse, const 
                         int32_t hkv, int32_t head_dim, const int32_t* seg_start, float scale, void* dqkv,
                         void* workspace, void* stream);
 
+/* RoPE in place on the first n_rot heads of x [n][heads][head_dim] bf16;
+ * position_ids: DEVICE int64 [n] or NULL (positions pos_offset + t); inverse = 1 for the backward. */
+spt_status spt_rope(void* x, int64_t n, int32_t heads, int32_t n_rot, int32_t head_dim, const int64_t* position_ids,
+                    int64_t pos_offset, float theta, int32_t inverse, void* stream);
+
 /* Label pre-pass of cross_entropy: count of non-ignored labels (int64, added to
  * *count_accum) and a device error flag set to 1 when a label is outside [0,V) U {-100}. */
 spt_status spt_label_stats(const int64_t* labels, int64_t n, int64_t vocab, int64_t* count_accum, int32_t* err_flag,
@@ -176,6 +181,9 @@ typedef struct {
                           (layer inputs saved, each layer re-run in backward) */
     int32_t ckpt_offload; /* 1: checkpoints in pinned host memory, copied on a side stream
                              (checkpoint_offload); implies checkpointing */
+    float rope_theta;     /* > 0: rotary position embedding on q and k (Llama rotate_half convention, base
+                             theta; positions = position_ids when packed, else the global token index).
+                             0 = off, the reference's model (SPEC.md:261 omits RoPE) */
 } spt_layer_config;
 
 typedef struct spt_layer spt_layer;

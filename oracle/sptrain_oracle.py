@@ -545,9 +545,37 @@ def synth_batch(cfg: LayerConfig, n: int, seed: int, ignore_frac: float = 0.05, 
     return x, shift, position_ids
 
 
-def decoder_layer_fwd(p, cfg: LayerConfig, xs: list, starts, P: int, mlp_tiles=None):
+def rope_angles(positions, head_dim: int, theta: float):
+    """Rotary position embedding angles (the reference SPEC omits RoPE).
+    Llama / HF convention: inv_freq[j] = theta^(-2j/d), angle[t, j] = position[t] * inv_freq[j], both in
+    float32 exactly as HF computes them (so long positions carry the same fp32 rounding), cos/sin in f64."""
+    j = np.arange(0, head_dim, 2, dtype=np.int64).astype(np.float32) / np.float32(head_dim)
+    inv_freq = (np.float32(1.0) / np.power(np.float32(theta), j)).astype(np.float32)
+    ang = (np.asarray(positions, np.int64).astype(np.float32)[:, None] * inv_freq[None, :]).astype(np.float32)
+    return np.cos(ang.astype(np.float64)), np.sin(ang.astype(np.float64))
+
+
+def rope_apply(x, cos, sin, inverse: bool = False):
+    """x [n, heads, d] -> x*cos + rotate_half(x)*sin (rotate_half(x) = [-x2, x1]); inverse=True applies the
+    transpose rotation (the backward of the forward rotation)."""
+    h = x.shape[-1] // 2
+    x1, x2 = x[..., :h], x[..., h:]
+    c, s = cos[:, None, :], sin[:, None, :]
+    if inverse:
+        s = -s
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def rope_positions(position_ids, packed: bool):
+    """RoPE positions: the position_ids themselves for packed samples (each sample restarts at 0), else the
+    global token index (SPEC.md:333 position_ids_full = arange for a single sample)."""
+    return np.asarray(position_ids, np.int64)
+
+
+def decoder_layer_fwd(p, cfg: LayerConfig, xs: list, starts, P: int, mlp_tiles=None, rope=None):
     """One decoder layer forward over P in-process ranks: per rank
-    x1 = x + Wo·ulysses_attention(Wqkv·rms1(x)), x2 = x1 + tiled_mlp(rms2(x1)).  Returns (x2 per rank, cache)."""
+    x1 = x + Wo·ulysses_attention(Wqkv·rms1(x)), x2 = x1 + tiled_mlp(rms2(x1)).  rope: None or per-rank
+    (cos, sin) applied to q and k after the projection (row f4).  Returns (x2 per rank, cache)."""
     Hq, Hkv, d = cfg.q_heads, cfg.kv_heads, cfg.head_dim
     plan = plan_head_shards(Hq, Hkv, P)
     n_loc = xs[0].shape[0]
@@ -558,6 +586,9 @@ def decoder_layer_fwd(p, cfg: LayerConfig, xs: list, starts, P: int, mlp_tiles=N
         q = qkv[:, :Hq * d].reshape(n_loc, Hq, d)
         k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(n_loc, Hkv, d)
         v = qkv[:, (Hq + Hkv) * d:].reshape(n_loc, Hkv, d)
+        if rope is not None:
+            q = rope_apply(q, *rope[r])
+            k = rope_apply(k, *rope[r])
         st[r].update(xn1=xn1, rstd1=rstd1, q=q, k=k, v=v)
     # seq -> head all-to-all, inner attention over the full sequence, head -> seq
     qh = seq_to_head([s_["q"] for s_ in st], plan.q_heads_of)
@@ -575,7 +606,7 @@ def decoder_layer_fwd(p, cfg: LayerConfig, xs: list, starts, P: int, mlp_tiles=N
         xn2, rstd2 = rmsnorm_fwd(x1, p.g2)
         x2 = x1 + tiled_mlp(xn2, p.wg, p.wu, p.wd, mlp_tiles)
         st[r].update(o=o, x1=x1, xn2=xn2, rstd2=rstd2, x2=x2)
-    cache = dict(st=st, qh=qh, kh=kh, vh=vh, oh=oh, lse=lse, plan=plan, starts=starts, mlp_tiles=mlp_tiles)
+    cache = dict(st=st, qh=qh, kh=kh, vh=vh, oh=oh, lse=lse, plan=plan, starts=starts, mlp_tiles=mlp_tiles, rope=rope)
     return [s_["x2"] for s_ in st], cache
 
 
@@ -609,7 +640,11 @@ def decoder_layer_bwd(p, cfg: LayerConfig, cache: dict, dys: list, P: int):
     dxs = []
     for r in range(P):
         s_ = st[r]
-        dqkv = np.concatenate([dqs[r].reshape(n_loc, -1), dks[r].reshape(n_loc, -1), dvs[r].reshape(n_loc, -1)], axis=1)
+        dq_r, dk_r = dqs[r], dks[r]
+        if cache["rope"] is not None:  # back through the rotation (transpose)
+            dq_r = rope_apply(dq_r, *cache["rope"][r], inverse=True)
+            dk_r = rope_apply(dk_r, *cache["rope"][r], inverse=True)
+        dqkv = np.concatenate([dq_r.reshape(n_loc, -1), dk_r.reshape(n_loc, -1), dvs[r].reshape(n_loc, -1)], axis=1)
         grads[r]["wqkv"] = dqkv.T @ s_["xn1"]
         dxn1 = dqkv @ p.wqkv
         dx0n, dg1 = rmsnorm_bwd(s_["x"], p.g1, s_["rstd1"], dxn1)
@@ -622,7 +657,7 @@ LAYER_NAMES = ("g1", "wqkv", "wo", "g2", "wg", "wu", "wd")
 
 
 def model_step(layers: list, g3, wlm, cfg: LayerConfig, x, shift_labels, position_ids=None, P: int = 1,
-               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False) -> StepResult:
+               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False, rope_theta: float = 0.0) -> StepResult:
     """One SP=P training step (fwd+bwd) of an L-layer decoder stack + final norm + lm_head as
     P in-process ranks.  `layers` holds one dict / LayerParams-like object per layer with LAYER_NAMES.
     Global mean loss via all_reduce of (sum, count); weight grads all-reduced over the SP group
@@ -647,9 +682,13 @@ def model_step(layers: list, g3, wlm, cfg: LayerConfig, x, shift_labels, positio
     loss_tile = n_loc if loss_tile is None else loss_tile
     xs = shard_sequence(x, P)
     labs = shard_sequence(np.asarray(shift_labels, np.int64), P)
+    rope = None
+    if rope_theta > 0:  # row f4: positions = position_ids (per packed sample) / global token index
+        cos, sin = rope_angles(rope_positions(position_ids, True), cfg.head_dim, rope_theta)
+        rope = [(cos[r * n_loc:(r + 1) * n_loc], sin[r * n_loc:(r + 1) * n_loc]) for r in range(P)]
     caches = []
     for p in ps:
-        xs, cache = decoder_layer_fwd(p, cfg, xs, starts, P, mlp_tiles)
+        xs, cache = decoder_layer_fwd(p, cfg, xs, starts, P, mlp_tiles, rope)
         caches.append(cache)
     # final norm + tiled logits/loss; global (sum, count) via all-reduce
     counts = [int(np.sum(l_ != IGNORE_INDEX)) for l_ in labs]

@@ -55,7 +55,7 @@ class LayerConfig(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("intermediate", C.c_int32), ("vocab", C.c_int64), ("seq_len", C.c_int64), ("mlp_tiles", C.c_int32),
                 ("loss_tile", C.c_int64), ("rms_eps", C.c_float), ("packed", C.c_int32), ("lr", C.c_float),
-                ("n_layers", C.c_int32), ("ckpt_offload", C.c_int32)]
+                ("n_layers", C.c_int32), ("ckpt_offload", C.c_int32), ("rope_theta", C.c_float)]
 
 
 P = C.c_void_p
@@ -83,6 +83,7 @@ SIGNATURES = {
     "spt_label_stats": (I32, [P, I64, I64, P, P, P]),
     "spt_segment_starts": (I32, [P, I64, P, P, P]),
     "spt_flce_workspace": (SZ, [I64, I64]),
+    "spt_rope": (I32, [P, I64, I32, I32, I32, P, I64, F32, I32, P]),
     "spt_flce": (I32, [P, P, P, I64, I64, I64, I64, P, P, P, P, I32, P, P, P]),
     "spt_mlp_workspace": (SZ, [I64, I64]),
     "spt_mlp_fwd": (I32, [P, P, P, P, P, I64, I64, I64, I64, P, P]),
@@ -304,11 +305,11 @@ class UlyssesLayerStep:
 
     def __init__(self, shape: ModelShape, seq_len: int, group: ProcessGroup, mlp_tiles: int = 0,
                  loss_tile: int = 0, packed: bool = False, lr: float = 0.0, rms_eps: float = 1e-5,
-                 n_layers: int = 1, ckpt_offload: bool = False):
+                 n_layers: int = 1, ckpt_offload: bool = False, rope_theta: float = 0.0):
         self.shape, self.seq_len, self.group, self.n_layers = shape, seq_len, group, n_layers
         self.cfg = LayerConfig(shape.hidden, shape.q_heads, shape.kv_heads, shape.head_dim, shape.intermediate,
                                shape.vocab, seq_len, mlp_tiles, loss_tile, rms_eps, int(packed), lr, n_layers,
-                               int(ckpt_offload))
+                               int(ckpt_offload), rope_theta)
         h = C.c_void_p()
         check(lib().spt_layer_create(C.byref(self.cfg), group.handle, C.byref(h)))
         self.handle = h

@@ -374,6 +374,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     auto& c = Ly->cfg;
     const bool gbase = mode == 2;  // grads accumulate onto the previous micro-steps'
     const bool micro = mode != 0;
+    const bool rope_on = c.rope_theta > 0.f;
     spt_comm* cm = Ly->comm;
     const int L = Ly->L, P = Ly->P, d = c.head_dim, NL = Ly->NL;
     const int64_t nl = Ly->n_loc, N = Ly->N, h = Ly->h, I = Ly->I, V = Ly->V, qd = Ly->qd, qo = Ly->qkv_out;
@@ -439,6 +440,11 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             e.C = b.qkv;
             e.ldc = qo;
             gemm({b.xn1, h, false}, {w.wqkv, h, false}, nl, qo, h, EPI_BF16, e, st);
+            if (rope_on)  // row f4: rotate q and k heads in place before the reshard / attention
+                pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
+                    rope_apply(b.qkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
+                               c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, false, st);
+                });
             if (P > 1)
                 pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
                     reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv,
@@ -523,6 +529,11 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             auto& b = Ly->rb[r];
             const bool acc = r > 0 || gbase;
             bf16* dxn1 = b.dz;
+            if (rope_on)  // d(q, k) through the rotation's transpose, before the projection's backward
+                pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
+                    rope_apply(b.dqkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
+                               c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, true, st);
+                });
             EpiParams e1;
             e1.C = dxn1;
             e1.ldc = h;
@@ -839,7 +850,8 @@ spt_status spt_layer_memory_json(spt_layer* Ly, char* buf, size_t cap) {
         os << "{\"ledger\":" << Ly->led.summary_json() << ",\"tokens_per_rank\":" << Ly->n_loc
            << ",\"local_ranks\":" << Ly->L << ",\"n_layers\":" << Ly->NL << ",\"activation_checkpointing\":"
            << (Ly->ckpt ? "true" : "false") << ",\"ckpt_offload\":" << (Ly->offload ? "true" : "false")
-           << ",\"mlp_tile\":" << Ly->mlp_tile << ",\"loss_tile\":" << Ly->loss_tile
+           << ",\"rope_theta\":" << Ly->cfg.rope_theta << ",\"mlp_tile\":" << Ly->mlp_tile
+           << ",\"loss_tile\":" << Ly->loss_tile
            << ",\"comm\":" << Ly->comm->stats_json() << "}";
         std::string s = os.str();
         SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small");

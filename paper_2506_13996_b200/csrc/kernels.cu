@@ -345,6 +345,54 @@ void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim,
     SPT_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------------ RoPE
+// In-place rotary embedding of the first n_rot heads of each token row of x [n][heads][d] (bf16), Llama / HF
+// rotate_half convention: (x1, x2) -> (x1 cos - x2 sin, x2 cos + x1 sin) with angle = pos * theta^(-2j/d)
+// computed in fp32 exactly as HF does; inverse = the transpose rotation (backward).  pos: DEVICE int64 [n]
+// or NULL (then pos = pos_offset + t).  One thread per (token, head, 8 consecutive j): 16-byte loads/stores.
+__global__ void rope_kernel(bf16* __restrict__ x, int64_t n, int heads, int n_rot, int d,
+                            const int64_t* __restrict__ pos, int64_t pos_offset, float theta, int inverse) {
+    const int half = d / 2, g8 = half / 8;  // 8-wide groups per half
+    const int64_t total = n * n_rot * g8;
+    const float sgn = inverse ? -1.f : 1.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int gi = (int)(i % g8);
+        const int64_t q = i / g8;
+        const int hh = (int)(q % n_rot);
+        const int64_t t = q / n_rot;
+        const float p = (float)(pos ? pos[t] : pos_offset + t);
+        bf16* row = x + (t * heads + hh) * d;
+        float a[8], b[8];
+        load8(row + gi * 8, a);
+        load8(row + half + gi * 8, b);
+        float o1[8], o2[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = gi * 8 + k;
+            const float inv_freq = 1.f / powf(theta, (float)(2 * j) / (float)d);
+            float s, c;
+            sincosf(p * inv_freq, &s, &c);
+            s *= sgn;
+            o1[k] = a[k] * c - b[k] * s;
+            o2[k] = b[k] * c + a[k] * s;
+        }
+        store8(row + gi * 8, o1);
+        store8(row + half + gi * 8, o2);
+    }
+}
+
+void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
+                bool inverse, cudaStream_t st) {
+    SPT_CHECK(d % 16 == 0, SPT_ERR_SHAPE, "rope: head_dim must be a multiple of 16");
+    SPT_CHECK(theta > 0.f, SPT_ERR_CONFIG, "rope: theta must be > 0");
+    const int64_t total = n * n_rot * (d / 16);
+    if (total == 0) return;
+    rope_kernel<<<grid_for(total, 256), 256, 0, st>>>((bf16*)x, n, heads, n_rot, d, pos, pos_offset, theta,
+                                                      inverse ? 1 : 0);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------------------ K10 label / position pre-passes
 __global__ void label_stats_kernel(const int64_t* __restrict__ labels, int64_t n, int64_t V, int64_t* count,
                                    int32_t* err) {

@@ -56,6 +56,9 @@ void window_accumulate(const double* loss_sum, const int64_t* count, double* win
 void window_finalize(const double* win_sum, const int64_t* win_count, double* loss_sum, int64_t* count, float* loss,
                      cudaStream_t st);
 void scale_by_inverse_count(float* g, int64_t n, const int64_t* count, cudaStream_t st);
+// RoPE on the first n_rot heads of x [n][heads][d] (bf16, in place); inverse = backward rotation.
+void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
+                bool inverse, cudaStream_t st);
 void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st);
 // W(bf16) -= lr * G(fp32)
 void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st);

@@ -187,6 +187,15 @@ spt_status spt_mlp_bwd(const void* x, const void* wgu, const void* wd, const voi
     return capi_guard(
         [&] { mlp_bwd(x, wgu, wd, dy, dx, dwgu, dwd, accumulate != 0, n, h, inter, tile_n, workspace, ST); });
 }
+spt_status spt_rope(void* x, int64_t n, int32_t heads, int32_t n_rot, int32_t head_dim, const int64_t* position_ids,
+                    int64_t pos_offset, float theta, int32_t inverse, void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(n_rot >= 0 && n_rot <= heads, SPT_ERR_SHAPE, "rope: n_rot must be in [0, heads]");
+        rope_apply(x, n, heads, n_rot, head_dim, position_ids, pos_offset, theta, inverse != 0,
+                   (cudaStream_t)stream);
+    });
+}
+
 size_t spt_attn_bwd_workspace(int64_t s, int32_t hq, int32_t hkv, int32_t head_dim) {
     size_t r = 0;
     capi_guard([&] { r = attn_bwd_workspace(s, hq, hkv, head_dim); });

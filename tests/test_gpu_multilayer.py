@@ -34,11 +34,11 @@ def _params(cfg, L, seed):
     return layers, head["g3"], head["wlm"]
 
 
-def _run(L, P, N, offload=False, packed=False, cfg=CFG, shape=SHAPE, seed=3):
+def _run(L, P, N, offload=False, packed=False, cfg=CFG, shape=SHAPE, seed=3, rope=0.0):
     layers, g3, wlm = _params(cfg, L, seed)
     x, lab, pos = O.synth_batch(cfg, N, seed, packed=packed)
     grp = S.ProcessGroup.loopback_group(P)
-    eng = S.UlyssesLayerStep(shape, N, grp, packed=packed, n_layers=L, ckpt_offload=offload)
+    eng = S.UlyssesLayerStep(shape, N, grp, packed=packed, n_layers=L, ckpt_offload=offload, rope_theta=rope)
     try:
         for i, lp in enumerate(layers):
             for k in O.LAYER_NAMES:
@@ -57,8 +57,9 @@ def _run(L, P, N, offload=False, packed=False, cfg=CFG, shape=SHAPE, seed=3):
                 lab=lab, pos=pos)
 
 
-def _check(r, L, P, packed=False, cfg=CFG):
-    ref = O.model_step(r["layers"], r["g3"], r["wlm"], cfg, r["x"], r["lab"], r["pos"] if packed else None, P=P)
+def _check(r, L, P, packed=False, cfg=CFG, rope=0.0):
+    ref = O.model_step(r["layers"], r["g3"], r["wlm"], cfg, r["x"], r["lab"], r["pos"] if packed else None, P=P,
+                       rope_theta=rope)
     assert r["count"] == ref.count
     assert abs(r["loss"] - ref.loss) / abs(ref.loss) <= LOSS_TOL, (r["loss"], ref.loss)
     for k, g in r["grads"].items():
@@ -142,3 +143,37 @@ def test_grad_accumulation_window_matches_oracle(P):
         ref_g = sum(r.grads[k] * r.count for r in refs) / tot
         e = rel_err(grads[k], ref_g)
         assert e <= GRAD_TOL, (k, e)
+
+
+
+# ---- RoPE (row f4): the rotation on q/k after the projection, its transpose in the backward
+@pytest.mark.parametrize("L,P,packed,cfg,shape", [(1, 1, False, CFG, SHAPE), (2, 2, True, CFG, SHAPE),
+                                                   (1, 4, False, CFG, SHAPE), (2, 2, False, TINY, TINY_SHAPE)])
+def test_rope_matches_oracle(L, P, packed, cfg, shape):
+    r = _run(L, P, 1024 if cfg is CFG else 512, packed=packed, cfg=cfg, shape=shape, rope=10000.0)
+    assert r["mem"]["rope_theta"] == 10000.0
+    _check(r, L, P, packed, cfg=cfg, rope=10000.0)
+
+
+def test_rope_op_vs_oracle_and_inverse():
+    from tests.gpu_util import bf16_dev, to_np, torch
+
+    T = torch()
+    rng = np.random.default_rng(4)
+    n, heads, n_rot, d = 300, 6, 4, 128
+    x = O.round_bf16(rng.standard_normal((n, heads, d), dtype=np.float32))
+    pos = rng.integers(0, 1 << 19, n).astype(np.int64)
+    xd = bf16_dev(x)
+    pd = T.from_numpy(pos).cuda()
+    L_ = S.lib()
+    S.check(L_.spt_rope(xd.data_ptr(), n, heads, n_rot, d, pd.data_ptr(), 0, 10000.0, 0, None))
+    T.cuda.synchronize()
+    cos, sin = O.rope_angles(pos, d, 10000.0)
+    ref = x.astype(np.float64).copy()
+    ref[:, :n_rot] = O.rope_apply(ref[:, :n_rot], cos, sin)
+    got = to_np(xd)
+    assert rel_err(got, ref) < 1e-2
+    assert np.array_equal(got[:, n_rot:], x[:, n_rot:])  # v heads untouched
+    S.check(L_.spt_rope(xd.data_ptr(), n, heads, n_rot, d, pd.data_ptr(), 0, 10000.0, 1, None))
+    T.cuda.synchronize()
+    assert rel_err(to_np(xd), x) < 1e-2  # inverse undoes the rotation (up to bf16 rounding)

@@ -156,3 +156,37 @@ def test_layer_step_is_one_layer_model_step():
     assert a.loss == b.loss and np.array_equal(a.dx, b.dx)
     for k in O.LayerParams.NAMES:
         assert np.array_equal(a.grads[k], b.grads[k])
+
+
+# ---- RoPE (row f4; the SPEC omits it, so these are self-oracles: rotation, FD gradient, SP invariance)
+def test_rope_is_a_rotation_and_its_inverse():
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((6, 3, 8))
+    cos, sin = O.rope_angles(np.arange(6), 8, 10000.0)
+    y = O.rope_apply(x, cos, sin)
+    assert np.allclose(np.linalg.norm(y, axis=-1), np.linalg.norm(x, axis=-1))  # norm preserving
+    assert np.allclose(O.rope_apply(y, cos, sin, inverse=True), x)
+    assert np.allclose(y[0], x[0])  # position 0: identity
+
+
+def test_model_step_with_rope_fd_and_sp():
+    cfg = O.LayerConfig(hidden=16, q_heads=4, kv_heads=2, head_dim=4, intermediate=32, vocab=40)
+    rng = np.random.default_rng(9)
+    layers = [{k: v for k, v in O.synth_params(cfg, 21 + i, wstd=0.3).items() if k in O.LAYER_NAMES} for i in range(2)]
+    head = O.synth_params(cfg, 4, wstd=0.3)
+    N = 8
+    x = rng.standard_normal((N, cfg.hidden))
+    lab = rng.integers(0, cfg.vocab, N)
+    r1 = O.model_step(layers, head["g3"], head["wlm"], cfg, x, lab, P=1, rope_theta=100.0)
+    r2 = O.model_step(layers, head["g3"], head["wlm"], cfg, x, lab, P=2, rope_theta=100.0)
+    r0 = O.model_step(layers, head["g3"], head["wlm"], cfg, x, lab, P=1)
+    assert abs(r1.loss - r2.loss) <= 1e-12 and abs(r1.loss - r0.loss) > 1e-6  # rope changes the model
+    for k in r1.grads:
+        assert np.max(np.abs(r1.grads[k] - r2.grads[k])) <= 1e-10, k
+
+    def loss_with(w):
+        ls = [dict(l_) for l_ in layers]
+        ls[0]["wqkv"] = w
+        return O.model_step(ls, head["g3"], head["wlm"], cfg, x, lab, P=1, rope_theta=100.0).loss
+    fd = O.finite_diff_grad(loss_with, np.asarray(layers[0]["wqkv"], np.float64))
+    assert np.linalg.norm(fd - r1.grads["layers.0.wqkv"]) / np.linalg.norm(fd) < 1e-6
