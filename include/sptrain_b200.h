@@ -74,6 +74,39 @@ spt_status spt_block_causal_starts(const int64_t* position_ids, int64_t s, int64
 spt_status spt_a2a_counts(const spt_head_shard_plan* plan, int64_t s_loc, int32_t head_dim, int32_t direction,
                           int64_t* send_counts, int64_t* recv_counts);
 
+/* ================================ memest ================================ */
+typedef struct {
+    double weights_bytes, optimizer_bytes, master_weights_bytes, grads_bytes, total_bytes; /* 2/8/4/4 B per param */
+    double device_bytes_per_gpu; /* fixed share on one GPU (ZeRO-3 divides by world size; optimizer offload
+                                    moves optimizer + master weights to host) */
+    double host_bytes_per_gpu;
+} spt_memest_fixed;
+/* estimate_fixed: 8e9 params -> 144 GiB total (PAPER §2.1). */
+spt_status spt_memest_fixed_bytes(double param_count, int32_t world_size, int32_t zero3, int32_t offload_optimizer,
+                                  spt_memest_fixed* out);
+/* estimate_logits: seqlen * vocab * bytes (4 for fp32). */
+double spt_memest_logits_bytes(double seqlen, double vocab, double bytes);
+/* estimate_activation_ckpt: device bytes per GPU without offload, host bytes per node with it. */
+spt_status spt_memest_activation_ckpt_bytes(double seqlen, double hidden, double layers, double bytes, int32_t sp,
+                                            int32_t gpus_per_node, double* device_bytes, double* host_bytes_per_node);
+/* estimate_4d_mask / estimate_position_ids. */
+double spt_memest_4d_mask_bytes(double seqlen, double bytes);
+double spt_memest_position_ids_bytes(double seqlen, double bytes);
+/* This engine's per-rank device bytes: weights, grads, logits tile workspace, checkpoints and the per-token
+ * activation coefficients (act_bytes_per_token: per local token; act_bytes_per_seq_token: per GLOBAL token,
+ * e.g. the full-sequence Q/K/V of the local heads), calibrated from the measured ledger. */
+typedef struct {
+    int32_t hidden, q_heads, kv_heads, head_dim, intermediate;
+    int64_t vocab;
+    int32_t n_layers, sp, ckpt_offload;
+    double act_bytes_per_token, act_bytes_per_seq_token;
+} spt_memest_engine;
+spt_status spt_memest_engine_device_bytes(const spt_memest_engine* cfg, double seqlen, double* out);
+/* max_seqlen_solver: largest multiple of `granularity` whose estimate fits device_budget
+ * (bisection); SPT_ERR_OOM (infeasibility report in spt_last_error) when none does. */
+spt_status spt_max_seqlen_solver(const spt_memest_engine* cfg, double device_budget_bytes, int64_t granularity,
+                                 int64_t* out);
+
 /* ==================================== device kernels ==================================== */
 
 /* matmul on tcgen05: C[m,n] = alpha * sum_k A(m,k) B(n,k) (+ residual | + C).

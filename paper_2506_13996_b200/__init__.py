@@ -84,6 +84,13 @@ SIGNATURES = {
     "spt_segment_starts": (I32, [P, I64, P, P, P]),
     "spt_flce_workspace": (SZ, [I64, I64]),
     "spt_rope": (I32, [P, I64, I32, I32, I32, P, I64, F32, I32, P]),
+    "spt_memest_fixed_bytes": (I32, [C.c_double, I32, I32, I32, P]),
+    "spt_memest_logits_bytes": (C.c_double, [C.c_double, C.c_double, C.c_double]),
+    "spt_memest_activation_ckpt_bytes": (I32, [C.c_double, C.c_double, C.c_double, C.c_double, I32, I32, P, P]),
+    "spt_memest_4d_mask_bytes": (C.c_double, [C.c_double, C.c_double]),
+    "spt_memest_position_ids_bytes": (C.c_double, [C.c_double, C.c_double]),
+    "spt_memest_engine_device_bytes": (I32, [P, C.c_double, P]),
+    "spt_max_seqlen_solver": (I32, [P, C.c_double, I64, P]),
     "spt_flce": (I32, [P, P, P, I64, I64, I64, I64, P, P, P, P, I32, P, P, P]),
     "spt_mlp_workspace": (SZ, [I64, I64]),
     "spt_mlp_fwd": (I32, [P, P, P, P, P, I64, I64, I64, I64, P, P]),
@@ -190,6 +197,63 @@ def block_causal_starts(position_ids):
     out = np.empty_like(a)
     check(lib().spt_block_causal_starts(ptr(a), a.size, ptr(out)))
     return out
+
+
+# ---------------------------------------------------------------- memest
+class MemestFixed(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("weights_bytes", "optimizer_bytes", "master_weights_bytes", "grads_bytes",
+                                           "total_bytes", "device_bytes_per_gpu", "host_bytes_per_gpu")]
+
+
+class MemestEngine(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("intermediate", C.c_int32), ("vocab", C.c_int64), ("n_layers", C.c_int32), ("sp", C.c_int32),
+                ("ckpt_offload", C.c_int32), ("act_bytes_per_token", C.c_double),
+                ("act_bytes_per_seq_token", C.c_double)]
+
+
+def memest_fixed(param_count: float, world_size: int = 1, zero3: bool = False, offload_optimizer: bool = False):
+    out = MemestFixed()
+    check(lib().spt_memest_fixed_bytes(float(param_count), world_size, int(zero3), int(offload_optimizer),
+                                       C.byref(out)))
+    return {n: getattr(out, n) for n, _ in MemestFixed._fields_}
+
+
+def memest_logits(seqlen, vocab, nbytes=4):
+    return lib().spt_memest_logits_bytes(float(seqlen), float(vocab), float(nbytes))
+
+
+def memest_activation_ckpt(seqlen, hidden, layers, nbytes=2, sp=1, gpus_per_node=8):
+    dev, host = C.c_double(), C.c_double()
+    check(lib().spt_memest_activation_ckpt_bytes(float(seqlen), float(hidden), float(layers), float(nbytes), sp,
+                                                 gpus_per_node, C.byref(dev), C.byref(host)))
+    return dev.value, host.value
+
+
+def memest_4d_mask(seqlen, nbytes=2):
+    return lib().spt_memest_4d_mask_bytes(float(seqlen), float(nbytes))
+
+
+def memest_position_ids(seqlen, nbytes=2):
+    return lib().spt_memest_position_ids_bytes(float(seqlen), float(nbytes))
+
+
+def memest_engine(shape: "ModelShape", n_layers=1, sp=1, ckpt_offload=False, act_bytes_per_token=0.0,
+                  act_bytes_per_seq_token=0.0) -> MemestEngine:
+    return MemestEngine(shape.hidden, shape.q_heads, shape.kv_heads, shape.head_dim, shape.intermediate, shape.vocab,
+                        n_layers, sp, int(ckpt_offload), act_bytes_per_token, act_bytes_per_seq_token)
+
+
+def memest_engine_bytes(cfg: MemestEngine, seqlen) -> float:
+    out = C.c_double()
+    check(lib().spt_memest_engine_device_bytes(C.byref(cfg), float(seqlen), C.byref(out)))
+    return out.value
+
+
+def max_seqlen(cfg: MemestEngine, device_budget_bytes, granularity=128) -> int:
+    out = C.c_int64()
+    check(lib().spt_max_seqlen_solver(C.byref(cfg), float(device_budget_bytes), granularity, C.byref(out)))
+    return out.value
 
 
 def sp_over_dp_iterator(loader, group=None, rank: int = 0, world_size: int = 1):
