@@ -38,6 +38,9 @@ typedef enum {
 } spt_status;
 
 const char* spt_last_error(void);
+/* Run-time tuning switches for A/B experiments (gemm_1sm, gemm_pair_mn, gemm_bn, epi_tstore); the defaults
+ * are the measured-best configuration. */
+spt_status spt_tuning_set(const char* name, int32_t value);
 const char* spt_version(void);
 
 /* ============================ host-only logic (no GPU needed) ============================ */

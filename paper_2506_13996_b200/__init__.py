@@ -65,6 +65,7 @@ PI32, PI64, PF32 = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_flo
 SIGNATURES = {
     "spt_last_error": (C.c_char_p, []),
     "spt_version": (C.c_char_p, []),
+    "spt_tuning_set": (I32, [C.c_char_p, I32]),
     "spt_plan_head_shards": (I32, [I32, I32, I32, C.POINTER(HeadShardPlan)]),
     "spt_plan_heads_of": (I32, [C.POINTER(HeadShardPlan), I32, I32, PI32, I32, PI32]),
     "spt_preshift_labels": (I32, [P, I64, P]),

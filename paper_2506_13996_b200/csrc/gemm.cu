@@ -1,6 +1,7 @@
 // Host side of the tcgen05 GEMM: TMA descriptor encoding, instantiation dispatch, C-ABI entry.
 #include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "common.h"
 #include "gemm.cuh"
@@ -59,9 +60,28 @@ CUtensorMap make_tmap_f32_3d(const void* ptr, uint64_t d0, uint64_t d1, uint64_t
     return m;
 }
 
+// fp32 [M, N] output with row pitch ldc as a 2-D TMA map, 32 x 32 boxes, 128-byte swizzle (epi_tma_block)
+static CUtensorMap make_tmap_f32_c(void* C, int64_t M, int64_t N, int64_t ldc) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)ldc * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    SPT_CHECK((reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc * 4) % 16 == 0, SPT_ERR_SHAPE,
+              "fp32 TMA epilogue needs 16-byte aligned C and pitch");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SPT_CHECK(r == CUDA_SUCCESS, SPT_ERR_CUDA, "cuTensorMapEncodeTiled (fp32 C) failed: " + std::to_string((int)r));
+    return m;
+}
+
 template <int BN, bool A_MN, bool B_MN, int KIND>
-static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep,
+static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep_in,
                         cudaStream_t st) {
+    EpiParams ep = ep_in;
+    CUtensorMap tc = ta;  // unused unless the TMA fp32 epilogue runs
+    if (KIND == EPI_F32 && ep.tstore == 2) tc = make_tmap_f32_c(ep.C, M, N, ep.ldc);
     auto kern = gemm_tc_kernel<BN, A_MN, B_MN, KIND>;
     constexpr int smem = GemmCfg<BN>::SMEM_BYTES;
     static bool attr_done = false;
@@ -72,7 +92,7 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
     const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
     const int grid = std::min(ntiles, num_sms());
     prof_run(P_GEMM, 2.0 * M * N * K, 0, st, [&] {
-        kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep);
+        kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep, tc);
         count_launch("gemm");
     });
     SPT_CUDA(cudaGetLastError());
@@ -112,28 +132,25 @@ static int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
     return (e && e[0]) ? atoi(e) : dflt;
 }
-// Experiment / tuning switches (read once): SPT_GEMM_1SM=1 disables CTA pairs, SPT_GEMM_PAIR_MN=1 also
-// runs MN-major operand shapes as pairs, SPT_GEMM_BN=128|256 forces the N tile (0 = per-shape choice).
-static bool use_pair_gemm() {
-    static const bool v = env_int("SPT_GEMM_1SM", 0) != 1;
-    return v;
+// Experiment / tuning switches: initialised from the environment, changeable at run time through
+// spt_tuning_set (A/B comparisons inside one process).  gemm_1sm=1 disables CTA pairs, gemm_pair_mn=1 also
+// runs MN-major operand shapes as pairs, gemm_bn=128|256 forces the N tile (0 = per-shape choice),
+// epi_tstore = fp32 epilogue mode: 0 per-thread stores, 1 smem-transposed coalesced stores, 2 (default) TMA
+// store / reduce-add on the 1-SM kernel (the pair kernel and the stats epilogue use mode 1).
+struct GemmTuning {
+    int gemm_1sm = env_int("SPT_GEMM_1SM", 0);
+    int gemm_pair_mn = env_int("SPT_GEMM_PAIR_MN", 0);
+    int gemm_bn = env_int("SPT_GEMM_BN", 0);
+    int epi_tstore = env_int("SPT_EPI_TSTORE", 2);
+};
+static GemmTuning& tuning() {
+    static GemmTuning t;
+    return t;
 }
-static bool pair_mn() {
-    static const bool v = env_int("SPT_GEMM_PAIR_MN", 0) == 1;
-    return v;
-}
-static int forced_bn() {
-    static const int v = env_int("SPT_GEMM_BN", 0);
-    return v;
-}
-
-static int epi_tstore() {
-    static const int v = [] {
-        const char* e = getenv("SPT_EPI_TSTORE");
-        return (e && e[0] == '0') ? 0 : 1;
-    }();
-    return v;
-}
+static bool use_pair_gemm() { return tuning().gemm_1sm != 1; }
+static bool pair_mn() { return tuning().gemm_pair_mn == 1; }
+static int forced_bn() { return tuning().gemm_bn; }
+static int epi_tstore() { return tuning().epi_tstore; }
 
 template <int BN>
 static void dispatch_pair(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int64_t K, int kind,
@@ -200,10 +217,12 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
     // CTA pairs win for K-major x K-major (forward / logits) GEMMs; with MN-major operands the 1-SM
     // kernel measured faster inside the layer step (profiles/README.md, per-site breakdown).
     if (M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn()) && use_pair_gemm()) {
+        if (ep.tstore == 2) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
         else dispatch_pair<256>(A, B, M, N, K, kind, ep, st);
         return;
     }
+    if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
     if (bn == 128) dispatch_1sm<128>(A, B, M, N, K, kind, ep, st);
     else dispatch_1sm<256>(A, B, M, N, K, kind, ep, st);
 }
@@ -224,5 +243,17 @@ extern "C" spt_status spt_gemm_bf16(const void* A, int64_t lda, int32_t a_mn_maj
         ep.alpha = alpha;
         spt::gemm({A, lda, a_mn_major != 0}, {B, ldb, b_mn_major != 0}, M, N, K, c_f32 ? spt::EPI_F32 : spt::EPI_BF16,
                   ep, reinterpret_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
+    return spt::capi_guard([&] {
+        const std::string n(name);
+        auto& t = spt::tuning();
+        if (n == "gemm_1sm") t.gemm_1sm = value;
+        else if (n == "gemm_pair_mn") t.gemm_pair_mn = value;
+        else if (n == "gemm_bn") t.gemm_bn = value;
+        else if (n == "epi_tstore") t.epi_tstore = value;
+        else SPT_THROW(SPT_ERR_CONFIG, "unknown tuning switch '" + n + "'");
     });
 }

@@ -40,7 +40,8 @@ struct EpiParams {
     float alpha = 1.f;
     float* stats = nullptr;  // EPI_F32_STATS: [M][ld_stats] float2 (max, sumexp) per 256-column tile
     int64_t ld_stats = 0;
-    int tstore = 1;  // fp32 epilogues: coalesced stores through the warp's smem transpose tile
+    int tstore = 1;  // fp32 epilogues: 0 per-thread stores, 1 smem transpose + coalesced stores, 2 TMA store /
+                     // reduce-add (1-SM kernel, EPI_F32)
 };
 
 constexpr int GEMM_BM = 128;
@@ -50,6 +51,11 @@ constexpr int EPI_TBUF_BYTES = 4 * EPI_TBUF_FLOATS * 4;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 256;
 
+// fp32 epilogue through TMA: per epilogue warp two 32 x 32 fp32 staging tiles (128B-swizzled, 4 KiB each);
+// the tile goes to global memory with cp.async.bulk.tensor (store) or cp.reduce.async.bulk.tensor .add
+// (accumulate: the L2 does the read-modify-write, so the epilogue never waits on a load of C)
+constexpr int EPI_STG_BYTES = 4 * 2 * 32 * 32 * 4;
+
 template <int BN>
 struct GemmCfg {
     static constexpr int STAGES = BN == 256 ? 4 : 6;
@@ -57,8 +63,45 @@ struct GemmCfg {
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_TBUF_BYTES;
+    // [stages][barriers: 1 KiB][epilogue staging / transpose tiles: 32 KiB, 1 KiB-aligned] + alignment slack
+    static constexpr int OFF_EPI = STAGES * STAGE_BYTES + 1024;
+    static constexpr int SMEM_BYTES = OFF_EPI + EPI_STG_BYTES + 1024;
+    static_assert(EPI_STG_BYTES >= EPI_TBUF_BYTES, "transpose tiles alias the staging region");
 };
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t smem, int32_t c0, int32_t c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     map),
+                 "r"(smem), "r"(c0), "r"(c1)
+                 : "memory");
+}
+
+// One 32 x 32 fp32 block (lane = row, v[] = 32 consecutive columns) -> 128B-swizzled staging tile -> TMA.
+__device__ __forceinline__ void epi_tma_block(const CUtensorMap* tmC, uint32_t stg, int64_t row0, int64_t col0,
+                                              const float* v, float alpha, bool accumulate) {
+    const int lane = lane_id();
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this buffer's last use read
+    __syncwarp();
+    const uint32_t rowp = stg + lane * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(rowp + ((c ^ (lane & 7)) << 4)),
+                     "f"(v[4 * c] * alpha), "f"(v[4 * c + 1] * alpha), "f"(v[4 * c + 2] * alpha),
+                     "f"(v[4 * c + 3] * alpha)
+                     : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        if (accumulate) tma_reduce_add_2d(tmC, stg, (int32_t)col0, (int32_t)row0);
+        else tma_store_2d(tmC, stg, (int32_t)col0, (int32_t)row0);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 
@@ -194,7 +237,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 template <int BN, bool A_MN, bool B_MN, int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, EpiParams ep) {
+                   int K, EpiParams ep, const __grid_constant__ CUtensorMap tmC) {
     using Cfg = GemmCfg<BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -204,7 +247,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* tbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);  // epilogue transpose tiles
+    float* tbuf = reinterpret_cast<float*>(smem + Cfg::OFF_EPI);  // epilogue transpose tiles (non-TMA paths)
 
     const int warp = warp_id(), lane = lane_id();
     const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
@@ -337,8 +380,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld32(tbase + c, r0);
                 tmem_ld32(tbase + c + 32, r1);
                 tmem_ld_wait();
+                if constexpr (KIND == EPI_F32) {
+                    if (col < N && ep.tstore == 2) {  // TMA store / reduce-add (rows and columns clipped by TMA)
+                        const uint32_t stg = smem_u32(smem + Cfg::OFF_EPI) + (uint32_t)(warp & 3) * 8192u;
+                        const int64_t row0 = row - lane;
+                        epi_tma_block(&tmC, stg, row0, col, reinterpret_cast<const float*>(r0), ep.alpha,
+                                      ep.accumulate != 0);
+                        epi_tma_block(&tmC, stg + 4096, row0, col + 32, reinterpret_cast<const float*>(r1), ep.alpha,
+                                      ep.accumulate != 0);
+                    }
+                }
                 if constexpr (KIND == EPI_F32 || KIND == EPI_F32_STATS) {
-                    if (col < N && ep.tstore) {  // warp-uniform (N % 64 == 0); rows bounds-checked inside
+                    if (col < N && ep.tstore == 1) {  // warp-uniform (N % 64 == 0); rows bounds-checked inside
                         float* tb = tbuf + (warp & 3) * EPI_TBUF_FLOATS;
                         const int64_t row0 = row - lane;
                         store_block_t<KIND>(ep, tb, row0, col, M, reinterpret_cast<const float*>(r0));
@@ -371,6 +424,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 acc = 0;
                 acc_phase ^= 1;
             }
+        }
+        if constexpr (KIND == EPI_F32) {
+            if (ep.tstore == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
     }
     tc_fence_before();

@@ -33,6 +33,9 @@ SITES = [
     ("o_fwd", 32768, 4096, 4096, 0, 0, 0, 0, 1),
 ]
 check = "--check" in sys.argv
+# --ab key=v1,v2[,v3]: interleaved A/B of a tuning switch inside this process (best of --rounds per value)
+ab = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--ab=")), None)
+rounds = int(next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--rounds=")), "3"))
 only = [a for a in sys.argv[1:] if not a.startswith("--")]
 res = {}
 tot_ms = 0.0
@@ -48,17 +51,32 @@ for name, M, N, K, amn, bmn, f32, acc, calls in SITES:
         S.check(L.spt_gemm_bf16(A.data_ptr(), A.shape[1], amn, B.data_ptr(), B.shape[1], bmn, C.data_ptr(), N, f32, a,
                                 None, 0, M, N, K, 1.0, None))
 
-    for _ in range(3):
-        run()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    e0.record()
-    for _ in range(reps):
-        run()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    def timed(reps=10):
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    if ab:
+        key, vals = ab.split("=")
+        best = {}
+        for _ in range(rounds):
+            for v in vals.split(","):
+                S.check(L.spt_tuning_set(key.encode(), int(v)))
+                best[v] = min(best.get(v, 1e9), timed())
+        S.check(L.spt_tuning_set(key.encode(), int(vals.split(",")[0])))
+        print(f"{name:10s} " + "  ".join(f"{key}={v}: {2 * M * N * K / t / 1e9:7.1f} TF/s" for v, t in best.items()),
+              flush=True)
+        del A, B, C
+        torch.cuda.empty_cache()
+        continue
+    ms = timed()
     tf = 2 * M * N * K / ms / 1e9
     line = f"{name:10s} M={M:6d} N={N:6d} K={K:6d} {'MN' if amn else 'K'}{'MN' if bmn else 'K'} " \
            f"{'f32' if f32 else 'bf16'}{'+acc' if acc else ''}: {ms:7.3f} ms {tf:7.1f} TF/s"

@@ -58,11 +58,14 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     tot, cnt = collections.defaultdict(float), collections.Counter()
-    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue  # launch lists that also carry dram counters: durations only
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         name = r[ki].split("(")[0][:60]
         tot[name] += v
