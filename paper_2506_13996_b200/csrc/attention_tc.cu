@@ -470,11 +470,17 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int j = jb + li / 2, w = li & 1;
                 const int slot = li % NSL;
                 mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
+#ifdef SPT_EXP_HALF_KV  // experiment (wrong results): half the K/V bytes, to test for L2->SM bandwidth limits
+                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES / 2);
+                const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES, col, j * BKB);
+#else
                 mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
                 const int col = (hq + (w ? hkv : 0) + kvh) * D;
                 for (int r = 0; r < 2; ++r)
                     tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
                                 j * BKB);
+#endif
             }
         }
     } else if (warp == BW_MMA) {
