@@ -44,6 +44,15 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return x < -126.f ? 0.f : y;
 }
 
+#ifndef SPT_DQ_MC_DEFAULT
+#define SPT_DQ_MC_DEFAULT 0
+#endif
+#ifndef SPT_DKDV_MC_DEFAULT
+#define SPT_DKDV_MC_DEFAULT 1
+#endif
+#ifndef SPT_FWD_ORDER
+#define SPT_FWD_ORDER 0
+#endif
 #ifndef SPT_DQ_POLY_EVERY
 #define SPT_DQ_POLY_EVERY 0
 #endif
@@ -237,6 +246,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (uses(1, j)) issue_s(1, j);
                 mma_commit_w(&kv_empty[slot(j, 0)]);  // K_j consumed by both tiles' S MMAs
             }
+#if SPT_FWD_ORDER == 1
+            // per tile: PV_t(j) then S_t(j+2) right away, so tile 0's next scores do not wait for tile 1's softmax
+            for (int j = jlo; j <= jhi; ++j) {
+                const bool more = j + 2 <= jhi;
+                if (uses(0, j)) issue_pv(0, j);
+                if (more && uses(0, j + 2)) issue_s(0, j + 2);
+                if (uses(1, j)) issue_pv(1, j);
+                mma_commit_w(&kv_empty[slot(j, 1)]);  // V_j consumed
+                if (more) {
+                    if (uses(1, j + 2)) issue_s(1, j + 2);
+                    mma_commit_w(&kv_empty[slot(j + 2, 0)]);  // K_{j+2} consumed by both tiles
+                }
+            }
+#else
             for (int j = jlo; j <= jhi; ++j) {
                 if (uses(0, j)) issue_pv(0, j);
                 if (uses(1, j)) issue_pv(1, j);
@@ -247,6 +270,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mma_commit_w(&kv_empty[slot(j + 2, 0)]);
                 }
             }
+#endif
             mma_commit_w(&o_done[0]);
             mma_commit_w(&o_done[1]);
         }
@@ -413,6 +437,10 @@ constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dq
 
+// MC: q heads (2m, 2m+1) of the same kv head and q tile form a cluster; their K/V streams are identical, so
+// rank 0 multicasts the K blocks and rank 1 the V blocks into both CTAs (half the L2->SM bytes per CTA);
+// a K/V slot is released by both CTAs' MMAs (multicast commit, count 2).
+template <bool MC>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                  const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
@@ -441,7 +469,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         mbar_init(q_full, 1);
         for (int i = 0; i < NSL; ++i) {
             mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&kv_empty[i], MC ? 2 : 1);
         }
         for (int t = 0; t < NB; ++t) {
             mbar_init(&s_full[t], 1);
@@ -455,10 +483,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tmem_relinquish();
     }
     tc_fence_before();
-    __syncthreads();
+    if (MC) cluster_sync();  // both CTAs' barriers initialised before any multicast load / remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // provably warp-uniform: descriptor math stays in uniform registers
     const uint32_t sbase = smem_u32(smem);
+    const uint32_t crank = MC ? cluster_ctarank() : 0;
     if (warp == BW_TMA) {
         if (lane == 0) {
             mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
@@ -477,9 +507,16 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 #else
                 mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
                 const int col = (hq + (w ? hkv : 0) + kvh) * D;
-                for (int r = 0; r < 2; ++r)
-                    tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
-                                j * BKB);
+                if constexpr (MC) {
+                    if ((uint32_t)w == crank)  // rank 0: K blocks, rank 1: V blocks, each into both CTAs
+                        for (int r = 0; r < 2; ++r)
+                            tma_load_2d_mc(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192,
+                                           col + 64 * r, j * BKB, 0x3);
+                } else {
+                    for (int r = 0; r < 2; ++r)
+                        tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
+                                    j * BKB);
+                }
 #endif
             }
         }
@@ -503,7 +540,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 for (int kk = 0; kk < D / 16; ++kk)
                     mma_bf16_ss_w(d_s + 64, kdesc_r(da, kk, 16384), kdesc_r(vb, kk, 8192), id_s, kk > 0);
                 mma_commit_w(&s_full[it % NB]);
-                mma_commit_w(&kv_empty[vs]);  // V_j only feeds dP
+                if constexpr (MC) mma_commit_mc_w(&kv_empty[vs], 0x3);  // V_j only feeds dP
+                else mma_commit_w(&kv_empty[vs]);
             };
             auto issue_dq = [&](int it) {
                 mbar_wait(&ds_full[it % NB], (it / NB) & 1);
@@ -515,7 +553,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 for (int kk = 0; kk < BKB / 16; ++kk)
                     mma_bf16_ts_w(tmem + DQ_COL, tmem + (it % NB) * 128 + kk * 16, mndesc_r(kb, kk, 8192), id_q,
                                   (it > 0 || kk > 0));
-                mma_commit_w(&kv_empty[ks]);
+                if constexpr (MC) mma_commit_mc_w(&kv_empty[ks], 0x3);
+                else mma_commit_w(&kv_empty[ks]);
             };
             for (int it = 0; it < min(NB, nblk); ++it) issue_sdp(it);
             for (int it = 0; it < nblk; ++it) {
@@ -602,6 +641,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (MC) cluster_sync();  // the peer's multicast loads / remote arrives target this CTA until it is done
     if (warp == BW_MMA) {
         __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
@@ -624,6 +664,11 @@ constexpr int OFF_BAR = OFF_LD + NQS * 512;                         // P^T / dS^
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dkv
 
+// MC: CTAs (2m, 2m+1) form a cluster and stream ONE shared Q/dO sequence (the pair's union of visible q
+// blocks, starting at the even CTA's first block — the odd CTA's extra blocks are fully masked), each CTA
+// multicasting half of every stage into both CTAs' smem: half the L2->SM bytes per CTA.  Stage release needs
+// both CTAs' MMAs (multicast commit onto qs_empty, count 2).
+template <bool MC>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                    const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
@@ -646,11 +691,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const int grp = hq / hkv;
     const int64_t k0 = (int64_t)kb * 128;
     (void)nkb;
-    // visible q range: q >= k0 and (block-causal) start[q] <= k0 + 127
-    const int qb_first = (int)(k0 / BQB);
+    const uint32_t crank = MC ? cluster_ctarank() : 0;
+    // visible q range: q >= k0 and (block-causal) start[q] <= k0 + 127 (MC: the pair's union)
+    const int qb_first = (int)(((MC ? (k0 & ~int64_t(255)) : k0)) / BQB);
     int qb_last = (int)((s - 1) / BQB);
     if (seg) {
-        const int64_t klast = k0 + 127;
+        const int64_t klast = (MC ? (k0 | 128) : k0) + 127;  // the odd CTA's last key
         int64_t lo = k0, hi = s - 1;
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) / 2;
@@ -665,7 +711,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         mbar_init(kv_full, 1);
         for (int i = 0; i < NQS; ++i) {
             mbar_init(&qs_full[i], 1);
-            mbar_init(&qs_empty[i], 1);
+            mbar_init(&qs_empty[i], MC ? 2 : 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
@@ -679,7 +725,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         tmem_relinquish();
     }
     tc_fence_before();
-    __syncthreads();
+    if (MC) cluster_sync();  // both CTAs' barriers initialised before any multicast load / remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // provably warp-uniform: descriptor math stays in uniform registers
     const uint32_t sbase = smem_u32(smem);
@@ -699,13 +746,25 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int hcur = hh;
                 if (++qblk == nqb) { qblk = 0; ++hh; }
                 uint8_t* base = smem + OFF_QS + st * 2 * QS_BYTES;
-                for (int r = 0; r < 2; ++r) {
-                    tma_load_2d(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq);
-                    tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq);
+                if constexpr (MC) {  // rank 0 brings Q + lse, rank 1 brings dO + D, into both CTAs
+                    if (crank == 0) {
+                        for (int r = 0; r < 2; ++r)
+                            tma_load_2d_mc(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq, 0x3);
+                        bulk_load_mc(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st], 0x3);
+                    } else {
+                        for (int r = 0; r < 2; ++r)
+                            tma_load_2d_mc(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq, 0x3);
+                        bulk_load_mc(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st], 0x3);
+                    }
+                } else {
+                    for (int r = 0; r < 2; ++r) {
+                        tma_load_2d(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq);
+                        tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq);
+                    }
+                    // per-column softmax statistics of this q block (lse*log2e, D) for the elementwise warps
+                    bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st]);
+                    bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st]);
                 }
-                // per-column softmax statistics of this q block (lse*log2e, D) for the elementwise warps
-                bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st]);
-                bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st]);
             }
         }
     } else if (warp == BW_MMA) {
@@ -742,7 +801,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 for (int kk = 0; kk < BQB / 16; ++kk)
                     mma_bf16_ts_w(tmem + 384, tmem + b * 128 + kk * 16 + 8, mndesc_r(qb_, kk, 8192), id_a,
                                   (it > 0 || kk > 0));
-                mma_commit_w(&qs_empty[st]);
+                if constexpr (MC) mma_commit_mc_w(&qs_empty[st], 0x3);  // the stage is free in both CTAs
+                else mma_commit_w(&qs_empty[st]);
             };
             if (total > 0) issue_sdp(0);
             if (total > 1) issue_sdp(1);
@@ -854,6 +914,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (MC) cluster_sync();  // the peer's multicast loads / remote arrives target this CTA until it is done
     if (warp == BW_MMA) {
         __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
         tc_fence_after();
@@ -1307,6 +1368,24 @@ static int bwd_mode() {
     return v;
 }
 
+// SPT_ATTN_DKDV_MC=0|1: cluster-pair multicast of the dK/dV pass's Q/dO stream (default from measurement)
+static bool dkdv_multicast() {
+    static const bool v = [] {
+        const char* e = getenv("SPT_ATTN_DKDV_MC");
+        return e ? e[0] == '1' : SPT_DKDV_MC_DEFAULT != 0;
+    }();
+    return v;
+}
+
+// SPT_ATTN_DQ_MC=0|1: cluster-pair multicast of the dQ pass's K/V stream (head pairs of a GQA group)
+static bool dq_multicast() {
+    static const bool v = [] {
+        const char* e = getenv("SPT_ATTN_DQ_MC");
+        return e ? e[0] == '1' : SPT_DQ_MC_DEFAULT != 0;
+    }();
+    return v;
+}
+
 size_t attn_bwd_tc_workspace(int64_t s, int hq) {
     if (bwd_mode() != 1) return 0;
     return (size_t)s * hq * fatc::D * 4 + (size_t)hq * (s / 64) * 4 + 256;
@@ -1324,8 +1403,13 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
     CUtensorMap do64 = make_tmap_bf16_2d(dout, (uint64_t)hq * d, (uint64_t)s, (uint64_t)hq * d, 64, 64);
     static bool attr = false;
     if (!attr) {
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::dq::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dq::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dq::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dkv::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdvq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkvq::SMEM));
@@ -1346,12 +1430,46 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         SPT_CUDA(cudaGetLastError());
         return true;
     }
-    fatc::dkdv_tc_kernel<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM, st>>>(
-        t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+    if (dkdv_multicast()) {  // CTA pairs along the key blocks share one multicast Q/dO stream
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(s / 128), (unsigned)hkv);
+        cfg.blockDim = dim3(fatc::BW_THREADS);
+        cfg.dynamicSmemBytes = fatc::dkv::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, fatc::dkdv_tc_kernel<true>, t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale,
+                                    (bf16*)dqkv));
+    } else {
+        fatc::dkdv_tc_kernel<false><<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM,
+                                      st>>>(t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+    }
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
-    fatc::dq_tc_kernel<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dq::SMEM, st>>>(
-        t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+    if (dq_multicast() && (hq / hkv) % 2 == 0) {  // head pairs of one kv head share a multicast K/V stream
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)hq, (unsigned)(s / 128));
+        cfg.blockDim = dim3(fatc::BW_THREADS);
+        cfg.dynamicSmemBytes = fatc::dq::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, fatc::dq_tc_kernel<true>, t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale,
+                                    (bf16*)dqkv));
+    } else {
+        fatc::dq_tc_kernel<false><<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dq::SMEM, st>>>(
+            t128, t64, do128, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+    }
     count_launch("attn_dq_tc");
     SPT_CUDA(cudaGetLastError());
     return true;
