@@ -44,6 +44,9 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return x < -126.f ? 0.f : y;
 }
 
+#ifndef SPT_DQ_TMEM_DEFAULT
+#define SPT_DQ_TMEM_DEFAULT 1
+#endif
 #ifndef SPT_DQ_MC_DEFAULT
 #define SPT_DQ_MC_DEFAULT 0
 #endif
@@ -52,6 +55,15 @@ __device__ __forceinline__ float ex2_poly(float x) {
 #endif
 #ifndef SPT_FWD_ORDER
 #define SPT_FWD_ORDER 0
+#endif
+#ifdef SPT_DQ_PROF
+__device__ unsigned long long g_dq_prof[8];  // [0] MMA wait kv, [1] MMA wait ds_full, [2] elem wait s_full,
+                                             // [3] elem busy, [4] MMA total, [5] CTAs, [6] iterations
+#define DQP_T0() const long long _t0 = clock64()
+#define DQP_ADD(i) atomicAdd(&g_dq_prof[i], (unsigned long long)(clock64() - _t0))
+#else
+#define DQP_T0()
+#define DQP_ADD(i)
 #endif
 #ifndef SPT_DQ_POLY_EVERY
 #define SPT_DQ_POLY_EVERY 0
@@ -528,8 +540,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const uint32_t qa = sbase + OFF_Q, da = sbase + OFF_DO;
             auto issue_sdp = [&](int it) {
                 const int ks = (2 * it) % NSL, vs = (2 * it + 1) % NSL;
-                mbar_wait(&kv_full[ks], ((2 * it) / NSL) & 1);
-                mbar_wait(&kv_full[vs], ((2 * it + 1) / NSL) & 1);
+                {
+                    DQP_T0();
+                    mbar_wait(&kv_full[ks], ((2 * it) / NSL) & 1);
+                    mbar_wait(&kv_full[vs], ((2 * it + 1) / NSL) & 1);
+                    if (lane == 0) DQP_ADD(0);
+                }
                 tc_fence_after();
                 const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES, vb = sbase + OFF_KV + vs * KV_BYTES;
                 const uint32_t d_s = tmem + (it % NB) * 128;
@@ -544,7 +560,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 else mma_commit_w(&kv_empty[vs]);
             };
             auto issue_dq = [&](int it) {
-                mbar_wait(&ds_full[it % NB], (it / NB) & 1);
+                {
+                    DQP_T0();
+                    mbar_wait(&ds_full[it % NB], (it / NB) & 1);
+                    if (lane == 0) DQP_ADD(1);
+                }
                 tc_fence_after();
                 const int ks = (2 * it) % NSL;
                 const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES;
@@ -556,12 +576,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 if constexpr (MC) mma_commit_mc_w(&kv_empty[ks], 0x3);
                 else mma_commit_w(&kv_empty[ks]);
             };
+#ifdef SPT_DQ_PROF
+            const long long _tm0 = clock64();
+#endif
             for (int it = 0; it < min(NB, nblk); ++it) issue_sdp(it);
             for (int it = 0; it < nblk; ++it) {
                 issue_dq(it);
                 if (it + NB < nblk) issue_sdp(it + NB);
             }
             mma_commit_w(dq_done);
+#ifdef SPT_DQ_PROF
+            if (lane == 0) {
+                atomicAdd(&g_dq_prof[4], (unsigned long long)(clock64() - _tm0));
+                atomicAdd(&g_dq_prof[5], 1ull);
+                atomicAdd(&g_dq_prof[6], (unsigned long long)nblk);
+            }
+#endif
         }
     } else {
         const int sub = warp & 3, grp = warp >> 2;  // lanes [32 sub, +32), keys [16 grp, +16) of each block
@@ -575,7 +605,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         for (int it = 0; it < nblk; ++it) {
             const int b = it % NB;
-            mbar_wait(&s_full[b], (it / NB) & 1);
+            {
+                DQP_T0();
+                mbar_wait(&s_full[b], (it / NB) & 1);
+                if (threadIdx.x == 0) DQP_ADD(2);
+            }
             tc_fence_after();
 #ifdef SPT_EXP_NO_ELEM
             tc_fence_before();
@@ -644,6 +678,212 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     if (MC) cluster_sync();  // the peer's multicast loads / remote arrives target this CTA until it is done
     if (warp == BW_MMA) {
         __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ------------------------------------------------------------------ dQ pass, Q / dO resident in TMEM
+// Same schedule as dq_tc_kernel, but the S = Q K^T and dP = dO V^T MMAs take their A operand (Q, dO) from
+// TMEM ("ts" form) instead of shared memory.  A tcgen05.mma M=128 N=64 K=16 with both operands in smem reads
+// 4 KiB (A) + 2 KiB (B) of smem at 128 B/clk = 48 cycles for 32 cycles of math (tools/micro/mma_rate.cu:
+// N=64 runs at 67% of peak, N>=128 at 100%); with A in TMEM only the 2 KiB B operand is read from smem.
+// TMEM: S/dP double buffer [0, 256) | dQ [256, 384) | Q [384, 448) | dO [448, 512) (bf16 pairs per column).
+namespace dqt {
+constexpr int BKB = 64;
+constexpr int KV_BYTES = BKB * D * 2;  // 16 KiB (two 8 KiB regions)
+constexpr int NSL = 12;                // K/V ring slots: 6 blocks of K+V in flight (Q/dO no longer in smem)
+constexpr int NB = 2;
+constexpr int DQ_COL = 256, QT_COL = 384, DOT_COL = 448;
+constexpr int OFF_KV = 0;
+constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+}  // namespace dqt
+
+__global__ void __launch_bounds__(BW_THREADS, 1)
+    dq_tmem_kernel(const __grid_constant__ CUtensorMap tkv, const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
+                   int64_t s, int hq, int hkv, const int32_t* __restrict__ seg, const float* __restrict__ lse2v,
+                   const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
+    using namespace dqt;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* qt_ready = bar;
+    uint64_t* kv_full = bar + 1;
+    uint64_t* kv_empty = kv_full + NSL;
+    uint64_t* s_full = kv_empty + NSL;  // [NB]
+    uint64_t* ds_full = s_full + NB;    // [NB]
+    uint64_t* dq_done = ds_full + NB;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+    const int warp = warp_id(), lane = lane_id();
+    const int nqb = (int)(s / 128);
+    const int qb = nqb - 1 - (int)blockIdx.y;  // longest rows first; heads vary fastest
+    const int h = blockIdx.x;
+    const int kvh = h / (hq / hkv);
+    const int64_t q0 = (int64_t)qb * 128;
+    const int jb = seg ? (int)(seg[q0] / BKB) : 0;
+    const int je = (int)((q0 + 127) / BKB);
+    const int nblk = je - jb + 1;
+    if (threadIdx.x == 0) {
+        mbar_init(qt_ready, BW_NEW * 32);
+        for (int i = 0; i < NSL; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int t = 0; t < NB; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&ds_full[t], BW_NEW * 32);
+        }
+        mbar_init(dq_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == BW_MMA) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t sbase = smem_u32(smem);
+    if (warp == BW_TMA) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tkv);
+            for (int li = 0; li < 2 * nblk; ++li) {  // K_j, V_j, K_j+1, ...
+                const int j = jb + li / 2, w = li & 1;
+                const int slot = li % NSL;
+                mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
+                const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
+                                j * BKB);
+            }
+        }
+    } else if (warp == BW_MMA) {
+        constexpr uint32_t id_s = make_idesc_bf16(128, BKB, false, false);
+        constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);
+        mbar_wait(qt_ready, 0);
+        tc_fence_after();
+        auto issue_sdp = [&](int it) {
+            const int ks = (2 * it) % NSL, vs = (2 * it + 1) % NSL;
+            mbar_wait(&kv_full[ks], ((2 * it) / NSL) & 1);
+            mbar_wait(&kv_full[vs], ((2 * it + 1) / NSL) & 1);
+            tc_fence_after();
+            const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES, vb = sbase + OFF_KV + vs * KV_BYTES;
+            const uint32_t d_s = tmem + (it & 1) * 128;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)  // S = Q K^T, Q from TMEM: d chunk kk = 8 packed columns
+                mma_bf16_ts_w(d_s, tmem + QT_COL + kk * 8, kdesc_r(kb, kk, 8192), id_s, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)  // dP = dO V^T
+                mma_bf16_ts_w(d_s + 64, tmem + DOT_COL + kk * 8, kdesc_r(vb, kk, 8192), id_s, kk > 0);
+            mma_commit_w(&s_full[it & 1]);
+            mma_commit_w(&kv_empty[vs]);  // V_j only feeds dP
+        };
+        auto issue_dq = [&](int it) {
+            mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
+            tc_fence_after();
+            const int ks = (2 * it) % NSL;
+            const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES;
+            // A = dS in TMEM: keys [16g, 16g+16) packed in S columns [16g, 16g+8) of buffer it&1
+#pragma unroll
+            for (int kk = 0; kk < BKB / 16; ++kk)
+                mma_bf16_ts_w(tmem + DQ_COL, tmem + (it & 1) * 128 + kk * 16, mndesc_r(kb, kk, 8192), id_q,
+                              (it > 0 || kk > 0));
+            mma_commit_w(&kv_empty[ks]);
+        };
+        for (int it = 0; it < min(NB, nblk); ++it) issue_sdp(it);
+        for (int it = 0; it < nblk; ++it) {
+            issue_dq(it);
+            if (it + NB < nblk) issue_sdp(it + NB);
+        }
+        mma_commit_w(dq_done);
+    } else {
+        const int sub = warp & 3, grp = warp >> 2;  // lanes [32 sub, +32), keys [16 grp, +16) of each block
+        const int r = sub * 32 + lane;
+        const int64_t q = q0 + r;
+        const int q32 = (int)q, q0i = (int)q0;
+        const uint32_t lo = (uint32_t)(sub * 32) << 16;
+        {  // Q and dO rows -> TMEM (this warp: d elements [32 grp, 32 grp + 32) = packed columns [16 grp, +16))
+            const int64_t width = (int64_t)(hq + 2 * hkv) * D;
+            const uint4* qs = reinterpret_cast<const uint4*>(qkv + q * width + (int64_t)h * D + 32 * grp);
+            const uint4* ds = reinterpret_cast<const uint4*>(dout + (q * hq + h) * D + 32 * grp);
+            uint32_t qv[16], dv[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint4 a = __ldg(qs + k), b = __ldg(ds + k);
+                qv[4 * k] = a.x; qv[4 * k + 1] = a.y; qv[4 * k + 2] = a.z; qv[4 * k + 3] = a.w;
+                dv[4 * k] = b.x; dv[4 * k + 1] = b.y; dv[4 * k + 2] = b.z; dv[4 * k + 3] = b.w;
+            }
+            tmem_st16(tmem + lo + QT_COL + grp * 16, qv);
+            tmem_st16(tmem + lo + DOT_COL + grp * 16, dv);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(qt_ready);
+        }
+        const int start = seg ? seg[q] : 0;
+        const float nlse2 = -lse2v[(int64_t)h * s + q];
+        const float Dq = Dv[(int64_t)h * s + q];
+        const float sl2 = scale * LOG2E;
+        for (int it = 0; it < nblk; ++it) {
+            const int b = it & 1;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t sv[16], dv[16];
+            tmem_ld16(tmem + lo + b * 128 + grp * 16, sv);
+            tmem_ld16(tmem + lo + b * 128 + 64 + grp * 16, dv);
+            tmem_ld_wait();
+            const int k0 = (jb + it) * BKB + grp * 16;
+            uint32_t w[8];
+            auto body = [&](auto mask_c) {
+                constexpr bool MASK = decltype(mask_c)::value;
+                const int hi = q32 - k0, lo_ = start - k0;
+                const uint64_t sl2x = f2pack(sl2, sl2), nlx = f2pack(nlse2, nlse2), dqx = f2pack(Dq, Dq);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    float x0, x1;
+                    f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * k]), __uint_as_float(sv[2 * k + 1])), sl2x, nlx), x0, x1);
+                    float p0 = ex2(x0), p1 = ex2(x1);
+                    if constexpr (MASK) {
+                        p0 = (2 * k > hi || 2 * k < lo_) ? 0.f : p0;
+                        p1 = (2 * k + 1 > hi || 2 * k + 1 < lo_) ? 0.f : p1;
+                    }
+                    const uint64_t d2 = fmul2(f2pack(p0, p1),
+                                              fsub2(f2pack(__uint_as_float(dv[2 * k]), __uint_as_float(dv[2 * k + 1])), dqx));
+                    float d0, d1;
+                    f2unpack(d2, d0, d1);
+                    w[k] = pack_bf16x2(d0, d1);
+                }
+            };
+            if (seg != nullptr || k0 + 15 > q0i) body(std::true_type{});
+            else body(std::false_type{});
+            tmem_st8(tmem + lo + b * 128 + grp * 16, w);  // over this warp's consumed S columns
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&ds_full[b]);
+        }
+        mbar_wait(dq_done, 0);
+        tc_fence_after();
+        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * D + grp * 32;
+        uint32_t v[32];
+        tmem_ld32(tmem + lo + DQ_COL + grp * 32, v);
+        tmem_ld_wait();
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint4 o;
+            o.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * scale, __uint_as_float(v[8 * k + 1]) * scale);
+            o.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * scale, __uint_as_float(v[8 * k + 3]) * scale);
+            o.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * scale, __uint_as_float(v[8 * k + 5]) * scale);
+            o.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * scale, __uint_as_float(v[8 * k + 7]) * scale);
+            d4[k] = o;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == BW_MMA) {
+        __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -1334,6 +1574,22 @@ __global__ void dq_convert_kernel(const float* __restrict__ acc, int64_t s, int 
 
 }  // namespace fatc
 
+// debug builds (SPT_DQ_PROF): accumulated wait cycles of the dQ pass, see g_dq_prof
+extern "C" int spt_debug_dq_prof(unsigned long long* out, int reset) {
+#ifdef SPT_DQ_PROF
+    cudaMemcpyFromSymbol(out, fatc::g_dq_prof, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(fatc::g_dq_prof, z, sizeof(z));
+    }
+    return 1;
+#else
+    (void)out;
+    (void)reset;
+    return 0;
+#endif
+}
+
 bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
                  float* lse, cudaStream_t st) {
     if (d != fatc::D || s % 256 != 0) return false;
@@ -1377,6 +1633,14 @@ static bool dkdv_multicast() {
     return v;
 }
 
+// SPT_ATTN_DQ_TMEM=0|1: dQ pass with Q / dO resident in TMEM (default from measurement); also settable at run
+// time through spt_tuning_set("attn_dq_tmem", v) for in-process A/B
+int g_attn_dq_tmem = [] {
+    const char* e = getenv("SPT_ATTN_DQ_TMEM");
+    return e ? (e[0] == '1' ? 1 : 0) : (SPT_DQ_TMEM_DEFAULT != 0 ? 1 : 0);
+}();
+static bool dq_tmem() { return g_attn_dq_tmem != 0; }
+
 // SPT_ATTN_DQ_MC=0|1: cluster-pair multicast of the dQ pass's K/V stream (head pairs of a GQA group)
 static bool dq_multicast() {
     static const bool v = [] {
@@ -1407,6 +1671,8 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dq::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dq::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dqt::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1451,7 +1717,10 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
     }
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
-    if (dq_multicast() && (hq / hkv) % 2 == 0) {  // head pairs of one kv head share a multicast K/V stream
+    if (dq_tmem()) {  // Q / dO resident in TMEM: S and dP MMAs read only their B operand from smem
+        fatc::dq_tmem_kernel<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dqt::SMEM, st>>>(
+            t64, (const bf16*)qkv, (const bf16*)dout, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+    } else if (dq_multicast() && (hq / hkv) % 2 == 0) {  // head pairs of one kv head share a multicast K/V stream
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)hq, (unsigned)(s / 128));
         cfg.blockDim = dim3(fatc::BW_THREADS);

@@ -246,10 +246,18 @@ extern "C" spt_status spt_gemm_bf16(const void* A, int64_t lda, int32_t a_mn_maj
     });
 }
 
+namespace spt {
+extern int g_attn_dq_tmem;  // attention_tc.cu
+}
+
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
     return spt::capi_guard([&] {
         const std::string n(name);
         auto& t = spt::tuning();
+        if (n == "attn_dq_tmem") {
+            spt::g_attn_dq_tmem = value;
+            return;
+        }
         if (n == "gemm_1sm") t.gemm_1sm = value;
         else if (n == "gemm_pair_mn") t.gemm_pair_mn = value;
         else if (n == "gemm_bn") t.gemm_bn = value;
