@@ -428,6 +428,297 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
+namespace fwt {  // forward with Q resident in TMEM (fwd_tmem_kernel)
+constexpr int BKB = 64;
+constexpr int KV_BYTES = BKB * D * 2;  // 16 KiB per K or V block (two 8 KiB regions)
+constexpr int NSL = 13;
+constexpr int OFF_KV = 0;
+constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
+constexpr int SMEM = OFF_BAR + 512 + 1024;
+}  // namespace fwt
+
+// Forward with Q resident in TMEM: per tile one S buffer (64 cols) + Q (64 cols, bf16 pairs) + O (128 cols).
+// S = Q K^T becomes a ts-form MMA that reads only its 2 KiB B operand (K) from smem: with both operands in
+// smem an M=128 N=64 K=16 MMA is smem-bandwidth bound (48 cycles for 32 of math, tools/micro/mma_rate.cu).
+__global__ void __launch_bounds__(THREADS, 1)
+    fwd_tmem_kernel(const __grid_constant__ CUtensorMap tkv, const bf16* __restrict__ qkv_in, int64_t s, int hq,
+                  int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
+                  float* __restrict__ lse) {
+    using namespace fwt;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* q_full = bar;  // here: Q tiles written into TMEM by the softmax warps (256 arrivals)
+    uint64_t* kv_full = bar + 1;
+    uint64_t* kv_empty = kv_full + NSL;
+    uint64_t* s_full = kv_empty + NSL;  // [t*2 + b]
+    uint64_t* p_full = s_full + 4;      // [t*2 + b]  per buffer: the softmax may run 2 blocks ahead
+    uint64_t* pv_done = p_full + 4;     // [t]
+    uint64_t* o_done = pv_done + 2;     // [t]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+    const int warp = warp_id(), lane = lane_id();
+    const int npairs = (int)(s / (2 * BQ));
+    // grid = (q head, query-tile pair): heads vary fastest so one wave of CTAs streams the K/V of every kv
+    // head at once instead of 148 CTAs hammering the same K/V lines (L2-slice hot spot); longest rows first
+    const int pair = npairs - 1 - (int)blockIdx.y;
+    const int h = blockIdx.x;
+    const int kvh = h / (hq / hkv);
+    const int64_t q0 = (int64_t)pair * 2 * BQ;
+    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = seg ? (int)(seg[q0 + BQ] / BKB) : 0;
+    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = (int)((q0 + 2 * BQ - 1) / BKB);
+    const int jlo = jb0, jhi = je1;  // jb0 <= jb1 (starts are monotone), je0 < je1
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 256);
+        for (int i = 0; i < NSL; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&pv_done[t], 1);
+            mbar_init(&o_done[t], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 8) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // provably warp-uniform: descriptor math stays in uniform registers
+    const uint32_t sbase = smem_u32(smem);
+
+    if (warp == 9) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tkv);
+            const int nload = 2 * (jhi - jlo + 1);
+            for (int li = 0; li < nload; ++li) {
+                const int j = jlo + li / 2, w = li & 1;
+                const int slot = li % NSL;
+                mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
+                const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r, j * BKB);
+            }
+        }
+    } else if (warp == 8) {
+        {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
+            constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKB, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(BQ, D, false, true);
+            mbar_wait(q_full, 0);  // Q tiles resident in TMEM
+            tc_fence_after();
+            const int jb[2] = {jb0, jb1}, je[2] = {je0, je1};
+            int pv_count[2] = {0, 0};
+            auto uses = [&](int t, int j) { return j >= jb[t] && j <= je[t]; };
+            auto slot = [&](int j, int w) { return (2 * (j - jlo) + w) % NSL; };
+            auto phase = [&](int j, int w) { return (uint32_t)(((2 * (j - jlo) + w) / NSL) & 1); };
+            // S_t(j) = Q_t K_j^T with Q_t from TMEM (ts form: only K is read from smem)
+            auto issue_s = [&](int t, int j) {
+                mbar_wait(&kv_full[slot(j, 0)], phase(j, 0));
+                tc_fence_after();
+                const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ts_w(tmem + t * 256, tmem + t * 256 + 64 + kk * 8, kdesc_r(kb, kk, 8192), idesc_s, kk > 0);
+                mma_commit_w(&s_full[t * 2]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                mbar_wait(&p_full[t * 2], (j - jb[t]) & 1);
+                mbar_wait(&kv_full[slot(j, 1)], phase(j, 1));
+                tc_fence_after();
+                const uint32_t vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BKB / 16; ++kk)
+                    mma_bf16_ts_w(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, mndesc_r(vb, kk, 8192), idesc_o,
+                                  (pv_count[t] > 0 || kk > 0));
+                mma_commit_w(&pv_done[t]);
+                ++pv_count[t];
+            };
+            // one S buffer per tile: S_t(j+1) overwrites P_t(j) right after PV_t(j) (in-order tensor pipe);
+            // the two tiles ping-pong so one tile's softmax overlaps the other tile's MMAs
+            if (uses(0, jlo)) issue_s(0, jlo);
+            if (uses(1, jlo)) issue_s(1, jlo);
+            mma_commit_w(&kv_empty[slot(jlo, 0)]);
+            for (int j = jlo; j <= jhi; ++j) {
+                const bool more = j + 1 <= jhi;
+                if (uses(0, j)) issue_pv(0, j);
+                if (more && uses(0, j + 1)) issue_s(0, j + 1);
+                if (uses(1, j)) issue_pv(1, j);
+                mma_commit_w(&kv_empty[slot(j, 1)]);  // V_j consumed
+                if (more) {
+                    if (uses(1, j + 1)) issue_s(1, j + 1);
+                    mma_commit_w(&kv_empty[slot(j + 1, 0)]);  // K_{j+1} consumed by both tiles
+                }
+            }
+            mma_commit_w(&o_done[0]);
+            mma_commit_w(&o_done[1]);
+        }
+    } else {
+        // ---------------- softmax warpgroups (thread = query row)
+        const int t = warp >> 2;
+        const int sub = warp & 3;
+        const int r = sub * 32 + lane;
+        const int64_t q = q0 + t * BQ + r;
+        const int start = seg ? seg[q] : 0;
+        const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+        const uint32_t t_tm = tmem + lane_off + t * 256;
+        const uint32_t o_tm = t_tm + 128;
+        {  // this thread's Q row (q head h) -> TMEM columns [t*256 + 64, +64) as bf16 pairs (A operand of S)
+            const uint4* qs = reinterpret_cast<const uint4*>(qkv_in + q * (int64_t)(hq + 2 * hkv) * D + (int64_t)h * D);
+            uint32_t qv[32];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                for (int k4 = 0; k4 < 8; ++k4) {
+                    const uint4 a4 = __ldg(qs + half * 8 + k4);
+                    qv[4 * k4] = a4.x; qv[4 * k4 + 1] = a4.y; qv[4 * k4 + 2] = a4.z; qv[4 * k4 + 3] = a4.w;
+                }
+                tmem_st32(t_tm + 64 + half * 32, qv);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(q_full);
+        }
+        const int jb_t = t ? jb1 : jb0, je_t = t ? je1 : je0;
+        float m_use = -INFINITY, l = 0.f;  // running max in log2 units (scaled)
+        for (int j = jb_t; j <= je_t; ++j) {
+            const int n = j - jb_t, b = 0;
+            const uint32_t s_tm = t_tm + b * 64;
+#ifdef SPT_WATCHDOG
+            volatile int* dbg = reinterpret_cast<volatile int*>(tmem_slot + 4);
+            if (r == 0) { dbg[2 * t] = j; dbg[2 * t + 1] = 1; }
+#endif
+            mbar_wait(&s_full[t * 2], n & 1);
+#ifdef SPT_WATCHDOG
+            if (r == 0) dbg[2 * t + 1] = 2;
+#endif
+            tc_fence_after();
+            const int64_t k0 = (int64_t)j * BKB;
+            const bool need_mask = seg != nullptr || (k0 + BKB - 1 > q0 + t * BQ);  // warp-uniform
+            uint32_t v[2][32];
+            tmem_ld32(s_tm, v[0]);
+            tmem_ld32(s_tm + 32, v[1]);
+            tmem_ld_wait();
+            // row max over the 64 columns: 8 independent partial maxima (short dependency chains; the two
+            // softmax warps per SMSP cannot hide a 64-long serial FMNMX chain)
+            float mp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mp[u] = -INFINITY;
+            if (need_mask) {
+                const int hi = (int)(q - k0), lo_ = start - (int)k0;  // keep columns lo_ <= i <= hi
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int col = c * 32 + i;
+                        if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
+                        mp[col & 7] = fmaxf(mp[col & 7], __uint_as_float(v[c][i]));
+                    }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2)
+                        mp[(c * 32 + i) >> 1 & 7] =
+                            fmaxf(mp[(c * 32 + i) >> 1 & 7], fmaxf(__uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1])));
+            }
+            const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                     fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+            const float mx = mraw * scale_log2;
+            // lazy rescale (warp-uniform: tcgen05.ld/st are warp-collective); needs PV_t(j-1) complete
+            const bool grow = mx > m_use + RESCALE_THRESHOLD;
+            const bool resc = grow && m_use != -INFINITY && n > 0;
+            const float alpha = resc ? ex2(m_use - mx) : 1.f;
+            if (__any_sync(0xffffffffu, resc)) {
+                mbar_wait(&pv_done[t], (n - 1) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t ov[32];
+                    tmem_ld32(o_tm + c * 32, ov);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                    tmem_st32(o_tm + c * 32, ov);
+                }
+            }
+            l *= alpha;
+            if (grow) m_use = mx;
+            const float nbase = m_use == -INFINITY ? 0.f : -m_use;
+            uint32_t pw[32];
+            const uint64_t sc2 = f2pack(scale_log2, scale_log2), nb2 = f2pack(nbase, nbase);
+            uint64_t rs2[4];  // 4 independent packed row-sum accumulators (short FADD2 chains)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const int c0 = 2 * k;
+                const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c0 >> 5][c0 & 31]), __uint_as_float(v[c0 >> 5][(c0 + 1) & 31])),
+                                          sc2, nb2);
+                float x0, x1;
+                f2unpack(x2, x0, x1);
+                const bool poly = SPT_FWD_POLY_EVERY > 0 && (k % (SPT_FWD_POLY_EVERY > 0 ? SPT_FWD_POLY_EVERY : 1)) ==
+                                                                (SPT_FWD_POLY_EVERY > 0 ? SPT_FWD_POLY_EVERY - 1 : 0);
+                const float p0 = poly ? ex2_poly(x0) : ex2(x0);
+                const float p1 = poly ? ex2_poly(x1) : ex2(x1);
+                rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
+                pw[k] = pack_bf16x2(p0, p1);
+            }
+            float rs0, rs1;
+            f2unpack(fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3])), rs0, rs1);
+            const float rs = rs0 + rs1;
+            l += rs;
+#ifdef SPT_WATCHDOG
+            if (r == 0) dbg[2 * t + 1] = 3;
+#endif
+            tmem_st32(s_tm, pw);  // packed P over the consumed S columns [0, 32)
+            tmem_st_wait();
+#ifdef SPT_WATCHDOG
+            if (r == 0) dbg[2 * t + 1] = 4;
+#endif
+            tc_fence_before();
+            mbar_arrive(&p_full[t * 2]);
+        }
+        // epilogue: O_t / l -> global, lse
+        mbar_wait(&o_done[t], 0);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* orow = o + (q * hq + h) * D;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(o_tm + c * 32, ov);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 w;
+                w.x = pack_bf16x2(__uint_as_float(ov[8 * k + 0]) * inv, __uint_as_float(ov[8 * k + 1]) * inv);
+                w.y = pack_bf16x2(__uint_as_float(ov[8 * k + 2]) * inv, __uint_as_float(ov[8 * k + 3]) * inv);
+                w.z = pack_bf16x2(__uint_as_float(ov[8 * k + 4]) * inv, __uint_as_float(ov[8 * k + 5]) * inv);
+                w.w = pack_bf16x2(__uint_as_float(ov[8 * k + 6]) * inv, __uint_as_float(ov[8 * k + 7]) * inv);
+                dst[k] = w;
+            }
+        }
+        lse[(int64_t)h * s + q] = l > 0.f ? (m_use + __log2f(l)) * LN2 : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        __syncwarp();  // role branches diverged lane 0; dealloc is warp-collective (.sync.aligned)
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ===================================================================================== backward
 
 // ------------------------------------------------------------------ dQ pass
@@ -1590,20 +1881,32 @@ extern "C" int spt_debug_dq_prof(unsigned long long* out, int reset) {
 #endif
 }
 
+// SPT_ATTN_FWD_TMEM=0|1 (run time: spt_tuning_set("attn_fwd_tmem", v)): forward with Q resident in TMEM
+int g_attn_fwd_tmem = [] {
+    const char* e = getenv("SPT_ATTN_FWD_TMEM");
+    return e ? (e[0] == '1' ? 1 : 0) : 0;
+}();
+
 bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
                  float* lse, cudaStream_t st) {
     if (d != fatc::D || s % 256 != 0) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap tq = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
     CUtensorMap tkv = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);
-    auto k = fatc::fwd_tc_kernel;
     static bool attr = false;
     if (!attr) {
-        SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::fwt::SMEM));
         attr = true;
     }
     dim3 grid((unsigned)hq, (unsigned)(s / 256));
-    k<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse);
+    if (g_attn_fwd_tmem)
+        fatc::fwd_tmem_kernel<<<grid, fatc::THREADS, fatc::fwt::SMEM, st>>>(tkv, (const bf16*)qkv, s, hq, hkv, seg,
+                                                                              scale * fatc::LOG2E, (bf16*)o, lse);
+    else
+        fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
+                                                                          (bf16*)o, lse);
     count_launch("attn_fwd_tc");
     SPT_CUDA(cudaGetLastError());
     return true;

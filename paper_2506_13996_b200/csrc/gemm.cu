@@ -247,7 +247,8 @@ extern "C" spt_status spt_gemm_bf16(const void* A, int64_t lda, int32_t a_mn_maj
 }
 
 namespace spt {
-extern int g_attn_dq_tmem;  // attention_tc.cu
+extern int g_attn_dq_tmem;   // attention_tc.cu
+extern int g_attn_fwd_tmem;  // attention_tc.cu
 }
 
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
@@ -256,6 +257,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         auto& t = spt::tuning();
         if (n == "attn_dq_tmem") {
             spt::g_attn_dq_tmem = value;
+            return;
+        }
+        if (n == "attn_fwd_tmem") {
+            spt::g_attn_fwd_tmem = value;
             return;
         }
         if (n == "gemm_1sm") t.gemm_1sm = value;
