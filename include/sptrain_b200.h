@@ -238,6 +238,12 @@ spt_status spt_layer_step(spt_layer* layer, const void* x, const int64_t* shift_
 spt_status spt_layer_step_async(spt_layer* layer, const void* x, const int64_t* shift_labels,
                                 const int64_t* position_ids, int32_t inputs_on_host, void* stream);
 spt_status spt_layer_read_loss(spt_layer* layer, float* loss_out, int64_t* count_out, void* stream);
+/* Pipelined per-step results: enqueue a D2H of the step's (loss, count, error flags) into slot [0, 64) of a
+ * pinned ring without synchronising, and read a slot after the stream has passed it.  With host inputs,
+ * spt_layer_step_async copies them on a separate stream into a double-buffered staging area, so the H2D of
+ * step i+1 overlaps step i when steps are enqueued back to back. */
+spt_status spt_layer_loss_async(spt_layer* layer, int32_t slot, void* stream);
+spt_status spt_layer_loss_slot(spt_layer* layer, int32_t slot, float* loss_out, int64_t* count_out);
 /* Gradient accumulation over a window of micro-steps: each micro-step accumulates the grads of
  * the loss SUM (first_micro_step = 1 starts a new window); finish all-reduces the accumulated grads over the
  * SP group, divides them by the window's global valid count, applies the update (lr > 0) and returns the

@@ -107,6 +107,8 @@ SIGNATURES = {
     "spt_layer_step": (I32, [P, P, P, P, I32, PF32, PI64, P]),
     "spt_layer_step_async": (I32, [P, P, P, P, I32, P]),
     "spt_layer_read_loss": (I32, [P, PF32, PI64, P]),
+    "spt_layer_loss_async": (I32, [P, I32, P]),
+    "spt_layer_loss_slot": (I32, [P, I32, PF32, PI64]),
     "spt_layer_step_accumulate": (I32, [P, P, P, P, I32, I32, P]),
     "spt_layer_finish_accumulation": (I32, [P, PF32, PI64, P]),
     "spt_layer_get_grad": (I32, [P, C.c_char_p, P]),
@@ -408,6 +410,15 @@ class UlyssesLayerStep:
         """All-reduce the window's grads, divide by its global valid count; returns (mean loss, count)."""
         loss, cnt = C.c_float(), C.c_int64()
         check(lib().spt_layer_finish_accumulation(self.handle, C.byref(loss), C.byref(cnt), ptr(stream)))
+        return loss.value, cnt.value
+
+    def loss_async(self, slot: int, stream=None):
+        """Enqueue the D2H of this step's (loss, count) into pinned slot `slot` (no synchronisation)."""
+        check(lib().spt_layer_loss_async(self.handle, slot, ptr(stream)))
+
+    def loss_slot(self, slot: int):
+        loss, cnt = C.c_float(), C.c_int64()
+        check(lib().spt_layer_loss_slot(self.handle, slot, C.byref(loss), C.byref(cnt)))
         return loss.value, cnt.value
 
     def read_loss(self, stream=None):

@@ -188,6 +188,16 @@ struct spt_layer {
     std::vector<RankBufs> rb;
     std::vector<std::vector<bf16*>> ck;  // [layer][local rank] checkpointed layer inputs (device or host)
     std::vector<bf16*> xpf;              // [local rank] prefetch buffer for offloaded checkpoints
+    // host inputs: copied on their own stream into one of two device staging slots, so the H2D of step i+1
+    // overlaps step i's compute when the caller enqueues steps asynchronously (spt_layer_step_async)
+    cudaStream_t in_stream = nullptr;
+    bf16* in_x[2] = {nullptr, nullptr};
+    int64_t* in_lab[2] = {nullptr, nullptr};
+    int64_t* in_pos[2] = {nullptr, nullptr};
+    cudaEvent_t ev_in_ready[2] = {nullptr, nullptr}, ev_in_free[2] = {nullptr, nullptr};
+    int in_slot = 0;
+    Scalars* loss_host = nullptr;  // pinned ring for spt_layer_loss_async
+    int loss_ring = 0;
     cudaStream_t cstream = nullptr;      // checkpoint copy stream
     cudaEvent_t ev_x_ready = nullptr, ev_ck_done = nullptr, ev_pf_free = nullptr, ev_pf_done = nullptr;
     void *ws_flce, *ws_mlp, *ws_rms, *ws_attn;
@@ -391,12 +401,48 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
 
     // ---- inputs, label pre-pass, global count
     SPT_CUDA(cudaMemsetAsync(Ly->sc, 0, sizeof(Scalars), st));
-    for (int r = 0; r < L; ++r) {
-        auto& b = Ly->rb[r];
-        SPT_CUDA(cudaMemcpyAsync(b.x, (const bf16*)x + r * nl * h, nl * h * 2, kind, st));
-        SPT_CUDA(cudaMemcpyAsync(b.labels, labels + r * nl, nl * 8, kind, st));
-        if (c.packed) SPT_CUDA(cudaMemcpyAsync(b.pos, pos + r * nl, nl * 8, kind, st));
-        label_stats(b.labels, nl, V, &Ly->sc->count, &Ly->sc->err_label, st);
+    if (on_host) {
+        // H2D on the input stream into a staging slot (overlaps the previous step's compute), then one fast
+        // D2D into the working buffers once the copy landed
+        if (!Ly->in_stream) {
+            SPT_CUDA(cudaStreamCreateWithFlags(&Ly->in_stream, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) {
+                Ly->in_x[k] = Ly->abf((int64_t)L * nl * h);
+                Ly->in_lab[k] = (int64_t*)Ly->led.alloc((size_t)L * nl * 8, kWorkspace);
+                Ly->in_pos[k] = (int64_t*)Ly->led.alloc((size_t)L * nl * 8, kWorkspace);
+                SPT_CUDA(cudaEventCreateWithFlags(&Ly->ev_in_ready[k], cudaEventDisableTiming));
+                SPT_CUDA(cudaEventCreateWithFlags(&Ly->ev_in_free[k], cudaEventDisableTiming));
+                SPT_CUDA(cudaEventRecord(Ly->ev_in_free[k], st));
+            }
+        }
+        const int k = Ly->in_slot;
+        Ly->in_slot ^= 1;
+        SPT_CUDA(cudaStreamWaitEvent(Ly->in_stream, Ly->ev_in_free[k], 0));
+        SPT_CUDA(cudaMemcpyAsync(Ly->in_x[k], x, (size_t)L * nl * h * 2, cudaMemcpyHostToDevice, Ly->in_stream));
+        SPT_CUDA(cudaMemcpyAsync(Ly->in_lab[k], labels, (size_t)L * nl * 8, cudaMemcpyHostToDevice, Ly->in_stream));
+        if (c.packed)
+            SPT_CUDA(cudaMemcpyAsync(Ly->in_pos[k], pos, (size_t)L * nl * 8, cudaMemcpyHostToDevice, Ly->in_stream));
+        SPT_CUDA(cudaEventRecord(Ly->ev_in_ready[k], Ly->in_stream));
+        SPT_CUDA(cudaStreamWaitEvent(st, Ly->ev_in_ready[k], 0));
+        x = Ly->in_x[k];
+        labels = Ly->in_lab[k];
+        pos = c.packed ? Ly->in_pos[k] : pos;
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            SPT_CUDA(cudaMemcpyAsync(b.x, (const bf16*)x + r * nl * h, nl * h * 2, cudaMemcpyDeviceToDevice, st));
+            SPT_CUDA(cudaMemcpyAsync(b.labels, labels + r * nl, nl * 8, cudaMemcpyDeviceToDevice, st));
+            if (c.packed) SPT_CUDA(cudaMemcpyAsync(b.pos, pos + r * nl, nl * 8, cudaMemcpyDeviceToDevice, st));
+        }
+        SPT_CUDA(cudaEventRecord(Ly->ev_in_free[k], st));  // staging slot consumed
+        for (int r = 0; r < L; ++r) label_stats(Ly->rb[r].labels, nl, V, &Ly->sc->count, &Ly->sc->err_label, st);
+    } else {
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            SPT_CUDA(cudaMemcpyAsync(b.x, (const bf16*)x + r * nl * h, nl * h * 2, kind, st));
+            SPT_CUDA(cudaMemcpyAsync(b.labels, labels + r * nl, nl * 8, kind, st));
+            if (c.packed) SPT_CUDA(cudaMemcpyAsync(b.pos, pos + r * nl, nl * 8, kind, st));
+            label_stats(b.labels, nl, V, &Ly->sc->count, &Ly->sc->err_label, st);
+        }
     }
     cm->all_reduce("all_reduce_count", &Ly->sc->count, 1, ncclInt64, st);
     finalize_scale(micro ? &Ly->win->one : &Ly->sc->count, &Ly->sc->scale, st);
@@ -749,6 +795,12 @@ spt_status spt_layer_destroy(spt_layer* Ly) {
         for (cudaEvent_t e : {Ly->ev_x_ready, Ly->ev_ck_done, Ly->ev_pf_free, Ly->ev_pf_done})
             if (e) cudaEventDestroy(e);
         if (Ly->cstream) cudaStreamDestroy(Ly->cstream);
+        if (Ly->in_stream) cudaStreamDestroy(Ly->in_stream);
+        for (int k = 0; k < 2; ++k) {
+            if (Ly->ev_in_ready[k]) cudaEventDestroy(Ly->ev_in_ready[k]);
+            if (Ly->ev_in_free[k]) cudaEventDestroy(Ly->ev_in_free[k]);
+        }
+        if (Ly->loss_host) cudaFreeHost(Ly->loss_host);
         delete Ly;
     });
 }
@@ -797,6 +849,28 @@ spt_status spt_layer_finish_accumulation(spt_layer* Ly, float* loss_out, int64_t
     return capi_guard([&] {
         finish_accumulation(Ly, (cudaStream_t)stream);
         read_scalars(Ly, (cudaStream_t)stream, loss_out, count_out);
+    });
+}
+
+// Enqueue (no sync) a D2H copy of this step's scalars into slot `slot` of a pinned ring of 64 entries; the
+// value is valid once the stream reaches it: read it with spt_layer_loss_slot after synchronising.
+spt_status spt_layer_loss_async(spt_layer* Ly, int32_t slot, void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(slot >= 0 && slot < 64, SPT_ERR_SHAPE, "loss slot must be in [0, 64)");
+        if (!Ly->loss_host) SPT_CUDA(cudaMallocHost(&Ly->loss_host, 64 * sizeof(Scalars)));
+        SPT_CUDA(cudaMemcpyAsync(Ly->loss_host + slot, Ly->sc, sizeof(Scalars), cudaMemcpyDeviceToHost,
+                                 (cudaStream_t)stream));
+    });
+}
+
+spt_status spt_layer_loss_slot(spt_layer* Ly, int32_t slot, float* loss_out, int64_t* count_out) {
+    return capi_guard([&] {
+        SPT_CHECK(Ly->loss_host && slot >= 0 && slot < 64, SPT_ERR_SHAPE, "no such loss slot");
+        const Scalars& v = Ly->loss_host[slot];
+        SPT_CHECK(v.err_label == 0, SPT_ERR_VALIDATION, "label out of range [0, vocab) and != -100");
+        SPT_CHECK(v.err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
+        if (loss_out) *loss_out = v.loss;
+        if (count_out) *count_out = v.count;
     });
 }
 
