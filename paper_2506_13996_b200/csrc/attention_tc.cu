@@ -149,16 +149,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
     const int warp = warp_id(), lane = lane_id();
-    const int npairs = (int)(s / (2 * BQ));
+    const int npairs = (int)((s + 2 * BQ - 1) / (2 * BQ));  // s % 256 == 128: the last pair holds one tile
     // grid = (q head, query-tile pair): heads vary fastest so one wave of CTAs streams the K/V of every kv
     // head at once instead of 148 CTAs hammering the same K/V lines (L2-slice hot spot); longest rows first
     const int pair = npairs - 1 - (int)blockIdx.y;
     const int h = blockIdx.x;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)pair * 2 * BQ;
-    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = seg ? (int)(seg[q0 + BQ] / BKB) : 0;
-    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = (int)((q0 + 2 * BQ - 1) / BKB);
-    const int jlo = jb0, jhi = je1;  // jb0 <= jb1 (starts are monotone), je0 < je1
+    const bool has1 = q0 + BQ < s;  // second query tile present
+    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = (seg && has1) ? (int)(seg[q0 + BQ] / BKB) : 0;
+    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = has1 ? (int)((q0 + 2 * BQ - 1) / BKB) : -1;
+    const int jlo = jb0, jhi = has1 ? je1 : je0;  // jb0 <= jb1 (starts are monotone), je0 < je1
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -292,7 +293,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int sub = warp & 3;
         const int r = sub * 32 + lane;
         const int64_t q = q0 + t * BQ + r;
-        const int start = seg ? seg[q] : 0;
+        const bool row_ok = q < s;  // false only for the absent second tile of a half pair
+        const int start = (seg && row_ok) ? seg[q] : 0;
         const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
         const uint32_t t_tm = tmem + lane_off + t * 256;
         const uint32_t o_tm = t_tm + 128;
@@ -399,6 +401,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // epilogue: O_t / l -> global, lse
         mbar_wait(&o_done[t], 0);
         tc_fence_after();
+        if (t == 1 && !has1) goto fwd_done;  // warp-uniform: the whole tile is absent
+        {
         const float inv = l > 0.f ? 1.f / l : 0.f;
         bf16* orow = o + (q * hq + h) * D;
 #pragma unroll 1
@@ -418,6 +422,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         lse[(int64_t)h * s + q] = l > 0.f ? (m_use + __log2f(l)) * LN2 : -INFINITY;
+        }
+    fwd_done:;
     }
     tc_fence_before();
     __syncthreads();
@@ -458,16 +464,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
     const int warp = warp_id(), lane = lane_id();
-    const int npairs = (int)(s / (2 * BQ));
+    const int npairs = (int)((s + 2 * BQ - 1) / (2 * BQ));  // s % 256 == 128: the last pair holds one tile
     // grid = (q head, query-tile pair): heads vary fastest so one wave of CTAs streams the K/V of every kv
     // head at once instead of 148 CTAs hammering the same K/V lines (L2-slice hot spot); longest rows first
     const int pair = npairs - 1 - (int)blockIdx.y;
     const int h = blockIdx.x;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)pair * 2 * BQ;
-    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = seg ? (int)(seg[q0 + BQ] / BKB) : 0;
-    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = (int)((q0 + 2 * BQ - 1) / BKB);
-    const int jlo = jb0, jhi = je1;  // jb0 <= jb1 (starts are monotone), je0 < je1
+    const bool has1 = q0 + BQ < s;  // second query tile present
+    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = (seg && has1) ? (int)(seg[q0 + BQ] / BKB) : 0;
+    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = has1 ? (int)((q0 + 2 * BQ - 1) / BKB) : -1;
+    const int jlo = jb0, jhi = has1 ? je1 : je0;  // jb0 <= jb1 (starts are monotone), je0 < je1
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 256);
@@ -567,12 +574,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int sub = warp & 3;
         const int r = sub * 32 + lane;
         const int64_t q = q0 + t * BQ + r;
-        const int start = seg ? seg[q] : 0;
+        const bool row_ok = q < s;  // false only for the absent second tile of a half pair
+        const int start = (seg && row_ok) ? seg[q] : 0;
         const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
         const uint32_t t_tm = tmem + lane_off + t * 256;
         const uint32_t o_tm = t_tm + 128;
         {  // this thread's Q row (q head h) -> TMEM columns [t*256 + 64, +64) as bf16 pairs (A operand of S)
-            const uint4* qs = reinterpret_cast<const uint4*>(qkv_in + q * (int64_t)(hq + 2 * hkv) * D + (int64_t)h * D);
+            const uint4* qs = reinterpret_cast<const uint4*>(qkv_in + (row_ok ? q : 0) * (int64_t)(hq + 2 * hkv) * D +
+                                                             (int64_t)h * D);
             uint32_t qv[32];
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
@@ -690,6 +699,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // epilogue: O_t / l -> global, lse
         mbar_wait(&o_done[t], 0);
         tc_fence_after();
+        if (t == 1 && !has1) goto fwd_done;  // warp-uniform: the whole tile is absent
+        {
         const float inv = l > 0.f ? 1.f / l : 0.f;
         bf16* orow = o + (q * hq + h) * D;
 #pragma unroll 1
@@ -709,6 +720,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         lse[(int64_t)h * s + q] = l > 0.f ? (m_use + __log2f(l)) * LN2 : -INFINITY;
+        }
+    fwd_done:;
     }
     tc_fence_before();
     __syncthreads();
@@ -1889,7 +1902,7 @@ int g_attn_fwd_tmem = [] {
 
 bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
                  float* lse, cudaStream_t st) {
-    if (d != fatc::D || s % 256 != 0) return false;
+    if (d != fatc::D || s % 128 != 0) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap tq = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
     CUtensorMap tkv = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);
@@ -1900,7 +1913,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                                       fatc::fwt::SMEM));
         attr = true;
     }
-    dim3 grid((unsigned)hq, (unsigned)(s / 256));
+    dim3 grid((unsigned)hq, (unsigned)((s + 255) / 256));
     if (g_attn_fwd_tmem)
         fatc::fwd_tmem_kernel<<<grid, fatc::THREADS, fatc::fwt::SMEM, st>>>(tkv, (const bf16*)qkv, s, hq, hkv, seg,
                                                                               scale * fatc::LOG2E, (bf16*)o, lse);
@@ -1962,7 +1975,7 @@ size_t attn_bwd_tc_workspace(int64_t s, int hq) {
 // ws: attn_bwd_tc_workspace bytes (fp32 dQ accumulator + per-(head, q block) ordering counters).
 bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const float* Dv, int64_t s, int hq, int hkv,
                  int d, const int32_t* seg, float scale, void* dqkv, void* ws, cudaStream_t st) {
-    if (d != fatc::D || s % 256 != 0 || s >= (int64_t(1) << 31) - 256) return false;
+    if (d != fatc::D || s % 128 != 0 || s >= (int64_t(1) << 31) - 256) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap t128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
     CUtensorMap t64 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);
@@ -1984,7 +1997,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dkvq::SMEM));
         attr = true;
     }
-    if (bwd_mode() == 1 && ws != nullptr && attn_bwd_tc_workspace(s, hq) > 0) {
+    if (bwd_mode() == 1 && ws != nullptr && attn_bwd_tc_workspace(s, hq) > 0 && s % 256 == 0) {
         float* dq_acc = (float*)ws;
         int* cnt = (int*)(dq_acc + (size_t)s * hq * fatc::D);
         SPT_CUDA(cudaMemsetAsync(ws, 0, attn_bwd_tc_workspace(s, hq), st));
@@ -1999,7 +2012,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         SPT_CUDA(cudaGetLastError());
         return true;
     }
-    if (dkdv_multicast()) {  // CTA pairs along the key blocks share one multicast Q/dO stream
+    if (dkdv_multicast() && (s / 128) % 2 == 0) {  // CTA pairs along the key blocks share one Q/dO stream
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(s / 128), (unsigned)hkv);
         cfg.blockDim = dim3(fatc::BW_THREADS);
