@@ -101,6 +101,8 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
 template <int BN, bool A_MN, bool B_MN, int KIND>
 static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep,
                          cudaStream_t st) {
+    CUtensorMap tc = ta;  // unused unless the TMA fp32 epilogue runs
+    if (KIND == EPI_F32 && ep.tstore == 2) tc = make_tmap_f32_c(ep.C, M, N, ep.ldc);
     auto kern = gemm_tc2_kernel<BN, A_MN, B_MN, KIND>;
     constexpr int smem = Gemm2Cfg<BN>::SMEM_BYTES;
     static bool attr_done = false;
@@ -123,7 +125,7 @@ static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, int M, in
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     prof_run(P_GEMM, 2.0 * M * N * K, 0, st, [&] {
-        SPT_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep));
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep, tc));
         count_launch("gemm2");
     });
 }
@@ -217,7 +219,7 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
     // CTA pairs win for K-major x K-major (forward / logits) GEMMs; with MN-major operands the 1-SM
     // kernel measured faster inside the layer step (profiles/README.md, per-site breakdown).
     if (M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn()) && use_pair_gemm()) {
-        if (ep.tstore == 2) ep.tstore = 1;
+        if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
         else dispatch_pair<256>(A, B, M, N, K, kind, ep, st);
         return;

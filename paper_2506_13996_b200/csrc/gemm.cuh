@@ -451,13 +451,14 @@ struct Gemm2Cfg {
     static constexpr int B_BYTES = (BN / 2) * GEMM_BK * 2;       // this CTA's half of B
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + EPI_TBUF_BYTES;
+    static constexpr int OFF_EPI = STAGES * STAGE_BYTES + 1024;   // staging / transpose tiles, 1 KiB-aligned
+    static constexpr int SMEM_BYTES = OFF_EPI + EPI_STG_BYTES + 1024;
 };
 
 template <int BN, bool A_MN, bool B_MN, int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, EpiParams ep) {
+                    int K, EpiParams ep, const __grid_constant__ CUtensorMap tmC) {
     using Cfg = Gemm2Cfg<BN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* tbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);  // epilogue transpose tiles
+    float* tbuf = reinterpret_cast<float*>(smem + Cfg::OFF_EPI);  // epilogue transpose tiles (non-TMA paths)
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_ctarank();
@@ -603,8 +604,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld32(tbase + c, r0);
                 tmem_ld32(tbase + c + 32, r1);
                 tmem_ld_wait();
+                if constexpr (KIND == EPI_F32) {
+                    if (col < N && ep.tstore == 2) {  // TMA store / reduce-add (rows and columns clipped by TMA)
+                        const uint32_t stg = smem_u32(smem + Cfg::OFF_EPI) + (uint32_t)(warp & 3) * 8192u;
+                        const int64_t row0 = row - lane;
+                        epi_tma_block(&tmC, stg, row0, col, reinterpret_cast<const float*>(r0), ep.alpha,
+                                      ep.accumulate != 0);
+                        epi_tma_block(&tmC, stg + 4096, row0, col + 32, reinterpret_cast<const float*>(r1), ep.alpha,
+                                      ep.accumulate != 0);
+                    }
+                }
                 if constexpr (KIND == EPI_F32 || KIND == EPI_F32_STATS) {
-                    if (col < N && ep.tstore) {  // warp-uniform (N % 64 == 0); rows bounds-checked inside
+                    if (col < N && ep.tstore == 1) {  // warp-uniform (N % 64 == 0); rows bounds-checked inside
                         float* tb = tbuf + (warp & 3) * EPI_TBUF_FLOATS;
                         const int64_t row0 = row - lane;
                         store_block_t<KIND>(ep, tb, row0, col, M, reinterpret_cast<const float*>(r0));
@@ -638,6 +649,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 acc = 0;
                 acc_phase ^= 1;
             }
+        }
+        if constexpr (KIND == EPI_F32) {
+            if (ep.tstore == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
     }
     tc_fence_before();
