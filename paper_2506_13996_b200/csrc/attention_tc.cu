@@ -1212,11 +1212,18 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 // blocks, starting at the even CTA's first block — the odd CTA's extra blocks are fully masked), each CTA
 // multicasting half of every stage into both CTAs' smem: half the L2->SM bytes per CTA.  Stage release needs
 // both CTAs' MMAs (multicast commit onto qs_empty, count 2).
-template <bool MC>
+// KT: the K block lives in TMEM (written once by the elementwise warps) and S^T = K Q^T reads only its B
+// operand from smem: M=128 N=64 MMAs run at the full tensor rate from TMEM but at 2/3 of it with both
+// operands in smem (tools/micro/mma_pair_rate.cu).  The 64 columns come from single-buffering dP^T:
+// TMEM = S^T[2] (64 each) | dP^T (64) | K (64) | dV (128) | dK (128).  dP^T(it+1) is issued as soon as
+// the elementwise warps have consumed dP^T(it) (pd_full(it)), ahead of acc(it), so the elementwise phase of
+// it+1 still overlaps acc(it) + S^T(it+2).
+template <bool MC, bool KT>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                    const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
-                   const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
+                   const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv,
+                   const bf16* __restrict__ qkv) {
     using namespace dkv;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1227,7 +1234,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint64_t* s_full = qs_empty + NQS;    // [2]
     uint64_t* pd_full = s_full + 2;       // [2]
     uint64_t* acc_done = pd_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+    uint64_t* dp_full = acc_done + 1;     // KT: single dP^T buffer
+    uint64_t* k_ready = dp_full + 1;      // KT: K block written to TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(k_ready + 1);
+    constexpr uint32_t DP_COL = 128, K_COL = 192;  // KT layout
     const int warp = warp_id(), lane = lane_id();
     const int nkb = (int)(s / 128);
     const int kb = (int)blockIdx.x;  // small kb = most work: launched first
@@ -1262,6 +1272,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             mbar_init(&pd_full[i], BW_NEW * 32);
         }
         mbar_init(acc_done, 1);
+        mbar_init(dp_full, 1);
+        mbar_init(k_ready, BW_NEW * 32);
         fence_barrier_init();
     }
     if (warp == BW_MMA) {
@@ -1276,9 +1288,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t sbase = smem_u32(smem);
     if (warp == BW_TMA) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(kv_full, 2 * KB_BYTES);
+            mbar_arrive_expect_tx(kv_full, (KT ? 1 : 2) * KB_BYTES);
             for (int r = 0; r < 2; ++r) {
-                tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
+                if (!KT) tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
                 tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
             }
             int hh = kvh * grp, qblk = 0;
@@ -1316,7 +1328,27 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             constexpr uint32_t id_s = make_idesc_bf16(128, BQB, false, false);
             constexpr uint32_t id_a = make_idesc_bf16(128, D, false, true);
             mbar_wait(kv_full, 0);
+            if (KT) mbar_wait(k_ready, 0);
             const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V;
+            auto issue_s = [&](int it) {  // KT: S^T only, A = K from TMEM
+                const int st = it % NQS;
+                mbar_wait(&qs_full[st], (it / NQS) & 1);
+                tc_fence_after();
+                const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES;
+                const uint32_t d_s = tmem + (it & 1) * 64;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ts_w(d_s, tmem + K_COL + kk * 8, kdesc_r(qb_, kk, 8192), id_s, kk > 0);
+                mma_commit_w(&s_full[it & 1]);
+            };
+            auto issue_dp = [&](int it) {  // KT: dP^T into the single dP^T buffer (qs_full(it) already waited)
+                const int st = it % NQS;
+                const uint32_t dob = sbase + OFF_QS + st * 2 * QS_BYTES + QS_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss_w(tmem + DP_COL, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
+                mma_commit_w(dp_full);
+            };
             auto issue_sdp = [&](int it) {
                 const int st = it % NQS;
                 mbar_wait(&qs_full[st], (it / NQS) & 1);
@@ -1331,28 +1363,40 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     mma_bf16_ss_w(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
                 mma_commit_w(&s_full[it & 1]);
             };
-            auto issue_acc = [&](int it) {
+            auto issue_acc = [&](int it, auto&& before) {
                 const int b = it & 1, st = it % NQS;
                 mbar_wait(&pd_full[b], (it >> 1) & 1);
                 tc_fence_after();
+                before();
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+                const uint32_t sb = tmem + b * (KT ? 64 : 128);
                 // A operands from TMEM: column group g packed P^T for q [16g, 16g+16) into S^T columns
                 // [16g, 16g+8) and dS^T into [16g+8, 16g+16) of buffer b
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ts_w(tmem + 256, tmem + b * 128 + kk * 16, mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
+                    mma_bf16_ts_w(tmem + 256, sb + kk * 16, mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
 #pragma unroll
                 for (int kk = 0; kk < BQB / 16; ++kk)
-                    mma_bf16_ts_w(tmem + 384, tmem + b * 128 + kk * 16 + 8, mndesc_r(qb_, kk, 8192), id_a,
+                    mma_bf16_ts_w(tmem + 384, sb + kk * 16 + 8, mndesc_r(qb_, kk, 8192), id_a,
                                   (it > 0 || kk > 0));
                 if constexpr (MC) mma_commit_mc_w(&qs_empty[st], 0x3);  // the stage is free in both CTAs
                 else mma_commit_w(&qs_empty[st]);
             };
-            if (total > 0) issue_sdp(0);
-            if (total > 1) issue_sdp(1);
-            for (int it = 0; it < total; ++it) {
-                issue_acc(it);
-                if (it + 2 < total) issue_sdp(it + 2);
+            if constexpr (KT) {
+                // order: S(0) dP(0) S(1) | per it: [wait pd_full(it)] dP(it+1) acc(it) S(it+2)
+                if (total > 0) { issue_s(0); issue_dp(0); }
+                if (total > 1) issue_s(1);
+                for (int it = 0; it < total; ++it) {
+                    issue_acc(it, [&] { if (it + 1 < total) issue_dp(it + 1); });
+                    if (it + 2 < total) issue_s(it + 2);
+                }
+            } else {
+                if (total > 0) issue_sdp(0);
+                if (total > 1) issue_sdp(1);
+                for (int it = 0; it < total; ++it) {
+                    issue_acc(it, [] {});
+                    if (it + 2 < total) issue_sdp(it + 2);
+                }
             }
             mma_commit_w(acc_done);
         }
@@ -1364,12 +1408,28 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int key32 = (int)key;  // s < 2^31 (attn_bwd_tc checks)
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         const float sl2 = scale * LOG2E;
+        if constexpr (KT) {  // K row `key` -> TMEM (this warp: d elements [32 grp, +32) = packed columns [16 grp, +16))
+            const int64_t width = (int64_t)(hq + 2 * hkv) * D;
+            const uint4* ks = reinterpret_cast<const uint4*>(qkv + key * width + (int64_t)(hq + kvh) * D + 32 * grp);
+            uint32_t kv[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint4 a = __ldg(ks + k);
+                kv[4 * k] = a.x; kv[4 * k + 1] = a.y; kv[4 * k + 2] = a.z; kv[4 * k + 3] = a.w;
+            }
+            tmem_st16(tmem + lo + K_COL + grp * 16, kv);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(k_ready);
+        }
+        const uint32_t sstride = KT ? 64 : 128, dpoff = KT ? DP_COL : 64;
         int qblk = 0;  // iteration it = (q head it / nqb, q block qb_first + it % nqb), kept incrementally
         for (int it = 0; it < total; ++it) {
             const int b = it & 1;
             const int qq = (qb_first + qblk) * BQB + grp * 16;
             if (++qblk == nqb) qblk = 0;
             mbar_wait(&s_full[b], (it >> 1) & 1);
+            if (KT) mbar_wait(dp_full, it & 1);
             tc_fence_after();
 #ifdef SPT_EXP_NO_ELEM
             tc_fence_before();
@@ -1377,8 +1437,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             continue;
 #endif
             uint32_t sv[16], dv[16];
-            tmem_ld16(tmem + lo + b * 128 + grp * 16, sv);
-            tmem_ld16(tmem + lo + b * 128 + 64 + grp * 16, dv);
+            const uint32_t sbuf = tmem + lo + b * sstride;
+            tmem_ld16(sbuf + grp * 16, sv);
+            tmem_ld16((KT ? tmem + lo + dpoff : sbuf + dpoff) + grp * 16, dv);
             tmem_ld_wait();
             // the stage's statistics landed with Q/dO (s_full(it) follows the MMA's qs_full wait) and the
             // stage is not recycled before acc(it) completes, which needs this warp's arrival
@@ -1419,8 +1480,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             };
             if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
             else body(std::false_type{});
-            tmem_st8(tmem + lo + b * 128 + grp * 16, pw);
-            tmem_st8(tmem + lo + b * 128 + grp * 16 + 8, sw);
+            tmem_st8(sbuf + grp * 16, pw);
+            tmem_st8(sbuf + grp * 16 + 8, sw);
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&pd_full[b]);
@@ -1466,6 +1527,258 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
 }
 
+// ------------------------------------------------------------------ dK / dV pass, CTA pair (cta_group::2)
+// Same iteration space as dkdv_tc_kernel<true> (cluster (2m, 2m+1) over 256 keys, one shared Q/dO sequence),
+// but every MMA is a 2-SM tcgen05.mma issued by the leader: M = 256 keys (each CTA's K / V block and TMEM
+// hold its own 128), B split across the pair.  The score MMAs (S^T = K Q^T, dP^T = V dO^T, N = 64 queries)
+// take queries [32c, 32c+32) of the block from CTA c, so each SM reads 4 KiB (A) + 1 KiB (B) of smem per
+// K=16 step instead of 4 + 2 KiB: the smem-read cap of those MMAs rises from 32/48 to 32/40 of the tensor
+// rate.  The accumulating MMAs (dV += P^T dO, dK += dS^T Q, N = d = 128) take head-dim columns
+// [64c, 64c+64) from CTA c.  A stage therefore holds, per CTA and per tensor (Q, dO), its 32-query half
+// (both 64-column regions) for the score MMAs and its 64-column region (all 64 queries) for the
+// accumulating ones: 16 KiB, as before.  P^T / dS^T stay in each CTA's TMEM (A operand of the 2-SM MMA).
+namespace dkp {
+constexpr int BQB = 64;
+constexpr int KB_BYTES = 128 * D * 2;                  // K or V block, 32 KiB
+constexpr int STG = 32768;                             // QS(8K) DS(8K) QA(8K) DA(8K)
+constexpr int ST_QS = 0, ST_DS = 8192, ST_QA = 16384, ST_DA = 24576;
+constexpr int NQS = 4;
+constexpr int OFF_K = 0, OFF_V = KB_BYTES, OFF_QS = 2 * KB_BYTES;
+constexpr int OFF_LD = OFF_QS + NQS * STG;             // NQS x (lse*log2e[64], D[64]) fp32, per CTA
+constexpr int OFF_BAR = OFF_LD + NQS * 512;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+}  // namespace dkp
+
+__global__ void __launch_bounds__(BW_THREADS, 1)
+    dkdv_pair_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq32,
+                     const __grid_constant__ CUtensorMap tdo32, const __grid_constant__ CUtensorMap tq64,
+                     const __grid_constant__ CUtensorMap tdo64, int64_t s, int hq, int hkv,
+                     const int32_t* __restrict__ seg, const float* __restrict__ lse2v, const float* __restrict__ Dv,
+                     float scale, bf16* __restrict__ dqkv) {
+    using namespace dkp;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* kv_full = bar;              // leader's copy counts both CTAs' bytes
+    uint64_t* qs_full = bar + 1;          // [NQS] leader's copy counts both CTAs' bytes
+    uint64_t* qs_empty = qs_full + NQS;   // [NQS] multicast commit from the leader
+    uint64_t* ld_full = qs_empty + NQS;   // [NQS] local statistics
+    uint64_t* s_full = ld_full + NQS;     // [2] multicast commit
+    uint64_t* pd_full = s_full + 2;       // [2] leader's copy: one arrival per elementwise warp of both CTAs
+    uint64_t* acc_done = pd_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+    const int warp = warp_id(), lane = lane_id();
+    const int kb = (int)blockIdx.x;
+    const int kvh = blockIdx.y;
+    const int grp = hq / hkv;
+    const int64_t k0 = (int64_t)kb * 128;
+    const uint32_t crank = cluster_ctarank();
+    const int qb_first = (int)((k0 & ~int64_t(255)) / BQB);
+    int qb_last = (int)((s - 1) / BQB);
+    if (seg) {
+        const int64_t klast = (k0 | 128) + 127;  // the odd CTA's last key
+        int64_t lo = k0 & ~int64_t(255), hi = s - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (seg[mid] <= klast) lo = mid;
+            else hi = mid - 1;
+        }
+        qb_last = (int)(lo / BQB);
+    }
+    const int nqb = qb_last - qb_first + 1;
+    const int total = nqb * grp;
+    if (threadIdx.x == 0) {
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < NQS; ++i) {
+            mbar_init(&qs_full[i], 1);
+            mbar_init(&qs_empty[i], 1);
+            mbar_init(&ld_full[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&pd_full[i], 2 * BW_NEW);
+        }
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == BW_MMA) {
+        tmem_alloc_pair(tmem_slot, 512);
+        tmem_relinquish_pair();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t sbase = smem_u32(smem);
+    if (warp == BW_TMA) {
+        if (lane == 0) {
+            if (crank == 0) mbar_arrive_expect_tx(kv_full, 4 * KB_BYTES);
+            for (int r = 0; r < 2; ++r) {
+                tma_load_2d_pair(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
+                tma_load_2d_pair(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
+            }
+            int hh = kvh * grp, qblk = 0;
+            for (int it = 0; it < total; ++it) {
+                const int st = it % NQS;
+                mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);
+                if (crank == 0) mbar_arrive_expect_tx(&qs_full[st], 2 * STG);
+                mbar_arrive_expect_tx(&ld_full[st], 512);
+                const int qq = (qb_first + qblk) * BQB;
+                const int hcur = hh;
+                if (++qblk == nqb) { qblk = 0; ++hh; }
+                uint8_t* base = smem + OFF_QS + st * STG;
+                for (int r = 0; r < 2; ++r) {
+                    tma_load_2d_pair(&tq32, &qs_full[st], base + ST_QS + r * 4096, hcur * D + 64 * r, qq + 32 * (int)crank);
+                    tma_load_2d_pair(&tdo32, &qs_full[st], base + ST_DS + r * 4096, hcur * D + 64 * r, qq + 32 * (int)crank);
+                }
+                tma_load_2d_pair(&tq64, &qs_full[st], base + ST_QA, hcur * D + 64 * (int)crank, qq);
+                tma_load_2d_pair(&tdo64, &qs_full[st], base + ST_DA, hcur * D + 64 * (int)crank, qq);
+                bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &ld_full[st]);
+                bulk_load(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &ld_full[st]);
+            }
+        }
+    } else if (warp == BW_MMA) {
+        if (crank == 0) {  // whole warp, converged; elect.sync inside the wrappers picks the issuing lane
+            constexpr uint32_t id_s = make_idesc_bf16(256, BQB, false, false);
+            constexpr uint32_t id_a = make_idesc_bf16(256, D, false, true);
+            mbar_wait(kv_full, 0);
+            const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V;
+            auto issue_sdp = [&](int it) {
+                const int st = it % NQS;
+                mbar_wait(&qs_full[st], (it / NQS) & 1);
+                tc_fence_after();
+                const uint32_t b_ = sbase + OFF_QS + st * STG;
+                const uint32_t d_s = tmem + (it & 1) * 128;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss_pair_w(d_s, kdesc_r(ka, kk, 16384), kdesc_r(b_ + ST_QS, kk, 4096), id_s, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss_pair_w(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(b_ + ST_DS, kk, 4096), id_s, kk > 0);
+                mma_commit_pair_w(&s_full[it & 1], 0x3);
+            };
+            auto issue_acc = [&](int it) {
+                const int b = it & 1, st = it % NQS;
+                mbar_wait(&pd_full[b], (it >> 1) & 1);
+                tc_fence_after();
+                const uint32_t b_ = sbase + OFF_QS + st * STG;
+#pragma unroll
+                for (int kk = 0; kk < BQB / 16; ++kk)
+                    mma_bf16_ts_pair_w(tmem + 256, tmem + b * 128 + kk * 16, mndesc_r(b_ + ST_DA, kk, 8192), id_a,
+                                       (it > 0 || kk > 0));
+#pragma unroll
+                for (int kk = 0; kk < BQB / 16; ++kk)
+                    mma_bf16_ts_pair_w(tmem + 384, tmem + b * 128 + kk * 16 + 8, mndesc_r(b_ + ST_QA, kk, 8192), id_a,
+                                       (it > 0 || kk > 0));
+                mma_commit_pair_w(&qs_empty[st], 0x3);
+            };
+            if (total > 0) issue_sdp(0);
+            if (total > 1) issue_sdp(1);
+            for (int it = 0; it < total; ++it) {
+                issue_acc(it);
+                if (it + 2 < total) issue_sdp(it + 2);
+            }
+            mma_commit_pair_w(acc_done, 0x3);
+        }
+    } else {
+        // elementwise (both CTAs, own 128 keys): warp w: TMEM lanes (w&3)*32.., q columns [16g, 16g+16), g = w>>2
+        const int sub = warp & 3, grp = warp >> 2;
+        const int r = sub * 32 + lane;
+        const int64_t key = k0 + r;
+        const int key32 = (int)key;
+        const uint32_t lo = (uint32_t)(sub * 32) << 16;
+        const float sl2 = scale * LOG2E;
+        const uint32_t pd_leader0 = mapa_shared(smem_u32(&pd_full[0]), 0);
+        const uint32_t pd_leader1 = mapa_shared(smem_u32(&pd_full[1]), 0);
+        int qblk = 0;
+        for (int it = 0; it < total; ++it) {
+            const int b = it & 1;
+            const int qq = (qb_first + qblk) * BQB + grp * 16;
+            if (++qblk == nqb) qblk = 0;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
+            mbar_wait(&ld_full[it % NQS], (it / NQS) & 1);
+            tc_fence_after();
+            uint32_t sv[16], dv[16];
+            tmem_ld16(tmem + lo + b * 128 + grp * 16, sv);
+            tmem_ld16(tmem + lo + b * 128 + 64 + grp * 16, dv);
+            tmem_ld_wait();
+            const uint32_t lsm = sbase + OFF_LD + (it % NQS) * 512 + grp * 64;
+            uint32_t pw[8], sw[8];
+            auto body = [&](auto mask_c) {
+                constexpr bool MASK = decltype(mask_c)::value;
+                const int lo_ = key32 - qq;
+                const uint64_t sl2x = f2pack(sl2, sl2);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float lv[8], dd[8];
+                    lds128(lsm + 32 * k, lv[0], lv[1], lv[2], lv[3]);
+                    lds128(lsm + 32 * k + 16, lv[4], lv[5], lv[6], lv[7]);
+                    lds128(lsm + 256 + 32 * k, dd[0], dd[1], dd[2], dd[3]);
+                    lds128(lsm + 256 + 32 * k + 16, dd[4], dd[5], dd[6], dd[7]);
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int i = 8 * k + e;
+                        float x0, x1;
+                        f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sl2x,
+                                       f2pack(-lv[e], -lv[e + 1])),
+                                 x0, x1);
+                        float p0 = ex2(x0), p1 = ex2(x1);
+                        if constexpr (MASK) {
+                            if (i < lo_ || (seg && key32 < seg[qq + i])) p0 = 0.f;
+                            if (i + 1 < lo_ || (seg && key32 < seg[qq + i + 1])) p1 = 0.f;
+                        }
+                        const uint64_t ds = fmul2(f2pack(p0, p1), fsub2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
+                                                                        f2pack(dd[e], dd[e + 1])));
+                        float s0, s1;
+                        f2unpack(ds, s0, s1);
+                        pw[4 * k + e / 2] = pack_bf16x2(p0, p1);
+                        sw[4 * k + e / 2] = pack_bf16x2(s0, s1);
+                    }
+                }
+            };
+            if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
+            else body(std::false_type{});
+            tmem_st8(tmem + lo + b * 128 + grp * 16, pw);
+            tmem_st8(tmem + lo + b * 128 + grp * 16 + 8, sw);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(b ? pd_leader1 : pd_leader0);
+        }
+        mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const int64_t rs = (int64_t)(hq + 2 * hkv) * D;
+        const bool isk = grp >= 2;
+        const int c0 = (grp & 1) * 64;
+        bf16* dst = dqkv + key * rs + (int64_t)(isk ? (hq + kvh) : (hq + hkv + kvh)) * D + c0;
+        const float mul = isk ? scale : 1.f;
+        const uint32_t acc_tm = tmem + lo + (isk ? 384 : 256) + c0;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            uint32_t v[32];
+            tmem_ld32(acc_tm + c * 32, v);
+            tmem_ld_wait();
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 w;
+                w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+                w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+                w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+                w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+                d4[k] = w;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // the leader's MMAs read this CTA's smem / TMEM and its commits target this CTA
+    if (warp == BW_MMA) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc_pair(tmem, 512);
+    }
+}
 
 // ------------------------------------------------------------------ fused dK / dV / dQ pass
 // One KV-outer pass computes all three gradients (5 matmuls per tile instead of the 7 of the two-pass
@@ -1966,6 +2279,25 @@ static bool dq_multicast() {
     return v;
 }
 
+#ifndef SPT_DKDV_PAIR_DEFAULT
+#define SPT_DKDV_PAIR_DEFAULT 0
+#endif
+// SPT_ATTN_DKDV_PAIR=0|1: dK/dV pass on CTA pairs with 2-SM MMAs (dkdv_pair_kernel); also settable at run time
+// through spt_tuning_set("attn_dkdv_pair", v)
+int g_attn_dkdv_pair = [] {
+    const char* e = getenv("SPT_ATTN_DKDV_PAIR");
+    return e ? (e[0] == '1' ? 1 : 0) : (SPT_DKDV_PAIR_DEFAULT != 0 ? 1 : 0);
+}();
+
+#ifndef SPT_DKDV_KT_DEFAULT
+#define SPT_DKDV_KT_DEFAULT 0
+#endif
+// SPT_ATTN_DKDV_KT=0|1: dK/dV pass with the K block resident in TMEM; spt_tuning_set("attn_dkdv_kt", v)
+int g_attn_dkdv_kt = [] {
+    const char* e = getenv("SPT_ATTN_DKDV_KT");
+    return e ? (e[0] == '1' ? 1 : 0) : (SPT_DKDV_KT_DEFAULT != 0 ? 1 : 0);
+}();
+
 size_t attn_bwd_tc_workspace(int64_t s, int hq) {
     if (bwd_mode() != 1) return 0;
     return (size_t)s * hq * fatc::D * 4 + (size_t)hq * (s / 64) * 4 + 256;
@@ -1989,12 +2321,18 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dq::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dqt::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::dkv::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dkv::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdvq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkvq::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dkp::SMEM));
         attr = true;
     }
     if (bwd_mode() == 1 && ws != nullptr && attn_bwd_tc_workspace(s, hq) > 0 && s % 256 == 0) {
@@ -2012,7 +2350,24 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         SPT_CUDA(cudaGetLastError());
         return true;
     }
-    if (dkdv_multicast() && (s / 128) % 2 == 0) {  // CTA pairs along the key blocks share one Q/dO stream
+    if (g_attn_dkdv_pair != 0 && (s / 128) % 2 == 0) {  // 2-SM MMAs over key-block pairs
+        CUtensorMap t32 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 32);
+        CUtensorMap do32 = make_tmap_bf16_2d(dout, (uint64_t)hq * d, (uint64_t)s, (uint64_t)hq * d, 64, 32);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(s / 128), (unsigned)hkv);
+        cfg.blockDim = dim3(fatc::BW_THREADS);
+        cfg.dynamicSmemBytes = fatc::dkp::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, fatc::dkdv_pair_kernel, t128, t32, do32, t64, do64, s, hq, hkv, seg, lse2, Dv,
+                                    scale, (bf16*)dqkv));
+    } else if (dkdv_multicast() && (s / 128) % 2 == 0) {  // CTA pairs along the key blocks share one Q/dO stream
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(s / 128), (unsigned)hkv);
         cfg.blockDim = dim3(fatc::BW_THREADS);
@@ -2025,11 +2380,12 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        SPT_CUDA(cudaLaunchKernelEx(&cfg, fatc::dkdv_tc_kernel<true>, t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale,
-                                    (bf16*)dqkv));
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, g_attn_dkdv_kt ? fatc::dkdv_tc_kernel<true, true> : fatc::dkdv_tc_kernel<true, false>,
+                                    t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, (const bf16*)qkv));
     } else {
-        fatc::dkdv_tc_kernel<false><<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM,
-                                      st>>>(t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+        auto kern = g_attn_dkdv_kt ? fatc::dkdv_tc_kernel<false, true> : fatc::dkdv_tc_kernel<false, false>;
+        kern<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM, st>>>(
+            t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, (const bf16*)qkv);
     }
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());

@@ -132,7 +132,12 @@ struct DeviceLedger {
     }
 };
 
-
+// TiledMLP backward tile grouping (1 = the forward's tiles, 2 = pairs of consecutive tiles per recompute /
+// weight-gradient pass); SPT_MLP_BWD_GROUP or spt_tuning_set("mlp_bwd_group", v)
+int g_mlp_bwd_group = [] {
+    const char* e = getenv("SPT_MLP_BWD_GROUP");
+    return e ? atoi(e) : 1;
+}();
 
 }  // namespace spt
 
@@ -167,7 +172,7 @@ struct spt_layer {
     spt_comm* comm;
     spt_head_shard_plan plan;
     int P, L;
-    int64_t N, n_loc, h, I, V, qkv_out, qd, qkv_loc, hq_loc, hkv_loc, mlp_tile, loss_tile;
+    int64_t N, n_loc, h, I, V, qkv_out, qd, qkv_loc, hq_loc, hkv_loc, mlp_tile, loss_tile, mlp_bwd_tile_max;
     float eps;
     DeviceLedger led;
     Prof prof;
@@ -346,7 +351,11 @@ static void build_layer(spt_layer* Ly) {
     }
     // workspaces (shared by local ranks; phases run back to back on one stream)
     Ly->ws_flce = L_.alloc(flce_workspace(Ly->loss_tile, V), kLogits);
-    Ly->ws_mlp = L_.alloc(mlp_workspace(Ly->mlp_tile, I), kWorkspace);
+    // the backward may run the TiledMLP tiles in groups of g_mlp_bwd_group (fewer, longer weight-gradient
+    // accumulation passes); the workspace is sized for the group in force at construction and the backward
+    // never uses a larger one
+    Ly->mlp_bwd_tile_max = std::min<int64_t>(Ly->n_loc, Ly->mlp_tile * std::max(1, std::min(2, g_mlp_bwd_group)));
+    Ly->ws_mlp = L_.alloc(mlp_workspace(Ly->mlp_bwd_tile_max, I), kWorkspace);
     Ly->ws_rms = L_.alloc(rmsnorm_bwd_workspace(nl, h), kWorkspace);
     Ly->ws_attn = L_.alloc(attn_bwd_workspace(N, Ly->hq_loc, Ly->hkv_loc, c.head_dim), kWorkspace);
     // reshard tables
@@ -534,7 +543,9 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             const bool acc = r > 0 || gbase;  // loopback ranks share the grad buffer: rank-ascending
             bf16* dx2 = b.dx;
             bf16* dxn2 = b.dz;
-            mlp_bwd(b.xn2, w.wgu, w.wd, dx2, dxn2, w.dwgu, w.dwd, acc, nl, h, I, Ly->mlp_tile, Ly->ws_mlp, st);
+            mlp_bwd(b.xn2, w.wgu, w.wd, dx2, dxn2, w.dwgu, w.dwd, acc, nl, h, I,
+                    std::min<int64_t>(Ly->mlp_bwd_tile_max, Ly->mlp_tile * std::max(1, g_mlp_bwd_group)), Ly->ws_mlp,
+                    st);
             pf.run(P_NORM, 0, 4.0 * nl * h * 2, st,
                    [&] { rmsnorm_bwd(b.x1, w.g2, b.rstd2, dxn2, dx2, b.dx1, w.dg2, Ly->ws_rms, nl, h, st); });
             EpiParams e1;

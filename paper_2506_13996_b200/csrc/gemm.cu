@@ -251,6 +251,9 @@ extern "C" spt_status spt_gemm_bf16(const void* A, int64_t lda, int32_t a_mn_maj
 namespace spt {
 extern int g_attn_dq_tmem;   // attention_tc.cu
 extern int g_attn_fwd_tmem;  // attention_tc.cu
+extern int g_mlp_bwd_group;  // engine.cu
+extern int g_attn_dkdv_pair;  // attention_tc.cu
+extern int g_attn_dkdv_kt;    // attention_tc.cu
 }
 
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
@@ -263,6 +266,18 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         }
         if (n == "attn_fwd_tmem") {
             spt::g_attn_fwd_tmem = value;
+            return;
+        }
+        if (n == "attn_dkdv_kt") {
+            spt::g_attn_dkdv_kt = value;
+            return;
+        }
+        if (n == "attn_dkdv_pair") {
+            spt::g_attn_dkdv_pair = value;
+            return;
+        }
+        if (n == "mlp_bwd_group") {
+            spt::g_mlp_bwd_group = value;
             return;
         }
         if (n == "gemm_1sm") t.gemm_1sm = value;

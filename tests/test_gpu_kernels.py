@@ -323,3 +323,38 @@ def test_attention_bwd_fused_scheme(s, hq, hkv, packed):
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "fused_bwd_case.py"), str(s), str(hq), str(hkv),
                         "1" if packed else "0"], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("switch", ["attn_dkdv_pair", "attn_dkdv_kt", "attn_dq_tmem"])
+@pytest.mark.parametrize("s,hq,hkv,packed", [(1024, 4, 1, False), (2048, 8, 2, True), (768, 2, 2, False)])
+def test_attention_bwd_variants_bitwise(switch, s, hq, hkv, packed):
+    """The measured-and-kept-opt-in dK/dV variants (2-SM MMAs over CTA pairs; K resident in TMEM) and the dQ
+    variant toggle compute the same sums in the same order as the default kernels: bitwise equal dQ/dK/dV."""
+    T = torch()
+    L = _lib()
+    d = 128
+    qkv, dout, starts = _attn_case(s, hq, hkv, d, packed, s + hq)
+    qkvd, doutd = bf16_dev(qkv), bf16_dev(dout)
+    o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+    lse = T.empty(hq, s, device="cuda")
+    seg = T.from_numpy(starts.astype(np.int32)).cuda() if starts is not None else None
+    scale = 1.0 / math.sqrt(d)
+    S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, S.ptr(seg), scale, o.data_ptr(), lse.data_ptr(), None))
+    ws = T.empty(L.spt_attn_bwd_workspace(s, hq, hkv, d), dtype=T.uint8, device="cuda")
+    outs = []
+    default = 1 if switch == "attn_dq_tmem" else 0
+    try:
+        for v in (default, 1 - default):
+            S.check(L.spt_tuning_set(switch.encode(), v))
+            g = T.zeros(s, hq + 2 * hkv, d, dtype=T.bfloat16, device="cuda")
+            S.check(L.spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
+                                   S.ptr(seg), scale, g.data_ptr(), ws.data_ptr(), None))
+            outs.append(g)
+        T.cuda.synchronize()
+    finally:
+        S.check(L.spt_tuning_set(switch.encode(), default))
+    if switch == "attn_dq_tmem":  # different dQ kernels: same dK/dV, dQ within bf16 rounding
+        assert T.equal(outs[0][:, hq:].view(T.int16), outs[1][:, hq:].view(T.int16))
+        assert rel_err(to_np(outs[1][:, :hq]), to_np(outs[0][:, :hq]).astype(np.float64)) < 1e-2
+    else:
+        assert T.equal(outs[0].view(T.int16), outs[1].view(T.int16))
