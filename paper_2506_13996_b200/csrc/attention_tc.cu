@@ -1214,10 +1214,10 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 // both CTAs' MMAs (multicast commit onto qs_empty, count 2).
 // KT: the K block lives in TMEM (written once by the elementwise warps) and S^T = K Q^T reads only its B
 // operand from smem: M=128 N=64 MMAs run at the full tensor rate from TMEM but at 2/3 of it with both
-// operands in smem (tools/micro/mma_pair_rate.cu).  The 64 columns come from single-buffering dP^T:
-// TMEM = S^T[2] (64 each) | dP^T (64) | K (64) | dV (128) | dK (128).  dP^T(it+1) is issued as soon as
-// the elementwise warps have consumed dP^T(it) (pd_full(it)), ahead of acc(it), so the elementwise phase of
-// it+1 still overlaps acc(it) + S^T(it+2).
+// operands in smem (tools/micro/mma_pair_rate.cu).  The 64 columns come from single-buffering S^T:
+// TMEM = S^T (64) | dP^T[2] (64 each) | K (64) | dV (128) | dK (128).  The elementwise warps release S^T
+// (s_free) right after loading it and write P^T / dS^T into the consumed dP^T buffer, so S^T(it+1) and
+// dP^T(it+1) run while the elementwise phase of it computes.
 template <bool MC, bool KT>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
@@ -1234,10 +1234,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint64_t* s_full = qs_empty + NQS;    // [2]
     uint64_t* pd_full = s_full + 2;       // [2]
     uint64_t* acc_done = pd_full + 2;
-    uint64_t* dp_full = acc_done + 1;     // KT: single dP^T buffer
-    uint64_t* k_ready = dp_full + 1;      // KT: K block written to TMEM
+    uint64_t* s_free = acc_done + 1;      // KT: the single S^T buffer has been read
+    uint64_t* k_ready = s_free + 1;       // KT: K block written to TMEM
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(k_ready + 1);
-    constexpr uint32_t DP_COL = 128, K_COL = 192;  // KT layout
+    constexpr uint32_t DP_COL = 64, K_COL = 192;  // KT layout: S^T at 0, dP^T[b] at 64 + 64 b
     const int warp = warp_id(), lane = lane_id();
     const int nkb = (int)(s / 128);
     const int kb = (int)blockIdx.x;  // small kb = most work: launched first
@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             mbar_init(&pd_full[i], BW_NEW * 32);
         }
         mbar_init(acc_done, 1);
-        mbar_init(dp_full, 1);
+        mbar_init(s_free, BW_NEW * 32);
         mbar_init(k_ready, BW_NEW * 32);
         fence_barrier_init();
     }
@@ -1330,24 +1330,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             mbar_wait(kv_full, 0);
             if (KT) mbar_wait(k_ready, 0);
             const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V;
-            auto issue_s = [&](int it) {  // KT: S^T only, A = K from TMEM
+            auto issue_sdp_kt = [&](int it) {  // KT: S^T (A = K from TMEM) into the single S^T buffer, dP^T[it&1]
                 const int st = it % NQS;
                 mbar_wait(&qs_full[st], (it / NQS) & 1);
+                if (it > 0) mbar_wait(s_free, (it - 1) & 1);
                 tc_fence_after();
-                const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES;
-                const uint32_t d_s = tmem + (it & 1) * 64;
+                const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ts_w(d_s, tmem + K_COL + kk * 8, kdesc_r(qb_, kk, 8192), id_s, kk > 0);
+                    mma_bf16_ts_w(tmem, tmem + K_COL + kk * 8, kdesc_r(qb_, kk, 8192), id_s, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss_w(tmem + DP_COL + (it & 1) * 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s,
+                                  kk > 0);
                 mma_commit_w(&s_full[it & 1]);
-            };
-            auto issue_dp = [&](int it) {  // KT: dP^T into the single dP^T buffer (qs_full(it) already waited)
-                const int st = it % NQS;
-                const uint32_t dob = sbase + OFF_QS + st * 2 * QS_BYTES + QS_BYTES;
-#pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
-                    mma_bf16_ss_w(tmem + DP_COL, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
-                mma_commit_w(dp_full);
             };
             auto issue_sdp = [&](int it) {
                 const int st = it % NQS;
@@ -1369,7 +1365,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 tc_fence_after();
                 before();
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
-                const uint32_t sb = tmem + b * (KT ? 64 : 128);
+                const uint32_t sb = KT ? tmem + DP_COL + b * 64 : tmem + b * 128;
                 // A operands from TMEM: column group g packed P^T for q [16g, 16g+16) into S^T columns
                 // [16g, 16g+8) and dS^T into [16g+8, 16g+16) of buffer b
 #pragma unroll
@@ -1383,12 +1379,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 else mma_commit_w(&qs_empty[st]);
             };
             if constexpr (KT) {
-                // order: S(0) dP(0) S(1) | per it: [wait pd_full(it)] dP(it+1) acc(it) S(it+2)
-                if (total > 0) { issue_s(0); issue_dp(0); }
-                if (total > 1) issue_s(1);
+                // order: S/dP(0) | per it: [wait s_free(it)] S/dP(it+1) [wait pd_full(it)] acc(it)
+                if (total > 0) issue_sdp_kt(0);
                 for (int it = 0; it < total; ++it) {
-                    issue_acc(it, [&] { if (it + 1 < total) issue_dp(it + 1); });
-                    if (it + 2 < total) issue_s(it + 2);
+                    if (it + 1 < total) issue_sdp_kt(it + 1);
+                    issue_acc(it, [] {});
                 }
             } else {
                 if (total > 0) issue_sdp(0);
@@ -1422,25 +1417,32 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             tc_fence_before();
             mbar_arrive(k_ready);
         }
-        const uint32_t sstride = KT ? 64 : 128, dpoff = KT ? DP_COL : 64;
+
         int qblk = 0;  // iteration it = (q head it / nqb, q block qb_first + it % nqb), kept incrementally
         for (int it = 0; it < total; ++it) {
             const int b = it & 1;
             const int qq = (qb_first + qblk) * BQB + grp * 16;
             if (++qblk == nqb) qblk = 0;
             mbar_wait(&s_full[b], (it >> 1) & 1);
-            if (KT) mbar_wait(dp_full, it & 1);
             tc_fence_after();
 #ifdef SPT_EXP_NO_ELEM
             tc_fence_before();
+            if (KT) mbar_arrive(s_free);
             mbar_arrive(&pd_full[b]);
             continue;
 #endif
             uint32_t sv[16], dv[16];
-            const uint32_t sbuf = tmem + lo + b * sstride;
+            // P^T / dS^T go back into the consumed S^T columns (KT: into the consumed dP^T buffer)
+            const uint32_t sbuf = KT ? tmem + lo : tmem + lo + b * 128;
+            const uint32_t dpbuf = KT ? tmem + lo + DP_COL + b * 64 : sbuf + 64;
+            const uint32_t pbuf = KT ? dpbuf : sbuf;
             tmem_ld16(sbuf + grp * 16, sv);
-            tmem_ld16((KT ? tmem + lo + dpoff : sbuf + dpoff) + grp * 16, dv);
+            tmem_ld16(dpbuf + grp * 16, dv);
             tmem_ld_wait();
+            if constexpr (KT) {
+                tc_fence_before();
+                mbar_arrive(s_free);
+            }
             // the stage's statistics landed with Q/dO (s_full(it) follows the MMA's qs_full wait) and the
             // stage is not recycled before acc(it) completes, which needs this warp's arrival
             const uint32_t lsm = sbase + OFF_LD + (it % NQS) * 512 + grp * 64;
@@ -1480,8 +1482,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             };
             if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
             else body(std::false_type{});
-            tmem_st8(sbuf + grp * 16, pw);
-            tmem_st8(sbuf + grp * 16 + 8, sw);
+            tmem_st8(pbuf + grp * 16, pw);
+            tmem_st8(pbuf + grp * 16 + 8, sw);
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&pd_full[b]);
@@ -2289,13 +2291,12 @@ int g_attn_dkdv_pair = [] {
     return e ? (e[0] == '1' ? 1 : 0) : (SPT_DKDV_PAIR_DEFAULT != 0 ? 1 : 0);
 }();
 
-#ifndef SPT_DKDV_KT_DEFAULT
-#define SPT_DKDV_KT_DEFAULT 0
-#endif
-// SPT_ATTN_DKDV_KT=0|1: dK/dV pass with the K block resident in TMEM; spt_tuning_set("attn_dkdv_kt", v)
+// SPT_ATTN_DKDV_KT=0|1|2: dK/dV pass with the K block resident in TMEM: off, on, or (2, default) on for
+// plain causal attention and off for packed sequences, as measured (profiles/r1z3_dkdv_variants.txt);
+// spt_tuning_set("attn_dkdv_kt", v)
 int g_attn_dkdv_kt = [] {
     const char* e = getenv("SPT_ATTN_DKDV_KT");
-    return e ? (e[0] == '1' ? 1 : 0) : (SPT_DKDV_KT_DEFAULT != 0 ? 1 : 0);
+    return e ? atoi(e) : 2;
 }();
 
 size_t attn_bwd_tc_workspace(int64_t s, int hq) {
@@ -2350,6 +2351,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         SPT_CUDA(cudaGetLastError());
         return true;
     }
+    const bool kt = g_attn_dkdv_kt == 1 || (g_attn_dkdv_kt == 2 && seg == nullptr);
     if (g_attn_dkdv_pair != 0 && (s / 128) % 2 == 0) {  // 2-SM MMAs over key-block pairs
         CUtensorMap t32 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 32);
         CUtensorMap do32 = make_tmap_bf16_2d(dout, (uint64_t)hq * d, (uint64_t)s, (uint64_t)hq * d, 64, 32);
@@ -2380,10 +2382,10 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        SPT_CUDA(cudaLaunchKernelEx(&cfg, g_attn_dkdv_kt ? fatc::dkdv_tc_kernel<true, true> : fatc::dkdv_tc_kernel<true, false>,
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, kt ? fatc::dkdv_tc_kernel<true, true> : fatc::dkdv_tc_kernel<true, false>,
                                     t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, (const bf16*)qkv));
     } else {
-        auto kern = g_attn_dkdv_kt ? fatc::dkdv_tc_kernel<false, true> : fatc::dkdv_tc_kernel<false, false>;
+        auto kern = kt ? fatc::dkdv_tc_kernel<false, true> : fatc::dkdv_tc_kernel<false, false>;
         kern<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM, st>>>(
             t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, (const bf16*)qkv);
     }

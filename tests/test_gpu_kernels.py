@@ -328,8 +328,9 @@ def test_attention_bwd_fused_scheme(s, hq, hkv, packed):
 @pytest.mark.parametrize("switch", ["attn_dkdv_pair", "attn_dkdv_kt", "attn_dq_tmem"])
 @pytest.mark.parametrize("s,hq,hkv,packed", [(1024, 4, 1, False), (2048, 8, 2, True), (768, 2, 2, False)])
 def test_attention_bwd_variants_bitwise(switch, s, hq, hkv, packed):
-    """The measured-and-kept-opt-in dK/dV variants (2-SM MMAs over CTA pairs; K resident in TMEM) and the dQ
-    variant toggle compute the same sums in the same order as the default kernels: bitwise equal dQ/dK/dV."""
+    """The dK/dV variants (2-SM MMAs over CTA pairs, opt-in; K resident in TMEM, default for causal) and the
+    smem-operand dQ pass compute the same sums in the same order as the kernels they replace: bitwise equal
+    dK/dV (and dQ for the dK/dV switches)."""
     T = torch()
     L = _lib()
     d = 128
@@ -342,9 +343,9 @@ def test_attention_bwd_variants_bitwise(switch, s, hq, hkv, packed):
     S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, S.ptr(seg), scale, o.data_ptr(), lse.data_ptr(), None))
     ws = T.empty(L.spt_attn_bwd_workspace(s, hq, hkv, d), dtype=T.uint8, device="cuda")
     outs = []
-    default = 1 if switch == "attn_dq_tmem" else 0
+    first, second, default = {"attn_dkdv_pair": (0, 1, 0), "attn_dkdv_kt": (0, 1, 2), "attn_dq_tmem": (1, 0, 1)}[switch]
     try:
-        for v in (default, 1 - default):
+        for v in (first, second):
             S.check(L.spt_tuning_set(switch.encode(), v))
             g = T.zeros(s, hq + 2 * hkv, d, dtype=T.bfloat16, device="cuda")
             S.check(L.spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
