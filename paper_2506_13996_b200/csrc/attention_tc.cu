@@ -73,6 +73,24 @@ __device__ unsigned long long g_dq_prof[8];  // [0] MMA wait kv, [1] MMA wait ds
                               // forward softmax is issue-bound, not MUFU-bound, on B200)
 #endif
 
+// Grid-order remap for the Q-outer kernels (grid = (q head, row block), row blocks longest first).
+// kv_major = 0: q heads fastest — one wave streams the K/V of every kv head.  kv_major = 1: kv heads
+// slowest, then row block, then the q heads of the GQA group — consecutive waves share one kv head's K/V,
+// which then stays in L2 instead of being re-read from HBM by every wave.
+__device__ __forceinline__ void grid_head_row(int kv_major, int hq, int hkv, int& h, int& yb) {
+    if (!kv_major) {
+        h = blockIdx.x;
+        yb = blockIdx.y;
+        return;
+    }
+    const int grp = hq / hkv;
+    const int L = blockIdx.x + blockIdx.y * gridDim.x;
+    const int per = grp * gridDim.y;
+    const int kvh = L / per, rem = L - kvh * per;
+    yb = rem / grp;
+    h = kvh * grp + (rem - yb * grp);
+}
+
 __device__ __forceinline__ void lds128(uint32_t addr, float& a, float& b, float& c, float& d) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
 }
@@ -134,7 +152,7 @@ constexpr int SMEM = OFF_BAR + 512 + 1024;
 __global__ void __launch_bounds__(THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                   int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
-                  float* __restrict__ lse) {
+                  float* __restrict__ lse, int kv_major) {
     using namespace fw;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -152,8 +170,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int npairs = (int)((s + 2 * BQ - 1) / (2 * BQ));  // s % 256 == 128: the last pair holds one tile
     // grid = (q head, query-tile pair): heads vary fastest so one wave of CTAs streams the K/V of every kv
     // head at once instead of 148 CTAs hammering the same K/V lines (L2-slice hot spot); longest rows first
-    const int pair = npairs - 1 - (int)blockIdx.y;
-    const int h = blockIdx.x;
+    int h, yb;
+    grid_head_row(kv_major, hq, hkv, h, yb);
+    const int pair = npairs - 1 - yb;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)pair * 2 * BQ;
     const bool has1 = q0 + BQ < s;  // second query tile present
@@ -1007,7 +1026,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dq_tmem_kernel(const __grid_constant__ CUtensorMap tkv, const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
                    int64_t s, int hq, int hkv, const int32_t* __restrict__ seg, const float* __restrict__ lse2v,
-                   const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv) {
+                   const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv, int kv_major) {
     using namespace dqt;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1021,8 +1040,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
     const int warp = warp_id(), lane = lane_id();
     const int nqb = (int)(s / 128);
-    const int qb = nqb - 1 - (int)blockIdx.y;  // longest rows first; heads vary fastest
-    const int h = blockIdx.x;
+    int h, yb;
+    grid_head_row(kv_major, hq, hkv, h, yb);
+    const int qb = nqb - 1 - yb;  // longest rows first
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)qb * 128;
     const int jb = seg ? (int)(seg[q0] / BKB) : 0;
@@ -2209,6 +2229,20 @@ extern "C" int spt_debug_dq_prof(unsigned long long* out, int reset) {
 #endif
 }
 
+// SPT_ATTN_KV_MAJOR (bit 0: forward, bit 1: dQ pass; run time: spt_tuning_set("attn_kv_major", v)): grid
+// order of the Q-outer kernels, see grid_head_row.  -1 (default): kv-major for both once K and V of all kv
+// heads (s * hkv * d * 4 bytes) outgrow ~L2 — measured (profiles/r1z3_kv_major.txt): 32K x 8 kv heads
+// (134 MB) is faster heads-fastest, 48K x 8 (201 MB) and beyond kv-major (forward -10% at 48K, -13% at
+// 128K; dQ pass -1.4% / -2.7%).  With one kv head the two orders coincide.
+int g_attn_kv_major = [] {
+    const char* e = getenv("SPT_ATTN_KV_MAJOR");
+    return e ? atoi(e) : -1;
+}();
+static int kv_major_mask(int64_t s, int hkv, int d) {
+    if (g_attn_kv_major >= 0) return g_attn_kv_major;
+    return (double)s * hkv * d * 4 > 160e6 ? 3 : 0;
+}
+
 // SPT_ATTN_FWD_TMEM=0|1 (run time: spt_tuning_set("attn_fwd_tmem", v)): forward with Q resident in TMEM
 int g_attn_fwd_tmem = [] {
     const char* e = getenv("SPT_ATTN_FWD_TMEM");
@@ -2234,7 +2268,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                                                                               scale * fatc::LOG2E, (bf16*)o, lse);
     else
         fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
-                                                                          (bf16*)o, lse);
+                                                                          (bf16*)o, lse, kv_major_mask(s, hkv, d) & 1);
     count_launch("attn_fwd_tc");
     SPT_CUDA(cudaGetLastError());
     return true;
@@ -2393,7 +2427,8 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
     SPT_CUDA(cudaGetLastError());
     if (dq_tmem()) {  // Q / dO resident in TMEM: S and dP MMAs read only their B operand from smem
         fatc::dq_tmem_kernel<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dqt::SMEM, st>>>(
-            t64, (const bf16*)qkv, (const bf16*)dout, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv);
+            t64, (const bf16*)qkv, (const bf16*)dout, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv,
+            (kv_major_mask(s, hkv, d) >> 1) & 1);
     } else if (dq_multicast() && (hq / hkv) % 2 == 0) {  // head pairs of one kv head share a multicast K/V stream
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)hq, (unsigned)(s / 128));

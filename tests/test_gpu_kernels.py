@@ -359,3 +359,34 @@ def test_attention_bwd_variants_bitwise(switch, s, hq, hkv, packed):
         assert rel_err(to_np(outs[1][:, :hq]), to_np(outs[0][:, :hq]).astype(np.float64)) < 1e-2
     else:
         assert T.equal(outs[0].view(T.int16), outs[1].view(T.int16))
+
+
+@pytest.mark.parametrize("s,hq,hkv,packed", [(1024, 8, 2, False), (1536, 12, 3, True), (640, 4, 4, False)])
+def test_attention_grid_order_bitwise(s, hq, hkv, packed):
+    """kv-major grid order of the forward and dQ pass (attn_kv_major, default above ~L2-sized K/V) only
+    reorders CTAs: O, lse and dQ/dK/dV are bitwise equal to the heads-fastest order."""
+    T = torch()
+    L = _lib()
+    d = 128
+    qkv, dout, starts = _attn_case(s, hq, hkv, d, packed, s + 7 * hq)
+    qkvd, doutd = bf16_dev(qkv), bf16_dev(dout)
+    seg = T.from_numpy(starts.astype(np.int32)).cuda() if starts is not None else None
+    scale = 1.0 / math.sqrt(d)
+    ws = T.empty(L.spt_attn_bwd_workspace(s, hq, hkv, d), dtype=T.uint8, device="cuda")
+    outs = []
+    try:
+        for v in (0, 3):
+            S.check(L.spt_tuning_set(b"attn_kv_major", v))
+            o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+            lse = T.empty(hq, s, device="cuda")
+            S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, S.ptr(seg), scale, o.data_ptr(), lse.data_ptr(),
+                                   None))
+            g = T.zeros(s, hq + 2 * hkv, d, dtype=T.bfloat16, device="cuda")
+            S.check(L.spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
+                                   S.ptr(seg), scale, g.data_ptr(), ws.data_ptr(), None))
+            outs.append((o, lse, g))
+        T.cuda.synchronize()
+    finally:
+        S.check(L.spt_tuning_set(b"attn_kv_major", -1))
+    for a, b in zip(outs[0], outs[1]):
+        assert T.equal(a.view(T.int16) if a.dtype == T.bfloat16 else a, b.view(T.int16) if b.dtype == T.bfloat16 else b)
