@@ -74,21 +74,23 @@ __device__ unsigned long long g_dq_prof[8];  // [0] MMA wait kv, [1] MMA wait ds
 #endif
 
 // Grid-order remap for the Q-outer kernels (grid = (q head, row block), row blocks longest first).
-// kv_major = 0: q heads fastest — one wave streams the K/V of every kv head.  kv_major = 1: kv heads
-// slowest, then row block, then the q heads of the GQA group — consecutive waves share one kv head's K/V,
-// which then stays in L2 instead of being re-read from HBM by every wave.
-__device__ __forceinline__ void grid_head_row(int kv_major, int hq, int hkv, int& h, int& yb) {
-    if (!kv_major) {
+// CTAs are dispatched in order of groups of `kvg` kv heads (slowest), then row block, then the q heads of
+// the group.  kvg >= hkv: q heads fastest — one wave streams the K/V of every kv head.  kvg = 1: kv-major —
+// consecutive waves share one kv head's K/V, which then stays in L2 instead of being re-read from HBM by
+// every wave, at the price of more CTAs reading the same lines at once.
+__device__ __forceinline__ void grid_head_row(int kvg, int hq, int hkv, int& h, int& yb) {
+    if (kvg >= hkv) {
         h = blockIdx.x;
         yb = blockIdx.y;
         return;
     }
-    const int grp = hq / hkv;
+    const int hg = kvg * (hq / hkv);  // q heads per full group; the last group may be partial
     const int L = blockIdx.x + blockIdx.y * gridDim.x;
-    const int per = grp * gridDim.y;
-    const int kvh = L / per, rem = L - kvh * per;
-    yb = rem / grp;
-    h = kvh * grp + (rem - yb * grp);
+    const int per = hg * gridDim.y;
+    const int g = L / per, rem = L - g * per;
+    const int hgl = min(hg, hq - g * hg);
+    yb = rem / hgl;
+    h = g * hg + (rem - yb * hgl);
 }
 
 __device__ __forceinline__ void lds128(uint32_t addr, float& a, float& b, float& c, float& d) {
@@ -152,7 +154,7 @@ constexpr int SMEM = OFF_BAR + 512 + 1024;
 __global__ void __launch_bounds__(THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                   int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
-                  float* __restrict__ lse, int kv_major) {
+                  float* __restrict__ lse, int kvg) {
     using namespace fw;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // grid = (q head, query-tile pair): heads vary fastest so one wave of CTAs streams the K/V of every kv
     // head at once instead of 148 CTAs hammering the same K/V lines (L2-slice hot spot); longest rows first
     int h, yb;
-    grid_head_row(kv_major, hq, hkv, h, yb);
+    grid_head_row(kvg, hq, hkv, h, yb);
     const int pair = npairs - 1 - yb;
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)pair * 2 * BQ;
@@ -1026,7 +1028,7 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dq_tmem_kernel(const __grid_constant__ CUtensorMap tkv, const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
                    int64_t s, int hq, int hkv, const int32_t* __restrict__ seg, const float* __restrict__ lse2v,
-                   const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv, int kv_major) {
+                   const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv, int kvg) {
     using namespace dqt;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1041,7 +1043,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const int warp = warp_id(), lane = lane_id();
     const int nqb = (int)(s / 128);
     int h, yb;
-    grid_head_row(kv_major, hq, hkv, h, yb);
+    grid_head_row(kvg, hq, hkv, h, yb);
     const int qb = nqb - 1 - yb;  // longest rows first
     const int kvh = h / (hq / hkv);
     const int64_t q0 = (int64_t)qb * 128;
@@ -2229,18 +2231,18 @@ extern "C" int spt_debug_dq_prof(unsigned long long* out, int reset) {
 #endif
 }
 
-// SPT_ATTN_KV_MAJOR (bit 0: forward, bit 1: dQ pass; run time: spt_tuning_set("attn_kv_major", v)): grid
-// order of the Q-outer kernels, see grid_head_row.  -1 (default): kv-major for both once K and V of all kv
-// heads (s * hkv * d * 4 bytes) outgrow ~L2 — measured (profiles/r1z3_kv_major.txt): 32K x 8 kv heads
-// (134 MB) is faster heads-fastest, 48K x 8 (201 MB) and beyond kv-major (forward -10% at 48K, -13% at
-// 128K; dQ pass -1.4% / -2.7%).  With one kv head the two orders coincide.
-int g_attn_kv_major = [] {
-    const char* e = getenv("SPT_ATTN_KV_MAJOR");
-    return e ? atoi(e) : -1;
+// SPT_ATTN_KV_GROUP (run time: spt_tuning_set("attn_kv_group", v)): kv heads per dispatch group of the
+// Q-outer kernels' grid, see grid_head_row.  0 (default): heads fastest while K and V of all kv heads
+// (s * hkv * d * 4 bytes) fit ~L2, kv-major (1) beyond — measured (profiles/r1z3_kv_major.txt): 32K x 8 kv
+// heads (134 MB) is faster heads-fastest, 48K x 8 (201 MB) and beyond kv-major (forward -10% at 48K, -13% at
+// 128K; dQ pass -1.4% / -2.7%).  With one kv head all orders coincide.
+int g_attn_kv_group = [] {
+    const char* e = getenv("SPT_ATTN_KV_GROUP");
+    return e ? atoi(e) : 0;
 }();
-static int kv_major_mask(int64_t s, int hkv, int d) {
-    if (g_attn_kv_major >= 0) return g_attn_kv_major;
-    return (double)s * hkv * d * 4 > 160e6 ? 3 : 0;
+static int kv_group(int64_t s, int hkv, int d) {
+    if (g_attn_kv_group > 0) return g_attn_kv_group;
+    return (double)s * hkv * d * 4 > 160e6 ? 1 : hkv;
 }
 
 // SPT_ATTN_FWD_TMEM=0|1 (run time: spt_tuning_set("attn_fwd_tmem", v)): forward with Q resident in TMEM
@@ -2268,7 +2270,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                                                                               scale * fatc::LOG2E, (bf16*)o, lse);
     else
         fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
-                                                                          (bf16*)o, lse, kv_major_mask(s, hkv, d) & 1);
+                                                                          (bf16*)o, lse, kv_group(s, hkv, d));
     count_launch("attn_fwd_tc");
     SPT_CUDA(cudaGetLastError());
     return true;
@@ -2428,7 +2430,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
     if (dq_tmem()) {  // Q / dO resident in TMEM: S and dP MMAs read only their B operand from smem
         fatc::dq_tmem_kernel<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dqt::SMEM, st>>>(
             t64, (const bf16*)qkv, (const bf16*)dout, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv,
-            (kv_major_mask(s, hkv, d) >> 1) & 1);
+            kv_group(s, hkv, d));
     } else if (dq_multicast() && (hq / hkv) % 2 == 0) {  // head pairs of one kv head share a multicast K/V stream
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)hq, (unsigned)(s / 128));

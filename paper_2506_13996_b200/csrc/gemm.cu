@@ -254,7 +254,7 @@ extern int g_attn_fwd_tmem;  // attention_tc.cu
 extern int g_mlp_bwd_group;  // engine.cu
 extern int g_attn_dkdv_pair;  // attention_tc.cu
 extern int g_attn_dkdv_kt;    // attention_tc.cu
-extern int g_attn_kv_major;   // attention_tc.cu
+extern int g_attn_kv_group;   // attention_tc.cu
 }
 
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
@@ -269,8 +269,8 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
             spt::g_attn_fwd_tmem = value;
             return;
         }
-        if (n == "attn_kv_major") {
-            spt::g_attn_kv_major = value;
+        if (n == "attn_kv_group") {
+            spt::g_attn_kv_group = value;
             return;
         }
         if (n == "attn_dkdv_kt") {

@@ -363,8 +363,8 @@ def test_attention_bwd_variants_bitwise(switch, s, hq, hkv, packed):
 
 @pytest.mark.parametrize("s,hq,hkv,packed", [(1024, 8, 2, False), (1536, 12, 3, True), (640, 4, 4, False)])
 def test_attention_grid_order_bitwise(s, hq, hkv, packed):
-    """kv-major grid order of the forward and dQ pass (attn_kv_major, default above ~L2-sized K/V) only
-    reorders CTAs: O, lse and dQ/dK/dV are bitwise equal to the heads-fastest order."""
+    """Grouped / kv-major grid orders of the forward and dQ pass (attn_kv_group; kv-major is the default above
+    ~L2-sized K/V) only reorder CTAs: O, lse and dQ/dK/dV are bitwise equal to the heads-fastest order."""
     T = torch()
     L = _lib()
     d = 128
@@ -375,8 +375,8 @@ def test_attention_grid_order_bitwise(s, hq, hkv, packed):
     ws = T.empty(L.spt_attn_bwd_workspace(s, hq, hkv, d), dtype=T.uint8, device="cuda")
     outs = []
     try:
-        for v in (0, 3):
-            S.check(L.spt_tuning_set(b"attn_kv_major", v))
+        for v in (hkv, 1, 2):
+            S.check(L.spt_tuning_set(b"attn_kv_group", v))
             o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
             lse = T.empty(hq, s, device="cuda")
             S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, S.ptr(seg), scale, o.data_ptr(), lse.data_ptr(),
@@ -387,6 +387,8 @@ def test_attention_grid_order_bitwise(s, hq, hkv, packed):
             outs.append((o, lse, g))
         T.cuda.synchronize()
     finally:
-        S.check(L.spt_tuning_set(b"attn_kv_major", -1))
-    for a, b in zip(outs[0], outs[1]):
-        assert T.equal(a.view(T.int16) if a.dtype == T.bfloat16 else a, b.view(T.int16) if b.dtype == T.bfloat16 else b)
+        S.check(L.spt_tuning_set(b"attn_kv_group", 0))
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert T.equal(a.view(T.int16) if a.dtype == T.bfloat16 else a,
+                           b.view(T.int16) if b.dtype == T.bfloat16 else b)
