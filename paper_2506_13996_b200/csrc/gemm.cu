@@ -135,8 +135,8 @@ static int env_int(const char* name, int dflt) {
     return (e && e[0]) ? atoi(e) : dflt;
 }
 // Experiment / tuning switches: initialised from the environment, changeable at run time through
-// spt_tuning_set (A/B comparisons inside one process).  gemm_1sm=1 disables CTA pairs, gemm_pair_mn=1 also
-// runs MN-major operand shapes as pairs, gemm_bn=128|256 forces the N tile (0 = per-shape choice),
+// spt_tuning_set (A/B comparisons inside one process).  gemm_1sm=1 disables CTA pairs, gemm_pair_mn selects
+// which MN-major operand shapes run as pairs (0 = default none, 1 all, 2 by shape: see pair_mn), gemm_bn=128|256 forces the N tile (0 = per-shape choice),
 // epi_tstore = fp32 epilogue mode: 0 per-thread stores, 1 smem-transposed coalesced stores, 2 (default) TMA
 // store / reduce-add on the 1-SM kernel (the pair kernel and the stats epilogue use mode 1).
 struct GemmTuning {
@@ -150,7 +150,17 @@ static GemmTuning& tuning() {
     return t;
 }
 static bool use_pair_gemm() { return tuning().gemm_1sm != 1; }
-static bool pair_mn() { return tuning().gemm_pair_mn == 1; }
+// MN-major operand shapes as CTA pairs: 0 never, 1 always, 2 by shape — pairs where the isolated per-site
+// A/B (profiles/README.md, gemm_sites) had them ahead: fp32-accumulate weight gradients with a long K
+// (lm_head, QKV / O projections over the whole sequence) and bf16 data gradients except the short-M /
+// long-K TiledMLP dX (whose 1-SM kernel keeps the TMA reduce-add epilogue and fills the SMs better).
+static bool pair_mn(int64_t M, int64_t K, int kind) {
+    const int v = tuning().gemm_pair_mn;
+    if (v != 2) return v == 1;
+    if (kind == EPI_F32) return K >= 8192;
+    if (kind == EPI_BF16) return !(M <= 4096 && K >= 16384);
+    return false;
+}
 static int forced_bn() { return tuning().gemm_bn; }
 static int epi_tstore() { return tuning().epi_tstore; }
 
@@ -216,9 +226,10 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
     // per 256 columns, so those kinds keep BN = 256.
     const bool bn_free = kind == EPI_BF16 || kind == EPI_F32;
     const int bn = bn_free && (forced_bn() == 128) ? 128 : 256;
-    // CTA pairs win for K-major x K-major (forward / logits) GEMMs; with MN-major operands the 1-SM
-    // kernel measured faster inside the layer step (profiles/README.md, per-site breakdown).
-    if (M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn()) && use_pair_gemm()) {
+    // CTA pairs win for K-major x K-major (forward / logits) GEMMs.  MN-major operand shapes (backward) go
+    // by pair_mn: pairs win short bursts (3 steps: -1.4..-3.3% per L1 step with the shape rule) but lose
+    // sustained, power-capped runs (12 steps: +3.7%), so the default keeps them on the 1-SM kernel.
+    if (M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn(M, K, kind)) && use_pair_gemm()) {
         if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
         else dispatch_pair<256>(A, B, M, N, K, kind, ep, st);

@@ -1,5 +1,5 @@
 """Step-level A/B of a run-time tuning switch (spt_tuning_set) inside one process: the L1 layer step is timed
-(CUDA events, 3 steps after 1 warm-up) alternately under each value, several rounds, and the best time per
+(CUDA events, --group steps, default 3, after 1 warm-up) alternately under each value, several rounds, and the best time per
 value is reported.  Interleaving cancels most of the pod-to-pod and thermal/power drift that makes separate
 bench runs differ by several percent.
 
@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("switch")
 ap.add_argument("--rounds", type=int, default=4)
 ap.add_argument("--seq", type=int, default=32768)
+ap.add_argument("--group", type=int, default=3, help="timed steps per value per round (10+: sustained, power-capped)")
 a = ap.parse_args()
 key, vals = a.switch.split("=")
 vals = [int(v) for v in vals.split(",")]
@@ -44,11 +45,11 @@ for _ in range(a.rounds):
         eng.step_async(x, lab, None, on_host=False)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(3):
+        for _ in range(a.group):
             eng.step_async(x, lab, None, on_host=False)
         e1.record()
         torch.cuda.synchronize()
-        best[v] = min(best[v], e0.elapsed_time(e1) / 3)
+        best[v] = min(best[v], e0.elapsed_time(e1) / a.group)
         losses[v] = eng.read_loss()[0]
 S.check(L.spt_tuning_set(key.encode(), vals[0]))
 print(json.dumps({"switch": key, "ms_per_step_best": {str(v): round(t, 2) for v, t in best.items()},
