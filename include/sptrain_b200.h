@@ -164,6 +164,17 @@ spt_status spt_label_stats(const int64_t* labels, int64_t n, int64_t vocab, int6
 spt_status spt_segment_starts(const int64_t* position_ids, int64_t n, int32_t* starts, int32_t* err_flag,
                               void* stream);
 
+/* Token embedding.  input_ids: DEVICE int64 [n]; table: [vocab][h]
+ * bf16; x: [n][h] bf16.  err_flag (device int32) is set to 3 when an id is outside [0, vocab).
+ * Backward: dtable [vocab][h] fp32 (+)= per-id sums of dx rows, each summed in ascending token order
+ * (deterministic, no atomics); accumulate = 0 overwrites (rows with no token become 0).
+ * workspace: spt_embed_bwd_workspace(n, vocab) bytes. */
+spt_status spt_embed_fwd(const int64_t* input_ids, int64_t n, int64_t vocab, int64_t h, const void* table, void* x,
+                         int32_t* err_flag, void* stream);
+size_t spt_embed_bwd_workspace(int64_t n, int64_t vocab);
+spt_status spt_embed_bwd(const int64_t* input_ids, int64_t n, int64_t vocab, int64_t h, const void* dx, float* dtable,
+                         int32_t accumulate, int32_t* err_flag, void* workspace, void* stream);
+
 /* tiled_logits_loss fused fwd+bwd: for each tile of `tile_n` tokens,
  * logits = x W^T (fp32, [tile_n, V] workspace only), CE (sum, count), dlogits scaled by
  * *grad_scale_dev (1/global count, device scalar), dx = dlogits W (bf16), dW (fp32) +=

@@ -545,6 +545,34 @@ def synth_batch(cfg: LayerConfig, n: int, seed: int, ignore_frac: float = 0.05, 
     return x, shift, position_ids
 
 
+def embed_fwd(input_ids, table):
+    """Token embedding gather (SPEC.md:205 model "embedding", :223-227 forward(model, input_ids, ...)):
+    x[t] = table[input_ids[t]]; an id outside [0, V) is a validation error."""
+    ids = np.asarray(input_ids, dtype=np.int64)
+    V = table.shape[0]
+    if ids.size and (ids.min() < 0 or ids.max() >= V):
+        raise ValueError("token id outside [0, V)")
+    return table[ids]
+
+
+def embed_bwd(input_ids, dx, vocab: int, dtable=None):
+    """Embedding backward: dtable[v] (+)= sum of dx[t] over t with input_ids[t] == v, each per-id sum taken
+    in ascending t in float32 and then added to the existing row (the CUDA path's deterministic order).
+    Plain loops: test sizes only."""
+    ids = np.asarray(input_ids, dtype=np.int64)
+    dx = np.asarray(dx, dtype=np.float32)
+    out = np.zeros((vocab, dx.shape[1]), np.float32) if dtable is None else np.array(dtable, np.float32)
+    sums = {}
+    for t, v in enumerate(ids.tolist()):
+        if v in sums:
+            sums[v] = sums[v] + dx[t]
+        else:
+            sums[v] = dx[t].copy()
+    for v, acc in sums.items():
+        out[v] = out[v] + acc
+    return out
+
+
 def rope_angles(positions, head_dim: int, theta: float):
     """Rotary position embedding angles (the reference SPEC omits RoPE).
     Llama / HF convention: inv_freq[j] = theta^(-2j/d), angle[t, j] = position[t] * inv_freq[j], both in

@@ -85,6 +85,9 @@ SIGNATURES = {
     "spt_segment_starts": (I32, [P, I64, P, P, P]),
     "spt_flce_workspace": (SZ, [I64, I64]),
     "spt_rope": (I32, [P, I64, I32, I32, I32, P, I64, F32, I32, P]),
+    "spt_embed_fwd": (I32, [P, I64, I64, I64, P, P, P, P]),
+    "spt_embed_bwd_workspace": (SZ, [I64, I64]),
+    "spt_embed_bwd": (I32, [P, I64, I64, I64, P, P, I32, P, P, P]),
     "spt_memest_fixed_bytes": (I32, [C.c_double, I32, I32, I32, P]),
     "spt_memest_logits_bytes": (C.c_double, [C.c_double, C.c_double, C.c_double]),
     "spt_memest_activation_ckpt_bytes": (I32, [C.c_double, C.c_double, C.c_double, C.c_double, I32, I32, P, P]),

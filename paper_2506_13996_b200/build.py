@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = (["-DSPT_WATCHDOG"] if os.environ.get("SPT_WATCHDOG") else []) + \
         [f"-D{x}" for x in os.environ.get("SPT_EXTRA_DEFS", "").split(",") if x] + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I/usr/include"]
-SOURCES = ["util.cpp", "plan.cpp", "memest.cpp", "comm.cpp", "gemm.cu", "kernels.cu", "attention.cu", "attention_tc.cu", "tiled.cu", "engine.cu"]
+SOURCES = ["util.cpp", "plan.cpp", "memest.cpp", "comm.cpp", "gemm.cu", "kernels.cu", "attention.cu", "attention_tc.cu", "tiled.cu", "embed.cu", "engine.cu"]
 DEPS_HDR = [f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + ["../../include/sptrain_b200.h"]
 
 

@@ -41,6 +41,12 @@ void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim,
                     const int32_t* gather, int max_src, void* dst, cudaStream_t st);
 void label_stats(const int64_t* labels, int64_t n, int64_t vocab, int64_t* count_accum, int32_t* err, cudaStream_t st);
 void segment_starts(const int64_t* pos, int64_t n, int32_t* starts, int32_t* err, cudaStream_t st);
+// token embedding (embed.cu)
+size_t embed_bwd_workspace(int64_t n, int64_t V);
+void embed_fwd(const int64_t* ids, int64_t n, int64_t V, int64_t h, const void* E, void* x, int32_t* err,
+               cudaStream_t st);
+void embed_bwd(const int64_t* ids, int64_t n, int64_t V, int64_t h, const void* dx, float* dE, bool accumulate,
+               int32_t* err, void* ws, cudaStream_t st);
 // Row-wise CE over fp32 logits [rows, V]: loss_rows[r] (0 if ignored), dlogits bf16 = (softmax-onehot)*scale.
 void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V, const float* scale_dev,
              float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st);

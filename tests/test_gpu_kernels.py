@@ -392,3 +392,66 @@ def test_attention_grid_order_bitwise(s, hq, hkv, packed):
         for a, b in zip(outs[0], other):
             assert T.equal(a.view(T.int16) if a.dtype == T.bfloat16 else a,
                            b.view(T.int16) if b.dtype == T.bfloat16 else b)
+
+
+# ------------------------------------------------------------------ token embedding (f4)
+@pytest.mark.parametrize("n,V,h,repeat", [(3000, 500, 256, True), (777, 50000, 64, False), (1, 7, 8, False),
+                                          (32768, 128256, 2304, False)])
+def test_embedding_fwd_bwd_bitexact(n, V, h, repeat):
+    """Gather is bit-exact; the backward's per-id sums (ascending token order, fp32) are bit-exact against the
+    oracle, for overwrite and accumulate, and bitwise deterministic run to run."""
+    T = torch()
+    L = _lib()
+    rng = np.random.default_rng(n + V)
+    ids = rng.integers(0, 40 if repeat else V, n).astype(np.int64)
+    table = O.round_bf16(rng.standard_normal((V, h), dtype=np.float32))
+    dx = O.round_bf16(rng.standard_normal((n, h), dtype=np.float32))
+    idsd = T.from_numpy(ids).cuda()
+    tabd, dxd = bf16_dev(table), bf16_dev(dx)
+    err = T.zeros(1, dtype=T.int32, device="cuda")
+    x = T.empty(n, h, dtype=T.bfloat16, device="cuda")
+    S.check(L.spt_embed_fwd(idsd.data_ptr(), n, V, h, tabd.data_ptr(), x.data_ptr(), err.data_ptr(), None))
+    touched = np.unique(ids)
+    if n <= 4096:
+        assert np.array_equal(to_np(x), O.embed_fwd(ids, table))
+    else:  # large case: check a sample of rows
+        sel = rng.integers(0, n, 512)
+        assert np.array_equal(to_np(x)[sel], table[ids[sel]])
+    ws = T.empty(L.spt_embed_bwd_workspace(n, V), dtype=T.uint8, device="cuda")
+    base = rng.standard_normal((V, h), dtype=np.float32)
+    dE = T.from_numpy(base).cuda()
+    S.check(L.spt_embed_bwd(idsd.data_ptr(), n, V, h, dxd.data_ptr(), dE.data_ptr(), 1, err.data_ptr(),
+                            ws.data_ptr(), None))
+    dE0 = T.full((V, h), 7.0, device="cuda")
+    S.check(L.spt_embed_bwd(idsd.data_ptr(), n, V, h, dxd.data_ptr(), dE0.data_ptr(), 0, err.data_ptr(),
+                            ws.data_ptr(), None))
+    dE1 = T.full((V, h), 7.0, device="cuda")
+    S.check(L.spt_embed_bwd(idsd.data_ptr(), n, V, h, dxd.data_ptr(), dE1.data_ptr(), 0, err.data_ptr(),
+                            ws.data_ptr(), None))
+    T.cuda.synchronize()
+    assert int(err) == 0
+    assert T.equal(dE0, dE1)
+    if n <= 4096:
+        assert np.array_equal(to_np(dE), O.embed_bwd(ids, dx, V, base))
+        assert np.array_equal(to_np(dE0), O.embed_bwd(ids, dx, V))
+    else:
+        got = to_np(dE0)
+        ref = O.embed_bwd(ids, dx, V)
+        assert np.array_equal(got[touched], ref[touched])
+        assert not np.any(np.delete(got, touched, axis=0)[:1000])
+
+
+def test_embedding_rejects_bad_ids():
+    T = torch()
+    L = _lib()
+    V, h = 16, 8
+    tab = T.zeros(V, h, dtype=T.bfloat16, device="cuda")
+    x = T.empty(3, h, dtype=T.bfloat16, device="cuda")
+    for bad in ([0, 16, 1], [0, -1, 2]):
+        err = T.zeros(1, dtype=T.int32, device="cuda")
+        ids = T.tensor(bad, dtype=T.int64, device="cuda")
+        S.check(L.spt_embed_fwd(ids.data_ptr(), 3, V, h, tab.data_ptr(), x.data_ptr(), err.data_ptr(), None))
+        T.cuda.synchronize()
+        assert int(err) == 3
+    ids = T.tensor([0, 1, 2], dtype=T.int64, device="cuda")
+    assert L.spt_embed_fwd(ids.data_ptr(), 3, V, 12, tab.data_ptr(), x.data_ptr(), err.data_ptr(), None) != 0

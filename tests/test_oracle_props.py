@@ -190,3 +190,20 @@ def test_model_step_with_rope_fd_and_sp():
         return O.model_step(ls, head["g3"], head["wlm"], cfg, x, lab, P=1, rope_theta=100.0).loss
     fd = O.finite_diff_grad(loss_with, np.asarray(layers[0]["wqkv"], np.float64))
     assert np.linalg.norm(fd - r1.grads["layers.0.wqkv"]) / np.linalg.norm(fd) < 1e-6
+
+
+def test_embedding_oracle_properties():
+    """embed_bwd is the adjoint of embed_fwd: <embed_fwd(ids, E), dx> == <E, embed_bwd(ids, dx)> (f64 check),
+    and ids outside [0, V) are rejected."""
+    rng = np.random.default_rng(5)
+    V, h, n = 37, 6, 200
+    ids = rng.integers(0, V, n)
+    E = rng.standard_normal((V, h))
+    dx = rng.standard_normal((n, h)).astype(np.float32)
+    lhs = float(np.sum(O.embed_fwd(ids, E) * dx))
+    rhs = float(np.sum(E * O.embed_bwd(ids, dx, V)))
+    assert abs(lhs - rhs) < 1e-4 * max(1.0, abs(lhs))
+    with pytest.raises(ValueError):
+        O.embed_fwd([0, V], E)
+    with pytest.raises(ValueError):
+        O.embed_fwd([-1], E)
