@@ -184,6 +184,7 @@ struct StepOptions {
     float lr = 0.f;              // > 0: plain SGD update after the step
     float rms_eps = 1e-5f;
     float rope_theta = 0.f;      // > 0: rotary embedding on q/k (row f4; the reference model has none)
+    bool embed = false;          // token embedding "emb" in front of the stack; step x = int64 input_ids
 };
 
 class UlyssesLayerStep {
@@ -205,6 +206,7 @@ public:
         c.n_layers = o.n_layers;
         c.ckpt_offload = o.ckpt_offload ? 1 : 0;
         c.rope_theta = o.rope_theta;
+        c.embed = o.embed ? 1 : 0;
         check(spt_layer_create(&c, group.handle(), &l_));
     }
     UlyssesLayerStep(const UlyssesLayerStep&) = delete;

@@ -103,6 +103,7 @@ typedef struct {
     int64_t vocab;
     int32_t n_layers, sp, ckpt_offload;
     double act_bytes_per_token, act_bytes_per_seq_token;
+    int32_t embed; /* 1: token embedding table [vocab][hidden] in front of the stack (weights + grads) */
 } spt_memest_engine;
 spt_status spt_memest_engine_device_bytes(const spt_memest_engine* cfg, double seqlen, double* out);
 /* max_seqlen_solver: largest multiple of `granularity` whose estimate fits device_budget
@@ -231,6 +232,10 @@ typedef struct {
     float rope_theta;     /* > 0: rotary position embedding on q and k (Llama rotate_half convention, base
                              theta; positions = position_ids when packed, else the global token index).
                              0 = off, the reference's model (SPEC.md:261 omits RoPE) */
+    int32_t embed;        /* 1: token embedding table "emb" [vocab][hidden] in front of the stack (SPEC.md:205,
+                             :223); the step's x argument is then int64 input_ids [local_ranks * s_loc], ids
+                             outside [0, vocab) are a validation error, and grad "emb" is the per-id sum of the
+                             stack's input gradient (deterministic) */
 } spt_layer_config;
 
 typedef struct spt_layer spt_layer;

@@ -685,19 +685,26 @@ LAYER_NAMES = ("g1", "wqkv", "wo", "g2", "wg", "wu", "wd")
 
 
 def model_step(layers: list, g3, wlm, cfg: LayerConfig, x, shift_labels, position_ids=None, P: int = 1,
-               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False, rope_theta: float = 0.0) -> StepResult:
+               mlp_tiles=None, loss_tile=None, dtype=np.float64, keep_out=False, rope_theta: float = 0.0,
+               emb=None) -> StepResult:
     """One SP=P training step (fwd+bwd) of an L-layer decoder stack + final norm + lm_head as
     P in-process ranks.  `layers` holds one dict / LayerParams-like object per layer with LAYER_NAMES.
     Global mean loss via all_reduce of (sum, count); weight grads all-reduced over the SP group
     (SPEC.md:353).  Activation checkpointing and offload do not change these values,
     so this uncheckpointed restatement is the oracle for every checkpoint mode.
-    Grads are returned as {"layers.<i>.<name>": ..., "g3": ..., "wlm": ...} (plus bare names for layer 0)."""
+    Grads are returned as {"layers.<i>.<name>": ..., "g3": ..., "wlm": ...} (plus bare names for layer 0).
+    emb: token embedding table [V, h]; x then holds input_ids [N] and grads["emb"] is
+    embed_bwd of the stack's input gradient (summed over ranks like every weight grad)."""
     def get(o, k):
         return np.asarray(o[k] if isinstance(o, dict) else getattr(o, k), dtype=dtype)
 
     ps = [type("LP", (), {k: get(lp, k) for k in LAYER_NAMES}) for lp in layers]
     g3 = np.asarray(g3, dtype=dtype)
     wlm = np.asarray(wlm, dtype=dtype)
+    ids = None
+    if emb is not None:
+        ids = np.asarray(x, dtype=np.int64)
+        x = embed_fwd(ids, np.asarray(emb, dtype=dtype))
     x = np.asarray(x, dtype=dtype)
     N, h = x.shape
     if N % P:
@@ -739,6 +746,11 @@ def model_step(layers: list, g3, wlm, cfg: LayerConfig, x, shift_labels, positio
             out_grads[f"layers.{i}.{k}"] = all_reduce_sum([grads[r][k] for r in range(P)])[0]
     for k in LAYER_NAMES:
         out_grads[k] = out_grads[f"layers.0.{k}"]
+    if ids is not None:
+        dx_all = np.concatenate(dys, axis=0)
+        demb = np.zeros((wlm.shape[0], h), dtype)
+        np.add.at(demb, ids, dx_all)
+        out_grads["emb"] = demb
     res = StepResult(loss_sum=loss_sum, count=int(count), loss=loss_sum * scale, dx=np.concatenate(dys, axis=0),
                      grads=out_grads)
     if keep_out:

@@ -55,7 +55,8 @@ class LayerConfig(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("intermediate", C.c_int32), ("vocab", C.c_int64), ("seq_len", C.c_int64), ("mlp_tiles", C.c_int32),
                 ("loss_tile", C.c_int64), ("rms_eps", C.c_float), ("packed", C.c_int32), ("lr", C.c_float),
-                ("n_layers", C.c_int32), ("ckpt_offload", C.c_int32), ("rope_theta", C.c_float)]
+                ("n_layers", C.c_int32), ("ckpt_offload", C.c_int32), ("rope_theta", C.c_float),
+                ("embed", C.c_int32)]
 
 
 P = C.c_void_p
@@ -215,7 +216,7 @@ class MemestEngine(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("intermediate", C.c_int32), ("vocab", C.c_int64), ("n_layers", C.c_int32), ("sp", C.c_int32),
                 ("ckpt_offload", C.c_int32), ("act_bytes_per_token", C.c_double),
-                ("act_bytes_per_seq_token", C.c_double)]
+                ("act_bytes_per_seq_token", C.c_double), ("embed", C.c_int32)]
 
 
 def memest_fixed(param_count: float, world_size: int = 1, zero3: bool = False, offload_optimizer: bool = False):
@@ -375,11 +376,11 @@ class UlyssesLayerStep:
 
     def __init__(self, shape: ModelShape, seq_len: int, group: ProcessGroup, mlp_tiles: int = 0,
                  loss_tile: int = 0, packed: bool = False, lr: float = 0.0, rms_eps: float = 1e-5,
-                 n_layers: int = 1, ckpt_offload: bool = False, rope_theta: float = 0.0):
+                 n_layers: int = 1, ckpt_offload: bool = False, rope_theta: float = 0.0, embed: bool = False):
         self.shape, self.seq_len, self.group, self.n_layers = shape, seq_len, group, n_layers
         self.cfg = LayerConfig(shape.hidden, shape.q_heads, shape.kv_heads, shape.head_dim, shape.intermediate,
                                shape.vocab, seq_len, mlp_tiles, loss_tile, rms_eps, int(packed), lr, n_layers,
-                               int(ckpt_offload), rope_theta)
+                               int(ckpt_offload), rope_theta, int(embed))
         h = C.c_void_p()
         check(lib().spt_layer_create(C.byref(self.cfg), group.handle, C.byref(h)))
         self.handle = h
@@ -437,7 +438,8 @@ class UlyssesLayerStep:
         shapes = {"g1": (s.hidden,), "g2": (s.hidden,), "g3": (s.hidden,),
                   "wqkv": ((s.q_heads + 2 * s.kv_heads) * s.head_dim, s.hidden),
                   "wo": (s.hidden, s.q_heads * s.head_dim), "wg": (s.intermediate, s.hidden),
-                  "wu": (s.intermediate, s.hidden), "wd": (s.hidden, s.intermediate), "wlm": (s.vocab, s.hidden)}
+                  "wu": (s.intermediate, s.hidden), "wd": (s.hidden, s.intermediate), "wlm": (s.vocab, s.hidden),
+                  "emb": (s.vocab, s.hidden)}
         out = np.empty(shapes[bare], dtype=np.float32)
         check(lib().spt_layer_get_grad(self.handle, name.encode(), ptr(out)))
         return out

@@ -150,6 +150,7 @@ struct Scalars {
     float loss;
     int32_t err_label;
     int32_t err_pos;
+    int32_t err_embed;
 };
 // Gradient-accumulation window ("divide by global valid_count summed over the accumulation
 // window"): micro-steps accumulate grads of the loss SUM; finish divides by the window's global count.
@@ -162,7 +163,7 @@ struct Window {
 struct RankBufs {
     bf16 *x, *xn1, *qkv, *o, *x1, *xn2, *x2, *z;
     float *rstd1, *rstd2, *rstd3, *lse;
-    int64_t *labels, *pos;
+    int64_t *labels, *pos, *ids;
     bf16 *send_qkv, *qkv_head, *o_head, *recv_o;
     bf16 *dz, *dx1, *dO, *dx, *send_do, *do_head, *dqkv_head, *recv_dqkv, *dqkv;
 };
@@ -186,10 +187,13 @@ struct spt_layer {
     bool offload = false;  // checkpoints in pinned host memory
     std::vector<LayerW> lw;
     bf16 *g3, *wlm;
+    bool embed = false;      // token embedding in front of the stack: step inputs are input_ids
+    bf16* emb = nullptr;     // [V][h]
+    void* ws_emb = nullptr;
     // grads (one contiguous fp32 buffer; SP all-reduce is one call)
     float* gbuf;
     size_t gsize;
-    float *dg3, *dwlm;
+    float *dg3, *dwlm, *demb = nullptr;
     std::vector<RankBufs> rb;
     std::vector<std::vector<bf16*>> ck;  // [layer][local rank] checkpointed layer inputs (device or host)
     std::vector<bf16*> xpf;              // [local rank] prefetch buffer for offloaded checkpoints
@@ -272,11 +276,13 @@ static void build_layer(spt_layer* Ly) {
     }
     Ly->g3 = Ly->abf(h, kWeights);
     Ly->wlm = Ly->abf(V * h, kWeights);
-    // grads: [layer 0 .. NL-1: g1, wqkv, wo, g2, wgu, wd] [g3] [wlm], 64-float aligned segments
+    Ly->embed = c.embed != 0;
+    if (Ly->embed) Ly->emb = Ly->abf(V * h, kWeights);
+    // grads: [layer 0 .. NL-1: g1, wqkv, wo, g2, wgu, wd] [g3] [wlm] [emb], 64-float aligned segments
     const size_t lsz[6] = {(size_t)h, (size_t)(Ly->qkv_out * h), (size_t)(h * Ly->qd), (size_t)h, (size_t)(2 * I * h),
                            (size_t)(h * I)};
     auto al = [](size_t s) { return (s + 63) / 64 * 64; };
-    size_t tot = al((size_t)h) + al((size_t)(V * h));
+    size_t tot = al((size_t)h) + al((size_t)(V * h)) + (Ly->embed ? al((size_t)(V * h)) : 0);
     for (int l = 0; l < Ly->NL; ++l)
         for (size_t s : lsz) tot += al(s);
     Ly->gsize = tot;
@@ -292,6 +298,8 @@ static void build_layer(spt_layer* Ly) {
     Ly->dg3 = gp;
     gp += al((size_t)h);
     Ly->dwlm = gp;
+    gp += al((size_t)(V * h));
+    if (Ly->embed) Ly->demb = gp;
     // per-rank activations
     const int64_t nl = Ly->n_loc, N = Ly->N, P = Ly->P;
     Ly->rb.resize(Ly->L);
@@ -312,6 +320,7 @@ static void build_layer(spt_layer* Ly) {
         r.lse = Ly->af32(Ly->hq_loc * N);
         r.labels = (int64_t*)L_.alloc(nl * 8, kWorkspace);
         r.pos = (int64_t*)L_.alloc(nl * 8, kWorkspace);
+        r.ids = Ly->embed ? (int64_t*)L_.alloc(nl * 8, kWorkspace) : nullptr;
         r.dz = Ly->abf(nl * h);
         r.dx1 = Ly->abf(nl * h);
         r.dO = Ly->abf(nl * Ly->qd);
@@ -358,6 +367,7 @@ static void build_layer(spt_layer* Ly) {
     Ly->ws_mlp = L_.alloc(mlp_workspace(Ly->mlp_bwd_tile_max, I), kWorkspace);
     Ly->ws_rms = L_.alloc(rmsnorm_bwd_workspace(nl, h), kWorkspace);
     Ly->ws_attn = L_.alloc(attn_bwd_workspace(N, Ly->hq_loc, Ly->hkv_loc, c.head_dim), kWorkspace);
+    if (Ly->embed) Ly->ws_emb = L_.alloc(embed_bwd_workspace(nl, V), kWorkspace);
     // reshard tables
     auto up = [&](const std::vector<int32_t>& v) {
         int32_t* d = (int32_t*)L_.alloc(v.size() * 4, kWorkspace);
@@ -410,6 +420,16 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
 
     // ---- inputs, label pre-pass, global count
     SPT_CUDA(cudaMemsetAsync(Ly->sc, 0, sizeof(Scalars), st));
+    // x rows: bf16 hidden rows, or (embedding on) int64 input_ids gathered through the table
+    const size_t xrow = Ly->embed ? 8 : (size_t)h * 2;
+    auto load_x = [&](RankBufs& b, const uint8_t* src, cudaMemcpyKind kd) {
+        if (!Ly->embed) {
+            SPT_CUDA(cudaMemcpyAsync(b.x, src, nl * h * 2, kd, st));
+            return;
+        }
+        SPT_CUDA(cudaMemcpyAsync(b.ids, src, nl * 8, kd, st));
+        pf.run(P_OTHER, 0, 2.0 * nl * h * 2, st, [&] { embed_fwd(b.ids, nl, V, h, Ly->emb, b.x, &Ly->sc->err_embed, st); });
+    };
     if (on_host) {
         // H2D on the input stream into a staging slot (overlaps the previous step's compute), then one fast
         // D2D into the working buffers once the copy landed
@@ -427,7 +447,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         const int k = Ly->in_slot;
         Ly->in_slot ^= 1;
         SPT_CUDA(cudaStreamWaitEvent(Ly->in_stream, Ly->ev_in_free[k], 0));
-        SPT_CUDA(cudaMemcpyAsync(Ly->in_x[k], x, (size_t)L * nl * h * 2, cudaMemcpyHostToDevice, Ly->in_stream));
+        SPT_CUDA(cudaMemcpyAsync(Ly->in_x[k], x, (size_t)L * nl * xrow, cudaMemcpyHostToDevice, Ly->in_stream));
         SPT_CUDA(cudaMemcpyAsync(Ly->in_lab[k], labels, (size_t)L * nl * 8, cudaMemcpyHostToDevice, Ly->in_stream));
         if (c.packed)
             SPT_CUDA(cudaMemcpyAsync(Ly->in_pos[k], pos, (size_t)L * nl * 8, cudaMemcpyHostToDevice, Ly->in_stream));
@@ -438,7 +458,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         pos = c.packed ? Ly->in_pos[k] : pos;
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
-            SPT_CUDA(cudaMemcpyAsync(b.x, (const bf16*)x + r * nl * h, nl * h * 2, cudaMemcpyDeviceToDevice, st));
+            load_x(b, (const uint8_t*)x + r * nl * xrow, cudaMemcpyDeviceToDevice);
             SPT_CUDA(cudaMemcpyAsync(b.labels, labels + r * nl, nl * 8, cudaMemcpyDeviceToDevice, st));
             if (c.packed) SPT_CUDA(cudaMemcpyAsync(b.pos, pos + r * nl, nl * 8, cudaMemcpyDeviceToDevice, st));
         }
@@ -447,7 +467,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     } else {
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
-            SPT_CUDA(cudaMemcpyAsync(b.x, (const bf16*)x + r * nl * h, nl * h * 2, kind, st));
+            load_x(b, (const uint8_t*)x + r * nl * xrow, kind);
             SPT_CUDA(cudaMemcpyAsync(b.labels, labels + r * nl, nl * 8, kind, st));
             if (c.packed) SPT_CUDA(cudaMemcpyAsync(b.pos, pos + r * nl, nl * 8, kind, st));
             label_stats(b.labels, nl, V, &Ly->sc->count, &Ly->sc->err_label, st);
@@ -669,6 +689,14 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         }
         layer_bwd(Ly->lw[l]);
     }
+    if (Ly->embed) {  // d loss / d table: per-id sums of the stack's input gradient, ascending token order
+        for (int r = 0; r < L; ++r) {
+            auto& b = Ly->rb[r];
+            pf.run(P_OTHER, 0, 2.0 * nl * h * 2, st, [&] {
+                embed_bwd(b.ids, nl, V, h, b.dx, Ly->demb, r > 0 || gbase, &Ly->sc->err_embed, Ly->ws_emb, st);
+            });
+        }
+    }
     // ---- SP-group reductions
     if (micro) {  // window totals only; the grad all-reduce waits for the end of the window
         cm->all_reduce("all_reduce_loss_sum", &Ly->sc->loss_sum, 1, ncclFloat64, st);
@@ -713,6 +741,7 @@ static void apply_update(spt_layer* Ly, cudaStream_t st) {
             }
             sgd_update(Ly->wlm, Ly->dwlm, V * h, c.lr, st);
             sgd_update(Ly->g3, Ly->dg3, h, c.lr, st);
+            if (Ly->embed) sgd_update(Ly->emb, Ly->demb, V * h, c.lr, st);
         });
     }
 }
@@ -723,6 +752,7 @@ static void read_scalars(spt_layer* Ly, cudaStream_t st, float* loss, int64_t* c
     Ly->comm->check_async();
     SPT_CHECK(Ly->sc_host->err_label == 0, SPT_ERR_VALIDATION, "label out of range [0, vocab) and != -100");
     SPT_CHECK(Ly->sc_host->err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
+    SPT_CHECK(Ly->sc_host->err_embed == 0, SPT_ERR_VALIDATION, "input id out of range [0, vocab)");
     if (loss) *loss = Ly->sc_host->loss;
     if (count) *count = Ly->sc_host->count;
 }
@@ -736,11 +766,12 @@ static int split_name(spt_layer* Ly, const std::string& full, std::string* bare)
         const int l = std::atoi(full.substr(7, dot - 7).c_str());
         SPT_CHECK(l >= 0 && l < Ly->NL, SPT_ERR_VALIDATION, "layer index out of range in '" + full + "'");
         *bare = full.substr(dot + 1);
-        SPT_CHECK(*bare != "g3" && *bare != "wlm", SPT_ERR_VALIDATION, "'" + *bare + "' is not a per-layer parameter");
+        SPT_CHECK(*bare != "g3" && *bare != "wlm" && *bare != "emb", SPT_ERR_VALIDATION,
+                  "'" + *bare + "' is not a per-layer parameter");
         return l;
     }
     *bare = full;
-    return (full == "g3" || full == "wlm") ? -1 : 0;
+    return (full == "g3" || full == "wlm" || full == "emb") ? -1 : 0;
 }
 
 static bf16* param_ptr(spt_layer* Ly, const std::string& full, int64_t* numel, int* layer = nullptr) {
@@ -750,6 +781,10 @@ static bf16* param_ptr(spt_layer* Ly, const std::string& full, int64_t* numel, i
     if (layer) *layer = l;
     if (n == "g3") return *numel = h, Ly->g3;
     if (n == "wlm") return *numel = Ly->V * h, Ly->wlm;
+    if (n == "emb") {
+        SPT_CHECK(Ly->embed, SPT_ERR_VALIDATION, "'emb' needs a layer created with embed = 1");
+        return *numel = Ly->V * h, Ly->emb;
+    }
     auto& w = Ly->lw[l];
     if (n == "g1") return *numel = h, w.g1;
     if (n == "g2") return *numel = h, w.g2;
@@ -765,6 +800,10 @@ static float* grad_ptr(spt_layer* Ly, const std::string& full) {
     const int l = split_name(Ly, full, &n);
     if (n == "g3") return Ly->dg3;
     if (n == "wlm") return Ly->dwlm;
+    if (n == "emb") {
+        SPT_CHECK(Ly->embed, SPT_ERR_VALIDATION, "'emb' needs a layer created with embed = 1");
+        return Ly->demb;
+    }
     auto& w = Ly->lw[l];
     if (n == "g1") return w.dg1;
     if (n == "g2") return w.dg2;
@@ -880,6 +919,7 @@ spt_status spt_layer_loss_slot(spt_layer* Ly, int32_t slot, float* loss_out, int
         const Scalars& v = Ly->loss_host[slot];
         SPT_CHECK(v.err_label == 0, SPT_ERR_VALIDATION, "label out of range [0, vocab) and != -100");
         SPT_CHECK(v.err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
+        SPT_CHECK(v.err_embed == 0, SPT_ERR_VALIDATION, "input id out of range [0, vocab)");
         if (loss_out) *loss_out = v.loss;
         if (count_out) *count_out = v.count;
     });

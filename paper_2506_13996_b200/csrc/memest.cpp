@@ -69,7 +69,7 @@ static double engine_device_bytes(const spt_memest_engine& e, double s) {
     const double nl = s / std::max(1, e.sp);
     const double qkv = (double)(e.q_heads + 2 * e.kv_heads) * e.head_dim, qd = (double)e.q_heads * e.head_dim;
     const double p_layer = e.hidden * qkv + e.hidden * qd + 3.0 * e.hidden * e.intermediate + 2.0 * e.hidden;
-    const double p_fixed = e.n_layers * p_layer + e.vocab * e.hidden + e.hidden;
+    const double p_fixed = e.n_layers * p_layer + (e.embed ? 2.0 : 1.0) * e.vocab * e.hidden + e.hidden;
     const double weights = 2.0 * p_fixed, grads = 4.0 * p_fixed;
     const double tile = std::min<double>(nl, std::max(128.0, std::floor(4.0 * GiB / (e.vocab * 4.0) / 128.0) * 128.0));
     const double logits_ws = tile * e.vocab * (4.0 + 2.0);

@@ -177,3 +177,61 @@ def test_rope_op_vs_oracle_and_inverse():
     S.check(L_.spt_rope(xd.data_ptr(), n, heads, n_rot, d, pd.data_ptr(), 0, 10000.0, 1, None))
     T.cuda.synchronize()
     assert rel_err(to_np(xd), x) < 1e-2  # inverse undoes the rotation (up to bf16 rounding)
+
+
+def _run_embed(L, P, N, offload=False, packed=False, seed=11, bad_id=False):
+    cfg, shape = CFG, SHAPE
+    layers, g3, wlm = _params(cfg, L, seed)
+    _, lab, pos = O.synth_batch(cfg, N, seed, packed=packed)
+    rng = np.random.default_rng(seed)
+    ids = rng.integers(0, 64, N).astype(np.int64)  # few distinct ids: long per-id runs in the backward
+    if bad_id:
+        ids[N // 2] = cfg.vocab
+    emb = O.round_bf16(rng.standard_normal((cfg.vocab, cfg.hidden), dtype=np.float32))
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(shape, N, grp, packed=packed, n_layers=L, ckpt_offload=offload, embed=True)
+    try:
+        for i, lp in enumerate(layers):
+            for k in O.LAYER_NAMES:
+                eng.set_param(f"layers.{i}.{k}", O.f32_to_bf16_bits(lp[k]))
+        eng.set_param("g3", O.f32_to_bf16_bits(g3))
+        eng.set_param("wlm", O.f32_to_bf16_bits(wlm))
+        eng.set_param("emb", O.f32_to_bf16_bits(emb))
+        loss, cnt = eng.step(ids, lab, pos if packed else None)
+        names = [f"layers.{i}.{k}" for i in range(L) for k in O.LAYER_NAMES] + ["g3", "wlm", "emb"]
+        grads = {k: eng.grad(k) for k in names}
+        dx_bits = eng.dx_bits(N)
+    finally:
+        eng.close()
+        grp.close()
+    return dict(loss=loss, count=cnt, grads=grads, dx_bits=dx_bits, layers=layers, g3=g3, wlm=wlm, ids=ids,
+                emb=emb, lab=lab, pos=pos)
+
+
+@pytest.mark.parametrize("L,P,offload,packed", [(1, 1, False, False), (2, 2, True, False), (2, 4, False, True)])
+def test_embedding_stack_matches_oracle(L, P, offload, packed):
+    """Token embedding in front of the stack: the step takes
+    input_ids, and loss, every weight grad, d x and grad "emb" match the oracle's model_step(emb=...)."""
+    r = _run_embed(L, P, 1024, offload=offload, packed=packed)
+    ref = O.model_step(r["layers"], r["g3"], r["wlm"], CFG, r["ids"], r["lab"], r["pos"] if packed else None, P=P,
+                       emb=r["emb"])
+    assert r["count"] == ref.count
+    assert abs(r["loss"] - ref.loss) / abs(ref.loss) <= LOSS_TOL, (r["loss"], ref.loss)
+    for k, g in r["grads"].items():
+        e = rel_err(g, ref.grads[k])
+        assert e <= GRAD_TOL, (k, e)
+    assert rel_err(O.bf16_bits_to_f32(r["dx_bits"]), ref.dx) <= GRAD_TOL
+    # the embedding grad is exactly the per-id sums of the engine's own d x (bf16) rows, rank by rank (the
+    # loopback ranks accumulate into one grad buffer in rank order)
+    dx = O.bf16_bits_to_f32(r["dx_bits"])
+    n_loc = len(r["ids"]) // P
+    demb = None
+    for k in range(P):
+        sl = slice(k * n_loc, (k + 1) * n_loc)
+        demb = O.embed_bwd(r["ids"][sl], dx[sl], CFG.vocab, demb)
+    assert np.array_equal(r["grads"]["emb"], demb)
+
+
+def test_embedding_rejects_out_of_range_ids():
+    with pytest.raises(S.SptError):
+        _run_embed(1, 1, 512, bad_id=True)
