@@ -132,6 +132,13 @@ struct DeviceLedger {
     }
 };
 
+// RoPE fused into the K1 pack / K2 unpack when P > 1 (row f4); SPT_ROPE_FUSED=0 or
+// spt_tuning_set("rope_fused", 0) keeps the separate in-place rotation pass
+int g_rope_fused = [] {
+    const char* e = getenv("SPT_ROPE_FUSED");
+    return e ? atoi(e) : 1;
+}();
+
 // TiledMLP backward tile grouping (1 = the forward's tiles, 2 = pairs of consecutive tiles per recompute /
 // weight-gradient pass); SPT_MLP_BWD_GROUP or spt_tuning_set("mlp_bwd_group", v)
 int g_mlp_bwd_group = [] {
@@ -515,12 +522,20 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             e.C = b.qkv;
             e.ldc = qo;
             gemm({b.xn1, h, false}, {w.wqkv, h, false}, nl, qo, h, EPI_BF16, e, st);
-            if (rope_on)  // row f4: rotate q and k heads in place before the reshard / attention
+            const int64_t rope_off = (int64_t)cm->global_rank(r) * nl;
+            bool rope_done = false;
+            if (rope_on && P > 1 && g_rope_fused)  // row f4: RoPE fused into the K1 pack
+                pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
+                    rope_done = reshard_pack_rope(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc,
+                                                  Ly->map_qkv, b.send_qkv, c.q_heads + c.kv_heads,
+                                                  c.packed ? b.pos : nullptr, rope_off, c.rope_theta, st);
+                });
+            if (rope_on && !rope_done)  // rotate q and k heads in place before the reshard / attention
                 pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
                     rope_apply(b.qkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
-                               c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, false, st);
+                               c.packed ? b.pos : nullptr, rope_off, c.rope_theta, false, st);
                 });
-            if (P > 1)
+            if (P > 1 && !rope_done)
                 pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
                     reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv,
                                  st);
@@ -558,6 +573,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     };
     // ---- one decoder layer backward: dy = b.dx (d of the layer output) -> b.dx (d of the layer input)
     auto layer_bwd = [&](const spt_layer::LayerW& w) {
+        std::vector<char> dqkv_rotated(L, 0);  // inverse RoPE already applied by the fused K2 unpack
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
             const bool acc = r > 0 || gbase;  // loopback ranks share the grad buffer: rank-ascending
@@ -597,6 +613,14 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             for (int r = 0; r < L; ++r) {
                 auto& b = Ly->rb[r];
                 pf.run(P_RESHARD, 0, 2.0 * nl * qo * 2, st, [&] {
+                    if (rope_on && g_rope_fused &&  // row f4: inverse RoPE fused into the K2 unpack
+                        reshard_unpack_rope(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, c.q_heads + 2 * c.kv_heads,
+                                            Ly->gather_qkv, Ly->max_src_qkv, b.dqkv, c.q_heads + c.kv_heads,
+                                            c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl,
+                                            c.rope_theta, st)) {
+                        dqkv_rotated[r] = 1;
+                        return;
+                    }
                     reshard_unpack(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, P, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
                                    Ly->max_src_qkv, b.dqkv, st);
                 });
@@ -606,7 +630,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             auto& b = Ly->rb[r];
             const bool acc = r > 0 || gbase;
             bf16* dxn1 = b.dz;
-            if (rope_on)  // d(q, k) through the rotation's transpose, before the projection's backward
+            if (rope_on && !dqkv_rotated[r])  // d(q, k) through the rotation's transpose, before the projection's backward
                 pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
                     rope_apply(b.dqkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
                                c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, true, st);

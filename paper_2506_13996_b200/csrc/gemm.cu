@@ -263,6 +263,7 @@ namespace spt {
 extern int g_attn_dq_tmem;   // attention_tc.cu
 extern int g_attn_fwd_tmem;  // attention_tc.cu
 extern int g_mlp_bwd_group;  // engine.cu
+extern int g_rope_fused;     // engine.cu
 extern int g_attn_dkdv_pair;  // attention_tc.cu
 extern int g_attn_dkdv_kt;    // attention_tc.cu
 extern int g_attn_kv_group;   // attention_tc.cu
@@ -290,6 +291,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         }
         if (n == "attn_dkdv_pair") {
             spt::g_attn_dkdv_pair = value;
+            return;
+        }
+        if (n == "rope_fused") {
+            spt::g_rope_fused = value;
             return;
         }
         if (n == "mlp_bwd_group") {

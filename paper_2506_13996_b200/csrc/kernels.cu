@@ -203,6 +203,142 @@ __global__ void reshard_unpack_kernel(const uint4* __restrict__ recv, int64_t s_
 // division per row instead of several per 16-byte element, and loads batched ahead of the stores so each
 // lane keeps several 16-byte requests in flight (the generic kernels above were issue-bound at ~60% of
 // the HBM copy bandwidth).
+// RoPE rotation of 8 consecutive pairs (j = 8 gi .. 8 gi + 7 of the first half against the second half) at
+// position p, Llama / HF rotate_half convention with HF's fp32 angles; explicit roundings so the standalone
+// kernel and the pack/unpack-fused kernels produce identical bits.
+__device__ __forceinline__ void rope_rotate8(const float* a, const float* b, float p, int gi, int d, float theta,
+                                             float sgn, float* o1, float* o2) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int j = gi * 8 + k;
+        const float inv_freq = 1.f / powf(theta, (float)(2 * j) / (float)d);
+        float sn, cs;
+        sincosf(p * inv_freq, &sn, &cs);
+        sn *= sgn;
+        o1[k] = __fsub_rn(__fmul_rn(a[k], cs), __fmul_rn(b[k], sn));
+        o2[k] = __fadd_rn(__fmul_rn(b[k], cs), __fmul_rn(a[k], sn));
+    }
+}
+
+__device__ __forceinline__ void u4_to_f8(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 v = unpack_bf16x2(w[k]);
+        f[2 * k] = v.x;
+        f[2 * k + 1] = v.y;
+    }
+}
+
+__device__ __forceinline__ uint4 f8_to_u4(const float* f) {
+    return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                      pack_bf16x2(f[6], f[7]));
+}
+
+// K1 pack with RoPE fused: the q and k heads (source head < n_rot) are rotated on the
+// way from the token rows to the per-peer send buffer, replacing the separate in-place rope pass.  A lane
+// handles one (head, chunk pair): chunk c of the first half of the head row and chunk c of the second half.
+template <int VPD>
+__global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __restrict__ src, int64_t s_loc,
+                                                                int heads_in, int P, int heads_out,
+                                                                const int32_t* __restrict__ head_map,
+                                                                uint4* __restrict__ dst, int n_rot,
+                                                                const int64_t* __restrict__ pos, int64_t pos_offset,
+                                                                float theta) {
+    extern __shared__ int32_t smap[];  // [P][heads_out]
+    for (int i = threadIdx.x; i < P * heads_out; i += blockDim.x) smap[i] = head_map[i];
+    __syncthreads();
+    constexpr int HP = VPD / 2;  // chunk pairs per head
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows = (int64_t)P * s_loc;
+    const int row_pairs = heads_out * HP;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < nrows; r += nw) {
+        const int j = (int)(r / s_loc);
+        const int64_t t = r - (int64_t)j * s_loc;
+        const float p = (float)(pos ? pos[t] : pos_offset + t);
+        const uint4* srow = src + t * heads_in * VPD;
+        uint4* drow = dst + r * heads_out * VPD;
+        const int32_t* m = smap + j * heads_out;
+        for (int e = lane; e < row_pairs; e += 32) {
+            const int hs = e / HP, c = e - hs * HP;
+            const int sh = m[hs];
+            uint4 a = __ldg(srow + sh * VPD + c), b = __ldg(srow + sh * VPD + c + HP);
+            if (sh < n_rot) {
+                float fa[8], fb[8], o1[8], o2[8];
+                u4_to_f8(a, fa);
+                u4_to_f8(b, fb);
+                rope_rotate8(fa, fb, p, c, VPD * 8, theta, 1.f, o1, o2);
+                a = f8_to_u4(o1);
+                b = f8_to_u4(o2);
+            }
+            drow[hs * VPD + c] = a;
+            drow[hs * VPD + c + HP] = b;
+        }
+    }
+}
+
+// K2 unpack of d(q, k, v) with the inverse RoPE fused: replicas summed in fp32 (rank order) and rounded to
+// bf16 exactly as the plain unpack writes them, then the q / k heads (< n_rot) rotated back.
+template <int VPD>
+__global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const uint4* __restrict__ recv, int64_t s_loc,
+                                                                  int heads_in, int heads_out,
+                                                                  const int32_t* __restrict__ gather, int max_src,
+                                                                  uint4* __restrict__ dst, int n_rot,
+                                                                  const int64_t* __restrict__ pos, int64_t pos_offset,
+                                                                  float theta) {
+    extern __shared__ int32_t sg[];  // [heads_out][max_src]
+    for (int i = threadIdx.x; i < heads_out * max_src; i += blockDim.x) sg[i] = gather[i];
+    __syncthreads();
+    constexpr int HP = VPD / 2;
+    const int lane = threadIdx.x & 31;
+    const int row_pairs = heads_out * HP;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t rank_stride = s_loc * heads_in * VPD;
+    for (int64_t t = w0; t < s_loc; t += nw) {
+        const uint4* trow = recv + t * heads_in * VPD;
+        uint4* drow = dst + t * heads_out * VPD;
+        const float p = (float)(pos ? pos[t] : pos_offset + t);
+        for (int e = lane; e < row_pairs; e += 32) {
+            const int h = e / HP, c = e - h * HP;
+            const int32_t* gl = sg + h * max_src;
+            auto at = [&](int g, int v) {
+                return trow + (int64_t)(g / heads_in) * rank_stride + (g % heads_in) * VPD + v;
+            };
+            uint4 a = __ldg(at(gl[0], c)), b = __ldg(at(gl[0], c + HP));
+            if (max_src > 1 && gl[1] >= 0) {  // replica sum in fp32, rank order (as reshard_unpack_rows_kernel)
+                float fa[8], fb[8];
+                u4_to_f8(a, fa);
+                u4_to_f8(b, fb);
+                for (int sidx = 1; sidx < max_src && gl[sidx] >= 0; ++sidx) {
+                    float ga[8], gb[8];
+                    u4_to_f8(__ldg(at(gl[sidx], c)), ga);
+                    u4_to_f8(__ldg(at(gl[sidx], c + HP)), gb);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        fa[k] += ga[k];
+                        fb[k] += gb[k];
+                    }
+                }
+                a = f8_to_u4(fa);
+                b = f8_to_u4(fb);
+            }
+            if (h < n_rot) {
+                float fa[8], fb[8], o1[8], o2[8];
+                u4_to_f8(a, fa);
+                u4_to_f8(b, fb);
+                rope_rotate8(fa, fb, p, c, VPD * 8, theta, -1.f, o1, o2);
+                a = f8_to_u4(o1);
+                b = f8_to_u4(o2);
+            }
+            drow[h * VPD + c] = a;
+            drow[h * VPD + c + HP] = b;
+        }
+    }
+}
+
 template <int VPD>
 __global__ void __launch_bounds__(256) reshard_pack_rows_kernel(const uint4* __restrict__ src, int64_t s_loc,
                                                                 int heads_in, int P, int heads_out,
@@ -345,6 +481,39 @@ void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim,
     SPT_CUDA(cudaGetLastError());
 }
 
+bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                       const int32_t* head_map, void* dst, int n_rot, const int64_t* pos, int64_t pos_offset,
+                       float theta, cudaStream_t st) {
+    const int vpd = head_dim / 8;
+    const size_t smem = (size_t)P * heads_out * 4;
+    if (head_dim % 16 != 0 || !(vpd == 4 || vpd == 8 || vpd == 16) || smem > 48 * 1024) return false;
+    if ((int64_t)P * s_loc * heads_out == 0) return true;
+    const int g = reshard_rows_grid((int64_t)P * s_loc);
+    auto k = vpd == 16 ? reshard_pack_rope_kernel<16> : vpd == 8 ? reshard_pack_rope_kernel<8> : reshard_pack_rope_kernel<4>;
+    k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, (uint4*)dst, n_rot, pos,
+                            pos_offset, theta);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+    return true;
+}
+
+bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head_dim, int heads_out,
+                         const int32_t* gather, int max_src, void* dst, int n_rot, const int64_t* pos,
+                         int64_t pos_offset, float theta, cudaStream_t st) {
+    const int vpd = head_dim / 8;
+    const size_t smem = (size_t)heads_out * max_src * 4;
+    if (head_dim % 16 != 0 || !(vpd == 4 || vpd == 8 || vpd == 16) || smem > 48 * 1024) return false;
+    if (s_loc * heads_out == 0) return true;
+    const int g = reshard_rows_grid(s_loc);
+    auto k = vpd == 16 ? reshard_unpack_rope_kernel<16>
+                       : vpd == 8 ? reshard_unpack_rope_kernel<8> : reshard_unpack_rope_kernel<4>;
+    k<<<g, 256, smem, st>>>((const uint4*)recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst, n_rot, pos,
+                            pos_offset, theta);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+    return true;
+}
+
 // ------------------------------------------------------------------ RoPE
 // In-place rotary embedding of the first n_rot heads of each token row of x [n][heads][d] (bf16), Llama / HF
 // rotate_half convention: (x1, x2) -> (x1 cos - x2 sin, x2 cos + x1 sin) with angle = pos * theta^(-2j/d)
@@ -366,16 +535,7 @@ __global__ void rope_kernel(bf16* __restrict__ x, int64_t n, int heads, int n_ro
         load8(row + gi * 8, a);
         load8(row + half + gi * 8, b);
         float o1[8], o2[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int j = gi * 8 + k;
-            const float inv_freq = 1.f / powf(theta, (float)(2 * j) / (float)d);
-            float s, c;
-            sincosf(p * inv_freq, &s, &c);
-            s *= sgn;
-            o1[k] = a[k] * c - b[k] * s;
-            o2[k] = b[k] * c + a[k] * s;
-        }
+        rope_rotate8(a, b, p, gi, d, theta, sgn, o1, o2);
         store8(row + gi * 8, o1);
         store8(row + half + gi * 8, o2);
     }

@@ -235,3 +235,23 @@ def test_embedding_stack_matches_oracle(L, P, offload, packed):
 def test_embedding_rejects_out_of_range_ids():
     with pytest.raises(S.SptError):
         _run_embed(1, 1, 512, bad_id=True)
+
+
+@pytest.mark.parametrize("P,packed", [(2, False), (4, True)])
+def test_rope_fused_into_reshard_bitwise(P, packed):
+    """RoPE fused into the K1 pack and the inverse rotation into the K2 unpack (row f4; P=4 with 2 kv heads also
+    exercises the KV-replica sum before the rotation) gives bitwise the same step as the separate pass."""
+    L = S.lib()
+    out = []
+    try:
+        for v in (0, 1):
+            S.check(L.spt_tuning_set(b"rope_fused", v))
+            out.append(_run(2, P, 1024, packed=packed, rope=10000.0))
+    finally:
+        S.check(L.spt_tuning_set(b"rope_fused", 1))
+    a, b = out
+    assert a["loss"] == b["loss"] and a["count"] == b["count"]
+    assert np.array_equal(a["dx_bits"], b["dx_bits"])
+    for k in a["grads"]:
+        assert np.array_equal(a["grads"][k], b["grads"][k]), k
+    _check(b, 2, P, packed, rope=10000.0)
