@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
             tc_fence_after();
             const int64_t k0 = (int64_t)j * BKB;
-            const bool need_mask = seg != nullptr || (k0 + BKB - 1 > q0 + t * BQ);  // warp-uniform
+            // warp-uniform: causal diagonal, or (packed) some row of this warp starts its sample inside the block
+            const bool need_mask = (k0 + BKB - 1 > q0 + t * BQ) || (seg != nullptr && __any_sync(0xffffffffu, start > k0));
             uint32_t v[2][32];
             tmem_ld32(s_tm, v[0]);
             tmem_ld32(s_tm + 32, v[1]);
@@ -632,7 +633,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
             tc_fence_after();
             const int64_t k0 = (int64_t)j * BKB;
-            const bool need_mask = seg != nullptr || (k0 + BKB - 1 > q0 + t * BQ);  // warp-uniform
+            // warp-uniform: causal diagonal, or (packed) some row of this warp starts its sample inside the block
+            const bool need_mask = (k0 + BKB - 1 > q0 + t * BQ) || (seg != nullptr && __any_sync(0xffffffffu, start > k0));
             uint32_t v[2][32];
             tmem_ld32(s_tm, v[0]);
             tmem_ld32(s_tm + 32, v[1]);
@@ -972,7 +974,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     w[k] = pack_bf16x2(d0, d1);
                 }
             };
-            if (seg != nullptr || k0 + 15 > q0i) body(std::true_type{});
+            if (k0 + 15 > q0i || (seg != nullptr && __any_sync(0xffffffffu, start > k0))) body(std::true_type{});
             else body(std::false_type{});
             tmem_st8(tmem + lo + b * 128 + grp * 16, w);  // over this warp's consumed S columns
             tmem_st_wait();
@@ -1182,7 +1184,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     w[k] = pack_bf16x2(d0, d1);
                 }
             };
-            if (seg != nullptr || k0 + 15 > q0i) body(std::true_type{});
+            if (k0 + 15 > q0i || (seg != nullptr && __any_sync(0xffffffffu, start > k0))) body(std::true_type{});
             else body(std::false_type{});
             tmem_st8(tmem + lo + b * 128 + grp * 16, w);  // over this warp's consumed S columns
             tmem_st_wait();
@@ -1502,7 +1504,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     }
                 }
             };
-            if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
+            // packed: the 16 queries' sample starts are nondecreasing, so seg[qq + 15] bounds them all; the
+            // warp's smallest key is key32 - lane
+            if (qq < key32 - r + 127 || (seg != nullptr && seg[qq + 15] > key32 - lane)) body(std::true_type{});
             else body(std::false_type{});
             tmem_st8(pbuf + grp * 16, pw);
             tmem_st8(pbuf + grp * 16 + 8, sw);
@@ -1760,7 +1764,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     }
                 }
             };
-            if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
+            // packed: the 16 queries' sample starts are nondecreasing, so seg[qq + 15] bounds them all; the
+            // warp's smallest key is key32 - lane
+            if (qq < key32 - r + 127 || (seg != nullptr && seg[qq + 15] > key32 - lane)) body(std::true_type{});
             else body(std::false_type{});
             tmem_st8(tmem + lo + b * 128 + grp * 16, pw);
             tmem_st8(tmem + lo + b * 128 + grp * 16 + 8, sw);
@@ -2142,7 +2148,9 @@ __global__ void __launch_bounds__(dkvq::THREADS, 1)
                     }
                 }
             };
-            if (seg != nullptr || qq < key32 - r + 127) body(std::true_type{});
+            // packed: the 16 queries' sample starts are nondecreasing, so seg[qq + 15] bounds them all; the
+            // warp's smallest key is key32 - lane
+            if (qq < key32 - r + 127 || (seg != nullptr && seg[qq + 15] > key32 - lane)) body(std::true_type{});
             else body(std::false_type{});
             tmem_st8(tmem + lo + b * 128 + grp4 * 16, pw);
             tmem_st8(tmem + lo + b * 128 + grp4 * 16 + 8, sw);
