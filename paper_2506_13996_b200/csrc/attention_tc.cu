@@ -456,6 +456,278 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
+// Forward with 128-key blocks (fwd_tc128_kernel): same CTA / TMEM shape as fwd_tc_kernel (two 128-row query
+// tiles, 256 TMEM columns each), but each tile's 128 S columns hold ONE 128-key score block instead of two
+// double-buffered 64-key blocks.  The score MMA is then M=128 N=128 — full tensor rate with both operands in
+// smem (64 of 64 cycles), where the N=64 form takes 48 of 32 (tools/micro/mma_rate.cu) — and per-block
+// barrier / rescale overheads halve.  The price is a single S buffer per tile: S_t(j+1) is issued right after
+// PV_t(j) (which consumes P_t(j) from the same columns), so the two tiles ping-pong: one tile's softmax runs
+// under the other tile's MMAs.  MMA order per block j: PV0(j) S0(j+1) PV1(j) S1(j+1).
+namespace fw2 {
+constexpr int BKB = 128;
+constexpr int Q_BYTES = BQ * D * 2;    // 32 KiB per tile
+constexpr int KV_BYTES = BKB * D * 2;  // 32 KiB per K or V block (two 16 KiB regions)
+constexpr int NSL = 4;
+constexpr int OFF_Q = 0, OFF_KV = 2 * Q_BYTES;
+constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
+constexpr int SMEM = OFF_BAR + 512 + 1024;
+}  // namespace fw2
+
+// POLY > 0: every POLY-th exponential pair goes through ex2_poly on the FMA pipe (MUFU relief: with 128-key
+// blocks the exponentials of both tiles need the whole MUFU throughput at full tensor rate).
+template <int POLY>
+__global__ void __launch_bounds__(THREADS, 1)
+    fwd_tc128_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
+                     int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
+                     float* __restrict__ lse, int kvg) {
+    using namespace fw2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* q_full = bar;
+    uint64_t* kv_full = bar + 1;
+    uint64_t* kv_empty = kv_full + NSL;
+    uint64_t* s_full = kv_empty + NSL;  // [t]
+    uint64_t* p_full = s_full + 2;      // [t]
+    uint64_t* pv_done = p_full + 2;     // [t]
+    uint64_t* o_done = pv_done + 2;     // [t]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+    const int warp = warp_id(), lane = lane_id();
+    const int npairs = (int)((s + 2 * BQ - 1) / (2 * BQ));
+    int h, yb;
+    grid_head_row(kvg, hq, hkv, h, yb);
+    const int pair = npairs - 1 - yb;
+    const int kvh = h / (hq / hkv);
+    const int64_t q0 = (int64_t)pair * 2 * BQ;
+    const bool has1 = q0 + BQ < s;
+    const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = (seg && has1) ? (int)(seg[q0 + BQ] / BKB) : 0;
+    const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = has1 ? (int)((q0 + 2 * BQ - 1) / BKB) : -1;
+    const int jlo = jb0, jhi = has1 ? je1 : je0;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < NSL; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 128);
+            mbar_init(&pv_done[t], 1);
+            mbar_init(&o_done[t], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 8) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t sbase = smem_u32(smem);
+
+    if (warp == 9) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tq);
+            tma_prefetch_desc(&tkv);
+            mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
+            for (int t = 0; t < 2; ++t)
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tq, q_full, smem + OFF_Q + t * Q_BYTES + r * 16384, h * D + 64 * r,
+                                (int)(q0 + t * BQ));
+            const int nload = 2 * (jhi - jlo + 1);
+            for (int li = 0; li < nload; ++li) {
+                const int j = jlo + li / 2, w = li & 1;
+                const int slot = li % NSL;
+                mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
+                const int col = (hq + (w ? hkv : 0) + kvh) * D;
+                for (int r = 0; r < 2; ++r)
+                    tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 16384, col + 64 * r,
+                                j * BKB);
+            }
+        }
+    } else if (warp == 8) {
+        {
+            constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKB, false, false);
+            constexpr uint32_t idesc_o = make_idesc_bf16(BQ, D, false, true);
+            mbar_wait(q_full, 0);
+            const int jb[2] = {jb0, jb1}, je[2] = {je0, je1};
+            int pv_count[2] = {0, 0};
+            auto uses = [&](int t, int j) { return j >= jb[t] && j <= je[t]; };
+            auto slot = [&](int j, int w) { return (2 * (j - jlo) + w) % NSL; };
+            auto phase = [&](int j, int w) { return (uint32_t)(((2 * (j - jlo) + w) / NSL) & 1); };
+            auto issue_s = [&](int t, int j) {
+                mbar_wait(&kv_full[slot(j, 0)], phase(j, 0));
+                tc_fence_after();
+                const uint32_t qa = sbase + OFF_Q + t * Q_BYTES;
+                const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    mma_bf16_ss_w(tmem + t * 256, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 16384), idesc_s, kk > 0);
+                mma_commit_w(&s_full[t]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                mbar_wait(&p_full[t], (j - jb[t]) & 1);
+                mbar_wait(&kv_full[slot(j, 1)], phase(j, 1));
+                tc_fence_after();
+                const uint32_t vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BKB / 16; ++kk)
+                    mma_bf16_ts_w(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, mndesc_r(vb, kk, 16384), idesc_o,
+                                  (pv_count[t] > 0 || kk > 0));
+                mma_commit_w(&pv_done[t]);
+                ++pv_count[t];
+            };
+            if (uses(0, jlo)) issue_s(0, jlo);
+            if (uses(1, jlo)) issue_s(1, jlo);
+            mma_commit_w(&kv_empty[slot(jlo, 0)]);
+            for (int j = jlo; j <= jhi; ++j) {
+                const bool more = j + 1 <= jhi;
+                if (uses(0, j)) issue_pv(0, j);
+                if (more && uses(0, j + 1)) issue_s(0, j + 1);
+                if (uses(1, j)) issue_pv(1, j);
+                mma_commit_w(&kv_empty[slot(j, 1)]);  // V_j consumed
+                if (more) {
+                    if (uses(1, j + 1)) issue_s(1, j + 1);
+                    mma_commit_w(&kv_empty[slot(j + 1, 0)]);  // K_{j+1} consumed by both tiles
+                }
+            }
+            mma_commit_w(&o_done[0]);
+            mma_commit_w(&o_done[1]);
+        }
+    } else {
+        // ---------------- softmax warpgroups (thread = query row), 128 columns per block in 4 chunks of 32
+        const int t = warp >> 2;
+        const int sub = warp & 3;
+        const int r = sub * 32 + lane;
+        const int64_t q = q0 + t * BQ + r;
+        const bool row_ok = q < s;
+        const int start = (seg && row_ok) ? seg[q] : 0;
+        const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+        const uint32_t t_tm = tmem + lane_off + t * 256;
+        const uint32_t o_tm = t_tm + 128;
+        const int jb_t = t ? jb1 : jb0, je_t = t ? je1 : je0;
+        float m_use = -INFINITY, l = 0.f;
+        for (int j = jb_t; j <= je_t; ++j) {
+            const int n = j - jb_t;
+            mbar_wait(&s_full[t], n & 1);
+            tc_fence_after();
+            const int64_t k0 = (int64_t)j * BKB;
+            const bool need_mask = (k0 + BKB - 1 > q0 + t * BQ) || (seg != nullptr && __any_sync(0xffffffffu, start > k0));
+            uint32_t v[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(t_tm + c * 32, v[c]);
+            tmem_ld_wait();
+            float mp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mp[u] = -INFINITY;
+            if (need_mask) {
+                const int hi = (int)(q - k0), lo_ = start - (int)k0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int col = c * 32 + i;
+                        if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
+                        mp[col & 7] = fmaxf(mp[col & 7], __uint_as_float(v[c][i]));
+                    }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2)
+                        mp[(c * 32 + i) >> 1 & 7] =
+                            fmaxf(mp[(c * 32 + i) >> 1 & 7], fmaxf(__uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1])));
+            }
+            const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                     fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+            const float mx = mraw * scale_log2;
+            const bool grow = mx > m_use + RESCALE_THRESHOLD;
+            const bool resc = grow && m_use != -INFINITY && n > 0;
+            const float alpha = resc ? ex2(m_use - mx) : 1.f;
+            if (__any_sync(0xffffffffu, resc)) {  // needs PV_t(j-1) complete
+                mbar_wait(&pv_done[t], (n - 1) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t ov[32];
+                    tmem_ld32(o_tm + c * 32, ov);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                    tmem_st32(o_tm + c * 32, ov);
+                }
+            }
+            l *= alpha;
+            if (grow) m_use = mx;
+            const float nbase = m_use == -INFINITY ? 0.f : -m_use;
+            const uint64_t sc2 = f2pack(scale_log2, scale_log2), nb2 = f2pack(nbase, nbase);
+            uint64_t rs2[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
+            // P for chunk c (32 keys) -> 16 packed columns at [16c, 16c+16): the chunk's S columns [32c, 32c+32)
+            // were already read into registers, and chunk c's P never lands on a chunk not yet read
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pw[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), sc2, nb2);
+                    float x0, x1;
+                    f2unpack(x2, x0, x1);
+                    const bool poly = POLY > 0 && ((c * 16 + k) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY - 1 : 0);
+                    const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
+                    rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
+                    pw[k] = pack_bf16x2(p0, p1);
+                }
+                tmem_st16(t_tm + c * 16, pw);
+            }
+            float rs0, rs1;
+            f2unpack(fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3])), rs0, rs1);
+            l += rs0 + rs1;
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_full[t]);
+        }
+        mbar_wait(&o_done[t], 0);
+        tc_fence_after();
+        if (t == 1 && !has1) goto fwd2_done;
+        {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* orow = o + (q * hq + h) * D;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(o_tm + c * 32, ov);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 w;
+                w.x = pack_bf16x2(__uint_as_float(ov[8 * k + 0]) * inv, __uint_as_float(ov[8 * k + 1]) * inv);
+                w.y = pack_bf16x2(__uint_as_float(ov[8 * k + 2]) * inv, __uint_as_float(ov[8 * k + 3]) * inv);
+                w.z = pack_bf16x2(__uint_as_float(ov[8 * k + 4]) * inv, __uint_as_float(ov[8 * k + 5]) * inv);
+                w.w = pack_bf16x2(__uint_as_float(ov[8 * k + 6]) * inv, __uint_as_float(ov[8 * k + 7]) * inv);
+                dst[k] = w;
+            }
+        }
+        lse[(int64_t)h * s + q] = l > 0.f ? (m_use + __log2f(l)) * LN2 : -INFINITY;
+        }
+    fwd2_done:;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 namespace fwt {  // forward with Q resident in TMEM (fwd_tmem_kernel)
 constexpr int BKB = 64;
 constexpr int KV_BYTES = BKB * D * 2;  // 16 KiB per K or V block (two 8 KiB regions)
@@ -2253,6 +2525,20 @@ static int kv_group(int64_t s, int hkv, int d) {
     return (double)s * hkv * d * 4 > 160e6 ? 1 : hkv;
 }
 
+// SPT_ATTN_FWD_BK128=0|1|4|8 (run time: spt_tuning_set("attn_fwd_bk128", v)): forward with 128-key blocks
+// (4 / 8: every 4th / 8th exponential pair on the FMA pipe, measured slower).  -1 (default): 128-key blocks
+// for large problems, s * hq >= 2^21 (profiles/r1z3_fwd_bk128.txt: -3% at 128K x 32 heads, -4% at the L8
+// rank shape, -5% at the Q8 rank shape; +3..7% at 32K x 32 and 128K x 4, where the 64-key kernel's double
+// buffer overlaps better)
+int g_attn_fwd_bk128 = [] {
+    const char* e = getenv("SPT_ATTN_FWD_BK128");
+    return e ? atoi(e) : -1;
+}();
+static int fwd_bk128(int64_t s, int hq) {
+    if (g_attn_fwd_bk128 >= 0) return g_attn_fwd_bk128;
+    return (double)s * hq >= 2097152.0 ? 1 : 0;
+}
+
 // SPT_ATTN_FWD_TMEM=0|1 (run time: spt_tuning_set("attn_fwd_tmem", v)): forward with Q resident in TMEM
 int g_attn_fwd_tmem = [] {
     const char* e = getenv("SPT_ATTN_FWD_TMEM");
@@ -2268,12 +2554,20 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
     static bool attr = false;
     if (!attr) {
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
+        for (auto k : {fatc::fwd_tc128_kernel<0>, fatc::fwd_tc128_kernel<4>, fatc::fwd_tc128_kernel<8>})
+            SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw2::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::fwt::SMEM));
         attr = true;
     }
     dim3 grid((unsigned)hq, (unsigned)((s + 255) / 256));
-    if (g_attn_fwd_tmem)
+    const int bk128 = fwd_bk128(s, hq);
+    if (bk128) {
+        CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
+        auto k = bk128 == 4 ? fatc::fwd_tc128_kernel<4> : bk128 == 8 ? fatc::fwd_tc128_kernel<8> : fatc::fwd_tc128_kernel<0>;
+        k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
+                                                        kv_group(s, hkv, d));
+    } else if (g_attn_fwd_tmem)
         fatc::fwd_tmem_kernel<<<grid, fatc::THREADS, fatc::fwt::SMEM, st>>>(tkv, (const bf16*)qkv, s, hq, hkv, seg,
                                                                               scale * fatc::LOG2E, (bf16*)o, lse);
     else

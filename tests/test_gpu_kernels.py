@@ -455,3 +455,30 @@ def test_embedding_rejects_bad_ids():
         assert int(err) == 3
     ids = T.tensor([0, 1, 2], dtype=T.int64, device="cuda")
     assert L.spt_embed_fwd(ids.data_ptr(), 3, V, 12, tab.data_ptr(), x.data_ptr(), err.data_ptr(), None) != 0
+
+
+@pytest.mark.parametrize("s,hq,hkv,packed,amp", [(1024, 4, 2, False, 1), (640, 4, 1, True, 1), (2048, 2, 1, False, 2.5),
+                                                 (1536, 2, 2, True, 2.5), (384, 8, 2, False, 1)])
+@pytest.mark.parametrize("mode", [1, 8])
+def test_attention_fwd_128key_blocks(s, hq, hkv, packed, amp, mode):
+    """The 128-key-block forward (default for s * hq >= 2^21; forced here at small sizes, with and without the
+    FMA-pipe exp2 for every 8th pair) against the float64 oracle: O rel-err < 1e-2, lse abs err < 2e-3."""
+    T = torch()
+    L = _lib()
+    d = 128
+    qkv, _, starts = _attn_case(s, hq, hkv, d, packed, s + d + 1, amp)
+    q, k, v = qkv[:, :hq], qkv[:, hq:hq + hkv], qkv[:, hq + hkv:]
+    o_r, lse_r = O.attention_fwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), starts)
+    qkvd = bf16_dev(qkv)
+    o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+    lse = T.empty(hq, s, device="cuda")
+    seg = T.from_numpy(starts.astype(np.int32)).cuda() if starts is not None else None
+    try:
+        S.check(L.spt_tuning_set(b"attn_fwd_bk128", mode))
+        S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, S.ptr(seg), 1.0 / math.sqrt(d), o.data_ptr(),
+                               lse.data_ptr(), None))
+        T.cuda.synchronize()
+    finally:
+        S.check(L.spt_tuning_set(b"attn_fwd_bk128", -1))
+    assert rel_err(to_np(o), o_r) < 1e-2
+    assert np.max(np.abs(to_np(lse) - lse_r)) < 2e-3
