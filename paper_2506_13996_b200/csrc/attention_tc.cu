@@ -488,8 +488,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* kv_full = bar + 1;
     uint64_t* kv_empty = kv_full + NSL;
     uint64_t* s_full = kv_empty + NSL;  // [t]
-    uint64_t* p_full = s_full + 2;      // [t]
-    uint64_t* pv_done = p_full + 2;     // [t]
+    uint64_t* p_full = s_full + 2;      // [t * 2 + half]: P for keys [64 half, 64 half + 64) written
+    uint64_t* pv_done = p_full + 4;     // [t]
     uint64_t* o_done = pv_done + 2;     // [t]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
@@ -513,7 +513,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&p_full[t], 128);
+            mbar_init(&p_full[2 * t], 128);
+            mbar_init(&p_full[2 * t + 1], 128);
             mbar_init(&pv_done[t], 1);
             mbar_init(&o_done[t], 1);
         }
@@ -570,15 +571,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mma_bf16_ss_w(tmem + t * 256, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 16384), idesc_s, kk > 0);
                 mma_commit_w(&s_full[t]);
             };
-            auto issue_pv = [&](int t, int j) {
-                mbar_wait(&p_full[t], (j - jb[t]) & 1);
+            auto issue_pv = [&](int t, int j) {  // in two halves: the first starts while the softmax finishes
                 mbar_wait(&kv_full[slot(j, 1)], phase(j, 1));
-                tc_fence_after();
                 const uint32_t vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < BKB / 16; ++kk)
-                    mma_bf16_ts_w(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, mndesc_r(vb, kk, 16384), idesc_o,
-                                  (pv_count[t] > 0 || kk > 0));
+                for (int half = 0; half < 2; ++half) {
+                    mbar_wait(&p_full[2 * t + half], (j - jb[t]) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kq = 0; kq < BKB / 32; ++kq) {
+                        const int kk = half * (BKB / 32) + kq;
+                        mma_bf16_ts_w(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, mndesc_r(vb, kk, 16384), idesc_o,
+                                      (pv_count[t] > 0 || kk > 0));
+                    }
+                }
                 mma_commit_w(&pv_done[t]);
                 ++pv_count[t];
             };
@@ -685,13 +691,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                     pw[k] = pack_bf16x2(p0, p1);
                 }
                 tmem_st16(t_tm + c * 16, pw);
+                if (c == 1) {  // keys [0, 64) done: the first half of PV can start
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(&p_full[2 * t]);
+                }
             }
             float rs0, rs1;
             f2unpack(fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3])), rs0, rs1);
             l += rs0 + rs1;
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&p_full[t]);
+            mbar_arrive(&p_full[2 * t + 1]);
         }
         mbar_wait(&o_done[t], 0);
         tc_fence_after();
@@ -2526,17 +2537,24 @@ static int kv_group(int64_t s, int hkv, int d) {
 }
 
 // SPT_ATTN_FWD_BK128=0|1|4|8 (run time: spt_tuning_set("attn_fwd_bk128", v)): forward with 128-key blocks
-// (4 / 8: every 4th / 8th exponential pair on the FMA pipe, measured slower).  -1 (default): 128-key blocks
-// for large problems, s * hq >= 2^21 (profiles/r1z3_fwd_bk128.txt: -3% at 128K x 32 heads, -4% at the L8
-// rank shape, -5% at the Q8 rank shape; +3..7% at 32K x 32 and 128K x 4, where the 64-key kernel's double
-// buffer overlaps better)
+// (default 1; 4 / 8: every 4th / 8th exponential pair on the FMA pipe, measured slower; 0: the 64-key
+// double-buffered kernel).  With the P hand-off split in halves it measured -3% at 32K x 32 heads, -3.4% at
+// 128K x 4, -6% at the L8 rank shape (profiles/r1z3_fwd_bk128.txt).  -1: 128-key only for s * hq >= 2^21
+// (the rule before the split hand-off).
 int g_attn_fwd_bk128 = [] {
     const char* e = getenv("SPT_ATTN_FWD_BK128");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 1;
 }();
-static int fwd_bk128(int64_t s, int hq) {
-    if (g_attn_fwd_bk128 >= 0) return g_attn_fwd_bk128;
-    return (double)s * hq >= 2097152.0 ? 1 : 0;
+// Packed sequences keep the 64-key kernel: with short samples most 128-key blocks straddle a sample start
+// (s=128K, mean sample 2048: 6.57 vs 4.56 ms), while long samples gain only a few % (32768: 57.7 vs 61.3 ms).
+// Values: 1 (default) 128-key unless packed, 2 128-key always, 0 64-key, 4 / 8 128-key + FMA-pipe exp2,
+// -1 128-key for s * hq >= 2^21.  Returns 0 (64-key) or the 128-key kernel's POLY selector (1, 4, 8).
+static int fwd_bk128(int64_t s, int hq, const int32_t* seg) {
+    const int v = g_attn_fwd_bk128;
+    if (v == 1) return seg != nullptr ? 0 : 1;
+    if (v == 2) return 1;
+    if (v == -1) return (double)s * hq >= 2097152.0 ? 1 : 0;
+    return v;
 }
 
 // SPT_ATTN_FWD_TMEM=0|1 (run time: spt_tuning_set("attn_fwd_tmem", v)): forward with Q resident in TMEM
@@ -2561,7 +2579,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
         attr = true;
     }
     dim3 grid((unsigned)hq, (unsigned)((s + 255) / 256));
-    const int bk128 = fwd_bk128(s, hq);
+    const int bk128 = fwd_bk128(s, hq, seg);
     if (bk128) {
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
         auto k = bk128 == 4 ? fatc::fwd_tc128_kernel<4> : bk128 == 8 ? fatc::fwd_tc128_kernel<8> : fatc::fwd_tc128_kernel<0>;
