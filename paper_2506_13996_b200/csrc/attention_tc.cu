@@ -465,6 +465,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 // under the other tile's MMAs.  MMA order per block j: PV0(j) S0(j+1) PV1(j) S1(j+1).
 namespace fw2 {
 constexpr int BKB = 128;
+#ifndef SPT_FWD2_NPART
+#define SPT_FWD2_NPART 4
+#endif
+constexpr int NPART = SPT_FWD2_NPART;  // P hand-off parts per block (PV MMAs start per part)
 constexpr int Q_BYTES = BQ * D * 2;    // 32 KiB per tile
 constexpr int KV_BYTES = BKB * D * 2;  // 32 KiB per K or V block (two 16 KiB regions)
 constexpr int NSL = 4;
@@ -488,8 +492,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* kv_full = bar + 1;
     uint64_t* kv_empty = kv_full + NSL;
     uint64_t* s_full = kv_empty + NSL;  // [t]
-    uint64_t* p_full = s_full + 2;      // [t * 2 + half]: P for keys [64 half, 64 half + 64) written
-    uint64_t* pv_done = p_full + 4;     // [t]
+    uint64_t* p_full = s_full + 2;      // [t * NPART + part]: P for keys [part, part + 1) * 128 / NPART written
+    uint64_t* pv_done = p_full + 2 * NPART;  // [t]
     uint64_t* o_done = pv_done + 2;     // [t]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
@@ -513,8 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&s_full[t], 1);
-            mbar_init(&p_full[2 * t], 128);
-            mbar_init(&p_full[2 * t + 1], 128);
+            for (int part = 0; part < NPART; ++part) mbar_init(&p_full[NPART * t + part], 128);
             mbar_init(&pv_done[t], 1);
             mbar_init(&o_done[t], 1);
         }
@@ -575,12 +578,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&kv_full[slot(j, 1)], phase(j, 1));
                 const uint32_t vb = sbase + OFF_KV + slot(j, 1) * KV_BYTES;
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    mbar_wait(&p_full[2 * t + half], (j - jb[t]) & 1);
+                for (int part = 0; part < NPART; ++part) {
+                    mbar_wait(&p_full[NPART * t + part], (j - jb[t]) & 1);
                     tc_fence_after();
 #pragma unroll
-                    for (int kq = 0; kq < BKB / 32; ++kq) {
-                        const int kk = half * (BKB / 32) + kq;
+                    for (int kq = 0; kq < BKB / 16 / NPART; ++kq) {
+                        const int kk = part * (BKB / 16 / NPART) + kq;
                         mma_bf16_ts_w(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, mndesc_r(vb, kk, 16384), idesc_o,
                                       (pv_count[t] > 0 || kk > 0));
                     }
@@ -691,10 +694,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     pw[k] = pack_bf16x2(p0, p1);
                 }
                 tmem_st16(t_tm + c * 16, pw);
-                if (c == 1) {  // keys [0, 64) done: the first half of PV can start
+                if (c < 3 && (c + 1) % (4 / NPART) == 0) {  // this part of P done: its PV MMAs can start
                     tmem_st_wait();
                     tc_fence_before();
-                    mbar_arrive(&p_full[2 * t]);
+                    mbar_arrive(&p_full[NPART * t + (c + 1) / (4 / NPART) - 1]);
                 }
             }
             float rs0, rs1;
@@ -702,7 +705,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             l += rs0 + rs1;
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&p_full[2 * t + 1]);
+            mbar_arrive(&p_full[NPART * t + NPART - 1]);
         }
         mbar_wait(&o_done[t], 0);
         tc_fence_after();
