@@ -206,7 +206,8 @@ def _attn_case(s, hq, hkv, d, packed, seed, amp=1.0):
                                                    (1536, 2, 2, 128, False, 1), (1024, 2, 1, 128, False, 2.5),
                                                    (1024, 2, 2, 128, True, 2.5), (1024, 4, 1, 128, False, 1),
                                                    (1024, 8, 1, 128, True, 1), (640, 4, 2, 128, True, 1),
-                                                   (896, 8, 1, 128, False, 2.5)])
+                                                   (896, 8, 1, 128, False, 2.5), (128, 2, 1, 128, False, 1),
+                                                   (256, 4, 4, 128, False, 1), (128, 4, 2, 128, True, 1)])
 def test_attention_fwd_bwd(s, hq, hkv, d, packed, amp):
     """amp > 1 gives peaked softmax rows: exercises the lazy O-rescale path of the tcgen05 forward."""
     T = torch()
