@@ -353,16 +353,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int i = 0; i < 32; ++i) {
                         const int col = c * 32 + i;
                         if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
-                        mp[col & 7] = fmaxf(mp[col & 7], __uint_as_float(v[c][i]));
                     }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 2; ++c)
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2)
-                        mp[(c * 32 + i) >> 1 & 7] =
-                            fmaxf(mp[(c * 32 + i) >> 1 & 7], fmaxf(__uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1])));
             }
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int i = 0; i < 32; i += 2)
+                    mp[(c * 32 + i) >> 1 & 7] =
+                        fmax3(mp[(c * 32 + i) >> 1 & 7], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
             const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                                      fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
             const float mx = mraw * scale_log2;
@@ -642,16 +640,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int i = 0; i < 32; ++i) {
                         const int col = c * 32 + i;
                         if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
-                        mp[col & 7] = fmaxf(mp[col & 7], __uint_as_float(v[c][i]));
                     }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2)
-                        mp[(c * 32 + i) >> 1 & 7] =
-                            fmaxf(mp[(c * 32 + i) >> 1 & 7], fmaxf(__uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1])));
             }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int i = 0; i < 32; i += 2)
+                    mp[(c * 32 + i) >> 1 & 7] =
+                        fmax3(mp[(c * 32 + i) >> 1 & 7], __uint_as_float(v[c][i]), __uint_as_float(v[c][i + 1]));
             const float mraw = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                                      fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
             const float mx = mraw * scale_log2;

@@ -341,6 +341,17 @@ __device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
 }
 
 // ------------------------------------------------------------------ misc
+// Three-input fp32 max (FMNMX3 on sm_100a): one ALU instruction per two new values in a max reduction.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+#ifdef SPT_FWD_MAX2  // A/B build: the two-instruction form
+    return fmaxf(a, fmaxf(b, c));
+#else
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+#endif
+}
+
 // Packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2 / FMUL2: two lanes of fp32 per instruction, same
 // IEEE rounding as the scalar ops).  The softmax / elementwise loops of the attention kernels are
 // issue-bound, so halving their FMA-pipe instruction count is a direct speed-up.
