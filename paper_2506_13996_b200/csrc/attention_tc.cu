@@ -93,6 +93,17 @@ __device__ __forceinline__ void grid_head_row(int kvg, int hq, int hkv, int& h, 
     h = g * hg + (rem - yb * hgl);
 }
 
+// 2^x0, 2^x1 with one ex2.approx.f16x2 (inputs rounded to f16: |x| <= 2^-11 relative, results f16-accurate,
+// 2^-24 flush; the forward uses x <= RESCALE_THRESHOLD, so no overflow), widened back to fp32.
+__device__ __forceinline__ void ex2_f16x2(float x0, float x1, float& p0, float& p1) {
+    uint32_t h, e;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+    asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+        : "=f"(p0), "=f"(p1)
+        : "r"(e));
+}
+
 __device__ __forceinline__ void lds128(uint32_t addr, float& a, float& b, float& c, float& d) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
 }
@@ -684,8 +695,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), sc2, nb2);
                     float x0, x1;
                     f2unpack(x2, x0, x1);
-                    const bool poly = POLY > 0 && ((c * 16 + k) % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY - 1 : 0);
-                    const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
+                    float p0, p1;
+                    if constexpr (POLY == 1) {  // two exponentials per MUFU op in f16 (P is bf16 anyway)
+                        ex2_f16x2(x0, x1, p0, p1);
+                    } else {
+                        const bool poly = POLY > 1 && ((c * 16 + k) % (POLY > 1 ? POLY : 1)) == (POLY > 1 ? POLY - 1 : 0);
+                        p0 = poly ? ex2_poly(x0) : ex2(x0);
+                        p1 = poly ? ex2_poly(x1) : ex2(x1);
+                    }
                     rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
                     pw[k] = pack_bf16x2(p0, p1);
                 }
@@ -2547,6 +2564,7 @@ int g_attn_fwd_bk128 = [] {
 // Packed sequences keep the 64-key kernel: with short samples most 128-key blocks straddle a sample start
 // (s=128K, mean sample 2048: 6.57 vs 4.56 ms), while long samples gain only a few % (32768: 57.7 vs 61.3 ms).
 // Values: 1 (default) 128-key unless packed, 2 128-key always, 0 64-key, 4 / 8 128-key + FMA-pipe exp2,
+// 3 128-key with f16x2 exponentials,
 // -1 128-key for s * hq >= 2^21.  Returns 0 (64-key) or the 128-key kernel's POLY selector (1, 4, 8).
 static int fwd_bk128(int64_t s, int hq, const int32_t* seg) {
     const int v = g_attn_fwd_bk128;
@@ -2571,7 +2589,8 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
     static bool attr = false;
     if (!attr) {
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
-        for (auto k : {fatc::fwd_tc128_kernel<0>, fatc::fwd_tc128_kernel<4>, fatc::fwd_tc128_kernel<8>})
+        for (auto k : {fatc::fwd_tc128_kernel<0>, fatc::fwd_tc128_kernel<1>, fatc::fwd_tc128_kernel<4>,
+                       fatc::fwd_tc128_kernel<8>})
             SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw2::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::fwt::SMEM));
@@ -2581,7 +2600,10 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
     const int bk128 = fwd_bk128(s, hq, seg);
     if (bk128) {
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
-        auto k = bk128 == 4 ? fatc::fwd_tc128_kernel<4> : bk128 == 8 ? fatc::fwd_tc128_kernel<8> : fatc::fwd_tc128_kernel<0>;
+        auto k = bk128 == 4   ? fatc::fwd_tc128_kernel<4>
+                 : bk128 == 8 ? fatc::fwd_tc128_kernel<8>
+                 : bk128 == 3 ? fatc::fwd_tc128_kernel<1>
+                              : fatc::fwd_tc128_kernel<0>;
         k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
                                                         kv_group(s, hkv, d));
     } else if (g_attn_fwd_tmem)
