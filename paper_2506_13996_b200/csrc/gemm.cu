@@ -136,7 +136,7 @@ static int env_int(const char* name, int dflt) {
 }
 // Experiment / tuning switches: initialised from the environment, changeable at run time through
 // spt_tuning_set (A/B comparisons inside one process).  gemm_1sm=1 disables CTA pairs, gemm_pair_mn selects
-// which MN-major operand shapes run as pairs (0 = default none, 1 all, 2 by shape: see pair_mn), gemm_bn=128|256 forces the N tile (0 = per-shape choice),
+// which MN-major operand shapes run as pairs (0 = default none, 1 all, 2 by shape: see pair_mn), gemm_bn=128|256 forces the N tile (0 = 256, 2 = 128 where it fills the last wave better),
 // epi_tstore = fp32 epilogue mode: 0 per-thread stores, 1 smem-transposed coalesced stores, 2 (default) TMA
 // store / reduce-add on the 1-SM kernel (the pair kernel and the stats epilogue use mode 1).
 struct GemmTuning {
@@ -225,11 +225,29 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
     // The SwiGLU epilogues pair gate/up 32-column blocks inside a 64-column chunk and the logits stats are
     // per 256 columns, so those kinds keep BN = 256.
     const bool bn_free = kind == EPI_BF16 || kind == EPI_F32;
-    const int bn = bn_free && (forced_bn() == 128) ? 128 : 256;
     // CTA pairs win for K-major x K-major (forward / logits) GEMMs.  MN-major operand shapes (backward) go
     // by pair_mn: pairs win short bursts (3 steps: -1.4..-3.3% per L1 step with the shape rule) but lose
     // sustained, power-capped runs (12 steps: +3.7%), so the default keeps them on the 1-SM kernel.
-    if (M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn(M, K, kind)) && use_pair_gemm()) {
+    const bool pair = M >= 2 * GEMM_BM && ((!A.mn_major && !B.mn_major) || pair_mn(M, K, kind)) && use_pair_gemm();
+    // N tile: 256, or forced by gemm_bn (128 / 256), or (gemm_bn = 2) 128 where the tile count leaves the
+    // last wave of the persistent grid mostly idle and 128-wide tiles fill it (the TiledMLP GEMMs with
+    // 4096-row tiles and a long K: 512 tiles = 3.46 waves of 148 SMs at BN=256, 6.92 at BN=128).  That rule
+    // measured 4% slower per sustained L1 step (168.7 -> 175.5 ms): the 128-wide MMAs read a third more
+    // smem per flop, and under the power cap that costs more than the idle tail.
+    int bn = 256;
+    if (bn_free) {
+        if (forced_bn() == 128 || forced_bn() == 256) bn = forced_bn();
+        else if (forced_bn() == 2) {
+            const int64_t units = pair ? num_sms() / 2 : num_sms(), rows = pair ? 2 * GEMM_BM : GEMM_BM;
+            auto eff = [&](int64_t bnx) {
+                const int64_t tiles = ((M + rows - 1) / rows) * ((N + bnx - 1) / bnx);
+                const int64_t waves = (tiles + units - 1) / units;
+                return (double)tiles / (double)(waves * units);
+            };
+            if (eff(128) >= eff(256) + 0.06) bn = 128;
+        }
+    }
+    if (pair) {
         if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
         else dispatch_pair<256>(A, B, M, N, K, kind, ep, st);
