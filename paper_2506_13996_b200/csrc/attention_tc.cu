@@ -23,6 +23,9 @@ constexpr int THREADS = 320;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 constexpr float RESCALE_THRESHOLD = 8.f;  // log2 units
+// packed sequences: a tile pair whose first sample started at least this many keys before its end runs on
+// the 128-key forward, the rest on the 64-key forward (short samples straddle 128-key blocks)
+constexpr int64_t FWD_LONG_KEYS = 4096;
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -165,7 +168,7 @@ constexpr int SMEM = OFF_BAR + 512 + 1024;
 __global__ void __launch_bounds__(THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                   int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
-                  float* __restrict__ lse, int kvg) {
+                  float* __restrict__ lse, int kvg, int filter) {
     using namespace fw;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -191,7 +194,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool has1 = q0 + BQ < s;  // second query tile present
     const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = (seg && has1) ? (int)(seg[q0 + BQ] / BKB) : 0;
     const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = has1 ? (int)((q0 + 2 * BQ - 1) / BKB) : -1;
-    const int jlo = jb0, jhi = has1 ? je1 : je0;  // jb0 <= jb1 (starts are monotone), je0 < je1
+    const int jlo = jb0, jhi = has1 ? je1 : je0;
+    if (filter) {  // packed hybrid: this launch handles only the long (1) or short (2) tile pairs
+        const bool longp = q0 + 2 * BQ - (seg ? seg[q0] : 0) >= FWD_LONG_KEYS;
+        if ((filter == 1) != longp) return;  // whole CTA, before any barrier / TMEM allocation
+    }  // jb0 <= jb1 (starts are monotone), je0 < je1
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -492,7 +499,7 @@ template <int POLY>
 __global__ void __launch_bounds__(THREADS, 1)
     fwd_tc128_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                      int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
-                     float* __restrict__ lse, int kvg) {
+                     float* __restrict__ lse, int kvg, int filter) {
     using namespace fw2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -517,6 +524,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int jb0 = seg ? (int)(seg[q0] / BKB) : 0, jb1 = (seg && has1) ? (int)(seg[q0 + BQ] / BKB) : 0;
     const int je0 = (int)((q0 + BQ - 1) / BKB), je1 = has1 ? (int)((q0 + 2 * BQ - 1) / BKB) : -1;
     const int jlo = jb0, jhi = has1 ? je1 : je0;
+    if (filter) {  // packed hybrid: this launch handles only the long (1) or short (2) tile pairs
+        const bool longp = q0 + 2 * BQ - (seg ? seg[q0] : 0) >= FWD_LONG_KEYS;
+        if ((filter == 1) != longp) return;  // whole CTA, before any barrier / TMEM allocation
+    }
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -2557,6 +2568,15 @@ static int kv_group(int64_t s, int hkv, int d) {
 // double-buffered kernel).  With the P hand-off split in halves it measured -3% at 32K x 32 heads, -3.4% at
 // 128K x 4, -6% at the L8 rank shape (profiles/r1z3_fwd_bk128.txt).  -1: 128-key only for s * hq >= 2^21
 // (the rule before the split hand-off).
+// SPT_ATTN_FWD_HYBRID=0|1 (run time: spt_tuning_set("attn_fwd_hybrid", v)): packed sequences split per tile
+// pair between the 128-key and the 64-key forward.  Opt-in: with the packed mask fast path both kernels
+// measured within run-to-run noise on packed sequences (tools/packed_attn_bench.py, s=128K, mean sample
+// 2K / 8K / 32K), so the single 64-key launch stays the default there.
+int g_attn_fwd_hybrid = [] {
+    const char* e = getenv("SPT_ATTN_FWD_HYBRID");
+    return e ? atoi(e) : 0;
+}();
+
 int g_attn_fwd_bk128 = [] {
     const char* e = getenv("SPT_ATTN_FWD_BK128");
     return e ? atoi(e) : 1;
@@ -2605,13 +2625,20 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                  : bk128 == 3 ? fatc::fwd_tc128_kernel<1>
                               : fatc::fwd_tc128_kernel<0>;
         k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
-                                                        kv_group(s, hkv, d));
+                                                        kv_group(s, hkv, d), 0);
+    } else if (seg != nullptr && g_attn_fwd_bk128 == 1 && g_attn_fwd_hybrid) {
+        // packed: long-sample tile pairs on the 128-key kernel, short ones on the 64-key kernel
+        CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
+        fatc::fwd_tc128_kernel<0><<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(
+            tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse, kv_group(s, hkv, d), 1);
+        fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
+                                                                          (bf16*)o, lse, kv_group(s, hkv, d), 2);
     } else if (g_attn_fwd_tmem)
         fatc::fwd_tmem_kernel<<<grid, fatc::THREADS, fatc::fwt::SMEM, st>>>(tkv, (const bf16*)qkv, s, hq, hkv, seg,
                                                                               scale * fatc::LOG2E, (bf16*)o, lse);
     else
         fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
-                                                                          (bf16*)o, lse, kv_group(s, hkv, d));
+                                                                          (bf16*)o, lse, kv_group(s, hkv, d), 0);
     count_launch("attn_fwd_tc");
     SPT_CUDA(cudaGetLastError());
     return true;

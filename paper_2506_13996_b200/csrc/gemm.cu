@@ -286,6 +286,7 @@ extern int g_attn_dkdv_pair;  // attention_tc.cu
 extern int g_attn_dkdv_kt;    // attention_tc.cu
 extern int g_attn_kv_group;   // attention_tc.cu
 extern int g_attn_fwd_bk128;  // attention_tc.cu
+extern int g_attn_fwd_hybrid;  // attention_tc.cu
 }
 
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
@@ -298,6 +299,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         }
         if (n == "attn_fwd_tmem") {
             spt::g_attn_fwd_tmem = value;
+            return;
+        }
+        if (n == "attn_fwd_hybrid") {
+            spt::g_attn_fwd_hybrid = value;
             return;
         }
         if (n == "attn_fwd_bk128") {

@@ -485,3 +485,33 @@ def test_attention_fwd_other_blocks(s, hq, hkv, packed, amp, mode):
         S.check(L.spt_tuning_set(b"attn_fwd_bk128", 1))
     assert rel_err(to_np(o), o_r) < 1e-2
     assert np.max(np.abs(to_np(lse) - lse_r)) < 2e-3
+
+
+def test_attention_fwd_packed_hybrid():
+    """Packed sequences split per tile pair between the 128-key forward (pairs inside a long sample) and the
+    64-key forward (the rest): a long and two short samples, against the float64 oracle."""
+    T = torch()
+    L = _lib()
+    s, hq, hkv, d = 6144, 2, 1, 128
+    rng = np.random.default_rng(11)
+    qkv = O.round_bf16(rng.standard_normal((s, hq + 2 * hkv, d), dtype=np.float32))
+    pos = np.concatenate([np.arange(4990), np.arange(777), np.arange(s - 4990 - 777)])
+    starts = O.block_causal_starts(pos)
+    q, k, v = qkv[:, :hq], qkv[:, hq:hq + hkv], qkv[:, hq + hkv:]
+    o_r, lse_r = O.attention_fwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), starts)
+    qkvd = bf16_dev(qkv)
+    seg = T.from_numpy(starts.astype(np.int32)).cuda()
+    outs = []
+    try:
+        for hyb in (1, 0):
+            S.check(L.spt_tuning_set(b"attn_fwd_hybrid", hyb))
+            o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+            lse = T.empty(hq, s, device="cuda")
+            S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, seg.data_ptr(), 1.0 / math.sqrt(d), o.data_ptr(),
+                                   lse.data_ptr(), None))
+            outs.append((to_np(o), to_np(lse)))
+    finally:
+        S.check(L.spt_tuning_set(b"attn_fwd_hybrid", 0))
+    for o_, lse_ in outs:
+        assert rel_err(o_, o_r) < 1e-2
+        assert np.max(np.abs(lse_ - lse_r)) < 2e-3
