@@ -255,3 +255,39 @@ def test_rope_fused_into_reshard_bitwise(P, packed):
     for k in a["grads"]:
         assert np.array_equal(a["grads"][k], b["grads"][k]), k
     _check(b, 2, P, packed, rope=10000.0)
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_embedding_grad_accumulation_window(P):
+    """Token embedding inside a gradient-accumulation window: grad "emb" accumulates the
+    micro-steps' per-id sums and is divided by the window's global count like every other grad."""
+    L, N, seed = 1, 512, 21
+    layers, g3, wlm = _params(CFG, L, seed)
+    rng = np.random.default_rng(seed)
+    emb = O.round_bf16(rng.standard_normal((CFG.vocab, CFG.hidden), dtype=np.float32))
+    batches = []
+    for b in range(2):
+        _, lab, _ = O.synth_batch(CFG, N, seed + 1 + b)
+        batches.append((rng.integers(0, 97, N).astype(np.int64), lab))
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(SHAPE, N, grp, n_layers=L, embed=True)
+    try:
+        for k in O.LAYER_NAMES:
+            eng.set_param(f"layers.0.{k}", O.f32_to_bf16_bits(layers[0][k]))
+        eng.set_param("g3", O.f32_to_bf16_bits(g3))
+        eng.set_param("wlm", O.f32_to_bf16_bits(wlm))
+        eng.set_param("emb", O.f32_to_bf16_bits(emb))
+        for i, (ids, lab) in enumerate(batches):
+            eng.step_accumulate(ids, lab, first=(i == 0))
+        loss, cnt = eng.finish_accumulation()
+        g_emb, g_wqkv = eng.grad("emb"), eng.grad("layers.0.wqkv")
+    finally:
+        eng.close()
+        grp.close()
+    refs = [O.model_step(layers, g3, wlm, CFG, ids, lab, P=P, emb=emb) for ids, lab in batches]
+    tot = sum(r.count for r in refs)
+    assert cnt == tot
+    assert abs(loss - sum(r.loss_sum for r in refs) / tot) / abs(refs[0].loss) <= LOSS_TOL
+    for name, got in (("emb", g_emb), ("wqkv", g_wqkv)):
+        ref_g = sum(r.grads[name] * r.count for r in refs) / tot
+        assert rel_err(got, ref_g) <= GRAD_TOL, name
