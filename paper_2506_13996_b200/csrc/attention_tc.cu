@@ -487,7 +487,10 @@ constexpr int BKB = 128;
 constexpr int NPART = SPT_FWD2_NPART;  // P hand-off parts per block (PV MMAs start per part)
 constexpr int Q_BYTES = BQ * D * 2;    // 32 KiB per tile
 constexpr int KV_BYTES = BKB * D * 2;  // 32 KiB per K or V block (two 16 KiB regions)
-constexpr int NSL = 4;
+#ifndef SPT_FWD2_NSL
+#define SPT_FWD2_NSL 4
+#endif
+constexpr int NSL = SPT_FWD2_NSL;  // K/V ring slots (5 is the most that fits next to the two Q tiles)
 constexpr int OFF_Q = 0, OFF_KV = 2 * Q_BYTES;
 constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 512 + 1024;
