@@ -15,7 +15,7 @@ def cls(n):
         return "gemm"
     if "fwd_tc" in n:
         return "attn_fwd"
-    if "dkdv" in n or "dq_tc" in n or "bwd_dot" in n:
+    if "dkdv" in n or "dq_tc" in n or "dq_tmem" in n or "bwd_dot" in n:
         return "attn_bwd"
     if "ce_rows" in n:
         return "ce_rows"
