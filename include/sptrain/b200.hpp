@@ -286,6 +286,17 @@ inline void tiled_mlp_bwd(const void* x, const void* wgu, const void* wd, const 
                           void* workspace, void* stream = nullptr) {
     check(spt_mlp_bwd(x, wgu, wd, dy, dx, dwgu, dwd, accumulate ? 1 : 0, n, h, inter, tile_n, workspace, stream));
 }
+// Token embedding: x[t] = table[input_ids[t]]; backward = per-id sums of dx rows in ascending
+// token order (deterministic).  An id outside [0, vocab) sets *err_flag (device) to 3.
+inline void embedding_fwd(const int64_t* input_ids, int64_t n, int64_t vocab, int64_t h, const void* table, void* x,
+                          int32_t* err_flag, void* stream = nullptr) {
+    check(spt_embed_fwd(input_ids, n, vocab, h, table, x, err_flag, stream));
+}
+inline void embedding_bwd(const int64_t* input_ids, int64_t n, int64_t vocab, int64_t h, const void* dx, float* dtable,
+                          bool accumulate, int32_t* err_flag, void* workspace, void* stream = nullptr) {
+    check(spt_embed_bwd(input_ids, n, vocab, h, dx, dtable, accumulate ? 1 : 0, err_flag, workspace, stream));
+}
+inline size_t embedding_bwd_workspace(int64_t n, int64_t vocab) { return spt_embed_bwd_workspace(n, vocab); }
 
 }  // namespace b200
 }  // namespace sptrain
