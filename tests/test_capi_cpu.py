@@ -1,6 +1,6 @@
 """CPU-only checks of the C-ABI library: it loads without a GPU, exports every symbol the public
 header declares, and its host-side logic (SPEC ops that need no device) matches the oracle and the
-reference's golden vectors.  No compute entry point is called here."""
+reference's golden vectors.  Compute entry points are only called to check that they fail without a GPU."""
 import ctypes as C
 import json
 import os
@@ -105,3 +105,20 @@ def test_a2a_counts_match_payloads(S, Hq, Hkv, P):
                            (2, p.q_heads_per_rank), (3, p.q_heads_per_rank + 2 * p.kv_heads_per_rank)):
         send, recv = S.a2a_counts(p, s_loc, d, direction)
         assert (send == s_loc * per * d).all() and (recv == send).all()
+
+
+def test_no_cpu_fallback(S):
+    """Without a B200 every compute entry point fails loudly (SPT_ERR_CUDA-class status and a message): there
+    is no CPU fallback on the product path.  Skipped where a GPU is visible."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    L = S.lib()
+    h = C.c_void_p()
+    assert L.spt_comm_init_loopback(1, 0, C.byref(h)) != 0
+    assert L.spt_last_error()
+    st = L.spt_attn_fwd(None, 256, 2, 1, 128, None, 0.1, None, None, None)
+    assert st != 0 and L.spt_last_error()
+    st = L.spt_embed_fwd(None, 8, 16, 8, None, None, None, None)
+    assert st != 0
