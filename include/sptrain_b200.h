@@ -134,6 +134,17 @@ spt_status spt_rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, 
  * head_map is a DEVICE int32 array of P*heads_out entries. */
 spt_status spt_reshard_pack(const void* src, int64_t s_loc, int32_t heads_in, int32_t head_dim, int32_t P,
                             int32_t heads_out, const int32_t* head_map, void* dst, void* stream);
+/* K1 with RoPE fused: as spt_reshard_pack, with source heads < n_rot (q and k heads)
+ * rotated on the way (positions: DEVICE int64 position_ids [s_loc] or pos_offset + t; base theta); bitwise
+ * equal to spt_rope followed by spt_reshard_pack.  head_dim % 16 == 0 and head_dim in {32, 64, 128}. */
+spt_status spt_reshard_pack_rope(const void* src, int64_t s_loc, int32_t heads_in, int32_t head_dim, int32_t P,
+                                 int32_t heads_out, const int32_t* head_map, void* dst, int32_t n_rot,
+                                 const int64_t* position_ids, int64_t pos_offset, float theta,
+                                 const void* cos_sin_table, void* stream);
+/* RoPE angle table for positions [0, npos): (cos, sin) fp32 pairs [npos][head_dim / 2], bit-identical to the
+ * angles the kernels compute themselves (npos * head_dim * 4 bytes).  Optional argument of
+ * spt_reshard_pack_rope (NULL: computed in-kernel); the layer engine builds one at creation. */
+spt_status spt_rope_table(void* cos_sin_table, int64_t npos, int32_t head_dim, float theta, void* stream);
 /* head_to_seq receive side (K2): recv [P][s_loc][heads_in][d] -> out [s_loc][heads_out][d];
  * out[t][h] = sum over the (src rank, slot) pairs listed for h, in rank order (replicate_kv backward,
  * SPEC.md:326).  gather: DEVICE int32 [heads_out][max_src] of (rank*heads_in + slot), -1 = unused. */

@@ -78,6 +78,8 @@ SIGNATURES = {
     "spt_rmsnorm_bwd_workspace": (SZ, [I64, I64]),
     "spt_rmsnorm_bwd": (I32, [P, P, P, P, P, P, P, P, I64, I64, P]),
     "spt_reshard_pack": (I32, [P, I64, I32, I32, I32, I32, P, P, P]),
+    "spt_reshard_pack_rope": (I32, [P, I64, I32, I32, I32, I32, P, P, I32, P, I64, F32, P, P]),
+    "spt_rope_table": (I32, [P, I64, I32, F32, P]),
     "spt_reshard_unpack": (I32, [P, I64, I32, I32, I32, I32, P, I32, P, P]),
     "spt_attn_fwd": (I32, [P, I64, I32, I32, I32, P, F32, P, P, P]),
     "spt_attn_bwd_workspace": (SZ, [I64, I32, I32, I32]),

@@ -194,6 +194,7 @@ struct spt_layer {
     bool offload = false;  // checkpoints in pinned host memory
     std::vector<LayerW> lw;
     bf16 *g3, *wlm;
+    void* rope_tab = nullptr;  // RoPE (cos, sin) per (position < N, j < d/2), built once at creation
     bool embed = false;      // token embedding in front of the stack: step inputs are input_ids
     bf16* emb = nullptr;     // [V][h]
     void* ws_emb = nullptr;
@@ -375,6 +376,11 @@ static void build_layer(spt_layer* Ly) {
     Ly->ws_rms = L_.alloc(rmsnorm_bwd_workspace(nl, h), kWorkspace);
     Ly->ws_attn = L_.alloc(attn_bwd_workspace(N, Ly->hq_loc, Ly->hkv_loc, c.head_dim), kWorkspace);
     if (Ly->embed) Ly->ws_emb = L_.alloc(embed_bwd_workspace(nl, V), kWorkspace);
+    if (c.rope_theta > 0.f) {  // every position a step can use is < N (global index, or within a packed sample)
+        Ly->rope_tab = L_.alloc((size_t)N * (c.head_dim / 2) * 8, kWorkspace);
+        rope_table(Ly->rope_tab, N, c.head_dim, c.rope_theta, nullptr);
+        SPT_CUDA(cudaStreamSynchronize(nullptr));
+    }
     // reshard tables
     auto up = [&](const std::vector<int32_t>& v) {
         int32_t* d = (int32_t*)L_.alloc(v.size() * 4, kWorkspace);
@@ -528,12 +534,12 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
                 pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
                     rope_done = reshard_pack_rope(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc,
                                                   Ly->map_qkv, b.send_qkv, c.q_heads + c.kv_heads,
-                                                  c.packed ? b.pos : nullptr, rope_off, c.rope_theta, st);
+                                                  c.packed ? b.pos : nullptr, rope_off, c.rope_theta, st, Ly->rope_tab);
                 });
             if (rope_on && !rope_done)  // rotate q and k heads in place before the reshard / attention
                 pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
                     rope_apply(b.qkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
-                               c.packed ? b.pos : nullptr, rope_off, c.rope_theta, false, st);
+                               c.packed ? b.pos : nullptr, rope_off, c.rope_theta, false, st, Ly->rope_tab);
                 });
             if (P > 1 && !rope_done)
                 pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
@@ -617,7 +623,7 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
                         reshard_unpack_rope(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, c.q_heads + 2 * c.kv_heads,
                                             Ly->gather_qkv, Ly->max_src_qkv, b.dqkv, c.q_heads + c.kv_heads,
                                             c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl,
-                                            c.rope_theta, st)) {
+                                            c.rope_theta, st, Ly->rope_tab)) {
                         dqkv_rotated[r] = 1;
                         return;
                     }
@@ -633,7 +639,8 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             if (rope_on && !dqkv_rotated[r])  // d(q, k) through the rotation's transpose, before the projection's backward
                 pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
                     rope_apply(b.dqkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
-                               c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, true, st);
+                               c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, true, st,
+                               Ly->rope_tab);
                 });
             EpiParams e1;
             e1.C = dxn1;

@@ -206,14 +206,36 @@ __global__ void reshard_unpack_kernel(const uint4* __restrict__ recv, int64_t s_
 // RoPE rotation of 8 consecutive pairs (j = 8 gi .. 8 gi + 7 of the first half against the second half) at
 // position p, Llama / HF rotate_half convention with HF's fp32 angles; explicit roundings so the standalone
 // kernel and the pack/unpack-fused kernels produce identical bits.
+// The (cos, sin) of one (position, j): HF's fp32 angle p * theta^(-2j/d).  Used by rope_table_kernel and by
+// the kernels when no table is given, so both paths give identical bits.
+__device__ __forceinline__ void rope_cos_sin(float p, int j, int d, float theta, float& cs, float& sn) {
+    const float inv_freq = 1.f / powf(theta, (float)(2 * j) / (float)d);
+    sincosf(p * inv_freq, &sn, &cs);
+}
+
+// tab: NULL (angles computed here: accurate sincosf of arguments up to ~1e6 rad takes the slow range
+// reduction, which made the kernels ALU-bound) or the (cos, sin) row of this position, entries 8 gi .. 8 gi + 7.
 __device__ __forceinline__ void rope_rotate8(const float* a, const float* b, float p, int gi, int d, float theta,
-                                             float sgn, float* o1, float* o2) {
+                                             float sgn, float* o1, float* o2, const float2* tab = nullptr) {
+    float2 cst[8];
+    if (tab) {
+        const float4* t4 = reinterpret_cast<const float4*>(tab + gi * 8);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float4 v = __ldg(t4 + k);
+            cst[2 * k] = make_float2(v.x, v.y);
+            cst[2 * k + 1] = make_float2(v.z, v.w);
+        }
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const int j = gi * 8 + k;
-        const float inv_freq = 1.f / powf(theta, (float)(2 * j) / (float)d);
         float sn, cs;
-        sincosf(p * inv_freq, &sn, &cs);
+        if (tab) {
+            cs = cst[k].x;
+            sn = cst[k].y;
+        } else {
+            rope_cos_sin(p, gi * 8 + k, d, theta, cs, sn);
+        }
         sn *= sgn;
         o1[k] = __fsub_rn(__fmul_rn(a[k], cs), __fmul_rn(b[k], sn));
         o2[k] = __fadd_rn(__fmul_rn(b[k], cs), __fmul_rn(a[k], sn));
@@ -244,7 +266,7 @@ __global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __r
                                                                 const int32_t* __restrict__ head_map,
                                                                 uint4* __restrict__ dst, int n_rot,
                                                                 const int64_t* __restrict__ pos, int64_t pos_offset,
-                                                                float theta) {
+                                                                float theta, const float2* __restrict__ tab) {
     extern __shared__ int32_t smap[];  // [P][heads_out]
     for (int i = threadIdx.x; i < P * heads_out; i += blockDim.x) smap[i] = head_map[i];
     __syncthreads();
@@ -257,7 +279,9 @@ __global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __r
     for (int64_t r = w0; r < nrows; r += nw) {
         const int j = (int)(r / s_loc);
         const int64_t t = r - (int64_t)j * s_loc;
-        const float p = (float)(pos ? pos[t] : pos_offset + t);
+        const int64_t pi = pos ? pos[t] : pos_offset + t;
+        const float p = (float)pi;
+        const float2* trow = tab ? tab + pi * (VPD * 4) : nullptr;
         const uint4* srow = src + t * heads_in * VPD;
         uint4* drow = dst + r * heads_out * VPD;
         const int32_t* m = smap + j * heads_out;
@@ -269,7 +293,7 @@ __global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __r
                 float fa[8], fb[8], o1[8], o2[8];
                 u4_to_f8(a, fa);
                 u4_to_f8(b, fb);
-                rope_rotate8(fa, fb, p, c, VPD * 8, theta, 1.f, o1, o2);
+                rope_rotate8(fa, fb, p, c, VPD * 8, theta, 1.f, o1, o2, trow);
                 a = f8_to_u4(o1);
                 b = f8_to_u4(o2);
             }
@@ -287,7 +311,7 @@ __global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const uint4* _
                                                                   const int32_t* __restrict__ gather, int max_src,
                                                                   uint4* __restrict__ dst, int n_rot,
                                                                   const int64_t* __restrict__ pos, int64_t pos_offset,
-                                                                  float theta) {
+                                                                  float theta, const float2* __restrict__ tab) {
     extern __shared__ int32_t sg[];  // [heads_out][max_src]
     for (int i = threadIdx.x; i < heads_out * max_src; i += blockDim.x) sg[i] = gather[i];
     __syncthreads();
@@ -300,7 +324,9 @@ __global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const uint4* _
     for (int64_t t = w0; t < s_loc; t += nw) {
         const uint4* trow = recv + t * heads_in * VPD;
         uint4* drow = dst + t * heads_out * VPD;
-        const float p = (float)(pos ? pos[t] : pos_offset + t);
+        const int64_t pi = pos ? pos[t] : pos_offset + t;
+        const float p = (float)pi;
+        const float2* crow = tab ? tab + pi * (VPD * 4) : nullptr;
         for (int e = lane; e < row_pairs; e += 32) {
             const int h = e / HP, c = e - h * HP;
             const int32_t* gl = sg + h * max_src;
@@ -329,7 +355,7 @@ __global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const uint4* _
                 float fa[8], fb[8], o1[8], o2[8];
                 u4_to_f8(a, fa);
                 u4_to_f8(b, fb);
-                rope_rotate8(fa, fb, p, c, VPD * 8, theta, -1.f, o1, o2);
+                rope_rotate8(fa, fb, p, c, VPD * 8, theta, -1.f, o1, o2, crow);
                 a = f8_to_u4(o1);
                 b = f8_to_u4(o2);
             }
@@ -483,7 +509,7 @@ void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim,
 
 bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
                        const int32_t* head_map, void* dst, int n_rot, const int64_t* pos, int64_t pos_offset,
-                       float theta, cudaStream_t st) {
+                       float theta, cudaStream_t st, const void* tab) {
     const int vpd = head_dim / 8;
     const size_t smem = (size_t)P * heads_out * 4;
     if (head_dim % 16 != 0 || !(vpd == 4 || vpd == 8 || vpd == 16) || smem > 48 * 1024) return false;
@@ -491,7 +517,7 @@ bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_di
     const int g = reshard_rows_grid((int64_t)P * s_loc);
     auto k = vpd == 16 ? reshard_pack_rope_kernel<16> : vpd == 8 ? reshard_pack_rope_kernel<8> : reshard_pack_rope_kernel<4>;
     k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, (uint4*)dst, n_rot, pos,
-                            pos_offset, theta);
+                            pos_offset, theta, (const float2*)tab);
     count_launch();
     SPT_CUDA(cudaGetLastError());
     return true;
@@ -499,7 +525,7 @@ bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_di
 
 bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head_dim, int heads_out,
                          const int32_t* gather, int max_src, void* dst, int n_rot, const int64_t* pos,
-                         int64_t pos_offset, float theta, cudaStream_t st) {
+                         int64_t pos_offset, float theta, cudaStream_t st, const void* tab) {
     const int vpd = head_dim / 8;
     const size_t smem = (size_t)heads_out * max_src * 4;
     if (head_dim % 16 != 0 || !(vpd == 4 || vpd == 8 || vpd == 16) || smem > 48 * 1024) return false;
@@ -508,7 +534,7 @@ bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head
     auto k = vpd == 16 ? reshard_unpack_rope_kernel<16>
                        : vpd == 8 ? reshard_unpack_rope_kernel<8> : reshard_unpack_rope_kernel<4>;
     k<<<g, 256, smem, st>>>((const uint4*)recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst, n_rot, pos,
-                            pos_offset, theta);
+                            pos_offset, theta, (const float2*)tab);
     count_launch();
     SPT_CUDA(cudaGetLastError());
     return true;
@@ -520,7 +546,8 @@ bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head
 // computed in fp32 exactly as HF does; inverse = the transpose rotation (backward).  pos: DEVICE int64 [n]
 // or NULL (then pos = pos_offset + t).  One thread per (token, head, 8 consecutive j): 16-byte loads/stores.
 __global__ void rope_kernel(bf16* __restrict__ x, int64_t n, int heads, int n_rot, int d,
-                            const int64_t* __restrict__ pos, int64_t pos_offset, float theta, int inverse) {
+                            const int64_t* __restrict__ pos, int64_t pos_offset, float theta, int inverse,
+                            const float2* __restrict__ tab) {
     const int half = d / 2, g8 = half / 8;  // 8-wide groups per half
     const int64_t total = n * n_rot * g8;
     const float sgn = inverse ? -1.f : 1.f;
@@ -529,26 +556,46 @@ __global__ void rope_kernel(bf16* __restrict__ x, int64_t n, int heads, int n_ro
         const int64_t q = i / g8;
         const int hh = (int)(q % n_rot);
         const int64_t t = q / n_rot;
-        const float p = (float)(pos ? pos[t] : pos_offset + t);
+        const int64_t pi = pos ? pos[t] : pos_offset + t;
+        const float p = (float)pi;
         bf16* row = x + (t * heads + hh) * d;
         float a[8], b[8];
         load8(row + gi * 8, a);
         load8(row + half + gi * 8, b);
         float o1[8], o2[8];
-        rope_rotate8(a, b, p, gi, d, theta, sgn, o1, o2);
+        rope_rotate8(a, b, p, gi, d, theta, sgn, o1, o2, tab ? tab + pi * half : nullptr);
         store8(row + gi * 8, o1);
         store8(row + half + gi * 8, o2);
     }
 }
 
+// Angle table for positions [0, npos): tab[p][j] = (cos, sin) of HF's fp32 angle, bit-identical to the in-kernel
+// computation (rope_cos_sin).  npos * d/2 * 8 bytes (16.8 MB for 32K positions at d=128).
+__global__ void rope_table_kernel(float2* __restrict__ tab, int64_t npos, int d, float theta) {
+    const int half = d / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npos * half; i += (int64_t)gridDim.x * blockDim.x) {
+        float cs, sn;
+        rope_cos_sin((float)(i / half), (int)(i % half), d, theta, cs, sn);
+        tab[i] = make_float2(cs, sn);
+    }
+}
+
+void rope_table(void* tab, int64_t npos, int d, float theta, cudaStream_t st) {
+    SPT_CHECK(d % 16 == 0 && theta > 0.f, SPT_ERR_CONFIG, "rope table: head_dim % 16 and theta > 0");
+    if (npos == 0) return;
+    rope_table_kernel<<<grid_for(npos * (d / 2), 256), 256, 0, st>>>((float2*)tab, npos, d, theta);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
 void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
-                bool inverse, cudaStream_t st) {
+                bool inverse, cudaStream_t st, const void* tab) {
     SPT_CHECK(d % 16 == 0, SPT_ERR_SHAPE, "rope: head_dim must be a multiple of 16");
     SPT_CHECK(theta > 0.f, SPT_ERR_CONFIG, "rope: theta must be > 0");
     const int64_t total = n * n_rot * (d / 16);
     if (total == 0) return;
     rope_kernel<<<grid_for(total, 256), 256, 0, st>>>((bf16*)x, n, heads, n_rot, d, pos, pos_offset, theta,
-                                                      inverse ? 1 : 0);
+                                                      inverse ? 1 : 0, (const float2*)tab);
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }

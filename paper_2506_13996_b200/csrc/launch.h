@@ -64,15 +64,17 @@ void window_finalize(const double* win_sum, const int64_t* win_count, double* lo
 void scale_by_inverse_count(float* g, int64_t n, const int64_t* count, cudaStream_t st);
 // RoPE on the first n_rot heads of x [n][heads][d] (bf16, in place); inverse = backward rotation.
 // K1 pack / K2 unpack with RoPE fused (false: shape not supported by the fused kernels, caller falls back)
+// tab: optional (cos, sin) table from rope_table covering every position used (NULL: computed in-kernel)
 bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
                        const int32_t* head_map, void* dst, int n_rot, const int64_t* pos, int64_t pos_offset,
-                       float theta, cudaStream_t st);
+                       float theta, cudaStream_t st, const void* tab = nullptr);
 bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head_dim, int heads_out,
                          const int32_t* gather, int max_src, void* dst, int n_rot, const int64_t* pos,
-                         int64_t pos_offset, float theta, cudaStream_t st);
+                         int64_t pos_offset, float theta, cudaStream_t st, const void* tab = nullptr);
+void rope_table(void* tab, int64_t npos, int d, float theta, cudaStream_t st);
 extern int g_rope_fused;  // engine.cu: 1 (default) fuse RoPE into K1 / K2 when P > 1
 void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
-                bool inverse, cudaStream_t st);
+                bool inverse, cudaStream_t st, const void* tab = nullptr);
 void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st);
 // W(bf16) -= lr * G(fp32)
 void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st);

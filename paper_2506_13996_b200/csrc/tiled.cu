@@ -155,6 +155,20 @@ spt_status spt_reshard_pack(const void* src, int64_t s_loc, int32_t heads_in, in
                             int32_t heads_out, const int32_t* head_map, void* dst, void* stream) {
     return capi_guard([&] { reshard_pack(src, s_loc, heads_in, head_dim, P, heads_out, head_map, dst, ST); });
 }
+spt_status spt_reshard_pack_rope(const void* src, int64_t s_loc, int32_t heads_in, int32_t head_dim, int32_t P,
+                                 int32_t heads_out, const int32_t* head_map, void* dst, int32_t n_rot,
+                                 const int64_t* position_ids, int64_t pos_offset, float theta,
+                                 const void* cos_sin_table, void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(theta > 0.f, SPT_ERR_CONFIG, "rope: theta must be > 0");
+        SPT_CHECK(reshard_pack_rope(src, s_loc, heads_in, head_dim, P, heads_out, head_map, dst, n_rot, position_ids,
+                                    pos_offset, theta, ST, cos_sin_table),
+                  SPT_ERR_SHAPE, "reshard_pack_rope: head_dim must be 32, 64 or 128 and the head map fit in smem");
+    });
+}
+spt_status spt_rope_table(void* cos_sin_table, int64_t npos, int32_t head_dim, float theta, void* stream) {
+    return capi_guard([&] { rope_table(cos_sin_table, npos, head_dim, theta, ST); });
+}
 spt_status spt_reshard_unpack(const void* recv, int64_t s_loc, int32_t heads_in, int32_t head_dim, int32_t P,
                               int32_t heads_out, const int32_t* gather, int32_t max_src, void* dst, void* stream) {
     return capi_guard([&] { reshard_unpack(recv, s_loc, heads_in, head_dim, P, heads_out, gather, max_src, dst, ST); });

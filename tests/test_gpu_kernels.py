@@ -515,3 +515,40 @@ def test_attention_fwd_packed_hybrid():
     for o_, lse_ in outs:
         assert rel_err(o_, o_r) < 1e-2
         assert np.max(np.abs(lse_ - lse_r)) < 2e-3
+
+
+@pytest.mark.parametrize("P,hq,hkv,d,packed", [(4, 8, 2, 128, False), (2, 4, 1, 64, True), (8, 8, 2, 32, False)])
+def test_reshard_pack_rope_bitwise(P, hq, hkv, d, packed):
+    """K1 with RoPE fused == in-place spt_rope then the plain K1 pack, bit for bit (row f4)."""
+    T = torch()
+    L = _lib()
+    s_loc = 384
+    plan = S.plan_head_shards(hq, hkv, P)
+    heads_in = hq + 2 * hkv
+    heads_out = plan.q_heads_per_rank + 2 * plan.kv_heads_per_rank
+    hm = []
+    for r in range(P):
+        kv = S.heads_of(plan, r, 1)
+        hm += list(S.heads_of(plan, r, 0)) + [hq + k for k in kv] + [hq + hkv + k for k in kv]
+    head_map = T.tensor(hm, dtype=T.int32, device="cuda")
+    g = T.Generator(device="cuda").manual_seed(P + d)
+    x = T.randn(s_loc, heads_in, d, device="cuda", generator=g).bfloat16()
+    pos = None
+    if packed:
+        pos = T.cat([T.arange(200), T.arange(s_loc - 200)]).to("cuda")
+    a = T.empty(P, s_loc, heads_out, d, device="cuda", dtype=T.bfloat16)
+    b = T.empty_like(a)
+    S.check(L.spt_reshard_pack_rope(x.data_ptr(), s_loc, heads_in, d, P, heads_out, head_map.data_ptr(), a.data_ptr(),
+                                    hq + hkv, S.ptr(pos), 1000, 10000.0, None, None))
+    tab = T.empty(1000 + s_loc, d // 2, 2, device="cuda")  # the angle table gives the same bits
+    S.check(L.spt_rope_table(tab.data_ptr(), 1000 + s_loc, d, 10000.0, None))
+    c = T.empty_like(a)
+    S.check(L.spt_reshard_pack_rope(x.data_ptr(), s_loc, heads_in, d, P, heads_out, head_map.data_ptr(), c.data_ptr(),
+                                    hq + hkv, S.ptr(pos), 1000, 10000.0, tab.data_ptr(), None))
+    xr = x.clone()
+    S.check(L.spt_rope(xr.data_ptr(), s_loc, heads_in, hq + hkv, d, S.ptr(pos), 1000, 10000.0, 0, None))
+    S.check(L.spt_reshard_pack(xr.data_ptr(), s_loc, heads_in, d, P, heads_out, head_map.data_ptr(), b.data_ptr(),
+                               None))
+    T.cuda.synchronize()
+    assert T.equal(a.view(T.int16), b.view(T.int16))
+    assert T.equal(a.view(T.int16), c.view(T.int16))
