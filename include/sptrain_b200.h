@@ -275,6 +275,13 @@ spt_status spt_layer_loss_slot(spt_layer* layer, int32_t slot, float* loss_out, 
  * the loss SUM (first_micro_step = 1 starts a new window); finish all-reduces the accumulated grads over the
  * SP group, divides them by the window's global valid count, applies the update (lr > 0) and returns the
  * window's mean loss and count.  Pair with sp_over_dp iteration. */
+/* CUDA graph of one step with DEVICE inputs at fixed addresses (their contents may change between replays):
+ * capture runs one eager step, then records the next into a graph on `stream` (non-default, profiling off);
+ * launch replays it (the ~100 kernels of a step without per-launch host work).  Read results as after
+ * spt_layer_step_async. */
+spt_status spt_layer_graph_capture(spt_layer* layer, const void* x, const int64_t* shift_labels,
+                                   const int64_t* position_ids, void* stream);
+spt_status spt_layer_graph_launch(spt_layer* layer, void* stream);
 spt_status spt_layer_step_accumulate(spt_layer* layer, const void* x, const int64_t* shift_labels,
                                      const int64_t* position_ids, int32_t inputs_on_host, int32_t first_micro_step,
                                      void* stream);

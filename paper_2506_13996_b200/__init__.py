@@ -78,6 +78,8 @@ SIGNATURES = {
     "spt_rmsnorm_bwd_workspace": (SZ, [I64, I64]),
     "spt_rmsnorm_bwd": (I32, [P, P, P, P, P, P, P, P, I64, I64, P]),
     "spt_reshard_pack": (I32, [P, I64, I32, I32, I32, I32, P, P, P]),
+    "spt_layer_graph_capture": (I32, [P, P, P, P, P]),
+    "spt_layer_graph_launch": (I32, [P, P]),
     "spt_reshard_pack_rope": (I32, [P, I64, I32, I32, I32, I32, P, P, I32, P, I64, F32, P, P]),
     "spt_rope_table": (I32, [P, I64, I32, F32, P]),
     "spt_reshard_unpack": (I32, [P, I64, I32, I32, I32, I32, P, I32, P, P]),
@@ -403,6 +405,14 @@ class UlyssesLayerStep:
     def step_async(self, x, shift_labels, position_ids=None, on_host=False, stream=None):
         check(lib().spt_layer_step_async(self.handle, ptr(x), ptr(shift_labels), ptr(position_ids), int(on_host),
                                          ptr(stream)))
+
+    def graph_capture(self, x, shift_labels, position_ids=None, stream=None):
+        """Capture one device-resident step (fixed input addresses) into a CUDA graph on `stream` (non-default)."""
+        check(lib().spt_layer_graph_capture(self.handle, ptr(x), ptr(shift_labels), ptr(position_ids), ptr(stream)))
+
+    def graph_launch(self, stream=None):
+        """Replay the captured step (same effect as step_async with the captured inputs)."""
+        check(lib().spt_layer_graph_launch(self.handle, ptr(stream)))
 
     def step_accumulate(self, x, shift_labels, position_ids=None, first: bool = False, on_host: bool | None = None,
                         stream=None):

@@ -227,6 +227,8 @@ struct spt_layer {
     Window* win;
     cudaEvent_t ev_step0, ev_step1;
     float last_step_ms = 0.f;
+    cudaGraphExec_t graph_exec = nullptr;  // spt_layer_graph_capture: one device-resident step
+    int64_t graph_kernels = 0;             // kernel nodes per replay (launch accounting)
 
     bf16* abf(int64_t n, int tag = kWorkspace) { return (bf16*)led.alloc((size_t)n * 2, tag); }
     float* af32(int64_t n, int tag = kWorkspace) { return (float*)led.alloc((size_t)n * 4, tag); }
@@ -868,6 +870,7 @@ spt_status spt_layer_destroy(spt_layer* Ly) {
     return capi_guard([&] {
         if (!Ly) return;
         cudaDeviceSynchronize();
+        if (Ly->graph_exec) cudaGraphExecDestroy(Ly->graph_exec);
         Ly->led.release_all();
         if (Ly->sc_host) cudaFreeHost(Ly->sc_host);
         for (auto e : Ly->prof.pool) cudaEventDestroy(e);
@@ -913,6 +916,47 @@ spt_status spt_layer_step_async(spt_layer* Ly, const void* x, const int64_t* shi
     return capi_guard([&] {
         SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
         layer_step(Ly, x, shift_labels, position_ids, inputs_on_host != 0, (cudaStream_t)stream);
+    });
+}
+
+// CUDA graph of one full step with device-resident inputs (fixed pointers; contents may change between
+// replays): the ~100 launches of a step replay without per-launch host overhead or inter-kernel gaps.
+// Capture on a non-default stream with profiling off; tuning switches are read at capture time.
+spt_status spt_layer_graph_capture(spt_layer* Ly, const void* x, const int64_t* shift_labels,
+                                   const int64_t* position_ids, void* stream) {
+    return capi_guard([&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        SPT_CHECK(st != nullptr, SPT_ERR_CONFIG, "graph capture needs a non-default stream");
+        SPT_CHECK(!Ly->prof.on, SPT_ERR_CONFIG, "graph capture needs profiling off");
+        SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
+        // one eager step first: first-use setup (kernel attributes, lazily created buffers) stays out of the graph
+        layer_step(Ly, x, shift_labels, position_ids, false, st);
+        SPT_CUDA(cudaStreamSynchronize(st));
+        cudaGraph_t g = nullptr;
+        SPT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const int64_t n0 = launch_count();
+        try {
+            layer_step(Ly, x, shift_labels, position_ids, false, st);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        SPT_CUDA(cudaStreamEndCapture(st, &g));
+        if (Ly->graph_exec) cudaGraphExecDestroy(Ly->graph_exec);
+        Ly->graph_exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&Ly->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        SPT_CUDA(e);
+        Ly->graph_kernels = launch_count() - n0;
+    });
+}
+
+spt_status spt_layer_graph_launch(spt_layer* Ly, void* stream) {
+    return capi_guard([&] {
+        SPT_CHECK(Ly->graph_exec != nullptr, SPT_ERR_CONFIG, "no captured step (spt_layer_graph_capture)");
+        SPT_CUDA(cudaGraphLaunch(Ly->graph_exec, (cudaStream_t)stream));
+        add_launches(Ly->graph_kernels);
     });
 }
 

@@ -18,6 +18,7 @@ struct GemmOperand {
 
 void count_launch(const char* tag = nullptr);
 int64_t launch_count();
+void add_launches(int64_t n);  // kernels replayed inside a CUDA graph
 
 // 3-D fp32 tensor map (no swizzle): dims {d0, d1, d2} innermost first, byte strides of dims 1 and 2.
 CUtensorMap make_tmap_f32_3d(const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,

@@ -32,6 +32,7 @@ void count_launch(const char* tag) {
     }
 }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 struct Prof;
 Prof*& current_prof() {

@@ -291,3 +291,36 @@ def test_embedding_grad_accumulation_window(P):
     for name, got in (("emb", g_emb), ("wqkv", g_wqkv)):
         ref_g = sum(r.grads[name] * r.count for r in refs) / tot
         assert rel_err(got, ref_g) <= GRAD_TOL, name
+
+
+def test_graph_replay_matches_eager():
+    """A CUDA-graph replay of the step (spt_layer_graph_capture / _launch) gives the eager step's loss and grads
+    bit for bit, and follows new input contents at the captured addresses."""
+    import torch
+
+    L_, P, N = 2, 2, 1024
+    eng, grp, _ = _engine(L_, P, N)
+    try:
+        xs, labs = [], []
+        for seed in (31, 32):
+            x, lab, _ = O.synth_batch(CFG, N, seed)
+            xs.append(torch.from_numpy(O.f32_to_bf16_bits(x).view(np.int16)).cuda().view(torch.bfloat16))
+            labs.append(torch.from_numpy(lab).cuda())
+        xd, ld = xs[0].clone(), labs[0].clone()
+        st = torch.cuda.Stream()
+        eager = []
+        for i in range(2):
+            eng.step_async(xs[i], labs[i], None, on_host=False, stream=st.cuda_stream)
+            eager.append((eng.read_loss(stream=st.cuda_stream), eng.grad("layers.1.wd"), eng.grad("wlm")))
+        eng.graph_capture(xd, ld, None, stream=st.cuda_stream)
+        for i in range(2):
+            xd.copy_(xs[i])
+            ld.copy_(labs[i])
+            torch.cuda.synchronize()
+            eng.graph_launch(stream=st.cuda_stream)
+            got = (eng.read_loss(stream=st.cuda_stream), eng.grad("layers.1.wd"), eng.grad("wlm"))
+            assert got[0] == eager[i][0]
+            assert np.array_equal(got[1], eager[i][1]) and np.array_equal(got[2], eager[i][2])
+    finally:
+        eng.close()
+        grp.close()
