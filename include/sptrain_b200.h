@@ -210,15 +210,68 @@ spt_status spt_mlp_bwd(const void* x, const void* wgu, const void* wd, const voi
 
 /* ===================================== communicator ===================================== */
 
-/* ProcessGroup over NCCL (one process per GPU) or a loopback group of P virtual
- * ranks on one GPU (the in-process SPMD of SPEC.md:183, with device-to-device copies). */
+/* ProcessGroup.  Three transports (spt_comm_world reports which):
+ *   0 loopback: P virtual ranks on one GPU driven by one host thread (the in-process SPMD of SPEC.md:183);
+ *   1 NCCL:     one process per GPU, grouped ncclSend/ncclRecv + ncclAllReduce (the library baseline);
+ *   2 peer:     one process (or thread) per GPU, buffers mapped into every peer over NVLink/NVSwitch (CUDA
+ *               IPC): the Ulysses pack/unpack kernels store into / load from the peers' buffers themselves,
+ *               ordered by device-side barriers; all-reduce sums in ascending rank order.
+ * Collectives are stream-ordered.  A barrier that waits longer than the group's timeout (default 300 s,
+ * spt_comm_set_timeout_ms) flags the group; the next host read (spt_layer_step / read_loss / spt_comm_check /
+ * spt_comm_wait) then fails with SPT_ERR_PROTOCOL (a dead or stalled rank), and an NCCL step
+ * that does not finish within the deadline aborts the communicator with SPT_ERR_PROTOCOL. */
 typedef struct spt_comm spt_comm;
 spt_status spt_comm_unique_id(uint8_t out_id[128]);
 spt_status spt_comm_init_rank(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, spt_comm** out);
 spt_status spt_comm_init_loopback(int32_t nranks, int32_t device, spt_comm** out);
+/* Peer group bootstrap: `exchange` all-gathers `bytes` from every rank into out[nranks * bytes] in rank order
+ * (torch.distributed, MPI, a TCP store, or threads of one process) and returns 0 on success.  It is called
+ * collectively by spt_comm_init_peer, spt_comm_connect and spt_layer_create (which map the symmetric
+ * allocations made since the previous call). */
+typedef int32_t (*spt_allgather_fn)(const void* in, void* out, size_t bytes, void* user);
+spt_status spt_comm_init_peer(int32_t nranks, int32_t rank, int32_t device, spt_allgather_fn exchange, void* user,
+                              spt_comm** out);
+spt_status spt_comm_set_timeout_ms(spt_comm* comm, int64_t ms);
+spt_status spt_comm_world(spt_comm* comm, int32_t* nranks, int32_t* rank, int32_t* transport);
+/* SPT_ERR_PROTOCOL if a barrier of this group timed out (no sync). */
+spt_status spt_comm_check(spt_comm* comm);
+/* Wait for `stream` with the group's deadline (the host watchdog); SPT_ERR_PROTOCOL on expiry or timeout. */
+spt_status spt_comm_wait(spt_comm* comm, void* stream);
+/* Communication buffer: peer mode a symmetric allocation (every rank must make the same calls in the same
+ * order, then spt_comm_connect), otherwise plain device memory.  Zero-filled. */
+spt_status spt_comm_alloc(spt_comm* comm, size_t bytes, void** out);
+spt_status spt_comm_free(spt_comm* comm, void* ptr);
+spt_status spt_comm_connect(spt_comm* comm);
+spt_status spt_comm_barrier(spt_comm* comm, void* stream);
 spt_status spt_comm_destroy(spt_comm* comm);
 /* CommStats as JSON: per collective call count and bytes sent per rank. */
 spt_status spt_comm_stats_json(spt_comm* comm, char* buf, size_t cap);
+
+/* SPEC.md:155-163 all_reduce_sum, in place.  bufs: one buffer per LOCAL rank (loopback: every virtual rank's,
+ * summed in rank order into all of them; NCCL / peer: bufs[0], from spt_comm_alloc in peer mode). */
+spt_status spt_all_reduce_f32(spt_comm* comm, void* const* bufs, int64_t n, void* stream);
+spt_status spt_all_reduce_f64(spt_comm* comm, void* const* bufs, int64_t n, void* stream);
+spt_status spt_all_reduce_i64(spt_comm* comm, void* const* bufs, int64_t n, void* stream);
+/* SPEC.md:145-153 all_to_all: recv[j] on rank i = send[i] from rank j, bytes_per_peer each; one [P][bytes]
+ * buffer per local rank (peer mode: send from spt_comm_alloc). */
+spt_status spt_all_to_all(spt_comm* comm, const void* const* send, void* const* recv, size_t bytes_per_peer,
+                          void* stream);
+
+/* SPEC.md:307-315 seq_to_head (K1 with the all-to-all fused) for one layer's projections.
+ * kind 0: x = fused qkv [s_loc][Hq + 2 Hkv][d] -> out [s][q_loc + 2 kv_loc][d] (replicate_kv: repeated kv head);
+ * kind 1: x = q-shaped [s_loc][Hq][d] (dO) -> out [s][q_loc][d].
+ * x / out: one pointer per LOCAL rank.  Peer mode: out from spt_comm_alloc (the peers store into it).  NCCL:
+ * scratch = spt_reshard_scratch_bytes staging bytes, else NULL. */
+size_t spt_reshard_scratch_bytes(const spt_head_shard_plan* plan, int32_t kind, int64_t s_loc, int32_t head_dim);
+spt_status spt_seq_to_head(spt_comm* comm, const spt_head_shard_plan* plan, int32_t kind, const void* const* x,
+                           int64_t s_loc, int32_t head_dim, void* const* out, void* scratch, void* stream);
+/* SPEC.md:317-326 head_to_seq (K2 with the all-to-all fused), the exact inverse.
+ * kind 0: x = o_head [s][q_loc][d] -> out [s_loc][Hq][d];
+ * kind 1: x = dqkv_head [s][q_loc + 2 kv_loc][d] -> out [s_loc][Hq + 2 Hkv][d] with the replicas of a kv head
+ *         summed in fp32 in rank order (replicate_kv backward).
+ * Peer mode: x from spt_comm_alloc (the peers load from it). */
+spt_status spt_head_to_seq(spt_comm* comm, const spt_head_shard_plan* plan, int32_t kind, const void* const* x,
+                           int64_t s_loc, int32_t head_dim, void* const* out, void* scratch, void* stream);
 
 /* ================================= layer step engine ================================= */
 

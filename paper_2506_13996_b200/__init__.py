@@ -39,7 +39,24 @@ class ConfigError(SptError):
     """errors.hpp:68"""
 
 
-_EXC = {1: ShapeError, 2: ValidationError, 7: ConfigError}
+class CollectiveError(SptError):
+    """errors.hpp:24-28: a collective saw incompatible payloads across ranks"""
+
+
+class ProtocolError(CollectiveError):
+    """errors.hpp:30-34: ranks diverged from lock-step collective order, or a rank died / timed out"""
+
+
+class OomError(SptError, MemoryError):
+    """errors.hpp:55-65 SimulatedOomError (ledger budget) or a device allocation failure"""
+
+
+class DeterminismError(SptError):
+    """errors.hpp:36-40: a replayed region produced values different from its recorded forward"""
+
+
+_EXC = {1: ShapeError, 2: ValidationError, 3: CollectiveError, 4: ProtocolError, 5: OomError, 7: ConfigError,
+        8: DeterminismError}
 
 _lib = None
 
@@ -108,6 +125,22 @@ SIGNATURES = {
     "spt_comm_init_rank": (I32, [P, I32, I32, I32, C.POINTER(P)]),
     "spt_comm_init_loopback": (I32, [I32, I32, C.POINTER(P)]),
     "spt_comm_destroy": (I32, [P]),
+    "spt_comm_init_peer": (I32, [I32, I32, I32, P, P, C.POINTER(P)]),
+    "spt_comm_set_timeout_ms": (I32, [P, I64]),
+    "spt_comm_world": (I32, [P, PI32, PI32, PI32]),
+    "spt_comm_check": (I32, [P]),
+    "spt_comm_wait": (I32, [P, P]),
+    "spt_comm_alloc": (I32, [P, SZ, C.POINTER(P)]),
+    "spt_comm_free": (I32, [P, P]),
+    "spt_comm_connect": (I32, [P]),
+    "spt_comm_barrier": (I32, [P, P]),
+    "spt_all_reduce_f32": (I32, [P, C.POINTER(P), I64, P]),
+    "spt_all_reduce_f64": (I32, [P, C.POINTER(P), I64, P]),
+    "spt_all_reduce_i64": (I32, [P, C.POINTER(P), I64, P]),
+    "spt_all_to_all": (I32, [P, C.POINTER(P), C.POINTER(P), SZ, P]),
+    "spt_reshard_scratch_bytes": (SZ, [C.POINTER(HeadShardPlan), I32, I64, I32]),
+    "spt_seq_to_head": (I32, [P, C.POINTER(HeadShardPlan), I32, C.POINTER(P), I64, I32, C.POINTER(P), P, P]),
+    "spt_head_to_seq": (I32, [P, C.POINTER(HeadShardPlan), I32, C.POINTER(P), I64, I32, C.POINTER(P), P, P]),
     "spt_comm_stats_json": (I32, [P, C.c_char_p, SZ]),
     "spt_layer_create": (I32, [C.POINTER(LayerConfig), P, C.POINTER(P)]),
     "spt_layer_destroy": (I32, [P]),
@@ -322,11 +355,114 @@ def a2a_counts(plan: HeadShardPlan, s_loc: int, head_dim: int, direction: int):
 
 
 # ----------------------------------------------------------------- process group + layer engine
-class ProcessGroup:
-    """SPEC.md:131-136 over NCCL (one process per GPU) or loopback virtual ranks on one GPU."""
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+TRANSPORTS = {0: "loopback", 1: "nccl", 2: "peer"}
 
-    def __init__(self, handle, world_size: int, rank: int, loopback: bool):
+
+def _torch_allgather(group=None):
+    """spt_allgather_fn over torch.distributed (any backend): every rank's `bytes` into out, rank order."""
+
+    def fn(inp, out, nbytes, _user):
+        try:
+            import torch.distributed as dist
+
+            mine = C.string_at(inp, nbytes)
+            objs = [None] * dist.get_world_size(group)
+            dist.all_gather_object(objs, mine, group=group)
+            for r, b in enumerate(objs):
+                if len(b) != nbytes:
+                    return 2
+                C.memmove(out + r * nbytes, b, nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 - the C side turns a non-zero return into CollectiveError
+            return 1
+
+    return ALLGATHER_FN(fn)
+
+
+class ProcessGroup:
+    """loopback virtual ranks on one GPU, NCCL (one process per GPU), or the peer-memory
+    transport (one process or thread per GPU; buffers mapped over NVLink, fused reshard collectives)."""
+
+    def __init__(self, handle, world_size: int, rank: int, loopback: bool, keep=None):
         self.handle, self.world_size, self.rank, self.loopback = handle, world_size, rank, loopback
+        self._keep = keep  # the exchange callback must outlive the group
+
+    @property
+    def transport(self) -> str:
+        t = C.c_int32()
+        check(lib().spt_comm_world(self.handle, None, None, C.byref(t)))
+        return TRANSPORTS[t.value]
+
+    @classmethod
+    def peer_group(cls, world_size: int, rank: int, device: int, exchange=None, group=None,
+                   timeout_ms: int | None = None) -> "ProcessGroup":
+        """Peer-memory group; `exchange(bytes) -> list[bytes]` all-gathers the handle blobs (default:
+        torch.distributed.all_gather_object over `group`, which must be initialised)."""
+        if exchange is None:
+            cb = _torch_allgather(group)
+        else:
+            def fn(inp, out, nbytes, _user):
+                try:
+                    blobs = exchange(C.string_at(inp, nbytes))
+                    for r, b in enumerate(blobs):
+                        C.memmove(out + r * nbytes, b, nbytes)
+                    return 0
+                except Exception:  # noqa: BLE001
+                    return 1
+            cb = ALLGATHER_FN(fn)
+        h = C.c_void_p()
+        check(lib().spt_comm_init_peer(world_size, rank, device, C.cast(cb, C.c_void_p), None, C.byref(h)))
+        g = cls(h, world_size, rank, False, keep=cb)
+        if timeout_ms is not None:
+            g.set_timeout_ms(timeout_ms)
+        return g
+
+    def set_timeout_ms(self, ms: int):
+        check(lib().spt_comm_set_timeout_ms(self.handle, int(ms)))
+
+    def check(self):
+        check(lib().spt_comm_check(self.handle))
+
+    def wait(self, stream=None):
+        check(lib().spt_comm_wait(self.handle, ptr(stream)))
+
+    def barrier(self, stream=None):
+        check(lib().spt_comm_barrier(self.handle, ptr(stream)))
+
+    def alloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        check(lib().spt_comm_alloc(self.handle, nbytes, C.byref(p)))
+        return p.value
+
+    def free(self, p: int):
+        check(lib().spt_comm_free(self.handle, p))
+
+    def connect(self):
+        check(lib().spt_comm_connect(self.handle))
+
+    def _ptrs(self, bufs):
+        bufs = bufs if isinstance(bufs, (list, tuple)) else [bufs]
+        return (C.c_void_p * len(bufs))(*[ptr(b) for b in bufs])
+
+    def all_reduce(self, bufs, n: int, dtype: str = "f32", stream=None):
+        """SPEC.md:155-163 in place; bufs: one per local rank (peer: from alloc())."""
+        f = {"f32": lib().spt_all_reduce_f32, "f64": lib().spt_all_reduce_f64, "i64": lib().spt_all_reduce_i64}[dtype]
+        check(f(self.handle, self._ptrs(bufs), n, ptr(stream)))
+
+    def all_to_all(self, send, recv, bytes_per_peer: int, stream=None):
+        """SPEC.md:145-153"""
+        check(lib().spt_all_to_all(self.handle, self._ptrs(send), self._ptrs(recv), bytes_per_peer, ptr(stream)))
+
+    def seq_to_head(self, plan, kind: int, x, s_loc: int, head_dim: int, out, scratch=None, stream=None):
+        """SPEC.md:307-315 (K1 with the all-to-all fused)"""
+        check(lib().spt_seq_to_head(self.handle, C.byref(plan), kind, self._ptrs(x), s_loc, head_dim, self._ptrs(out),
+                                    ptr(scratch), ptr(stream)))
+
+    def head_to_seq(self, plan, kind: int, x, s_loc: int, head_dim: int, out, scratch=None, stream=None):
+        """SPEC.md:317-326 (K2 with the all-to-all fused; kind 1 sums kv replicas in rank order)"""
+        check(lib().spt_head_to_seq(self.handle, C.byref(plan), kind, self._ptrs(x), s_loc, head_dim, self._ptrs(out),
+                                    ptr(scratch), ptr(stream)))
 
     @classmethod
     def loopback_group(cls, world_size: int, device: int = 0) -> "ProcessGroup":

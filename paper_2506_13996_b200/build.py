@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import concurrent.futures as cf
+import hashlib
 import os
 import shutil
 import subprocess
@@ -10,14 +11,19 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
+
 LIB = os.path.join(HERE, "libsptrain_b200.so")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = (["-DSPT_WATCHDOG"] if os.environ.get("SPT_WATCHDOG") else []) + \
         [f"-D{x}" for x in os.environ.get("SPT_EXTRA_DEFS", "").split(",") if x] + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I/usr/include"]
-SOURCES = ["util.cpp", "plan.cpp", "memest.cpp", "comm.cpp", "gemm.cu", "kernels.cu", "attention.cu", "attention_tc.cu", "tiled.cu", "embed.cu", "engine.cu"]
+SOURCES = ["util.cpp", "plan.cpp", "memest.cpp", "comm.cpp", "peer.cu", "ulysses.cpp", "gemm.cu", "kernels.cu",
+           "attention.cu", "attention_tc.cu", "tiled.cu", "embed.cu", "engine.cu"]
+# Objects live in a directory keyed by the compile flags, so a build with different -D switches (the A/B
+# scripts' SPT_EXTRA_DEFS, SPT_WATCHDOG) never reuses objects of another configuration.
+FLAG_KEY = hashlib.sha1(" ".join(ARCH + FLAGS).encode()).hexdigest()[:10]
+OBJ = os.path.join(HERE, "_build", FLAG_KEY)
 DEPS_HDR = [f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + ["../../include/sptrain_b200.h"]
 
 
@@ -45,11 +51,15 @@ def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+    stamp = LIB + ".flags"
+    same_flags = os.path.exists(stamp) and open(stamp).read() == FLAG_KEY
+    if not same_flags or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        with open(stamp, "w") as f:
+            f.write(FLAG_KEY)
     return LIB
 
 

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <unordered_map>
@@ -64,15 +65,23 @@ struct DeviceLedger {
     uint64_t tag_live[kNumTags] = {}, tag_peak[kNumTags] = {}, largest[kNumTags] = {};
     uint64_t events = 0;
     std::unordered_map<void*, std::pair<int, size_t>> allocs;
+    spt_comm* sym_comm = nullptr;  // peer mode: allocations made with alloc_sym are symmetric (comm.h)
+    std::unordered_map<void*, char> sym_allocs;
 
-    void* alloc(size_t bytes, int tag) {
+    // symmetric == true: a peer-group allocation, mapped into every rank (same call order on every rank)
+    void* alloc(size_t bytes, int tag, bool symmetric = false) {
         if (budget && live + bytes > budget)
             SPT_THROW(SPT_ERR_OOM, "simulated device OOM: required " + std::to_string(live + bytes) +
                                        " bytes, available " + std::to_string(budget));
         void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
-        if (e != cudaSuccess)
-            SPT_THROW(SPT_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+        if (symmetric && sym_comm) {
+            p = sym_comm->sym_alloc(bytes);
+            sym_allocs[p] = 1;
+        } else {
+            cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+            if (e != cudaSuccess)
+                SPT_THROW(SPT_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+        }
         live += bytes;
         peak = std::max(peak, live);
         tag_live[tag] += bytes;
@@ -87,7 +96,13 @@ struct DeviceLedger {
         if (it == allocs.end()) return;
         live -= it->second.second;
         tag_live[it->second.first] -= it->second.second;
-        cudaFree(p);
+        auto si = sym_allocs.find(p);
+        if (si != sym_allocs.end()) {
+            sym_comm->sym_free(p);
+            sym_allocs.erase(si);
+        } else {
+            cudaFree(p);
+        }
         allocs.erase(it);
         ++events;
     }
@@ -158,6 +173,7 @@ struct Scalars {
     int32_t err_label;
     int32_t err_pos;
     int32_t err_embed;
+    int32_t err_rope;  // a RoPE position outside [0, seq_len) (packed chunk whose ids run past the table)
 };
 // Gradient-accumulation window ("divide by global valid_count summed over the accumulation
 // window"): micro-steps accumulate grads of the loss SUM; finish divides by the window's global count.
@@ -229,9 +245,10 @@ struct spt_layer {
     float last_step_ms = 0.f;
     cudaGraphExec_t graph_exec = nullptr;  // spt_layer_graph_capture: one device-resident step
     int64_t graph_kernels = 0;             // kernel nodes per replay (launch accounting)
+    std::map<std::string, spt_comm::Stat> graph_comm;  // collectives per replay (CommStats accounting)
 
-    bf16* abf(int64_t n, int tag = kWorkspace) { return (bf16*)led.alloc((size_t)n * 2, tag); }
-    float* af32(int64_t n, int tag = kWorkspace) { return (float*)led.alloc((size_t)n * 4, tag); }
+    bf16* abf(int64_t n, int tag = kWorkspace, bool sym = false) { return (bf16*)led.alloc((size_t)n * 2, tag, sym); }
+    float* af32(int64_t n, int tag = kWorkspace, bool sym = false) { return (float*)led.alloc((size_t)n * 4, tag, sym); }
 };
 
 static void build_layer(spt_layer* Ly) {
@@ -241,6 +258,10 @@ static void build_layer(spt_layer* Ly) {
               SPT_ERR_CONFIG, "invalid layer config");
     Ly->P = cm->nranks;
     Ly->L = cm->local_ranks();
+    // peer mode: the buffers other ranks read or write (reshard receive / source buffers, grads and step
+    // scalars for the all-reduces, position ids for the all-gather) are symmetric allocations
+    const bool sym = cm->peer() && cm->nranks > 1;
+    if (sym) Ly->led.sym_comm = cm;
     Ly->plan = plan_head_shards(c.q_heads, c.kv_heads, Ly->P);
     SPT_CHECK(c.seq_len % Ly->P == 0, SPT_ERR_SHAPE,
               "seq_len " + std::to_string(c.seq_len) + " not divisible by SP degree; pad_to_multiple first");
@@ -296,7 +317,7 @@ static void build_layer(spt_layer* Ly) {
     for (int l = 0; l < Ly->NL; ++l)
         for (size_t s : lsz) tot += al(s);
     Ly->gsize = tot;
-    Ly->gbuf = Ly->af32(tot, kGrads);
+    Ly->gbuf = Ly->af32(tot, kGrads, sym);
     float* gp = Ly->gbuf;
     for (auto& w : Ly->lw) {
         float** dst[6] = {&w.dg1, &w.dwqkv, &w.dwo, &w.dg2, &w.dwgu, &w.dwd};
@@ -329,21 +350,25 @@ static void build_layer(spt_layer* Ly) {
         r.rstd3 = Ly->af32(nl);
         r.lse = Ly->af32(Ly->hq_loc * N);
         r.labels = (int64_t*)L_.alloc(nl * 8, kWorkspace);
-        r.pos = (int64_t*)L_.alloc(nl * 8, kWorkspace);
+        r.pos = (int64_t*)L_.alloc(nl * 8, kWorkspace, sym);
         r.ids = Ly->embed ? (int64_t*)L_.alloc(nl * 8, kWorkspace) : nullptr;
         r.dz = Ly->abf(nl * h);
         r.dx1 = Ly->abf(nl * h);
         r.dO = Ly->abf(nl * Ly->qd);
         r.dx = Ly->abf(nl * h);
         if (P > 1) {
-            r.send_qkv = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
-            r.qkv_head = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
-            r.o_head = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
-            r.recv_o = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
-            r.send_do = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
-            r.do_head = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer);
-            r.dqkv_head = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
-            r.recv_dqkv = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer);
+            // head-sharded buffers [N][heads_loc][d]: the seq_to_head receive buffers (q|k|v, dO) and the
+            // head_to_seq sources (O, dq|dk|dv).  Only NCCL needs the contiguous send / receive staging: the
+            // loopback and peer transports store into / load from these directly (comm.h fused_*).
+            const bool staged = cm->mode == spt_comm::kNccl;
+            r.qkv_head = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer, sym);
+            r.o_head = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer, sym);
+            r.do_head = Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer, sym);
+            r.dqkv_head = Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer, sym);
+            r.send_qkv = staged ? Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer) : nullptr;
+            r.recv_o = staged ? Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer) : nullptr;
+            r.send_do = staged ? Ly->abf(N * Ly->hq_loc * c.head_dim, kCommBuffer) : nullptr;
+            r.recv_dqkv = staged ? Ly->abf(N * Ly->qkv_loc * c.head_dim, kCommBuffer) : nullptr;
             r.dqkv = Ly->abf(nl * Ly->qkv_out);
         } else {
             r.send_qkv = r.recv_o = r.send_do = r.recv_dqkv = nullptr;
@@ -395,7 +420,7 @@ static void build_layer(spt_layer* Ly) {
     Ly->gather_qkv = up(qkv_gather_map(Ly->plan, &Ly->max_src_qkv));
     Ly->seg = c.packed ? (int32_t*)L_.alloc(N * 4, kWorkspace) : nullptr;
     Ly->pos_full = c.packed ? (int64_t*)L_.alloc(N * 8, kWorkspace) : nullptr;
-    Ly->sc = (Scalars*)L_.alloc(sizeof(Scalars), kWorkspace);
+    Ly->sc = (Scalars*)L_.alloc(sizeof(Scalars), kWorkspace, sym);
     Ly->win = (Window*)L_.alloc(sizeof(Window), kWorkspace);
     {
         const Window w0{0.0, 0, 1};
@@ -404,6 +429,7 @@ static void build_layer(spt_layer* Ly) {
     SPT_CUDA(cudaMallocHost(&Ly->sc_host, sizeof(Scalars)));
     SPT_CUDA(cudaEventCreate(&Ly->ev_step0));
     SPT_CUDA(cudaEventCreate(&Ly->ev_step1));
+    if (sym) cm->connect();  // collective: map every rank's symmetric allocations of this engine
 }
 
 static double gflop(int64_t m, int64_t n, int64_t k) { return 2.0 * (double)m * n * k; }
@@ -507,65 +533,65 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         }
     }
 
-    const size_t qkv_peer = (size_t)nl * Ly->qkv_loc * d * 2;
-    const size_t o_peer = (size_t)nl * hq * d * 2;
-    auto sends = [&](bf16* RankBufs::*m) {
-        std::vector<const void*> v;
-        for (auto& b : Ly->rb) v.push_back(b.*m);
-        return v;
-    };
-    auto recvs = [&](bf16* RankBufs::*m) {
+    const size_t qkv_row = (size_t)Ly->qkv_loc * d * 2, o_row = (size_t)hq * d * 2;  // bytes per head-sharded row
+    const double qkv_a2a = (double)nl * qkv_row * (P - 1), o_a2a = (double)nl * o_row * (P - 1);  // payload / rank
+    auto ptrs = [&](bf16* RankBufs::*m) {
         std::vector<void*> v;
         for (auto& b : Ly->rb) v.push_back(b.*m);
         return v;
     };
     const double attn_f = 4.0 * (double)N * N * hq * d / 2.0;  // causal half
+    // RoPE positions are < N (global index, or an index within a packed sample); anything else is flagged
+    const int64_t npos = N;
+    int32_t* rope_err = &Ly->sc->err_rope;
+    // K1 fused with RoPE when the rotation runs on the way into the peers' buffers (row f4)
+    const bool rope_in_pack = rope_on && P > 1 && g_rope_fused && d % 16 == 0 && (d == 32 || d == 64 || d == 128) &&
+                              (size_t)P * Ly->qkv_loc * 4 <= 48 * 1024;
 
     // ---- one decoder layer forward: b.x -> b.x2 (intermediates left in the rank buffers)
     auto layer_fwd = [&](const spt_layer::LayerW& w) {
-        for (int r = 0; r < L; ++r) {  // phase A: rms1, fused QKV projection, K1 pack
+        for (int r = 0; r < L; ++r) {  // phase A: rms1, fused QKV projection (+ RoPE in place unless fused below)
             auto& b = Ly->rb[r];
             pf.run(P_NORM, 0, 2.0 * nl * h * 2, st, [&] { rmsnorm_fwd(b.x, w.g1, b.xn1, b.rstd1, nl, h, Ly->eps, st); });
             EpiParams e;
             e.C = b.qkv;
             e.ldc = qo;
             gemm({b.xn1, h, false}, {w.wqkv, h, false}, nl, qo, h, EPI_BF16, e, st);
-            const int64_t rope_off = (int64_t)cm->global_rank(r) * nl;
-            bool rope_done = false;
-            if (rope_on && P > 1 && g_rope_fused)  // row f4: RoPE fused into the K1 pack
-                pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
-                    rope_done = reshard_pack_rope(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc,
-                                                  Ly->map_qkv, b.send_qkv, c.q_heads + c.kv_heads,
-                                                  c.packed ? b.pos : nullptr, rope_off, c.rope_theta, st, Ly->rope_tab);
-                });
-            if (rope_on && !rope_done)  // rotate q and k heads in place before the reshard / attention
+            if (rope_on && !rope_in_pack)  // rotate q and k heads in place before the reshard / attention
                 pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
                     rope_apply(b.qkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
-                               c.packed ? b.pos : nullptr, rope_off, c.rope_theta, false, st, Ly->rope_tab);
-                });
-            if (P > 1 && !rope_done)
-                pf.run(P_RESHARD, 0, 2.0 * nl * Ly->qkv_loc * P * d * 2, st, [&] {
-                    reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, b.send_qkv,
-                                 st);
+                               c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, false, st,
+                               Ly->rope_tab, npos, rope_err);
                 });
         }
-        if (P > 1)
-            pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st, [&] {
-                cm->all_to_all("all_to_all_qkv", sends(&RankBufs::send_qkv), recvs(&RankBufs::qkv_head), qkv_peer, st);
+        if (P > 1) {  // seq_to_head: K1 stores every packed row straight into its destination rank's buffer
+            pf.next_tag = "a2a_qkv";
+            pf.run(P_A2A, 0, qkv_a2a * L, st, [&] {
+                fused_seq_to_head(cm, "all_to_all_qkv", ptrs(&RankBufs::qkv_head), Ly->rb[0].send_qkv, nl,
+                                  (int64_t)qkv_row, st, [&](int r, const RowTab& t) {
+                    auto& b = Ly->rb[r];
+                    if (rope_in_pack)
+                        reshard_pack_rope(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv,
+                                          t, c.q_heads + c.kv_heads, c.packed ? b.pos : nullptr,
+                                          (int64_t)cm->global_rank(r) * nl, c.rope_theta, st, Ly->rope_tab, npos,
+                                          rope_err);
+                    else
+                        reshard_pack(b.qkv, nl, c.q_heads + 2 * c.kv_heads, d, P, (int)Ly->qkv_loc, Ly->map_qkv, t, st);
+                });
             });
+        }
         for (int r = 0; r < L; ++r) {  // attention over the full sequence, local heads
             auto& b = Ly->rb[r];
             pf.run(P_ATTN_F, attn_f, 0, st, [&] { attn_fwd(b.qkv_head, N, hq, hkv, d, Ly->seg, scale, b.o_head, b.lse, st); });
         }
-        if (P > 1) {
-            pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
-                   [&] { cm->all_to_all("all_to_all_o", sends(&RankBufs::o_head), recvs(&RankBufs::recv_o), o_peer, st); });
-            for (int r = 0; r < L; ++r) {
-                auto& b = Ly->rb[r];
-                pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st, [&] {
-                    reshard_unpack(b.recv_o, nl, hq, d, P, c.q_heads, Ly->gather_o, Ly->max_src_o, b.o, st);
+        if (P > 1) {  // head_to_seq: K2 loads every row straight from its source rank's attention output
+            pf.next_tag = "a2a_o";
+            pf.run(P_A2A, 0, o_a2a * L, st, [&] {
+                fused_head_to_seq(cm, "all_to_all_o", ptrs(&RankBufs::o_head), Ly->rb[0].recv_o, nl, (int64_t)o_row,
+                                  st, [&](int r, const RowTab& t) {
+                    reshard_unpack(t, nl, hq, d, P, c.q_heads, Ly->gather_o, Ly->max_src_o, Ly->rb[r].o, st);
                 });
-            }
+            });
         }
         for (int r = 0; r < L; ++r) {  // phase B: O projection + residual, rms2, TiledMLP + residual
             auto& b = Ly->rb[r];
@@ -581,7 +607,6 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
     };
     // ---- one decoder layer backward: dy = b.dx (d of the layer output) -> b.dx (d of the layer input)
     auto layer_bwd = [&](const spt_layer::LayerW& w) {
-        std::vector<char> dqkv_rotated(L, 0);  // inverse RoPE already applied by the fused K2 unpack
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
             const bool acc = r > 0 || gbase;  // loopback ranks share the grad buffer: rank-ascending
@@ -601,48 +626,50 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
             e2.ldc = qd;
             e2.accumulate = acc;
             gemm({b.dx1, h, true}, {b.o, qd, true}, h, qd, nl, EPI_F32, e2, st);
-            if (P > 1)
-                pf.run(P_RESHARD, 0, 2.0 * nl * qd * 2, st,
-                       [&] { reshard_pack(b.dO, nl, c.q_heads, d, P, hq, Ly->map_q, b.send_do, st); });
         }
-        if (P > 1)
-            pf.run(P_COMM, 0, (double)o_peer * (P - 1), st,
-                   [&] { cm->all_to_all("all_to_all_do", sends(&RankBufs::send_do), recvs(&RankBufs::do_head), o_peer, st); });
+        if (P > 1) {  // seq_to_head of dO (the mirror of head_to_seq of O)
+            pf.next_tag = "a2a_do";
+            pf.run(P_A2A, 0, o_a2a * L, st, [&] {
+                fused_seq_to_head(cm, "all_to_all_do", ptrs(&RankBufs::do_head), Ly->rb[0].send_do, nl,
+                                  (int64_t)o_row, st, [&](int r, const RowTab& t) {
+                    reshard_pack(Ly->rb[r].dO, nl, c.q_heads, d, P, hq, Ly->map_q, t, st);
+                });
+            });
+        }
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
             pf.run(P_ATTN_B, attn_f * 2.5, 0, st, [&] {
                 attn_bwd(b.qkv_head, b.o_head, b.lse, b.do_head, N, hq, hkv, d, Ly->seg, scale, b.dqkv_head, Ly->ws_attn, st);
             });
         }
-        if (P > 1) {
-            pf.run(P_COMM, 0, (double)qkv_peer * (P - 1), st, [&] {
-                cm->all_to_all("all_to_all_dqkv", sends(&RankBufs::dqkv_head), recvs(&RankBufs::recv_dqkv), qkv_peer, st);
-            });
-            for (int r = 0; r < L; ++r) {
-                auto& b = Ly->rb[r];
-                pf.run(P_RESHARD, 0, 2.0 * nl * qo * 2, st, [&] {
-                    if (rope_on && g_rope_fused &&  // row f4: inverse RoPE fused into the K2 unpack
-                        reshard_unpack_rope(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, c.q_heads + 2 * c.kv_heads,
-                                            Ly->gather_qkv, Ly->max_src_qkv, b.dqkv, c.q_heads + c.kv_heads,
-                                            c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl,
-                                            c.rope_theta, st, Ly->rope_tab)) {
-                        dqkv_rotated[r] = 1;
-                        return;
-                    }
-                    reshard_unpack(b.recv_dqkv, nl, (int)Ly->qkv_loc, d, P, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
-                                   Ly->max_src_qkv, b.dqkv, st);
+        bool dqkv_rotated = false;  // inverse RoPE already applied by the fused K2 unpack
+        if (P > 1) {  // head_to_seq of d(q|k|v), replicas of a kv head summed in fp32 rank order
+            dqkv_rotated = rope_in_pack;
+            pf.next_tag = "a2a_dqkv";
+            pf.run(P_A2A, 0, qkv_a2a * L, st, [&] {
+                fused_head_to_seq(cm, "all_to_all_dqkv", ptrs(&RankBufs::dqkv_head), Ly->rb[0].recv_dqkv, nl,
+                                  (int64_t)qkv_row, st, [&](int r, const RowTab& t) {
+                    auto& b = Ly->rb[r];
+                    if (rope_in_pack)  // row f4: inverse RoPE fused into the K2 unpack
+                        reshard_unpack_rope(t, nl, (int)Ly->qkv_loc, d, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
+                                            Ly->max_src_qkv, b.dqkv, c.q_heads + c.kv_heads, c.packed ? b.pos : nullptr,
+                                            (int64_t)cm->global_rank(r) * nl, c.rope_theta, st, Ly->rope_tab, npos,
+                                            rope_err);
+                    else
+                        reshard_unpack(t, nl, (int)Ly->qkv_loc, d, P, c.q_heads + 2 * c.kv_heads, Ly->gather_qkv,
+                                       Ly->max_src_qkv, b.dqkv, st);
                 });
-            }
+            });
         }
         for (int r = 0; r < L; ++r) {
             auto& b = Ly->rb[r];
             const bool acc = r > 0 || gbase;
             bf16* dxn1 = b.dz;
-            if (rope_on && !dqkv_rotated[r])  // d(q, k) through the rotation's transpose, before the projection's backward
+            if (rope_on && !dqkv_rotated)  // d(q, k) through the rotation's transpose, before the projection's backward
                 pf.run(P_OTHER, 0, 2.0 * nl * (c.q_heads + c.kv_heads) * d * 2, st, [&] {
                     rope_apply(b.dqkv, nl, c.q_heads + 2 * c.kv_heads, c.q_heads + c.kv_heads, d,
                                c.packed ? b.pos : nullptr, (int64_t)cm->global_rank(r) * nl, c.rope_theta, true, st,
-                               Ly->rope_tab);
+                               Ly->rope_tab, npos, rope_err);
                 });
             EpiParams e1;
             e1.C = dxn1;
@@ -781,11 +808,11 @@ static void apply_update(spt_layer* Ly, cudaStream_t st) {
 
 static void read_scalars(spt_layer* Ly, cudaStream_t st, float* loss, int64_t* count) {
     SPT_CUDA(cudaMemcpyAsync(Ly->sc_host, Ly->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
-    SPT_CUDA(cudaStreamSynchronize(st));
-    Ly->comm->check_async();
+    Ly->comm->wait_stream(st);  // host watchdog: a stalled collective -> ProtocolError, not a hang
     SPT_CHECK(Ly->sc_host->err_label == 0, SPT_ERR_VALIDATION, "label out of range [0, vocab) and != -100");
     SPT_CHECK(Ly->sc_host->err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
     SPT_CHECK(Ly->sc_host->err_embed == 0, SPT_ERR_VALIDATION, "input id out of range [0, vocab)");
+    SPT_CHECK(Ly->sc_host->err_rope == 0, SPT_ERR_VALIDATION, "RoPE position id outside [0, seq_len)");
     if (loss) *loss = Ly->sc_host->loss;
     if (count) *count = Ly->sc_host->count;
 }
@@ -933,6 +960,7 @@ spt_status spt_layer_graph_capture(spt_layer* Ly, const void* x, const int64_t* 
         layer_step(Ly, x, shift_labels, position_ids, false, st);
         SPT_CUDA(cudaStreamSynchronize(st));
         cudaGraph_t g = nullptr;
+        const auto stats0 = Ly->comm->stats;
         SPT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         const int64_t n0 = launch_count();
         try {
@@ -949,14 +977,34 @@ spt_status spt_layer_graph_capture(spt_layer* Ly, const void* x, const int64_t* 
         cudaGraphDestroy(g);
         SPT_CUDA(e);
         Ly->graph_kernels = launch_count() - n0;
+        // the collectives one replay performs (CommStats keep counting across replays)
+        Ly->graph_comm.clear();
+        for (auto& kv : Ly->comm->stats) {
+            auto it = stats0.find(kv.first);
+            spt_comm::Stat d = kv.second;
+            if (it != stats0.end()) {
+                d.calls -= it->second.calls;
+                d.bytes_sent -= it->second.bytes_sent;
+            }
+            if (d.calls) Ly->graph_comm[kv.first] = d;
+        }
     });
 }
 
 spt_status spt_layer_graph_launch(spt_layer* Ly, void* stream) {
     return capi_guard([&] {
         SPT_CHECK(Ly->graph_exec != nullptr, SPT_ERR_CONFIG, "no captured step (spt_layer_graph_capture)");
+        // step events recorded around the replay (inside the capture they were graph nodes, not records), so
+        // spt_layer_timing_json reports the replayed step
+        SPT_CUDA(cudaEventRecord(Ly->ev_step0, (cudaStream_t)stream));
         SPT_CUDA(cudaGraphLaunch(Ly->graph_exec, (cudaStream_t)stream));
+        SPT_CUDA(cudaEventRecord(Ly->ev_step1, (cudaStream_t)stream));
         add_launches(Ly->graph_kernels);
+        for (auto& kv : Ly->graph_comm) {
+            auto& st = Ly->comm->stats[kv.first];
+            st.calls += kv.second.calls;
+            st.bytes_sent += kv.second.bytes_sent;
+        }
     });
 }
 
@@ -995,6 +1043,7 @@ spt_status spt_layer_loss_slot(spt_layer* Ly, int32_t slot, float* loss_out, int
         SPT_CHECK(v.err_label == 0, SPT_ERR_VALIDATION, "label out of range [0, vocab) and != -100");
         SPT_CHECK(v.err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
         SPT_CHECK(v.err_embed == 0, SPT_ERR_VALIDATION, "input id out of range [0, vocab)");
+        SPT_CHECK(v.err_rope == 0, SPT_ERR_VALIDATION, "RoPE position id outside [0, seq_len)");
         if (loss_out) *loss_out = v.loss;
         if (count_out) *count_out = v.count;
     });

@@ -142,7 +142,7 @@ void rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void
 // ------------------------------------------------------------------ Ulysses reshard K1 / K2
 // K1: send[j][t][a][:] = src[t][head_map[j*heads_out + a]][:]   (payload layout :351)
 __global__ void reshard_pack_kernel(const uint4* __restrict__ src, int64_t s_loc, int heads_in, int vpd, int P,
-                                    int heads_out, const int32_t* __restrict__ head_map, uint4* __restrict__ dst) {
+                                    int heads_out, const int32_t* __restrict__ head_map, const RowTab dst) {
     const int64_t total = (int64_t)P * s_loc * heads_out * vpd;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int v = (int)(i % vpd);
@@ -152,12 +152,13 @@ __global__ void reshard_pack_kernel(const uint4* __restrict__ src, int64_t s_loc
         const int64_t t = q % s_loc;
         const int j = (int)(q / s_loc);
         const int hsrc = __ldg(head_map + j * heads_out + a);
-        dst[i] = __ldg(src + (t * heads_in + hsrc) * vpd + v);
+        static_cast<uint4*>(dst.p[j])[((dst.row_off + t) * heads_out + a) * vpd + v] =
+            __ldg(src + (t * heads_in + hsrc) * vpd + v);
     }
 }
 
 // K2: dst[t][h][:] = sum_e recv[i_e][t][a_e][:] over the listed sources, rank order
-__global__ void reshard_unpack_kernel(const uint4* __restrict__ recv, int64_t s_loc, int heads_in, int vpd,
+__global__ void reshard_unpack_kernel(const RowTab recv, int64_t s_loc, int heads_in, int vpd,
                                       int heads_out, const int32_t* __restrict__ gather, int max_src,
                                       uint4* __restrict__ dst) {
     const int64_t total = s_loc * heads_out * vpd;
@@ -170,16 +171,16 @@ __global__ void reshard_unpack_kernel(const uint4* __restrict__ recv, int64_t s_
         const int g0 = __ldg(gl);
         auto src_of = [&](int gidx) {
             const int rank = gidx / heads_in, slot = gidx % heads_in;
-            return recv + (((int64_t)rank * s_loc + t) * heads_in + slot) * vpd + v;
+            return static_cast<const uint4*>(recv.p[rank]) + ((recv.row_off + t) * heads_in + slot) * vpd + v;
         };
         int nsrc = 1;
         while (nsrc < max_src && __ldg(gl + nsrc) >= 0) ++nsrc;
         if (nsrc == 1) {
-            dst[i] = __ldg(src_of(g0));  // plain permutation: bit-exact
+            dst[i] = *src_of(g0);  // plain permutation: bit-exact (plain loads: the source may be a peer's buffer)
         } else {
             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int e = 0; e < nsrc; ++e) {
-                uint4 w = __ldg(src_of(__ldg(gl + e)));
+                uint4 w = *src_of(__ldg(gl + e));
                 const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -242,6 +243,19 @@ __device__ __forceinline__ void rope_rotate8(const float* a, const float* b, flo
     }
 }
 
+// The (cos, sin) row of position pi in a table of npos rows, or NULL (in-kernel angles) without a table or when
+// pi is outside it: a packed chunk whose position_ids run past the table must not read out of bounds (the
+// error flag turns the step into a ValidationError when the host reads it).
+__device__ __forceinline__ const float2* rope_row(const float2* tab, int64_t pi, int64_t npos, int row,
+                                                  int32_t* err) {
+    if (!tab) return nullptr;
+    if (pi < 0 || pi >= npos) {
+        if (err) *err = 4;
+        return nullptr;
+    }
+    return tab + pi * row;
+}
+
 __device__ __forceinline__ void u4_to_f8(const uint4& u, float* f) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
@@ -264,9 +278,10 @@ template <int VPD>
 __global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __restrict__ src, int64_t s_loc,
                                                                 int heads_in, int P, int heads_out,
                                                                 const int32_t* __restrict__ head_map,
-                                                                uint4* __restrict__ dst, int n_rot,
+                                                                const RowTab dst, int n_rot,
                                                                 const int64_t* __restrict__ pos, int64_t pos_offset,
-                                                                float theta, const float2* __restrict__ tab) {
+                                                                float theta, const float2* __restrict__ tab,
+                                                                int64_t npos, int32_t* err) {
     extern __shared__ int32_t smap[];  // [P][heads_out]
     for (int i = threadIdx.x; i < P * heads_out; i += blockDim.x) smap[i] = head_map[i];
     __syncthreads();
@@ -281,9 +296,9 @@ __global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __r
         const int64_t t = r - (int64_t)j * s_loc;
         const int64_t pi = pos ? pos[t] : pos_offset + t;
         const float p = (float)pi;
-        const float2* trow = tab ? tab + pi * (VPD * 4) : nullptr;
+        const float2* trow = rope_row(tab, pi, npos, VPD * 4, err);
         const uint4* srow = src + t * heads_in * VPD;
-        uint4* drow = dst + r * heads_out * VPD;
+        uint4* drow = static_cast<uint4*>(dst.p[j]) + (dst.row_off + t) * heads_out * VPD;
         const int32_t* m = smap + j * heads_out;
         for (int e = lane; e < row_pairs; e += 32) {
             const int hs = e / HP, c = e - hs * HP;
@@ -306,12 +321,13 @@ __global__ void __launch_bounds__(256) reshard_pack_rope_kernel(const uint4* __r
 // K2 unpack of d(q, k, v) with the inverse RoPE fused: replicas summed in fp32 (rank order) and rounded to
 // bf16 exactly as the plain unpack writes them, then the q / k heads (< n_rot) rotated back.
 template <int VPD>
-__global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const uint4* __restrict__ recv, int64_t s_loc,
+__global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const RowTab recv, int64_t s_loc,
                                                                   int heads_in, int heads_out,
                                                                   const int32_t* __restrict__ gather, int max_src,
                                                                   uint4* __restrict__ dst, int n_rot,
                                                                   const int64_t* __restrict__ pos, int64_t pos_offset,
-                                                                  float theta, const float2* __restrict__ tab) {
+                                                                  float theta, const float2* __restrict__ tab,
+                                                                  int64_t npos, int32_t* err) {
     extern __shared__ int32_t sg[];  // [heads_out][max_src]
     for (int i = threadIdx.x; i < heads_out * max_src; i += blockDim.x) sg[i] = gather[i];
     __syncthreads();
@@ -320,28 +336,27 @@ __global__ void __launch_bounds__(256) reshard_unpack_rope_kernel(const uint4* _
     const int row_pairs = heads_out * HP;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t rank_stride = s_loc * heads_in * VPD;
     for (int64_t t = w0; t < s_loc; t += nw) {
-        const uint4* trow = recv + t * heads_in * VPD;
+        const int64_t roff = (recv.row_off + t) * heads_in * VPD;
         uint4* drow = dst + t * heads_out * VPD;
         const int64_t pi = pos ? pos[t] : pos_offset + t;
         const float p = (float)pi;
-        const float2* crow = tab ? tab + pi * (VPD * 4) : nullptr;
+        const float2* crow = rope_row(tab, pi, npos, VPD * 4, err);
         for (int e = lane; e < row_pairs; e += 32) {
             const int h = e / HP, c = e - h * HP;
             const int32_t* gl = sg + h * max_src;
             auto at = [&](int g, int v) {
-                return trow + (int64_t)(g / heads_in) * rank_stride + (g % heads_in) * VPD + v;
+                return static_cast<const uint4*>(recv.p[g / heads_in]) + roff + (g % heads_in) * VPD + v;
             };
-            uint4 a = __ldg(at(gl[0], c)), b = __ldg(at(gl[0], c + HP));
+            uint4 a = *at(gl[0], c), b = *at(gl[0], c + HP);
             if (max_src > 1 && gl[1] >= 0) {  // replica sum in fp32, rank order (as reshard_unpack_rows_kernel)
                 float fa[8], fb[8];
                 u4_to_f8(a, fa);
                 u4_to_f8(b, fb);
                 for (int sidx = 1; sidx < max_src && gl[sidx] >= 0; ++sidx) {
                     float ga[8], gb[8];
-                    u4_to_f8(__ldg(at(gl[sidx], c)), ga);
-                    u4_to_f8(__ldg(at(gl[sidx], c + HP)), gb);
+                    u4_to_f8(*at(gl[sidx], c), ga);
+                    u4_to_f8(*at(gl[sidx], c + HP), gb);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         fa[k] += ga[k];
@@ -369,7 +384,7 @@ template <int VPD>
 __global__ void __launch_bounds__(256) reshard_pack_rows_kernel(const uint4* __restrict__ src, int64_t s_loc,
                                                                 int heads_in, int P, int heads_out,
                                                                 const int32_t* __restrict__ head_map,
-                                                                uint4* __restrict__ dst) {
+                                                                const RowTab dst) {
     extern __shared__ int32_t smap[];  // [P][heads_out]
     for (int i = threadIdx.x; i < P * heads_out; i += blockDim.x) smap[i] = head_map[i];
     __syncthreads();
@@ -382,7 +397,7 @@ __global__ void __launch_bounds__(256) reshard_pack_rows_kernel(const uint4* __r
         const int j = (int)(r / s_loc);
         const int64_t t = r - (int64_t)j * s_loc;
         const uint4* srow = src + t * heads_in * VPD;
-        uint4* drow = dst + r * row_elems;
+        uint4* drow = static_cast<uint4*>(dst.p[j]) + (dst.row_off + t) * row_elems;
         const int32_t* m = smap + j * heads_out;
         for (int e0 = 0; e0 < row_elems; e0 += 32 * 4) {
             uint4 buf[4];
@@ -401,7 +416,7 @@ __global__ void __launch_bounds__(256) reshard_pack_rows_kernel(const uint4* __r
 }
 
 template <int VPD>
-__global__ void __launch_bounds__(256) reshard_unpack_rows_kernel(const uint4* __restrict__ recv, int64_t s_loc,
+__global__ void __launch_bounds__(256) reshard_unpack_rows_kernel(const RowTab recv, int64_t s_loc,
                                                                   int heads_in, int heads_out,
                                                                   const int32_t* __restrict__ gather, int max_src,
                                                                   uint4* __restrict__ dst) {
@@ -412,9 +427,8 @@ __global__ void __launch_bounds__(256) reshard_unpack_rows_kernel(const uint4* _
     const int row_elems = heads_out * VPD;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t rank_stride = s_loc * heads_in * VPD;
     for (int64_t t = w0; t < s_loc; t += nw) {
-        const uint4* trow = recv + t * heads_in * VPD;
+        const int64_t roff = (recv.row_off + t) * heads_in * VPD;
         uint4* drow = dst + t * row_elems;
         for (int e0 = 0; e0 < row_elems; e0 += 32 * 4) {
             uint4 buf[4];
@@ -424,8 +438,10 @@ __global__ void __launch_bounds__(256) reshard_unpack_rows_kernel(const uint4* _
                 if (e >= row_elems) continue;
                 const int h = e / VPD, v = e % VPD;
                 const int32_t* gl = sg + h * max_src;
-                auto at = [&](int g) { return trow + (int64_t)(g / heads_in) * rank_stride + (g % heads_in) * VPD + v; };
-                buf[u] = __ldg(at(gl[0]));
+                auto at = [&](int g) {
+                    return static_cast<const uint4*>(recv.p[g / heads_in]) + roff + (g % heads_in) * VPD + v;
+                };
+                buf[u] = *at(gl[0]);
                 if (max_src > 1 && gl[1] >= 0) {  // replicate_kv backward: fp32 sum in rank order
                     float acc[8];
                     {
@@ -438,7 +454,7 @@ __global__ void __launch_bounds__(256) reshard_unpack_rows_kernel(const uint4* _
                         }
                     }
                     for (int s = 1; s < max_src && gl[s] >= 0; ++s) {
-                        const uint4 w = __ldg(at(gl[s]));
+                        const uint4 w = *at(gl[s]);
                         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
@@ -467,9 +483,18 @@ static int reshard_rows_grid(int64_t rows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms() * 8));
 }
 
+RowTab contiguous_rows(const void* base, int P, int64_t s_loc, int64_t row_bytes) {
+    SPT_CHECK(P >= 1 && P <= kMaxSP, SPT_ERR_CONFIG, "SP degree must be in [1, " + std::to_string(kMaxSP) + "]");
+    RowTab t{};
+    for (int j = 0; j < P; ++j) t.p[j] = (char*)base + (size_t)j * s_loc * row_bytes;
+    t.row_off = 0;
+    return t;
+}
+
 void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
-                  const int32_t* head_map, void* dst, cudaStream_t st) {
+                  const int32_t* head_map, const RowTab& dst, cudaStream_t st) {
     SPT_CHECK(head_dim % 8 == 0, SPT_ERR_SHAPE, "head_dim must be a multiple of 8");
+    SPT_CHECK(P >= 1 && P <= kMaxSP, SPT_ERR_CONFIG, "SP degree out of range");
     const int vpd = head_dim / 8;
     const int64_t total = (int64_t)P * s_loc * heads_out * vpd;
     if (total == 0) return;
@@ -477,16 +502,22 @@ void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, in
     if ((vpd == 4 || vpd == 8 || vpd == 16) && smem <= 48 * 1024) {
         const int g = reshard_rows_grid((int64_t)P * s_loc);
         auto k = vpd == 16 ? reshard_pack_rows_kernel<16> : vpd == 8 ? reshard_pack_rows_kernel<8> : reshard_pack_rows_kernel<4>;
-        k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, (uint4*)dst);
+        k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, dst);
     } else {
         reshard_pack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)src, s_loc, heads_in, vpd, P, heads_out,
-                                                                   head_map, (uint4*)dst);
+                                                                   head_map, dst);
     }
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }
 
-void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                  const int32_t* head_map, void* dst, cudaStream_t st) {
+    reshard_pack(src, s_loc, heads_in, head_dim, P, heads_out, head_map,
+                 contiguous_rows(dst, P, s_loc, (int64_t)heads_out * head_dim * 2), st);
+}
+
+void reshard_unpack(const RowTab& recv, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
                     const int32_t* gather, int max_src, void* dst, cudaStream_t st) {
     SPT_CHECK(head_dim % 8 == 0, SPT_ERR_SHAPE, "head_dim must be a multiple of 8");
     (void)P;
@@ -498,34 +529,41 @@ void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim,
         const int g = reshard_rows_grid(s_loc);
         auto k = vpd == 16 ? reshard_unpack_rows_kernel<16>
                            : vpd == 8 ? reshard_unpack_rows_kernel<8> : reshard_unpack_rows_kernel<4>;
-        k<<<g, 256, smem, st>>>((const uint4*)recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst);
+        k<<<g, 256, smem, st>>>(recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst);
     } else {
-        reshard_unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>((const uint4*)recv, s_loc, heads_in, vpd,
-                                                                     heads_out, gather, max_src, (uint4*)dst);
+        reshard_unpack_kernel<<<grid_for(total, 256), 256, 0, st>>>(recv, s_loc, heads_in, vpd, heads_out, gather,
+                                                                     max_src, (uint4*)dst);
     }
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }
 
+void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                    const int32_t* gather, int max_src, void* dst, cudaStream_t st) {
+    reshard_unpack(contiguous_rows(recv, P, s_loc, (int64_t)heads_in * head_dim * 2), s_loc, heads_in, head_dim, P,
+                   heads_out, gather, max_src, dst, st);
+}
+
 bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
-                       const int32_t* head_map, void* dst, int n_rot, const int64_t* pos, int64_t pos_offset,
-                       float theta, cudaStream_t st, const void* tab) {
+                       const int32_t* head_map, const RowTab& dst, int n_rot, const int64_t* pos, int64_t pos_offset,
+                       float theta, cudaStream_t st, const void* tab, int64_t npos, int32_t* err) {
     const int vpd = head_dim / 8;
     const size_t smem = (size_t)P * heads_out * 4;
     if (head_dim % 16 != 0 || !(vpd == 4 || vpd == 8 || vpd == 16) || smem > 48 * 1024) return false;
     if ((int64_t)P * s_loc * heads_out == 0) return true;
     const int g = reshard_rows_grid((int64_t)P * s_loc);
     auto k = vpd == 16 ? reshard_pack_rope_kernel<16> : vpd == 8 ? reshard_pack_rope_kernel<8> : reshard_pack_rope_kernel<4>;
-    k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, (uint4*)dst, n_rot, pos,
-                            pos_offset, theta, (const float2*)tab);
+    k<<<g, 256, smem, st>>>((const uint4*)src, s_loc, heads_in, P, heads_out, head_map, dst, n_rot, pos, pos_offset,
+                            theta, (const float2*)tab, npos, err);
     count_launch();
     SPT_CUDA(cudaGetLastError());
     return true;
 }
 
-bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head_dim, int heads_out,
+bool reshard_unpack_rope(const RowTab& recv, int64_t s_loc, int heads_in, int head_dim, int heads_out,
                          const int32_t* gather, int max_src, void* dst, int n_rot, const int64_t* pos,
-                         int64_t pos_offset, float theta, cudaStream_t st, const void* tab) {
+                         int64_t pos_offset, float theta, cudaStream_t st, const void* tab, int64_t npos,
+                         int32_t* err) {
     const int vpd = head_dim / 8;
     const size_t smem = (size_t)heads_out * max_src * 4;
     if (head_dim % 16 != 0 || !(vpd == 4 || vpd == 8 || vpd == 16) || smem > 48 * 1024) return false;
@@ -533,8 +571,8 @@ bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head
     const int g = reshard_rows_grid(s_loc);
     auto k = vpd == 16 ? reshard_unpack_rope_kernel<16>
                        : vpd == 8 ? reshard_unpack_rope_kernel<8> : reshard_unpack_rope_kernel<4>;
-    k<<<g, 256, smem, st>>>((const uint4*)recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst, n_rot, pos,
-                            pos_offset, theta, (const float2*)tab);
+    k<<<g, 256, smem, st>>>(recv, s_loc, heads_in, heads_out, gather, max_src, (uint4*)dst, n_rot, pos, pos_offset,
+                            theta, (const float2*)tab, npos, err);
     count_launch();
     SPT_CUDA(cudaGetLastError());
     return true;
@@ -547,7 +585,7 @@ bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head
 // or NULL (then pos = pos_offset + t).  One thread per (token, head, 8 consecutive j): 16-byte loads/stores.
 __global__ void rope_kernel(bf16* __restrict__ x, int64_t n, int heads, int n_rot, int d,
                             const int64_t* __restrict__ pos, int64_t pos_offset, float theta, int inverse,
-                            const float2* __restrict__ tab) {
+                            const float2* __restrict__ tab, int64_t npos, int32_t* err) {
     const int half = d / 2, g8 = half / 8;  // 8-wide groups per half
     const int64_t total = n * n_rot * g8;
     const float sgn = inverse ? -1.f : 1.f;
@@ -563,7 +601,7 @@ __global__ void rope_kernel(bf16* __restrict__ x, int64_t n, int heads, int n_ro
         load8(row + gi * 8, a);
         load8(row + half + gi * 8, b);
         float o1[8], o2[8];
-        rope_rotate8(a, b, p, gi, d, theta, sgn, o1, o2, tab ? tab + pi * half : nullptr);
+        rope_rotate8(a, b, p, gi, d, theta, sgn, o1, o2, rope_row(tab, pi, npos, half, err));
         store8(row + gi * 8, o1);
         store8(row + half + gi * 8, o2);
     }
@@ -589,13 +627,13 @@ void rope_table(void* tab, int64_t npos, int d, float theta, cudaStream_t st) {
 }
 
 void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
-                bool inverse, cudaStream_t st, const void* tab) {
+                bool inverse, cudaStream_t st, const void* tab, int64_t npos, int32_t* err) {
     SPT_CHECK(d % 16 == 0, SPT_ERR_SHAPE, "rope: head_dim must be a multiple of 16");
     SPT_CHECK(theta > 0.f, SPT_ERR_CONFIG, "rope: theta must be > 0");
     const int64_t total = n * n_rot * (d / 16);
     if (total == 0) return;
     rope_kernel<<<grid_for(total, 256), 256, 0, st>>>((bf16*)x, n, heads, n_rot, d, pos, pos_offset, theta,
-                                                      inverse ? 1 : 0, (const float2*)tab);
+                                                      inverse ? 1 : 0, (const float2*)tab, npos, err);
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }

@@ -36,9 +36,24 @@ void rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int64_t
 size_t rmsnorm_bwd_workspace(int64_t n, int64_t h);
 void rmsnorm_bwd(const void* x, const void* gamma, const float* rstd, const void* dy, const void* dres, void* dx,
                  float* dgamma_accum, void* ws, int64_t n, int64_t h, cudaStream_t st);
+// Per-rank row bases of a reshard's far side: K1 writes destination rank j's rows at p[j] + (row_off + t) * row,
+// K2 reads source rank j's rows at p[j] + (row_off + t) * row.  Contiguous [P][s_loc][row] buffers (NCCL
+// send / receive staging) have p[j] = base + j * s_loc * row and row_off = 0; the fused peer collectives point
+// p[j] straight at rank j's receive (K1) / attention output (K2) buffer, mapped over NVLink, with
+// row_off = rank * s_loc (SPEC.md:351 payload layout: rank i's block of the global sequence).
+constexpr int kMaxSP = 64;
+struct RowTab {
+    void* p[kMaxSP];
+    int64_t row_off;
+};
+RowTab contiguous_rows(const void* base, int P, int64_t s_loc, int64_t row_bytes);
 void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
                   const int32_t* head_map, void* dst, cudaStream_t st);
+void reshard_pack(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                  const int32_t* head_map, const RowTab& dst, cudaStream_t st);
 void reshard_unpack(const void* recv, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
+                    const int32_t* gather, int max_src, void* dst, cudaStream_t st);
+void reshard_unpack(const RowTab& src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
                     const int32_t* gather, int max_src, void* dst, cudaStream_t st);
 void label_stats(const int64_t* labels, int64_t n, int64_t vocab, int64_t* count_accum, int32_t* err, cudaStream_t st);
 void segment_starts(const int64_t* pos, int64_t n, int32_t* starts, int32_t* err, cudaStream_t st);
@@ -66,16 +81,20 @@ void scale_by_inverse_count(float* g, int64_t n, const int64_t* count, cudaStrea
 // RoPE on the first n_rot heads of x [n][heads][d] (bf16, in place); inverse = backward rotation.
 // K1 pack / K2 unpack with RoPE fused (false: shape not supported by the fused kernels, caller falls back)
 // tab: optional (cos, sin) table from rope_table covering every position used (NULL: computed in-kernel)
+// tab: (cos, sin) rows for positions [0, npos); a position outside that range sets *err = 4 (when err is
+// given) and takes the in-kernel angles instead of reading past the table
 bool reshard_pack_rope(const void* src, int64_t s_loc, int heads_in, int head_dim, int P, int heads_out,
-                       const int32_t* head_map, void* dst, int n_rot, const int64_t* pos, int64_t pos_offset,
-                       float theta, cudaStream_t st, const void* tab = nullptr);
-bool reshard_unpack_rope(const void* recv, int64_t s_loc, int heads_in, int head_dim, int heads_out,
+                       const int32_t* head_map, const RowTab& dst, int n_rot, const int64_t* pos, int64_t pos_offset,
+                       float theta, cudaStream_t st, const void* tab = nullptr, int64_t npos = 0,
+                       int32_t* err = nullptr);
+bool reshard_unpack_rope(const RowTab& src, int64_t s_loc, int heads_in, int head_dim, int heads_out,
                          const int32_t* gather, int max_src, void* dst, int n_rot, const int64_t* pos,
-                         int64_t pos_offset, float theta, cudaStream_t st, const void* tab = nullptr);
+                         int64_t pos_offset, float theta, cudaStream_t st, const void* tab = nullptr,
+                         int64_t npos = 0, int32_t* err = nullptr);
 void rope_table(void* tab, int64_t npos, int d, float theta, cudaStream_t st);
 extern int g_rope_fused;  // engine.cu: 1 (default) fuse RoPE into K1 / K2 when P > 1
 void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
-                bool inverse, cudaStream_t st, const void* tab = nullptr);
+                bool inverse, cudaStream_t st, const void* tab = nullptr, int64_t npos = 0, int32_t* err = nullptr);
 void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st);
 // W(bf16) -= lr * G(fp32)
 void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st);

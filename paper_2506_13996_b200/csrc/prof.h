@@ -26,9 +26,10 @@ struct Prof {
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
-    static constexpr int NCLS = 8;
+    static constexpr int NCLS = 9;
     static const char* name(int c) {
-        static const char* n[] = {"gemm", "attn_fwd", "attn_bwd", "rmsnorm", "reshard", "ce_rows", "comm", "other"};
+        static const char* n[] = {"gemm", "attn_fwd", "attn_bwd", "rmsnorm", "reshard", "ce_rows", "comm", "other",
+                                  "a2a"};
         return n[c];
     }
     cudaEvent_t ev() {
@@ -72,7 +73,7 @@ struct Prof {
         std::ostringstream os;
         // per-tag breakdown (GEMM call sites)
         std::vector<std::string> tags;
-        std::vector<double> tms, tfl;
+        std::vector<double> tms, tfl, tby;
         std::vector<int> tn;
         for (auto& r : recs) {
             if (r.tag.empty()) continue;
@@ -84,16 +85,19 @@ struct Prof {
                 tags.push_back(r.tag);
                 tms.push_back(0);
                 tfl.push_back(0);
+                tby.push_back(0);
                 tn.push_back(0);
             }
             tms[i] += t;
             tfl[i] += r.flops;
+            tby[i] += r.bytes;
             tn[i] += 1;
         }
         os << "{\"sites\":{";
         for (size_t i = 0; i < tags.size(); ++i)
             os << (i ? "," : "") << "\"" << tags[i] << "\":{\"ms\":" << tms[i] << ",\"calls\":" << tn[i]
-               << ",\"tflops\":" << (tms[i] > 0 ? tfl[i] / (tms[i] * 1e9) : 0) << "}";
+               << ",\"tflops\":" << (tms[i] > 0 ? tfl[i] / (tms[i] * 1e9) : 0)
+               << ",\"bytes\":" << tby[i] << ",\"gbps\":" << (tms[i] > 0 ? tby[i] / (tms[i] * 1e6) : 0) << "}";
         os << "},";
         for (int c = 0; c < NCLS; ++c)
             os << (c ? "," : "") << "\"" << name(c) << "\":{\"ms\":" << ms[c] << ",\"launches\":" << cnt[c]
@@ -102,7 +106,8 @@ struct Prof {
         return os.str();
     }
 };
-enum { P_GEMM = 0, P_ATTN_F, P_ATTN_B, P_NORM, P_RESHARD, P_CE, P_COMM, P_OTHER };
+// P_A2A: a Ulysses all-to-all with its pack / unpack kernel fused in (bytes = payload sent to peers)
+enum { P_GEMM = 0, P_ATTN_F, P_ATTN_B, P_NORM, P_RESHARD, P_CE, P_COMM, P_OTHER, P_A2A };
 
 // The engine installs its Prof here for the duration of a step; library launchers (gemm, ce_rows)
 // self-report so multi-kernel helpers (flce, mlp) are attributed per kernel class.

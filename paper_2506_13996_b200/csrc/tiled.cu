@@ -161,8 +161,10 @@ spt_status spt_reshard_pack_rope(const void* src, int64_t s_loc, int32_t heads_i
                                  const void* cos_sin_table, void* stream) {
     return capi_guard([&] {
         SPT_CHECK(theta > 0.f, SPT_ERR_CONFIG, "rope: theta must be > 0");
-        SPT_CHECK(reshard_pack_rope(src, s_loc, heads_in, head_dim, P, heads_out, head_map, dst, n_rot, position_ids,
-                                    pos_offset, theta, ST, cos_sin_table),
+        // the caller's table covers every position it passes (spt_rope_table documents the extent)
+        SPT_CHECK(reshard_pack_rope(src, s_loc, heads_in, head_dim, P, heads_out, head_map,
+                                    contiguous_rows(dst, P, s_loc, (int64_t)heads_out * head_dim * 2), n_rot,
+                                    position_ids, pos_offset, theta, ST, cos_sin_table, INT64_MAX),
                   SPT_ERR_SHAPE, "reshard_pack_rope: head_dim must be 32, 64 or 128 and the head map fit in smem");
     });
 }
