@@ -1,11 +1,15 @@
 #!/usr/bin/env python
 """Benchmark: fwd+bwd tokens/s of one Llama-3-8B-shaped decoder layer + lm_head with Ulysses SP.
 
-Default (N=1): BASELINE.json configs[1] — h 4096, 32 q / 8 kv heads (d 128), I 14336, V 128256,
-seq 32768 on 1 B200.  N>1 (torchrun, one process per GPU, NCCL over NVLink): weak scaling, 32768
-tokens per GPU, Ulysses SP=N over the whole sequence.
+Default (N=1): BASELINE.json configs[1] (L1) — h 4096, 32 q / 8 kv heads (d 128), I 14336, V 128256,
+seq 32768 on 1 B200.  N>1: one process per GPU (torchrun; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run), Ulysses SP=N over the whole sequence: 32768 tokens per GPU at N=2/4 and
+BASELINE configs[2] (L8: 524288 tokens, 65536 per GPU) at N=8.  The SP exchange runs on the peer-memory
+transport (fused pack-store / load-unpack all-to-alls over NVLink, `--comm peer`, default) or NCCL
+(`--comm nccl`, the library baseline).  `--workload tiny` runs BASELINE configs[0] (h 256, 8q/2kv d32,
+V 32000, seq 8192) instead.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--seq-per-gpu S] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--seq S] [--impl ours|reference] [--comm peer|nccl]
 
 `--impl reference` times the CPU port of the reference algorithm (oracle/, float32 numpy/OpenBLAS on
 all host cores) on a bounded token sample of the same workload; rank 0 only.
@@ -25,13 +29,28 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fwd+bwd tokens/s, Llama-8B-shape layer, 1/2/4/8-GPU Ulysses; peak HBM bytes"
-SHAPE = dict(hidden=4096, q_heads=32, kv_heads=8, head_dim=128, intermediate=14336, vocab=128256)
+SHAPES = {
+    "l1": dict(hidden=4096, q_heads=32, kv_heads=8, head_dim=128, intermediate=14336, vocab=128256),
+    "tiny": dict(hidden=256, q_heads=8, kv_heads=2, head_dim=32, intermediate=1024, vocab=32000),
+}
+SHAPE = SHAPES["l1"]
 CPU_SAMPLE_TOKENS = 256
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (spec)
 
 
-def workload_name(seq, n, layers=1, offload=False):
+def default_seq(workload, n):
+    """L1 (N=1, 32768), weak scaling at 32768 tokens per GPU for N=2/4, the L8 config at N=8 (524288)."""
+    if workload == "tiny":
+        return 8192 * n
+    return 524288 if n == 8 else 32768 * n
+
+
+def workload_name(seq, n, layers=1, offload=False, workload="l1"):
     stack = "layer" if layers == 1 and not offload else (
         f"{layers}-layer stack (activation checkpoints {'offloaded to host' if offload else 'on device'})")
+    if workload == "tiny":
+        return (f"tiny llama-shape {stack} + lm_head (h256, 8q/2kv d32, I1024, V32000; BASELINE configs[0]), "
+                f"seq {seq} over {n} GPU(s), Ulysses SP={n}, TiledMLP + tiled logits/CE")
     return (f"llama3-8b-shape {stack} + lm_head (h4096, 32q/8kv d128, I14336, V128256), "
             f"seq {seq} over {n} GPU(s), Ulysses SP={n}, TiledMLP + tiled logits/CE")
 
@@ -47,14 +66,14 @@ def peaks():
 _CPU_CACHE = {}
 
 
-def cpu_layer_sample(n_tokens: int, seed: int = 0):
+def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1"):
     """One oracle layer step (fwd+bwd) on an n_tokens sample of the workload; returns (seconds, loss)."""
     import numpy as np
 
     from oracle import sptrain_oracle as O
 
-    cfg = O.LLAMA8B
-    key = (n_tokens, seed)
+    cfg = O.LLAMA8B if workload == "l1" else O.LayerConfig(**SHAPES["tiny"])
+    key = (n_tokens, seed, workload)
     if key not in _CPU_CACHE:  # synthetic weights/batch are set-up, not part of the timed step
         p = O.LayerParams(**O.synth_params(cfg, seed)).astype(np.float32)
         _CPU_CACHE[key] = (p, O.synth_batch(cfg, n_tokens, seed))
@@ -64,29 +83,47 @@ def cpu_layer_sample(n_tokens: int, seed: int = 0):
     return time.perf_counter() - t0, res.loss
 
 
+def cpu_sample_desc(n, workload):
+    attn = ("attention is ~15% of the per-token model flops at N=32768 and negligible at this sample size, so "
+            "the CPU rate is an upper bound of its full-sequence rate" if workload == "l1" else
+            "full configs[0] shape")
+    return (f"{n}-token sample of the workload per step (oracle/sptrain_oracle.py layer_step, float32 "
+            f"numpy/OpenBLAS, SP=1); {attn}")
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    n = CPU_SAMPLE_TOKENS
+    n = args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 2048)
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_layer_sample(n)
-    times = [cpu_layer_sample(n)[0] for _ in range(args.steps)]
+        cpu_layer_sample(n, workload=args.workload)
+    times = [cpu_layer_sample(n, workload=args.workload)[0] for _ in range(args.steps)]
     tot = sum(times)
     v = n * len(times) / tot
-    seq = args.seq_per_gpu * world
+    seq = args.seq or default_seq(args.workload, world)
     line = {
         "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * tot / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": workload_name(seq, world), "seq_len": seq, "sp_degree": world},
+        "config": {"workload": workload_name(seq, world, workload=args.workload), "seq_len": seq,
+                   "sp_degree": world, "cpu_model": cpu_model()},
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{n}-token sample of the workload per step (oracle/sptrain_oracle.py "
-                                   f"layer_step, float32 numpy/OpenBLAS, SP=1)"},
+                         "sample": cpu_sample_desc(n, args.workload)},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ------------------------------------------------------------------------------- clocks
@@ -137,6 +174,43 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------- GPU arm
+def make_group(S, args, rank, world, local_rank):
+    """Loopback (N=1), the peer-memory transport (default for N>1) or NCCL (--comm nccl)."""
+    import torch
+
+    if world == 1:
+        return S.ProcessGroup.loopback_group(1, local_rank)
+    if args.comm == "peer":
+        return S.ProcessGroup.peer_group(world, rank, local_rank)  # IPC handles exchanged over torch.distributed
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", local_rank)
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(S.ProcessGroup.unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    return S.ProcessGroup.nccl_group(bytes(uid.cpu().numpy().tobytes()), world, rank, local_rank)
+
+
+def est_max_seq(S, shp, mem, n_loc, world):
+    """max_seqlen_solver on this engine's memory model, calibrated from this run's ledger: the
+    fixed bytes (weights, grads, logits tile workspace) are modelled exactly, the rest of the measured peak
+    is charged per local token."""
+    led = mem["ledger"]["device"]
+    tags = led["tags"]
+    fixed = tags["weights"]["peak"] + tags["grads"]["peak"] + tags["logits"]["peak"]
+    per_tok = max(1.0, (led["peak_bytes"] - fixed) / n_loc)
+    total = mem["ledger"].get("cuda_mem_total_bytes", 0)
+    if not total:
+        return None, per_tok
+    cfg = S.memest_engine(shp, n_layers=1, sp=world, act_bytes_per_token=per_tok)
+    budget = total - 3 * (1 << 30)  # CUDA context, allocator slack
+    try:
+        return S.max_seqlen(cfg, budget, granularity=128 * world), per_tok
+    except S.SptError:
+        return None, per_tok
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -144,19 +218,11 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        import torch.distributed as dist
-
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(S.ProcessGroup.unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        grp = S.ProcessGroup.nccl_group(bytes(uid.cpu().numpy().tobytes()), world, rank, local_rank)
-    else:
-        grp = S.ProcessGroup.loopback_group(1, local_rank)
-    seq = args.seq_per_gpu * world
-    n_loc = args.seq_per_gpu
-    shp = S.ModelShape(**SHAPE)
+    grp = make_group(S, args, rank, world, local_rank)
+    seq = args.seq or default_seq(args.workload, world)
+    assert seq % world == 0, "seq must be divisible by the GPU count"
+    n_loc = seq // world
+    shp = S.ModelShape(**SHAPES[args.workload])
     eng = S.UlyssesLayerStep(shp, seq, grp, lr=args.lr, n_layers=args.layers, ckpt_offload=args.offload,
                              rope_theta=args.rope)
     # random-init weights of the architecture, identical on every rank (same seed)
@@ -190,77 +256,80 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             import torch.distributed as dist
 
-            dist.barrier(device_ids=[local_rank])
+            dist.barrier()
             torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         eng.step_async(x, lab, None, on_host=False, stream=sp)
-    loss0, cnt = eng.read_loss(stream=sp)
+    eng.read_loss(stream=sp)
+    # ---- profiled eager pass: per-kernel-class breakdown, roofline and all-to-all GB/s (not the timed value)
     eng.set_profiling(True)
     barrier()
-    n0 = S.kernel_launch_count()
+    prof_acc, sites_acc = {}, {}
+    prof_steps = max(1, min(args.steps, 3))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    prof_acc = {}
-    sites_acc = {}
-    with Clocks(local_rank) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            eng.step_async(x, lab, None, on_host=False, stream=sp)
-            t = eng.timing()  # syncs on the step's end event only after it is recorded: accumulate per step
-            for site, v in t["classes"].get("sites", {}).items():
-                a = sites_acc.setdefault(site, {"ms": 0.0, "calls": 0})
-                a["ms"] += v["ms"]
-                a["calls"] += v["calls"]
-                a["tflops"] = v["tflops"]
-            for c, v in t["classes"].items():
-                if c == "sites":
-                    continue
-                a = prof_acc.setdefault(c, {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0})
-                for kk in a:
-                    a[kk] += v[kk]
-        ev1.record(stream)
-        barrier()
-    launches = S.kernel_launch_count() - n0
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms_eager = ms
-    loss, cnt = eng.read_loss(stream=sp)
+    ev0.record(stream)
+    for _ in range(prof_steps):
+        eng.step_async(x, lab, None, on_host=False, stream=sp)
+        t = eng.timing()  # syncs on the step's end event only after it is recorded: accumulate per step
+        for site, v in t["classes"].get("sites", {}).items():
+            a = sites_acc.setdefault(site, {"ms": 0.0, "calls": 0, "bytes": 0.0})
+            a["ms"] += v["ms"]
+            a["calls"] += v["calls"]
+            a["bytes"] += v.get("bytes", 0.0)
+            a["tflops"] = v["tflops"]
+        for c, v in t["classes"].items():
+            if c == "sites":
+                continue
+            a = prof_acc.setdefault(c, {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0})
+            for kk in a:
+                a[kk] += v[kk]
+    ev1.record(stream)
+    barrier()
+    ms_eager = max_over_ranks(ev0.elapsed_time(ev1) / prof_steps)
     eng.set_profiling(False)
-    # ---- the same step replayed as one CUDA graph (device-resident inputs at fixed addresses, 1 GPU): this is
-    # the timed `value` when the capture succeeds; the profiled eager loop above supplies the breakdown
+    # ---- the timed value: K replays of one CUDA graph of the whole step (device-resident inputs at fixed
+    # addresses), the same method at every world size; eager launches only if the capture fails
     graph_used = False
-    if args.graph and world == 1:
+    gs = torch.cuda.Stream(dev)
+    gs.wait_stream(stream)
+    if args.graph:
         try:
-            gs = torch.cuda.Stream(dev)
-            gs.wait_stream(stream)
             eng.graph_capture(x, lab, None, stream=gs.cuda_stream)
             for _ in range(2):
                 eng.graph_launch(stream=gs.cuda_stream)
-            gs.synchronize()
-            barrier()
-            n0 = S.kernel_launch_count()
-            with Clocks(local_rank) as clk:
-                ev0.record(gs)
-                for _ in range(args.steps):
-                    eng.graph_launch(stream=gs.cuda_stream)
-                ev1.record(gs)
-                gs.synchronize()
-                barrier()
-            launches = S.kernel_launch_count() - n0
-            ms = ev0.elapsed_time(ev1) / args.steps
-            loss, cnt = eng.read_loss(stream=gs.cuda_stream)
             graph_used = True
-        except S.SptError as e:  # eager timing stands; the reason goes into the JSON line
+        except S.SptError as e:
             graph_used = f"capture failed: {e}"
-    # max over ranks
-    if world > 1:
-        import torch.distributed as dist
-
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    barrier()
+    n0 = S.kernel_launch_count()
+    with Clocks(local_rank) as clk:
+        ev0.record(gs)
+        for _ in range(args.steps):
+            if graph_used is True:
+                eng.graph_launch(stream=gs.cuda_stream)
+            else:
+                eng.step_async(x, lab, None, on_host=False, stream=gs.cuda_stream)
+        ev1.record(gs)
+        gs.synchronize()
+        barrier()
+    launches = S.kernel_launch_count() - n0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    loss, cnt = eng.read_loss(stream=gs.cuda_stream)
     # ---- end-to-end through the public API with host buffers (H2D inputs, D2H loss every step)
     xh = x.cpu().pin_memory()
     labh = lab.cpu().pin_memory()
+    eng.step_async(xh, labh, None, on_host=True, stream=sp)  # untimed: creates the H2D staging buffers
+    eng.read_loss(stream=sp)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -269,15 +338,9 @@ def run_ours(args, rank, world, local_rank):
         eng.loss_async(i % 64, stream=sp)
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     e2e_losses = [eng.loss_slot(i % 64)[0] for i in range(min(args.steps, 64))]
     assert all(math.isfinite(v) for v in e2e_losses), e2e_losses
-    if world > 1:
-        import torch.distributed as dist
-
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
     mem = eng.memory()
     if rank != 0:
         eng.close()
@@ -286,8 +349,8 @@ def run_ours(args, rank, world, local_rank):
     pk, pk_kind = peaks()
     led = mem["ledger"]
     peak_b = led["device"]["peak_bytes"]
-    # roofline for the dominant kernel class (per launch averages over the timed region)
-    cls = max(prof_acc.items(), key=lambda kv: kv[1]["ms"])
+    # roofline for the dominant kernel class (per launch averages over the profiled steps)
+    cls = max(((k, v) for k, v in prof_acc.items() if k != "a2a"), key=lambda kv: kv[1]["ms"])
     name, c = cls
     if c["flops"] > 0:
         achieved = c["flops"] / (c["ms"] / 1e3) / 1e12
@@ -300,50 +363,56 @@ def run_ours(args, rank, world, local_rank):
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_kind": f"{pk_kind} hbm copy"}
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof_path):
+    if os.path.exists(prof_path) and args.workload == "l1":
         try:
-            tr = json.load(open(prof_path))
-            roof["traffic"] = tr.get(name)
+            roof["traffic"] = json.load(open(prof_path)).get(name)
         except Exception:
             pass
-    step_s = ms / 1e3
-    tokens = seq  # whole-job tokens per step (all ranks)
-    breakdown = {k: round(v["ms"] / args.steps, 3) for k, v in prof_acc.items() if v["ms"] > 0}
+    breakdown = {k: round(v["ms"] / prof_steps, 3) for k, v in prof_acc.items() if v["ms"] > 0}
     tflops = {k: round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) for k, v in prof_acc.items() if v["ms"] > 0 and v["flops"]}
+    # Ulysses all-to-alls (pack / unpack fused in on the peer transport): payload bytes per rank / time
+    a2a = {k: {"ms_per_step": round(v["ms"] / prof_steps, 3), "bytes_per_step": v["bytes"] / prof_steps,
+               "gbps": round(v["bytes"] / (v["ms"] * 1e6), 1) if v["ms"] > 0 else None,
+               "frac_of_nvlink": round(v["bytes"] / (v["ms"] * 1e6) / NVLINK_GBS, 3) if v["ms"] > 0 else None}
+           for k, v in sites_acc.items() if k.startswith("a2a_")}
     cpu_v = None
     if world == 1 and not args.no_cpu_baseline:
-        n = CPU_SAMPLE_TOKENS
-        cpu_layer_sample(n)
-        ts = [cpu_layer_sample(n)[0] for _ in range(2)]
+        n = args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 2048)
+        cpu_layer_sample(n, workload=args.workload)
+        ts = [cpu_layer_sample(n, workload=args.workload)[0] for _ in range(2)]
         cpu_v = {"value": n * len(ts) / sum(ts), "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "port",
-                 "sample": f"{n}-token sample of the workload (oracle layer_step, float32 numpy/OpenBLAS, SP=1), "
-                           f"2 steps"}
-    fixed = led["device"]["tags"]["weights"]["peak"] + led["device"]["tags"]["grads"]["peak"]
-    per_tok = (peak_b - fixed) / n_loc
-    free_total = mem["ledger"].get("cuda_mem_total_bytes", 0)
-    est_max = int((0.95 * free_total - fixed) / per_tok) if free_total else None
+                 "sample": cpu_sample_desc(n, args.workload) + ", 2 steps", "cpu_model": cpu_model()}
+    est, per_tok = est_max_seq(S, shp, mem, n_loc, world)
+    tokens = seq  # whole-job tokens per step (all ranks)
     line = {
-        "metric": METRIC, "value": tokens / step_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": tokens / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) hidden, uniform labels)",
-        "config": {"workload": workload_name(seq, world, args.layers, args.offload), "seq_len": seq, "tokens_per_gpu": n_loc,
-                   "sp_degree": world, "mlp_tile": mem["mlp_tile"], "loss_tile": mem["loss_tile"],
-                   "l2": "inputs larger than L2 (x 256 MiB/GPU, weights 1.5 GiB, activations ~3 GiB per step)",
+        "config": {"workload": workload_name(seq, world, args.layers, args.offload, args.workload), "seq_len": seq,
+                   "tokens_per_gpu": n_loc, "sp_degree": world,
+                   "transport": grp.transport if world > 1 else "none (SP=1)",
+                   "mlp_tile": mem["mlp_tile"], "loss_tile": mem["loss_tile"],
+                   "l2": "inputs larger than L2 (x 256 MiB/GPU, weights 1.5 GiB, activations ~3 GiB per step)"
+                         if args.workload == "l1" else "no flush (tiny config: weights and activations fit in L2)",
                    "optimizer": f"sgd lr={args.lr}" if args.lr > 0 else "none (fwd+bwd+SP grad all-reduce)",
                    "n_layers": args.layers, "rope_theta": args.rope,
                    "activation_checkpointing": ("offload to pinned host" if args.offload else
                                                 ("device" if args.layers > 1 else "none (single layer)"))},
         "peak_hbm_bytes": peak_b, "peak_hbm_bytes_per_token": peak_b / n_loc,
-        "est_max_seq_per_gpu": est_max,
+        "est_max_seq_per_gpu": est,
+        "est_max_seq_method": (f"spt_max_seqlen_solver: weights + grads + logits tile exact, "
+                               f"{per_tok:.0f} B per local token from this run's ledger, HBM total - 3 GiB"),
         "loss": loss, "valid_tokens": cnt,
         "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(x.numel() * 2 + lab.numel() * 8), "d2h_bytes_per_step": 32},
+                "h2d_bytes_per_step": int(x.numel() * 2 + lab.numel() * 8) * world, "d2h_bytes_per_step": 32 * world},
         "gpu_launches": launches,
+        "timing": "cuda-graph replay" if graph_used is True else f"eager launches ({graph_used or 'graph off'})",
         "cuda_graph": graph_used, "ms_per_step_eager_profiled": ms_eager,
         "roofline": roof,
         "breakdown_ms_per_step": breakdown, "class_tflops": tflops,
-        "gemm_sites": {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "tflops": round(v["tflops"], 1)}
-                       for k, v in sorted(sites_acc.items(), key=lambda kv: -kv[1]["ms"])},
+        "all_to_all": a2a or None,
+        "gemm_sites": {k: {"ms_per_step": round(v["ms"] / prof_steps, 3), "tflops": round(v["tflops"], 1)}
+                       for k, v in sorted(sites_acc.items(), key=lambda kv: -kv[1]["ms"]) if not k.startswith("a2a_")},
         "clocks": clk.summary(),
         "cpu_baseline": cpu_v,
     }
@@ -352,15 +421,28 @@ def run_ours(args, rank, world, local_rank):
     grp.close()
 
 
+def free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--seq-per-gpu", type=int, default=32768)
+    ap.add_argument("--seq", type=int, default=0, help="global sequence length (0: the workload's default for N)")
+    ap.add_argument("--workload", default="l1", choices=sorted(SHAPES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"], help="SP transport for N > 1")
     ap.add_argument("--lr", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 256 for l1, 2048 for tiny)")
     ap.add_argument("--layers", type=int, default=1,
                     help="decoder layers (> 1: per-layer activation checkpointing; not the BASELINE config)")
     ap.add_argument("--offload", action="store_true", help="activation checkpoints in pinned host memory")
@@ -368,9 +450,17 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time `value` with eager launches instead of a CUDA-graph replay of the step")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run (what the driver does for N > 1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -371,6 +371,105 @@ def attention_bwd(q, k, v, o, lse, do, starts=None, scale=None, q_block=256):
     return dq, dk, dv
 
 
+# ---- attention restricted to sampled rows / columns (SURVEY.md §8(c) parity protocol item 3: the L8 / Q8 rank
+# shapes, s = 2^19 .. 2^20, are checked on sampled query rows and key columns; the full [s, s] problem is
+# out of reach on the CPU).  Same formulas as attention_fwd / attention_bwd above (SPEC.md:216-219, :243-251,
+# :59-67), float64, keys or queries walked in chunks with a running (max, sum) so no [rows, s] matrix lives.
+
+
+def _chunk64(a, lo, hi):
+    return np.asarray(a[lo:hi], dtype=np.float64)
+
+
+def attention_rows(q, k, v, rows, starts=None, scale=None, key_chunk=65536):
+    """O and LSE of query rows `rows` (int array) of attention_fwd: q [s, Hq, d], k / v [s, Hkv, d] (any float
+    dtype, upcast per chunk).  Returns o [R, Hq, d] and lse [Hq, R] in float64."""
+    rows = np.asarray(rows, np.int64)
+    s, Hq, d = q.shape
+    Hkv = k.shape[1]
+    g = Hq // Hkv
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    st = np.zeros(len(rows), np.int64) if starts is None else np.asarray(starts)[rows]
+    qr = np.asarray(q[rows], np.float64)  # [R, Hq, d]
+    m = np.full((Hq, len(rows)), -np.inf)
+    l = np.zeros((Hq, len(rows)))
+    acc = np.zeros((Hq, len(rows), d))
+    for k0 in range(0, int(rows.max()) + 1, key_chunk):
+        k1 = min(s, k0 + key_chunk)
+        kc, vc = _chunk64(k, k0, k1), _chunk64(v, k0, k1)
+        kj = np.arange(k0, k1)
+        allowed = (kj[None, :] <= rows[:, None]) & (kj[None, :] >= st[:, None])
+        for h in range(Hq):
+            sc = (qr[:, h, :] @ kc[:, h // g, :].T) * scale
+            sc = np.where(allowed, sc, -np.inf)
+            mn = np.maximum(m[h], sc.max(axis=1))
+            safe = np.where(np.isfinite(mn), mn, 0.0)
+            p = np.exp(sc - safe[:, None])
+            alpha = np.exp(np.where(np.isfinite(m[h]), m[h] - safe, -np.inf))
+            l[h] = l[h] * alpha + p.sum(axis=1)
+            acc[h] = acc[h] * alpha[:, None] + p @ vc[:, h // g, :]
+            m[h] = mn
+    o = (acc / l[:, :, None]).transpose(1, 0, 2)
+    return o, m + np.log(l)
+
+
+def attention_bwd_rows(q, k, v, do, rows, o_rows, lse_rows, starts=None, scale=None, key_chunk=65536):
+    """dQ of query rows `rows` (attention_bwd): dq_i = scale * sum_j P_ij (dO_i . v_j - D_i) k_j, D_i = dO_i . o_i,
+    with o_rows [R, Hq, d] / lse_rows [Hq, R] from attention_rows.  Returns dq [R, Hq, d] float64."""
+    rows = np.asarray(rows, np.int64)
+    s, Hq, d = q.shape
+    Hkv = k.shape[1]
+    g = Hq // Hkv
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    st = np.zeros(len(rows), np.int64) if starts is None else np.asarray(starts)[rows]
+    qr = np.asarray(q[rows], np.float64)
+    dor = np.asarray(do[rows], np.float64)
+    D = np.sum(dor * o_rows, axis=2)  # [R, Hq]
+    dq = np.zeros((len(rows), Hq, d))
+    for k0 in range(0, int(rows.max()) + 1, key_chunk):
+        k1 = min(s, k0 + key_chunk)
+        kc, vc = _chunk64(k, k0, k1), _chunk64(v, k0, k1)
+        kj = np.arange(k0, k1)
+        allowed = (kj[None, :] <= rows[:, None]) & (kj[None, :] >= st[:, None])
+        for h in range(Hq):
+            sc = (qr[:, h, :] @ kc[:, h // g, :].T) * scale
+            p = np.where(allowed, np.exp(sc - lse_rows[h][:, None]), 0.0)
+            dp = dor[:, h, :] @ vc[:, h // g, :].T
+            dq[:, h, :] += (p * (dp - D[:, h][:, None]) * scale) @ kc[:, h // g, :]
+    return dq
+
+
+def attention_bwd_cols(q, k, v, do, lse, D, cols, starts=None, scale=None, row_chunk=65536):
+    """dK and dV of key rows `cols` (attention_bwd): every query i >= j of every q head of the kv head's group
+    contributes.  Needs the LSE [Hq, s] and D = rowsum(dO * O) [s, Hq] of ALL queries (callers pass the
+    device's, checked separately on sampled rows).  Returns dk, dv [C, Hkv, d] float64."""
+    cols = np.asarray(cols, np.int64)
+    s, Hq, d = q.shape
+    Hkv = k.shape[1]
+    g = Hq // Hkv
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    kc = np.asarray(k[cols], np.float64)
+    vc = np.asarray(v[cols], np.float64)
+    st_all = None if starts is None else np.asarray(starts)
+    dk = np.zeros((len(cols), Hkv, d))
+    dv = np.zeros((len(cols), Hkv, d))
+    for i0 in range(int(cols.min()) // row_chunk * row_chunk, s, row_chunk):
+        i1 = min(s, i0 + row_chunk)
+        qi = np.arange(i0, i1)
+        st = np.zeros(i1 - i0, np.int64) if st_all is None else st_all[i0:i1]
+        allowed = (cols[None, :] <= qi[:, None]) & (cols[None, :] >= st[:, None])  # [c, C]
+        qc, doc = _chunk64(q, i0, i1), _chunk64(do, i0, i1)
+        for h in range(Hq):
+            hk = h // g
+            sc = (qc[:, h, :] @ kc[:, hk, :].T) * scale
+            p = np.where(allowed, np.exp(sc - np.asarray(lse[h, i0:i1], np.float64)[:, None]), 0.0)
+            dv[:, hk, :] += p.T @ doc[:, h, :]
+            dp = doc[:, h, :] @ vc[:, hk, :].T
+            ds = p * (dp - np.asarray(D[i0:i1, h], np.float64)[:, None]) * scale
+            dk[:, hk, :] += ds.T @ qc[:, h, :]
+    return dk, dv
+
+
 def tile_bounds(s: int, num_tiles: int) -> list[tuple[int, int]]:
     """SPEC.md:378-381 TileSpec: uniform tiles of ceil(s/num_tiles), final tile may be smaller."""
     if num_tiles < 1:

@@ -324,3 +324,27 @@ def test_graph_replay_matches_eager():
     finally:
         eng.close()
         grp.close()
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_rope_out_of_range_positions_are_a_validation_error(P):
+    """Packed position ids that run past the RoPE table (here: offset by 10^6) must not read outside it
+    (ADVICE r1): the step reports ValidationError and the CUDA context stays usable for the next step."""
+    N = 1024
+    layers, g3, wlm = _params(CFG, 1, 3)
+    x, lab, pos = O.synth_batch(CFG, N, 3, packed=True)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(SHAPE, N, grp, packed=True, rope_theta=10000.0)
+    try:
+        for k in O.LAYER_NAMES:
+            eng.set_param(k, O.f32_to_bf16_bits(layers[0][k]))
+        eng.set_param("g3", O.f32_to_bf16_bits(g3))
+        eng.set_param("wlm", O.f32_to_bf16_bits(wlm))
+        bad = pos + 1_000_000
+        with pytest.raises(S.ValidationError):
+            eng.step(O.f32_to_bf16_bits(x), lab, bad)
+        loss, cnt = eng.step(O.f32_to_bf16_bits(x), lab, pos)  # the same engine still works
+        assert np.isfinite(loss) and cnt > 0
+    finally:
+        eng.close()
+        grp.close()

@@ -1,8 +1,10 @@
-"""The NCCL communicator path of the engine (one process per GPU, `spt_comm_init_rank`) on the one GPU this
-environment has: a single-rank NCCL group.  It exercises the dlopen'ed NCCL binding, communicator init /
-destroy, and the all-reduce (count, loss sum, grads) and all-gather (position ids) calls of a layer step,
-which must give bitwise the same step as the loopback group (SP=1: both are identities).  Multi-rank NCCL
-needs one GPU per rank; the multi-rank logic is covered by the loopback ranks and the gloo tests.
+"""The NCCL transport of the engine (one process per GPU, `spt_comm_init_rank`) on the one GPU this
+environment has: a single-rank NCCL group.  spt_comm_init_rank creates a real 1-rank communicator
+(ncclCommInitRank) and the step's all-reduces (count, loss sum, grads) and the position-id all-gather
+(packed) are issued as real ncclAllReduce / ncclAllGather calls; the step must be bitwise equal to the
+loopback group's (SP=1: every collective is an identity).  A 1-rank group issues no all-to-all (P = 1 has no
+reshard), and NCCL refuses two ranks on one GPU ("Duplicate GPU detected"), so the multi-rank grouped
+send/recv stays unexecuted here; multi-rank exchange is tested with the peer transport (test_gpu_peer.py).
 (pytest -m gpu)"""
 import numpy as np
 import pytest

@@ -1,0 +1,203 @@
+"""Parity at the north-star target sizes (SURVEY.md §8(c) parity protocol item 3; pytest -m gpu).
+
+The full problems are far beyond a CPU checker, so each is checked where the answer is exactly computable:
+  * the attention of one SP rank at the L8 target (BASELINE configs[2]: s = 524288, 4 q / 1 kv heads) and at
+    the Q8 target (configs[4]: s = 1048576, 8 q / 1 kv heads) on the tcgen05 kernels: O and LSE of sampled
+    query rows and dQ of the same rows against the float64 oracle restricted to those rows
+    (oracle.attention_rows / attention_bwd_rows), dK / dV of sampled key columns against
+    oracle.attention_bwd_cols (which needs every row's LSE and D: the device's, themselves checked on the
+    sampled rows).  Sampled rows include the first / last tiles, where 64-bit index and tail bugs would show;
+  * the Ulysses reshard at the L8 rank size (s_loc = 65536, P = 8 loopback ranks, Llama-3-8B heads, and a
+    kv-replication variant Hkv = 2, r = 4): seq_to_head bit-exact against the index formula on the device,
+    and the head_to_seq round trip bit-exact;
+  * the full L8 step (524288 tokens, 8 loopback SP ranks, Llama-3-8B layer + lm_head on one GPU) with labels
+    on 4096 sampled tokens only: its loss (the mean CE over exactly those tokens) and the lm_head / final-norm
+    grads (only those tokens contribute) against a plain-PyTorch fp32 restatement evaluated at those tokens.
+Tolerances (north_star): loss rel-err <= 1e-3, grads / attention outputs rel-err <= 2e-2 (norm-wise), LSE
+abs-err <= 1e-3."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import sptrain_oracle as O
+from tests.gpu_util import rel_err, torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2506_13996_b200 as S  # noqa: E402
+
+
+def _bf16_np(t):
+    return t.float().cpu().numpy()
+
+
+def _sample(rng, s, n, tile=128):
+    fixed = [0, 1, tile - 1, tile, s // 2, s - tile - 1, s - tile, s - 2, s - 1]
+    return np.unique(np.concatenate([fixed, rng.choice(s, n - len(fixed), replace=False)]))
+
+
+@pytest.mark.parametrize("name,s,hq,hkv,n_rows,n_cols", [("L8_rank", 524288, 4, 1, 256, 64),
+                                                         ("Q8_rank", 1048576, 8, 1, 128, 24)])
+def test_attention_at_target_rank_shape(name, s, hq, hkv, n_rows, n_cols):
+    T = torch()
+    L = S.lib()
+    d = 128
+    scale = 1.0 / math.sqrt(d)
+    g = T.Generator(device="cuda").manual_seed(2506)
+    qkv = T.randn(s, hq + 2 * hkv, d, device="cuda", generator=g).bfloat16()
+    dout = T.randn(s, hq, d, device="cuda", generator=g).bfloat16()
+    o = T.empty(s, hq, d, device="cuda", dtype=T.bfloat16)
+    lse = T.empty(hq, s, device="cuda", dtype=T.float32)
+    S.check(L.spt_attn_fwd(qkv.data_ptr(), s, hq, hkv, d, None, scale, o.data_ptr(), lse.data_ptr(), None))
+    ws = T.empty(L.spt_attn_bwd_workspace(s, hq, hkv, d), device="cuda", dtype=T.uint8)
+    dqkv = T.empty_like(qkv)
+    S.check(L.spt_attn_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), s, hq, hkv, d, None, scale,
+                           dqkv.data_ptr(), ws.data_ptr(), None))
+    T.cuda.synchronize()
+    q = _bf16_np(qkv[:, :hq])
+    k = _bf16_np(qkv[:, hq:hq + hkv])
+    v = _bf16_np(qkv[:, hq + hkv:])
+    do = _bf16_np(dout)
+    o_d = _bf16_np(o)
+    lse_d = lse.cpu().numpy()
+    dq_d = _bf16_np(dqkv[:, :hq])
+    dk_d = _bf16_np(dqkv[:, hq:hq + hkv])
+    dv_d = _bf16_np(dqkv[:, hq + hkv:])
+    del qkv, dout, o, lse, ws, dqkv
+    T.cuda.empty_cache()
+    rng = np.random.default_rng(13)
+    rows = _sample(rng, s, n_rows)
+    o_r, lse_r = O.attention_rows(q, k, v, rows)
+    assert rel_err(o_d[rows], o_r) <= 2e-2, rel_err(o_d[rows], o_r)
+    assert np.max(np.abs(lse_d[:, rows] - lse_r)) <= 1e-3
+    dq_r = O.attention_bwd_rows(q, k, v, do, rows, o_r, lse_r)
+    assert rel_err(dq_d[rows], dq_r) <= 2e-2, rel_err(dq_d[rows], dq_r)
+    cols = _sample(rng, s, n_cols)
+    D = np.einsum("shd,shd->sh", do, o_d, dtype=np.float64)
+    dk_r, dv_r = O.attention_bwd_cols(q, k, v, do, lse_d, D, cols)
+    assert rel_err(dk_d[cols], dk_r) <= 2e-2, rel_err(dk_d[cols], dk_r)
+    assert rel_err(dv_d[cols], dv_r) <= 2e-2, rel_err(dv_d[cols], dv_r)
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (32, 2)])
+def test_reshard_bit_exact_at_l8_rank_size(hq, hkv):
+    """seq_to_head (K1 fused with the loopback all-to-all) at s_loc = 65536, P = 8, against the index formula
+    on the device; then head_to_seq of the result as d(q|k|v): q exact, kv heads times r (bf16-exact)."""
+    T = torch()
+    P, s_loc, d = 8, 65536, 128
+    plan = S.plan_head_shards(hq, hkv, P)
+    grp = S.ProcessGroup.loopback_group(P)
+    try:
+        g = T.Generator(device="cuda").manual_seed(7)
+        xs = [T.randn(s_loc, hq + 2 * hkv, d, device="cuda", generator=g).bfloat16() for _ in range(P)]
+        hl = plan.q_heads_per_rank + 2 * plan.kv_heads_per_rank
+        outs = [T.empty(P * s_loc, hl, d, device="cuda", dtype=T.bfloat16) for _ in range(P)]
+        grp.seq_to_head(plan, 0, [x.data_ptr() for x in xs], s_loc, d, [o.data_ptr() for o in outs])
+        T.cuda.synchronize()
+        for j in range(P):
+            heads = S.heads_of(plan, j, 0) + [hq + h for h in S.heads_of(plan, j, 1)] + \
+                [hq + hkv + h for h in S.heads_of(plan, j, 1)]
+            idx = T.tensor(heads, device="cuda")
+            want = T.cat([x.index_select(1, idx) for x in xs], dim=0)
+            assert T.equal(outs[j].view(T.int16), want.view(T.int16)), j
+        backs = [T.empty_like(x) for x in xs]
+        grp.head_to_seq(plan, 1, [o.data_ptr() for o in outs], s_loc, d, [b.data_ptr() for b in backs])
+        T.cuda.synchronize()
+        r = plan.kv_replication
+        for x, b in zip(xs, backs):
+            assert T.equal(b[:, :hq].view(T.int16), x[:, :hq].view(T.int16))
+            assert T.equal(b[:, hq:].float(), x[:, hq:].float() * r)
+        st = grp.stats()["collectives"]
+        assert st["all_to_all_qkv"]["bytes_sent_per_rank"] == s_loc * hl * d * 2 * (P - 1)
+    finally:
+        grp.close()
+
+
+def _rms(x, g, eps=1e-5):
+    T = torch()
+    return x * T.rsqrt((x * x).mean(-1, keepdim=True) + eps) * g
+
+
+def _attn_rows_torch(q, rows, K, V, scale, key_chunk=32768):
+    """fp32 attention of query rows `rows` (q [R, Hq, d]) over the causal prefix of K / V [s, Hkv, d]."""
+    T = torch()
+    R, Hq, d = q.shape
+    g = Hq // K.shape[1]
+    m = T.full((Hq, R), -float("inf"), device="cuda")
+    l = T.zeros(Hq, R, device="cuda")
+    acc = T.zeros(Hq, R, d, device="cuda")
+    qh = q.permute(1, 0, 2)
+    for k0 in range(0, int(rows.max()) + 1, key_chunk):
+        k1 = min(K.shape[0], k0 + key_chunk)
+        kh = K[k0:k1].permute(1, 0, 2).repeat_interleave(g, 0)
+        vh = V[k0:k1].permute(1, 0, 2).repeat_interleave(g, 0)
+        sc = T.matmul(qh, kh.transpose(1, 2)) * scale
+        allowed = T.arange(k0, k1, device="cuda")[None, :] <= rows[:, None]
+        sc = sc.masked_fill(~allowed[None], -float("inf"))
+        mn = T.maximum(m, sc.amax(-1))
+        p = T.exp(sc - mn[..., None])
+        alpha = T.exp(m - mn)
+        l = l * alpha + p.sum(-1)
+        acc = acc * alpha[..., None] + T.matmul(p, vh)
+        m = mn
+    return (acc / l[..., None]).permute(1, 0, 2)
+
+
+def test_l8_full_step_loss_on_sampled_tokens():
+    T = torch()
+    T.backends.cuda.matmul.allow_tf32 = False
+    shp = S.LLAMA8B
+    N, P, n_lab = 524288, 8, 4096
+    h, Hq, Hkv, d, I, V = shp.hidden, shp.q_heads, shp.kv_heads, shp.head_dim, shp.intermediate, shp.vocab
+    g = T.Generator(device="cuda").manual_seed(88)
+    qkv_out = (Hq + 2 * Hkv) * d
+    shapes = {"g1": (h,), "wqkv": (qkv_out, h), "wo": (h, Hq * d), "g2": (h,), "wg": (I, h), "wu": (I, h),
+              "wd": (h, I), "g3": (h,), "wlm": (V, h)}
+    params = {k: ((1 + 0.05 * T.randn(s_, device="cuda", generator=g)) if k[0] == "g" else
+                  0.02 * T.randn(s_, device="cuda", generator=g)).bfloat16() for k, s_ in shapes.items()}
+    x = T.randn(N, h, device="cuda", generator=g).bfloat16()
+    rng = np.random.default_rng(4)
+    tok = np.sort(rng.choice(N, n_lab, replace=False))
+    tok_d = T.from_numpy(tok).cuda()
+    lab = T.full((N,), -100, dtype=T.int64, device="cuda")
+    lab[tok_d] = T.randint(0, V, (n_lab,), device="cuda", generator=g)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(shp, N, grp)
+    try:
+        for k, w in params.items():
+            eng.set_param(k, w, on_host=False)
+        loss, cnt = eng.step(x, lab, None, on_host=False)
+        gwlm = T.from_numpy(eng.grad("wlm")).cuda()
+        gg3 = T.from_numpy(eng.grad("g3")).cuda()
+    finally:
+        eng.close()
+        grp.close()
+    T.cuda.empty_cache()
+    assert cnt == n_lab
+    # fp32 restatement at the sampled tokens: K / V of every token, the rest only at the sampled ones
+    p = {k: v.float() for k, v in params.items()}
+    K = T.empty(N, Hkv, d, device="cuda")
+    Vv = T.empty(N, Hkv, d, device="cuda")
+    wk = p["wqkv"][Hq * d:(Hq + Hkv) * d]
+    wv = p["wqkv"][(Hq + Hkv) * d:]
+    for a in range(0, N, 65536):
+        xn = _rms(x[a:a + 65536].float(), p["g1"])
+        K[a:a + 65536] = (xn @ wk.t()).view(-1, Hkv, d)
+        Vv[a:a + 65536] = (xn @ wv.t()).view(-1, Hkv, d)
+    xt = x[tok_d].float()
+    q = (_rms(xt, p["g1"]) @ p["wqkv"][:Hq * d].t()).view(n_lab, Hq, d)
+    o = T.cat([_attn_rows_torch(q[i:i + 512], tok_d[i:i + 512], K, Vv, 1.0 / math.sqrt(d))
+               for i in range(0, n_lab, 512)])
+    del K, Vv
+    x1 = xt + o.reshape(n_lab, Hq * d) @ p["wo"].t()
+    xn2 = _rms(x1, p["g2"])
+    x2 = x1 + (T.nn.functional.silu(xn2 @ p["wg"].t()) * (xn2 @ p["wu"].t())) @ p["wd"].t()
+    g3 = p["g3"].clone().requires_grad_(True)
+    wlm = p["wlm"].clone().requires_grad_(True)
+    z = _rms(x2, g3)
+    ref = T.nn.functional.cross_entropy(z @ wlm.t(), lab[tok_d], reduction="mean")
+    ref.backward()
+    assert abs(loss - float(ref)) / abs(float(ref)) <= 1e-3, (loss, float(ref))
+    assert rel_err(gwlm.cpu().numpy(), wlm.grad.cpu().numpy()) <= 2e-2
+    assert rel_err(gg3.cpu().numpy(), g3.grad.cpu().numpy()) <= 2e-2

@@ -207,3 +207,25 @@ def test_embedding_oracle_properties():
         O.embed_fwd([0, V], E)
     with pytest.raises(ValueError):
         O.embed_fwd([-1], E)
+
+
+def test_attention_row_and_column_restrictions_match_full_attention():
+    """attention_rows / attention_bwd_rows / attention_bwd_cols (the checkers of the L8 / Q8 rank-shape GPU
+    tests) equal the full oracle attention on every sampled row / column, causal and packed."""
+    rng = np.random.default_rng(5)
+    s, Hq, Hkv, d = 300, 4, 2, 16
+    q, k, v, do = (rng.standard_normal((s, h, d)) for h in (Hq, Hkv, Hkv, Hq))
+    for starts in (None, O.block_causal_starts(np.concatenate([np.arange(120), np.arange(180)]))):
+        o, lse = O.attention_fwd(q, k, v, starts)
+        dq, dk, dv = O.attention_bwd(q, k, v, o, lse, do, starts)
+        rows = np.array([0, 1, 57, 119, 120, 121, 299])
+        orow, lrow = O.attention_rows(q, k, v, rows, starts, key_chunk=64)
+        np.testing.assert_allclose(orow, o[rows], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(lrow, lse[:, rows], rtol=1e-12, atol=1e-12)
+        dqr = O.attention_bwd_rows(q, k, v, do, rows, orow, lrow, starts, key_chunk=64)
+        np.testing.assert_allclose(dqr, dq[rows], rtol=1e-9, atol=1e-11)
+        cols = np.array([0, 5, 119, 120, 200, 299])
+        D = np.sum(do * o, axis=2)
+        dkc, dvc = O.attention_bwd_cols(q, k, v, do, lse, D, cols, starts, row_chunk=64)
+        np.testing.assert_allclose(dkc, dk[cols], rtol=1e-9, atol=1e-11)
+        np.testing.assert_allclose(dvc, dv[cols], rtol=1e-9, atol=1e-11)
