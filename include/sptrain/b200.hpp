@@ -185,6 +185,7 @@ struct StepOptions {
     float rms_eps = 1e-5f;
     float rope_theta = 0.f;      // > 0: rotary embedding on q/k (row f4; the reference model has none)
     bool embed = false;          // token embedding "emb" in front of the stack; step x = int64 input_ids
+    bool verify_replay = false;  // fingerprint checkpoint replays vs the recorded forward (autograd.hpp:26-30)
 };
 
 class UlyssesLayerStep {
@@ -207,6 +208,7 @@ public:
         c.ckpt_offload = o.ckpt_offload ? 1 : 0;
         c.rope_theta = o.rope_theta;
         c.embed = o.embed ? 1 : 0;
+        c.verify_replay = o.verify_replay ? 1 : 0;
         check(spt_layer_create(&c, group.handle(), &l_));
     }
     UlyssesLayerStep(const UlyssesLayerStep&) = delete;

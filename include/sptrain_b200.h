@@ -300,6 +300,10 @@ typedef struct {
                              :223); the step's x argument is then int64 input_ids [local_ranks * s_loc], ids
                              outside [0, vocab) are a validation error, and grad "emb" is the per-id sum of the
                              stack's input gradient (deterministic) */
+    int32_t verify_replay; /* 1 (with checkpointing): every checkpoint replay in the backward is fingerprinted
+                              against the recorded forward (autograd.hpp:26-30); a mismatch makes the step
+                              fail with SPT_ERR_DETERMINISM (errors.hpp:36-40).  Costs one read of each
+                              replayed layer's output. */
 } spt_layer_config;
 
 typedef struct spt_layer spt_layer;

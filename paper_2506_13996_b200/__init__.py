@@ -73,7 +73,7 @@ class LayerConfig(C.Structure):
                 ("intermediate", C.c_int32), ("vocab", C.c_int64), ("seq_len", C.c_int64), ("mlp_tiles", C.c_int32),
                 ("loss_tile", C.c_int64), ("rms_eps", C.c_float), ("packed", C.c_int32), ("lr", C.c_float),
                 ("n_layers", C.c_int32), ("ckpt_offload", C.c_int32), ("rope_theta", C.c_float),
-                ("embed", C.c_int32)]
+                ("embed", C.c_int32), ("verify_replay", C.c_int32)]
 
 
 P = C.c_void_p
@@ -516,11 +516,12 @@ class UlyssesLayerStep:
 
     def __init__(self, shape: ModelShape, seq_len: int, group: ProcessGroup, mlp_tiles: int = 0,
                  loss_tile: int = 0, packed: bool = False, lr: float = 0.0, rms_eps: float = 1e-5,
-                 n_layers: int = 1, ckpt_offload: bool = False, rope_theta: float = 0.0, embed: bool = False):
+                 n_layers: int = 1, ckpt_offload: bool = False, rope_theta: float = 0.0, embed: bool = False,
+                 verify_replay: bool = False):
         self.shape, self.seq_len, self.group, self.n_layers = shape, seq_len, group, n_layers
         self.cfg = LayerConfig(shape.hidden, shape.q_heads, shape.kv_heads, shape.head_dim, shape.intermediate,
                                shape.vocab, seq_len, mlp_tiles, loss_tile, rms_eps, int(packed), lr, n_layers,
-                               int(ckpt_offload), rope_theta, int(embed))
+                               int(ckpt_offload), rope_theta, int(embed), int(verify_replay))
         h = C.c_void_p()
         check(lib().spt_layer_create(C.byref(self.cfg), group.handle, C.byref(h)))
         self.handle = h

@@ -156,6 +156,10 @@ int g_rope_fused = [] {
 
 // TiledMLP backward tile grouping (1 = the forward's tiles, 2 = pairs of consecutive tiles per recompute /
 // weight-gradient pass); SPT_MLP_BWD_GROUP or spt_tuning_set("mlp_bwd_group", v)
+// test-only fault injection for the replay verification: flip one bit of the restored checkpoint before the
+// next replay (spt_tuning_set("replay_fault", 1)); cleared after use
+int g_replay_fault = 0;
+
 int g_mlp_bwd_group = [] {
     const char* e = getenv("SPT_MLP_BWD_GROUP");
     return e ? atoi(e) : 1;
@@ -174,6 +178,7 @@ struct Scalars {
     int32_t err_pos;
     int32_t err_embed;
     int32_t err_rope;  // a RoPE position outside [0, seq_len) (packed chunk whose ids run past the table)
+    int32_t err_replay;  // 1 + layer index whose checkpoint replay differed from its recorded forward
 };
 // Gradient-accumulation window ("divide by global valid_count summed over the accumulation
 // window"): micro-steps accumulate grads of the loss SUM; finish divides by the window's global count.
@@ -208,6 +213,8 @@ struct spt_layer {
     int NL = 1;            // decoder layers
     bool ckpt = false;     // activation checkpointing (every layer input saved, layers re-run in backward)
     bool offload = false;  // checkpoints in pinned host memory
+    bool verify = false;   // checkpoint replays fingerprinted against the recorded forward (autograd.hpp:26-30)
+    uint64_t* fp = nullptr;  // [NL + 1]: recorded fingerprint of each layer's output, scratch for the replay's
     std::vector<LayerW> lw;
     bf16 *g3, *wlm;
     void* rope_tab = nullptr;  // RoPE (cos, sin) per (position < N, j < d/2), built once at creation
@@ -295,6 +302,7 @@ static void build_layer(spt_layer* Ly) {
     Ly->NL = std::max(1, c.n_layers);
     Ly->offload = c.ckpt_offload != 0;
     Ly->ckpt = Ly->NL > 1 || Ly->offload;
+    Ly->verify = Ly->ckpt && c.verify_replay != 0;
     // weights
     Ly->lw.resize(Ly->NL);
     for (auto& w : Ly->lw) {
@@ -421,6 +429,7 @@ static void build_layer(spt_layer* Ly) {
     Ly->seg = c.packed ? (int32_t*)L_.alloc(N * 4, kWorkspace) : nullptr;
     Ly->pos_full = c.packed ? (int64_t*)L_.alloc(N * 8, kWorkspace) : nullptr;
     Ly->sc = (Scalars*)L_.alloc(sizeof(Scalars), kWorkspace, sym);
+    if (Ly->verify) Ly->fp = (uint64_t*)L_.alloc((Ly->NL + 1) * 8, kWorkspace);
     Ly->win = (Window*)L_.alloc(sizeof(Window), kWorkspace);
     {
         const Window w0{0.0, 0, 1};
@@ -716,10 +725,16 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         for (int r = 0; r < L; ++r) std::swap(Ly->rb[r].x, Ly->xpf[r]);
     };
 
+    // fingerprint of a layer's output (every local rank's rows), for the replay verification
+    auto fingerprint = [&](uint64_t* out) {
+        SPT_CUDA(cudaMemsetAsync(out, 0, 8, st));
+        for (int r = 0; r < L; ++r) fingerprint_bf16(Ly->rb[r].x2, nl * h, out, st);
+    };
     // ---- forward through the layers (only the checkpoints survive when checkpointing)
     for (int l = 0; l < NL; ++l) {
         if (Ly->ckpt) ckpt_save(l);
         layer_fwd(Ly->lw[l]);
+        if (Ly->verify && l + 1 < NL) fingerprint(Ly->fp + l);  // the recorded forward of a replayed layer
         if (l + 1 < NL) {
             if (Ly->offload) SPT_CUDA(cudaStreamWaitEvent(st, Ly->ev_ck_done, 0));  // b.x copied out
             for (int r = 0; r < L; ++r)
@@ -745,7 +760,15 @@ static void layer_step(spt_layer* Ly, const void* x, const int64_t* labels, cons
         if (Ly->ckpt && l < NL - 1) {
             ckpt_restore(l);
             if (Ly->offload && l > 0) prefetch(l - 1);  // overlaps this layer's recompute + backward
+            if (g_replay_fault) {
+                flip_lowest_bit(Ly->rb[0].x, st);
+                g_replay_fault = 0;
+            }
             layer_fwd(Ly->lw[l]);
+            if (Ly->verify) {  // the replay must be bit-identical to the recorded forward (autograd.hpp:26-30)
+                fingerprint(Ly->fp + NL);
+                fingerprint_compare(Ly->fp + l, Ly->fp + NL, &Ly->sc->err_replay, l + 1, st);
+            }
         }
         layer_bwd(Ly->lw[l]);
     }
@@ -813,6 +836,9 @@ static void read_scalars(spt_layer* Ly, cudaStream_t st, float* loss, int64_t* c
     SPT_CHECK(Ly->sc_host->err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
     SPT_CHECK(Ly->sc_host->err_embed == 0, SPT_ERR_VALIDATION, "input id out of range [0, vocab)");
     SPT_CHECK(Ly->sc_host->err_rope == 0, SPT_ERR_VALIDATION, "RoPE position id outside [0, seq_len)");
+    SPT_CHECK(Ly->sc_host->err_replay == 0, SPT_ERR_DETERMINISM,
+              "checkpoint replay of layer " + std::to_string(Ly->sc_host->err_replay - 1) +
+                  " is not bit-identical to its recorded forward");
     if (loss) *loss = Ly->sc_host->loss;
     if (count) *count = Ly->sc_host->count;
 }
@@ -1044,6 +1070,9 @@ spt_status spt_layer_loss_slot(spt_layer* Ly, int32_t slot, float* loss_out, int
         SPT_CHECK(v.err_pos == 0, SPT_ERR_VALIDATION, "position_ids not zero-based ascending runs");
         SPT_CHECK(v.err_embed == 0, SPT_ERR_VALIDATION, "input id out of range [0, vocab)");
         SPT_CHECK(v.err_rope == 0, SPT_ERR_VALIDATION, "RoPE position id outside [0, seq_len)");
+        SPT_CHECK(v.err_replay == 0, SPT_ERR_DETERMINISM,
+                  "checkpoint replay of layer " + std::to_string(v.err_replay - 1) +
+                      " is not bit-identical to its recorded forward");
         if (loss_out) *loss_out = v.loss;
         if (count_out) *count_out = v.count;
     });

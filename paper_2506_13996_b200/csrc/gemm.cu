@@ -287,6 +287,7 @@ extern int g_attn_dkdv_kt;    // attention_tc.cu
 extern int g_attn_kv_group;   // attention_tc.cu
 extern int g_attn_fwd_bk128;  // attention_tc.cu
 extern int g_attn_fwd_hybrid;  // attention_tc.cu
+extern int g_replay_fault;     // engine.cu
 }
 
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
@@ -323,6 +324,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         }
         if (n == "rope_fused") {
             spt::g_rope_fused = value;
+            return;
+        }
+        if (n == "replay_fault") {  // test-only: corrupt the next checkpoint replay (DeterminismError path)
+            spt::g_replay_fault = value;
             return;
         }
         if (n == "mlp_bwd_group") {

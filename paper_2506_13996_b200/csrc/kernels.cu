@@ -993,3 +993,50 @@ void deinterleave_gu_f32(const float* gu, float* g, float* u, int64_t inter, int
 }
 
 }  // namespace spt
+
+namespace spt {
+
+// ------------------------------------------------------------------ checkpoint replay verification
+// (autograd.hpp:26-30: the replay of a checkpointed region must be bit-identical to its recorded forward)
+// Order-independent 64-bit fingerprint of a bf16 buffer: sum mod 2^64 of a mixed (index, bits) word per
+// element, so the atomics' arrival order cannot change it; any bit flip changes it.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void fingerprint_kernel(const uint16_t* __restrict__ x, int64_t n, uint64_t* out) {
+    uint64_t acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += mix64(((uint64_t)i << 16) | x[i]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long*)out, (unsigned long long)acc);
+}
+
+__global__ void fingerprint_compare_kernel(const uint64_t* want, const uint64_t* got, int32_t* err, int32_t tag) {
+    if (*want != *got && *err == 0) *err = tag;
+}
+
+__global__ void flip_bit_kernel(uint16_t* x) { x[0] ^= 1; }
+
+void fingerprint_bf16(const void* x, int64_t n, uint64_t* out, cudaStream_t st) {
+    fingerprint_kernel<<<grid_for(n, 256), 256, 0, st>>>((const uint16_t*)x, n, out);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+void fingerprint_compare(const uint64_t* want, const uint64_t* got, int32_t* err, int32_t tag, cudaStream_t st) {
+    fingerprint_compare_kernel<<<1, 1, 0, st>>>(want, got, err, tag);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+void flip_lowest_bit(void* x, cudaStream_t st) {
+    flip_bit_kernel<<<1, 1, 0, st>>>((uint16_t*)x);
+    count_launch();
+    SPT_CUDA(cudaGetLastError());
+}
+
+}  // namespace spt

@@ -96,6 +96,11 @@ extern int g_rope_fused;  // engine.cu: 1 (default) fuse RoPE into K1 / K2 when 
 void rope_apply(void* x, int64_t n, int heads, int n_rot, int d, const int64_t* pos, int64_t pos_offset, float theta,
                 bool inverse, cudaStream_t st, const void* tab = nullptr, int64_t npos = 0, int32_t* err = nullptr);
 void finalize_loss(const double* loss_sum, const int64_t* count, float* loss_out, cudaStream_t st);
+// checkpoint replay verification (autograd.hpp:26-30): *out += order-independent fingerprint of n bf16 values;
+// compare sets *err = tag when the fingerprints differ; flip_lowest_bit is the test-only fault injection
+void fingerprint_bf16(const void* x, int64_t n, uint64_t* out, cudaStream_t st);
+void fingerprint_compare(const uint64_t* want, const uint64_t* got, int32_t* err, int32_t tag, cudaStream_t st);
+void flip_lowest_bit(void* x, cudaStream_t st);
 // W(bf16) -= lr * G(fp32)
 void sgd_update(void* w, const float* g, int64_t n, float lr, cudaStream_t st);
 // Interleave/deinterleave gate/up in blocks of 32 rows: dst [2I, h] from wg [I,h], wu [I,h].

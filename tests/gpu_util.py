@@ -30,3 +30,14 @@ def rel_err(a, b):
     b = np.asarray(b, np.float64)
     nb = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def record(name, **vals):
+    """Append measured parity numbers to $SPT_PARITY_LOG (JSON lines) when set: the margins behind a pass."""
+    import json
+    import os
+
+    path = os.environ.get("SPT_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": name, **{k: float(v) for k, v in vals.items()}}) + "\n")

@@ -348,3 +348,76 @@ def test_rope_out_of_range_positions_are_a_validation_error(P):
     finally:
         eng.close()
         grp.close()
+
+
+# ---- checkpoint replay verification (autograd.hpp:26-30, errors.hpp:36-40 DeterminismError)
+@pytest.mark.parametrize("offload", [False, True])
+def test_replay_verification_passes_and_catches_a_corrupted_replay(offload):
+    N, L, P = 512, 2, 2
+    layers, g3, wlm = _params(CFG, L, 3)
+    x, lab, _ = O.synth_batch(CFG, N, 3)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(SHAPE, N, grp, n_layers=L, ckpt_offload=offload, verify_replay=True)
+    try:
+        for i, lp in enumerate(layers):
+            for k in O.LAYER_NAMES:
+                eng.set_param(f"layers.{i}.{k}", O.f32_to_bf16_bits(lp[k]))
+        eng.set_param("g3", O.f32_to_bf16_bits(g3))
+        eng.set_param("wlm", O.f32_to_bf16_bits(wlm))
+        xb = O.f32_to_bf16_bits(x)
+        loss, _ = eng.step(xb, lab)  # deterministic kernels: every replay matches its recorded forward
+        g0 = eng.grad("layers.0.wqkv")
+        S.check(S.lib().spt_tuning_set(b"replay_fault", 1))  # flip one bit of the restored checkpoint
+        with pytest.raises(S.DeterminismError, match="layer 0"):
+            eng.step(xb, lab)
+        loss2, _ = eng.step(xb, lab)  # the fault is one-shot; the engine recovers
+        assert loss2 == loss and np.array_equal(eng.grad("layers.0.wqkv"), g0)
+    finally:
+        S.check(S.lib().spt_tuning_set(b"replay_fault", 0))
+        eng.close()
+        grp.close()
+    r = _run(L, P, N, offload=offload)  # the verification does not change any value
+    assert r["loss"] == loss
+
+
+# ---- the SGD update and multi-step SP equivalence (SPEC.md:697 acceptance #1)
+def _train(cfg, shape, P, N, steps, lr, seed=21):
+    p = O.synth_params(cfg, seed)
+    x, lab, _ = O.synth_batch(cfg, N, seed)
+    grp = S.ProcessGroup.loopback_group(P)
+    eng = S.UlyssesLayerStep(shape, N, grp, lr=lr)
+    losses = []
+    try:
+        for k in O.LayerParams.NAMES:
+            eng.set_param(k, O.f32_to_bf16_bits(p[k]))
+        xb = O.f32_to_bf16_bits(x)
+        for _ in range(steps):
+            losses.append(eng.step(xb, lab)[0])
+    finally:
+        eng.close()
+        grp.close()
+    return np.array(losses), p, x, lab
+
+
+def test_sgd_update_matches_oracle_over_steps():
+    """Three SGD steps (W_bf16 <- bf16(W - lr * grad_fp32), engine.cu apply_update) against the oracle running the
+    same update on bf16-rounded weights: per-step loss within the contract's 1e-3."""
+    lr, steps, N = 2.0, 3, 512
+    losses, p, x, lab = _train(CFG, SHAPE, 1, N, steps, lr)
+    w = {k: O.round_bf16(np.asarray(p[k], np.float64)) for k in O.LayerParams.NAMES}
+    for t in range(steps):
+        ref = O.layer_step(O.LayerParams(**w), CFG, O.round_bf16(x), lab, None, P=1)
+        assert abs(losses[t] - ref.loss) / ref.loss <= 1e-3, (t, losses[t], ref.loss)
+        w = {k: O.round_bf16(w[k] - lr * ref.grads[k]) for k in w}
+    assert losses[-1] < losses[0]
+
+
+@pytest.mark.parametrize("P,cfg,shape", [(2, CFG, SHAPE), (4, CFG, SHAPE), (8, TINY, TINY_SHAPE)])
+def test_sgd_20_steps_sp_equals_sp1(P, cfg, shape):
+    """20 optimizer steps at SP=P track SP=1 step for step (bf16 weights: within 2e-3)."""
+    lr, steps, N = 2.0, 20, 1024
+    l1, *_ = _train(cfg, shape, 1, N, steps, lr)
+    lp, *_ = _train(cfg, shape, P, N, steps, lr)
+    dev = np.abs(lp - l1) / l1
+    assert dev.max() <= 2e-3, (dev.max(), l1, lp)
+    assert l1[-1] < l1[0] - 0.05  # the updates do train

@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 
 from oracle import sptrain_oracle as O
-from tests.gpu_util import rel_err, torch
+from tests.gpu_util import record, rel_err, torch
 
 pytestmark = pytest.mark.gpu
 
@@ -78,6 +78,9 @@ def test_attention_at_target_rank_shape(name, s, hq, hkv, n_rows, n_cols):
     dk_r, dv_r = O.attention_bwd_cols(q, k, v, do, lse_d, D, cols)
     assert rel_err(dk_d[cols], dk_r) <= 2e-2, rel_err(dk_d[cols], dk_r)
     assert rel_err(dv_d[cols], dv_r) <= 2e-2, rel_err(dv_d[cols], dv_r)
+    record(f"attention_{name}", o_rows=rel_err(o_d[rows], o_r), lse_max_abs=np.max(np.abs(lse_d[:, rows] - lse_r)),
+           dq_rows=rel_err(dq_d[rows], dq_r), dk_cols=rel_err(dk_d[cols], dk_r), dv_cols=rel_err(dv_d[cols], dv_r),
+           rows=len(rows), cols=len(cols))
 
 
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (32, 2)])
@@ -198,6 +201,9 @@ def test_l8_full_step_loss_on_sampled_tokens():
     z = _rms(x2, g3)
     ref = T.nn.functional.cross_entropy(z @ wlm.t(), lab[tok_d], reduction="mean")
     ref.backward()
-    assert abs(loss - float(ref)) / abs(float(ref)) <= 1e-3, (loss, float(ref))
+    ref = float(ref.detach())
+    record("l8_full_step_sampled_tokens", loss=loss, ref_loss=ref, loss_rel=abs(loss - ref) / abs(ref),
+           dwlm=rel_err(gwlm.cpu().numpy(), wlm.grad.cpu().numpy()), dg3=rel_err(gg3.cpu().numpy(), g3.grad.cpu().numpy()))
+    assert abs(loss - ref) / abs(ref) <= 1e-3, (loss, ref)
     assert rel_err(gwlm.cpu().numpy(), wlm.grad.cpu().numpy()) <= 2e-2
     assert rel_err(gg3.cpu().numpy(), g3.grad.cpu().numpy()) <= 2e-2
