@@ -63,5 +63,50 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+
+
+# ---------------------------------------------------------------------------------------------------------
+# The reference-API drop-in (include/sptrain/gpu.hpp): sptrain::gpu ops and the autograd.hpp definitions,
+# compiled against the reference's own headers and linked with the reference's own tensor.cpp / ledger.cpp,
+# both compiled in place from /root/reference (never copied into this repo).  Built here, where the reference
+# exists; the outputs in _ext/ travel to the GPU box with the snapshot (git-ignored, not gpurun-ignored).
+REF = "/root/reference/proj"
+EXT = os.path.join(HERE, "_ext")
+EXT_LIB = os.path.join(EXT, "libsptrain_ext.so")
+EXT_TEST = os.path.join(EXT, "tensor_ext_test")
+CUDA = "/usr/local/cuda"
+
+
+def build_ext() -> str | None:
+    """Build _ext/libsptrain_ext.so and the C++ test program; None when the reference is not present."""
+    if not os.path.isdir(os.path.join(REF, "include", "sptrain")):
+        return None
+    os.makedirs(EXT, exist_ok=True)
+    srcs = [os.path.join(REF, "src", "tensor.cpp"), os.path.join(REF, "src", "ledger.cpp"),
+            os.path.join(HERE, "sptrain_ext", "autograd.cpp"), os.path.join(HERE, "sptrain_ext", "gpu_ops.cpp")]
+    hdrs = [os.path.join(ROOT, "include", "sptrain", "gpu.hpp"), os.path.join(ROOT, "include", "sptrain_b200.h")]
+    inc = ["-I", os.path.join(REF, "include"), "-I", os.path.join(ROOT, "include"), "-I", os.path.join(CUDA, "include")]
+    link = ["-L", HERE, "-lsptrain_b200", f"-Wl,-rpath,{HERE}", "-L", os.path.join(CUDA, "lib64"), "-lcudart",
+            f"-Wl,-rpath,{os.path.join(CUDA, 'lib64')}", "-lpthread"]
+
+    def stale(out, deps):
+        return not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(d) for d in deps)
+
+    if stale(EXT_LIB, srcs + hdrs + [LIB]):
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", *inc, *srcs, "-o", EXT_LIB, *link]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"libsptrain_ext build failed:\n{r.stderr}")
+    test_src = os.path.join(ROOT, "tests", "cpp", "tensor_ext_test.cpp")
+    if stale(EXT_TEST, [test_src, EXT_LIB] + hdrs):
+        cmd = ["g++", "-std=c++20", "-O2", *inc, test_src, "-o", EXT_TEST, "-L", EXT, "-lsptrain_ext",
+               f"-Wl,-rpath,{EXT}", *link]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"tensor_ext_test build failed:\n{r.stderr}")
+    return EXT_LIB
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    print(build_ext())
