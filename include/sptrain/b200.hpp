@@ -179,7 +179,7 @@ struct StepOptions {
     int n_layers = 1;            // > 1: per-layer activation checkpointing
     bool ckpt_offload = false;   // checkpoints in pinned host memory
     bool packed = false;         // block-causal attention from position_ids
-    int mlp_tiles = 0;           // 0 -> ceil(s_loc / hidden)
+    int mlp_tiles = 0;           // 0: 2 GiB intermediate budget; -1: ceil(s_loc / hidden)
     int64_t loss_tile = 0;       // tokens per logits tile, 0 -> auto
     float lr = 0.f;              // > 0: plain SGD update after the step
     float rms_eps = 1e-5f;

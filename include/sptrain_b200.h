@@ -284,7 +284,8 @@ typedef struct {
     int32_t intermediate;
     int64_t vocab;
     int64_t seq_len;   /* global sequence length (sum over ranks), bs = 1 */
-    int32_t mlp_tiles; /* 0 -> ceil(s_loc / hidden) */
+    int32_t mlp_tiles; /* > 0: that many TiledMLP tiles; -1: ceil(s_loc / hidden); 0: fewest tiles whose
+                          intermediates fit 2 GiB (16384-token tiles at Llama-3-8B shapes) */
     int64_t loss_tile; /* tokens per logits tile, 0 -> auto */
     float rms_eps;     /* 0 -> 1e-5 */
     int32_t packed;    /* 1: block-causal attention from position_ids */

@@ -286,8 +286,20 @@ static void build_layer(spt_layer* Ly) {
     SPT_CHECK(Ly->h % 64 == 0 && Ly->qkv_out % 64 == 0 && Ly->I % 32 == 0 && Ly->V % 64 == 0, SPT_ERR_CONFIG,
               "hidden, qkv width and vocab must be multiples of 64, intermediate of 32");
     SPT_CHECK(Ly->N % 128 == 0, SPT_ERR_CONFIG, "seq_len must be a multiple of 128 (attention tile)");
-    const int64_t mtiles = c.mlp_tiles > 0 ? c.mlp_tiles : std::max<int64_t>(1, (Ly->n_loc + Ly->h - 1) / Ly->h);
-    Ly->mlp_tile = (Ly->n_loc + mtiles - 1) / mtiles;  // SPEC.md:398 ceil(s/h) tiles
+    // TiledMLP tiles.  mlp_tiles > 0: that many; -1: the SPEC default ceil(s/h); 0 (default): the
+    // fewest tiles whose per-tile intermediates ([tile, I] x 2 + [tile, 2I] bf16 = tile * I * 8 bytes) fit a
+    // fixed 2 GiB budget, split evenly — still O(1) in the sequence length, but 16384-token tiles at
+    // Llama-3-8B shapes instead of 4096: the weight-gradient GEMMs accumulate over 4x longer K and the
+    // 4096-row GEMMs stop wasting a partial last wave (tools/config_ab.py mlp_tiles: -2.3% step time at L1,
+    // profiles/r2_mlp_tiles_ab.json).  Values are tiling-invariant.
+    int64_t mtiles;
+    if (c.mlp_tiles > 0) mtiles = c.mlp_tiles;
+    else if (c.mlp_tiles < 0) mtiles = std::max<int64_t>(1, (Ly->n_loc + Ly->h - 1) / Ly->h);
+    else {
+        const int64_t tmax = std::max<int64_t>(128, (int64_t)((2ll << 30) / (Ly->I * 8)) / 128 * 128);
+        mtiles = std::max<int64_t>(1, (Ly->n_loc + tmax - 1) / tmax);
+    }
+    Ly->mlp_tile = (Ly->n_loc + mtiles - 1) / mtiles;
     if (c.loss_tile > 0) Ly->loss_tile = std::min<int64_t>(c.loss_tile, Ly->n_loc);
     else {
         // tile_len * V * 4 <= 4 GiB (SPEC.md:423 budget).  8192 tokens at V=128256: the 4096 x 4096

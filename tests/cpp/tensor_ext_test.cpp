@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <random>
 #include <string>
 #include <thread>
@@ -257,6 +258,10 @@ static void write_out(const char* path, const std::vector<std::pair<std::string,
 }
 
 static void gpu_step(int P, const char* in_path, const char* out_path, bool ckpt) {
+    // one MemoryLedger per rank thread, declared first: it must outlive every buffer registered in it (the
+    // replicated weights' grads are created lazily inside the rank threads)
+    std::vector<std::unique_ptr<MemoryLedger>> leds;
+    for (int r = 0; r < P; ++r) leds.push_back(std::make_unique<MemoryLedger>());
     const Inputs in = read_inputs(in_path);
     const Cfg& c = in.c;
     const int64_t s_loc = c.N / P;
@@ -273,7 +278,7 @@ static void gpu_step(int P, const char* in_path, const char* out_path, bool ckpt
     for (int r = 0; r < P; ++r)
         th.emplace_back([&, r] {
             try {
-                MemoryLedger led;
+                MemoryLedger& led = *leds[r];
                 LedgerScope scope(led);
                 xs[r] = leaf(in.x, {s_loc, c.h}, true, r * s_loc * c.h);
                 std::vector<int64_t> lab(in.labels.begin() + r * s_loc, in.labels.begin() + (r + 1) * s_loc);
