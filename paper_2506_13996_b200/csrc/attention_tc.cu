@@ -53,6 +53,9 @@ __device__ __forceinline__ float ex2_poly(float x) {
 #ifndef SPT_DQ_MC_DEFAULT
 #define SPT_DQ_MC_DEFAULT 0
 #endif
+#ifndef SPT_ATTN_BWD_DEFAULT
+#define SPT_ATTN_BWD_DEFAULT 0
+#endif
 #ifndef SPT_DKDV_MC_DEFAULT
 #define SPT_DKDV_MC_DEFAULT 1
 #endif
@@ -2516,6 +2519,417 @@ __global__ void __launch_bounds__(dkvq::THREADS, 1)
     }
 }
 
+// ------------------------------------------------------------------ fused dK / dV / dQ pass, clusters of 4
+// The fused pass above computes 5 matmuls per tile pair instead of 7, but sends a 32 KiB fp32 dQ partial per
+// (128-key, 64-query) tile pair through L2 reductions, which sustain only ~2.2 TB/s (69 GB at s = 32K).  Here
+// four CTAs with CONSECUTIVE key blocks form a cluster and walk one shared (q head, q block) sequence in
+// lockstep (the union of their visible q blocks; blocks below a CTA's own keys are fully masked): each CTA
+// TMA-multicasts a quarter of every Q / dO stage into all four (a quarter of the L2->SM bytes per CTA), and
+// the four dQ partials of an iteration are summed through distributed shared memory before ONE reduction per
+// cluster reaches global memory — CTA c adds rows [16c, 16c + 16) of the 64-query block, summing the four
+// partials in descending key-block order.  A quarter of the reduction bytes, so the pass stays tensor-bound.
+//
+// Determinism: within a cluster the order is fixed (key block 4cl+3 down to 4cl); across
+// clusters the contributions to a (q head, q block) are added in descending cluster order, enforced by the
+// per-(head, q block) counter as in dkdvq_tc_kernel (4 publications per cluster).  Clusters are launched in
+// descending order, so a cluster only ever waits on clusters launched before it.  Plain causal attention only
+// (packed sequences keep the two-pass scheme), s % 512 == 0.
+namespace dkvq4 {
+constexpr int BQB = 64;
+constexpr int KB_BYTES = 128 * D * 2;                             // K or V block, 32 KiB
+constexpr int QS_BYTES = BQB * D * 2;                             // Q or dO tile, 16 KiB (two 8 KiB regions)
+constexpr int NQS = 3;                                            // Q/dO ring stages
+constexpr int DS_BYTES = 128 * BQB * 2;                           // dS^T [128 keys][64 q] bf16, 16 KiB
+constexpr int STG_BYTES = BQB * D * 4;                            // this CTA's dQ partial [64 q][128 d] fp32
+constexpr int OUT_BYTES = 16 * D * 4;                             // reduced rows [16 q][128 d] fp32
+constexpr int OFF_K = 0, OFF_V = KB_BYTES, OFF_QS = 2 * KB_BYTES;  // NQS stages x (Q, dO)
+constexpr int OFF_DS = OFF_QS + NQS * 2 * QS_BYTES;
+constexpr int OFF_STG = OFF_DS + DS_BYTES;
+constexpr int OFF_OUT = OFF_STG + STG_BYTES;                      // 2 buffers
+constexpr int OFF_LD = OFF_OUT + 2 * OUT_BYTES;                   // NQS x (lse*log2e[64], D[64]) fp32
+constexpr int OFF_BAR = OFF_LD + NQS * 512;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr int NDRAIN = 4;
+constexpr int THREADS = (BW_NEW + 2 + NDRAIN) * 32;
+constexpr int W_DRAIN0 = BW_NEW + 2;
+constexpr int CL = 4;  // cluster size (key blocks per cluster)
+static_assert(SMEM <= 232448, "dkvq4 smem");
+}  // namespace dkvq4
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void drain4_bar() { asm volatile("bar.sync 1, %0;" ::"n"(dkvq4::NDRAIN * 32) : "memory"); }
+
+__global__ void __launch_bounds__(dkvq4::THREADS, 1)
+    dkdvq4_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
+                  const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const float* __restrict__ lse2v,
+                  const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv,
+                  const __grid_constant__ CUtensorMap tdq, int* __restrict__ dq_cnt) {
+    using namespace dkvq4;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* kv_full = bar;
+    uint64_t* qs_full = bar + 1;          // [NQS]
+    uint64_t* qs_empty = qs_full + NQS;   // [NQS] count 4: every CTA's MMAs are done with the stage
+    uint64_t* s_full = qs_empty + NQS;    // [2]
+    uint64_t* pd_full = s_full + 2;       // [2]
+    uint64_t* dq_full = pd_full + 2;      // [2]
+    uint64_t* dq_drained = dq_full + 2;   // [2]
+    uint64_t* ds_free = dq_drained + 2;
+    uint64_t* acc_done = ds_free + 1;
+    uint64_t* stg_full = acc_done + 1;    // count 4: every CTA's dQ partial of the iteration is staged
+    uint64_t* stg_free = stg_full + 1;    // count 4: every CTA has read this CTA's staged partial
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_free + 1);
+    const int warp = warp_id(), lane = lane_id();
+    const int nkb = (int)(s / 128);
+    const uint32_t crank = cluster_ctarank();
+    const int cl = nkb / CL - 1 - (int)(blockIdx.y / CL);  // DESCENDING clusters (dQ ordering)
+    const int kb = cl * CL + (int)crank;
+    const int kvh = blockIdx.x;
+    const int grp = hq / hkv;
+    const int64_t k0 = (int64_t)kb * 128;
+    const int nqb_all = (int)(s / BQB);
+    const int qb_first = cl * CL * 128 / BQB;  // the cluster's lowest key block's first q block
+    const int nqb = nqb_all - qb_first;
+    const int total = nqb * grp;
+    if (threadIdx.x == 0) {
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < NQS; ++i) {
+            mbar_init(&qs_full[i], 1);
+            mbar_init(&qs_empty[i], CL);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&pd_full[i], BW_NEW * 32);
+            mbar_init(&dq_full[i], 1);
+            mbar_init(&dq_drained[i], NDRAIN * 32);
+        }
+        mbar_init(ds_free, 1);
+        mbar_init(acc_done, 1);
+        mbar_init(stg_full, CL);
+        mbar_init(stg_free, CL);
+        fence_barrier_init();
+    }
+    if (warp == BW_MMA) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    cluster_sync();  // every CTA's barriers initialised before any multicast load / remote arrive
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t sbase = smem_u32(smem);
+    if (warp == BW_TMA) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(kv_full, 2 * KB_BYTES);
+            for (int r = 0; r < 2; ++r) {
+                tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
+                tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
+            }
+            int hh = kvh * grp, qblk = 0;
+            for (int it = 0; it < total; ++it) {
+                const int st = it % NQS;
+                mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);  // all four CTAs released the stage
+                mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES + 512);
+                const int qq = (qb_first + qblk) * BQB;
+                const int hcur = hh;
+                if (++qblk == nqb) { qblk = 0; ++hh; }
+                uint8_t* base = smem + OFF_QS + st * 2 * QS_BYTES;
+                // this CTA's quarter of the stage, multicast into all four: Q / dO 64-column regions, lse / D
+                const int r = (int)(crank & 1);
+                if (crank < 2) {
+                    tma_load_2d_mc(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq, 0xF);
+                    if (crank == 0)
+                        bulk_load_mc(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st], 0xF);
+                } else {
+                    tma_load_2d_mc(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq, 0xF);
+                    if (crank == 2)
+                        bulk_load_mc(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st],
+                                     0xF);
+                }
+            }
+        }
+    } else if (warp == BW_MMA) {
+        constexpr uint32_t id_s = make_idesc_bf16(128, BQB, false, false);
+        constexpr uint32_t id_a = make_idesc_bf16(128, D, false, true);
+        constexpr uint32_t id_q = make_idesc_bf16(128, BQB, true, true);  // dQ^T = K^T dS^T: both MN-major
+        mbar_wait(kv_full, 0);
+        const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V, dsa = sbase + OFF_DS;
+        auto issue_sdp = [&](int it) {
+            const int st = it % NQS;
+            mbar_wait(&qs_full[st], (it / NQS) & 1);
+            tc_fence_after();
+            const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+            const uint32_t d_s = tmem + (it & 1) * 128;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+                mma_bf16_ss_w(d_s, kdesc_r(ka, kk, 16384), kdesc_r(qb_, kk, 8192), id_s, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+                mma_bf16_ss_w(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
+            mma_commit_w(&s_full[it & 1]);
+        };
+        auto issue_acc = [&](int it) {
+            const int b = it & 1, st = it % NQS;
+            mbar_wait(&pd_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < 128 / 16; ++kk)
+                mma_bf16_ss_w(tmem + b * 128 + 64, mndesc_r(ka, kk, 16384), mndesc_r(dsa, kk, 16384), id_q, kk > 0);
+            mma_commit_w(&dq_full[b]);
+            mma_commit_w(ds_free);
+#pragma unroll
+            for (int kk = 0; kk < BQB / 16; ++kk)
+                mma_bf16_ts_w(tmem + 256, tmem + b * 128 + kk * 16, mndesc_r(dob, kk, 8192), id_a, (it > 0 || kk > 0));
+#pragma unroll
+            for (int kk = 0; kk < BQB / 16; ++kk)
+                mma_bf16_ts_w(tmem + 384, tmem + b * 128 + kk * 16 + 8, mndesc_r(qb_, kk, 8192), id_a,
+                              (it > 0 || kk > 0));
+            mma_commit_mc_w(&qs_empty[st], 0xF);  // the stage is free once every CTA's MMAs have read it
+        };
+        if (total > 0) issue_sdp(0);
+        if (total > 1) issue_sdp(1);
+        for (int it = 0; it < total; ++it) {
+            issue_acc(it);
+            if (it + 2 < total) {
+                mbar_wait(&dq_drained[it & 1], (it >> 1) & 1);
+                tc_fence_after();
+                issue_sdp(it + 2);
+            }
+        }
+        mma_commit_w(acc_done);
+    } else if (warp >= W_DRAIN0) {
+        // ---- drain: dQ^T partial (TMEM lane = d) -> staging [q][d] -> cluster sum of rows [16c, 16c+16) ->
+        // ordered bulk add into dq_acc
+        const int dw = warp & 3;
+        const int d = dw * 32 + lane;
+        const uint32_t lo = (uint32_t)(dw * 32) << 16;
+        const int t = threadIdx.x - W_DRAIN0 * 32;  // 0..127
+        const bool leader = t == 0;
+        const uint32_t stg = sbase + OFF_STG;
+        uint32_t peer_stg[CL], peer_full[CL], peer_free[CL];
+#pragma unroll
+        for (int j = 0; j < CL; ++j) {
+            peer_stg[j] = mapa_shared(stg, (uint32_t)j);
+            peer_full[j] = mapa_shared(smem_u32(stg_full), (uint32_t)j);
+            peer_free[j] = mapa_shared(smem_u32(stg_free), (uint32_t)j);
+        }
+        const int rrow = (int)crank * 16 + (t >> 3);  // the q row of the block this thread reduces
+        const int rcol = (t & 7) * 16;                // its 16 d columns
+        int hh = kvh * grp, qblk = 0;
+        int prev_cnt_idx = -1;
+        for (int it = 0; it < total; ++it) {
+            const int b = it & 1;
+            const int jq = qb_first + qblk;
+            const int hcur = hh;
+            if (++qblk == nqb) { qblk = 0; ++hh; }
+            mbar_wait(&dq_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t v[64];
+            tmem_ld32(tmem + lo + b * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+            tmem_ld32(tmem + lo + b * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&dq_drained[b]);
+            // the staging buffer is free once all four CTAs read the previous iteration's partial from it
+            if (it > 0) mbar_wait_cluster(stg_free, (it - 1) & 1);
+#pragma unroll
+            for (int q = 0; q < 64; ++q)
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg + q * 512 + d * 4), "f"(__uint_as_float(v[q])) : "memory");
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");  // rows visible to the peers' DSMEM loads
+            drain4_bar();
+            if (leader) {
+#pragma unroll
+                for (int j = 0; j < CL; ++j) mbar_arrive_cluster(peer_full[j]);  // release.cluster: rows visible
+            }
+            mbar_wait_cluster(stg_full, it & 1);  // all four partials staged
+            // sum rows [16c, 16c+16) over the four CTAs, descending key block (fixed order)
+            float4 acc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = ld_dsmem_f4(peer_stg[CL - 1] + rrow * 512 + (rcol + 4 * k) * 4);
+#pragma unroll
+            for (int j = CL - 2; j >= 0; --j) {
+                float4 x[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[k] = ld_dsmem_f4(peer_stg[j] + rrow * 512 + (rcol + 4 * k) * 4);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    acc[k].x += x[k].x;
+                    acc[k].y += x[k].y;
+                    acc[k].z += x[k].z;
+                    acc[k].w += x[k].w;
+                }
+            }
+            drain4_bar();  // every thread of this CTA finished reading the four partials
+            if (leader) {
+#pragma unroll
+                for (int j = 0; j < CL; ++j) mbar_arrive_cluster(peer_free[j]);
+                bulk_wait_read<1>();  // the reduction issued two iterations ago has read out[b]
+            }
+            drain4_bar();
+            const uint32_t out = sbase + OFF_OUT + b * OUT_BYTES;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(out + (t >> 3) * 512 + (rcol + 4 * k) * 4),
+                             "f"(acc[k].x), "f"(acc[k].y), "f"(acc[k].z), "f"(acc[k].w)
+                             : "memory");
+            fence_proxy_async();
+            drain4_bar();
+            const int cnt_idx = hcur * nqb_all + jq;
+            if (leader) {
+                const int need = CL * ((jq * BQB / 128) / CL - cl);  // publications of the clusters above
+                if (ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
+                    const long long t0 = clock64();
+                    while (ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
+                        if (clock64() - t0 > (1ll << 35)) {
+                            printf("[spt] dQ4 ordering wait timed out: cluster %d rank %u head %d qblock %d need %d\n",
+                                   cl, crank, hcur, jq, need);
+                            __trap();
+                        }
+                    }
+                }
+                asm volatile(
+                    "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                        &tdq),
+                    "r"(0), "r"(hcur), "r"(jq * BQB + (int)crank * 16), "r"(out)
+                    : "memory");
+                bulk_commit();
+                if (prev_cnt_idx >= 0) {  // publish the previous iteration once its reduction completed
+                    bulk_wait<1>();
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
+                }
+                prev_cnt_idx = cnt_idx;
+            }
+        }
+        if (leader && prev_cnt_idx >= 0) {
+            bulk_wait<0>();
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
+        }
+    } else {
+        // elementwise (as dkdvq_tc_kernel; queries below this CTA's keys come out fully masked)
+        const int sub = warp & 3, grp4 = warp >> 2;
+        const int r = sub * 32 + lane;
+        const int64_t key = k0 + r;
+        const int key32 = (int)key;
+        const uint32_t lo = (uint32_t)(sub * 32) << 16;
+        const float sl2 = scale * LOG2E;
+        const uint32_t ds_row = sbase + OFF_DS + (r >> 3) * 1024 + (r & 7) * 128;
+        const uint32_t ds_c0 = ds_row + ((((uint32_t)(2 * grp4)) ^ (r & 7)) << 4);
+        const uint32_t ds_c1 = ds_row + ((((uint32_t)(2 * grp4 + 1)) ^ (r & 7)) << 4);
+        int qblk = 0;
+        for (int it = 0; it < total; ++it) {
+            const int b = it & 1;
+            const int qq = (qb_first + qblk) * BQB + grp4 * 16;
+            if (++qblk == nqb) qblk = 0;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            uint32_t sv[16], dv[16];
+            tmem_ld16(tmem + lo + b * 128 + grp4 * 16, sv);
+            tmem_ld16(tmem + lo + b * 128 + 64 + grp4 * 16, dv);
+            tmem_ld_wait();
+            const uint32_t lsm = sbase + OFF_LD + (it % NQS) * 512 + grp4 * 64;
+            uint32_t pw[8], sw[8];
+            auto body = [&](auto mask_c) {
+                constexpr bool MASK = decltype(mask_c)::value;
+                const int lo_ = key32 - qq;
+                const uint64_t sl2x = f2pack(sl2, sl2);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float lv[8], dd[8];
+                    lds128(lsm + 32 * k, lv[0], lv[1], lv[2], lv[3]);
+                    lds128(lsm + 32 * k + 16, lv[4], lv[5], lv[6], lv[7]);
+                    lds128(lsm + 256 + 32 * k, dd[0], dd[1], dd[2], dd[3]);
+                    lds128(lsm + 256 + 32 * k + 16, dd[4], dd[5], dd[6], dd[7]);
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int i = 8 * k + e;
+                        float x0, x1;
+                        f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sl2x,
+                                       f2pack(-lv[e], -lv[e + 1])),
+                                 x0, x1);
+                        float p0 = ex2(x0), p1 = ex2(x1);
+                        if constexpr (MASK) {
+                            if (i < lo_) p0 = 0.f;
+                            if (i + 1 < lo_) p1 = 0.f;
+                        }
+                        const uint64_t ds = fmul2(f2pack(p0, p1), fsub2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
+                                                                        f2pack(dd[e], dd[e + 1])));
+                        float s0, s1;
+                        f2unpack(ds, s0, s1);
+                        pw[4 * k + e / 2] = pack_bf16x2(p0, p1);
+                        sw[4 * k + e / 2] = pack_bf16x2(s0, s1);
+                    }
+                }
+            };
+            if (qq < key32 - r + 127) body(std::true_type{});
+            else body(std::false_type{});
+            tmem_st8(tmem + lo + b * 128 + grp4 * 16, pw);
+            tmem_st8(tmem + lo + b * 128 + grp4 * 16 + 8, sw);
+            if (it > 0) mbar_wait(ds_free, (it - 1) & 1);
+            sts128(ds_c0, sw[0], sw[1], sw[2], sw[3]);
+            sts128(ds_c1, sw[4], sw[5], sw[6], sw[7]);
+            fence_proxy_async();
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&pd_full[b]);
+        }
+        mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const int64_t rs = (int64_t)(hq + 2 * hkv) * D;
+        const bool isk = grp4 >= 2;
+        const int c0 = (grp4 & 1) * 64;
+        bf16* dst = dqkv + key * rs + (int64_t)(isk ? (hq + kvh) : (hq + hkv + kvh)) * D + c0;
+        const float mul = isk ? scale : 1.f;
+        const uint32_t acc_tm = tmem + lo + (isk ? 384 : 256) + c0;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            uint32_t v[32];
+            tmem_ld32(acc_tm + c * 32, v);
+            tmem_ld_wait();
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 w;
+                w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+                w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+                w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+                w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+                d4[k] = w;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while a peer may still read its staged partial or multicast into it
+    if (warp == BW_MMA) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // dq (bf16, inside dqkv) = dq_acc * scale
 __global__ void dq_convert_kernel(const float* __restrict__ acc, int64_t s, int hq, int hkv, float scale,
                                   bf16* __restrict__ dqkv) {
@@ -2654,13 +3068,16 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
 // for the two-pass scheme (profiles/README.md).  Experiments: unordered 47.3 ms; unordered and never
 // waiting for reduction completion 31.9 ms, i.e. the reductions alone sustain only ~2.2 TB/s.  Kept for
 // larger tiles (fewer reduction bytes per flop) / GPUs with faster L2 reductions.
-static int bwd_mode() {
-    static const int v = [] {
-        const char* e = getenv("SPT_ATTN_BWD");
-        return (e && std::string(e) == "fused") ? 1 : 0;
-    }();
-    return v;
-}
+// SPT_ATTN_BWD=fused4 (or spt_tuning_set("attn_bwd", 2)): the fused pass on clusters of four key blocks
+// with the dQ partials summed through distributed shared memory first (dkdvq4_kernel; plain causal,
+// s % 512 == 0; anything else takes the two-pass scheme).
+int g_attn_bwd = [] {
+    const char* e = getenv("SPT_ATTN_BWD");
+    if (!e) return SPT_ATTN_BWD_DEFAULT;
+    const std::string v(e);
+    return v == "fused" ? 1 : v == "fused4" ? 2 : 0;
+}();
+static int bwd_mode() { return g_attn_bwd; }
 
 // SPT_ATTN_DKDV_MC=0|1: cluster-pair multicast of the dK/dV pass's Q/dO stream (default from measurement)
 static bool dkdv_multicast() {
@@ -2707,7 +3124,7 @@ int g_attn_dkdv_kt = [] {
 }();
 
 size_t attn_bwd_tc_workspace(int64_t s, int hq) {
-    if (bwd_mode() != 1) return 0;
+    if (bwd_mode() == 0) return 0;
     return (size_t)s * hq * fatc::D * 4 + (size_t)hq * (s / 64) * 4 + 256;
 }
 
@@ -2741,7 +3158,36 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dkvq::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkp::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdvq4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dkvq4::SMEM));
         attr = true;
+    }
+    if (bwd_mode() == 2 && ws != nullptr && seg == nullptr && s % 512 == 0) {
+        float* dq_acc = (float*)ws;
+        int* cnt = (int*)(dq_acc + (size_t)s * hq * fatc::D);
+        SPT_CUDA(cudaMemsetAsync(ws, 0, attn_bwd_tc_workspace(s, hq), st));
+        CUtensorMap tdq = make_tmap_f32_3d(dq_acc, fatc::D, (uint64_t)hq, (uint64_t)s, (uint64_t)fatc::D * 4,
+                                           (uint64_t)hq * fatc::D * 4, fatc::D, 1, 16);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)hkv, (unsigned)(s / 128));
+        cfg.blockDim = dim3(fatc::dkvq4::THREADS);
+        cfg.dynamicSmemBytes = fatc::dkvq4::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.y = fatc::dkvq4::CL;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, fatc::dkdvq4_kernel, t128, t64, do64, s, hq, hkv, lse2, Dv, scale,
+                                    (bf16*)dqkv, tdq, cnt));
+        count_launch("attn_dkdvq4_tc");
+        SPT_CUDA(cudaGetLastError());
+        fatc::dq_convert_kernel<<<148 * 8, 256, 0, st>>>(dq_acc, s, hq, hkv, scale, (bf16*)dqkv);
+        count_launch("attn_dq_convert");
+        SPT_CUDA(cudaGetLastError());
+        return true;
     }
     if (bwd_mode() == 1 && ws != nullptr && attn_bwd_tc_workspace(s, hq) > 0 && s % 256 == 0) {
         float* dq_acc = (float*)ws;

@@ -552,3 +552,45 @@ def test_reshard_pack_rope_bitwise(P, hq, hkv, d, packed):
     T.cuda.synchronize()
     assert T.equal(a.view(T.int16), b.view(T.int16))
     assert T.equal(a.view(T.int16), c.view(T.int16))
+
+
+@pytest.mark.parametrize("s,hq,hkv", [(1024, 4, 1), (2048, 8, 2), (1536, 2, 2), (3072, 16, 4), (512, 4, 4)])
+def test_attention_bwd_fused_cluster4(s, hq, hkv):
+    """Single-pass backward on clusters of four key blocks (attn_bwd=2: 5 matmuls per tile pair, dQ partials
+    summed through distributed shared memory before one ordered reduction per cluster): dQ / dK / dV against
+    the float64 oracle, bitwise deterministic, and dK / dV equal to the two-pass scheme's within bf16 rounding."""
+    T = torch()
+    L = _lib()
+    d = 128
+    qkv, dout, _ = _attn_case(s, hq, hkv, d, False, s + 3 * hq)
+    q, k, v = qkv[:, :hq], qkv[:, hq:hq + hkv], qkv[:, hq + hkv:]
+    qkvd, doutd = bf16_dev(qkv), bf16_dev(dout)
+    o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+    lse = T.empty(hq, s, device="cuda")
+    scale = 1.0 / math.sqrt(d)
+    S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, None, scale, o.data_ptr(), lse.data_ptr(), None))
+    T.cuda.synchronize()
+    outs = {}
+    try:
+        for mode in (0, 2, 2):
+            S.check(L.spt_tuning_set(b"attn_bwd", mode))
+            ws = T.empty(max(1, L.spt_attn_bwd_workspace(s, hq, hkv, d)), dtype=T.uint8, device="cuda")
+            g = T.zeros(s, hq + 2 * hkv, d, dtype=T.bfloat16, device="cuda")
+            S.check(L.spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
+                                   None, scale, g.data_ptr(), ws.data_ptr(), None))
+            T.cuda.synchronize()
+            outs.setdefault(mode, []).append(g)
+    finally:
+        S.check(L.spt_tuning_set(b"attn_bwd", 0))
+    f4 = outs[2][0]
+    assert T.equal(f4.view(T.int16), outs[2][1].view(T.int16))  # deterministic (SPEC.md:102)
+    o_bf = to_np(o).astype(np.float64)
+    _, lse_r = O.attention_fwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), None)
+    dq_r, dk_r, dv_r = O.attention_bwd(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), o_bf, lse_r,
+                                       dout.astype(np.float64), None)
+    g = to_np(f4)
+    assert rel_err(g[:, :hq], dq_r) < 2e-2
+    assert rel_err(g[:, hq:hq + hkv], dk_r) < 2e-2
+    assert rel_err(g[:, hq + hkv:], dv_r) < 2e-2
+    two = to_np(outs[0][0])
+    assert rel_err(g[:, hq:], two[:, hq:].astype(np.float64)) < 1e-2

@@ -34,7 +34,11 @@ for shp in a.shapes.split(","):
     o = torch.empty(s, hq, d, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(hq, s, device="cuda")
     do = torch.randn(s, hq, d, device="cuda", generator=g).bfloat16()
-    ws = torch.empty(L.spt_attn_bwd_workspace(s, hq, hkv, d), dtype=torch.uint8, device="cuda")
+    wsz = 0
+    for v in vals:  # the workspace depends on the backward scheme (attn_bwd): size it for every value
+        S.check(L.spt_tuning_set(key.encode(), v))
+        wsz = max(wsz, L.spt_attn_bwd_workspace(s, hq, hkv, d))
+    ws = torch.empty(max(wsz, 1), dtype=torch.uint8, device="cuda")
     seg = None
     if a.seg:  # segment starts: documents of ragged lengths
         starts = torch.zeros(s, dtype=torch.int32, device="cuda")
