@@ -2583,7 +2583,10 @@ __global__ void __launch_bounds__(dkvq4::THREADS, 1)
     dkdvq4_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                   const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const float* __restrict__ lse2v,
                   const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv,
-                  const __grid_constant__ CUtensorMap tdq, int* __restrict__ dq_cnt) {
+                  const __grid_constant__ CUtensorMap tdq, int* __restrict__ dq_cnt, int dbg) {
+    // dbg (experiments only, spt_tuning_set("attn_bwd4_dbg", bits)): 1 = no dQ reduction at all, 2 = no
+    // cross-cluster ordering wait, 4 = sum only this CTA's own partial (no DSMEM loads), 8 = no in-cluster
+    // staging handshakes, 16 = no global reduction (TMA)
     using namespace dkvq4;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -2738,7 +2741,12 @@ __global__ void __launch_bounds__(dkvq4::THREADS, 1)
         const int rrow = (int)crank * 16 + (t >> 3);  // the q row of the block this thread reduces
         const int rcol = (t & 7) * 16;                // its 16 d columns
         int hh = kvh * grp, qblk = 0;
-        int prev_cnt_idx = -1;
+        // publication of an iteration waits for its reduction to COMPLETE in L2 (~2 us); deferring it by
+        // LAG iterations keeps that round trip off the loop (the next cluster down needs (head, q block) only
+        // 8 iterations after this one produced it)
+        constexpr int LAG = 6;
+        int pend[LAG + 1];
+        int npend = 0;
         for (int it = 0; it < total; ++it) {
             const int b = it & 1;
             const int jq = qb_first + qblk;
@@ -2752,24 +2760,25 @@ __global__ void __launch_bounds__(dkvq4::THREADS, 1)
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(&dq_drained[b]);
+            if (dbg & 1) continue;
             // the staging buffer is free once all four CTAs read the previous iteration's partial from it
-            if (it > 0) mbar_wait_cluster(stg_free, (it - 1) & 1);
+            if (it > 0 && !(dbg & 8)) mbar_wait_cluster(stg_free, (it - 1) & 1);
 #pragma unroll
             for (int q = 0; q < 64; ++q)
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg + q * 512 + d * 4), "f"(__uint_as_float(v[q])) : "memory");
-            asm volatile("fence.acq_rel.cluster;" ::: "memory");  // rows visible to the peers' DSMEM loads
-            drain4_bar();
-            if (leader) {
+            drain4_bar();  // the leader's release.cluster arrive below is cumulative over these rows
+            if (leader && !(dbg & 8)) {
 #pragma unroll
                 for (int j = 0; j < CL; ++j) mbar_arrive_cluster(peer_full[j]);  // release.cluster: rows visible
             }
-            mbar_wait_cluster(stg_full, it & 1);  // all four partials staged
+            if (!(dbg & 8)) mbar_wait_cluster(stg_full, it & 1);  // all four partials staged
             // sum rows [16c, 16c+16) over the four CTAs, descending key block (fixed order)
             float4 acc[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] = ld_dsmem_f4(peer_stg[CL - 1] + rrow * 512 + (rcol + 4 * k) * 4);
+            for (int k = 0; k < 4; ++k)
+                acc[k] = ld_dsmem_f4(peer_stg[(dbg & 4) ? crank : CL - 1] + rrow * 512 + (rcol + 4 * k) * 4);
 #pragma unroll
-            for (int j = CL - 2; j >= 0; --j) {
+            for (int j = CL - 2; j >= 0 && !(dbg & 4); --j) {
                 float4 x[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) x[k] = ld_dsmem_f4(peer_stg[j] + rrow * 512 + (rcol + 4 * k) * 4);
@@ -2783,8 +2792,10 @@ __global__ void __launch_bounds__(dkvq4::THREADS, 1)
             }
             drain4_bar();  // every thread of this CTA finished reading the four partials
             if (leader) {
+                if (!(dbg & 8)) {
 #pragma unroll
-                for (int j = 0; j < CL; ++j) mbar_arrive_cluster(peer_free[j]);
+                    for (int j = 0; j < CL; ++j) mbar_arrive_cluster(peer_free[j]);
+                }
                 bulk_wait_read<1>();  // the reduction issued two iterations ago has read out[b]
             }
             drain4_bar();
@@ -2799,7 +2810,7 @@ __global__ void __launch_bounds__(dkvq4::THREADS, 1)
             const int cnt_idx = hcur * nqb_all + jq;
             if (leader) {
                 const int need = CL * ((jq * BQB / 128) / CL - cl);  // publications of the clusters above
-                if (ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
+                if (!(dbg & 2) && ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
                     const long long t0 = clock64();
                     while (ld_acquire_gpu(dq_cnt + cnt_idx) < need) {
                         if (clock64() - t0 > (1ll << 35)) {
@@ -2809,24 +2820,29 @@ __global__ void __launch_bounds__(dkvq4::THREADS, 1)
                         }
                     }
                 }
-                asm volatile(
-                    "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                        &tdq),
-                    "r"(0), "r"(hcur), "r"(jq * BQB + (int)crank * 16), "r"(out)
-                    : "memory");
+                if (!(dbg & 16))
+                    asm volatile(
+                        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                            &tdq),
+                        "r"(0), "r"(hcur), "r"(jq * BQB + (int)crank * 16), "r"(out)
+                        : "memory");
                 bulk_commit();
-                if (prev_cnt_idx >= 0) {  // publish the previous iteration once its reduction completed
-                    bulk_wait<1>();
+                pend[npend++] = cnt_idx;
+                if (dbg & 32) npend = 0;
+                if (npend > LAG) {  // the oldest pending iteration's reduction is complete: publish it
+                    bulk_wait<LAG>();
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
+                    red_release_gpu_add(dq_cnt + pend[0], 1);
+#pragma unroll
+                    for (int i = 0; i < LAG; ++i) pend[i] = pend[i + 1];
+                    --npend;
                 }
-                prev_cnt_idx = cnt_idx;
             }
         }
-        if (leader && prev_cnt_idx >= 0) {
+        if (leader && npend > 0) {
             bulk_wait<0>();
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            red_release_gpu_add(dq_cnt + prev_cnt_idx, 1);
+            for (int i = 0; i < npend; ++i) red_release_gpu_add(dq_cnt + pend[i], 1);
         }
     } else {
         // elementwise (as dkdvq_tc_kernel; queries below this CTA's keys come out fully masked)
@@ -3078,6 +3094,7 @@ int g_attn_bwd = [] {
     return v == "fused" ? 1 : v == "fused4" ? 2 : 0;
 }();
 static int bwd_mode() { return g_attn_bwd; }
+int g_attn_bwd4_dbg = 0;  // dkdvq4_kernel experiment bits (wrong dQ when non-zero; timing only)
 
 // SPT_ATTN_DKDV_MC=0|1: cluster-pair multicast of the dK/dV pass's Q/dO stream (default from measurement)
 static bool dkdv_multicast() {
@@ -3181,7 +3198,7 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         cfg.attrs = at;
         cfg.numAttrs = 1;
         SPT_CUDA(cudaLaunchKernelEx(&cfg, fatc::dkdvq4_kernel, t128, t64, do64, s, hq, hkv, lse2, Dv, scale,
-                                    (bf16*)dqkv, tdq, cnt));
+                                    (bf16*)dqkv, tdq, cnt, g_attn_bwd4_dbg));
         count_launch("attn_dkdvq4_tc");
         SPT_CUDA(cudaGetLastError());
         fatc::dq_convert_kernel<<<148 * 8, 256, 0, st>>>(dq_acc, s, hq, hkv, scale, (bf16*)dqkv);

@@ -289,6 +289,7 @@ extern int g_attn_fwd_bk128;  // attention_tc.cu
 extern int g_attn_fwd_hybrid;  // attention_tc.cu
 extern int g_replay_fault;     // engine.cu
 extern int g_attn_bwd;         // attention_tc.cu
+extern int g_attn_bwd4_dbg;    // attention_tc.cu
 }
 
 extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
@@ -329,6 +330,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         }
         if (n == "attn_bwd") {  // 0 two-pass, 1 fused (ordered L2 reductions), 2 fused on clusters of 4
             spt::g_attn_bwd = value;
+            return;
+        }
+        if (n == "attn_bwd4_dbg") {  // timing experiments of the cluster-4 backward (results wrong when set)
+            spt::g_attn_bwd4_dbg = value;
             return;
         }
         if (n == "replay_fault") {  // test-only: corrupt the next checkpoint replay (DeterminismError path)

@@ -21,10 +21,14 @@ ap.add_argument("--shapes", default="32768x32x8,131072x4x1")
 ap.add_argument("--rounds", type=int, default=5)
 ap.add_argument("--seg", action="store_true", help="packed sequences (block-causal) instead of plain causal")
 ap.add_argument("--fwd", action="store_true", help="time (and compare) the forward instead of the backward")
+ap.add_argument("--set", action="append", default=[], help="extra fixed switch name=value (repeatable)")
 a = ap.parse_args()
 key, vals = a.switch.split("=")
 vals = [int(v) for v in vals.split(",")]
 L = S.lib()
+for kv in a.set:
+    k_, v_ = kv.split("=")
+    S.check(L.spt_tuning_set(k_.encode(), int(v_)))
 d = 128
 out = []
 for shp in a.shapes.split(","):
