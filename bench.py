@@ -184,12 +184,11 @@ def make_group(S, args, rank, world, local_rank):
         return S.ProcessGroup.peer_group(world, rank, local_rank)  # IPC handles exchanged over torch.distributed
     import torch.distributed as dist
 
-    dev = torch.device("cuda", local_rank)
-    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    uid = torch.zeros(128, dtype=torch.uint8)
     if rank == 0:
         uid.copy_(torch.frombuffer(bytearray(S.ProcessGroup.unique_id()), dtype=torch.uint8))
     dist.broadcast(uid, 0)
-    return S.ProcessGroup.nccl_group(bytes(uid.cpu().numpy().tobytes()), world, rank, local_rank)
+    return S.ProcessGroup.nccl_group(bytes(uid.numpy().tobytes()), world, rank, local_rank)
 
 
 def est_max_seq(S, shp, mem, n_loc, world):
@@ -459,6 +458,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SPT_BENCH_SAME_GPU") == "1":
+        # functional test of the multi-process path on a one-GPU box: every rank on cuda:0 (the peer transport
+        # maps the other processes' buffers with CUDA IPC as across GPUs; timings are time-sliced, not scaling)
+        local_rank = 0
     if world != args.gpus and rank == 0:
         print(f"[bench] note: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
@@ -469,7 +472,9 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # torch.distributed is only the control plane (IPC-handle / NCCL-id exchange, barriers, the max over
+        # ranks of the timings): gloo on host tensors; the data plane is the engine's own transport
+        dist.init_process_group("gloo")
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -51,3 +51,23 @@ def test_b200_arm_contract():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("port", "reference")
+
+
+@pytest.mark.gpu
+def test_b200_arm_two_ranks_peer_transport_same_gpu():
+    """The N > 1 bench path end to end on the one-GPU box: `--gpus 2` re-launches itself under
+    torch.distributed.run, both ranks run on cuda:0 (SPT_BENCH_SAME_GPU=1) on the peer transport (CUDA IPC),
+    the step is graph-captured and replayed in both processes, rank 0 prints one line with n_gpus = 2 and the
+    per-collective all-to-all payload rates.  (Timings are time-sliced between the processes: this checks the
+    plumbing, not scaling.)"""
+    env = dict(os.environ, SPT_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+                        "--seq", "4096"], capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["sp_degree"] == 2 and d["config"]["transport"] == "peer"
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["timing"] == "cuda-graph replay"
+    assert {"a2a_qkv", "a2a_o", "a2a_do", "a2a_dqkv"} <= set(d["all_to_all"])
+    assert all(v["gbps"] and v["gbps"] > 0 for v in d["all_to_all"].values())
