@@ -223,7 +223,7 @@ def run_ours(args, rank, world, local_rank):
     n_loc = seq // world
     shp = S.ModelShape(**SHAPES[args.workload])
     eng = S.UlyssesLayerStep(shp, seq, grp, lr=args.lr, n_layers=args.layers, ckpt_offload=args.offload,
-                             rope_theta=args.rope)
+                             rope_theta=args.rope, loss_tile=args.loss_tile)
     # random-init weights of the architecture, identical on every rank (same seed)
     g = torch.Generator(device=dev).manual_seed(1234)
     qkv_out = (shp.q_heads + 2 * shp.kv_heads) * shp.head_dim
@@ -440,6 +440,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--comm", default="peer", choices=["peer", "nccl"], help="SP transport for N > 1")
     ap.add_argument("--lr", type=float, default=0.0)
+    ap.add_argument("--loss-tile", type=int, default=0, help="tokens per tiled-logits/CE tile (0: the engine's rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 256 for l1, 2048 for tiny)")
     ap.add_argument("--layers", type=int, default=1,

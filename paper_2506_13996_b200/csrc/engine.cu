@@ -41,6 +41,7 @@
 namespace spt {
 
 size_t flce_workspace(int64_t tile_n, int64_t V);
+int64_t flce_default_tile(int64_t n_loc, int64_t V);
 void flce(const void* x, const void* w, const int64_t* labels, int64_t n, int64_t h, int64_t V, int64_t tile_n,
           const float* scale_dev, double* loss_sum_accum, void* dx, float* dw, bool dw_accumulate, int32_t* err,
           void* ws, cudaStream_t st);
@@ -302,12 +303,7 @@ static void build_layer(spt_layer* Ly) {
     Ly->mlp_tile = (Ly->n_loc + mtiles - 1) / mtiles;
     if (c.loss_tile > 0) Ly->loss_tile = std::min<int64_t>(c.loss_tile, Ly->n_loc);
     else {
-        // tile_len * V * 4 <= 4 GiB (SPEC.md:423 budget).  8192 tokens at V=128256: the 4096 x 4096
-        // dx GEMM then has 2x the cluster tiles (no wave-quantisation tail) and dW is re-read half as often.
-        const int64_t tmax = std::max<int64_t>(128, (int64_t)((4ll << 30) / (Ly->V * 4)) / 128 * 128);
-        const int64_t ntl = (Ly->n_loc + tmax - 1) / tmax;            // fewest tiles within the budget,
-        const int64_t t = ((Ly->n_loc + ntl - 1) / ntl + 127) / 128 * 128;  // split evenly
-        Ly->loss_tile = std::min<int64_t>(std::min(t, tmax), Ly->n_loc);
+        Ly->loss_tile = flce_default_tile(Ly->n_loc, Ly->V);  // tiled.cu
     }
     auto& L_ = Ly->led;
     const int64_t h = Ly->h, I = Ly->I, V = Ly->V;

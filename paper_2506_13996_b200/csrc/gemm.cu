@@ -179,6 +179,7 @@ static void dispatch_pair(const GemmOperand& A, const GemmOperand& B, int64_t M,
         case 0 * 8 + EPI_SWIGLU: launch_gemm2<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); return;
         case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm2<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); return;
         case 0 * 8 + EPI_F32_STATS: launch_gemm2<BN, false, false, EPI_F32_STATS>(ta, tb, m, n, k, ep, st); return;
+        case 0 * 8 + EPI_EXP_STATS: launch_gemm2<BN, false, false, EPI_EXP_STATS>(ta, tb, m, n, k, ep, st); return;
         case 1 * 8 + EPI_BF16: launch_gemm2<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
         case 1 * 8 + EPI_F32: launch_gemm2<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); return;
         case 3 * 8 + EPI_BF16: launch_gemm2<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); return;
@@ -202,6 +203,7 @@ static void dispatch_1sm(const GemmOperand& A, const GemmOperand& B, int64_t M, 
         case 0 * 8 + EPI_SWIGLU: launch_gemm<BN, false, false, EPI_SWIGLU>(ta, tb, m, n, k, ep, st); break;
         case 0 * 8 + EPI_SWIGLU_BWD: launch_gemm<BN, false, false, EPI_SWIGLU_BWD>(ta, tb, m, n, k, ep, st); break;
         case 0 * 8 + EPI_F32_STATS: launch_gemm<BN, false, false, EPI_F32_STATS>(ta, tb, m, n, k, ep, st); break;
+        case 0 * 8 + EPI_EXP_STATS: launch_gemm<BN, false, false, EPI_EXP_STATS>(ta, tb, m, n, k, ep, st); break;
         case 1 * 8 + EPI_BF16: launch_gemm<BN, false, true, EPI_BF16>(ta, tb, m, n, k, ep, st); break;
         case 1 * 8 + EPI_F32: launch_gemm<BN, false, true, EPI_F32>(ta, tb, m, n, k, ep, st); break;
         case 3 * 8 + EPI_BF16: launch_gemm<BN, true, true, EPI_BF16>(ta, tb, m, n, k, ep, st); break;
@@ -215,7 +217,7 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
     EpiParams ep = ep_in;
     ep.tstore = epi_tstore();
     if (Prof* pf = current_prof(); pf && pf->on) {
-        static const char* kn[] = {"bf16", "f32", "swiglu", "swiglu_bwd", "f32_stats"};
+        static const char* kn[] = {"bf16", "f32", "swiglu", "swiglu_bwd", "f32_stats", "exp_stats"};
         pf->next_tag = std::string(A.mn_major ? "MN" : "K") + (B.mn_major ? "MN" : "K") + "_" + kn[kind] + "_" +
                        std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K);
     }

@@ -25,6 +25,8 @@ enum EpiKind : int {
     EPI_SWIGLU = 2,      // columns interleaved [g32|u32]...: C(bf16)[m, n/2] = silu(g) * u
     EPI_SWIGLU_BWD = 3,  // same interleave; aux = dA[m, n/2]; C = dGU (interleaved), C2 = A = silu(g)u
     EPI_F32_STATS = 4,   // C(f32) = acc, plus per-(row, BN-column tile) softmax stats (max, sum exp(x-max))
+    EPI_EXP_STATS = 5,   // per (row, BN-column tile): m = max, C(bf16) = exp(acc - m), stats (m, sum exp(acc - m)),
+                         // label_logit[row] = acc at column labels[row] when it falls in the tile (fp32, exact)
 };
 
 struct EpiParams {
@@ -40,6 +42,8 @@ struct EpiParams {
     float alpha = 1.f;
     float* stats = nullptr;  // EPI_F32_STATS: [M][ld_stats] float2 (max, sumexp) per 256-column tile
     int64_t ld_stats = 0;
+    const int64_t* labels = nullptr;  // EPI_EXP_STATS: per-row label (column index; anything else matches none)
+    float* label_logit = nullptr;     // EPI_EXP_STATS: [M] fp32 logit of the row's label
     int tstore = 1;  // fp32 epilogues: 0 per-thread stores, 1 smem transpose + coalesced stores, 2 TMA store /
                      // reduce-add (1-SM kernel, EPI_F32)
 };
@@ -215,7 +219,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
             v[i] = silu_f(g) * u;
         }
         store_bf16x32(reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col / 2, v);
-    } else {  // EPI_SWIGLU_BWD
+    } else if constexpr (KIND == EPI_SWIGLU_BWD) {
         float da[32], dg[32], du[32];
         load_bf16x32(ep.aux + row * ep.ldaux + col / 2, da);
 #pragma unroll
@@ -231,6 +235,62 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
         bf16* dgu = reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col;
         store_bf16x32(dgu, dg);
         store_bf16x32(dgu + 32, du);
+    }
+}
+
+// EPI_EXP_STATS for one accumulator row (thread = TMEM lane = row) of a BN-column tile: pass 1 reads the row's
+// columns out of TMEM for the max m (and picks the label's logit), pass 2 re-reads them and stores e = exp(x - m)
+// as bf16 together with sum(e).  e is in (0, 1] with its largest entries exactly where the probabilities are,
+// so bf16 keeps them to 2^-9 relative; the loss uses the fp32 label logit, never a rounded value.  The fp32
+// logits never reach memory (the CE pass needs only e, the stats and the label logit).  tcgen05.ld is
+// warp-collective: every lane runs both passes, only the stores are predicated on the row.
+template <int BN>
+__device__ __forceinline__ void exp_stats_tile(const EpiParams& ep, uint32_t tbase, int64_t row, int nb, int64_t M,
+                                               int64_t N) {
+    const int64_t col0 = (int64_t)nb * BN;
+    const int64_t lab = row < M ? ep.labels[row] : -1;
+    float mx = -INFINITY, ll = 0.f;
+    bool has = false;
+#pragma unroll 1
+    for (int c = 0; c < BN && col0 + c < N; c += 64) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tbase + c, r0);
+        tmem_ld32(tbase + c + 32, r1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[i]), __uint_as_float(r1[i])));
+        const int64_t j = lab - (col0 + c);
+        if (j >= 0 && j < 64) {
+            has = true;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (j == i) ll = __uint_as_float(r0[i]);
+                if (j == i + 32) ll = __uint_as_float(r1[i]);
+            }
+        }
+    }
+    float sum = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN && col0 + c < N; c += 64) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tbase + c, r0);
+        tmem_ld32(tbase + c + 32, r1);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t* r = h ? r1 : r0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                v[i] = __expf(__uint_as_float(r[i]) - mx);
+                sum += v[i];
+            }
+            if (row < M) store_bf16x32(reinterpret_cast<bf16*>(ep.C) + row * ep.ldc + col0 + c + 32 * h, v);
+        }
+    }
+    if (row < M && col0 < N) {
+        reinterpret_cast<float2*>(ep.stats)[row * ep.ld_stats + nb] = make_float2(mx, sum);
+        if (has) ep.label_logit[row] = ll;
     }
 }
 
@@ -373,8 +433,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int64_t row = (int64_t)mb * GEMM_BM + sub * 32 + lane;
             const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
             float st_m = -INFINITY, st_s = 0.f;  // EPI_F32_STATS running (max, sum exp) over the tile row
+            if constexpr (KIND == EPI_EXP_STATS) exp_stats_tile<BN>(ep, tbase, row, nb, M, N);
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 64) {
+            for (int c = 0; c < (KIND == EPI_EXP_STATS ? 0 : BN); c += 64) {
                 const int64_t col = (int64_t)nb * BN + c;
                 uint32_t r0[32], r1[32];
                 tmem_ld32(tbase + c, r0);
@@ -597,8 +658,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int64_t row = (int64_t)mb * 2 * GEMM_BM + rank * GEMM_BM + sub * 32 + lane;
             const uint32_t tbase = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
             float st_m = -INFINITY, st_s = 0.f;  // EPI_F32_STATS running (max, sum exp) over the tile row
+            if constexpr (KIND == EPI_EXP_STATS) exp_stats_tile<BN>(ep, tbase, row, nb, M, N);
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 64) {
+            for (int c = 0; c < (KIND == EPI_EXP_STATS ? 0 : BN); c += 64) {
                 const int64_t col = (int64_t)nb * BN + c;
                 uint32_t r0[32], r1[32];
                 tmem_ld32(tbase + c, r0);

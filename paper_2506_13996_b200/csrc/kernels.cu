@@ -835,6 +835,100 @@ __global__ void __launch_bounds__(512) ce_rows_stats_kernel(const float* __restr
     }
 }
 
+// Variant fed by the EPI_EXP_STATS logits epilogue (the fp32 logits never reach memory): e = exp(x - m_t) in
+// bf16 per (row, 256-column tile t), stats (m_t, sum e), the fp32 label logit.  lse = combine(stats), then
+// p = e * exp(m_t - lse): one multiply by a per-tile factor instead of an exponential per element, and the
+// dlogits overwrite e in place.  Traffic per row: 2V read + 2V write (the fp32 form moves 4V + 2V plus the
+// epilogue's 4V write).
+constexpr int CE_MAX_TILES = 1024;  // V <= 262144
+__global__ void __launch_bounds__(512) ce_rows_exp_kernel(bf16* __restrict__ e_dlogits, const float2* __restrict__ stats,
+                                                          int ntile, const int64_t* __restrict__ labels,
+                                                          const float* __restrict__ label_logit, int64_t V,
+                                                          const float* __restrict__ scale_dev,
+                                                          float* __restrict__ loss_rows, int32_t* err) {
+    __shared__ float sm_m[32], sm_s[32];
+    __shared__ float fac[CE_MAX_TILES];
+    __shared__ float sh_lse;
+    const int64_t r = blockIdx.x;
+    const int64_t label = labels[r];
+    const bool valid = label != -100 && label >= 0 && label < V;
+    if (label != -100 && !valid && threadIdx.x == 0) *err = 1;
+    uint4* drow = reinterpret_cast<uint4*>(e_dlogits + r * V);
+    const int64_t nv = V / 8;
+    if (!valid) {
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) drow[i] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x == 0) loss_rows[r] = 0.f;
+        return;
+    }
+    float m = -INFINITY, s = 0.f;
+    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+        const float2 p = stats[r * ntile + i];
+        const float nm = fmaxf(m, p.x);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (p.x == -INFINITY ? 0.f : p.y * __expf(p.x - nm));
+        m = nm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+        const float nm = fmaxf(m, om);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sm_m[w] = m;
+        sm_s[w] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY, S = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            const float nm = fmaxf(M, sm_m[i]);
+            S = (M == -INFINITY ? 0.f : S * __expf(M - nm)) + (sm_m[i] == -INFINITY ? 0.f : sm_s[i] * __expf(sm_m[i] - nm));
+            M = nm;
+        }
+        const float lse = M + __logf(S);
+        sh_lse = lse;
+        loss_rows[r] = lse - label_logit[r];
+    }
+    __syncthreads();
+    const float lse = sh_lse;
+    const float scale = *scale_dev;
+    for (int i = threadIdx.x; i < ntile; i += blockDim.x) fac[i] = __expf(stats[r * ntile + i].x - lse) * scale;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+        const uint4 u = __ldcs(drow + i);
+        const float f = fac[i >> 5];  // 32 uint4 = 256 columns per stats tile
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[2 * k] = __uint_as_float(w4[k] << 16) * f;
+            v[2 * k + 1] = __uint_as_float(w4[k] & 0xffff0000u) * f;
+        }
+        const int64_t j = label - 8 * i;
+        if (j >= 0 && j < 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k == j) v[k] -= scale;
+        }
+        store8(e_dlogits + r * V + 8 * i, v);
+    }
+}
+
+void ce_rows_exp(void* e_dlogits, const float* stats, int ntile, const int64_t* labels, const float* label_logit,
+                 int64_t rows, int64_t V, const float* scale_dev, float* loss_rows, int32_t* err, cudaStream_t st) {
+    SPT_CHECK(V % 8 == 0, SPT_ERR_SHAPE, "vocab must be a multiple of 8");
+    SPT_CHECK(ntile <= CE_MAX_TILES, SPT_ERR_SHAPE, "vocab too large for the fused CE pass (max 262144)");
+    if (rows == 0) return;
+    prof_run(P_CE, 0, 4.0 * rows * V, st, [&] {
+        ce_rows_exp_kernel<<<(unsigned)rows, 512, 0, st>>>((bf16*)e_dlogits, (const float2*)stats, ntile, labels,
+                                                           label_logit, V, scale_dev, loss_rows, err);
+        count_launch("ce_rows_exp");
+    });
+    SPT_CUDA(cudaGetLastError());
+}
+
 void ce_rows_stats(const float* logits, const float* stats, int ntile, const int64_t* labels, int64_t rows, int64_t V,
                    const float* scale_dev, float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st) {
     SPT_CHECK(V % 8 == 0, SPT_ERR_SHAPE, "vocab must be a multiple of 8");

@@ -67,6 +67,8 @@ void embed_bwd(const int64_t* ids, int64_t n, int64_t V, int64_t h, const void* 
 void ce_rows(const float* logits, const int64_t* labels, int64_t rows, int64_t V, const float* scale_dev,
              float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st);
 // Same, from per-(row, 256-column tile) (max, sumexp) stats written by the logits GEMM epilogue.
+void ce_rows_exp(void* e_dlogits, const float* stats, int ntile, const int64_t* labels, const float* label_logit,
+                 int64_t rows, int64_t V, const float* scale_dev, float* loss_rows, int32_t* err, cudaStream_t st);
 void ce_rows_stats(const float* logits, const float* stats, int ntile, const int64_t* labels, int64_t rows, int64_t V,
                    const float* scale_dev, float* loss_rows, void* dlogits, int32_t* err, cudaStream_t st);
 // Deterministic fixed-order sum of n fp32 values into an fp64 accumulator.

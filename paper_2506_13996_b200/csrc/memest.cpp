@@ -9,6 +9,8 @@
 #include "common.h"
 
 namespace spt {
+size_t flce_workspace(int64_t tile_n, int64_t V);  // tiled.cu
+int64_t flce_default_tile(int64_t n_loc, int64_t V);
 namespace {
 constexpr double GiB = 1024.0 * 1024.0 * 1024.0;
 
@@ -71,8 +73,8 @@ static double engine_device_bytes(const spt_memest_engine& e, double s) {
     const double p_layer = e.hidden * qkv + e.hidden * qd + 3.0 * e.hidden * e.intermediate + 2.0 * e.hidden;
     const double p_fixed = e.n_layers * p_layer + (e.embed ? 2.0 : 1.0) * e.vocab * e.hidden + e.hidden;
     const double weights = 2.0 * p_fixed, grads = 4.0 * p_fixed;
-    const double tile = std::min<double>(nl, std::max(128.0, std::floor(4.0 * GiB / (e.vocab * 4.0) / 128.0) * 128.0));
-    const double logits_ws = tile * e.vocab * (4.0 + 2.0);
+    // the engine's loss tile and FLCE workspace (tiled.cu), exactly
+    const double logits_ws = nl >= 1 ? (double)flce_workspace(flce_default_tile((int64_t)nl, e.vocab), e.vocab) : 0.0;
     const double ckpt = e.n_layers > 1 || e.ckpt_offload ? (e.ckpt_offload ? 0.0 : e.n_layers * nl * e.hidden * 2.0) : 0.0;
     return weights + grads + logits_ws + ckpt + e.act_bytes_per_token * nl + e.act_bytes_per_seq_token * s;
 }

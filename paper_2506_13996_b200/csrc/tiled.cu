@@ -13,12 +13,32 @@ static inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 // ---------------------------------------------------------------- K5: fused logits + CE
 static int64_t flce_ntile(int64_t V) { return (V + 255) / 256; }
 
-size_t flce_workspace(int64_t tile_n, int64_t V) {
-    return align256((size_t)tile_n * V * 4) + align256((size_t)tile_n * V * 2) + align256((size_t)tile_n * 4) +
-           align256((size_t)tile_n * flce_ntile(V) * 8);
+// SPT_FLCE_EXP (read once at load): 1 (default) the logits GEMM's epilogue writes e = exp(x - m_tile) in bf16
+// straight into the dlogits buffer and the CE pass rewrites it in place (no fp32 [tile, V] buffer); 0 the
+// earlier form (fp32 logits from the epilogue, CE pass reads them and writes bf16 dlogits), kept for A/B.
+int g_flce_exp = [] {
+    const char* e = getenv("SPT_FLCE_EXP");
+    return (e && e[0]) ? atoi(e) : 1;
+}();
+
+// Default loss tile for n_loc local tokens (engine and memest): the fewest tiles whose [tile, V] workspace
+// stays within 4 GiB (SPEC.md:423 budget), split evenly, multiples of 128.  The budget is counted at 4 bytes
+// per logit whichever form runs, so both forms use the same tiles (8192 tokens at V=128256: the 4096 x 4096
+// dx GEMM then has 2x the cluster tiles of 4096 and dW is re-read half as often).
+int64_t flce_default_tile(int64_t n_loc, int64_t V) {
+    const int64_t tmax = std::max<int64_t>(128, (int64_t)((4ll << 30) / (V * 4)) / 128 * 128);
+    const int64_t ntl = std::max<int64_t>(1, (n_loc + tmax - 1) / tmax);
+    const int64_t t = ((n_loc + ntl - 1) / ntl + 127) / 128 * 128;
+    return std::max<int64_t>(1, std::min<int64_t>(std::min(t, tmax), n_loc));
 }
 
-// Per tile t (ascending): logits_t = x_t W^T (fp32, never more than [tile_n, V] live — SPEC.md:408),
+size_t flce_workspace(int64_t tile_n, int64_t V) {
+    return (g_flce_exp ? 0 : align256((size_t)tile_n * V * 4)) + align256((size_t)tile_n * V * 2) +
+           2 * align256((size_t)tile_n * 4) + align256((size_t)tile_n * flce_ntile(V) * 8);
+}
+
+// Per tile t (ascending): logits_t = x_t W^T (only per-256-column exp / stats of it reach memory, in the bf16
+// [tile_n, V] buffer that becomes dlogits — SPEC.md:408),
 // CE rows -> (loss_sum, dlogits scaled by 1/global_count), dx_t = dlogits W, dW += dlogits^T x_t.
 // Gradient-in-forward: loss is terminal, so dlogits is formed while the tile's logits are live and no
 // backward recompute is needed (results equal the spec's recompute up to fp order).
@@ -28,10 +48,12 @@ void flce(const void* x, const void* w, const int64_t* labels, int64_t n, int64_
     SPT_CHECK(tile_n > 0 && n >= 0, SPT_ERR_SHAPE, "flce: tile_n must be > 0");
     uint8_t* p = (uint8_t*)ws;
     float* logits = (float*)p;
-    p += align256((size_t)tile_n * V * 4);
+    if (!g_flce_exp) p += align256((size_t)tile_n * V * 4);
     bf16* dlog = (bf16*)p;
     p += align256((size_t)tile_n * V * 2);
     float* loss_rows = (float*)p;
+    p += align256((size_t)tile_n * 4);
+    float* label_logit = (float*)p;
     p += align256((size_t)tile_n * 4);
     float* stats = (float*)p;
     const int64_t ntile = flce_ntile(V);
@@ -41,12 +63,20 @@ void flce(const void* x, const void* w, const int64_t* labels, int64_t n, int64_
         // logits + per-(row, 256-col tile) softmax stats from the GEMM epilogue: the CE pass reads the
         // fp32 logits once (SPEC.md:69 cross_entropy on the tile, never an [s, V] tensor — :408)
         EpiParams e1;
-        e1.C = logits;
         e1.ldc = V;
         e1.stats = stats;
         e1.ld_stats = ntile;
-        gemm({xb + a * h, h, false}, {w, h, false}, rows, V, h, EPI_F32_STATS, e1, st);
-        ce_rows_stats(logits, stats, (int)ntile, labels + a, rows, V, scale_dev, loss_rows, dlog, err, st);
+        if (g_flce_exp) {
+            e1.C = dlog;
+            e1.labels = labels + a;
+            e1.label_logit = label_logit;
+            gemm({xb + a * h, h, false}, {w, h, false}, rows, V, h, EPI_EXP_STATS, e1, st);
+            ce_rows_exp(dlog, stats, (int)ntile, labels + a, label_logit, rows, V, scale_dev, loss_rows, err, st);
+        } else {
+            e1.C = logits;
+            gemm({xb + a * h, h, false}, {w, h, false}, rows, V, h, EPI_F32_STATS, e1, st);
+            ce_rows_stats(logits, stats, (int)ntile, labels + a, rows, V, scale_dev, loss_rows, dlog, err, st);
+        }
         sum_rows(loss_rows, rows, loss_sum_accum, st);
         EpiParams e2;
         e2.C = (bf16*)dx + a * h;
