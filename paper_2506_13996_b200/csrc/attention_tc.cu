@@ -47,6 +47,25 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return x < -126.f ? 0.f : y;
 }
 
+// 2^x for a PAIR on the FMA pipe with packed f32x2 arithmetic (FADD2 / FFMA2: half the instructions of two
+// ex2_poly calls): the same Cody-Waite split and degree-3 fit, exponent inserted by an integer add.  Inputs are
+// clamped to >= -126 so the inserted exponent never underflows into the sign (the result there is ~1e-38, not
+// exactly 0: callers use it only on unmasked score blocks, where masked -inf never occurs).
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+    const uint64_t big = f2pack(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+    const uint64_t t = fadd2(xc, big);
+    const uint64_t f = fsub2(xc, fsub2(t, big));
+    uint64_t p = ffma2(f2pack(0.05508868f, 0.05508868f), f, f2pack(0.24260405f, 0.24260405f));
+    p = ffma2(p, f, f2pack(0.69327624f, 0.69327624f));
+    p = ffma2(p, f, f2pack(0.99992894f, 0.99992894f));
+    float p0, p1, t0, t1;
+    f2unpack(p, p0, p1);
+    f2unpack(t, t0, t1);
+    y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+    y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 #ifndef SPT_DQ_TMEM_DEFAULT
 #define SPT_DQ_TMEM_DEFAULT 1
 #endif
@@ -501,12 +520,18 @@ constexpr int SMEM = OFF_BAR + 512 + 1024;
 
 // POLY > 0: every POLY-th exponential pair goes through ex2_poly on the FMA pipe (MUFU relief: with 128-key
 // blocks the exponentials of both tiles need the whole MUFU throughput at full tensor rate).
-template <int POLY>
+// DH: head dim (128, 64 or 32).  Shared memory and TMEM keep the d=128 layout; a d < 128 tile fills DP = max(DH, 64)
+// columns of it (one 64-column TMA box: for d = 32 the box also brings the next head's 32 columns, or TMA's zero
+// fill past the last head).  The score MMA contracts over DH only; the PV MMA runs N = DP, and output columns
+// >= DH (the neighbour's V) are never stored.
+template <int POLY, int DH>
 __global__ void __launch_bounds__(THREADS, 1)
     fwd_tc128_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                      int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
                      float* __restrict__ lse, int kvg, int filter) {
     using namespace fw2;
+    constexpr int DP = DH < 64 ? 64 : DH, NR = DP / 64;
+    constexpr int QB = BQ * DP * 2, KVB = BKB * DP * 2;  // bytes one tile / block load brings
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -563,19 +588,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             tma_prefetch_desc(&tq);
             tma_prefetch_desc(&tkv);
-            mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
+            mbar_arrive_expect_tx(q_full, 2 * QB);
             for (int t = 0; t < 2; ++t)
-                for (int r = 0; r < 2; ++r)
-                    tma_load_2d(&tq, q_full, smem + OFF_Q + t * Q_BYTES + r * 16384, h * D + 64 * r,
+                for (int r = 0; r < NR; ++r)
+                    tma_load_2d(&tq, q_full, smem + OFF_Q + t * Q_BYTES + r * 16384, h * DH + 64 * r,
                                 (int)(q0 + t * BQ));
             const int nload = 2 * (jhi - jlo + 1);
             for (int li = 0; li < nload; ++li) {
                 const int j = jlo + li / 2, w = li & 1;
                 const int slot = li % NSL;
                 mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
-                const int col = (hq + (w ? hkv : 0) + kvh) * D;
-                for (int r = 0; r < 2; ++r)
+                mbar_arrive_expect_tx(&kv_full[slot], KVB);
+                const int col = (hq + (w ? hkv : 0) + kvh) * DH;
+                for (int r = 0; r < NR; ++r)
                     tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 16384, col + 64 * r,
                                 j * BKB);
             }
@@ -583,7 +608,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 8) {
         {
             constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKB, false, false);
-            constexpr uint32_t idesc_o = make_idesc_bf16(BQ, D, false, true);
+            constexpr uint32_t idesc_o = make_idesc_bf16(BQ, DP, false, true);
             mbar_wait(q_full, 0);
             const int jb[2] = {jb0, jb1}, je[2] = {je0, je1};
             int pv_count[2] = {0, 0};
@@ -596,7 +621,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t qa = sbase + OFF_Q + t * Q_BYTES;
                 const uint32_t kb = sbase + OFF_KV + slot(j, 0) * KV_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
+                for (int kk = 0; kk < DH / 16; ++kk)
                     mma_bf16_ss_w(tmem + t * 256, kdesc_r(qa, kk, 16384), kdesc_r(kb, kk, 16384), idesc_s, kk > 0);
                 mma_commit_w(&s_full[t]);
             };
@@ -704,32 +729,45 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
             // P for chunk c (32 keys) -> 16 packed columns at [16c, 16c+16): the chunk's S columns [32c, 32c+32)
             // were already read into registers, and chunk c's P never lands on a chunk not yet read
+            // POLY > 1: on unmasked blocks every POLY-th exponential pair runs on the FMA pipe (ex2_poly2), so
+            // the MUFU pipe — exactly saturated by two 128x128 tiles at full tensor rate — is no longer the
+            // co-bottleneck; masked blocks stay on MUFU (masked entries exactly 0).
+            auto exps = [&](auto use_poly) {
+                constexpr bool UP = decltype(use_poly)::value;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t pw[16];
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pw[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), sc2, nb2);
-                    float x0, x1;
-                    f2unpack(x2, x0, x1);
-                    float p0, p1;
-                    if constexpr (POLY == 1) {  // two exponentials per MUFU op in f16 (P is bf16 anyway)
-                        ex2_f16x2(x0, x1, p0, p1);
-                    } else {
-                        const bool poly = POLY > 1 && ((c * 16 + k) % (POLY > 1 ? POLY : 1)) == (POLY > 1 ? POLY - 1 : 0);
-                        p0 = poly ? ex2_poly(x0) : ex2(x0);
-                        p1 = poly ? ex2_poly(x1) : ex2(x1);
+                    for (int k = 0; k < 16; ++k) {
+                        const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), sc2, nb2);
+                        float x0, x1;
+                        f2unpack(x2, x0, x1);
+                        float p0, p1;
+                        if constexpr (POLY == 1) {  // two exponentials per MUFU op in f16 (P is bf16 anyway)
+                            ex2_f16x2(x0, x1, p0, p1);
+                        } else if constexpr (UP) {
+                            if ((c * 16 + k) % POLY == POLY - 1) ex2_poly2(x0, x1, p0, p1);
+                            else {
+                                p0 = ex2(x0);
+                                p1 = ex2(x1);
+                            }
+                        } else {
+                            p0 = ex2(x0);
+                            p1 = ex2(x1);
+                        }
+                        rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
+                        pw[k] = pack_bf16x2(p0, p1);
                     }
-                    rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
-                    pw[k] = pack_bf16x2(p0, p1);
+                    tmem_st16(t_tm + c * 16, pw);
+                    if (c < 3 && (c + 1) % (4 / NPART) == 0) {  // this part of P done: its PV MMAs can start
+                        tmem_st_wait();
+                        tc_fence_before();
+                        mbar_arrive(&p_full[NPART * t + (c + 1) / (4 / NPART) - 1]);
+                    }
                 }
-                tmem_st16(t_tm + c * 16, pw);
-                if (c < 3 && (c + 1) % (4 / NPART) == 0) {  // this part of P done: its PV MMAs can start
-                    tmem_st_wait();
-                    tc_fence_before();
-                    mbar_arrive(&p_full[NPART * t + (c + 1) / (4 / NPART) - 1]);
-                }
-            }
+            };
+            if (POLY > 1 && !need_mask) exps(std::true_type{});
+            else exps(std::false_type{});
             float rs0, rs1;
             f2unpack(fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3])), rs0, rs1);
             l += rs0 + rs1;
@@ -742,9 +780,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (t == 1 && !has1) goto fwd2_done;
         {
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        bf16* orow = o + (q * hq + h) * D;
+        bf16* orow = o + (q * hq + h) * DH;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < DH / 32; ++c) {
             uint32_t ov[32];
             tmem_ld32(o_tm + c * 32, ov);
             tmem_ld_wait();
@@ -1343,11 +1381,15 @@ constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 }  // namespace dqt
 
+// DH = 64 / 32: DP = 64 columns of the d=128 layout (see fwd_tc128_kernel); dQ runs N = DP, columns >= DH unused.
+template <int DH>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dq_tmem_kernel(const __grid_constant__ CUtensorMap tkv, const bf16* __restrict__ qkv, const bf16* __restrict__ dout,
                    int64_t s, int hq, int hkv, const int32_t* __restrict__ seg, const float* __restrict__ lse2v,
                    const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv, int kvg) {
     using namespace dqt;
+    constexpr int DP = DH < 64 ? 64 : DH, NR = DP / 64;
+    constexpr int KVB = BKB * DP * 2;  // bytes one K or V block load brings
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -1397,16 +1439,16 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int j = jb + li / 2, w = li & 1;
                 const int slot = li % NSL;
                 mbar_wait(&kv_empty[slot], ((li / NSL) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[slot], KV_BYTES);
-                const int col = (hq + (w ? hkv : 0) + kvh) * D;
-                for (int r = 0; r < 2; ++r)
+                mbar_arrive_expect_tx(&kv_full[slot], KVB);
+                const int col = (hq + (w ? hkv : 0) + kvh) * DH;
+                for (int r = 0; r < NR; ++r)
                     tma_load_2d(&tkv, &kv_full[slot], smem + OFF_KV + slot * KV_BYTES + r * 8192, col + 64 * r,
                                 j * BKB);
             }
         }
     } else if (warp == BW_MMA) {
         constexpr uint32_t id_s = make_idesc_bf16(128, BKB, false, false);
-        constexpr uint32_t id_q = make_idesc_bf16(128, D, false, true);
+        constexpr uint32_t id_q = make_idesc_bf16(128, DP, false, true);
         mbar_wait(qt_ready, 0);
         tc_fence_after();
         auto issue_sdp = [&](int it) {
@@ -1417,10 +1459,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const uint32_t kb = sbase + OFF_KV + ks * KV_BYTES, vb = sbase + OFF_KV + vs * KV_BYTES;
             const uint32_t d_s = tmem + (it & 1) * 128;
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)  // S = Q K^T, Q from TMEM: d chunk kk = 8 packed columns
+            for (int kk = 0; kk < DH / 16; ++kk)  // S = Q K^T, Q from TMEM: d chunk kk = 8 packed columns
                 mma_bf16_ts_w(d_s, tmem + QT_COL + kk * 8, kdesc_r(kb, kk, 8192), id_s, kk > 0);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)  // dP = dO V^T
+            for (int kk = 0; kk < DH / 16; ++kk)  // dP = dO V^T
                 mma_bf16_ts_w(d_s + 64, tmem + DOT_COL + kk * 8, kdesc_r(vb, kk, 8192), id_s, kk > 0);
             mma_commit_w(&s_full[it & 1]);
             mma_commit_w(&kv_empty[vs]);  // V_j only feeds dP
@@ -1450,18 +1492,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int q32 = (int)q, q0i = (int)q0;
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         {  // Q and dO rows -> TMEM (this warp: d elements [32 grp, 32 grp + 32) = packed columns [16 grp, +16))
-            const int64_t width = (int64_t)(hq + 2 * hkv) * D;
-            const uint4* qs = reinterpret_cast<const uint4*>(qkv + q * width + (int64_t)h * D + 32 * grp);
-            const uint4* ds = reinterpret_cast<const uint4*>(dout + (q * hq + h) * D + 32 * grp);
-            uint32_t qv[16], dv[16];
+            if (32 * grp < DH) {
+                const int64_t width = (int64_t)(hq + 2 * hkv) * DH;
+                const uint4* qs = reinterpret_cast<const uint4*>(qkv + q * width + (int64_t)h * DH + 32 * grp);
+                const uint4* ds = reinterpret_cast<const uint4*>(dout + (q * hq + h) * DH + 32 * grp);
+                uint32_t qv[16], dv[16];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint4 a = __ldg(qs + k), b = __ldg(ds + k);
-                qv[4 * k] = a.x; qv[4 * k + 1] = a.y; qv[4 * k + 2] = a.z; qv[4 * k + 3] = a.w;
-                dv[4 * k] = b.x; dv[4 * k + 1] = b.y; dv[4 * k + 2] = b.z; dv[4 * k + 3] = b.w;
+                for (int k = 0; k < 4; ++k) {
+                    const uint4 a = __ldg(qs + k), b = __ldg(ds + k);
+                    qv[4 * k] = a.x; qv[4 * k + 1] = a.y; qv[4 * k + 2] = a.z; qv[4 * k + 3] = a.w;
+                    dv[4 * k] = b.x; dv[4 * k + 1] = b.y; dv[4 * k + 2] = b.z; dv[4 * k + 3] = b.w;
+                }
+                tmem_st16(tmem + lo + QT_COL + grp * 16, qv);
+                tmem_st16(tmem + lo + DOT_COL + grp * 16, dv);
             }
-            tmem_st16(tmem + lo + QT_COL + grp * 16, qv);
-            tmem_st16(tmem + lo + DOT_COL + grp * 16, dv);
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(qt_ready);
@@ -1509,7 +1553,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         mbar_wait(dq_done, 0);
         tc_fence_after();
-        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * D + grp * 32;
+        if (32 * grp >= DH) goto dq_done_label;
+        {
+        bf16* dst = dqkv + (q * (hq + 2 * hkv) + h) * DH + grp * 32;
         uint32_t v[32];
         tmem_ld32(tmem + lo + DQ_COL + grp * 32, v);
         tmem_ld_wait();
@@ -1523,6 +1569,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             o.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * scale, __uint_as_float(v[8 * k + 7]) * scale);
             d4[k] = o;
         }
+        }
+    dq_done_label:;
     }
     tc_fence_before();
     __syncthreads();
@@ -1558,13 +1606,17 @@ constexpr int SMEM = OFF_BAR + 256 + 1024;
 // TMEM = S^T (64) | dP^T[2] (64 each) | K (64) | dV (128) | dK (128).  The elementwise warps release S^T
 // (s_free) right after loading it and write P^T / dS^T into the consumed dP^T buffer, so S^T(it+1) and
 // dP^T(it+1) run while the elementwise phase of it computes.
-template <bool MC, bool KT>
+// DH = 64 / 32: the d=128 layout with DP = max(DH, 64) columns filled (see fwd_tc128_kernel); S^T / dP^T contract
+// over DH, dV / dK run N = DP and their columns >= DH are never stored.
+template <bool MC, bool KT, int DH>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                    const __grid_constant__ CUtensorMap tdo, int64_t s, int hq, int hkv, const int32_t* __restrict__ seg,
                    const float* __restrict__ lse2v, const float* __restrict__ Dv, float scale, bf16* __restrict__ dqkv,
                    const bf16* __restrict__ qkv) {
     using namespace dkv;
+    constexpr int DP = DH < 64 ? 64 : DH, NR = DP / 64;
+    constexpr int KBB = 128 * DP * 2, QSB = BQB * DP * 2;  // bytes one K/V block / Q or dO tile load brings
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -1628,34 +1680,34 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t sbase = smem_u32(smem);
     if (warp == BW_TMA) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(kv_full, (KT ? 1 : 2) * KB_BYTES);
-            for (int r = 0; r < 2; ++r) {
-                if (!KT) tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * D + 64 * r, (int)k0);
-                tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * D + 64 * r, (int)k0);
+            mbar_arrive_expect_tx(kv_full, (KT ? 1 : 2) * KBB);
+            for (int r = 0; r < NR; ++r) {
+                if (!KT) tma_load_2d(&tkv, kv_full, smem + OFF_K + r * 16384, (hq + kvh) * DH + 64 * r, (int)k0);
+                tma_load_2d(&tkv, kv_full, smem + OFF_V + r * 16384, (hq + hkv + kvh) * DH + 64 * r, (int)k0);
             }
             int hh = kvh * grp, qblk = 0;
             for (int it = 0; it < total; ++it) {
                 const int st = it % NQS;
                 mbar_wait(&qs_empty[st], ((it / NQS) & 1) ^ 1);
-                mbar_arrive_expect_tx(&qs_full[st], 2 * QS_BYTES + 512);
+                mbar_arrive_expect_tx(&qs_full[st], 2 * QSB + 512);
                 const int qq = (qb_first + qblk) * BQB;
                 const int hcur = hh;
                 if (++qblk == nqb) { qblk = 0; ++hh; }
                 uint8_t* base = smem + OFF_QS + st * 2 * QS_BYTES;
                 if constexpr (MC) {  // rank 0 brings Q + lse, rank 1 brings dO + D, into both CTAs
                     if (crank == 0) {
-                        for (int r = 0; r < 2; ++r)
-                            tma_load_2d_mc(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq, 0x3);
+                        for (int r = 0; r < NR; ++r)
+                            tma_load_2d_mc(&tq, &qs_full[st], base + r * 8192, hcur * DH + 64 * r, qq, 0x3);
                         bulk_load_mc(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st], 0x3);
                     } else {
-                        for (int r = 0; r < 2; ++r)
-                            tma_load_2d_mc(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq, 0x3);
+                        for (int r = 0; r < NR; ++r)
+                            tma_load_2d_mc(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * DH + 64 * r, qq, 0x3);
                         bulk_load_mc(smem + OFF_LD + st * 512 + 256, Dv + (int64_t)hcur * s + qq, 256, &qs_full[st], 0x3);
                     }
                 } else {
-                    for (int r = 0; r < 2; ++r) {
-                        tma_load_2d(&tq, &qs_full[st], base + r * 8192, hcur * D + 64 * r, qq);
-                        tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * D + 64 * r, qq);
+                    for (int r = 0; r < NR; ++r) {
+                        tma_load_2d(&tq, &qs_full[st], base + r * 8192, hcur * DH + 64 * r, qq);
+                        tma_load_2d(&tdo, &qs_full[st], base + QS_BYTES + r * 8192, hcur * DH + 64 * r, qq);
                     }
                     // per-column softmax statistics of this q block (lse*log2e, D) for the elementwise warps
                     bulk_load(smem + OFF_LD + st * 512, lse2v + (int64_t)hcur * s + qq, 256, &qs_full[st]);
@@ -1666,7 +1718,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     } else if (warp == BW_MMA) {
         {  // whole warp, converged; elect.sync inside the MMA/commit wrappers picks the issuing lane
             constexpr uint32_t id_s = make_idesc_bf16(128, BQB, false, false);
-            constexpr uint32_t id_a = make_idesc_bf16(128, D, false, true);
+            constexpr uint32_t id_a = make_idesc_bf16(128, DP, false, true);
             mbar_wait(kv_full, 0);
             if (KT) mbar_wait(k_ready, 0);
             const uint32_t ka = sbase + OFF_K, va = sbase + OFF_V;
@@ -1677,10 +1729,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 tc_fence_after();
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
+                for (int kk = 0; kk < DH / 16; ++kk)
                     mma_bf16_ts_w(tmem, tmem + K_COL + kk * 8, kdesc_r(qb_, kk, 8192), id_s, kk > 0);
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
+                for (int kk = 0; kk < DH / 16; ++kk)
                     mma_bf16_ss_w(tmem + DP_COL + (it & 1) * 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s,
                                   kk > 0);
                 mma_commit_w(&s_full[it & 1]);
@@ -1692,10 +1744,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const uint32_t qb_ = sbase + OFF_QS + st * 2 * QS_BYTES, dob = qb_ + QS_BYTES;
                 const uint32_t d_s = tmem + (it & 1) * 128;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
+                for (int kk = 0; kk < DH / 16; ++kk)
                     mma_bf16_ss_w(d_s, kdesc_r(ka, kk, 16384), kdesc_r(qb_, kk, 8192), id_s, kk > 0);
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
+                for (int kk = 0; kk < DH / 16; ++kk)
                     mma_bf16_ss_w(d_s + 64, kdesc_r(va, kk, 16384), kdesc_r(dob, kk, 8192), id_s, kk > 0);
                 mma_commit_w(&s_full[it & 1]);
             };
@@ -1744,15 +1796,17 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const uint32_t lo = (uint32_t)(sub * 32) << 16;
         const float sl2 = scale * LOG2E;
         if constexpr (KT) {  // K row `key` -> TMEM (this warp: d elements [32 grp, +32) = packed columns [16 grp, +16))
-            const int64_t width = (int64_t)(hq + 2 * hkv) * D;
-            const uint4* ks = reinterpret_cast<const uint4*>(qkv + key * width + (int64_t)(hq + kvh) * D + 32 * grp);
-            uint32_t kv[16];
+            if (32 * grp < DH) {
+                const int64_t width = (int64_t)(hq + 2 * hkv) * DH;
+                const uint4* ks = reinterpret_cast<const uint4*>(qkv + key * width + (int64_t)(hq + kvh) * DH + 32 * grp);
+                uint32_t kv[16];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint4 a = __ldg(ks + k);
-                kv[4 * k] = a.x; kv[4 * k + 1] = a.y; kv[4 * k + 2] = a.z; kv[4 * k + 3] = a.w;
+                for (int k = 0; k < 4; ++k) {
+                    const uint4 a = __ldg(ks + k);
+                    kv[4 * k] = a.x; kv[4 * k + 1] = a.y; kv[4 * k + 2] = a.z; kv[4 * k + 3] = a.w;
+                }
+                tmem_st16(tmem + lo + K_COL + grp * 16, kv);
             }
-            tmem_st16(tmem + lo + K_COL + grp * 16, kv);
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(k_ready);
@@ -1833,18 +1887,19 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         // epilogue: column groups 0,1 write dV, 2,3 write dK (scaled); 64 columns each
         mbar_wait(acc_done, 0);
         tc_fence_after();
-        const int64_t rs = (int64_t)(hq + 2 * hkv) * D;
+        const int64_t rs = (int64_t)(hq + 2 * hkv) * DH;
         const bool isk = grp >= 2;
         const int c0 = (grp & 1) * 64;
-        bf16* dst = dqkv + key * rs + (int64_t)(isk ? (hq + kvh) : (hq + hkv + kvh)) * D + c0;
+        bf16* dst = dqkv + key * rs + (int64_t)(isk ? (hq + kvh) : (hq + hkv + kvh)) * DH + c0;
         const float mul = isk ? scale : 1.f;
         const uint32_t acc_tm = tmem + lo + (isk ? 384 : 256) + c0;
-        if (total == 0) {
+        if (c0 >= DH) {
+        } else if (total == 0) {
             uint4* d4 = reinterpret_cast<uint4*>(dst);
-            for (int k = 0; k < 8; ++k) d4[k] = make_uint4(0, 0, 0, 0);
+            for (int k = 0; k < (DH < 64 ? DH : 64) / 8; ++k) d4[k] = make_uint4(0, 0, 0, 0);
         } else {
 #pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
+            for (int c = 0; c < (DH < 64 ? DH : 64) / 32; ++c) {
                 uint32_t v[32];
                 tmem_ld32(acc_tm + c * 32, v);
                 tmem_ld_wait();
@@ -3017,7 +3072,8 @@ int g_attn_fwd_bk128 = [] {
 // Packed sequences keep the 64-key kernel: with short samples most 128-key blocks straddle a sample start
 // (s=128K, mean sample 2048: 6.57 vs 4.56 ms), while long samples gain only a few % (32768: 57.7 vs 61.3 ms).
 // Values: 1 (default) 128-key unless packed, 2 128-key always, 0 64-key, 4 / 8 128-key + FMA-pipe exp2,
-// 3 128-key with f16x2 exponentials,
+// 3 128-key with f16x2 exponentials, 10 + n (n = 2, 3, 4, 6, 8): 128-key with every n-th exponential pair of
+// an unmasked block on the FMA pipe (packed ex2_poly2),
 // -1 128-key for s * hq >= 2^21.  Returns 0 (64-key) or the 128-key kernel's POLY selector (1, 4, 8).
 static int fwd_bk128(int64_t s, int hq, const int32_t* seg) {
     const int v = g_attn_fwd_bk128;
@@ -3035,34 +3091,47 @@ int g_attn_fwd_tmem = [] {
 
 bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32_t* seg, float scale, void* o,
                  float* lse, cudaStream_t st) {
-    if (d != fatc::D || s % 128 != 0) return false;
+    if ((d != 128 && d != 64 && d != 32) || s % 128 != 0) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap tq = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
     CUtensorMap tkv = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);
     static bool attr = false;
     if (!attr) {
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
-        for (auto k : {fatc::fwd_tc128_kernel<0>, fatc::fwd_tc128_kernel<1>, fatc::fwd_tc128_kernel<4>,
-                       fatc::fwd_tc128_kernel<8>})
+        for (auto k : {fatc::fwd_tc128_kernel<0, 128>, fatc::fwd_tc128_kernel<1, 128>, fatc::fwd_tc128_kernel<2, 128>,
+                       fatc::fwd_tc128_kernel<3, 128>, fatc::fwd_tc128_kernel<4, 128>, fatc::fwd_tc128_kernel<6, 128>,
+                       fatc::fwd_tc128_kernel<8, 128>, fatc::fwd_tc128_kernel<0, 64>, fatc::fwd_tc128_kernel<0, 32>})
             SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw2::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::fwt::SMEM));
         attr = true;
     }
     dim3 grid((unsigned)hq, (unsigned)((s + 255) / 256));
+    if (d != 128) {  // head dims 64 / 32: the 128-key kernel (plain causal and packed) on DP = 64 columns
+        CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
+        auto k = d == 64 ? fatc::fwd_tc128_kernel<0, 64> : fatc::fwd_tc128_kernel<0, 32>;
+        k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
+                                                        kv_group(s, hkv, d), 0);
+        count_launch("attn_fwd_tc");
+        SPT_CUDA(cudaGetLastError());
+        return true;
+    }
     const int bk128 = fwd_bk128(s, hq, seg);
     if (bk128) {
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
-        auto k = bk128 == 4   ? fatc::fwd_tc128_kernel<4>
-                 : bk128 == 8 ? fatc::fwd_tc128_kernel<8>
-                 : bk128 == 3 ? fatc::fwd_tc128_kernel<1>
-                              : fatc::fwd_tc128_kernel<0>;
+        auto k = bk128 == 4 || bk128 == 14 ? fatc::fwd_tc128_kernel<4, 128>
+                 : bk128 == 8 || bk128 == 18 ? fatc::fwd_tc128_kernel<8, 128>
+                 : bk128 == 12 ? fatc::fwd_tc128_kernel<2, 128>
+                 : bk128 == 13 ? fatc::fwd_tc128_kernel<3, 128>
+                 : bk128 == 16 ? fatc::fwd_tc128_kernel<6, 128>
+                 : bk128 == 3 ? fatc::fwd_tc128_kernel<1, 128>
+                              : fatc::fwd_tc128_kernel<0, 128>;
         k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
                                                         kv_group(s, hkv, d), 0);
     } else if (seg != nullptr && g_attn_fwd_bk128 == 1 && g_attn_fwd_hybrid) {
         // packed: long-sample tile pairs on the 128-key kernel, short ones on the 64-key kernel
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
-        fatc::fwd_tc128_kernel<0><<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(
+        fatc::fwd_tc128_kernel<0, 128><<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(
             tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse, kv_group(s, hkv, d), 1);
         fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
                                                                           (bf16*)o, lse, kv_group(s, hkv, d), 2);
@@ -3149,7 +3218,7 @@ size_t attn_bwd_tc_workspace(int64_t s, int hq) {
 // ws: attn_bwd_tc_workspace bytes (fp32 dQ accumulator + per-(head, q block) ordering counters).
 bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const float* Dv, int64_t s, int hq, int hkv,
                  int d, const int32_t* seg, float scale, void* dqkv, void* ws, cudaStream_t st) {
-    if (d != fatc::D || s % 128 != 0 || s >= (int64_t(1) << 31) - 256) return false;
+    if ((d != 128 && d != 64 && d != 32) || s % 128 != 0 || s >= (int64_t(1) << 31) - 256) return false;
     const int64_t width = (int64_t)(hq + 2 * hkv) * d;
     CUtensorMap t128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
     CUtensorMap t64 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 64);
@@ -3161,15 +3230,15 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dq::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dq::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tmem_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dqt::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false, false>,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false, false, 128>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::dkv::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true, false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<false, true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
-        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dkdv_tc_kernel<true, true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkv::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdvq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkvq::SMEM));
@@ -3177,7 +3246,46 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
                                       fatc::dkp::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::dkdvq4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::dkvq4::SMEM));
+        for (auto k : {fatc::dkdv_tc_kernel<false, false, 64>, fatc::dkdv_tc_kernel<true, false, 64>,
+                       fatc::dkdv_tc_kernel<false, true, 64>, fatc::dkdv_tc_kernel<true, true, 64>,
+                       fatc::dkdv_tc_kernel<false, false, 32>, fatc::dkdv_tc_kernel<true, false, 32>,
+                       fatc::dkdv_tc_kernel<false, true, 32>, fatc::dkdv_tc_kernel<true, true, 32>})
+            SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::dkv::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tmem_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dqt::SMEM));
+        SPT_CUDA(cudaFuncSetAttribute(fatc::dq_tmem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fatc::dqt::SMEM));
         attr = true;
+    }
+    if (d != 128) {  // head dims 64 / 32: the default two-pass scheme (dK/dV KV-outer + dQ with Q/dO in TMEM)
+        const bool kt_ = g_attn_dkdv_kt == 1 || (g_attn_dkdv_kt == 2 && seg == nullptr);
+        const bool mc = dkdv_multicast() && (s / 128) % 2 == 0;
+        auto kern = d == 64 ? (mc ? (kt_ ? fatc::dkdv_tc_kernel<true, true, 64> : fatc::dkdv_tc_kernel<true, false, 64>)
+                                  : (kt_ ? fatc::dkdv_tc_kernel<false, true, 64> : fatc::dkdv_tc_kernel<false, false, 64>))
+                            : (mc ? (kt_ ? fatc::dkdv_tc_kernel<true, true, 32> : fatc::dkdv_tc_kernel<true, false, 32>)
+                                  : (kt_ ? fatc::dkdv_tc_kernel<false, true, 32> : fatc::dkdv_tc_kernel<false, false, 32>));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(s / 128), (unsigned)hkv);
+        cfg.blockDim = dim3(fatc::BW_THREADS);
+        cfg.dynamicSmemBytes = fatc::dkv::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = mc ? 2 : 1;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, kern, t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv,
+                                    (const bf16*)qkv));
+        count_launch("attn_dkdv_tc");
+        SPT_CUDA(cudaGetLastError());
+        auto kq = d == 64 ? fatc::dq_tmem_kernel<64> : fatc::dq_tmem_kernel<32>;
+        kq<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dqt::SMEM, st>>>(
+            t64, (const bf16*)qkv, (const bf16*)dout, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, kv_group(s, hkv, d));
+        count_launch("attn_dq_tc");
+        SPT_CUDA(cudaGetLastError());
+        return true;
     }
     if (bwd_mode() == 2 && ws != nullptr && seg == nullptr && s % 512 == 0) {
         float* dq_acc = (float*)ws;
@@ -3252,17 +3360,17 @@ bool attn_bwd_tc(const void* qkv, const void* dout, const float* lse2, const flo
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        SPT_CUDA(cudaLaunchKernelEx(&cfg, kt ? fatc::dkdv_tc_kernel<true, true> : fatc::dkdv_tc_kernel<true, false>,
+        SPT_CUDA(cudaLaunchKernelEx(&cfg, kt ? fatc::dkdv_tc_kernel<true, true, 128> : fatc::dkdv_tc_kernel<true, false, 128>,
                                     t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, (const bf16*)qkv));
     } else {
-        auto kern = kt ? fatc::dkdv_tc_kernel<false, true> : fatc::dkdv_tc_kernel<false, false>;
+        auto kern = kt ? fatc::dkdv_tc_kernel<false, true, 128> : fatc::dkdv_tc_kernel<false, false, 128>;
         kern<<<dim3((unsigned)(s / 128), (unsigned)hkv), fatc::BW_THREADS, fatc::dkv::SMEM, st>>>(
             t128, t64, do64, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv, (const bf16*)qkv);
     }
     count_launch("attn_dkdv_tc");
     SPT_CUDA(cudaGetLastError());
     if (dq_tmem()) {  // Q / dO resident in TMEM: S and dP MMAs read only their B operand from smem
-        fatc::dq_tmem_kernel<<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dqt::SMEM, st>>>(
+        fatc::dq_tmem_kernel<128><<<dim3((unsigned)hq, (unsigned)(s / 128)), fatc::BW_THREADS, fatc::dqt::SMEM, st>>>(
             t64, (const bf16*)qkv, (const bf16*)dout, s, hq, hkv, seg, lse2, Dv, scale, (bf16*)dqkv,
             kv_group(s, hkv, d));
     } else if (dq_multicast() && (hq / hkv) % 2 == 0) {  // head pairs of one kv head share a multicast K/V stream

@@ -144,6 +144,7 @@ struct GemmTuning {
     int gemm_pair_mn = env_int("SPT_GEMM_PAIR_MN", 0);
     int gemm_bn = env_int("SPT_GEMM_BN", 0);
     int epi_tstore = env_int("SPT_EPI_TSTORE", 2);
+    int gemm_raster = env_int("SPT_GEMM_RASTER", 0);
 };
 static GemmTuning& tuning() {
     static GemmTuning t;
@@ -249,6 +250,30 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
             if (eff(128) >= eff(256) + 0.06) bn = 128;
         }
     }
+    // Tile order by operand footprint (gemm_raster = 1, default): when one operand fits in L2 with room to spare
+    // (<= 80 MB of the 126 MB), sweep the tiles so that it is re-read from L2 and the other operand streams from
+    // HBM exactly once, and tell the L2 so (evict_last on the resident operand, evict_first on the streamed one).
+    // The lm_head weight gradient (B = the x tile, 67 MB; A = dlogits^T streamed) and the logits GEMM (A = the
+    // x tile; B = W_lm streamed) are the cases that matter; with neither operand resident the grouped order stays.
+    // gemm_raster = 0 (default): grouped order and no hints everywhere; 1: order only, 2: hints only, 3: both.
+    // Measured (profiles/r2b_gemm_raster.txt): 3 is 4.7% SLOWER per L1 step — the lm_head GEMMs read 40-50% MORE
+    // from HBM with the resident-operand order than with the grouped one.
+    if (const int rm = tuning().gemm_raster; rm != 0) {  // bit 0: tile order, bit 1: L2 hints
+        const double ba = 2.0 * M * K, bb = 2.0 * N * K, cap = 80.0 * (1 << 20);
+        if (bb <= cap && bb <= ba) {
+            if (rm & 1) ep.raster = 1;
+            if (rm & 2) {
+                ep.hint_a = 1;
+                ep.hint_b = 2;
+            }
+        } else if (ba <= cap) {
+            if (rm & 1) ep.raster = 2;
+            if (rm & 2) {
+                ep.hint_a = 2;
+                ep.hint_b = 1;
+            }
+        }
+    }
     if (pair) {
         if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
@@ -298,6 +323,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
     return spt::capi_guard([&] {
         const std::string n(name);
         auto& t = spt::tuning();
+        if (n == "gemm_raster") {
+            t.gemm_raster = value;
+            return;
+        }
         if (n == "attn_dq_tmem") {
             spt::g_attn_dq_tmem = value;
             return;

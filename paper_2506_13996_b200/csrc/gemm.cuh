@@ -44,6 +44,12 @@ struct EpiParams {
     int64_t ld_stats = 0;
     const int64_t* labels = nullptr;  // EPI_EXP_STATS: per-row label (column index; anything else matches none)
     float* label_logit = nullptr;     // EPI_EXP_STATS: [M] fp32 logit of the row's label
+    // Tile order and L2 hints (gemm() picks them per shape, see gemm.cu raster rule): raster 0 = groups of GROUP_M
+    // row blocks sweeping all column blocks, 1 = column blocks fastest (the whole B stays in L2, every A panel is
+    // read once), 2 = row blocks fastest (A stays, B panels read once); hint_a / hint_b: TMA L2 policy of the
+    // operand loads (0 none, 1 evict_first, 2 evict_last).
+    int raster = 0;
+    int hint_a = 0, hint_b = 0;
     int tstore = 1;  // fp32 epilogues: 0 per-thread stores, 1 smem transpose + coalesced stores, 2 TMA store /
                      // reduce-add (1-SM kernel, EPI_F32)
 };
@@ -341,6 +347,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     auto tile_coords = [&](int t, int& mb, int& nb) {
+        if (ep.raster == 1) {
+            mb = t / num_n;
+            nb = t - mb * num_n;
+            return;
+        }
+        if (ep.raster == 2) {
+            nb = t / num_m;
+            mb = t - nb * num_m;
+            return;
+        }
         const int per_group = GROUP_M * num_n;
         const int gid = t / per_group;
         const int first_m = gid * GROUP_M;
@@ -354,6 +370,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol_a = l2_policy(ep.hint_a), pol_b = l2_policy(ep.hint_b);
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 int mb, nb;
                 tile_coords(t, mb, nb);
@@ -363,18 +380,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint8_t* sB = sA + Cfg::A_BYTES;
                     mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
                     if constexpr (!A_MN) {
-                        tma_load_2d(&tmA, &full[stage], sA, kb * GEMM_BK, mb * GEMM_BM);
+                        tma_load_2d_hint(&tmA, &full[stage], sA, kb * GEMM_BK, mb * GEMM_BM, pol_a);
                     } else {
 #pragma unroll
                         for (int i = 0; i < GEMM_BM / 64; ++i)
-                            tma_load_2d(&tmA, &full[stage], sA + i * 8192, mb * GEMM_BM + i * 64, kb * GEMM_BK);
+                            tma_load_2d_hint(&tmA, &full[stage], sA + i * 8192, mb * GEMM_BM + i * 64, kb * GEMM_BK, pol_a);
                     }
                     if constexpr (!B_MN) {
-                        tma_load_2d(&tmB, &full[stage], sB, kb * GEMM_BK, nb * BN);
+                        tma_load_2d_hint(&tmB, &full[stage], sB, kb * GEMM_BK, nb * BN, pol_b);
                     } else {
 #pragma unroll
                         for (int i = 0; i < BN / 64; ++i)
-                            tma_load_2d(&tmB, &full[stage], sB + i * 8192, nb * BN + i * 64, kb * GEMM_BK);
+                            tma_load_2d_hint(&tmB, &full[stage], sB + i * 8192, nb * BN + i * 64, kb * GEMM_BK, pol_b);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -565,6 +582,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     auto tile_coords = [&](int t, int& mb, int& nb) {
+        if (ep.raster == 1) {
+            mb = t / num_n;
+            nb = t - mb * num_n;
+            return;
+        }
+        if (ep.raster == 2) {
+            nb = t / num_m;
+            mb = t - nb * num_m;
+            return;
+        }
         const int per_group = GROUP_M * num_n;
         const int gid = t / per_group;
         const int first_m = gid * GROUP_M;
@@ -578,6 +605,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol_a = l2_policy(ep.hint_a), pol_b = l2_policy(ep.hint_b);
             for (int t = cid; t < ntiles; t += ncl) {
                 int mb, nb;
                 tile_coords(t, mb, nb);
@@ -589,18 +617,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint8_t* sB = sA + Cfg::A_BYTES;
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
                     if constexpr (!A_MN) {
-                        tma_load_2d_pair(&tmA, &full[stage], sA, kb * GEMM_BK, m0);
+                        tma_load_2d_pair_hint(&tmA, &full[stage], sA, kb * GEMM_BK, m0, pol_a);
                     } else {
 #pragma unroll
                         for (int i = 0; i < GEMM_BM / 64; ++i)
-                            tma_load_2d_pair(&tmA, &full[stage], sA + i * 8192, m0 + i * 64, kb * GEMM_BK);
+                            tma_load_2d_pair_hint(&tmA, &full[stage], sA + i * 8192, m0 + i * 64, kb * GEMM_BK, pol_a);
                     }
                     if constexpr (!B_MN) {
-                        tma_load_2d_pair(&tmB, &full[stage], sB, kb * GEMM_BK, n0);
+                        tma_load_2d_pair_hint(&tmB, &full[stage], sB, kb * GEMM_BK, n0, pol_b);
                     } else {
 #pragma unroll
                         for (int i = 0; i < BN / 128; ++i)
-                            tma_load_2d_pair(&tmB, &full[stage], sB + i * 8192, n0 + i * 64, kb * GEMM_BK);
+                            tma_load_2d_pair_hint(&tmB, &full[stage], sB + i * 8192, n0 + i * 64, kb * GEMM_BK, pol_b);
                     }
                     if (++stage == STAGES) {
                         stage = 0;

@@ -207,7 +207,10 @@ def _attn_case(s, hq, hkv, d, packed, seed, amp=1.0):
                                                    (1024, 2, 2, 128, True, 2.5), (1024, 4, 1, 128, False, 1),
                                                    (1024, 8, 1, 128, True, 1), (640, 4, 2, 128, True, 1),
                                                    (896, 8, 1, 128, False, 2.5), (128, 2, 1, 128, False, 1),
-                                                   (256, 4, 4, 128, False, 1), (128, 4, 2, 128, True, 1)])
+                                                   (256, 4, 4, 128, False, 1), (128, 4, 2, 128, True, 1),
+                                                   (1024, 8, 2, 32, False, 1), (640, 4, 1, 64, False, 2.5),
+                                                   (640, 4, 2, 32, True, 1), (1024, 4, 4, 64, True, 1),
+                                                   (2048, 8, 2, 32, True, 2.5), (128, 2, 1, 64, False, 1)])
 def test_attention_fwd_bwd(s, hq, hkv, d, packed, amp):
     """amp > 1 gives peaked softmax rows: exercises the lazy O-rescale path of the tcgen05 forward."""
     T = torch()
@@ -241,6 +244,32 @@ def test_attention_fwd_bwd(s, hq, hkv, d, packed, amp):
     S.check(_lib().spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
                                 S.ptr(seg), scale, dqkv2.data_ptr(), ws.data_ptr(), None))
     assert T.equal(dqkv.view(T.int16), dqkv2.view(T.int16))
+
+
+@pytest.mark.parametrize("d", [32, 64])
+def test_attention_small_head_dim_runs_tcgen05(d):
+    """head_dim 32 / 64 run the tcgen05 kernels (fwd_tc128_kernel, dkdv_tc_kernel, dq_tmem_kernel), never the
+    mma.sync fallback (kept only behind SPT_ATTN_IMPL=mma): kernel names from the CUDA profiler."""
+    T = torch()
+    from torch.profiler import ProfilerActivity, profile
+    s, hq, hkv = 1024, 8, 2
+    qkv, dout, _ = _attn_case(s, hq, hkv, d, False, 7, 1)
+    qkvd, doutd = bf16_dev(qkv), bf16_dev(dout)
+    o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
+    lse = T.empty(hq, s, device="cuda")
+    dqkv = T.zeros(s, hq + 2 * hkv, d, dtype=T.bfloat16, device="cuda")
+    ws = T.empty(_lib().spt_attn_bwd_workspace(s, hq, hkv, d), dtype=T.uint8, device="cuda")
+    sc = 1.0 / math.sqrt(d)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        S.check(_lib().spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, None, sc, o.data_ptr(), lse.data_ptr(), None))
+        S.check(_lib().spt_attn_bwd(qkvd.data_ptr(), o.data_ptr(), lse.data_ptr(), doutd.data_ptr(), s, hq, hkv, d,
+                                    None, sc, dqkv.data_ptr(), ws.data_ptr(), None))
+        T.cuda.synchronize()
+    names = " ".join(e.name for e in prof.events())
+    for k in ("fwd_tc128_kernel", "dkdv_tc_kernel", "dq_tmem_kernel"):
+        assert k in names, (k, names[:400])
+    for k in ("fa::fwd_kernel", "fa::bwd_dkdv_kernel", "fa::bwd_dq_kernel"):  # the mma.sync kernels
+        assert k not in names, k
 
 
 # ------------------------------------------------------------------ fused logits + CE (tiled)
