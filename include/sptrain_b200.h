@@ -350,6 +350,9 @@ spt_status spt_layer_get_grad(spt_layer* layer, const char* name, float* host_ou
 spt_status spt_layer_get_dx(spt_layer* layer, void* host_out);
 /* MemoryLedger::summary_json (ledger.hpp:85) of the device tier + cudaMemGetInfo cross-check. */
 spt_status spt_layer_memory_json(spt_layer* layer, char* buf, size_t cap);
+/* MemoryLedger::timeline_csv (ledger.hpp:85, ledger.cpp:149-157): one row per tracked allocation / release,
+ * "ordinal,kind,tier,tag,delta_bytes,device_live,host_live".  SPT_ERR_SHAPE if cap is too small. */
+spt_status spt_layer_memory_timeline_csv(spt_layer* layer, char* buf, size_t cap);
 /* Per-phase CUDA-event timings of the last step (ms) as JSON (requires spt_layer_set_profiling(1)). */
 spt_status spt_layer_set_profiling(spt_layer* layer, int32_t on);
 spt_status spt_layer_timing_json(spt_layer* layer, char* buf, size_t cap);

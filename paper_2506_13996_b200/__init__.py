@@ -155,6 +155,7 @@ SIGNATURES = {
     "spt_layer_get_grad": (I32, [P, C.c_char_p, P]),
     "spt_layer_get_dx": (I32, [P, P]),
     "spt_layer_memory_json": (I32, [P, C.c_char_p, SZ]),
+    "spt_layer_memory_timeline_csv": (I32, [P, C.c_char_p, SZ]),
     "spt_layer_set_profiling": (I32, [P, I32]),
     "spt_layer_timing_json": (I32, [P, C.c_char_p, SZ]),
     "spt_kernel_launch_count": (I64, []),
@@ -604,6 +605,12 @@ class UlyssesLayerStep:
         b = C.create_string_buffer(1 << 16)
         check(lib().spt_layer_memory_json(self.handle, b, len(b)))
         return json.loads(b.value.decode())
+
+    def memory_timeline_csv(self) -> str:
+        """The device ledger's event timeline (reference MemoryLedger::timeline_csv columns)."""
+        b = C.create_string_buffer(1 << 20)
+        check(lib().spt_layer_memory_timeline_csv(self.handle, b, len(b)))
+        return b.value.decode()
 
     def set_profiling(self, on: bool):
         check(lib().spt_layer_set_profiling(self.handle, int(on)))

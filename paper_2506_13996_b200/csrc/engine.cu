@@ -65,6 +65,20 @@ struct DeviceLedger {
     uint64_t live = 0, peak = 0, budget = 0;
     uint64_t tag_live[kNumTags] = {}, tag_peak[kNumTags] = {}, largest[kNumTags] = {};
     uint64_t events = 0;
+    // event timeline in the reference's MemoryLedger::timeline_csv form (ledger.cpp:149-157): kind 'A' track /
+    // 'R' release, tier device / host, the tag, the signed byte delta and both tiers' live bytes after it
+    struct Event {
+        uint64_t ordinal;
+        char kind;
+        bool host;
+        int tag;
+        int64_t delta;
+        uint64_t device_live, host_live;
+    };
+    std::vector<Event> timeline;
+    void push(char kind, bool host, int tag, int64_t delta) {
+        timeline.push_back(Event{events, kind, host, tag, delta, live, host_live});
+    }
     std::unordered_map<void*, std::pair<int, size_t>> allocs;
     spt_comm* sym_comm = nullptr;  // peer mode: allocations made with alloc_sym are symmetric (comm.h)
     std::unordered_map<void*, char> sym_allocs;
@@ -89,6 +103,7 @@ struct DeviceLedger {
         tag_peak[tag] = std::max(tag_peak[tag], tag_live[tag]);
         largest[tag] = std::max<uint64_t>(largest[tag], bytes);
         allocs[p] = {tag, bytes};
+        push('A', false, tag, (int64_t)bytes);
         ++events;
         return p;
     }
@@ -104,6 +119,7 @@ struct DeviceLedger {
         } else {
             cudaFree(p);
         }
+        push('R', false, it->second.first, -(int64_t)it->second.second);
         allocs.erase(it);
         ++events;
     }
@@ -116,6 +132,7 @@ struct DeviceLedger {
         host_live += bytes;
         host_peak = std::max(host_peak, host_live);
         host_allocs[p] = bytes;
+        push('A', true, kActivationCkpt, (int64_t)bytes);
         ++events;
         return p;
     }
@@ -126,8 +143,18 @@ struct DeviceLedger {
         for (auto& kv : host_allocs) {
             cudaFreeHost(kv.first);
             host_live -= kv.second;
+            push('R', true, kActivationCkpt, -(int64_t)kv.second);
+            ++events;
         }
         host_allocs.clear();
+    }
+    std::string timeline_csv() const {
+        std::ostringstream os;
+        os << "ordinal,kind,tier,tag,delta_bytes,device_live,host_live\n";
+        for (const Event& e : timeline)
+            os << e.ordinal << "," << e.kind << "," << (e.host ? "host" : "device") << "," << tag_name(e.tag) << ","
+               << e.delta << "," << e.device_live << "," << e.host_live << "\n";
+        return os.str();
     }
     std::string summary_json() const {
         std::ostringstream os;
@@ -1141,6 +1168,14 @@ spt_status spt_layer_memory_json(spt_layer* Ly, char* buf, size_t cap) {
            << ",\"comm\":" << Ly->comm->stats_json() << "}";
         std::string s = os.str();
         SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+spt_status spt_layer_memory_timeline_csv(spt_layer* Ly, char* buf, size_t cap) {
+    return capi_guard([&] {
+        const std::string s = Ly->led.timeline_csv();
+        SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small: need " + std::to_string(s.size() + 1));
         std::memcpy(buf, s.c_str(), s.size() + 1);
     });
 }

@@ -578,6 +578,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     tc_fence_before();
     cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
+    // The cluster barrier (release / acquire) already orders tcgen05.alloc's write of the slot; the CTA barrier
+    // makes that ordering visible to compute-sanitizer's racecheck too (it models bar.sync, not barrier.cluster),
+    // once per kernel.
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 

@@ -50,6 +50,7 @@ def _run(L, P, N, offload=False, packed=False, cfg=CFG, shape=SHAPE, seed=3, rop
         grads = {k: eng.grad(k) for k in names}
         dx_bits = eng.dx_bits(N)
         mem = eng.memory()
+        mem["timeline_csv"] = eng.memory_timeline_csv()
     finally:
         eng.close()
         grp.close()
@@ -76,7 +77,7 @@ def test_multilayer_matches_oracle(L, P, offload, packed):
 
 
 def test_multilayer_tiny_shape_sp2():
-    """head_dim 32 (mma.sync attention path) through the same checkpointed stack."""
+    """head_dim 32 (tcgen05 attention on a 64-column tile) through the same checkpointed stack."""
     r = _run(2, 2, 512, offload=True, cfg=TINY, shape=TINY_SHAPE)
     _check(r, 2, 2, cfg=TINY)
 
@@ -421,3 +422,26 @@ def test_sgd_20_steps_sp_equals_sp1(P, cfg, shape):
     dev = np.abs(lp - l1) / l1
     assert dev.max() <= 2e-3, (dev.max(), l1, lp)
     assert l1[-1] < l1[0] - 0.05  # the updates do train
+
+
+def test_ledger_timeline_csv():
+    """The device ledger's event timeline (reference MemoryLedger::timeline_csv columns, ledger.cpp:149-157):
+    replaying the deltas reproduces the live counters of every row, the device peak of the summary and, with
+    offload, the pinned-host checkpoint bytes L * (s/P) * h * 2."""
+    L, P, N = 3, 2, 1024
+    r = _run(L, P, N, offload=True)
+    rows = r["mem"]["timeline_csv"].strip().splitlines()
+    assert rows[0] == "ordinal,kind,tier,tag,delta_bytes,device_live,host_live"
+    dev = host = peak = 0
+    for line in rows[1:]:
+        o, kind, tier, tag, delta, dl, hl = line.split(",")
+        assert kind in ("A", "R") and tier in ("device", "host")
+        if tier == "device":
+            dev += int(delta)
+        else:
+            host += int(delta)
+        peak = max(peak, dev)
+        assert (dev, host) == (int(dl), int(hl))
+    led = r["mem"]["ledger"]
+    assert peak == led["device"]["peak_bytes"]
+    assert host == led["host"]["live_bytes"] == L * (N // P) * CFG.hidden * 2 * P
