@@ -66,53 +66,91 @@ def peaks():
 _CPU_CACHE = {}
 
 
-def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1"):
-    """One oracle layer step (fwd+bwd) on an n_tokens sample of the workload; returns (seconds, loss)."""
+def cpu_sample_tokens(args):
+    """Tokens per CPU step: 256 of the L1 workload (each with its full causal attention context, below), the
+    whole configs[0] sequence (8192) for --workload tiny."""
+    return args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 8192)
+
+
+def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: int = 0):
+    """One CPU step of the reference algorithm (oracle/sptrain_oracle.py, float32) on an n-token sample of the
+    workload; returns (seconds, loss).
+
+    The step is the oracle's layer_step (fwd+bwd: projections, attention, TiledMLP, tiled logits/CE, RMSNorms) on
+    n tokens.  Every op but attention is token-local, so its per-token cost is the workload's.  Attention is not:
+    in a seq-token sequence a token attends to its whole causal prefix.  When seq > n the step therefore also
+    runs the attention of n query rows spread evenly over the seq-token sequence (mean context seq/2) against
+    their full prefix: forward O / LSE (attention_rows) and dQ (attention_bwd_rows), float32, on synthetic Q/K/V/dO
+    of the workload's shape (set up once, outside the timed region)."""
     import numpy as np
 
     from oracle import sptrain_oracle as O
 
     cfg = O.LLAMA8B if workload == "l1" else O.LayerConfig(**SHAPES["tiny"])
-    key = (n_tokens, seed, workload)
-    if key not in _CPU_CACHE:  # synthetic weights/batch are set-up, not part of the timed step
-        p = O.LayerParams(**O.synth_params(cfg, seed)).astype(np.float32)
-        _CPU_CACHE[key] = (p, O.synth_batch(cfg, n_tokens, seed))
-    p, (x, lab, pos) = _CPU_CACHE[key]
+    # synthetic weights / batches are set-up, not part of the timed step
+    if ("w", seed, workload) not in _CPU_CACHE:
+        _CPU_CACHE[("w", seed, workload)] = O.LayerParams(**O.synth_params(cfg, seed)).astype(np.float32)
+    if (n_tokens, seed, workload) not in _CPU_CACHE:
+        _CPU_CACHE[(n_tokens, seed, workload)] = O.synth_batch(cfg, n_tokens, seed)
+    p = _CPU_CACHE[("w", seed, workload)]
+    x, lab, pos = _CPU_CACHE[(n_tokens, seed, workload)]
+    attn = None
+    if seq > n_tokens:
+        akey = ("attn", seq, n_tokens, workload)
+        if akey not in _CPU_CACHE:
+            rng = np.random.default_rng(seed)
+            hq, hkv, d = cfg.q_heads, cfg.kv_heads, cfg.head_dim
+            qkv = [rng.standard_normal((seq, h, d), dtype=np.float32) for h in (hq, hkv, hkv, hq)]
+            rows = ((np.arange(n_tokens) + 0.5) * (seq / n_tokens)).astype(np.int64)
+            _CPU_CACHE[akey] = (qkv, rows)
+        attn = _CPU_CACHE[akey]
     t0 = time.perf_counter()
     res = O.layer_step(p, cfg, x.astype(np.float32), lab, None, P=1, dtype=np.float32)
+    if attn is not None:
+        (q, k, v, do), rows = attn
+        o, lse = O.attention_rows(q, k, v, rows, dtype=np.float32)
+        O.attention_bwd_rows(q, k, v, do, rows, o, lse, dtype=np.float32)
     return time.perf_counter() - t0, res.loss
 
 
-def cpu_sample_desc(n, workload):
-    attn = ("attention is ~15% of the per-token model flops at N=32768 and negligible at this sample size, so "
-            "the CPU rate is an upper bound of its full-sequence rate" if workload == "l1" else
-            "full configs[0] shape")
-    return (f"{n}-token sample of the workload per step (oracle/sptrain_oracle.py layer_step, float32 "
-            f"numpy/OpenBLAS, SP=1); {attn}")
+def cpu_sample_desc(n, workload, seq):
+    if workload == "l1":
+        ctx = (f" plus the attention forward + dQ of {n} query rows spread evenly over the {seq}-token sequence "
+               f"against their full causal prefix (mean context {seq // 2}; the dK/dV share of the backward, 2 of "
+               f"its 5 products, is not in the sample)") if seq > n else ""
+        return (f"{n}-token sample of the workload per step: oracle/sptrain_oracle.py layer_step (float32 "
+                f"numpy/OpenBLAS, SP=1){ctx}")
+    return f"{n}-token step of configs[0] (oracle/sptrain_oracle.py layer_step, float32 numpy/OpenBLAS, SP=1)"
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    n = args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 2048)
+    n = cpu_sample_tokens(args)
     cores = os.cpu_count() or 1
+    seq = args.seq or default_seq(args.workload, world)
     for _ in range(args.warmup):
-        cpu_layer_sample(n, workload=args.workload)
-    times = [cpu_layer_sample(n, workload=args.workload)[0] for _ in range(args.steps)]
+        cpu_layer_sample(n, workload=args.workload, seq=seq)
+    times = [cpu_layer_sample(n, workload=args.workload, seq=seq)[0] for _ in range(args.steps)]
     tot = sum(times)
     v = n * len(times) / tot
-    seq = args.seq or default_seq(args.workload, world)
     line = {
         "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * tot / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": workload_name(seq, world, workload=args.workload), "seq_len": seq,
-                   "sp_degree": world, "cpu_model": cpu_model()},
+                   "tokens_per_gpu": seq // world, "sp_degree": world, "cpu_model": cpu_model()},
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": cpu_sample_desc(n, args.workload)},
+                         "sample": cpu_sample_desc(n, args.workload, seq)},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.workload == "l1" and args.cpu_reduced_n:
+        # SURVEY.md §8(d): the L shape at a reduced N, measured whole (attention included), one timed step
+        nr = args.cpu_reduced_n
+        t, _ = cpu_layer_sample(nr, workload="l1")  # weights / batch set-up happens before the timer starts
+        line["cpu_reduced_n"] = {"seq_len": nr, "value": nr / t, "unit": "tokens/s", "ms_per_step": 1000.0 * t,
+                                 "note": "whole L-shape layer step at this N (1 timed step), not the L1 workload"}
     print(json.dumps(line), flush=True)
 
 
@@ -376,11 +414,11 @@ def run_ours(args, rank, world, local_rank):
            for k, v in sites_acc.items() if k.startswith("a2a_")}
     cpu_v = None
     if world == 1 and not args.no_cpu_baseline:
-        n = args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 2048)
-        cpu_layer_sample(n, workload=args.workload)
-        ts = [cpu_layer_sample(n, workload=args.workload)[0] for _ in range(2)]
+        n = cpu_sample_tokens(args)
+        cpu_layer_sample(n, workload=args.workload, seq=seq)
+        ts = [cpu_layer_sample(n, workload=args.workload, seq=seq)[0] for _ in range(2)]
         cpu_v = {"value": n * len(ts) / sum(ts), "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "port",
-                 "sample": cpu_sample_desc(n, args.workload) + ", 2 steps", "cpu_model": cpu_model()}
+                 "sample": cpu_sample_desc(n, args.workload, seq) + ", 2 steps", "cpu_model": cpu_model()}
     est, per_tok = est_max_seq(S, shp, mem, n_loc, world)
     tokens = seq  # whole-job tokens per step (all ranks)
     line = {
@@ -442,7 +480,9 @@ def main():
     ap.add_argument("--lr", type=float, default=0.0)
     ap.add_argument("--loss-tile", type=int, default=0, help="tokens per tiled-logits/CE tile (0: the engine's rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 256 for l1, 2048 for tiny)")
+    ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 256 for l1, 8192 for tiny)")
+    ap.add_argument("--cpu-reduced-n", type=int, default=2048,
+                    help="--impl reference, l1: also time one whole L-shape step at this N (0: skip)")
     ap.add_argument("--layers", type=int, default=1,
                     help="decoder layers (> 1: per-layer activation checkpointing; not the BASELINE config)")
     ap.add_argument("--offload", action="store_true", help="activation checkpoints in pinned host memory")

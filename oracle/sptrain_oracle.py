@@ -377,26 +377,27 @@ def attention_bwd(q, k, v, o, lse, do, starts=None, scale=None, q_block=256):
 # :59-67), float64, keys or queries walked in chunks with a running (max, sum) so no [rows, s] matrix lives.
 
 
-def _chunk64(a, lo, hi):
-    return np.asarray(a[lo:hi], dtype=np.float64)
+def _chunk64(a, lo, hi, dtype=np.float64):
+    return np.asarray(a[lo:hi], dtype=dtype)
 
 
-def attention_rows(q, k, v, rows, starts=None, scale=None, key_chunk=65536):
+def attention_rows(q, k, v, rows, starts=None, scale=None, key_chunk=65536, dtype=np.float64):
     """O and LSE of query rows `rows` (int array) of attention_fwd: q [s, Hq, d], k / v [s, Hkv, d] (any float
-    dtype, upcast per chunk).  Returns o [R, Hq, d] and lse [Hq, R] in float64."""
+    dtype, upcast per chunk).  Returns o [R, Hq, d] and lse [Hq, R] in `dtype` (float64 for parity checks; bench.py's
+    CPU arm times it in float32 like the rest of its f32 layer step)."""
     rows = np.asarray(rows, np.int64)
     s, Hq, d = q.shape
     Hkv = k.shape[1]
     g = Hq // Hkv
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     st = np.zeros(len(rows), np.int64) if starts is None else np.asarray(starts)[rows]
-    qr = np.asarray(q[rows], np.float64)  # [R, Hq, d]
-    m = np.full((Hq, len(rows)), -np.inf)
-    l = np.zeros((Hq, len(rows)))
-    acc = np.zeros((Hq, len(rows), d))
+    qr = np.asarray(q[rows], dtype)  # [R, Hq, d]
+    m = np.full((Hq, len(rows)), -np.inf, dtype)
+    l = np.zeros((Hq, len(rows)), dtype)
+    acc = np.zeros((Hq, len(rows), d), dtype)
     for k0 in range(0, int(rows.max()) + 1, key_chunk):
         k1 = min(s, k0 + key_chunk)
-        kc, vc = _chunk64(k, k0, k1), _chunk64(v, k0, k1)
+        kc, vc = _chunk64(k, k0, k1, dtype), _chunk64(v, k0, k1, dtype)
         kj = np.arange(k0, k1)
         allowed = (kj[None, :] <= rows[:, None]) & (kj[None, :] >= st[:, None])
         for h in range(Hq):
@@ -413,22 +414,23 @@ def attention_rows(q, k, v, rows, starts=None, scale=None, key_chunk=65536):
     return o, m + np.log(l)
 
 
-def attention_bwd_rows(q, k, v, do, rows, o_rows, lse_rows, starts=None, scale=None, key_chunk=65536):
+def attention_bwd_rows(q, k, v, do, rows, o_rows, lse_rows, starts=None, scale=None, key_chunk=65536,
+                       dtype=np.float64):
     """dQ of query rows `rows` (attention_bwd): dq_i = scale * sum_j P_ij (dO_i . v_j - D_i) k_j, D_i = dO_i . o_i,
-    with o_rows [R, Hq, d] / lse_rows [Hq, R] from attention_rows.  Returns dq [R, Hq, d] float64."""
+    with o_rows [R, Hq, d] / lse_rows [Hq, R] from attention_rows.  Returns dq [R, Hq, d] in `dtype`."""
     rows = np.asarray(rows, np.int64)
     s, Hq, d = q.shape
     Hkv = k.shape[1]
     g = Hq // Hkv
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     st = np.zeros(len(rows), np.int64) if starts is None else np.asarray(starts)[rows]
-    qr = np.asarray(q[rows], np.float64)
-    dor = np.asarray(do[rows], np.float64)
+    qr = np.asarray(q[rows], dtype)
+    dor = np.asarray(do[rows], dtype)
     D = np.sum(dor * o_rows, axis=2)  # [R, Hq]
-    dq = np.zeros((len(rows), Hq, d))
+    dq = np.zeros((len(rows), Hq, d), dtype)
     for k0 in range(0, int(rows.max()) + 1, key_chunk):
         k1 = min(s, k0 + key_chunk)
-        kc, vc = _chunk64(k, k0, k1), _chunk64(v, k0, k1)
+        kc, vc = _chunk64(k, k0, k1, dtype), _chunk64(v, k0, k1, dtype)
         kj = np.arange(k0, k1)
         allowed = (kj[None, :] <= rows[:, None]) & (kj[None, :] >= st[:, None])
         for h in range(Hq):

@@ -31,11 +31,15 @@ def _check_common(d):
 
 
 def test_reference_arm_contract():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], timeout=900)
+    # small sample (64 tokens, each with its full-context attention rows in the 32K sequence) + the reduced-N step
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--cpu-tokens", "64", "--cpu-reduced-n", "128"],
+             timeout=900)
     _check_common(d)
     assert d["impl"] == "reference"
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert "32768-token sequence" in cb["sample"]
+    assert d["cpu_reduced_n"]["seq_len"] == 128 and d["cpu_reduced_n"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
 
 
