@@ -513,6 +513,12 @@ constexpr int KV_BYTES = BKB * D * 2;  // 32 KiB per K or V block (two 16 KiB re
 #define SPT_FWD2_NSL 4
 #endif
 constexpr int NSL = SPT_FWD2_NSL;  // K/V ring slots (5 is the most that fits next to the two Q tiles)
+// 12 warps = 3 warpgroups: two softmax warpgroups (one per query tile) and one for the MMA issuer (warp 8), the
+// TMA producer (warp 9) and two idle warps.  ptxas sizes registers per warpgroup multiple (the old 10-warp launch
+// was capped at 65536 / 384 = 168 and spilled the softmax loop state); setmaxnreg moves them where they are used.
+constexpr int THREADS = 384;
+constexpr int REG_SOFTMAX = 216, REG_PRODUCER = 64;  // 2 * 128 * 216 + 128 * 64 <= 168 * 384
+static_assert(2 * 128 * REG_SOFTMAX + 128 * REG_PRODUCER <= 168 * THREADS, "register budget");
 constexpr int OFF_Q = 0, OFF_KV = 2 * Q_BYTES;
 constexpr int OFF_BAR = OFF_KV + NSL * KV_BYTES;
 constexpr int SMEM = OFF_BAR + 512 + 1024;
@@ -525,7 +531,7 @@ constexpr int SMEM = OFF_BAR + 512 + 1024;
 // fill past the last head).  The score MMA contracts over DH only; the PV MMA runs N = DP, and output columns
 // >= DH (the neighbour's V) are never stored.
 template <int POLY, int DH>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(fw2::THREADS, 1)
     fwd_tc128_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                      int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
                      float* __restrict__ lse, int kvg, int filter) {
@@ -583,8 +589,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
     const uint32_t sbase = smem_u32(smem);
-
+    // setmaxnreg inside each role branch, so every role's code is dominated by its own register limit
     if (warp == 9) {
+        reg_dealloc<REG_PRODUCER>();
         if (lane == 0) {
             tma_prefetch_desc(&tq);
             tma_prefetch_desc(&tkv);
@@ -606,6 +613,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 8) {
+        reg_dealloc<REG_PRODUCER>();
         {
             constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKB, false, false);
             constexpr uint32_t idesc_o = make_idesc_bf16(BQ, DP, false, true);
@@ -659,7 +667,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             mma_commit_w(&o_done[0]);
             mma_commit_w(&o_done[1]);
         }
-    } else {
+    } else if (warp < 8) {
+        reg_alloc<REG_SOFTMAX>();
         // ---------------- softmax warpgroups (thread = query row), 128 columns per block in 4 chunks of 32
         const int t = warp >> 2;
         const int sub = warp & 3;
@@ -800,6 +809,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         lse[(int64_t)h * s + q] = l > 0.f ? (m_use + __log2f(l)) * LN2 : -INFINITY;
         }
     fwd2_done:;
+    } else {
+        reg_dealloc<REG_PRODUCER>();  // warps 10, 11: no role
     }
     tc_fence_before();
     __syncthreads();
@@ -3051,9 +3062,8 @@ static int kv_group(int64_t s, int hkv, int d) {
     return (double)s * hkv * d * 4 > 160e6 ? 1 : hkv;
 }
 
-// SPT_ATTN_FWD_BK128=0|1|4|8 (run time: spt_tuning_set("attn_fwd_bk128", v)): forward with 128-key blocks
-// (default 1; 4 / 8: every 4th / 8th exponential pair on the FMA pipe, measured slower; 0: the 64-key
-// double-buffered kernel).  With the P hand-off split in halves it measured -3% at 32K x 32 heads, -3.4% at
+// SPT_ATTN_FWD_BK128 (run time: spt_tuning_set("attn_fwd_bk128", v)): forward with 128-key blocks
+// (default 1, values below fwd_bk128; 0: the 64-key double-buffered kernel).  With the P hand-off split in halves it measured -3% at 32K x 32 heads, -3.4% at
 // 128K x 4, -6% at the L8 rank shape (profiles/r1z3_fwd_bk128.txt).  -1: 128-key only for s * hq >= 2^21
 // (the rule before the split hand-off).
 // SPT_ATTN_FWD_HYBRID=0|1 (run time: spt_tuning_set("attn_fwd_hybrid", v)): packed sequences split per tile
@@ -3071,13 +3081,18 @@ int g_attn_fwd_bk128 = [] {
 }();
 // Packed sequences keep the 64-key kernel: with short samples most 128-key blocks straddle a sample start
 // (s=128K, mean sample 2048: 6.57 vs 4.56 ms), while long samples gain only a few % (32768: 57.7 vs 61.3 ms).
-// Values: 1 (default) 128-key unless packed, 2 128-key always, 0 64-key, 4 / 8 128-key + FMA-pipe exp2,
-// 3 128-key with f16x2 exponentials, 10 + n (n = 2, 3, 4, 6, 8): 128-key with every n-th exponential pair of
-// an unmasked block on the FMA pipe (packed ex2_poly2),
-// -1 128-key for s * hq >= 2^21.  Returns 0 (64-key) or the 128-key kernel's POLY selector (1, 4, 8).
+// Values: 1 (default) 128-key with every 3rd exponential pair of an unmasked block on the FMA pipe (= 13) unless
+// packed, 11 the same with every exponential on MUFU (the default before the 12-warp register split), 2 128-key
+// always, 0 64-key, 4 / 8 128-key + FMA-pipe exp2, 3 128-key with f16x2 exponentials, 10 + n (n = 2, 3, 4, 6, 8):
+// 128-key with every n-th exponential pair of an unmasked block on the FMA pipe (packed ex2_poly2),
+// -1 128-key for s * hq >= 2^21.  Returns 0 (64-key) or the 128-key kernel's POLY selector.
+// The FMA-pipe share became a win once the softmax stopped spilling (12 warps, setmaxnreg): every 3rd pair
+// measured -2.2% at 32K x 32q/8kv, -9.7% at 128K x 4q/1kv, -2.7% at the L8 rank shape, -9.1% at 64K x 8q/2kv
+// (profiles/r2d_fwd_regsplit.txt); every 2nd / 4th pair and MUFU-only were slower.
 static int fwd_bk128(int64_t s, int hq, const int32_t* seg) {
     const int v = g_attn_fwd_bk128;
-    if (v == 1) return seg != nullptr ? 0 : 1;
+    if (v == 1) return seg != nullptr ? 0 : 13;
+    if (v == 11) return seg != nullptr ? 0 : 11;
     if (v == 2) return 1;
     if (v == -1) return (double)s * hq >= 2097152.0 ? 1 : 0;
     return v;
@@ -3110,7 +3125,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
     if (d != 128) {  // head dims 64 / 32: the 128-key kernel (plain causal and packed) on DP = 64 columns
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
         auto k = d == 64 ? fatc::fwd_tc128_kernel<0, 64> : fatc::fwd_tc128_kernel<0, 32>;
-        k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
+        k<<<grid, fatc::fw2::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
                                                         kv_group(s, hkv, d), 0);
         count_launch("attn_fwd_tc");
         SPT_CUDA(cudaGetLastError());
@@ -3125,13 +3140,13 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                  : bk128 == 13 ? fatc::fwd_tc128_kernel<3, 128>
                  : bk128 == 16 ? fatc::fwd_tc128_kernel<6, 128>
                  : bk128 == 3 ? fatc::fwd_tc128_kernel<1, 128>
-                              : fatc::fwd_tc128_kernel<0, 128>;
-        k<<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
+                              : fatc::fwd_tc128_kernel<0, 128>;  // 1, 2, 11: every exponential on MUFU
+        k<<<grid, fatc::fw2::THREADS, fatc::fw2::SMEM, st>>>(tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse,
                                                         kv_group(s, hkv, d), 0);
     } else if (seg != nullptr && g_attn_fwd_bk128 == 1 && g_attn_fwd_hybrid) {
         // packed: long-sample tile pairs on the 128-key kernel, short ones on the 64-key kernel
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
-        fatc::fwd_tc128_kernel<0, 128><<<grid, fatc::THREADS, fatc::fw2::SMEM, st>>>(
+        fatc::fwd_tc128_kernel<0, 128><<<grid, fatc::fw2::THREADS, fatc::fw2::SMEM, st>>>(
             tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse, kv_group(s, hkv, d), 1);
         fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
                                                                           (bf16*)o, lse, kv_group(s, hkv, d), 2);

@@ -30,16 +30,31 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 // ------------------------------------------------------------------ RMSNorm
 // One thread owns 8 consecutive columns (one uint4); blockDim = max(32, h/8).
-__global__ void rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, bf16* __restrict__ y,
+// The next row's 16-byte loads are issued (kept packed, 4 registers each) before the current row's block
+// reduction, so two rows per CTA are in flight; the arithmetic is unchanged (bitwise equal to one row at a time).
+__device__ __forceinline__ void unpack8(const uint4 w, float* v) {
+    float2 a = unpack_bf16x2(w.x), b = unpack_bf16x2(w.y), c = unpack_bf16x2(w.z), d = unpack_bf16x2(w.w);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y; v[6] = d.x; v[7] = d.y;
+}
+__device__ __forceinline__ uint4 ld16(const bf16* p) { return *reinterpret_cast<const uint4*>(p); }
+
+// REGS: register cap (48 for h <= 5120: two 640-thread CTAs per SM; 64 for up to 1024 threads)
+template <int REGS>
+__global__ void __maxnreg__(REGS) rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, bf16* __restrict__ y,
                                    float* __restrict__ rstd, int64_t n, int h, float eps) {
     __shared__ float red[32];
     const int c = threadIdx.x * 8;
     const bool act = c < h;
     float gv[8];
     if (act) load8(g + c, gv);
+    uint4 xq = make_uint4(0, 0, 0, 0);
+    if (act && blockIdx.x < n) xq = ld16(x + (int64_t)blockIdx.x * h + c);
     for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
-        float xv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (act) load8(x + r * h + c, xv);
+        const int64_t rn = r + gridDim.x;
+        uint4 xqn = make_uint4(0, 0, 0, 0);
+        if (act && rn < n) xqn = ld16(x + rn * h + c);
+        float xv[8];
+        unpack8(xq, xv);
         float ss = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) ss += xv[i] * xv[i];
@@ -52,10 +67,11 @@ __global__ void rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __res
             store8(y + r * h + c, o);
         }
         if (threadIdx.x == 0) rstd[r] = rs;
+        xq = xqn;
     }
 }
 
-__global__ void rmsnorm_bwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+__global__ void __launch_bounds__(1024, 1) rmsnorm_bwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
                                    const float* __restrict__ rstd, const bf16* __restrict__ dy,
                                    const bf16* __restrict__ dres, bf16* __restrict__ dx, float* __restrict__ part,
                                    int64_t n, int h, int64_t rows_per_cta) {
@@ -66,20 +82,38 @@ __global__ void rmsnorm_bwd_kernel(const bf16* __restrict__ x, const bf16* __res
     float gv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dga[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (act) load8(g + c, gv);
     const int64_t r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
-    for (int64_t r = r0; r < r1; ++r) {
-        float xv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    uint4 xq = z, dq = z, rq = z;
+    float rs = 0.f;
+    if (r0 < r1) {
         if (act) {
-            load8(x + r * h + c, xv);
-            load8(dy + r * h + c, dv);
+            xq = ld16(x + r0 * h + c);
+            dq = ld16(dy + r0 * h + c);
+            if (dres) rq = ld16(dres + r0 * h + c);
         }
-        const float rs = rstd[r];
+        rs = rstd[r0];
+    }
+    for (int64_t r = r0; r < r1; ++r) {
+        uint4 xqn = z, dqn = z, rqn = z;  // next row, in flight during this row's reduction
+        float rsn = 0.f;
+        if (r + 1 < r1) {
+            if (act) {
+                xqn = ld16(x + (r + 1) * h + c);
+                dqn = ld16(dy + (r + 1) * h + c);
+                if (dres) rqn = ld16(dres + (r + 1) * h + c);
+            }
+            rsn = rstd[r + 1];
+        }
+        float xv[8], dv[8];
+        unpack8(xq, xv);
+        unpack8(dq, dv);
         float dot = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) dot += dv[i] * gv[i] * xv[i] * rs;
         const float tot = block_sum<32>(dot, red) / (float)h;
         if (act) {
-            float o[8], rr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (dres) load8(dres + r * h + c, rr);
+            float o[8], rr[8];
+            unpack8(rq, rr);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const float xh = xv[i] * rs;
@@ -88,6 +122,10 @@ __global__ void rmsnorm_bwd_kernel(const bf16* __restrict__ x, const bf16* __res
             }
             store8(dx + r * h + c, o);
         }
+        xq = xqn;
+        dq = dqn;
+        rq = rqn;
+        rs = rsn;
     }
     if (act) {
         float4* p = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * h + c);
@@ -113,8 +151,12 @@ void rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int64_t
                  cudaStream_t st) {
     if (n == 0) return;
     const int th = rms_threads(h);
-    rmsnorm_fwd_kernel<<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd, n,
-                                                         (int)h, eps);
+    if (th <= 640)
+        rmsnorm_fwd_kernel<48><<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd,
+                                                                 n, (int)h, eps);
+    else
+        rmsnorm_fwd_kernel<64><<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd,
+                                                                  n, (int)h, eps);
     count_launch();
     SPT_CUDA(cudaGetLastError());
 }

@@ -493,11 +493,12 @@ def test_embedding_rejects_bad_ids():
 
 @pytest.mark.parametrize("s,hq,hkv,packed,amp", [(1024, 4, 2, False, 1), (640, 4, 1, True, 1), (2048, 2, 1, False, 2.5),
                                                  (1536, 2, 2, True, 2.5), (384, 8, 2, False, 1)])
-@pytest.mark.parametrize("mode", [0, 2, 3, 8])
+@pytest.mark.parametrize("mode", [0, 2, 3, 8, 11])
 def test_attention_fwd_other_blocks(s, hq, hkv, packed, amp, mode):
     """Forward variants against the float64 oracle (O rel-err < 1e-2, lse abs err < 2e-3): 0 the 64-key
-    double-buffered kernel (default for packed sequences), 2 the 128-key kernel also on packed sequences, 8 the
-    128-key kernel with the FMA-pipe exp2 for every 8th pair.  The default choice is covered by every other
+    double-buffered kernel (default for packed sequences), 2 the 128-key MUFU-only kernel also on packed sequences,
+    8 the 128-key kernel with the FMA-pipe exp2 for every 8th pair, 11 the 128-key MUFU-only kernel (the causal
+    default before every 3rd pair moved to the FMA pipe).  The default choice is covered by every other
     attention test."""
     T = torch()
     L = _lib()
