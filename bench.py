@@ -34,7 +34,7 @@ SHAPES = {
     "tiny": dict(hidden=256, q_heads=8, kv_heads=2, head_dim=32, intermediate=1024, vocab=32000),
 }
 SHAPE = SHAPES["l1"]
-CPU_SAMPLE_TOKENS = 256
+CPU_SAMPLE_TOKENS = 512
 NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (spec)
 
 
@@ -67,7 +67,7 @@ _CPU_CACHE = {}
 
 
 def cpu_sample_tokens(args):
-    """Tokens per CPU step: 256 of the L1 workload (each with its full causal attention context, below), the
+    """Tokens per CPU step: 512 of the L1 workload (each with its full causal attention context, below), the
     whole configs[0] sequence (8192) for --workload tiny."""
     return args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 8192)
 
@@ -81,7 +81,7 @@ def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: in
     in a seq-token sequence a token attends to its whole causal prefix.  When seq > n the step therefore also
     runs the attention of n query rows spread evenly over the seq-token sequence (mean context seq/2) against
     their full prefix: forward O / LSE (attention_rows) and dQ (attention_bwd_rows), float32, on synthetic Q/K/V/dO
-    of the workload's shape (set up once, outside the timed region)."""
+    of the workload's shape (set up once, outside the timed region), one kv-head group per host thread."""
     import numpy as np
 
     from oracle import sptrain_oracle as O
@@ -108,9 +108,26 @@ def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: in
     res = O.layer_step(p, cfg, x.astype(np.float32), lab, None, P=1, dtype=np.float32)
     if attn is not None:
         (q, k, v, do), rows = attn
-        o, lse = O.attention_rows(q, k, v, rows, dtype=np.float32)
-        O.attention_bwd_rows(q, k, v, do, rows, o, lse, dtype=np.float32)
+        g = cfg.q_heads // cfg.kv_heads
+
+        def kv_group(j):  # one kv head and its q heads; numpy releases the GIL, so groups run on separate cores
+            qs, ks = slice(j * g, (j + 1) * g), slice(j, j + 1)
+            o, lse = O.attention_rows(q[:, qs], k[:, ks], v[:, ks], rows, dtype=np.float32)
+            O.attention_bwd_rows(q[:, qs], k[:, ks], v[:, ks], do[:, qs], rows, o, lse, dtype=np.float32)
+
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(1):  # one BLAS thread per group: the groups already fill the cores
+            list(_cpu_pool().map(kv_group, range(cfg.kv_heads)))
     return time.perf_counter() - t0, res.loss
+
+
+def _cpu_pool():
+    import concurrent.futures as cf
+
+    if "pool" not in _CPU_CACHE:
+        _CPU_CACHE["pool"] = cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 1)
+    return _CPU_CACHE["pool"]
 
 
 def cpu_sample_desc(n, workload, seq):
@@ -480,7 +497,7 @@ def main():
     ap.add_argument("--lr", type=float, default=0.0)
     ap.add_argument("--loss-tile", type=int, default=0, help="tokens per tiled-logits/CE tile (0: the engine's rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 256 for l1, 8192 for tiny)")
+    ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 512 for l1, 8192 for tiny)")
     ap.add_argument("--cpu-reduced-n", type=int, default=2048,
                     help="--impl reference, l1: also time one whole L-shape step at this N (0: skip)")
     ap.add_argument("--layers", type=int, default=1,

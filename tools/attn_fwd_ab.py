@@ -1,6 +1,7 @@
-"""Interleaved A/B of attention-forward variants (spt_tuning_set("attn_fwd_bk128", v)) at given shapes, with the
-output of every variant compared against the default (v=1): norm-wise O error and max |LSE| difference.
-  python tools/attn_fwd_ab.py 1,12,13,14 32768:32:8 131072:4:1 [--rounds 3]"""
+"""Interleaved A/B of attention-forward variants (spt_tuning_set(key, v), key attn_fwd_bk128 by default) at given
+shapes, with the output of every variant compared against the first value's: norm-wise O error and max |LSE|
+difference.
+  python tools/attn_fwd_ab.py 1,11,12,13 32768:32:8 131072:4:1 [--rounds 3] [--key attn_kv_group --reset 0]"""
 import math
 import os
 import sys
@@ -12,10 +13,15 @@ import paper_2506_13996_b200 as S  # noqa: E402
 
 vals = [int(v) for v in sys.argv[1].split(",")]
 rounds = 3
-args = [a for a in sys.argv[2:] if not a.startswith("--")]
-if "--rounds" in sys.argv:
-    rounds = int(sys.argv[sys.argv.index("--rounds") + 1])
-    args = [a for a in args if a != str(rounds)]
+key, reset = b"attn_fwd_bk128", 1
+opts = {}
+for o in ("--rounds", "--key", "--reset"):
+    if o in sys.argv:
+        opts[o] = sys.argv[sys.argv.index(o) + 1]
+args = [a for a in sys.argv[2:] if not a.startswith("--") and a not in opts.values()]
+rounds = int(opts.get("--rounds", rounds))
+key = opts.get("--key", key.decode()).encode()
+reset = int(opts.get("--reset", reset))
 L = S.lib()
 d = 128
 for shp in args:
@@ -29,7 +35,7 @@ for shp in args:
     n = max(1, int(2e13 / fl))
 
     def run(v, reps):
-        S.check(L.spt_tuning_set(b"attn_fwd_bk128", v))
+        S.check(L.spt_tuning_set(key, v))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
@@ -38,7 +44,7 @@ for shp in args:
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    run(1, 1)
+    run(vals[0], 1)
     o_ref, l_ref = o.float().clone(), lse.clone()
     best = {v: 1e30 for v in vals}
     for v in vals:
@@ -51,6 +57,6 @@ for shp in args:
             best[v] = min(best[v], run(v, n))
     print(f"s={s} hq={hq} hkv={hkv}: " + "  ".join(f"v={v} {best[v]:.3f} ms ({fl / best[v] / 1e9:.0f} TF/s)"
                                                     for v in vals), flush=True)
-    S.check(L.spt_tuning_set(b"attn_fwd_bk128", 1))
+    S.check(L.spt_tuning_set(key, reset))
     del qkv, o, lse
     torch.cuda.empty_cache()
