@@ -11,20 +11,22 @@ import time
 import numpy as np
 
 
-def _init(rank, world, port):
+def _init(rank, world, port, device=0):
     import torch
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(device)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     return torch, dist
 
 
-def engine_case(rank, world, port, outdir, cfg_kw, N, seed, packed, rope, graph):
-    """One layer step on this rank's sequence shard through a peer group; saves loss, grads, dx."""
-    torch, dist = _init(rank, world, port)
+def engine_case(rank, world, port, outdir, cfg_kw, N, seed, packed, rope, graph, transport="peer", multi_gpu=False):
+    """One layer step on this rank's sequence shard through a peer (or NCCL) group; saves loss, grads, dx.
+    multi_gpu: rank r runs on cuda:r (one process per GPU, as under torchrun) instead of every rank on cuda:0."""
+    device = rank if multi_gpu else 0
+    torch, dist = _init(rank, world, port, device)
     import paper_2506_13996_b200 as S
     from oracle import sptrain_oracle as O
 
@@ -34,8 +36,13 @@ def engine_case(rank, world, port, outdir, cfg_kw, N, seed, packed, rope, graph)
     x, lab, pos = O.synth_batch(cfg, N, seed, packed=packed)
     n_loc = N // world
     sl = slice(rank * n_loc, (rank + 1) * n_loc)
-    grp = S.ProcessGroup.peer_group(world, rank, 0, timeout_ms=60000)
-    assert grp.transport == "peer"
+    if transport == "nccl":
+        uid = [S.ProcessGroup.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        grp = S.ProcessGroup.nccl_group(uid[0], world, rank, device)
+    else:
+        grp = S.ProcessGroup.peer_group(world, rank, device, timeout_ms=60000)
+    assert grp.transport == transport
     eng = S.UlyssesLayerStep(shape, N, grp, packed=packed, rope_theta=rope)
     for k in O.LayerParams.NAMES:
         eng.set_param(k, O.f32_to_bf16_bits(params[k]))
@@ -47,7 +54,7 @@ def engine_case(rank, world, port, outdir, cfg_kw, N, seed, packed, rope, graph)
     for k in O.LayerParams.NAMES:
         out["g_" + k] = eng.grad(k)
     if graph:  # a captured step replays bit-identically (the barrier epochs live on the device)
-        dev = torch.device("cuda", 0)
+        dev = torch.device("cuda", device)
         xd = torch.from_numpy(xb.view(np.int16)).to(dev)
         ld = torch.from_numpy(lab_r).to(dev)
         pd = torch.from_numpy(pos_r).to(dev) if packed else None
