@@ -530,7 +530,7 @@ constexpr int SMEM = OFF_BAR + 512 + 1024;
 // columns of it (one 64-column TMA box: for d = 32 the box also brings the next head's 32 columns, or TMA's zero
 // fill past the last head).  The score MMA contracts over DH only; the PV MMA runs N = DP, and output columns
 // >= DH (the neighbour's V) are never stored.
-template <int POLY, int DH, bool EARLY = false>
+template <int POLY, int DH>
 __global__ void __launch_bounds__(fw2::THREADS, 1)
     fwd_tc128_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, int64_t s, int hq,
                      int hkv, const int32_t* __restrict__ seg, float scale_log2, bf16* __restrict__ o,
@@ -688,86 +688,21 @@ __global__ void __launch_bounds__(fw2::THREADS, 1)
             const int64_t k0 = (int64_t)j * BKB;
             const bool need_mask = (k0 + BKB - 1 > q0 + t * BQ) || (seg != nullptr && __any_sync(0xffffffffu, start > k0));
             uint32_t v[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(t_tm + c * 32, v[c]);
+            tmem_ld_wait();
             float mp[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) mp[u] = -INFINITY;
-            const int hi = (int)(q - k0), lo_ = start - (int)k0;
-            auto mask_chunk = [&](int c) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int col = c * 32 + i;
-                    if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
-                }
-            };
-            // EARLY: chunk 0 first, so its speculative exponentials (below) run while chunks 1-3 are still loading
-            tmem_ld32(t_tm, v[0]);
-            if (EARLY) {
-                tmem_ld_wait();
-                if (need_mask) mask_chunk(0);
-            }
-#pragma unroll
-            for (int c = 1; c < 4; ++c) tmem_ld32(t_tm + c * 32, v[c]);
-            if (!EARLY) {
-                tmem_ld_wait();
-                if (need_mask) mask_chunk(0);
-            }
-            const uint64_t sc2 = f2pack(scale_log2, scale_log2);
-            uint64_t rs2[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
-            // P for chunk c (32 keys) -> 16 packed columns at [16c, 16c+16): the chunk's S columns [32c, 32c+32)
-            // were already read into registers, and chunk c's P never lands on a chunk not yet read
-            // POLY > 1: on unmasked blocks every POLY-th exponential pair runs on the FMA pipe (ex2_poly2), so
-            // the MUFU pipe — exactly saturated by two 128x128 tiles at full tensor rate — is no longer the
-            // co-bottleneck; masked blocks stay on MUFU (masked entries exactly 0).
-            auto chunk = [&](int c, auto use_poly, uint64_t nb2, uint32_t(&pw)[16]) {
-                constexpr bool UP = decltype(use_poly)::value;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), sc2, nb2);
-                    float x0, x1;
-                    f2unpack(x2, x0, x1);
-                    float p0, p1;
-                    if constexpr (POLY == 1) {  // two exponentials per MUFU op in f16 (P is bf16 anyway)
-                        ex2_f16x2(x0, x1, p0, p1);
-                    } else if constexpr (UP) {
-                        if ((c * 16 + k) % POLY == POLY - 1) ex2_poly2(x0, x1, p0, p1);
-                        else {
-                            p0 = ex2(x0);
-                            p1 = ex2(x1);
-                        }
-                    } else {
-                        p0 = ex2(x0);
-                        p1 = ex2(x1);
-                    }
-                    rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
-                    pw[k] = pack_bf16x2(p0, p1);
-                }
-            };
-            auto put = [&](int c, const uint32_t(&pw)[16]) {
-                tmem_st16(t_tm + c * 16, pw);
-                if (c < 3 && (c + 1) % (4 / NPART) == 0) {  // this part of P done: its PV MMAs can start
-                    tmem_st_wait();
-                    tc_fence_before();
-                    mbar_arrive(&p_full[NPART * t + (c + 1) / (4 / NPART) - 1]);
-                }
-            };
-            const bool use_poly = POLY > 1 && !need_mask;
-            // EARLY: chunk 0's exponentials against the running maximum are issued BEFORE the block maximum is
-            // formed (MUFU / FMA work overlapping the 64 FMNMX3); they are exactly the ones the block needs unless
-            // some row of the warp raises its maximum by more than RESCALE_THRESHOLD, in which case they are
-            // recomputed.  Bitwise equal to the non-early kernel either way.
-            const bool spec = EARLY && n > 0 && __all_sync(0xffffffffu, m_use != -INFINITY);
-            uint32_t pw0[16];
-            if (spec) {
-                const uint64_t nbs = f2pack(-m_use, -m_use);
-                if (use_poly) chunk(0, std::true_type{}, nbs, pw0);
-                else chunk(0, std::false_type{}, nbs, pw0);
-            }
-            if (EARLY) tmem_ld_wait();
             if (need_mask) {
+                const int hi = (int)(q - k0), lo_ = start - (int)k0;
 #pragma unroll
-                for (int c = 1; c < 4; ++c) mask_chunk(c);
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int col = c * 32 + i;
+                        if (col > hi || col < lo_) v[c][i] = __float_as_uint(-INFINITY);
+                    }
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c)
@@ -779,7 +714,6 @@ __global__ void __launch_bounds__(fw2::THREADS, 1)
                                      fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
             const float mx = mraw * scale_log2;
             const bool grow = mx > m_use + RESCALE_THRESHOLD;
-            const bool keep0 = spec && !__any_sync(0xffffffffu, grow);  // chunk 0 computed above is exact
             const bool resc = grow && m_use != -INFINITY && n > 0;
             const float alpha = resc ? ex2(m_use - mx) : 1.f;
             if (__any_sync(0xffffffffu, resc)) {  // needs PV_t(j-1) complete
@@ -798,26 +732,51 @@ __global__ void __launch_bounds__(fw2::THREADS, 1)
             l *= alpha;
             if (grow) m_use = mx;
             const float nbase = m_use == -INFINITY ? 0.f : -m_use;
-            const uint64_t nb2 = f2pack(nbase, nbase);
-            auto rest = [&](auto up) {
-                if (keep0) {
-                    put(0, pw0);
-                } else {
+            const uint64_t sc2 = f2pack(scale_log2, scale_log2), nb2 = f2pack(nbase, nbase);
+            uint64_t rs2[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
-                    uint32_t pw[16];
-                    chunk(0, up, nb2, pw);
-                    put(0, pw);
-                }
+            for (int u = 0; u < 4; ++u) rs2[u] = f2pack(0.f, 0.f);
+            // P for chunk c (32 keys) -> 16 packed columns at [16c, 16c+16): the chunk's S columns [32c, 32c+32)
+            // were already read into registers, and chunk c's P never lands on a chunk not yet read
+            // POLY > 1: on unmasked blocks every POLY-th exponential pair runs on the FMA pipe (ex2_poly2), so
+            // the MUFU pipe — exactly saturated by two 128x128 tiles at full tensor rate — is no longer the
+            // co-bottleneck; masked blocks stay on MUFU (masked entries exactly 0).
+            auto exps = [&](auto use_poly) {
+                constexpr bool UP = decltype(use_poly)::value;
 #pragma unroll
-                for (int c = 1; c < 4; ++c) {
+                for (int c = 0; c < 4; ++c) {
                     uint32_t pw[16];
-                    chunk(c, up, nb2, pw);
-                    put(c, pw);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint64_t x2 = ffma2(f2pack(__uint_as_float(v[c][2 * k]), __uint_as_float(v[c][2 * k + 1])), sc2, nb2);
+                        float x0, x1;
+                        f2unpack(x2, x0, x1);
+                        float p0, p1;
+                        if constexpr (POLY == 1) {  // two exponentials per MUFU op in f16 (P is bf16 anyway)
+                            ex2_f16x2(x0, x1, p0, p1);
+                        } else if constexpr (UP) {
+                            if ((c * 16 + k) % POLY == POLY - 1) ex2_poly2(x0, x1, p0, p1);
+                            else {
+                                p0 = ex2(x0);
+                                p1 = ex2(x1);
+                            }
+                        } else {
+                            p0 = ex2(x0);
+                            p1 = ex2(x1);
+                        }
+                        rs2[k & 3] = fadd2(rs2[k & 3], f2pack(p0, p1));
+                        pw[k] = pack_bf16x2(p0, p1);
+                    }
+                    tmem_st16(t_tm + c * 16, pw);
+                    if (c < 3 && (c + 1) % (4 / NPART) == 0) {  // this part of P done: its PV MMAs can start
+                        tmem_st_wait();
+                        tc_fence_before();
+                        mbar_arrive(&p_full[NPART * t + (c + 1) / (4 / NPART) - 1]);
+                    }
                 }
             };
-            if (use_poly) rest(std::true_type{});
-            else rest(std::false_type{});
+            if (POLY > 1 && !need_mask) exps(std::true_type{});
+            else exps(std::false_type{});
             float rs0, rs1;
             f2unpack(fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3])), rs0, rs1);
             l += rs0 + rs1;
@@ -3156,8 +3115,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw::SMEM));
         for (auto k : {fatc::fwd_tc128_kernel<0, 128>, fatc::fwd_tc128_kernel<1, 128>, fatc::fwd_tc128_kernel<2, 128>,
                        fatc::fwd_tc128_kernel<3, 128>, fatc::fwd_tc128_kernel<4, 128>, fatc::fwd_tc128_kernel<6, 128>,
-                       fatc::fwd_tc128_kernel<8, 128>, fatc::fwd_tc128_kernel<0, 64>, fatc::fwd_tc128_kernel<0, 32>,
-                       fatc::fwd_tc128_kernel<3, 128, true>, fatc::fwd_tc128_kernel<0, 128, true>})
+                       fatc::fwd_tc128_kernel<8, 128>, fatc::fwd_tc128_kernel<0, 64>, fatc::fwd_tc128_kernel<0, 32>})
             SPT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, fatc::fw2::SMEM));
         SPT_CUDA(cudaFuncSetAttribute(fatc::fwd_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       fatc::fwt::SMEM));
@@ -3180,8 +3138,6 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
                  : bk128 == 8 || bk128 == 18 ? fatc::fwd_tc128_kernel<8, 128>
                  : bk128 == 12 ? fatc::fwd_tc128_kernel<2, 128>
                  : bk128 == 13 ? fatc::fwd_tc128_kernel<3, 128>
-                 : bk128 == 23 ? fatc::fwd_tc128_kernel<3, 128, true>
-                 : bk128 == 21 ? fatc::fwd_tc128_kernel<0, 128, true>
                  : bk128 == 16 ? fatc::fwd_tc128_kernel<6, 128>
                  : bk128 == 3 ? fatc::fwd_tc128_kernel<1, 128>
                               : fatc::fwd_tc128_kernel<0, 128>;  // 1, 2, 11: every exponential on MUFU

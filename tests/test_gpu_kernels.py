@@ -493,12 +493,12 @@ def test_embedding_rejects_bad_ids():
 
 @pytest.mark.parametrize("s,hq,hkv,packed,amp", [(1024, 4, 2, False, 1), (640, 4, 1, True, 1), (2048, 2, 1, False, 2.5),
                                                  (1536, 2, 2, True, 2.5), (384, 8, 2, False, 1)])
-@pytest.mark.parametrize("mode", [0, 2, 3, 8, 11, 21, 23])
+@pytest.mark.parametrize("mode", [0, 2, 3, 8, 11])
 def test_attention_fwd_other_blocks(s, hq, hkv, packed, amp, mode):
     """Forward variants against the float64 oracle (O rel-err < 1e-2, lse abs err < 2e-3): 0 the 64-key
     double-buffered kernel (default for packed sequences), 2 the 128-key MUFU-only kernel also on packed sequences,
     8 the 128-key kernel with the FMA-pipe exp2 for every 8th pair, 11 the 128-key MUFU-only kernel (the causal
-    default before every 3rd pair moved to the FMA pipe), 21 / 23 the early-exponential forms of 11 / 13.  The default choice is covered by every other
+    default before every 3rd pair moved to the FMA pipe).  The default choice is covered by every other
     attention test."""
     T = torch()
     L = _lib()
@@ -629,29 +629,3 @@ def test_attention_bwd_fused_cluster4(s, hq, hkv):
     two = to_np(outs[0][0])
     assert rel_err(g[:, hq:], two[:, hq:].astype(np.float64)) < 1e-2
 
-
-@pytest.mark.parametrize("s,hq,hkv,amp", [(2048, 4, 1, 1), (1280, 2, 2, 6), (4096, 8, 2, 2.5)])
-@pytest.mark.parametrize("pair", [(11, 21), (13, 23)])
-def test_attention_fwd_early_exps_bitwise(s, hq, hkv, amp, pair):
-    """The early-exponential forward (chunk 0 of each key block exponentiated against the running maximum while
-    the block maximum is formed, recomputed when a row's maximum jumps by more than the rescale threshold) is
-    bitwise equal to the plain form: amp scales the scores so that rescales do happen (amp 6)."""
-    T = torch()
-    L = _lib()
-    d = 128
-    qkv, _, _ = _attn_case(s, hq, hkv, d, False, s + d + 3, amp)
-    qkvd = bf16_dev(qkv)
-    outs = []
-    try:
-        for mode in pair:
-            o = T.empty(s, hq, d, dtype=T.bfloat16, device="cuda")
-            lse = T.empty(hq, s, device="cuda")
-            S.check(L.spt_tuning_set(b"attn_fwd_bk128", mode))
-            S.check(L.spt_attn_fwd(qkvd.data_ptr(), s, hq, hkv, d, None, 1.0 / math.sqrt(d), o.data_ptr(),
-                                   lse.data_ptr(), None))
-            T.cuda.synchronize()
-            outs.append((o.view(T.int16).cpu().numpy(), lse.cpu().numpy()))
-    finally:
-        S.check(L.spt_tuning_set(b"attn_fwd_bk128", 1))
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))

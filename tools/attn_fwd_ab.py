@@ -22,6 +22,9 @@ args = [a for a in sys.argv[2:] if not a.startswith("--") and a not in opts.valu
 rounds = int(opts.get("--rounds", rounds))
 key = opts.get("--key", key.decode()).encode()
 reset = int(opts.get("--reset", reset))
+for a_ in sys.argv[1:]:
+    if a_.startswith("--lib="):  # A/B against another build of the library (same switch values)
+        S.LIB_PATH = os.path.abspath(a_.split("=", 1)[1])
 L = S.lib()
 d = 128
 for shp in args:
