@@ -145,6 +145,10 @@ struct GemmTuning {
     int gemm_bn = env_int("SPT_GEMM_BN", 0);
     int epi_tstore = env_int("SPT_EPI_TSTORE", 2);
     int gemm_raster = env_int("SPT_GEMM_RASTER", 0);
+    // raster-0 group size override (0: the kernel default, 16 row blocks for 1-SM tiles and CTA pairs alike; the
+    // pairs' earlier 8 measured 6.0 vs 3.6 GB of HBM reads and 5.68 vs 5.52 ms on the logits GEMM, -0.3% per
+    // sustained L1 step: profiles/r2d_gemm_group.txt)
+    int gemm_group_m = env_int("SPT_GEMM_GROUP_M", 0);
 };
 static GemmTuning& tuning() {
     static GemmTuning t;
@@ -274,6 +278,7 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
             }
         }
     }
+    ep.group_m = tuning().gemm_group_m;
     if (pair) {
         if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
@@ -325,6 +330,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         auto& t = spt::tuning();
         if (n == "gemm_raster") {
             t.gemm_raster = value;
+            return;
+        }
+        if (n == "gemm_group_m") {
+            t.gemm_group_m = value;
             return;
         }
         if (n == "attn_dq_tmem") {

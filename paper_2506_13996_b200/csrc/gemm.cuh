@@ -49,6 +49,7 @@ struct EpiParams {
     // read once), 2 = row blocks fastest (A stays, B panels read once); hint_a / hint_b: TMA L2 policy of the
     // operand loads (0 none, 1 evict_first, 2 evict_last).
     int raster = 0;
+    int group_m = 0;  // raster 0: row blocks per group (0: the kernel's default, 16)
     int hint_a = 0, hint_b = 0;
     int tstore = 1;  // fp32 epilogues: 0 per-thread stores, 1 smem transpose + coalesced stores, 2 TMA store /
                      // reduce-add (1-SM kernel, EPI_F32)
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int num_n = (N + BN - 1) / BN;
     const int ntiles = num_m * num_n;
     const int nk = (K + GEMM_BK - 1) / GEMM_BK;
-    constexpr int GROUP_M = 16;
+    const int GROUP_M = ep.group_m > 0 ? ep.group_m : 16;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -555,7 +556,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int ntiles = num_m * num_n;
     const int nk = (K + GEMM_BK - 1) / GEMM_BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    constexpr int GROUP_M = 8;
+    // 16 cluster rows: the logits GEMM's x-tile group (16 x 256 rows x K=4096, 32 MB) stays in L2 while all of W_lm
+    // streams past it twice per loss tile instead of four times
+    const int GROUP_M = ep.group_m > 0 ? ep.group_m : 16;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {

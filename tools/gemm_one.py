@@ -1,6 +1,6 @@
 """One GEMM shape on the tcgen05 kernel (bf16 out, or fp32 accumulate with --f32) for ncu captures / quick timing.
 
-  python tools/gemm_one.py M N K a_mn b_mn [--f32] [--pair|--1sm] [--reps 5] [--raster R]  (R: gemm_raster mode)
+  python tools/gemm_one.py M N K a_mn b_mn [--f32] [--pair|--1sm] [--reps 5] [--raster R] [--group G]  (gemm_raster mode, raster-0 group size)
 e.g. the lm_head dgrad of one loss tile: python tools/gemm_one.py 8192 4096 128256 0 1"""
 import os
 import sys
@@ -10,8 +10,8 @@ import torch  # noqa: E402
 
 import paper_2506_13996_b200 as S  # noqa: E402
 
-opt_vals = {sys.argv[i + 1] for i, a in enumerate(sys.argv[:-1]) if a in ("--reps", "--raster")}
-pos = [int(a) for i, a in enumerate(sys.argv[1:], 1) if not a.startswith("--") and not (sys.argv[i - 1] in ("--reps", "--raster"))]
+opt_vals = {sys.argv[i + 1] for i, a in enumerate(sys.argv[:-1]) if a in ("--reps", "--raster", "--group")}
+pos = [int(a) for i, a in enumerate(sys.argv[1:], 1) if not a.startswith("--") and not (sys.argv[i - 1] in ("--reps", "--raster", "--group"))]
 M, N, K, amn, bmn = pos[:5]
 f32 = "--f32" in sys.argv
 reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 5
@@ -20,6 +20,8 @@ if "--pair" in sys.argv:
     L.spt_tuning_set(b"gemm_pair_mn", 1)
 if "--1sm" in sys.argv:
     L.spt_tuning_set(b"gemm_1sm", 1)
+if "--group" in sys.argv:
+    L.spt_tuning_set(b"gemm_group_m", int(sys.argv[sys.argv.index("--group") + 1]))
 if "--raster" in sys.argv:
     L.spt_tuning_set(b"gemm_raster", int(sys.argv[sys.argv.index("--raster") + 1]))
 g = torch.Generator(device="cuda").manual_seed(0)

@@ -1,0 +1,5 @@
+# raster-0 group size vs HBM bytes and time on the lm_head GEMM shapes (logits as bf16 out, dgrad, dW)
+run() { timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__cycles_elapsed.avg.per_second --clock-control none -k regex:gemm_tc -s 2 -c 1 --csv python tools/gemm_one.py "$@" --reps 1 2>/dev/null | grep -E "dram__|duration|cycles" | awk -F'","' -v a="$*" '{printf "%s | %s %s\n", a, $(NF-2), $(NF)}'; }
+for g in 4 8 16 32; do run 8192 128256 4096 0 0 --group $g; done
+for g in 4 8 16 32 64; do run 8192 4096 128256 0 1 --group $g; done
+for g in 4 8 16 32; do run 128256 4096 8192 1 1 --f32 --group $g; done
