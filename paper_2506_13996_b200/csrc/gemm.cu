@@ -149,6 +149,7 @@ struct GemmTuning {
     // pairs' earlier 8 measured 6.0 vs 3.6 GB of HBM reads and 5.68 vs 5.52 ms on the logits GEMM, -0.3% per
     // sustained L1 step: profiles/r2d_gemm_group.txt)
     int gemm_group_m = env_int("SPT_GEMM_GROUP_M", 0);
+    int gemm_colgroup = env_int("SPT_GEMM_COLGROUP", 8);
 };
 static GemmTuning& tuning() {
     static GemmTuning t;
@@ -262,7 +263,9 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
     // gemm_raster = 0 (default): grouped order and no hints everywhere; 1: order only, 2: hints only, 3: both.
     // Measured (profiles/r2b_gemm_raster.txt): 3 is 4.7% SLOWER per L1 step — the lm_head GEMMs read 40-50% MORE
     // from HBM with the resident-operand order than with the grouped one.
-    if (const int rm = tuning().gemm_raster; rm != 0) {  // bit 0: tile order, bit 1: L2 hints
+    if (tuning().gemm_raster >= 16) {
+        ep.raster = tuning().gemm_raster - 16;  // A/B: force tile order n on every GEMM
+    } else if (const int rm = tuning().gemm_raster; rm != 0) {  // bit 0: tile order, bit 1: L2 hints
         const double ba = 2.0 * M * K, bb = 2.0 * N * K, cap = 80.0 * (1 << 20);
         if (bb <= cap && bb <= ba) {
             if (rm & 1) ep.raster = 1;
@@ -279,6 +282,17 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
         }
     }
     ep.group_m = tuning().gemm_group_m;
+    // 1-SM GEMMs (the MN-major data / weight gradients) sweep groups of gemm_colgroup column blocks over all row
+    // blocks (raster 3): 8 x 256 columns at a time.  Measured on the lm_head backward GEMMs: dW 11.7 -> 9.1 GB and dX
+    // 10.5 -> 8.5 GB of HBM reads, and -3.7% per sustained L1 step over all 1-SM GEMMs (row groups of 16 before;
+    // column groups of 2 / 4 / 16: +1.4% / -2.4% / +0.8%; lm_head GEMMs only: -3.1%) — profiles/r2d_gemm_group.txt.
+    // gemm_colgroup = 0: row groups (raster 0); G + 1000: column groups on the lm_head (vocab-sized M or K) only.
+    if (const int cg = tuning().gemm_colgroup; cg > 0 && !pair && ep.raster == 0) {
+        if (cg < 1000 || std::max(M, K) >= 65536) {
+            ep.raster = 3;
+            if (ep.group_m <= 0) ep.group_m = cg % 1000;
+        }
+    }
     if (pair) {
         if (ep.tstore == 2 && kind != EPI_F32) ep.tstore = 1;
         if (bn == 128) dispatch_pair<128>(A, B, M, N, K, kind, ep, st);
@@ -334,6 +348,10 @@ extern "C" spt_status spt_tuning_set(const char* name, int32_t value) {
         }
         if (n == "gemm_group_m") {
             t.gemm_group_m = value;
+            return;
+        }
+        if (n == "gemm_colgroup") {
+            t.gemm_colgroup = value;
             return;
         }
         if (n == "attn_dq_tmem") {

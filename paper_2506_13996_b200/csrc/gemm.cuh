@@ -46,7 +46,8 @@ struct EpiParams {
     float* label_logit = nullptr;     // EPI_EXP_STATS: [M] fp32 logit of the row's label
     // Tile order and L2 hints (gemm() picks them per shape, see gemm.cu raster rule): raster 0 = groups of GROUP_M
     // row blocks sweeping all column blocks, 1 = column blocks fastest (the whole B stays in L2, every A panel is
-    // read once), 2 = row blocks fastest (A stays, B panels read once); hint_a / hint_b: TMA L2 policy of the
+    // read once), 2 = row blocks fastest (A stays, B panels read once), 3 = groups of group_m COLUMN blocks sweeping
+    // all row blocks; hint_a / hint_b: TMA L2 policy of the
     // operand loads (0 none, 1 evict_first, 2 evict_last).
     int raster = 0;
     int group_m = 0;  // raster 0: row blocks per group (0: the kernel's default, 16)
@@ -358,6 +359,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mb = t - nb * num_m;
             return;
         }
+        if (ep.raster == 3) {  // groups of GROUP_M column blocks sweeping all row blocks (B slice stays in L2)
+            const int per_group_n = GROUP_M * num_m;
+            const int gid = t / per_group_n;
+            const int first_n = gid * GROUP_M;
+            const int gsz = min(num_n - first_n, GROUP_M);
+            const int in = t % per_group_n;
+            nb = first_n + in % gsz;
+            mb = in / gsz;
+            return;
+        }
         const int per_group = GROUP_M * num_n;
         const int gid = t / per_group;
         const int first_m = gid * GROUP_M;
@@ -597,6 +608,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (ep.raster == 2) {
             nb = t / num_m;
             mb = t - nb * num_m;
+            return;
+        }
+        if (ep.raster == 3) {  // groups of GROUP_M column blocks sweeping all row blocks (B slice stays in L2)
+            const int per_group_n = GROUP_M * num_m;
+            const int gid = t / per_group_n;
+            const int first_n = gid * GROUP_M;
+            const int gsz = min(num_n - first_n, GROUP_M);
+            const int in = t % per_group_n;
+            nb = first_n + in % gsz;
+            mb = in / gsz;
             return;
         }
         const int per_group = GROUP_M * num_n;
