@@ -130,3 +130,10 @@ python tools/step_ab.py attn_kv_group=0,1 --rounds 3 --group 12 > gpurun_out/r2d
 # ---- r2d20
 python tools/config_ab.py mlp_tiles=0,1,4 --rounds 3 --group 12 > gpurun_out/r2d20_a.txt 2>&1; tail -1 gpurun_out/r2d20_a.txt
 python tools/config_ab.py loss_tile=0,16384,4096 --rounds 3 --group 12 > gpurun_out/r2d20_b.txt 2>&1; tail -1 gpurun_out/r2d20_b.txt
+
+# ---- r2e2: MLP-shaped pair GEMMs, row groups vs column groups (standalone DRAM bytes; defaults kept)
+run() { timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__cycles_elapsed.avg.per_second --clock-control none -k regex:gemm_tc -s 2 -c 1 --csv python tools/gemm_one.py "$@" --reps 1 2>/dev/null | grep -E "dram__|duration|cycles" | awk -F'","' -v a="$*" '{printf "%s | %s %s\n", a, $(NF-2), $(NF)}'; }
+for g in 4 8 16 32; do run 16384 28672 4096 0 0 --group $g; done
+for g in 4 8 16 32; do run 16384 28672 4096 0 0 --raster 19 --group $g; done
+for g in 8 16 32; do run 16384 4096 14336 0 0 --group $g; done
+for g in 4 8 16; do run 16384 4096 14336 0 0 --raster 19 --group $g; done
