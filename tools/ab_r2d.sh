@@ -137,3 +137,7 @@ for g in 4 8 16 32; do run 16384 28672 4096 0 0 --group $g; done
 for g in 4 8 16 32; do run 16384 28672 4096 0 0 --raster 19 --group $g; done
 for g in 8 16 32; do run 16384 4096 14336 0 0 --group $g; done
 for g in 4 8 16; do run 16384 4096 14336 0 0 --raster 19 --group $g; done
+
+# ---- r2e3: forward P hand-off variants as separate builds (SPT_EXTRA_DEFS=SPT_FWD2_NPART=2 / a deferred-arrive
+# form, since removed), interleaved in one process with tools/lib_ab_fwd.py: all within +-0.5% (bitwise equal)
+for i in 1 2; do timeout 900 python tools/lib_ab_fwd.py paper_2506_13996_b200/libsptrain_b200.so ab_var/libsptrain_b200.so ab_var2/libsptrain_b200.so ab_var3/libsptrain_b200.so --rounds 5; done
