@@ -507,7 +507,6 @@ constexpr int BKB = 128;
 #define SPT_FWD2_NPART 4
 #endif
 constexpr int NPART = SPT_FWD2_NPART;  // P hand-off parts per block (PV MMAs start per part)
-
 constexpr int Q_BYTES = BQ * D * 2;    // 32 KiB per tile
 constexpr int KV_BYTES = BKB * D * 2;  // 32 KiB per K or V block (two 16 KiB regions)
 #ifndef SPT_FWD2_NSL
