@@ -49,6 +49,42 @@ def test_gemm_majors(a_mn, b_mn, f32, acc, M, N, K):
     assert err < (1e-5 if f32 else 5e-3), err
 
 
+@pytest.mark.parametrize("a_mn,b_mn,f32,acc", [(0, 1, 0, 0), (1, 1, 1, 1), (0, 0, 0, 0)])
+def test_gemm_tile_orders_bitwise(a_mn, b_mn, f32, acc):
+    """Tile order changes which CTA computes a tile and when, never the arithmetic inside it: row groups / column
+    groups of any size (partial last groups: 10 column blocks, 8 row blocks) give bitwise equal results, equal to
+    torch within the usual tolerance.  Covers the default column groups of 8 (1-SM) and row groups of 16 (pairs)."""
+    T = torch()
+    L = _lib()
+    M, N, K = 1000, 9 * 256 + 64, 320
+    g = T.Generator(device="cuda").manual_seed(7)
+    A = T.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = T.randn(N, K, device="cuda", generator=g).bfloat16()
+    Ast = A.t().contiguous() if a_mn else A
+    Bst = B.t().contiguous() if b_mn else B
+    base = T.randn(M, N, device="cuda", generator=g)
+    outs = []
+    try:
+        for colgroup, group_m in ((8, 0), (0, 0), (3, 0), (0, 5), (8, 3), (1008, 0)):
+            S.check(L.spt_tuning_set(b"gemm_colgroup", colgroup))
+            S.check(L.spt_tuning_set(b"gemm_group_m", group_m))
+            if f32:
+                C = base.clone() if acc else T.empty(M, N, device="cuda")
+            else:
+                C = T.empty(M, N, device="cuda", dtype=T.bfloat16)
+            S.check(L.spt_gemm_bf16(Ast.data_ptr(), Ast.shape[1], a_mn, Bst.data_ptr(), Bst.shape[1], b_mn, C.data_ptr(),
+                                    N, f32, acc, None, 0, M, N, K, 1.0, None))
+            T.cuda.synchronize()
+            outs.append(C.clone())
+    finally:
+        S.check(L.spt_tuning_set(b"gemm_colgroup", 8))
+        S.check(L.spt_tuning_set(b"gemm_group_m", 0))
+    for o in outs[1:]:
+        assert T.equal(o, outs[0])
+    ref = A.float() @ B.float().t() + (base if f32 and acc else 0)
+    assert rel_err(to_np(outs[0]), to_np(ref)) < (1e-5 if f32 else 5e-3)
+
+
 def test_gemm_residual_alpha():
     T = torch()
     M, N, K = 256, 320, 192
