@@ -145,9 +145,8 @@ struct GemmTuning {
     int gemm_bn = env_int("SPT_GEMM_BN", 0);
     int epi_tstore = env_int("SPT_EPI_TSTORE", 2);
     int gemm_raster = env_int("SPT_GEMM_RASTER", 0);
-    // raster-0 group size override (0: the kernel default, 16 row blocks for 1-SM tiles and CTA pairs alike; the
-    // pairs' earlier 8 measured 6.0 vs 3.6 GB of HBM reads and 5.68 vs 5.52 ms on the logits GEMM, -0.3% per
-    // sustained L1 step: profiles/r2d_gemm_group.txt)
+    // tile-group size override (0: the defaults — row groups of 16 cluster rows for CTA pairs, whose earlier 8 read
+    // 6.0 vs 3.6 GB of HBM on the logits GEMM, and column groups of gemm_colgroup for 1-SM tiles; see gemm())
     int gemm_group_m = env_int("SPT_GEMM_GROUP_M", 0);
     int gemm_colgroup = env_int("SPT_GEMM_COLGROUP", 8);
 };
@@ -255,12 +254,13 @@ void gemm(const GemmOperand& A, const GemmOperand& B, int64_t M, int64_t N, int6
             if (eff(128) >= eff(256) + 0.06) bn = 128;
         }
     }
-    // Tile order by operand footprint (gemm_raster = 1, default): when one operand fits in L2 with room to spare
+    // Tile order by operand footprint (gemm_raster = 1, opt-in): when one operand fits in L2 with room to spare
     // (<= 80 MB of the 126 MB), sweep the tiles so that it is re-read from L2 and the other operand streams from
     // HBM exactly once, and tell the L2 so (evict_last on the resident operand, evict_first on the streamed one).
     // The lm_head weight gradient (B = the x tile, 67 MB; A = dlogits^T streamed) and the logits GEMM (A = the
     // x tile; B = W_lm streamed) are the cases that matter; with neither operand resident the grouped order stays.
-    // gemm_raster = 0 (default): grouped order and no hints everywhere; 1: order only, 2: hints only, 3: both.
+    // gemm_raster = 0 (default): grouped order and no hints everywhere; 1: order only, 2: hints only, 3: both;
+    // 16 + n: tile order n forced on every GEMM (A/B only).
     // Measured (profiles/r2b_gemm_raster.txt): 3 is 4.7% SLOWER per L1 step — the lm_head GEMMs read 40-50% MORE
     // from HBM with the resident-operand order than with the grouped one.
     if (tuning().gemm_raster >= 16) {
