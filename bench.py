@@ -248,12 +248,15 @@ def make_group(S, args, rank, world, local_rank):
 
 def est_max_seq(S, shp, mem, n_loc, world):
     """max_seqlen_solver on this engine's memory model, calibrated from this run's ledger: the
-    fixed bytes (weights, grads, logits tile workspace) are modelled exactly, the rest of the measured peak
-    is charged per local token."""
+    fixed bytes (weights, grads, logits tile and TiledMLP tile workspaces) are modelled exactly, the rest of the
+    measured peak is charged per local token."""
     led = mem["ledger"]["device"]
     tags = led["tags"]
-    fixed = tags["weights"]["peak"] + tags["grads"]["peak"] + tags["logits"]["peak"]
-    per_tok = max(1.0, (led["peak_bytes"] - fixed) / n_loc)
+    # the TiledMLP workspace is sized by the MLP tile (fixed by its 2 GiB rule once N exceeds a tile), not by N
+    mlp_ws = S.lib().spt_mlp_workspace(mem["mlp_tile"], shp.intermediate)
+    fixed = tags["weights"]["peak"] + tags["grads"]["peak"] + tags["logits"]["peak"] + mlp_ws
+    # + the caller's own device copy of the step inputs (x bf16 and int64 labels), which the ledger does not see
+    per_tok = max(1.0, (led["peak_bytes"] - fixed) / n_loc) + 2 * shp.hidden + 8
     total = mem["ledger"].get("cuda_mem_total_bytes", 0)
     if not total:
         return None, per_tok
@@ -457,8 +460,8 @@ def run_ours(args, rank, world, local_rank):
                                                 ("device" if args.layers > 1 else "none (single layer)"))},
         "peak_hbm_bytes": peak_b, "peak_hbm_bytes_per_token": peak_b / n_loc,
         "est_max_seq_per_gpu": est,
-        "est_max_seq_method": (f"spt_max_seqlen_solver: weights + grads + logits tile exact, "
-                               f"{per_tok:.0f} B per local token from this run's ledger, HBM total - 3 GiB"),
+        "est_max_seq_method": (f"spt_max_seqlen_solver: weights + grads + logits / MLP tile workspaces exact, "
+                               f"{per_tok:.0f} B per local token (this run's ledger + the caller's input copy), HBM total - 3 GiB"),
         "loss": loss, "valid_tokens": cnt,
         "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(x.numel() * 2 + lab.numel() * 8) * world, "d2h_bytes_per_step": 32 * world},

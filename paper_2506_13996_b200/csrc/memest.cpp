@@ -11,6 +11,17 @@
 namespace spt {
 size_t flce_workspace(int64_t tile_n, int64_t V);  // tiled.cu
 int64_t flce_default_tile(int64_t n_loc, int64_t V);
+size_t mlp_workspace(int64_t tile_n, int64_t I);  // tiled.cu
+
+// The engine's default TiledMLP tile (engine.cu: fewest tiles whose tile * I * 8 bytes of intermediates fit 2 GiB,
+// split evenly) and the workspace it sizes: fixed once the local sequence exceeds one tile.
+static double mlp_ws_bytes(const spt_memest_engine& e, double nl) {
+    if (nl < 1) return 0.0;
+    const int64_t n = (int64_t)nl, I = e.intermediate;
+    const int64_t tmax = std::max<int64_t>(128, (int64_t)((2ll << 30) / (I * 8)) / 128 * 128);
+    const int64_t mt = std::max<int64_t>(1, (n + tmax - 1) / tmax);
+    return (double)mlp_workspace((n + mt - 1) / mt, I);
+}
 namespace {
 constexpr double GiB = 1024.0 * 1024.0 * 1024.0;
 
@@ -66,7 +77,7 @@ double spt_memest_4d_mask_bytes(double seqlen, double bytes) { return seqlen * s
 double spt_memest_position_ids_bytes(double seqlen, double bytes) { return seqlen * bytes; }
 
 // This engine's per-rank device bytes at sequence length s (exact for its ledger, tools/max_seq.py measures
-// the same quantity): weights + grads + logits tile workspace + per-token activations.
+// the same quantity): weights + grads + logits and TiledMLP tile workspaces + per-token activations.
 static double engine_device_bytes(const spt_memest_engine& e, double s) {
     const double nl = s / std::max(1, e.sp);
     const double qkv = (double)(e.q_heads + 2 * e.kv_heads) * e.head_dim, qd = (double)e.q_heads * e.head_dim;
@@ -76,7 +87,8 @@ static double engine_device_bytes(const spt_memest_engine& e, double s) {
     // the engine's loss tile and FLCE workspace (tiled.cu), exactly
     const double logits_ws = nl >= 1 ? (double)flce_workspace(flce_default_tile((int64_t)nl, e.vocab), e.vocab) : 0.0;
     const double ckpt = e.n_layers > 1 || e.ckpt_offload ? (e.ckpt_offload ? 0.0 : e.n_layers * nl * e.hidden * 2.0) : 0.0;
-    return weights + grads + logits_ws + ckpt + e.act_bytes_per_token * nl + e.act_bytes_per_seq_token * s;
+    return weights + grads + logits_ws + mlp_ws_bytes(e, nl) + ckpt + e.act_bytes_per_token * nl +
+           e.act_bytes_per_seq_token * s;
 }
 
 spt_status spt_memest_engine_device_bytes(const spt_memest_engine* e, double seqlen, double* out) {
