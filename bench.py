@@ -162,12 +162,14 @@ def run_reference(args, rank, world):
                          "sample": cpu_sample_desc(n, args.workload, seq)},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    if args.workload == "l1" and args.cpu_reduced_n:
-        # the L shape at a reduced N, measured whole (attention included), one timed step
-        nr = args.cpu_reduced_n
-        t, _ = cpu_layer_sample(nr, workload="l1")  # weights / batch set-up happens before the timer starts
-        line["cpu_reduced_n"] = {"seq_len": nr, "value": nr / t, "unit": "tokens/s", "ms_per_step": 1000.0 * t,
-                                 "note": "whole L-shape layer step at this N (1 timed step), not the L1 workload"}
+    if args.workload == "l1" and args.cpu_reduced_n not in ("0", "", None):
+        # the L shape at reduced N (2048 and 4096), measured whole (attention included), one timed
+        # step each
+        line["cpu_reduced_n"] = []
+        for nr in (int(v) for v in str(args.cpu_reduced_n).split(",") if int(v) > 0):
+            t, _ = cpu_layer_sample(nr, workload="l1")  # weights / batch set-up happens before the timer starts
+            line["cpu_reduced_n"].append({"seq_len": nr, "value": nr / t, "unit": "tokens/s", "ms_per_step": 1000.0 * t,
+                                          "note": "whole L-shape layer step at this N (1 timed step), not the L1 workload"})
     print(json.dumps(line), flush=True)
 
 
@@ -504,8 +506,8 @@ def main():
     ap.add_argument("--loss-tile", type=int, default=0, help="tokens per tiled-logits/CE tile (0: the engine's rule)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=0, help="CPU sample size (0: 512 for l1, 8192 for tiny)")
-    ap.add_argument("--cpu-reduced-n", type=int, default=2048,
-                    help="--impl reference, l1: also time one whole L-shape step at this N (0: skip)")
+    ap.add_argument("--cpu-reduced-n", default="2048,4096",
+                    help="--impl reference, l1: also time one whole L-shape step at each of these N (0: skip)")
     ap.add_argument("--layers", type=int, default=1,
                     help="decoder layers (> 1: per-layer activation checkpointing; not the BASELINE config)")
     ap.add_argument("--offload", action="store_true", help="activation checkpoints in pinned host memory")
