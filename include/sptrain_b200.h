@@ -38,8 +38,10 @@ typedef enum {
 } spt_status;
 
 const char* spt_last_error(void);
-/* Run-time tuning switches for A/B experiments (gemm_1sm, gemm_pair_mn, gemm_bn, epi_tstore); the defaults
- * are the measured-best configuration. */
+/* Run-time tuning switches for A/B experiments (GEMM: gemm_1sm, gemm_pair_mn, gemm_bn, epi_tstore, gemm_raster,
+ * gemm_group_m, gemm_colgroup; attention: attn_fwd_bk128, attn_fwd_hybrid, attn_fwd_tmem, attn_kv_group,
+ * attn_dkdv_kt, attn_dkdv_pair, attn_dq_tmem, attn_bwd; engine: mlp_bwd_group, rope_fused).  The defaults are the
+ * measured-best configuration (DESIGN.md §4 lists every switch with its evidence); unknown names are an error. */
 spt_status spt_tuning_set(const char* name, int32_t value);
 const char* spt_version(void);
 
