@@ -72,7 +72,7 @@ def cpu_sample_tokens(args):
     return args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 8192)
 
 
-def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: int = 0):
+def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: int = 0, sp: int = 1):
     """One CPU step of the reference algorithm (oracle/sptrain_oracle.py, float32) on an n-token sample of the
     workload; returns (seconds, loss).
 
@@ -105,7 +105,7 @@ def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: in
             _CPU_CACHE[akey] = (qkv, rows)
         attn = _CPU_CACHE[akey]
     t0 = time.perf_counter()
-    res = O.layer_step(p, cfg, x.astype(np.float32), lab, None, P=1, dtype=np.float32)
+    res = O.layer_step(p, cfg, x.astype(np.float32), lab, None, P=sp, dtype=np.float32)
     if attn is not None:
         (q, k, v, do), rows = attn
         g = cfg.q_heads // cfg.kv_heads
@@ -162,6 +162,14 @@ def run_reference(args, rank, world):
                          "sample": cpu_sample_desc(n, args.workload, seq)},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.workload == "tiny":
+        # SURVEY.md §8(d) / BASELINE configs[0]: the same step as P in-process SP ranks (the oracle's SPMD form,
+        # reshard, kv replication at P = 4 / 8, fixed-order all-reduces), one timed step each
+        line["cpu_sp"] = []
+        for P in (2, 4, 8):
+            t, loss = cpu_layer_sample(n, workload="tiny", sp=P)
+            line["cpu_sp"].append({"sp_degree": P, "value": n / t, "unit": "tokens/s", "ms_per_step": 1000.0 * t,
+                                   "loss": loss})
     if args.workload == "l1" and args.cpu_reduced_n not in ("0", "", None):
         # the L shape at reduced N (2048 and 4096), measured whole (attention included), one timed
         # step each
