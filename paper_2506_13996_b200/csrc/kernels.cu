@@ -38,7 +38,8 @@ __device__ __forceinline__ void unpack8(const uint4 w, float* v) {
 }
 __device__ __forceinline__ uint4 ld16(const bf16* p) { return *reinterpret_cast<const uint4*>(p); }
 
-// REGS: register cap (48 for h <= 5120: two 640-thread CTAs per SM; 64 for up to 1024 threads)
+// REGS: register cap (32 for h <= 5120, no spills: four 512-thread / three 640-thread CTAs per SM, 107 vs 124 us at
+// 48 registers for the L1 shape, tools/rms_bench.py; 64 for up to 1024 threads)
 template <int REGS>
 __global__ void __maxnreg__(REGS) rmsnorm_fwd_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, bf16* __restrict__ y,
                                    float* __restrict__ rstd, int64_t n, int h, float eps) {
@@ -152,7 +153,7 @@ void rmsnorm_fwd(const void* x, const void* gamma, void* y, float* rstd, int64_t
     if (n == 0) return;
     const int th = rms_threads(h);
     if (th <= 640)
-        rmsnorm_fwd_kernel<48><<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd,
+        rmsnorm_fwd_kernel<32><<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd,
                                                                  n, (int)h, eps);
     else
         rmsnorm_fwd_kernel<64><<<grid_for(n, 1, 4), th, 0, st>>>((const bf16*)x, (const bf16*)gamma, (bf16*)y, rstd,
