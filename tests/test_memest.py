@@ -77,3 +77,16 @@ def test_engine_estimate_matches_measured_ledger():
     for N in (8192, 16384):
         est = S.memest_engine_bytes(cfg, N) + off
         assert abs(est - ledger(N, 1)) / ledger(N, 1) < 1e-3, N
+
+
+def test_engine_model_fixed_workspaces():
+    """The engine model's sequence-independent terms: weights + grads at s = 0; above that the logits tile and
+    TiledMLP tile workspaces (the engine's own tile rules: 4 GiB of logits, 2 GiB of MLP intermediates) and the
+    per-token activations.  Once the local sequence exceeds one MLP tile the MLP workspace stops growing."""
+    shp = S.LLAMA8B
+    cfg = S.memest_engine(shp)  # no per-token activations: only the fixed and tile terms
+    L = S.lib()
+    base = S.memest_engine_bytes(cfg, 0)
+    for n, mlp_tile, loss_tile in ((8192, 8192, 8192), (32768, 16384, 8192), (65536, 16384, 8192)):
+        want = L.spt_flce_workspace(loss_tile, shp.vocab) + L.spt_mlp_workspace(mlp_tile, shp.intermediate)
+        assert S.memest_engine_bytes(cfg, n) - base == want, n
