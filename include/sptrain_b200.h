@@ -275,6 +275,27 @@ spt_status spt_seq_to_head(spt_comm* comm, const spt_head_shard_plan* plan, int3
 spt_status spt_head_to_seq(spt_comm* comm, const spt_head_shard_plan* plan, int32_t kind, const void* const* x,
                            int64_t s_loc, int32_t head_dim, void* const* out, void* scratch, void* stream);
 
+/* SPEC.md:333-341 ulysses_attention as one collective op: seq_to_head -> tcgen05 attention on this rank's heads over
+ * the whole sequence (s = s_loc * P; causal, or block-causal from seg = run starts of the FULL sequence, identical
+ * on every rank) -> head_to_seq.  Arrays hold one pointer per LOCAL rank (loopback: every virtual rank's):
+ *   qkv [s_loc][Hq + 2 Hkv][d] in, out [s_loc][Hq][d] out;
+ *   qkv_head [s][q_loc + 2 kv_loc][d], o_head [s][q_loc][d] (peer mode: spt_comm_alloc) and lse [q_loc][s] fp32 are
+ *   filled for the backward, which the caller keeps them for.
+ * scratch: NCCL staging of spt_reshard_scratch_bytes(plan, 0, s_loc, d) bytes, else NULL.  Errors are those of the
+ * three ops it composes. */
+spt_status spt_ulysses_attention_fwd(spt_comm* comm, const spt_head_shard_plan* plan, const void* const* qkv,
+                                     int64_t s_loc, int32_t head_dim, const int32_t* seg, float scale,
+                                     void* const* qkv_head, void* const* o_head, float* const* lse, void* const* out,
+                                     void* scratch, void* stream);
+/* Backward: dout [s_loc][Hq][d] -> dqkv [s_loc][Hq + 2 Hkv][d] (replicas of a kv head summed in fp32, rank order,
+ * SPEC.md:326); do_head [s][q_loc][d] and dqkv_head [s][q_loc + 2 kv_loc][d] head-side buffers (peer mode:
+ * spt_comm_alloc), ws one spt_attn_bwd_workspace(s, q_loc, kv_loc, d) buffer per local rank. */
+spt_status spt_ulysses_attention_bwd(spt_comm* comm, const spt_head_shard_plan* plan, const void* const* qkv_head,
+                                     const void* const* o_head, const float* const* lse, const void* const* dout,
+                                     int64_t s_loc, int32_t head_dim, const int32_t* seg, float scale,
+                                     void* const* do_head, void* const* dqkv_head, void* const* ws,
+                                     void* const* dqkv, void* scratch, void* stream);
+
 /* ================================= layer step engine ================================= */
 
 /* ModelConfig for one layer + lm_head; head_dim explicit. */

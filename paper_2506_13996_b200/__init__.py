@@ -141,6 +141,11 @@ SIGNATURES = {
     "spt_reshard_scratch_bytes": (SZ, [C.POINTER(HeadShardPlan), I32, I64, I32]),
     "spt_seq_to_head": (I32, [P, C.POINTER(HeadShardPlan), I32, C.POINTER(P), I64, I32, C.POINTER(P), P, P]),
     "spt_head_to_seq": (I32, [P, C.POINTER(HeadShardPlan), I32, C.POINTER(P), I64, I32, C.POINTER(P), P, P]),
+    "spt_ulysses_attention_fwd": (I32, [P, C.POINTER(HeadShardPlan), C.POINTER(P), I64, I32, P, F32, C.POINTER(P),
+                                        C.POINTER(P), C.POINTER(P), C.POINTER(P), P, P]),
+    "spt_ulysses_attention_bwd": (I32, [P, C.POINTER(HeadShardPlan), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                        C.POINTER(P), I64, I32, P, F32, C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                        C.POINTER(P), P, P]),
     "spt_comm_stats_json": (I32, [P, C.c_char_p, SZ]),
     "spt_layer_create": (I32, [C.POINTER(LayerConfig), P, C.POINTER(P)]),
     "spt_layer_destroy": (I32, [P]),
@@ -464,6 +469,22 @@ class ProcessGroup:
         """SPEC.md:317-326 (K2 with the all-to-all fused; kind 1 sums kv replicas in rank order)"""
         check(lib().spt_head_to_seq(self.handle, C.byref(plan), kind, self._ptrs(x), s_loc, head_dim, self._ptrs(out),
                                     ptr(scratch), ptr(stream)))
+
+    def ulysses_attention_fwd(self, plan, qkv, s_loc: int, head_dim: int, seg, scale: float, qkv_head, o_head, lse,
+                              out, scratch=None, stream=None):
+        """SPEC.md:333-341 ulysses_attention: seq_to_head -> tcgen05 attention -> head_to_seq (one pointer per
+        local rank in every list; qkv_head / o_head / lse are kept by the caller for the backward)."""
+        check(lib().spt_ulysses_attention_fwd(self.handle, C.byref(plan), self._ptrs(qkv), s_loc, head_dim, ptr(seg),
+                                              scale, self._ptrs(qkv_head), self._ptrs(o_head), self._ptrs(lse),
+                                              self._ptrs(out), ptr(scratch), ptr(stream)))
+
+    def ulysses_attention_bwd(self, plan, qkv_head, o_head, lse, dout, s_loc: int, head_dim: int, seg, scale: float,
+                              do_head, dqkv_head, ws, dqkv, scratch=None, stream=None):
+        """The mirrored backward: dout [s_loc][Hq][d] -> dqkv [s_loc][Hq + 2 Hkv][d] (kv replicas summed in rank order)."""
+        check(lib().spt_ulysses_attention_bwd(self.handle, C.byref(plan), self._ptrs(qkv_head), self._ptrs(o_head),
+                                              self._ptrs(lse), self._ptrs(dout), s_loc, head_dim, ptr(seg), scale,
+                                              self._ptrs(do_head), self._ptrs(dqkv_head), self._ptrs(ws),
+                                              self._ptrs(dqkv), ptr(scratch), ptr(stream)))
 
     @classmethod
     def loopback_group(cls, world_size: int, device: int = 0) -> "ProcessGroup":

@@ -52,6 +52,11 @@ Dims dims_of(const spt_head_shard_plan& pl, int kind) {
     return {pl.q_heads, pl.q_heads_per_rank};
 }
 
+// Rethrow a nested C-ABI call's failure with its own status and message.
+void ck(spt_status st) {
+    if (st != SPT_OK) SPT_THROW(st, spt_last_error());
+}
+
 void check_plan(spt_comm* comm, const spt_head_shard_plan* plan, int kind, int head_dim) {
     SPT_CHECK(comm && plan, SPT_ERR_CONFIG, "null comm / plan");
     SPT_CHECK(kind == 0 || kind == 1, SPT_ERR_CONFIG, "kind must be 0 (q|k|v) or 1 (q-shaped)");
@@ -116,6 +121,43 @@ spt_status spt_head_to_seq(spt_comm* comm, const spt_head_shard_plan* plan, int3
                               reshard_unpack(t, s_loc, dm.heads_loc, head_dim, P, dm.heads_full, m.map, m.max_src,
                                              out[r], st);
                           });
+    });
+}
+
+// SPEC.md:333-341 ulysses_attention over a group: seq_to_head (K1 + all-to-all) -> the tcgen05 inner attention on
+// each rank's heads over the whole sequence -> head_to_seq (K2 + all-to-all), and the mirrored backward.  The same
+// sequence the layer engine runs inside its step, as one op for a host that composes its own layer.
+spt_status spt_ulysses_attention_fwd(spt_comm* comm, const spt_head_shard_plan* plan, const void* const* qkv,
+                                     int64_t s_loc, int32_t head_dim, const int32_t* seg, float scale,
+                                     void* const* qkv_head, void* const* o_head, float* const* lse, void* const* out,
+                                     void* scratch, void* stream) {
+    return capi_guard([&] {
+        check_plan(comm, plan, 0, head_dim);
+        SPT_CHECK(qkv && qkv_head && o_head && lse && out, SPT_ERR_CONFIG, "ulysses_attention_fwd: null buffer array");
+        const int64_t s = s_loc * comm->nranks;
+        ck(spt_seq_to_head(comm, plan, 0, qkv, s_loc, head_dim, qkv_head, scratch, stream));
+        for (int r = 0; r < comm->local_ranks(); ++r)
+            ck(spt_attn_fwd(qkv_head[r], s, plan->q_heads_per_rank, plan->kv_heads_per_rank, head_dim, seg, scale,
+                            o_head[r], lse[r], stream));
+        ck(spt_head_to_seq(comm, plan, 0, o_head, s_loc, head_dim, out, scratch, stream));
+    });
+}
+
+spt_status spt_ulysses_attention_bwd(spt_comm* comm, const spt_head_shard_plan* plan, const void* const* qkv_head,
+                                     const void* const* o_head, const float* const* lse, const void* const* dout,
+                                     int64_t s_loc, int32_t head_dim, const int32_t* seg, float scale,
+                                     void* const* do_head, void* const* dqkv_head, void* const* ws,
+                                     void* const* dqkv, void* scratch, void* stream) {
+    return capi_guard([&] {
+        check_plan(comm, plan, 1, head_dim);
+        SPT_CHECK(qkv_head && o_head && lse && dout && do_head && dqkv_head && ws && dqkv, SPT_ERR_CONFIG,
+                  "ulysses_attention_bwd: null buffer array");
+        const int64_t s = s_loc * comm->nranks;
+        ck(spt_seq_to_head(comm, plan, 1, dout, s_loc, head_dim, do_head, scratch, stream));
+        for (int r = 0; r < comm->local_ranks(); ++r)
+            ck(spt_attn_bwd(qkv_head[r], o_head[r], lse[r], do_head[r], s, plan->q_heads_per_rank,
+                            plan->kv_heads_per_rank, head_dim, seg, scale, dqkv_head[r], ws[r], stream));
+        ck(spt_head_to_seq(comm, plan, 1, dqkv_head, s_loc, head_dim, dqkv, scratch, stream));
     });
 }
 
