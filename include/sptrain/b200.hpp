@@ -165,6 +165,42 @@ public:
     }
     spt_comm* handle() const { return c_; }
 
+    // Collectives and reshards of SPEC.md:145-163 / :307-341 on caller-owned device buffers: one pointer per LOCAL
+    // rank (loopback: every virtual rank's; peer mode: buffers from spt_comm_alloc).  `stream` is a cudaStream_t.
+    void all_reduce_f32(const std::vector<void*>& bufs, int64_t n, void* stream = nullptr) {
+        check(spt_all_reduce_f32(c_, bufs.data(), n, stream));
+    }
+    void all_to_all(const std::vector<const void*>& send, const std::vector<void*>& recv, size_t bytes_per_peer,
+                    void* stream = nullptr) {
+        check(spt_all_to_all(c_, send.data(), recv.data(), bytes_per_peer, stream));
+    }
+    void seq_to_head(const HeadShardPlan& plan, int kind, const std::vector<const void*>& x, int64_t s_loc,
+                     int head_dim, const std::vector<void*>& out, void* scratch = nullptr, void* stream = nullptr) {
+        check(spt_seq_to_head(c_, &plan, kind, x.data(), s_loc, head_dim, out.data(), scratch, stream));
+    }
+    void head_to_seq(const HeadShardPlan& plan, int kind, const std::vector<const void*>& x, int64_t s_loc,
+                     int head_dim, const std::vector<void*>& out, void* scratch = nullptr, void* stream = nullptr) {
+        check(spt_head_to_seq(c_, &plan, kind, x.data(), s_loc, head_dim, out.data(), scratch, stream));
+    }
+    // ulysses_attention: seq_to_head -> tcgen05 attention -> head_to_seq, and its backward
+    void ulysses_attention_fwd(const HeadShardPlan& plan, const std::vector<const void*>& qkv, int64_t s_loc,
+                               int head_dim, const int32_t* seg, float scale, const std::vector<void*>& qkv_head,
+                               const std::vector<void*>& o_head, const std::vector<float*>& lse,
+                               const std::vector<void*>& out, void* scratch = nullptr, void* stream = nullptr) {
+        check(spt_ulysses_attention_fwd(c_, &plan, qkv.data(), s_loc, head_dim, seg, scale, qkv_head.data(),
+                                        o_head.data(), lse.data(), out.data(), scratch, stream));
+    }
+    void ulysses_attention_bwd(const HeadShardPlan& plan, const std::vector<const void*>& qkv_head,
+                               const std::vector<const void*>& o_head, const std::vector<const float*>& lse,
+                               const std::vector<const void*>& dout, int64_t s_loc, int head_dim, const int32_t* seg,
+                               float scale, const std::vector<void*>& do_head, const std::vector<void*>& dqkv_head,
+                               const std::vector<void*>& ws, const std::vector<void*>& dqkv, void* scratch = nullptr,
+                               void* stream = nullptr) {
+        check(spt_ulysses_attention_bwd(c_, &plan, qkv_head.data(), o_head.data(), lse.data(), dout.data(), s_loc,
+                                        head_dim, seg, scale, do_head.data(), dqkv_head.data(), ws.data(),
+                                        dqkv.data(), scratch, stream));
+    }
+
 private:
     explicit ProcessGroup(spt_comm* c) : c_(c) {}
     spt_comm* c_ = nullptr;
