@@ -3093,6 +3093,7 @@ static int fwd_bk128(int64_t s, int hq, const int32_t* seg) {
     const int v = g_attn_fwd_bk128;
     if (v == 1) return seg != nullptr ? 0 : 13;
     if (v == 11) return seg != nullptr ? 0 : 11;
+    if (v == 22) return 13;  // the default 128-key form also on packed sequences
     if (v == 2) return 1;
     if (v == -1) return (double)s * hq >= 2097152.0 ? 1 : 0;
     return v;
@@ -3146,7 +3147,7 @@ bool attn_fwd_tc(const void* qkv, int64_t s, int hq, int hkv, int d, const int32
     } else if (seg != nullptr && g_attn_fwd_bk128 == 1 && g_attn_fwd_hybrid) {
         // packed: long-sample tile pairs on the 128-key kernel, short ones on the 64-key kernel
         CUtensorMap tkv128 = make_tmap_bf16_2d(qkv, (uint64_t)width, (uint64_t)s, (uint64_t)width, 64, 128);
-        fatc::fwd_tc128_kernel<0, 128><<<grid, fatc::fw2::THREADS, fatc::fw2::SMEM, st>>>(
+        fatc::fwd_tc128_kernel<3, 128><<<grid, fatc::fw2::THREADS, fatc::fw2::SMEM, st>>>(
             tq, tkv128, s, hq, hkv, seg, scale * fatc::LOG2E, (bf16*)o, lse, kv_group(s, hkv, d), 1);
         fatc::fwd_tc_kernel<<<grid, fatc::THREADS, fatc::fw::SMEM, st>>>(tq, tkv, s, hq, hkv, seg, scale * fatc::LOG2E,
                                                                           (bf16*)o, lse, kv_group(s, hkv, d), 2);
