@@ -382,18 +382,20 @@ def test_replay_verification_passes_and_catches_a_corrupted_replay(offload):
 
 
 # ---- the SGD update and multi-step SP equivalence (SPEC.md:697 acceptance #1)
-def _train(cfg, shape, P, N, steps, lr, seed=21):
+def _train(cfg, shape, P, N, steps, lr, seed=21, packed=False, n_layers=1, offload=False):
     p = O.synth_params(cfg, seed)
-    x, lab, _ = O.synth_batch(cfg, N, seed)
+    x, lab, pos = O.synth_batch(cfg, N, seed, packed=packed)
     grp = S.ProcessGroup.loopback_group(P)
-    eng = S.UlyssesLayerStep(shape, N, grp, lr=lr)
+    eng = S.UlyssesLayerStep(shape, N, grp, lr=lr, packed=packed, n_layers=n_layers, ckpt_offload=offload)
     losses = []
     try:
-        for k in O.LayerParams.NAMES:
-            eng.set_param(k, O.f32_to_bf16_bits(p[k]))
+        names = O.LayerParams.NAMES if n_layers == 1 else (
+            [f"layers.{i}.{k}" for i in range(n_layers) for k in O.LAYER_NAMES] + ["g3", "wlm"])
+        for k in names:
+            eng.set_param(k, O.f32_to_bf16_bits(p[k.split(".")[-1]]))
         xb = O.f32_to_bf16_bits(x)
         for _ in range(steps):
-            losses.append(eng.step(xb, lab)[0])
+            losses.append(eng.step(xb, lab, pos if packed else None)[0])
     finally:
         eng.close()
         grp.close()
@@ -422,6 +424,19 @@ def test_sgd_20_steps_sp_equals_sp1(P, cfg, shape):
     dev = np.abs(lp - l1) / l1
     assert dev.max() <= 2e-3, (dev.max(), l1, lp)
     assert l1[-1] < l1[0] - 0.05  # the updates do train
+
+
+@pytest.mark.parametrize("P,packed", [(2, True), (4, True), (4, False)])
+def test_sgd_20_steps_all_features_sp_equals_sp1(P, packed):
+    """SPEC.md:697-698 (acceptance #1 and #2, attention-agnosticism): 20 optimizer steps of a 2-layer stack with
+    Ulysses SP=P, TiledMLP, tiled loss, activation checkpointing and checkpoint offload, on plain causal or packed
+    (block-diagonal) samples, track the SP=1 stack without offload step for step (bf16 weights: within 2e-3)."""
+    lr, steps, N = 2.0, 20, 1024
+    l1, *_ = _train(CFG, SHAPE, 1, N, steps, lr, packed=packed, n_layers=2)
+    lp, *_ = _train(CFG, SHAPE, P, N, steps, lr, packed=packed, n_layers=2, offload=True)
+    dev = np.abs(lp - l1) / l1
+    assert dev.max() <= 2e-3, (dev.max(), l1, lp)
+    assert l1[-1] < l1[0] - 0.05
 
 
 def test_ledger_timeline_csv():
