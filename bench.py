@@ -338,16 +338,9 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         eng.step_async(x, lab, None, on_host=False, stream=sp)
     eng.read_loss(stream=sp)
-    # ---- profiled eager pass: per-kernel-class breakdown, roofline and all-to-all GB/s (not the timed value)
-    eng.set_profiling(True)
-    barrier()
     prof_acc, sites_acc = {}, {}
-    prof_steps = max(1, min(args.steps, 3))
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(prof_steps):
-        eng.step_async(x, lab, None, on_host=False, stream=sp)
-        t = eng.timing()  # syncs on the step's end event only after it is recorded: accumulate per step
+
+    def accumulate(t):  # per-kernel-class CUDA-event times of one step (spt_layer_timing_json)
         for site, v in t["classes"].get("sites", {}).items():
             a = sites_acc.setdefault(site, {"ms": 0.0, "calls": 0, "bytes": 0.0})
             a["ms"] += v["ms"]
@@ -360,15 +353,17 @@ def run_ours(args, rank, world, local_rank):
             a = prof_acc.setdefault(c, {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0})
             for kk in a:
                 a[kk] += v[kk]
-    ev1.record(stream)
-    barrier()
-    ms_eager = max_over_ranks(ev0.elapsed_time(ev1) / prof_steps)
-    eng.set_profiling(False)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # ---- the timed value: K replays of one CUDA graph of the whole step (device-resident inputs at fixed
-    # addresses), the same method at every world size; eager launches only if the capture fails
+    # addresses), the same method at every world size.  The graph is captured with per-kernel-class profiling on:
+    # its CUDA events are event-record nodes of the graph, so the roofline and the breakdown are read from the
+    # last timed replay itself.  Eager launches (and a separate profiled eager pass) only if the capture fails.
     graph_used = False
     gs = torch.cuda.Stream(dev)
     gs.wait_stream(stream)
+    ms_eager = None
+    eng.set_profiling(True)
     if args.graph:
         try:
             eng.graph_capture(x, lab, None, stream=gs.cuda_stream)
@@ -377,6 +372,18 @@ def run_ours(args, rank, world, local_rank):
             graph_used = True
         except S.SptError as e:
             graph_used = f"capture failed: {e}"
+    prof_steps = 1
+    if graph_used is not True:  # fallback: profiled eager pass for the breakdown, unprofiled eager timed loop
+        barrier()
+        prof_steps = max(1, min(args.steps, 3))
+        ev0.record(stream)
+        for _ in range(prof_steps):
+            eng.step_async(x, lab, None, on_host=False, stream=sp)
+            accumulate(eng.timing())
+        ev1.record(stream)
+        barrier()
+        ms_eager = max_over_ranks(ev0.elapsed_time(ev1) / prof_steps)
+        eng.set_profiling(False)
     barrier()
     n0 = S.kernel_launch_count()
     with Clocks(local_rank) as clk:
@@ -391,6 +398,9 @@ def run_ours(args, rank, world, local_rank):
         barrier()
     launches = S.kernel_launch_count() - n0
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    if graph_used is True:
+        accumulate(eng.timing())  # the events of the last timed replay
+    eng.set_profiling(False)
     loss, cnt = eng.read_loss(stream=gs.cuda_stream)
     # ---- end-to-end through the public API with host buffers (H2D inputs, D2H loss every step)
     xh = x.cpu().pin_memory()
@@ -416,7 +426,7 @@ def run_ours(args, rank, world, local_rank):
     pk, pk_kind = peaks()
     led = mem["ledger"]
     peak_b = led["device"]["peak_bytes"]
-    # roofline for the dominant kernel class (per launch averages over the profiled steps)
+    # roofline for the dominant kernel class (per-launch averages over the profiled step(s))
     cls = max(((k, v) for k, v in prof_acc.items() if k != "a2a"), key=lambda kv: kv[1]["ms"])
     name, c = cls
     if c["flops"] > 0:
@@ -478,6 +488,8 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "timing": "cuda-graph replay" if graph_used is True else f"eager launches ({graph_used or 'graph off'})",
         "cuda_graph": graph_used, "ms_per_step_eager_profiled": ms_eager,
+        "breakdown_source": ("per-kernel-class CUDA events recorded inside the timed graph replays (the last one)"
+                             if graph_used is True else f"profiled eager pass of {prof_steps} step(s) before the timed loop"),
         "roofline": roof,
         "breakdown_ms_per_step": breakdown, "class_tflops": tflops,
         "all_to_all": a2a or None,

@@ -1009,13 +1009,13 @@ spt_status spt_layer_step_async(spt_layer* Ly, const void* x, const int64_t* shi
 
 // CUDA graph of one full step with device-resident inputs (fixed pointers; contents may change between
 // replays): the ~100 launches of a step replay without per-launch host overhead or inter-kernel gaps.
-// Capture on a non-default stream with profiling off; tuning switches are read at capture time.
+// Capture on a non-default stream; tuning switches are read at capture time.  With profiling on, the per-kernel-class
+// events are captured as external event-record nodes: spt_layer_timing_json after a replay reports that replay.
 spt_status spt_layer_graph_capture(spt_layer* Ly, const void* x, const int64_t* shift_labels,
                                    const int64_t* position_ids, void* stream) {
     return capi_guard([&] {
         cudaStream_t st = (cudaStream_t)stream;
         SPT_CHECK(st != nullptr, SPT_ERR_CONFIG, "graph capture needs a non-default stream");
-        SPT_CHECK(!Ly->prof.on, SPT_ERR_CONFIG, "graph capture needs profiling off");
         SPT_CHECK(!Ly->cfg.packed || position_ids, SPT_ERR_VALIDATION, "packed config needs position_ids");
         // one eager step first: first-use setup (kernel attributes, lazily created buffers) stays out of the graph
         layer_step(Ly, x, shift_labels, position_ids, false, st);

@@ -52,9 +52,15 @@ struct Prof {
         }
         cudaEvent_t a = ev(), b = ev();
         const int64_t n0 = launch_count();
-        SPT_CUDA(cudaEventRecord(a, st));
+        // External records: under stream capture they become event-record nodes of the graph, re-recorded by every
+        // replay, so the per-class times of a replayed step are readable afterwards (bench.py times its graph
+        // replays with profiling on: the roofline comes from inside the timed region).
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        SPT_CUDA(cudaStreamIsCapturing(st, &cs));
+        const unsigned fl = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+        SPT_CUDA(cudaEventRecordWithFlags(a, st, fl));
         f();
-        SPT_CUDA(cudaEventRecord(b, st));
+        SPT_CUDA(cudaEventRecordWithFlags(b, st, fl));
         recs.push_back({cls, a, b, flops, bytes, launch_count() - n0, next_tag});
         next_tag.clear();
     }
