@@ -7,7 +7,7 @@ under torch.distributed.run), Ulysses SP=N over the whole sequence: 32768 tokens
 BASELINE configs[2] (L8: 524288 tokens, 65536 per GPU) at N=8.  The SP exchange runs on the peer-memory
 transport (fused pack-store / load-unpack all-to-alls over NVLink, `--comm peer`, default) or NCCL
 (`--comm nccl`, the library baseline).  `--workload tiny` runs BASELINE configs[0] (h 256, 8q/2kv d32,
-V 32000, seq 8192) instead.
+V 32000, seq 8192) instead; `--workload qwen` BASELINE configs[4]'s layer shape (Qwen2.5-32B, 32K tokens per GPU).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--seq S] [--impl ours|reference] [--comm peer|nccl]
 
@@ -32,6 +32,9 @@ METRIC = "fwd+bwd tokens/s, Llama-8B-shape layer, 1/2/4/8-GPU Ulysses; peak HBM 
 SHAPES = {
     "l1": dict(hidden=4096, q_heads=32, kv_heads=8, head_dim=128, intermediate=14336, vocab=128256),
     "tiny": dict(hidden=256, q_heads=8, kv_heads=2, head_dim=32, intermediate=1024, vocab=32000),
+    # BASELINE configs[4]'s layer shape (Qwen2.5-32B: 64q/8kv, h=5120 != Hq*d, I=25600, V=151936); configs[4] itself
+    # is SP=8 at 1M tokens on 8 GPUs, so one GPU runs it at 32K tokens (and at N>1 with 32K tokens per GPU)
+    "qwen": dict(hidden=5120, q_heads=64, kv_heads=8, head_dim=128, intermediate=25600, vocab=151936),
 }
 SHAPE = SHAPES["l1"]
 CPU_SAMPLE_TOKENS = 512
@@ -42,12 +45,17 @@ def default_seq(workload, n):
     """L1 (N=1, 32768), weak scaling at 32768 tokens per GPU for N=2/4, the L8 config at N=8 (524288)."""
     if workload == "tiny":
         return 8192 * n
+    if workload == "qwen":
+        return 32768 * n
     return 524288 if n == 8 else 32768 * n
 
 
 def workload_name(seq, n, layers=1, offload=False, workload="l1"):
     stack = "layer" if layers == 1 and not offload else (
         f"{layers}-layer stack (activation checkpoints {'offloaded to host' if offload else 'on device'})")
+    if workload == "qwen":
+        return (f"qwen2.5-32b-shape {stack} + lm_head (h5120, 64q/8kv d128, I25600, V151936; BASELINE configs[4]'s "
+                f"layer), seq {seq} over {n} GPU(s), Ulysses SP={n}, TiledMLP + tiled logits/CE")
     if workload == "tiny":
         return (f"tiny llama-shape {stack} + lm_head (h256, 8q/2kv d32, I1024, V32000; BASELINE configs[0]), "
                 f"seq {seq} over {n} GPU(s), Ulysses SP={n}, TiledMLP + tiled logits/CE")
@@ -69,7 +77,7 @@ _CPU_CACHE = {}
 def cpu_sample_tokens(args):
     """Tokens per CPU step: 512 of the L1 workload (each with its full causal attention context, below), the
     whole configs[0] sequence (8192) for --workload tiny."""
-    return args.cpu_tokens or (CPU_SAMPLE_TOKENS if args.workload == "l1" else 8192)
+    return args.cpu_tokens or (8192 if args.workload == "tiny" else CPU_SAMPLE_TOKENS)
 
 
 def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: int = 0, sp: int = 1):
@@ -86,7 +94,7 @@ def cpu_layer_sample(n_tokens: int, seed: int = 0, workload: str = "l1", seq: in
 
     from oracle import sptrain_oracle as O
 
-    cfg = O.LLAMA8B if workload == "l1" else O.LayerConfig(**SHAPES["tiny"])
+    cfg = O.LayerConfig(**SHAPES[workload])
     # synthetic weights / batches are set-up, not part of the timed step
     if ("w", seed, workload) not in _CPU_CACHE:
         _CPU_CACHE[("w", seed, workload)] = O.LayerParams(**O.synth_params(cfg, seed)).astype(np.float32)
@@ -131,7 +139,7 @@ def _cpu_pool():
 
 
 def cpu_sample_desc(n, workload, seq):
-    if workload == "l1":
+    if workload != "tiny":
         ctx = (f" plus the attention forward + dQ of {n} query rows spread evenly over the {seq}-token sequence "
                f"against their full causal prefix (mean context {seq // 2}; the dK/dV share of the backward, 2 of "
                f"its 5 products, is not in the sample)") if seq > n else ""
@@ -473,7 +481,9 @@ def run_ours(args, rank, world, local_rank):
                    "transport": grp.transport if world > 1 else "none (SP=1)",
                    "mlp_tile": mem["mlp_tile"], "loss_tile": mem["loss_tile"],
                    "l2": "inputs larger than L2 (x 256 MiB/GPU, weights 1.5 GiB, activations ~3 GiB per step)"
-                         if args.workload == "l1" else "no flush (tiny config: weights and activations fit in L2)",
+                         if args.workload == "l1" else ("inputs larger than L2 (x 320 MiB/GPU, weights 2.5 GiB)"
+                                                        if args.workload == "qwen" else
+                                                        "no flush (tiny config: weights and activations fit in L2)"),
                    "optimizer": f"sgd lr={args.lr}" if args.lr > 0 else "none (fwd+bwd+SP grad all-reduce)",
                    "n_layers": args.layers, "rope_theta": args.rope,
                    "activation_checkpointing": ("offload to pinned host" if args.offload else
