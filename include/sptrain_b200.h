@@ -336,6 +336,9 @@ spt_status spt_layer_destroy(spt_layer* layer);
 /* name in {g1, wqkv, wo, g2, wg, wu, wd, g3, wlm} (per-layer names address layer 0; "layers.<i>.<name>"
  * addresses layer i); data = bf16 bits in [out, in] row-major. */
 spt_status spt_layer_set_param(spt_layer* layer, const char* name, const void* data, int32_t data_on_host);
+/* Number of bf16 elements spt_layer_set_param copies for `name` (the caller's buffer must hold that many);
+ * SPT_ERR_VALIDATION for an unknown name (like spt_layer_set_param). */
+spt_status spt_layer_param_numel(spt_layer* layer, const char* name, int64_t* numel);
 /* One fwd+bwd step.  x: bf16 [local_ranks * s_loc, hidden] (loopback: the whole sequence),
  * shift_labels / position_ids: int64 [local_ranks * s_loc] (already pre-shifted).
  * inputs_on_host: 1 -> host buffers (copied in inside the call), 0 -> device buffers.

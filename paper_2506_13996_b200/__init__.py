@@ -149,6 +149,7 @@ SIGNATURES = {
     "spt_comm_stats_json": (I32, [P, C.c_char_p, SZ]),
     "spt_layer_create": (I32, [C.POINTER(LayerConfig), P, C.POINTER(P)]),
     "spt_layer_destroy": (I32, [P]),
+    "spt_layer_param_numel": (I32, [P, C.c_char_p, C.POINTER(I64)]),
     "spt_layer_set_param": (I32, [P, C.c_char_p, P, I32]),
     "spt_layer_step": (I32, [P, P, P, P, I32, PF32, PI64, P]),
     "spt_layer_step_async": (I32, [P, P, P, P, I32, P]),
@@ -548,9 +549,18 @@ class UlyssesLayerStep:
         check(lib().spt_layer_create(C.byref(self.cfg), group.handle, C.byref(h)))
         self.handle = h
 
+    def param_numel(self, name: str) -> int:
+        n = C.c_int64()
+        check(lib().spt_layer_param_numel(self.handle, name.encode(), C.byref(n)))
+        return n.value
+
     def set_param(self, name: str, data, on_host: bool | None = None):
         if on_host is None:
             on_host = not hasattr(data, "is_cuda") or not data.is_cuda
+        size = data.numel() if hasattr(data, "numel") and callable(data.numel) else getattr(data, "size", None)
+        want = self.param_numel(name)
+        if size is not None and int(size) != want:  # the C-ABI copies `want` elements from the pointer
+            raise ShapeError(1, f"set_param({name!r}): {int(size)} elements given, the engine expects {want}")
         check(lib().spt_layer_set_param(self.handle, name.encode(), ptr(data), int(on_host)))
 
     def step(self, x, shift_labels, position_ids=None, on_host: bool | None = None, stream=None):

@@ -977,6 +977,13 @@ spt_status spt_layer_destroy(spt_layer* Ly) {
     });
 }
 
+spt_status spt_layer_param_numel(spt_layer* Ly, const char* name, int64_t* numel) {
+    return capi_guard([&] {
+        SPT_CHECK(numel != nullptr, SPT_ERR_CONFIG, "null numel");
+        param_ptr(Ly, std::string(name), numel);
+    });
+}
+
 spt_status spt_layer_set_param(spt_layer* Ly, const char* name, const void* data, int32_t data_on_host) {
     return capi_guard([&] {
         int64_t n = 0;

@@ -149,3 +149,22 @@ def test_layer_hidden_ne_heads_times_dim(P):
     for k in O.LayerParams.NAMES:
         e = rel_err(r["grads"][k], ref.grads[k])
         assert e <= GRAD_TOL, (k, e)
+
+
+def test_set_param_rejects_wrong_sizes():
+    """The C-ABI copies spt_layer_param_numel elements from the caller's pointer; the Python mirror checks the
+    buffer's size first, so a weight of another shape (e.g. W_o as [h, h] where Hq*d != h) fails loudly instead
+    of being read out of bounds."""
+    shape = S.ModelShape(256, 4, 2, 128, 512, 2048)  # Hq*d = 512 != h = 256
+    grp = S.ProcessGroup.loopback_group(1)
+    eng = S.UlyssesLayerStep(shape, 256, grp)
+    try:
+        assert eng.param_numel("wo") == 256 * 512 and eng.param_numel("wqkv") == (4 + 4) * 128 * 256
+        with pytest.raises(S.ShapeError):
+            eng.set_param("wo", np.zeros(256 * 256, np.uint16))
+        with pytest.raises(S.ValidationError):
+            eng.param_numel("nope")
+        eng.set_param("wo", np.zeros(256 * 512, np.uint16))
+    finally:
+        eng.close()
+        grp.close()

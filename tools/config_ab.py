@@ -18,16 +18,17 @@ ap.add_argument("field")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--group", type=int, default=10)
 ap.add_argument("--seq", type=int, default=32768)
+ap.add_argument("--shape", default="llama", choices=["llama", "qwen"])
 a = ap.parse_args()
 key, vals = a.field.split("=")
 vals = [int(v) for v in vals.split(",")]
-shp = S.LLAMA8B
+shp = S.LLAMA8B if a.shape == "llama" else S.QWEN32B
 grp = S.ProcessGroup.loopback_group(1)
 g = torch.Generator(device="cuda").manual_seed(0)
 qkv = (shp.q_heads + 2 * shp.kv_heads) * shp.head_dim
 ws = {k: ((1 + 0.05 * torch.randn(s_, device="cuda", generator=g)) if k[0] == "g" else
           0.02 * torch.randn(s_, device="cuda", generator=g)).bfloat16()
-      for k, s_ in {"g1": (shp.hidden,), "wqkv": (qkv, shp.hidden), "wo": (shp.hidden, shp.hidden),
+      for k, s_ in {"g1": (shp.hidden,), "wqkv": (qkv, shp.hidden), "wo": (shp.hidden, shp.q_heads * shp.head_dim),
                     "g2": (shp.hidden,), "wg": (shp.intermediate, shp.hidden), "wu": (shp.intermediate, shp.hidden),
                     "wd": (shp.hidden, shp.intermediate), "g3": (shp.hidden,), "wlm": (shp.vocab, shp.hidden)}.items()}
 x = torch.randn(a.seq, shp.hidden, device="cuda", generator=g).bfloat16()

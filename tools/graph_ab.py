@@ -23,7 +23,7 @@ grp = S.ProcessGroup.loopback_group(1)
 eng = S.UlyssesLayerStep(shp, a.seq, grp)
 g = torch.Generator(device="cuda").manual_seed(0)
 qkv = (shp.q_heads + 2 * shp.kv_heads) * shp.head_dim
-for k, s_ in {"g1": (shp.hidden,), "wqkv": (qkv, shp.hidden), "wo": (shp.hidden, shp.hidden), "g2": (shp.hidden,),
+for k, s_ in {"g1": (shp.hidden,), "wqkv": (qkv, shp.hidden), "wo": (shp.hidden, shp.q_heads * shp.head_dim), "g2": (shp.hidden,),
               "wg": (shp.intermediate, shp.hidden), "wu": (shp.intermediate, shp.hidden),
               "wd": (shp.hidden, shp.intermediate), "g3": (shp.hidden,), "wlm": (shp.vocab, shp.hidden)}.items():
     w = (1 + 0.05 * torch.randn(s_, device="cuda", generator=g)) if k[0] == "g" else 0.02 * torch.randn(
