@@ -256,6 +256,18 @@ public:
     void set_param(const std::string& name, const void* bf16_bits, bool on_host = true) {
         check(spt_layer_set_param(l_, name.c_str(), bf16_bits, on_host ? 1 : 0));
     }
+    // checked form: throws sptrain::ShapeError unless `numel` is what the engine copies for `name`
+    void set_param(const std::string& name, const void* bf16_bits, int64_t numel, bool on_host) {
+        if (numel != param_numel(name))
+            throw ShapeError("set_param(" + name + "): " + std::to_string(numel) + " elements given, the engine expects " +
+                             std::to_string(param_numel(name)));
+        set_param(name, bf16_bits, on_host);
+    }
+    int64_t param_numel(const std::string& name) const {  // bf16 elements set_param copies for `name`
+        int64_t n = 0;
+        check(spt_layer_param_numel(l_, name.c_str(), &n));
+        return n;
+    }
     // one fwd+bwd step (SPEC.md:655 train step): returns (global mean loss, global valid count)
     std::pair<float, int64_t> step(const void* x_bf16, const int64_t* shift_labels, const int64_t* position_ids = nullptr,
                                    bool on_host = true, void* stream = nullptr) {
