@@ -445,7 +445,9 @@ def run_ours(args, rank, world, local_rank):
                 "peak_note": "MEASURED_PEAKS.json bf16_tflops_sustained: cuBLAS 8192^3 back to back for 4 s on the pod "
                              "that wrote the file; under the same ~1 kW cap an in-step GEMM class can reach or pass it "
                              f"on a cooler box (burst figure: {pk['bf16_tflops']})",
-                "flops_per_launch": c["flops"] / max(1, c["launches"]), "avg_launch_ms": c["ms"] / max(1, c["launches"])}
+                "flops_per_launch": c["flops"] / max(1, c["launches"]), "avg_launch_ms": c["ms"] / max(1, c["launches"]),
+                # operands read once + outputs written once (csrc/gemm.cu gemm_alg_bytes), the yardstick for traffic
+                "algorithmic_bytes_per_launch": c["bytes"] / max(1, c["launches"]) if c["bytes"] else None}
     else:
         achieved = c["bytes"] / (c["ms"] / 1e3) / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -454,6 +456,8 @@ def run_ours(args, rank, world, local_rank):
     if os.path.exists(prof_path) and args.workload == "l1":
         try:
             roof["traffic"] = json.load(open(prof_path)).get(name)
+            if roof["traffic"] and roof.get("algorithmic_bytes_per_launch"):
+                roof["traffic_over_algorithmic"] = roof["traffic"] / roof["algorithmic_bytes_per_launch"]
         except Exception:
             pass
     breakdown = {k: round(v["ms"] / prof_steps, 3) for k, v in prof_acc.items() if v["ms"] > 0}

@@ -76,6 +76,23 @@ static CUtensorMap make_tmap_f32_c(void* C, int64_t M, int64_t N, int64_t ldc) {
     return m;
 }
 
+// Algorithmic HBM bytes of one GEMM: each operand read once, the output written once (read too for an fp32
+// accumulate or a residual), plus the epilogue's side inputs / outputs.  The per-site "bytes" of the profiler and
+// bench.py's roofline.algorithmic_bytes_per_launch, against which ncu's dram bytes (roofline.traffic) are read.
+static double gemm_alg_bytes(int64_t M, int64_t N, int64_t K, int kind, const EpiParams& ep) {
+    const double mn = (double)M * N;
+    double b = 2.0 * M * K + 2.0 * N * K;
+    switch (kind) {
+        case EPI_BF16: b += 2 * mn * (ep.R ? 2 : 1); break;
+        case EPI_F32: b += 4 * mn * (ep.accumulate ? 2 : 1); break;
+        case EPI_SWIGLU: b += mn; break;                              // bf16 [M, N/2]
+        case EPI_SWIGLU_BWD: b += mn + 2 * mn + mn; break;            // dA in, dGU + act out
+        case EPI_F32_STATS: b += 4 * mn + mn / 256 * 8; break;
+        case EPI_EXP_STATS: b += 2 * mn + mn / 256 * 8 + 12.0 * M; break;  // e, stats, labels + label logits
+    }
+    return b;
+}
+
 template <int BN, bool A_MN, bool B_MN, int KIND>
 static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiParams& ep_in,
                         cudaStream_t st) {
@@ -91,7 +108,7 @@ static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int
     }
     const int ntiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
     const int grid = std::min(ntiles, num_sms());
-    prof_run(P_GEMM, 2.0 * M * N * K, 0, st, [&] {
+    prof_run(P_GEMM, 2.0 * M * N * K, gemm_alg_bytes(M, N, K, KIND, ep), st, [&] {
         kern<<<grid, GEMM_THREADS, smem, st>>>(ta, tb, M, N, K, ep, tc);
         count_launch("gemm");
     });
@@ -124,7 +141,7 @@ static void launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, int M, in
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    prof_run(P_GEMM, 2.0 * M * N * K, 0, st, [&] {
+    prof_run(P_GEMM, 2.0 * M * N * K, gemm_alg_bytes(M, N, K, KIND, ep), st, [&] {
         SPT_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep, tc));
         count_launch("gemm2");
     });
