@@ -38,12 +38,13 @@ def _single(T, L, qkv, s, hq, hkv, d, seg, dout):
     return o, dqkv
 
 
-@pytest.mark.parametrize("P,hq,hkv,s,packed", [(2, 4, 2, 1024, False), (4, 8, 2, 2048, False), (2, 4, 2, 1024, True),
-                                               (8, 8, 2, 2048, False)])
-def test_ulysses_attention_op_matches_single_rank(P, hq, hkv, s, packed):
+@pytest.mark.parametrize("P,hq,hkv,s,packed,d", [(2, 4, 2, 1024, False, 128), (4, 8, 2, 2048, False, 128),
+                                                 (2, 4, 2, 1024, True, 128), (8, 8, 2, 2048, False, 128),
+                                                 (8, 8, 2, 2048, True, 128), (4, 8, 4, 2048, True, 64),
+                                                 (2, 4, 1, 1024, False, 32)])
+def test_ulysses_attention_op_matches_single_rank(P, hq, hkv, s, packed, d):
     T = torch()
     L = S.lib()
-    d = 128
     rng = np.random.default_rng(5 + P)
     qkv = T.from_numpy(O.f32_to_bf16_bits(rng.standard_normal((s, hq + 2 * hkv, d), dtype=np.float32)).view(np.int16)
                        ).cuda().view(T.bfloat16)
