@@ -348,7 +348,11 @@ def run_ours(args, rank, world, local_rank):
     eng.read_loss(stream=sp)
     prof_acc, sites_acc = {}, {}
 
+    gaps_last = {}
+
     def accumulate(t):  # per-kernel-class CUDA-event times of one step (spt_layer_timing_json)
+        gaps_last.clear()
+        gaps_last.update(t.get("gaps", {}))
         for site, v in t["classes"].get("sites", {}).items():
             a = sites_acc.setdefault(site, {"ms": 0.0, "calls": 0, "bytes": 0.0})
             a["ms"] += v["ms"]
@@ -506,6 +510,9 @@ def run_ours(args, rank, world, local_rank):
                              if graph_used is True else f"profiled eager pass of {prof_steps} step(s) before the timed loop"),
         "roofline": roof,
         "breakdown_ms_per_step": breakdown, "class_tflops": tflops,
+        # time of the step outside the profiled kernel regions (unprofiled small kernels + launch gaps), last step
+        "gaps_ms_per_step": ({"total": round(gaps_last["ms"], 3), "n": gaps_last["n"],
+                              "largest": {k: round(v, 3) for k, v in gaps_last["top"].items()}} if gaps_last else None),
         "all_to_all": a2a or None,
         "gemm_sites": {k: {"ms_per_step": round(v["ms"] / prof_steps, 3), "tflops": round(v["tflops"], 1)}
                        for k, v in sorted(sites_acc.items(), key=lambda kv: -kv[1]["ms"]) if not k.startswith("a2a_")},

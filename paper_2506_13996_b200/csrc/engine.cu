@@ -1197,7 +1197,8 @@ spt_status spt_layer_timing_json(spt_layer* Ly, char* buf, size_t cap) {
         float ms = 0;
         SPT_CUDA(cudaEventElapsedTime(&ms, Ly->ev_step0, Ly->ev_step1));
         std::ostringstream os;
-        os << "{\"step_ms\":" << ms << ",\"classes\":" << Ly->prof.json() << "}";
+        os << "{\"step_ms\":" << ms << ",\"classes\":" << Ly->prof.json() << ",\"gaps\":" << Ly->prof.gaps_json()
+           << "}";
         std::string s = os.str();
         SPT_CHECK(s.size() + 1 <= cap, SPT_ERR_SHAPE, "buffer too small");
         std::memcpy(buf, s.c_str(), s.size() + 1);

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -63,6 +64,29 @@ struct Prof {
         SPT_CUDA(cudaEventRecordWithFlags(b, st, fl));
         recs.push_back({cls, a, b, flops, bytes, launch_count() - n0, next_tag});
         next_tag.clear();
+    }
+    // Time between consecutive profiled regions of the last step (unprofiled kernels, launch gaps, kernel ramp-up
+    // outside the events): total and the largest few, keyed "<class before>-><class after>#<record index>".
+    std::string gaps_json() {
+        std::ostringstream os;
+        double gap_total = 0;
+        std::vector<std::pair<double, std::string>> gaps;
+        for (size_t i = 1; i < recs.size(); ++i) {
+            float t = 0;
+            if (cudaEventElapsedTime(&t, recs[i - 1].b, recs[i].a) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            if (t <= 0) continue;
+            gap_total += t;
+            gaps.push_back({t, std::string(name(recs[i - 1].cls)) + "->" + name(recs[i].cls) + "#" + std::to_string(i)});
+        }
+        std::sort(gaps.begin(), gaps.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+        os << "{\"ms\":" << gap_total << ",\"n\":" << gaps.size() << ",\"top\":{";
+        for (size_t i = 0; i < gaps.size() && i < 6; ++i)
+            os << (i ? "," : "") << "\"" << gaps[i].second << "\":" << gaps[i].first;
+        os << "}}";
+        return os.str();
     }
     std::string json() {
         double ms[NCLS] = {}, fl[NCLS] = {}, by[NCLS] = {};
