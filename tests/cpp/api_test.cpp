@@ -107,7 +107,17 @@ static void gpu_tests() {
     for (int P : {1, 2}) {
         auto grp = sb::ProcessGroup::loopback(P);
         sb::UlyssesLayerStep eng(m, N, grp);
-        for (auto& w : ws) eng.set_param(w.n, w.v.data());
+        for (auto& w : ws) eng.set_param(w.n, w.v.data(), (int64_t)w.v.size(), true);  // size-checked form
+        if (P == 1) {  // a W_o of the wrong element count is a ShapeError, not an out-of-bounds read
+            bool threw = false;
+            try {
+                eng.set_param("wo", ws[2].v.data(), (int64_t)ws[2].v.size() - 1, true);
+            } catch (const sptrain::ShapeError&) {
+                threw = true;
+            }
+            EXPECT(threw);
+            EXPECT(eng.param_numel("wlm") == (int64_t)m.vocab * m.hidden);
+        }
         auto a = eng.step(x.data(), lab.data());
         auto b = eng.step(x.data(), lab.data());
         EXPECT(std::isfinite(a.first) && a.first == b.first);  // deterministic
