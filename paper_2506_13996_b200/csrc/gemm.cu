@@ -178,6 +178,7 @@ static bool use_pair_gemm() { return tuning().gemm_1sm != 1; }
 // long-K TiledMLP dX (whose 1-SM kernel keeps the TMA reduce-add epilogue and fills the SMs better).
 static bool pair_mn(int64_t M, int64_t K, int kind) {
     const int v = tuning().gemm_pair_mn;
+    if (v == 3) return kind == EPI_BF16 && K >= 65536;  // the lm_head dX (vocab-long K) only
     if (v != 2) return v == 1;
     if (kind == EPI_F32) return K >= 8192;
     if (kind == EPI_BF16) return !(M <= 4096 && K >= 16384);
