@@ -153,7 +153,7 @@ static int env_int(const char* name, int dflt) {
 }
 // Experiment / tuning switches: initialised from the environment, changeable at run time through
 // spt_tuning_set (A/B comparisons inside one process).  gemm_1sm=1 disables CTA pairs, gemm_pair_mn selects
-// which MN-major operand shapes run as pairs (0 = default none, 1 all, 2 by shape: see pair_mn), gemm_bn=128|256 forces the N tile (0 = 256, 2 = 128 where it fills the last wave better),
+// which MN-major operand shapes run as pairs (0 = default none, 1 all, 2 by shape, 3 lm_head dX only: see pair_mn), gemm_bn=128|256 forces the N tile (0 = 256, 2 = 128 where it fills the last wave better),
 // epi_tstore = fp32 epilogue mode: 0 per-thread stores, 1 smem-transposed coalesced stores, 2 (default) TMA
 // store / reduce-add on the 1-SM kernel (the pair kernel and the stats epilogue use mode 1).
 struct GemmTuning {
@@ -172,7 +172,8 @@ static GemmTuning& tuning() {
     return t;
 }
 static bool use_pair_gemm() { return tuning().gemm_1sm != 1; }
-// MN-major operand shapes as CTA pairs: 0 never, 1 always, 2 by shape — pairs where the isolated per-site
+// MN-major operand shapes as CTA pairs: 0 never, 1 always, 3 the vocab-long-K data gradient only (+0.8% per
+// sustained L1 step, profiles/r2l_pair_mn_ab.json), 2 by shape — pairs where the isolated per-site
 // A/B (profiles/README.md, gemm_sites) had them ahead: fp32-accumulate weight gradients with a long K
 // (lm_head, QKV / O projections over the whole sequence) and bf16 data gradients except the short-M /
 // long-K TiledMLP dX (whose 1-SM kernel keeps the TMA reduce-add epilogue and fills the SMs better).
