@@ -41,7 +41,7 @@ def _single(T, L, qkv, s, hq, hkv, d, seg, dout):
 @pytest.mark.parametrize("P,hq,hkv,s,packed,d", [(2, 4, 2, 1024, False, 128), (4, 8, 2, 2048, False, 128),
                                                  (2, 4, 2, 1024, True, 128), (8, 8, 2, 2048, False, 128),
                                                  (8, 8, 2, 2048, True, 128), (4, 8, 4, 2048, True, 64),
-                                                 (2, 4, 1, 1024, False, 32)])
+                                                 (2, 4, 1, 1024, False, 32), (8, 32, 8, 8192, True, 128)])
 def test_ulysses_attention_op_matches_single_rank(P, hq, hkv, s, packed, d):
     T = torch()
     L = S.lib()
