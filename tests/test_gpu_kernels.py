@@ -26,7 +26,8 @@ def _cuda():
 # ------------------------------------------------------------------ GEMM (tcgen05)
 @pytest.mark.parametrize("a_mn,b_mn,f32,acc", [(0, 0, 0, 0), (0, 1, 0, 0), (1, 1, 1, 0), (1, 1, 1, 1), (0, 0, 1, 0),
                                                 (0, 1, 1, 0), (1, 1, 0, 0)])
-@pytest.mark.parametrize("M,N,K", [(320, 384, 320), (128, 256, 64), (1000, 512, 4160), (1024, 320, 640), (320, 640, 1024)])
+@pytest.mark.parametrize("M,N,K", [(320, 384, 320), (128, 256, 64), (1000, 512, 4160), (1024, 320, 640), (320, 640, 1024),
+                                   (200, 192, 72), (520, 192, 200)])
 def test_gemm_majors(a_mn, b_mn, f32, acc, M, N, K):
     T = torch()
     g = T.Generator(device="cuda").manual_seed(M + N + K)
